@@ -1,0 +1,386 @@
+"""Benchmark of the matrix-free tangent apply y = K(u_k) v on B200.
+
+Contract: one JSON line on rank 0.
+  * workload: BASELINE configs[1] — 32^3 affine cube, Q3, cNH (mu=1, lambda=10),
+    seeded u0/v (inputs.py).  At N GPUs: weak scaling, one 32^3 z-slab per GPU
+    (global mesh 32 x 32 x 32N), ghost faces exchanged with NCCL and
+    overlapped with interior elements.
+  * a "step" = one tangent apply of the headline variant (fp64, on-the-fly
+    "none" strategy); the other 7 variants (fp64/fp32 x none/cachedF/scalar/
+    tensor) are timed the same way and reported under "variants".
+  * L2 is flushed (256 MiB write) before every timed apply; each apply is
+    timed with CUDA events on the operator's stream; max over ranks.
+  * value = global DoFs / apply time (reference definition, runner.cpp:131-132).
+  * e2e = the same metric through the public host-vector call
+    (emfgpu_op_apply_host: pinned H2D of v, apply, D2H of y, sync).
+  * --impl reference: the reference's own CPU implementation (oracle/_ref,
+    ElasticOperator<double>, all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tangent-operator apply DoFs/s"
+UNIT = "DoF/s"
+N_EL, P = 32, 3
+MU, LAM = 1.0, 10.0
+
+# Algorithmic work per element: reference sweep structure
+# (8 forward + 9 transpose sweeps per component, u_k swept again when the
+# strategy reads it) + counted qp flops of the reference material pipeline.
+QP_FLOPS = {"cnh": {"none": 782, "scalar": 714, "tensor": 386, "cachedF": 746}}
+
+
+def flops_per_element(strategy, n=P + 1):
+    reads_uk = strategy in ("none", "scalar")
+    sf = (75 if reads_uk else 51) * n ** 3 * (2 * n - 1) + 9 * n ** 3
+    return sf + n ** 3 * QP_FLOPS["cnh"][strategy]
+
+
+def bytes_per_apply(strategy, prec, ndofs, nel, affine=True):
+    """Algorithmic bytes (SURVEY.md §8(d) ledger minus the u_k row, u_k per DoF;
+    geometry per qp is the yardstick even when stored per element)."""
+    s = prec // 8
+    nq = nel * (P + 1) ** 3
+    ledger = {"none": 72, "scalar": 80, "tensor": 320, "cachedF": 144}[strategy]  # cNH, material, fp64
+    k = 3 if strategy in ("none", "scalar") else 2
+    return ledger * s / 8 * nq + k * s * ndofs
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the reference's CPU ElasticOperator<double> (oracle/_ref),
+    same workload, all host threads; bounded sample per step."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import refbind as R
+    from paper_2408_12479_b200 import inputs as I
+    threads = os.cpu_count() or 1
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libemfref.so not built"}))
+        return
+    L = R.RefLevel(1, 5, P, 0.0, 1)
+    u0 = I.make_u0(N_EL, N_EL, N_EL, P)
+    v = I.make_v(L.ndofs)
+    op = R.RefOperator(L, "cnh", R.material_params(mu=MU, lam=LAM), "none", 64, threads=threads)
+    t0 = time.perf_counter()
+    op.update_linearization(u0)
+    t_lin = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        op.apply(v)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        op.apply(v)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    val = L.ndofs / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, SURVEY §8(c))",
+        "config": {"workload": "cfg1: 32^3 affine cube Q3 cNH mu=1 lambda=10, fp64, strategy none (reference CPU)",
+                   "ndofs": L.ndofs, "threads": threads, "update_linearization_s": t_lin},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} applies of the full cfg1 operator (ElasticOperator<double>)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline_sample(seconds=10.0):
+    """Reference CPU path on the GPU box's host (rank 0, N=1): a bounded sample
+    of the same workload (oracle/_ref, all threads; falls back to the C port)."""
+    from paper_2408_12479_b200 import inputs as I
+    threads = os.cpu_count() or 1
+    u0 = I.make_u0(N_EL, N_EL, N_EL, P)
+    v = I.make_v(u0.size)
+    try:
+        from oracle import refbind as R
+        if not R.available():
+            raise OSError
+        L = R.RefLevel(1, 5, P, 0.0, 1)
+        op = R.RefOperator(L, "cnh", R.material_params(mu=MU, lam=LAM), "none", 64, threads=threads)
+        kind = "reference"
+    except OSError:
+        from oracle import orcbind as O
+        op = O.OracleOperator(N_EL, N_EL, N_EL, P, model="cnh",
+                              params=np.array([MU, LAM, 1000, 2, 5, 3.62, 34.3, 0.7, 1, 0, 0, 0, 1, 0, 0, 0, 1]))
+        kind = "port"
+    op.update_linearization(u0)
+    op.apply(v)
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds or n < 2:
+        op.apply(v)
+        n += 1
+    dt = (time.perf_counter() - t0) / n
+    return {"value": u0.size / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{n} full cfg1 applies (ElasticOperator<double>, none, {threads} threads), "
+                      f"{dt * 1e3:.0f} ms each"}
+
+
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2408_12479_b200 import emfgpu as G
+    from paper_2408_12479_b200 import inputs as I
+    from paper_2408_12479_b200.slab import SlabPartition, SlabOperator
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        world = max(world, 1)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    part = SlabPartition(N_EL, N_EL, N_EL * world, P, world, rank, faces=1)
+    params = G.MaterialParams(mu=MU, lam=LAM)
+    # global seeded inputs restricted to this slab's node planes
+    u0_g = I.make_u0(N_EL, N_EL, N_EL * world, P, extent=(1.0, 1.0, float(world)))
+    v_g = I.make_v(u0_g.size)
+    u0 = u0_g[part.dof_slice]
+    v = v_g[part.dof_slice]
+    del u0_g
+    lev = part.make_level(extent=(1.0, 1.0, float(world)), device=local)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    variants = {}
+    head = None
+    launches = 0
+    order = [(64, "none"), (64, "cachedF"), (64, "scalar"), (64, "tensor"),
+             (32, "none"), (32, "cachedF"), (32, "scalar"), (32, "tensor")]
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
+    for prec, strat in order:
+        op = G.ElasticOperator(lev, "cnh", params, strat, prec)
+        op.update_linearization(u0)
+        dt = torch.float64 if prec == 64 else torch.float32
+        sop = SlabOperator(op, part, dt)
+        x = torch.tensor(v, dtype=dt, device="cuda")
+        y = torch.empty_like(x)
+        stream = torch.cuda.current_stream()
+        for _ in range(args.warmup):
+            sop.apply(x, y)
+        barrier()
+        tot, elem_ms = [], []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(stream)
+            sop.apply(x, y, ev_mid=ev[1])
+            ev[2].record(stream)
+            tot.append(ev)
+        barrier()
+        ms = [e[0].elapsed_time(e[2]) for e in tot]
+        ms_el = [e[0].elapsed_time(e[1]) for e in tot]
+        t = torch.tensor([sum(ms) / len(ms), sum(ms_el) / len(ms_el)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, ms_elem = t.tolist()
+        rec = {"dofs_per_s": part.global_dofs / (ms_step * 1e-3), "ms_per_apply": ms_step,
+               "ms_element_kernel": ms_elem}
+        if strat in ("none", "scalar", "tensor", "cachedF"):
+            fl = flops_per_element(strat) * part.nel_local
+            by = bytes_per_apply(strat, prec, lev.n_dofs, part.nel_local)
+            rec["element_kernel_tflops"] = fl / (ms_elem * 1e-3) / 1e12
+            rec["element_kernel_gbs"] = by / (ms_elem * 1e-3) / 1e9
+        variants[f"fp{prec}_{strat}"] = rec
+        if (prec, strat) == (64, "none"):
+            head = (op, sop, x, y, rec)
+            launches = sop.launches_per_apply * args.steps
+        else:
+            del op, sop
+    if sampler:
+        sampler.__exit__()
+    op, sop, x, y, rec = head
+
+    # e2e through the public host-vector API (pinned host buffers)
+    hx = torch.tensor(v, dtype=torch.float64).pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    e2e_ms = None
+    if world == 1:
+        import ctypes
+        for _ in range(max(1, args.warmup)):
+            G.lib().emfgpu_op_apply_host(op.h, hx.data_ptr(), hy.data_ptr())
+        ts = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st = G.lib().emfgpu_op_apply_host(op.h, hx.data_ptr(), hy.data_ptr())
+            ts.append(time.perf_counter() - t0)
+            assert st == 0
+        e2e_ms = 1e3 * sum(ts) / len(ts)
+        e2e = {"value": lev.n_dofs / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hx.numel() * 8,
+               "d2h_bytes_per_step": hy.numel() * 8, "ms_per_step": e2e_ms,
+               "call": "emfgpu_op_apply_host (pinned host vectors)"}
+    else:
+        # multi-GPU e2e: each rank copies its slab of v in and its slab of y out
+        stream = torch.cuda.current_stream()
+        ts = []
+        dx = torch.empty_like(x)
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            dx.copy_(hx, non_blocking=True)
+            sop.apply(dx, y)
+            hy.copy_(y, non_blocking=True)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        tt = torch.tensor([sum(ts) / len(ts)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item() * 1e3
+        e2e = {"value": part.global_dofs / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hx.numel() * 8,
+               "d2h_bytes_per_step": hy.numel() * 8, "ms_per_step": e2e_ms,
+               "call": "SlabOperator.apply with pinned H2D/D2H per rank"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = read_peaks()
+    fp64_peak = G.fma_peak_tflops(64, 0.5)
+    fp32_peak = G.fma_peak_tflops(32, 0.5)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    for k, r in variants.items():
+        pk = fp64_peak if k.startswith("fp64") else fp32_peak
+        r["fma_frac"] = r["element_kernel_tflops"] / pk
+        r["hbm_frac"] = r["element_kernel_gbs"] / hbm
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("fp64_none_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": rec["dofs_per_s"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": rec["ms_per_apply"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded splitmix64 u0/v (SURVEY §8(c)), cfg1 mesh generated on device",
+        "config": {"workload": "cfg1: 32^3 affine unit cube per GPU (z-slabs), Q3, cNH mu=1 lambda=10, "
+                               "headline fp64 strategy none",
+                   "global_mesh": [N_EL, N_EL, N_EL * world], "ndofs": part.global_dofs,
+                   "l2": "flushed (256 MiB write) before every timed apply", "parallelism": f"z-slab x{world}"},
+        "roofline": {"bound": "fp64_fma", "achieved": rec["element_kernel_tflops"], "peak": fp64_peak,
+                     "unit": "TFLOP/s", "frac": rec["element_kernel_tflops"] / fp64_peak, "traffic": traffic,
+                     "kernel": "apply_kernel<double,3,CNH,S_NONE> (element phase)",
+                     "peak_source": "measured FMA loop on this GPU (emfgpu_bench_fma_peak)",
+                     "flops_per_launch": flops_per_element("none") * part.nel_local,
+                     "hbm_achieved_gbs": rec["element_kernel_gbs"], "hbm_peak_gbs": hbm,
+                     "hbm_frac": rec["element_kernel_gbs"] / hbm},
+        "fma_peaks_tflops": {"fp64": fp64_peak, "fp32": fp32_peak},
+        "variants": variants,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": sampler.summary() if sampler else None,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/* emfgpu — B200 (sm_100a) matrix-free finite-strain tangent operator.
+ *
+ * C ABI of libemfgpu.so.  Plain pointers and sizes only.  Every entry point
+ * replaces one method of the reference's operator-level C++ interface
+ * (proj/include/elastmf/operator.hpp, solver.hpp, mesh.hpp — header-only
+ * templates, no C ABI of their own; the reference's only C ABI,
+ * proj/include/elastmf.h, is session-level).  Status codes and the per-handle
+ * last-error string follow that C ABI's convention (elastmf.h:19-38,
+ * capi.cpp:26-41).  A C++ adapter with the reference's exact method
+ * signatures is in include/emfgpu/operator.hpp; INTEGRATION.md shows the
+ * bindings a maintainer would add.
+ *
+ * Conventions (binding for parity):
+ *   DoF = 3*node + comp; node = (c*my + b)*mx + a (a fastest); element
+ *   e = (k*ny + j)*nx + i; Dirichlet faces bit f = -x,+x,-y,+y,-z,+z.
+ *   Device-pointer entry points are stream-ordered (stream = cudaStream_t,
+ *   NULL = the handle's own stream) and do not synchronise; *_host entry
+ *   points take host vectors, synchronise and report numerical errors.
+ */
+#ifndef EMFGPU_H
+#define EMFGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum emfgpu_status {
+  EMFGPU_OK = 0,
+  EMFGPU_ERR_CONFIG = 1,    /* bad arguments / unsupported configuration (ConfigError) */
+  EMFGPU_ERR_NUMERICAL = 2, /* det F <= 0, singular mapping (NonPositiveJacobian, ...) */
+  EMFGPU_ERR_IO = 3,        /* reserved (EMF_ERR_IO) */
+  EMFGPU_ERR_INVALID = 4,   /* null handle / out pointer */
+  EMFGPU_ERR_STALE = 5,     /* apply/diagonal before update_linearization (StaleCache) */
+  EMFGPU_ERR_CUDA = 6       /* CUDA runtime failure or no device */
+} emfgpu_status;
+
+typedef enum emfgpu_model { EMFGPU_CNH = 0, EMFGPU_INH = 1, EMFGPU_FIBER = 2 } emfgpu_model;
+/* Strategy: the reference's none/scalar/tensor (material.hpp:25) plus the
+ * cached displacement gradient (north star "cached F"). */
+typedef enum emfgpu_strategy {
+  EMFGPU_NONE = 0,
+  EMFGPU_SCALAR = 1,
+  EMFGPU_TENSOR = 2,
+  EMFGPU_CACHED_F = 3
+} emfgpu_strategy;
+typedef enum emfgpu_map {
+  EMFGPU_MAP_REFERENCE = 0, /* DeformMap, mesh.cpp:128-136: param[0] = amplitude */
+  EMFGPU_MAP_SHEAR_X = 1,   /* x' = x + param[0] sin(2 pi y) e_x (BASELINE cfg2) */
+  EMFGPU_MAP_COORDS = 2     /* node coordinates given in emfgpu_level_desc.coords */
+} emfgpu_map;
+
+/* FeLevel(HexMesh, degree, DeformMap) + set_dirichlet, mesh.hpp:71-138.
+ * EXT: boxes with nx,ny,nz elements and per-axis extents (the reference has a
+ * single n, mesh.hpp:48-58). */
+typedef struct emfgpu_level_desc {
+  int nx, ny, nz;        /* elements per axis */
+  int p;                 /* polynomial degree, 1..4 */
+  double extent[3];      /* box lengths */
+  int map;               /* emfgpu_map */
+  double map_param[4];
+  const double* coords;  /* host, 3 per node, when map == EMFGPU_MAP_COORDS */
+  int dirichlet_faces;   /* bit mask, clamped to zero */
+  int device;            /* CUDA device ordinal */
+  int z_offset;          /* global index of element layer 0 (z slabs; colour parity) */
+} emfgpu_level_desc;
+
+/* MaterialParams, material.hpp:36-50 (phi in radians; e1,e2,e3 frame). */
+typedef struct emfgpu_material {
+  double mu, lambda, kappa_b, k1, k2, a, b, phi;
+  double e1[3], e2[3], e3[3];
+} emfgpu_material;
+
+typedef struct emfgpu_level emfgpu_level;
+typedef struct emfgpu_op emfgpu_op;
+typedef struct emfgpu_transfer emfgpu_transfer;
+typedef struct emfgpu_cheb emfgpu_cheb;
+
+const char* emfgpu_version(void);
+/* Message of the last failure of a create call (thread-local). */
+const char* emfgpu_global_last_error(void);
+
+/* ---- FE level (FeLevel, mesh.hpp:71-138) -------------------------------- */
+emfgpu_status emfgpu_level_create(const emfgpu_level_desc* desc, emfgpu_level** out);
+void emfgpu_level_destroy(emfgpu_level* l);
+int64_t emfgpu_level_n_dofs(const emfgpu_level* l);          /* FeLevel::dof_count */
+int64_t emfgpu_level_n_elements(const emfgpu_level* l);
+int emfgpu_level_affine(const emfgpu_level* l);              /* 1: geometry stored per element */
+/* Reference->material Jacobians J0 (9 per qp, element-major, row = comp),
+ * FeLevel::jacobians (mesh.hpp:97-99). host_out holds nel*(p+1)^3*9. */
+emfgpu_status emfgpu_level_jacobians(const emfgpu_level* l, double* host_out);
+emfgpu_status emfgpu_level_coords(const emfgpu_level* l, double* host_out); /* node_coords */
+const char* emfgpu_level_last_error(const emfgpu_level* l);
+
+/* ---- operator (ElasticOperator<Number>, operator.hpp:49-204) ---------------
+ * domain: 0 material (spatial is not supported yet -> EMFGPU_ERR_CONFIG).
+ * precision: 64 (double) or 32 (float): the Number template argument. */
+emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_material* params, int domain,
+                               int strategy, int precision, emfgpu_op** out);
+void emfgpu_op_destroy(emfgpu_op* op);
+int64_t emfgpu_op_n_dofs(const emfgpu_op* op);               /* n_dofs, operator.hpp:82 */
+int emfgpu_op_precision(const emfgpu_op* op);
+const char* emfgpu_op_last_error(const emfgpu_op* op);
+
+/* update_linearization(u_k), operator.hpp:87/643-770: u_k in double, caches
+ * computed in double and stored in Number.  NonPositiveJacobian ->
+ * EMFGPU_ERR_NUMERICAL with the first (element, qpoint) in bad_element /
+ * bad_qpoint (either may be NULL). */
+emfgpu_status emfgpu_op_update_linearization_host(emfgpu_op* op, const double* u_k, int64_t* bad_element,
+                                                  int* bad_qpoint);
+emfgpu_status emfgpu_op_update_linearization(emfgpu_op* op, const double* d_u_k, int64_t* bad_element,
+                                             int* bad_qpoint, void* stream);
+int emfgpu_op_linearized(const emfgpu_op* op);               /* linearized(), :89 */
+uint64_t emfgpu_op_checksum(const emfgpu_op* op);            /* checksum(), FNV-1a of u_k, :90 */
+
+/* apply_tangent(du, y), operator.hpp:99-100/597-621: y = K(u_k) du with the
+ * Dirichlet identity.  x, y: device arrays of n_dofs Number values. */
+emfgpu_status emfgpu_op_apply(emfgpu_op* op, const void* d_x, void* d_y, void* stream);
+/* Same through host vectors (H2D, apply, D2H, synchronise, error check). */
+emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y);
+/* Numerical-error word of the stream-ordered calls (synchronises op's work). */
+emfgpu_status emfgpu_op_check(emfgpu_op* op, int64_t* bad_element, int* bad_qpoint);
+
+/* compute_diagonal(), operator.hpp:106-107/772-878: exact diag(K), 1 on
+ * constrained rows; *n_nonpositive = number of free rows with diag <= 0. */
+emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* n_nonpositive, void* stream);
+emfgpu_status emfgpu_op_compute_diagonal_host(emfgpu_op* op, void* diag, int64_t* n_nonpositive);
+
+/* Byte ledger (operator.hpp:109-116, ledger.cpp:22-76): analytic per-qp
+ * storage/traffic bytes of this operator's cell as stored on the device. */
+emfgpu_status emfgpu_op_ledger(const emfgpu_op* op, int* storage_bytes_per_qp, int* traffic_bytes_per_qp,
+                               double* traffic_bytes_per_dof);
+
+/* Split apply for z-slab multi-GPU: element-phase on the
+ * element layers [k0, k1) only, writing element-local results; then the node
+ * phase for node planes [c0, c1].  apply == elements(0,nz) + nodes(0, mz-1). */
+emfgpu_status emfgpu_op_apply_elements(emfgpu_op* op, const void* d_x, int k0, int k1, void* stream);
+emfgpu_status emfgpu_op_apply_nodes(emfgpu_op* op, const void* d_x, void* d_y, int c0, int c1,
+                                    const void* d_ghost_lo, const void* d_ghost_hi, void* stream);
+/* Element-local result buffer of the last element phase (device, Number,
+ * (e*(p+1)^3 + m)*3 + c) and its ghost-face layout size in values. */
+void* emfgpu_op_local_buffer(emfgpu_op* op);
+int64_t emfgpu_op_face_values(const emfgpu_op* op);
+/* Pack the element-local results of element layer k restricted to its lower
+ * (side 0) or upper (side 1) local node face into d_face (face_values). */
+emfgpu_status emfgpu_op_pack_face(emfgpu_op* op, int k, int side, void* d_face, void* stream);
+
+/* ---- hp-multigrid ingredients (solver.hpp, mesh.hpp) ------------------------ */
+/* TransferOp(fine, coarse), mesh.hpp:157-182: p-coarsening (same mesh) or one
+ * uniform h-step (n_fine = 2 n_coarse per axis). */
+emfgpu_status emfgpu_transfer_create(const emfgpu_level* fine, const emfgpu_level* coarse, emfgpu_transfer** out);
+void emfgpu_transfer_destroy(emfgpu_transfer* t);
+/* kind 0 prolongate (coarse->fine), 1 restrict_ (fine->coarse, transpose),
+ * 2 interpolate_down (fine->coarse nodal evaluation); precision 64|32. */
+emfgpu_status emfgpu_transfer_apply(emfgpu_transfer* t, int kind, int precision, const void* d_in, void* d_out,
+                                    void* stream);
+
+/* ChebyshevSmoother<Number>::setup/smooth, solver.hpp:312-362. */
+emfgpu_status emfgpu_cheb_create(emfgpu_op* op, const void* d_diag, double lmax_est, int degree,
+                                 double range_factor, double safety, emfgpu_cheb** out);
+void emfgpu_cheb_destroy(emfgpu_cheb* c);
+emfgpu_status emfgpu_cheb_smooth(emfgpu_cheb* c, void* d_x, const void* d_b, int zero_start, void* stream);
+
+/* estimate_eigenvalues(op, diag, iterations, seed), solver.hpp:262-308. */
+emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, int iterations, uint64_t seed,
+                                             double* lambda_min, double* lambda_max);
+
+/* Deterministic (fixed-order) double-accumulated dot product of two device
+ * vectors of Number (dot_d, solver.hpp:95-100). */
+emfgpu_status emfgpu_dot(int precision, const void* d_a, const void* d_b, int64_t n, double* out, void* stream);
+
+/* FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured by a register-resident
+ * FMA loop over one wave of CTAs for `seconds`: the FP64/FP32 roofline
+ * denominator (bench.py). */
+emfgpu_status emfgpu_bench_fma_peak(int precision, double seconds, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EMFGPU_H */

@@ -1,0 +1,1091 @@
+// C ABI of libemfgpu.so (include/emfgpu.h): handle lifetime, host setup
+// (basis tables, lattice coordinates, material constants), device buffers,
+// and stream-ordered orchestration of the kernels.  Host-side error model
+// follows the reference C layer (status code + per-handle message,
+// proj/src/capi.cpp:26-41); no CPU fallback exists — without a CUDA device
+// every create call fails with EMFGPU_ERR_CUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+
+#include "internal.h"
+
+using namespace emfgpu;
+
+namespace {
+
+thread_local std::string g_error;
+
+struct ApiError : std::runtime_error {
+  emfgpu_status code;
+  ApiError(emfgpu_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess)                                                                           \
+      throw ApiError(EMFGPU_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+
+template <typename Fn>
+emfgpu_status guarded(std::string* slot, Fn&& fn) {
+  try {
+    fn();
+    if (slot) slot->clear();
+    return EMFGPU_OK;
+  } catch (const ApiError& e) {
+    if (slot) *slot = e.what();
+    g_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (slot) *slot = e.what();
+    g_error = e.what();
+    return EMFGPU_ERR_CUDA;
+  }
+}
+
+cudaStream_t S(void* s, cudaStream_t def) { return s ? static_cast<cudaStream_t>(s) : def; }
+
+// ---- 1D basis: Gauss-Lobatto nodes, Gauss rule, Lagrange tables ----------
+// Standard Newton iterations on Legendre polynomials (the construction of
+// mesh.cpp:14-120), run on the host once per level.
+double legendre(int n, double x) {
+  double p0 = 1.0, p1 = x;
+  if (n == 0) return p0;
+  for (int k = 2; k <= n; ++k) {
+    const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+    p0 = p1;
+    p1 = p2;
+  }
+  return p1;
+}
+double dlegendre(int n, double x) {
+  if (n == 0) return 0.0;
+  return n * (legendre(n - 1, x) - x * legendre(n, x)) / (1.0 - x * x);
+}
+void gauss_rule(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double t = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      const double dx = legendre(n, t) / dlegendre(n, t);
+      t -= dx;
+      if (std::abs(dx) < 1e-15) break;
+    }
+    x[i] = t;
+  }
+  std::sort(x.begin(), x.end());
+  for (int i = 0; i < n; ++i) {
+    const double d = dlegendre(n, x[i]);
+    w[i] = 2.0 / ((1.0 - x[i] * x[i]) * d * d);
+  }
+}
+std::vector<double> lobatto_nodes(int n) {
+  std::vector<double> x(n);
+  x[0] = -1.0;
+  x[n - 1] = 1.0;
+  const int m = n - 1;
+  for (int i = 1; i < m; ++i) {
+    double t = std::cos(M_PI * (m - i) / m);
+    for (int it = 0; it < 100; ++it) {
+      const double g = dlegendre(m, t);
+      const double gp = (2.0 * t * g - m * (m + 1.0) * legendre(m, t)) / (1.0 - t * t);
+      const double dx = g / gp;
+      t -= dx;
+      if (std::abs(dx) < 1e-15) break;
+    }
+    x[i] = t;
+  }
+  std::sort(x.begin(), x.end());
+  return x;
+}
+double lagrange(const std::vector<double>& xs, int i, double x) {
+  double v = 1.0;
+  for (size_t k = 0; k < xs.size(); ++k)
+    if ((int)k != i) v *= (x - xs[k]) / (xs[i] - xs[k]);
+  return v;
+}
+double dlagrange(const std::vector<double>& xs, int i, double x) {
+  double sum = 0.0;
+  for (size_t m = 0; m < xs.size(); ++m) {
+    if ((int)m == i) continue;
+    double prod = 1.0 / (xs[i] - xs[m]);
+    for (size_t k = 0; k < xs.size(); ++k) {
+      if ((int)k == i || k == m) continue;
+      prod *= (x - xs[k]) / (xs[i] - xs[k]);
+    }
+    sum += prod;
+  }
+  return sum;
+}
+
+// ---- fibre structure tensors, material.cpp:50-82 (std special functions) --
+void structure_tensors(const emfgpu_material& p, double h[2][6], double m1[2][3]) {
+  const double h33 = 1.0 / (4.0 * p.b) - std::exp(-2.0 * p.b) / (std::sqrt(2.0 * M_PI * p.b) * std::erf(std::sqrt(2.0 * p.b)));
+  const double ratio = p.a == 0.0 ? 0.0 : std::cyl_bessel_i(1.0, p.a) / std::cyl_bessel_i(0.0, p.a);
+  const double h11 = 0.5 * (1.0 - h33) * (1.0 + ratio);
+  const double h22 = 0.5 * (1.0 - h33) * (1.0 - ratio);
+  const double c = std::cos(p.phi), s = std::sin(p.phi);
+  double v1[2][3], v2[2][3];
+  for (int k = 0; k < 3; ++k) {
+    v1[0][k] = c * p.e1[k] + s * p.e2[k];
+    v2[0][k] = -s * p.e1[k] + c * p.e2[k];
+    v1[1][k] = c * p.e1[k] - s * p.e2[k];
+    v2[1][k] = s * p.e1[k] + c * p.e2[k];
+  }
+  for (int f = 0; f < 2; ++f) {
+    for (int i = 0; i < 3; ++i)
+      for (int j = i; j < 3; ++j)
+        h[f][sidx(i, j)] = h11 * (v1[f][i] * v1[f][j]) + h22 * (v2[f][i] * v2[f][j]) + h33 * (p.e3[i] * p.e3[j]);
+    for (int k = 0; k < 3; ++k) m1[f][k] = v1[f][k];
+  }
+}
+
+template <typename T>
+MatConst<T> mat_const(const emfgpu_material& p, const double h[2][6], const double m1[2][3]) {
+  MatConst<T> m;
+  m.mu = T(p.mu);
+  m.lam = T(p.lambda);
+  m.half_k = T(0.5 * p.kappa_b);
+  m.kappa = T(p.kappa_b);
+  m.k2 = T(p.k2);
+  m.two_k1 = T(2.0 * p.k1);
+  for (int f = 0; f < 2; ++f) {
+    for (int k = 0; k < 6; ++k) m.h[f][k] = T(h[f][k]);
+    for (int k = 0; k < 3; ++k) m.m1[f][k] = T(m1[f][k]);
+  }
+  return m;
+}
+
+uint64_t fnv1a(const void* data, size_t bytes) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < bytes; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+template <typename T>
+KArgs<T> kargs(const emfgpu_op* op) {
+  const emfgpu_level* L = op->L;
+  KArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.loc = static_cast<T*>(op->d_loc);
+  a.uk = static_cast<const T*>(op->d_uk);
+  a.ukd = op->d_ukd;
+  a.geo = std::is_same<T, double>::value ? reinterpret_cast<const T*>(L->d_geo) : reinterpret_cast<const T*>(L->d_geo_f);
+  a.geod = L->d_geo;
+  a.geo_stride = L->geo_stride;
+  a.affine = L->affine;
+  a.cache = static_cast<T*>(op->d_cache);
+  a.cache_stride = op->cache_stride;
+  a.strategy = op->strategy;
+  a.nx = L->nx;
+  a.ny = L->ny;
+  a.nz = L->nz;
+  a.mx = L->mx;
+  a.my = L->my;
+  a.mz = L->mz;
+  a.nel = L->nel;
+  a.e_begin = 0;
+  a.faces = L->faces;
+  a.err = op->d_err;
+  if constexpr (std::is_same<T, double>::value)
+    a.mat = op->matd;
+  else
+    a.mat = op->matf;
+  a.matd = op->matd;
+  const int n = L->p + 1;
+  for (int t = 0; t < n * n; ++t) {
+    a.Bm[t] = T(L->B[t]);  // the reference casts the double tables per use (sumfact.hpp:28-29)
+    a.Dm[t] = T(L->D[t]);
+    a.Bd[t] = L->B[t];
+    a.Dd[t] = L->D[t];
+  }
+  for (int t = 0; t < n; ++t) a.qwd[t] = L->qwts[t];
+  return a;
+}
+
+template <typename T>
+void dispatch_apply(const emfgpu_op* op, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
+  switch (op->L->p) {
+    case 1: launch_apply<T, 1>(op->model, op->strategy, a, e0, e1, s); break;
+    case 2: launch_apply<T, 2>(op->model, op->strategy, a, e0, e1, s); break;
+    case 3: launch_apply<T, 3>(op->model, op->strategy, a, e0, e1, s); break;
+    case 4: launch_apply<T, 4>(op->model, op->strategy, a, e0, e1, s); break;
+  }
+}
+template <typename T>
+void dispatch_linearize(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) {
+  switch (op->L->p) {
+    case 1: launch_linearize<T, 1>(op->model, a, s); break;
+    case 2: launch_linearize<T, 2>(op->model, a, s); break;
+    case 3: launch_linearize<T, 3>(op->model, a, s); break;
+    case 4: launch_linearize<T, 4>(op->model, a, s); break;
+  }
+}
+template <typename T>
+void dispatch_diagonal(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) {
+  switch (op->L->p) {
+    case 1: launch_diagonal<T, 1>(op->model, a, s); break;
+    case 2: launch_diagonal<T, 2>(op->model, a, s); break;
+    case 3: launch_diagonal<T, 3>(op->model, a, s); break;
+    case 4: launch_diagonal<T, 4>(op->model, a, s); break;
+  }
+}
+
+size_t nsize(const emfgpu_op* op) { return op->precision == 64 ? 8 : 4; }
+
+void require_linearized(const emfgpu_op* op, const char* what) {
+  if (!op->linearized)
+    throw ApiError(EMFGPU_ERR_STALE, std::string(what) + ": update_linearization has not run");
+}
+
+void apply_elements(emfgpu_op* op, const void* x, int k0, int k1, cudaStream_t s) {
+  const emfgpu_level* L = op->L;
+  const int64_t e0 = (int64_t)k0 * L->nx * L->ny, e1 = (int64_t)k1 * L->nx * L->ny;
+  if (op->precision == 64) {
+    KArgs<double> a = kargs<double>(op);
+    a.x = static_cast<const double*>(x);
+    dispatch_apply<double>(op, a, e0, e1, s);
+  } else {
+    KArgs<float> a = kargs<float>(op);
+    a.x = static_cast<const float*>(x);
+    dispatch_apply<float>(op, a, e0, e1, s);
+  }
+  CK(cudaGetLastError());
+}
+
+void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const void* glo, const void* ghi, int kpar,
+                 cudaStream_t s) {
+  const emfgpu_level* L = op->L;
+  if (op->precision == 64)
+    launch_node_gather<double>(static_cast<const double*>(op->d_loc), static_cast<const double*>(glo),
+                               static_cast<const double*>(ghi), static_cast<const double*>(x),
+                               static_cast<double*>(y), L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, s);
+  else
+    launch_node_gather<float>(static_cast<const float*>(op->d_loc), static_cast<const float*>(glo),
+                              static_cast<const float*>(ghi), static_cast<const float*>(x), static_cast<float*>(y),
+                              L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, s);
+  CK(cudaGetLastError());
+}
+
+void check_err(emfgpu_op* op, cudaStream_t s, int64_t* be, int* bq, const char* what) {
+  CK(cudaMemcpyAsync(op->h_err, op->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long v = *op->h_err;
+  if (v != ~0ull) {
+    const int64_t e = (int64_t)(v / op->L->nq3);
+    const int q = (int)(v % op->L->nq3);
+    if (be) *be = e;
+    if (bq) *bq = q;
+    CK(cudaMemsetAsync(op->d_err, 0xff, sizeof(unsigned long long), s));
+    throw ApiError(EMFGPU_ERR_NUMERICAL, std::string(what) + ": det(F) <= 0 element=" + std::to_string(e) +
+                                             " qpoint=" + std::to_string(q));
+  }
+}
+
+}  // namespace
+
+// Transfer / smoother handles
+struct emfgpu_transfer {
+  const emfgpu_level* fine;
+  const emfgpu_level* coarse;
+  struct Axis {
+    int n_src, p_src, n_dst, p_dst;
+    int *src_elem = nullptr, *t_ptr = nullptr, *t_d = nullptr, *t_s = nullptr;
+    double* w = nullptr;
+  } up[3], down[3];
+  void* tmp[2] = {nullptr, nullptr};
+  size_t tmp_bytes = 0;
+  std::string last_error;
+};
+
+struct emfgpu_cheb {
+  emfgpu_op* op;
+  int degree;
+  double lambda_min, lambda_max;
+  void *inv_diag = nullptr, *r = nullptr, *d = nullptr, *ad = nullptr;
+};
+
+// Definitions keep the C linkage of their declarations in emfgpu.h.
+const char* emfgpu_version(void) { return "emfgpu 0.1 (sm_100a)"; }
+const char* emfgpu_global_last_error(void) { return g_error.c_str(); }
+
+// ---------------------------------------------------------------- level ----
+emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out) {
+  if (!d || !out) return EMFGPU_ERR_INVALID;
+  *out = nullptr;
+  auto L = std::make_unique<emfgpu_level>();
+  emfgpu_status st = guarded(nullptr, [&] {
+    if (d->p < 1 || d->p > kMaxP) throw ApiError(EMFGPU_ERR_CONFIG, "level: degree must be in 1..4");
+    if (d->nx < 1 || d->ny < 1 || d->nz < 1) throw ApiError(EMFGPU_ERR_CONFIG, "level: need nx,ny,nz >= 1");
+    if (d->map == EMFGPU_MAP_COORDS && !d->coords) throw ApiError(EMFGPU_ERR_CONFIG, "level: coords missing");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw ApiError(EMFGPU_ERR_CUDA, "level: no CUDA device (no CPU fallback by design)");
+    CK(cudaSetDevice(d->device));
+    L->device = d->device;
+    L->nx = d->nx;
+    L->ny = d->ny;
+    L->nz = d->nz;
+    L->p = d->p;
+    L->mx = d->nx * d->p + 1;
+    L->my = d->ny * d->p + 1;
+    L->mz = d->nz * d->p + 1;
+    L->nnodes = (int64_t)L->mx * L->my * L->mz;
+    L->ndofs = 3 * L->nnodes;
+    L->nel = (int64_t)d->nx * d->ny * d->nz;
+    const int n = d->p + 1;
+    L->nq3 = n * n * n;
+    L->faces = d->dirichlet_faces;
+    L->z_offset = d->z_offset;
+    for (int a = 0; a < 3; ++a) L->extent[a] = d->extent[a] > 0 ? d->extent[a] : 1.0;
+    L->nodes = lobatto_nodes(n);
+    gauss_rule(n, L->qpts, L->qwts);
+    L->B.assign(n * n, 0.0);
+    L->D.assign(n * n, 0.0);
+    for (int q = 0; q < n; ++q)
+      for (int i = 0; i < n; ++i) {
+        L->B[q * n + i] = lagrange(L->nodes, i, L->qpts[q]);
+        L->D[q * n + i] = dlagrange(L->nodes, i, L->qpts[q]);
+      }
+    // lattice coordinates (mesh.cpp:138-160), then the map
+    std::vector<double> coords(3 * L->nnodes);
+    if (d->map == EMFGPU_MAP_COORDS) {
+      std::memcpy(coords.data(), d->coords, coords.size() * sizeof(double));
+    } else {
+      const int ne[3] = {d->nx, d->ny, d->nz}, m[3] = {L->mx, L->my, L->mz};
+      std::vector<double> ax[3];
+      for (int a = 0; a < 3; ++a) {
+        ax[a].resize(m[a]);
+        const double h = L->extent[a] / ne[a];
+        for (int idx = 0; idx < m[a]; ++idx) {
+          const int e = std::min(idx / d->p, ne[a] - 1);
+          const int l = idx - e * d->p;
+          ax[a][idx] = (e + 0.5 * (L->nodes[l] + 1.0)) * h;
+        }
+      }
+      const double amp = d->map_param[0];
+      const double ext = L->extent[0];
+      for (int c = 0; c < m[2]; ++c)
+        for (int b = 0; b < m[1]; ++b)
+          for (int a = 0; a < m[0]; ++a) {
+            const double x = ax[0][a], y = ax[1][b], z = ax[2][c];
+            double r0 = x, r1 = y, r2 = z;
+            if (d->map == EMFGPU_MAP_REFERENCE && amp != 0.0) {  // DeformMap, mesh.cpp:128-136
+              const double s = M_PI / ext, A = amp * ext;
+              r0 += A * std::sin(s * y) * std::sin(s * z);
+              r1 += A * std::sin(s * x) * std::sin(s * z);
+              r2 += A * std::sin(s * x) * std::sin(s * y);
+            } else if (d->map == EMFGPU_MAP_SHEAR_X) {
+              r0 += amp * std::sin(2.0 * M_PI * y);
+            }
+            const int64_t node = ((int64_t)c * m[1] + b) * m[0] + a;
+            coords[3 * node] = r0;
+            coords[3 * node + 1] = r1;
+            coords[3 * node + 2] = r2;
+          }
+    }
+    CK(cudaMalloc(&L->d_coords, coords.size() * sizeof(double)));
+    CK(cudaMemcpy(L->d_coords, coords.data(), coords.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const int64_t nqp = L->nel * L->nq3;
+    double* geo_q = nullptr;
+    int* flags = nullptr;
+    CK(cudaMalloc(&geo_q, sizeof(double) * nqp * 11));
+    CK(cudaMalloc(&flags, 2 * sizeof(int)));
+    CK(cudaMemset(flags, 0, 2 * sizeof(int)));
+    launch_geometry(L->d_coords, geo_q, nullptr, L->nx, L->ny, L->nz, L->p, L->B.data(), L->D.data(),
+                    L->qwts.data(), flags, flags + 1, 0);
+    CK(cudaGetLastError());
+    int hf[2];
+    CK(cudaMemcpy(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost));
+    cudaFree(flags);
+    if (hf[1]) {
+      cudaFree(geo_q);
+      throw ApiError(EMFGPU_ERR_NUMERICAL, "level: mapping Jacobian not positive at a quadrature point");
+    }
+    L->affine = hf[0] ? 0 : 1;
+    if (L->affine) {
+      CK(cudaMalloc(&L->d_geo, sizeof(double) * L->nel * 10));
+      launch_geo_compact(geo_q, L->d_geo, L->nel, (int)L->nq3, 0);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      cudaFree(geo_q);
+      L->geo_stride = L->nel;
+    } else {
+      L->d_geo = geo_q;  // fields 0..9 used, stride nqp
+      L->geo_stride = nqp;
+    }
+    const int64_t gsz = 10 * L->geo_stride;
+    CK(cudaMalloc(&L->d_geo_f, sizeof(float) * gsz));
+    launch_cast_d2f(L->d_geo, L->d_geo_f, gsz, 0);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+  });
+  if (st != EMFGPU_OK) {
+    if (L->d_coords) cudaFree(L->d_coords);
+    if (L->d_geo) cudaFree(L->d_geo);
+    if (L->d_geo_f) cudaFree(L->d_geo_f);
+    return st;
+  }
+  *out = L.release();
+  return EMFGPU_OK;
+}
+
+void emfgpu_level_destroy(emfgpu_level* l) {
+  if (!l) return;
+  cudaFree(l->d_coords);
+  cudaFree(l->d_geo);
+  cudaFree(l->d_geo_f);
+  delete l;
+}
+
+int64_t emfgpu_level_n_dofs(const emfgpu_level* l) { return l ? l->ndofs : 0; }
+int64_t emfgpu_level_n_elements(const emfgpu_level* l) { return l ? l->nel : 0; }
+int emfgpu_level_affine(const emfgpu_level* l) { return l ? l->affine : 0; }
+const char* emfgpu_level_last_error(const emfgpu_level* l) { return l ? l->last_error.c_str() : ""; }
+
+emfgpu_status emfgpu_level_jacobians(const emfgpu_level* l, double* host_out) {
+  if (!l || !host_out) return EMFGPU_ERR_INVALID;
+  return guarded(nullptr, [&] {
+    CK(cudaSetDevice(l->device));
+    const int64_t nqp = l->nel * l->nq3;
+    double *geo_q = nullptr, *j0 = nullptr;
+    int* flags = nullptr;
+    CK(cudaMalloc(&geo_q, sizeof(double) * nqp * 11));
+    CK(cudaMalloc(&j0, sizeof(double) * nqp * 9));
+    CK(cudaMalloc(&flags, 2 * sizeof(int)));
+    launch_geometry(l->d_coords, geo_q, j0, l->nx, l->ny, l->nz, l->p, l->B.data(), l->D.data(), l->qwts.data(),
+                    flags, flags + 1, 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(host_out, j0, sizeof(double) * nqp * 9, cudaMemcpyDeviceToHost));
+    cudaFree(geo_q);
+    cudaFree(j0);
+    cudaFree(flags);
+  });
+}
+
+emfgpu_status emfgpu_level_coords(const emfgpu_level* l, double* host_out) {
+  if (!l || !host_out) return EMFGPU_ERR_INVALID;
+  return guarded(nullptr, [&] {
+    CK(cudaSetDevice(l->device));
+    CK(cudaMemcpy(host_out, l->d_coords, sizeof(double) * l->ndofs, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ------------------------------------------------------------------- op ----
+emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_material* params, int domain,
+                               int strategy, int precision, emfgpu_op** out) {
+  if (!l || !params || !out) return EMFGPU_ERR_INVALID;
+  *out = nullptr;
+  auto op = std::make_unique<emfgpu_op>();
+  emfgpu_status st = guarded(nullptr, [&] {
+    if (model < 0 || model > 2) throw ApiError(EMFGPU_ERR_CONFIG, "op: unknown model");
+    if (domain != 0) throw ApiError(EMFGPU_ERR_CONFIG, "op: spatial domain not supported (material only)");
+    if (strategy < 0 || strategy > 3) throw ApiError(EMFGPU_ERR_CONFIG, "op: unknown strategy");
+    if (precision != 64 && precision != 32) throw ApiError(EMFGPU_ERR_CONFIG, "op: precision must be 64 or 32");
+    // MaterialParams::validate, material.cpp:36-48
+    if (!(params->mu > 0)) throw ApiError(EMFGPU_ERR_CONFIG, "MaterialParams: mu must be positive");
+    if (model != 0 && !(params->kappa_b > 0)) throw ApiError(EMFGPU_ERR_CONFIG, "MaterialParams: kappa_b must be positive");
+    if (model == 2) {
+      if (!(params->k2 > 0)) throw ApiError(EMFGPU_ERR_CONFIG, "MaterialParams: k2 must be positive");
+      if (!(params->a > 0) || !(params->b > 0))
+        throw ApiError(EMFGPU_ERR_CONFIG, "build_structure_tensors: a and b must be positive");
+      auto dot3 = [](const double* u, const double* v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; };
+      const double tol = 1e-12;
+      if (std::abs(dot3(params->e1, params->e1) - 1) > tol || std::abs(dot3(params->e2, params->e2) - 1) > tol ||
+          std::abs(dot3(params->e3, params->e3) - 1) > tol || std::abs(dot3(params->e1, params->e2)) > tol ||
+          std::abs(dot3(params->e1, params->e3)) > tol || std::abs(dot3(params->e2, params->e3)) > tol)
+        throw ApiError(EMFGPU_ERR_CONFIG, "MaterialParams: frame {e1,e2,e3} not orthonormal");
+    }
+    CK(cudaSetDevice(l->device));
+    op->L = l;
+    op->model = model;
+    op->strategy = strategy;
+    op->precision = precision;
+    op->params = *params;
+    double h[2][6] = {}, m1[2][3] = {};
+    if (model == 2) structure_tensors(*params, h, m1);
+    op->matd = mat_const<double>(*params, h, m1);
+    op->matf = mat_const<float>(*params, h, m1);
+    const size_t ns = nsize(op.get());
+    CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&op->d_loc, ns * l->nel * l->nq3 * 3));
+    CK(cudaMalloc(&op->d_err, sizeof(unsigned long long)));
+    CK(cudaMemset(op->d_err, 0xff, sizeof(unsigned long long)));
+    CK(cudaMallocHost(&op->h_err, sizeof(unsigned long long)));
+    CK(cudaMalloc(&op->d_ukd, sizeof(double) * l->ndofs));
+    if (strategy == EMFGPU_NONE || strategy == EMFGPU_SCALAR) CK(cudaMalloc(&op->d_uk, ns * l->ndofs));
+    const int nf = strategy == EMFGPU_TENSOR ? C_NT : strategy == EMFGPU_SCALAR ? 8 : strategy == EMFGPU_CACHED_F ? C_NG : 0;
+    op->n_cache_fields = nf;
+    op->cache_stride = l->nel * l->nq3;
+    if (nf) CK(cudaMalloc(&op->d_cache, ns * nf * op->cache_stride));
+  });
+  if (st != EMFGPU_OK) {
+    emfgpu_op_destroy(op.release());
+    return st;
+  }
+  *out = op.release();
+  return EMFGPU_OK;
+}
+
+void emfgpu_op_destroy(emfgpu_op* op) {
+  if (!op) return;
+  cudaFree(op->d_cache);
+  cudaFree(op->d_uk);
+  cudaFree(op->d_ukd);
+  cudaFree(op->d_loc);
+  cudaFree(op->d_x);
+  cudaFree(op->d_y);
+  cudaFree(op->d_err);
+  if (op->h_err) cudaFreeHost(op->h_err);
+  if (op->stream) cudaStreamDestroy(op->stream);
+  delete op;
+}
+
+int64_t emfgpu_op_n_dofs(const emfgpu_op* op) { return op ? op->L->ndofs : 0; }
+int emfgpu_op_precision(const emfgpu_op* op) { return op ? op->precision : 0; }
+const char* emfgpu_op_last_error(const emfgpu_op* op) { return op ? op->last_error.c_str() : ""; }
+int emfgpu_op_linearized(const emfgpu_op* op) { return op && op->linearized ? 1 : 0; }
+uint64_t emfgpu_op_checksum(const emfgpu_op* op) { return op ? op->checksum : 0; }
+
+static void linearize_impl(emfgpu_op* op, int64_t* be, int* bq, cudaStream_t s) {
+  const emfgpu_level* L = op->L;
+  op->linearized = false;
+  if (op->d_uk) {
+    if (op->precision == 64)
+      CK(cudaMemcpyAsync(op->d_uk, op->d_ukd, sizeof(double) * L->ndofs, cudaMemcpyDeviceToDevice, s));
+    else
+      launch_cast_d2f(op->d_ukd, static_cast<float*>(op->d_uk), L->ndofs, s);
+  }
+  if (op->precision == 64)
+    dispatch_linearize<double>(op, kargs<double>(op), s);
+  else
+    dispatch_linearize<float>(op, kargs<float>(op), s);
+  CK(cudaGetLastError());
+  check_err(op, s, be, bq, "update_linearization");
+  op->linearized = true;
+}
+
+emfgpu_status emfgpu_op_update_linearization_host(emfgpu_op* op, const double* u_k, int64_t* be, int* bq) {
+  if (!op || !u_k) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    CK(cudaMemcpyAsync(op->d_ukd, u_k, sizeof(double) * op->L->ndofs, cudaMemcpyHostToDevice, op->stream));
+    op->checksum = fnv1a(u_k, sizeof(double) * op->L->ndofs);
+    linearize_impl(op, be, bq, op->stream);
+  });
+}
+
+emfgpu_status emfgpu_op_update_linearization(emfgpu_op* op, const double* d_u_k, int64_t* be, int* bq,
+                                             void* stream) {
+  if (!op || !d_u_k) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    cudaStream_t s = S(stream, op->stream);
+    CK(cudaMemcpyAsync(op->d_ukd, d_u_k, sizeof(double) * op->L->ndofs, cudaMemcpyDeviceToDevice, s));
+    op->checksum = 0;
+    linearize_impl(op, be, bq, s);
+  });
+}
+
+emfgpu_status emfgpu_op_apply(emfgpu_op* op, const void* d_x, void* d_y, void* stream) {
+  if (!op || !d_x || !d_y) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    require_linearized(op, "apply_tangent");
+    cudaStream_t s = S(stream, op->stream);
+    apply_elements(op, d_x, 0, op->L->nz, s);
+    apply_nodes(op, d_x, d_y, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+  });
+}
+
+emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y) {
+  if (!op || !x || !y) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    require_linearized(op, "apply_tangent");
+    CK(cudaSetDevice(op->L->device));
+    const size_t bytes = nsize(op) * op->L->ndofs;
+    if (!op->d_x) CK(cudaMalloc(&op->d_x, bytes));
+    if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
+    CK(cudaMemcpyAsync(op->d_x, x, bytes, cudaMemcpyHostToDevice, op->stream));
+    apply_elements(op, op->d_x, 0, op->L->nz, op->stream);
+    apply_nodes(op, op->d_x, op->d_y, 0, op->L->mz - 1, nullptr, nullptr, 0, op->stream);
+    CK(cudaMemcpyAsync(y, op->d_y, bytes, cudaMemcpyDeviceToHost, op->stream));
+    check_err(op, op->stream, nullptr, nullptr, "apply_tangent");
+  });
+}
+
+emfgpu_status emfgpu_op_check(emfgpu_op* op, int64_t* be, int* bq) {
+  if (!op) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    CK(cudaDeviceSynchronize());
+    check_err(op, op->stream, be, bq, "apply_tangent");
+  });
+}
+
+static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream_t s) {
+  require_linearized(op, "compute_diagonal");
+  const emfgpu_level* L = op->L;
+  unsigned long long* d_nbad = nullptr;
+  CK(cudaMallocAsync(&d_nbad, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(d_nbad, 0, sizeof(unsigned long long), s));
+  if (op->precision == 64) {
+    dispatch_diagonal<double>(op, kargs<double>(op), s);
+    double* d = static_cast<double*>(d_diag);
+    launch_node_gather<double>(static_cast<const double*>(op->d_loc), nullptr, nullptr, d, d, L->nx, L->ny, L->nz,
+                               L->p, 0, 0, 0, L->mz - 1, s);
+    launch_diag_finish<double>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, s);
+  } else {
+    dispatch_diagonal<float>(op, kargs<float>(op), s);
+    float* d = static_cast<float*>(d_diag);
+    launch_node_gather<float>(static_cast<const float*>(op->d_loc), nullptr, nullptr, d, d, L->nx, L->ny, L->nz,
+                              L->p, 0, 0, 0, L->mz - 1, s);
+    launch_diag_finish<float>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, s);
+  }
+  CK(cudaGetLastError());
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(op->h_err, d_nbad, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d_nbad, s));
+  CK(cudaStreamSynchronize(s));
+  h = *op->h_err;
+  *op->h_err = ~0ull;
+  if (nbad) *nbad = (int64_t)h;
+}
+
+emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* nbad, void* stream) {
+  if (!op || !d_diag) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    diagonal_impl(op, d_diag, nbad, S(stream, op->stream));
+  });
+}
+
+emfgpu_status emfgpu_op_compute_diagonal_host(emfgpu_op* op, void* diag, int64_t* nbad) {
+  if (!op || !diag) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    const size_t bytes = nsize(op) * op->L->ndofs;
+    if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
+    diagonal_impl(op, op->d_y, nbad, op->stream);
+    CK(cudaMemcpy(diag, op->d_y, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Per-qp bytes of the cell as stored here (the reference ledger, ledger.cpp:22-76,
+// with our SoA fields): geometry 80 B per qp (J0^-1 + det*w) or per element if
+// affine, u_k per DoF, caches per qp.
+emfgpu_status emfgpu_op_ledger(const emfgpu_op* op, int* storage, int* traffic, double* per_dof) {
+  if (!op) return EMFGPU_ERR_INVALID;
+  const emfgpu_level* L = op->L;
+  const int s = (int)nsize(op);
+  int fields = 0;
+  if (op->strategy == EMFGPU_CACHED_F) fields = 9;
+  if (op->strategy == EMFGPU_SCALAR || op->strategy == EMFGPU_TENSOR)
+    fields = (op->model == 0 ? 1 : 3) + (op->model == 2 ? 4 : 0);
+  if (op->strategy == EMFGPU_TENSOR) fields += 30;
+  const int geo = L->affine ? 0 : 10 * s;
+  if (storage) *storage = geo + fields * s;
+  if (traffic) *traffic = geo + fields * s;
+  if (per_dof) {
+    const bool uk = op->strategy == EMFGPU_NONE || op->strategy == EMFGPU_SCALAR;
+    const double qp = (double)(geo + fields * s) * L->nel * L->nq3;
+    const double el = L->affine ? 10.0 * s * L->nel : 0.0;
+    *per_dof = (qp + el) / L->ndofs + (uk ? 3 : 2) * s;
+  }
+  return EMFGPU_OK;
+}
+
+// ---- split apply (z slabs) --------------------------------------------------
+emfgpu_status emfgpu_op_apply_elements(emfgpu_op* op, const void* d_x, int k0, int k1, void* stream) {
+  if (!op || !d_x) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    require_linearized(op, "apply_tangent");
+    if (k0 < 0 || k1 > op->L->nz || k0 > k1) throw ApiError(EMFGPU_ERR_CONFIG, "apply_elements: bad layer range");
+    apply_elements(op, d_x, k0, k1, S(stream, op->stream));
+  });
+}
+
+emfgpu_status emfgpu_op_apply_nodes(emfgpu_op* op, const void* d_x, void* d_y, int c0, int c1, const void* glo,
+                                    const void* ghi, void* stream) {
+  if (!op || !d_x || !d_y) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    if (c0 < 0 || c1 >= op->L->mz || c0 > c1) throw ApiError(EMFGPU_ERR_CONFIG, "apply_nodes: bad plane range");
+    apply_nodes(op, d_x, d_y, c0, c1, glo, ghi, op->L->z_offset & 1, S(stream, op->stream));
+  });
+}
+
+void* emfgpu_op_local_buffer(emfgpu_op* op) { return op ? op->d_loc : nullptr; }
+int64_t emfgpu_op_face_values(const emfgpu_op* op) {
+  return op ? (int64_t)op->L->nx * op->L->ny * (op->L->p + 1) * (op->L->p + 1) * 3 : 0;
+}
+
+emfgpu_status emfgpu_op_pack_face(emfgpu_op* op, int k, int side, void* d_face, void* stream) {
+  if (!op || !d_face) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    const emfgpu_level* L = op->L;
+    if (k < 0 || k >= L->nz) throw ApiError(EMFGPU_ERR_CONFIG, "pack_face: bad layer");
+    cudaStream_t s = S(stream, op->stream);
+    if (op->precision == 64)
+      launch_pack_face<double>(static_cast<const double*>(op->d_loc), static_cast<double*>(d_face), L->nx, L->ny,
+                               L->p, k, side, s);
+    else
+      launch_pack_face<float>(static_cast<const float*>(op->d_loc), static_cast<float*>(d_face), L->nx, L->ny, L->p,
+                              k, side, s);
+    CK(cudaGetLastError());
+  });
+}
+
+// ---- transfers (mesh.hpp:157-289, mesh.cpp:248-288) ---------------------------
+static void build_axis(emfgpu_transfer::Axis& ax, int n_src, int p_src, int n_dst, int p_dst) {
+  ax.n_src = n_src;
+  ax.p_src = p_src;
+  ax.n_dst = n_dst;
+  ax.p_dst = p_dst;
+  const std::vector<double> sn = lobatto_nodes(p_src + 1), dn = lobatto_nodes(p_dst + 1);
+  const int nd = n_dst * p_dst + 1, stencil = p_src + 1, ns = n_src * p_src + 1;
+  std::vector<int> se(nd);
+  std::vector<double> w((size_t)nd * stencil);
+  for (int d = 0; d < nd; ++d) {
+    const int e_dst = std::min(d / p_dst, n_dst - 1);
+    const int l_dst = d - e_dst * p_dst;
+    const double s = (e_dst + 0.5 * (dn[l_dst] + 1.0)) / n_dst;
+    int e_src = std::min((int)(s * n_src), n_src - 1);
+    if (e_src > 0 && s * n_src <= e_src) e_src = e_src - (s * n_src < e_src);
+    const double xi = 2.0 * (s * n_src - e_src) - 1.0;
+    se[d] = e_src;
+    for (int i = 0; i < stencil; ++i) w[(size_t)d * stencil + i] = lagrange(sn, i, xi);
+  }
+  // transposed CSR: for each source index t, the (d, s) pairs in ascending d
+  std::vector<std::vector<std::pair<int, int>>> lists(ns);
+  for (int d = 0; d < nd; ++d)
+    for (int s = 0; s < stencil; ++s) lists[se[d] * p_src + s].push_back({d, s});
+  std::vector<int> ptr(ns + 1, 0), td, ts;
+  for (int t = 0; t < ns; ++t) {
+    ptr[t + 1] = ptr[t] + (int)lists[t].size();
+    for (auto& pr : lists[t]) {
+      td.push_back(pr.first);
+      ts.push_back(pr.second);
+    }
+  }
+  CK(cudaMalloc(&ax.src_elem, sizeof(int) * nd));
+  CK(cudaMalloc(&ax.w, sizeof(double) * w.size()));
+  CK(cudaMalloc(&ax.t_ptr, sizeof(int) * ptr.size()));
+  CK(cudaMalloc(&ax.t_d, sizeof(int) * std::max<size_t>(1, td.size())));
+  CK(cudaMalloc(&ax.t_s, sizeof(int) * std::max<size_t>(1, ts.size())));
+  CK(cudaMemcpy(ax.src_elem, se.data(), sizeof(int) * nd, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ax.w, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ax.t_ptr, ptr.data(), sizeof(int) * ptr.size(), cudaMemcpyHostToDevice));
+  if (!td.empty()) {
+    CK(cudaMemcpy(ax.t_d, td.data(), sizeof(int) * td.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ax.t_s, ts.data(), sizeof(int) * ts.size(), cudaMemcpyHostToDevice));
+  }
+}
+
+static void free_axis(emfgpu_transfer::Axis& ax) {
+  cudaFree(ax.src_elem);
+  cudaFree(ax.w);
+  cudaFree(ax.t_ptr);
+  cudaFree(ax.t_d);
+  cudaFree(ax.t_s);
+}
+
+emfgpu_status emfgpu_transfer_create(const emfgpu_level* fine, const emfgpu_level* coarse, emfgpu_transfer** out) {
+  if (!fine || !coarse || !out) return EMFGPU_ERR_INVALID;
+  *out = nullptr;
+  auto t = std::make_unique<emfgpu_transfer>();
+  emfgpu_status st = guarded(nullptr, [&] {
+    const int nf[3] = {fine->nx, fine->ny, fine->nz}, nc[3] = {coarse->nx, coarse->ny, coarse->nz};
+    const bool p_step = nf[0] == nc[0] && nf[1] == nc[1] && nf[2] == nc[2] && fine->p > coarse->p;
+    const bool h_step = fine->p == coarse->p && nf[0] == 2 * nc[0] && nf[1] == 2 * nc[1] && nf[2] == 2 * nc[2];
+    if (!p_step && !h_step)
+      throw ApiError(EMFGPU_ERR_CONFIG, "TransferOp: levels must differ by a p-coarsening or one uniform refinement");
+    CK(cudaSetDevice(fine->device));
+    t->fine = fine;
+    t->coarse = coarse;
+    for (int a = 0; a < 3; ++a) {
+      build_axis(t->up[a], nc[a], coarse->p, nf[a], fine->p);
+      build_axis(t->down[a], nf[a], fine->p, nc[a], coarse->p);
+    }
+    t->tmp_bytes = sizeof(double) * 3 * (size_t)std::max(fine->mx, coarse->mx) * std::max(fine->my, coarse->my) *
+                   std::max(fine->mz, coarse->mz);
+    CK(cudaMalloc(&t->tmp[0], t->tmp_bytes));
+    CK(cudaMalloc(&t->tmp[1], t->tmp_bytes));
+  });
+  if (st != EMFGPU_OK) {
+    emfgpu_transfer_destroy(t.release());
+    return st;
+  }
+  *out = t.release();
+  return EMFGPU_OK;
+}
+
+void emfgpu_transfer_destroy(emfgpu_transfer* t) {
+  if (!t) return;
+  for (int a = 0; a < 3; ++a) {
+    free_axis(t->up[a]);
+    free_axis(t->down[a]);
+  }
+  cudaFree(t->tmp[0]);
+  cudaFree(t->tmp[1]);
+  delete t;
+}
+
+template <typename T>
+static void transfer_run(emfgpu_transfer* t, int kind, const T* in, T* out, cudaStream_t s) {
+  // apply_axes (mesh.hpp:245-271): axis 0, then 1, then 2; source/destination
+  // lattices are coarse->fine (prolongate), fine->coarse (restrict, transposed
+  // up-map; interpolate_down, down-map).
+  const emfgpu_level* src = kind == 0 ? t->coarse : t->fine;
+  const emfgpu_level* dst = kind == 0 ? t->fine : t->coarse;
+  const emfgpu_transfer::Axis* ax = kind == 2 ? t->down : t->up;
+  const int transpose = kind == 1;
+  const int ms[3] = {src->mx, src->my, src->mz}, md[3] = {dst->mx, dst->my, dst->mz};
+  T* b0 = static_cast<T*>(t->tmp[0]);
+  T* b1 = static_cast<T*>(t->tmp[1]);
+  launch_transfer_axis<T>(in, b0, ax[0].src_elem, ax[0].w, ax[0].t_ptr, ax[0].t_d, ax[0].t_s, ax[0].p_src + 1,
+                          ax[0].p_src, transpose, 0, ms[0], ms[1], ms[2], md[0], s);
+  launch_transfer_axis<T>(b0, b1, ax[1].src_elem, ax[1].w, ax[1].t_ptr, ax[1].t_d, ax[1].t_s, ax[1].p_src + 1,
+                          ax[1].p_src, transpose, 1, md[0], ms[1], ms[2], md[1], s);
+  launch_transfer_axis<T>(b1, out, ax[2].src_elem, ax[2].w, ax[2].t_ptr, ax[2].t_d, ax[2].t_s, ax[2].p_src + 1,
+                          ax[2].p_src, transpose, 2, md[0], md[1], ms[2], md[2], s);
+}
+
+emfgpu_status emfgpu_transfer_apply(emfgpu_transfer* t, int kind, int precision, const void* in, void* out,
+                                    void* stream) {
+  if (!t || !in || !out) return EMFGPU_ERR_INVALID;
+  return guarded(&t->last_error, [&] {
+    if (kind < 0 || kind > 2) throw ApiError(EMFGPU_ERR_CONFIG, "transfer: kind must be 0,1,2");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (precision == 64)
+      transfer_run<double>(t, kind, static_cast<const double*>(in), static_cast<double*>(out), s);
+    else if (precision == 32)
+      transfer_run<float>(t, kind, static_cast<const float*>(in), static_cast<float*>(out), s);
+    else
+      throw ApiError(EMFGPU_ERR_CONFIG, "transfer: precision must be 64 or 32");
+    CK(cudaGetLastError());
+  });
+}
+
+// ---- Chebyshev (solver.hpp:312-362) -----------------------------------------
+emfgpu_status emfgpu_cheb_create(emfgpu_op* op, const void* d_diag, double lmax_est, int degree, double range_factor,
+                                 double safety, emfgpu_cheb** out) {
+  if (!op || !d_diag || !out) return EMFGPU_ERR_INVALID;
+  *out = nullptr;
+  auto c = std::make_unique<emfgpu_cheb>();
+  emfgpu_status st = guarded(&op->last_error, [&] {
+    if (degree < 1) throw ApiError(EMFGPU_ERR_CONFIG, "chebyshev: degree must be >= 1");
+    CK(cudaSetDevice(op->L->device));
+    c->op = op;
+    c->degree = degree;
+    c->lambda_max = safety * lmax_est;
+    c->lambda_min = c->lambda_max / range_factor;
+    const size_t bytes = nsize(op) * op->L->ndofs;
+    CK(cudaMalloc(&c->inv_diag, bytes));
+    CK(cudaMalloc(&c->r, bytes));
+    CK(cudaMalloc(&c->d, bytes));
+    CK(cudaMalloc(&c->ad, bytes));
+    if (op->precision == 64)
+      launch_inv<double>(static_cast<const double*>(d_diag), static_cast<double*>(c->inv_diag), op->L->ndofs,
+                         op->stream);
+    else
+      launch_inv<float>(static_cast<const float*>(d_diag), static_cast<float*>(c->inv_diag), op->L->ndofs, op->stream);
+    CK(cudaStreamSynchronize(op->stream));
+  });
+  if (st != EMFGPU_OK) {
+    emfgpu_cheb_destroy(c.release());
+    return st;
+  }
+  *out = c.release();
+  return EMFGPU_OK;
+}
+
+void emfgpu_cheb_destroy(emfgpu_cheb* c) {
+  if (!c) return;
+  cudaFree(c->inv_diag);
+  cudaFree(c->r);
+  cudaFree(c->d);
+  cudaFree(c->ad);
+  delete c;
+}
+
+template <typename T>
+static void cheb_run(emfgpu_cheb* c, T* x, const T* b, int zero_start, cudaStream_t s) {
+  emfgpu_op* op = c->op;
+  const int64_t n = op->L->ndofs;
+  const double theta = 0.5 * (c->lambda_max + c->lambda_min);
+  const double delta = 0.5 * (c->lambda_max - c->lambda_min);
+  const double sigma1 = theta / delta;
+  double rho_old = 1.0 / sigma1;
+  T* r = static_cast<T*>(c->r);
+  T* d = static_cast<T*>(c->d);
+  T* ad = static_cast<T*>(c->ad);
+  const T* inv = static_cast<const T*>(c->inv_diag);
+  if (!zero_start) {
+    apply_elements(op, x, 0, op->L->nz, s);
+    apply_nodes(op, x, r, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+  }
+  launch_cheb_first<T>(x, r, d, b, inv, 1.0 / theta, zero_start, n, s);
+  for (int k = 1; k < c->degree; ++k) {
+    apply_elements(op, d, 0, op->L->nz, s);
+    apply_nodes(op, d, ad, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+    const double rho_new = 1.0 / (2.0 * sigma1 - rho_old);
+    launch_cheb_step<T>(x, r, d, ad, inv, rho_new * rho_old, 2.0 * rho_new / delta, n, s);
+    rho_old = rho_new;
+  }
+}
+
+emfgpu_status emfgpu_cheb_smooth(emfgpu_cheb* c, void* d_x, const void* d_b, int zero_start, void* stream) {
+  if (!c || !d_x || !d_b) return EMFGPU_ERR_INVALID;
+  return guarded(&c->op->last_error, [&] {
+    require_linearized(c->op, "chebyshev");
+    cudaStream_t s = S(stream, c->op->stream);
+    if (c->op->precision == 64)
+      cheb_run<double>(c, static_cast<double*>(d_x), static_cast<const double*>(d_b), zero_start, s);
+    else
+      cheb_run<float>(c, static_cast<float*>(d_x), static_cast<const float*>(d_b), zero_start, s);
+    CK(cudaGetLastError());
+  });
+}
+
+// ---- dot & Lanczos (solver.hpp:95-106, 235-308) --------------------------------
+emfgpu_status emfgpu_dot(int precision, const void* a, const void* b, int64_t n, double* out, void* stream) {
+  if (!a || !b || !out) return EMFGPU_ERR_INVALID;
+  return guarded(nullptr, [&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* buf = nullptr;
+    CK(cudaMallocAsync(&buf, sizeof(double) * (dot_partial_count() + 1), s));
+    if (precision == 64)
+      launch_dot<double>(static_cast<const double*>(a), static_cast<const double*>(b), n, buf + 1, buf, s);
+    else
+      launch_dot<float>(static_cast<const float*>(a), static_cast<const float*>(b), n, buf + 1, buf, s);
+    CK(cudaMemcpyAsync(out, buf, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(buf, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+namespace {
+int sturm_count(const std::vector<double>& al, const std::vector<double>& be, double sigma) {
+  int count = 0;
+  double d = al[0] - sigma;
+  if (d < 0) ++count;
+  for (size_t i = 1; i < al.size(); ++i) {
+    d = al[i] - sigma - be[i - 1] * be[i - 1] / (d == 0 ? 1e-300 : d);
+    if (d < 0) ++count;
+  }
+  return count;
+}
+double tridiag_extreme(const std::vector<double>& al, const std::vector<double>& be, bool largest) {
+  double lo = al[0], hi = al[0];
+  for (size_t i = 0; i < al.size(); ++i) {
+    const double bl = i > 0 ? std::abs(be[i - 1]) : 0.0;
+    const double br = i < be.size() ? std::abs(be[i]) : 0.0;
+    lo = std::min(lo, al[i] - bl - br);
+    hi = std::max(hi, al[i] + bl + br);
+  }
+  const int nev = (int)al.size();
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const int below = sturm_count(al, be, mid);
+    if (largest ? below < nev : below < 1)
+      lo = mid;
+    else
+      hi = mid;
+    if (hi - lo < 1e-10 * std::max(1.0, std::abs(hi))) break;
+  }
+  return 0.5 * (lo + hi);
+}
+}  // namespace
+
+template <typename T>
+static void lanczos(emfgpu_op* op, const T* diag, int iterations, uint64_t seed, double* lmin, double* lmax,
+                    cudaStream_t s) {
+  const int64_t n = op->L->ndofs;
+  const int maxit = (int)std::min<int64_t>(iterations, n);
+  // start vector: splitmix64 uniform01 - 0.5 (solver.hpp:274-277), normalised
+  std::vector<double> hv(n);
+  uint64_t state = seed;
+  for (auto& x : hv) {
+    state += 0x9e3779b97f4a7c15ull;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    x = (double)(z >> 11) * 0x1.0p-53 - 0.5;
+  }
+  double nv = 0;
+  for (double x : hv) nv += x * x;
+  nv = std::sqrt(nv);
+  for (auto& x : hv) x /= nv;
+  double *dis, *basis, *w, *dbuf;
+  T *t, *at;
+  CK(cudaMalloc(&dis, sizeof(double) * n));
+  CK(cudaMalloc(&basis, sizeof(double) * n * std::max(1, maxit)));
+  CK(cudaMalloc(&w, sizeof(double) * n));
+  CK(cudaMalloc(&dbuf, sizeof(double) * (dot_partial_count() + 1)));
+  CK(cudaMalloc(&t, sizeof(T) * n));
+  CK(cudaMalloc(&at, sizeof(T) * n));
+  CK(cudaMemcpyAsync(basis, hv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  launch_dinv_sqrt<T>(diag, dis, n, s);
+  auto dot = [&](const double* x, const double* y) {
+    launch_dot<double>(x, y, n, dbuf + 1, dbuf, s);
+    double r;
+    CK(cudaMemcpyAsync(&r, dbuf, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return r;
+  };
+  std::vector<double> alpha, beta;
+  double beta_prev = 0.0;
+  for (int j = 0; j < maxit; ++j) {
+    double* v = basis + (size_t)j * n;
+    launch_scale_to_T<T>(dis, v, t, n, s);
+    apply_elements(op, t, 0, op->L->nz, s);
+    apply_nodes(op, t, at, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+    launch_scale_from_T<T>(dis, at, w, n, s);
+    if (j > 0) launch_axpy_minus(beta_prev, basis + (size_t)(j - 1) * n, w, n, s);
+    const double a = dot(w, v);
+    alpha.push_back(a);
+    launch_axpy_minus(a, v, w, n, s);
+    for (int qb = 0; qb <= j; ++qb) {
+      const double* q = basis + (size_t)qb * n;
+      launch_axpy_minus(dot(w, q), q, w, n, s);
+    }
+    const double b = std::sqrt(dot(w, w));
+    if (j + 1 < maxit) beta.push_back(b);
+    if (b < 1e-12) break;
+    if (j + 1 < maxit) launch_div(w, b, basis + (size_t)(j + 1) * n, n, s);
+    beta_prev = b;
+  }
+  beta.resize(alpha.empty() ? 0 : alpha.size() - 1);
+  *lmax = tridiag_extreme(alpha, beta, true);
+  *lmin = tridiag_extreme(alpha, beta, false);
+  cudaFree(dis);
+  cudaFree(basis);
+  cudaFree(w);
+  cudaFree(dbuf);
+  cudaFree(t);
+  cudaFree(at);
+}
+
+emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, int iterations, uint64_t seed,
+                                             double* lmin, double* lmax) {
+  if (!op || !d_diag || !lmin || !lmax) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    require_linearized(op, "estimate_eigenvalues");
+    CK(cudaSetDevice(op->L->device));
+    if (op->precision == 64)
+      lanczos<double>(op, static_cast<const double*>(d_diag), iterations, seed, lmin, lmax, op->stream);
+    else
+      lanczos<float>(op, static_cast<const float*>(d_diag), iterations, seed, lmin, lmax, op->stream);
+  });
+}
+

@@ -1,0 +1,177 @@
+// Node phase of the tangent apply: deterministic assembly of element-local
+// results onto the lattice, one thread per node, in the reference's colour
+// order.  The reference adds element results colour by colour
+// (colour = (i&1) + 2(j&1) + 4(k&1), operator.hpp:145-153, 439), so every
+// DoF accumulates its <=8 contributions sorted by (k parity, j parity,
+// i parity); summing in exactly that order here reproduces the reference's
+// association of the scatter sums, with no atomics and no colour passes.
+// Dirichlet rows return the input (operator.hpp:617-620).
+#include "internal.h"
+
+namespace emfgpu {
+
+// Candidate elements along one axis for lattice coordinate a (element size p,
+// n elements, lattice size m), sorted even-index first. Local node index in
+// the element along that axis is returned in loc[].  lo/hi ghost layers are
+// allowed along z (index -1 and n).
+__device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bool ghosts, int* el, int* loc) {
+  const int e1 = a / p;
+  if (a % p == 0) {
+    const bool has_lo = a > 0 || ghosts;
+    const bool has_hi = a < n * p || ghosts;
+    int cnt = 0;
+    int c_el[2], c_loc[2];
+    if (has_lo) {
+      c_el[cnt] = e1 - 1;
+      c_loc[cnt] = p;
+      ++cnt;
+    }
+    if (has_hi) {
+      c_el[cnt] = e1;
+      c_loc[cnt] = 0;
+      ++cnt;
+    }
+    if (cnt == 2 && (((c_el[0] + gpar) & 1) != 0)) {  // odd first -> swap so even (global) goes first
+      el[0] = c_el[1];
+      loc[0] = c_loc[1];
+      el[1] = c_el[0];
+      loc[1] = c_loc[0];
+    } else {
+      for (int t = 0; t < cnt; ++t) {
+        el[t] = c_el[t];
+        loc[t] = c_loc[t];
+      }
+    }
+    return cnt;
+  }
+  el[0] = e1;
+  loc[0] = a - e1 * p;
+  return 1;
+}
+
+template <typename T>
+__global__ void node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
+                                   const T* __restrict__ ghost_hi, const T* x, T* y,
+                                   int nx, int ny, int nz, int p, int faces, int kpar, int c0, int c1) {
+  const int mx = nx * p + 1, my = ny * p + 1, mz = nz * p + 1;
+  const int64_t plane = (int64_t)mx * my;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (int64_t)c0 * plane;
+  if (idx >= (int64_t)(c1 + 1) * plane) return;
+  const int a = (int)(idx % mx);
+  const int b = (int)((idx / mx) % my);
+  const int c = (int)(idx / plane);
+  if (node_constrained(a, b, c, mx, my, mz, faces)) {
+    y[3 * idx] = x[3 * idx];
+    y[3 * idx + 1] = x[3 * idx + 1];
+    y[3 * idx + 2] = x[3 * idx + 2];
+    return;
+  }
+  const int N = p + 1, N3 = N * N * N, N2 = N * N;
+  int ie[2], il[2], je[2], jl[2], ke[2], kl[2];
+  const int ni = axis_candidates(a, p, nx, 0, false, ie, il);
+  const int nj = axis_candidates(b, p, ny, 0, false, je, jl);
+  const bool ghosts = ghost_lo != nullptr || ghost_hi != nullptr;
+  int nk = axis_candidates(c, p, nz, kpar, ghosts, ke, kl);
+  T s0 = T(0), s1 = T(0), s2 = T(0);
+  bool first = true;
+  for (int tk = 0; tk < nk; ++tk) {
+    const int k = ke[tk];
+    const T* src;
+    for (int tj = 0; tj < nj; ++tj)
+      for (int ti = 0; ti < ni; ++ti) {
+        int64_t off;
+        if (k < 0 || k >= nz) {
+          src = k < 0 ? ghost_lo : ghost_hi;
+          if (!src) continue;
+          off = ((((int64_t)je[tj] * nx + ie[ti]) * N2) + jl[tj] * N + il[ti]) * 3;
+        } else {
+          src = loc;
+          const int64_t e = ((int64_t)k * ny + je[tj]) * nx + ie[ti];
+          off = (e * N3 + (kl[tk] * N + jl[tj]) * N + il[ti]) * 3;
+        }
+        const T v0 = src[off], v1 = src[off + 1], v2 = src[off + 2];
+        if (first) {
+          s0 = v0;
+          s1 = v1;
+          s2 = v2;
+          first = false;
+        } else {
+          s0 += v0;
+          s1 += v1;
+          s2 += v2;
+        }
+      }
+  }
+  y[3 * idx] = s0;
+  y[3 * idx + 1] = s1;
+  y[3 * idx + 2] = s2;
+}
+
+template <typename T>
+void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny, int nz,
+                        int p, int faces, int kpar, int c0, int c1, cudaStream_t s) {
+  const int64_t plane = (int64_t)(nx * p + 1) * (ny * p + 1);
+  const int64_t cnt = (int64_t)(c1 - c0 + 1) * plane;
+  if (cnt <= 0) return;
+  const int bs = 256;
+  node_gather_kernel<T><<<(unsigned)((cnt + bs - 1) / bs), bs, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, p,
+                                                                        faces, kpar, c0, c1);
+}
+
+// Face of element layer k: lower (side 0, local c=0) or upper (side 1, c=p)
+// node plane of each element's local results, ((j*nx+i)*N2 + b*N + a)*3 + comp.
+template <typename T>
+__global__ void pack_face_kernel(const T* __restrict__ loc, T* __restrict__ face, int nx, int ny, int p, int k,
+                                 int side) {
+  const int N = p + 1, N2 = N * N, N3 = N2 * N;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)nx * ny * N2 * 3;
+  if (idx >= total) return;
+  const int comp = (int)(idx % 3);
+  const int64_t fn = idx / 3;
+  const int m2 = (int)(fn % N2);
+  const int64_t ij = fn / N2;
+  const int64_t e = (int64_t)k * nx * ny + ij;
+  const int lc = side ? p : 0;
+  face[idx] = loc[(e * N3 + lc * N2 + m2) * 3 + comp];
+}
+
+template <typename T>
+void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int side, cudaStream_t s) {
+  const int64_t total = (int64_t)nx * ny * (p + 1) * (p + 1) * 3;
+  pack_face_kernel<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(loc, face, nx, ny, p, k, side);
+}
+
+// Diagonal epilogue: constrained rows -> 1, count free rows with d <= 0
+// (operator.hpp:869-877).
+template <typename T>
+__global__ void diag_finish_kernel(T* d, int64_t nnodes, int mx, int my, int mz, int faces,
+                                   unsigned long long* nbad) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nnodes) return;
+  const int a = (int)(idx % mx), b = (int)((idx / mx) % my), c = (int)(idx / ((int64_t)mx * my));
+  if (node_constrained(a, b, c, mx, my, mz, faces)) {
+    d[3 * idx] = d[3 * idx + 1] = d[3 * idx + 2] = T(1);
+    return;
+  }
+  int bad = 0;
+  for (int comp = 0; comp < 3; ++comp) bad += !(d[3 * idx + comp] > T(0));
+  if (bad) atomicAdd(nbad, (unsigned long long)bad);
+}
+
+template <typename T>
+void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces, unsigned long long* nbad,
+                        cudaStream_t s) {
+  diag_finish_kernel<T><<<(unsigned)((nnodes + 255) / 256), 256, 0, s>>>(d, nnodes, mx, my, mz, faces, nbad);
+}
+
+template void launch_node_gather<double>(const double*, const double*, const double*, const double*, double*, int,
+                                         int, int, int, int, int, int, int, cudaStream_t);
+template void launch_node_gather<float>(const float*, const float*, const float*, const float*, float*, int, int,
+                                        int, int, int, int, int, int, cudaStream_t);
+template void launch_pack_face<double>(const double*, double*, int, int, int, int, int, cudaStream_t);
+template void launch_pack_face<float>(const float*, float*, int, int, int, int, int, cudaStream_t);
+template void launch_diag_finish<double>(double*, int64_t, int, int, int, int, unsigned long long*, cudaStream_t);
+template void launch_diag_finish<float>(float*, int64_t, int, int, int, int, unsigned long long*, cudaStream_t);
+
+}  // namespace emfgpu

@@ -1,0 +1,53 @@
+// Explicit instantiation of the element kernels for one (Number, degree).
+// Included by inst_<t><p>.cu with EMF_T and EMF_P defined, so the 8 units
+// compile in parallel.
+#include "internal.h"
+
+namespace emfgpu {
+
+template <int MODEL, int STRAT>
+static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
+  constexpr int N = EMF_P + 1, EPB = Tile<EMF_P>::EPB;
+  const int64_t cnt = e1 - e0;
+  if (cnt <= 0) return;
+  KArgs<EMF_T> b = a;
+  b.e_begin = e0;
+  b.nel = e1;
+  const int64_t blocks = (cnt + EPB - 1) / EPB;
+  apply_kernel<EMF_T, EMF_P, MODEL, STRAT><<<(unsigned)blocks, EPB * N * N * N, 0, s>>>(b);
+}
+
+template <>
+void launch_apply<EMF_T, EMF_P>(int model, int strategy, const KArgs<EMF_T>& a, int64_t e0, int64_t e1,
+                               cudaStream_t s) {
+#define EMF_CASE(M, S) \
+  if (model == M && strategy == S) return apply_one<M, S>(a, e0, e1, s);
+  EMF_CASE(CNH, S_NONE) EMF_CASE(CNH, S_SCALAR) EMF_CASE(CNH, S_TENSOR) EMF_CASE(CNH, S_CACHEDF)
+  EMF_CASE(INH, S_NONE) EMF_CASE(INH, S_SCALAR) EMF_CASE(INH, S_TENSOR) EMF_CASE(INH, S_CACHEDF)
+  EMF_CASE(FIBER, S_NONE) EMF_CASE(FIBER, S_SCALAR) EMF_CASE(FIBER, S_TENSOR) EMF_CASE(FIBER, S_CACHEDF)
+#undef EMF_CASE
+}
+
+template <>
+void launch_linearize<EMF_T, EMF_P>(int model, const KArgs<EMF_T>& a, cudaStream_t s) {
+  constexpr int N = EMF_P + 1, EPB = Tile<EMF_P>::EPB;
+  KArgs<EMF_T> b = a;
+  b.e_begin = 0;
+  const unsigned blocks = (unsigned)((a.nel + EPB - 1) / EPB);
+  if (model == CNH) linearize_kernel<EMF_T, EMF_P, CNH><<<blocks, EPB * N * N * N, 0, s>>>(b);
+  if (model == INH) linearize_kernel<EMF_T, EMF_P, INH><<<blocks, EPB * N * N * N, 0, s>>>(b);
+  if (model == FIBER) linearize_kernel<EMF_T, EMF_P, FIBER><<<blocks, EPB * N * N * N, 0, s>>>(b);
+}
+
+template <>
+void launch_diagonal<EMF_T, EMF_P>(int model, const KArgs<EMF_T>& a, cudaStream_t s) {
+  constexpr int N = EMF_P + 1, EPB = Tile<EMF_P>::EPB;
+  KArgs<EMF_T> b = a;
+  b.e_begin = 0;
+  const unsigned blocks = (unsigned)((a.nel + EPB - 1) / EPB);
+  if (model == CNH) diagonal_kernel<EMF_T, EMF_P, CNH><<<blocks, EPB * N * N * N, 0, s>>>(b);
+  if (model == INH) diagonal_kernel<EMF_T, EMF_P, INH><<<blocks, EPB * N * N * N, 0, s>>>(b);
+  if (model == FIBER) diagonal_kernel<EMF_T, EMF_P, FIBER><<<blocks, EPB * N * N * N, 0, s>>>(b);
+}
+
+}  // namespace emfgpu

@@ -1,0 +1,102 @@
+// Internal declarations shared by the CUDA translation units of libemfgpu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/emfgpu.h"
+#include "kernels.cuh"
+
+namespace emfgpu {
+
+constexpr int kMaxP = 4;
+
+// Per-(T,P) launchers, defined in inst_<t><p>.cu.
+template <typename T, int P>
+void launch_apply(int model, int strategy, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s);
+template <typename T, int P>
+void launch_linearize(int model, const KArgs<T>& a, cudaStream_t s);
+template <typename T, int P>
+void launch_diagonal(int model, const KArgs<T>& a, cudaStream_t s);
+
+// gather.cu
+template <typename T>
+void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny,
+                        int nz, int p, int faces, int kpar, int c0, int c1, cudaStream_t s);
+template <typename T>
+void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int side, cudaStream_t s);
+template <typename T>
+void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces, unsigned long long* nbad,
+                        cudaStream_t s);
+
+// geometry.cu
+void launch_geometry(const double* coords, double* geo_q, double* j0_out, int nx, int ny, int nz, int p,
+                     const double* B, const double* D, const double* qw, int* nonaffine, int* degenerate,
+                     cudaStream_t s);
+void launch_geo_compact(const double* geo_q, double* geo_e, int64_t nel, int nq3, cudaStream_t s);
+void launch_cast_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
+
+// solver.cu
+template <typename T>
+void launch_transfer_axis(const T* in, T* out, const int* src_elem, const double* w, const int* t_ptr, const int* t_d,
+                          const int* t_s, int stencil, int p_src, int transpose, int axis, int in0, int in1, int in2,
+                          int out_na, cudaStream_t s);
+template <typename T>
+void launch_cheb_first(T* x, T* r, T* d, const T* b, const T* inv_diag, double inv_theta, int zero_start, int64_t n,
+                       cudaStream_t s);
+template <typename T>
+void launch_cheb_step(T* x, T* r, T* d, const T* ad, const T* inv_diag, double f1, double f2, int64_t n,
+                      cudaStream_t s);
+template <typename T>
+void launch_inv(const T* d, T* inv, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_dot(const T* a, const T* b, int64_t n, double* partial, double* out, cudaStream_t s);
+int dot_partial_count();
+template <typename T>
+void launch_scale_to_T(const double* s, const double* v, T* t, int64_t n, cudaStream_t st);
+template <typename T>
+void launch_scale_from_T(const double* s, const T* at, double* w, int64_t n, cudaStream_t st);
+template <typename T>
+void launch_dinv_sqrt(const T* d, double* s, int64_t n, cudaStream_t st);
+void launch_axpy_minus(double a, const double* x, double* y, int64_t n, cudaStream_t st);
+void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st);
+
+}  // namespace emfgpu
+
+struct emfgpu_level {
+  int nx = 0, ny = 0, nz = 0, p = 0, mx = 0, my = 0, mz = 0;
+  int64_t nnodes = 0, ndofs = 0, nel = 0, nq3 = 0;
+  int faces = 0, device = 0, affine = 0, z_offset = 0;
+  double extent[3] = {1, 1, 1};
+  // basis tables (host): GLL nodes, Gauss points/weights, B/D (row = qp)
+  std::vector<double> nodes, qpts, qwts, B, D;
+  double* d_coords = nullptr;  // 3 per node
+  double* d_geo = nullptr;     // SoA, 10 fields: J0^-1 (9), det J0 * w_q (or det J0 if affine)
+  float* d_geo_f = nullptr;
+  int64_t geo_stride = 0;
+  std::string last_error;
+};
+
+struct emfgpu_op {
+  const emfgpu_level* L = nullptr;
+  int model = 0, strategy = 0, precision = 64;
+  emfgpu_material params{};
+  emfgpu::MatConst<double> matd{};
+  emfgpu::MatConst<float> matf{};
+  void* d_cache = nullptr;
+  int64_t cache_stride = 0;
+  int n_cache_fields = 0;
+  void* d_uk = nullptr;        // u_k in Number (none/scalar)
+  double* d_ukd = nullptr;     // u_k in double (transfers / host checks)
+  void* d_loc = nullptr;       // element-local results, nel*nn3*3 Number
+  void* d_x = nullptr;         // staging for host entry points
+  void* d_y = nullptr;
+  unsigned long long* d_err = nullptr;
+  unsigned long long* h_err = nullptr;  // pinned
+  cudaStream_t stream = nullptr;
+  bool linearized = false;
+  uint64_t checksum = 0;
+  std::string last_error;
+};

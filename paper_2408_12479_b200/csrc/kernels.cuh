@@ -1,0 +1,590 @@
+// Element-batched, sum-factorized tangent kernels for sm_100a.
+//
+// Mapping (B200-first): one CUDA thread per quadrature
+// point, EPB elements per CTA, the whole element pipeline fused in one
+// kernel: lattice gather of the DoF vector -> 8 forward sweeps per component
+// through shared memory -> per-qp material kernel in registers -> 8 merged
+// transposed sweeps -> element-local result written to an L2-resident buffer.
+// A separate node-centric kernel (gather.cu) sums the element contributions
+// of every lattice node in the reference's colour order, which makes fp64
+// results deterministic and equal-order to the reference's 8-colour scatter
+// (operator.hpp:145-153, 439).
+//
+// Reference correspondence:
+//   gather / scatter        operator.hpp:237-276 (DoF = 3*node+c)
+//   gradient_at_qpoints     sumfact.hpp:67-85
+//   scatter_gradient_...    sumfact.hpp:90-110 (merged: Dx*Q0 + Bx*(Dy A1 + By A2))
+//   element_tangent_batch   operator.hpp:468-530
+//   update_linearization    operator.hpp:643-770
+//   compute_diagonal        operator.hpp:772-878 (as a per-qp 3x3 quadratic form,
+//                           not 3(p+1)^3 local unit applies)
+#pragma once
+#include "qp.cuh"
+
+namespace emfgpu {
+
+// elements per CTA for degree P (threads = EPB * (P+1)^3)
+template <int P>
+struct Tile;
+template <>
+struct Tile<1> { static constexpr int EPB = 16; };
+template <>
+struct Tile<2> { static constexpr int EPB = 4; };
+template <>
+struct Tile<3> { static constexpr int EPB = 2; };
+template <>
+struct Tile<4> { static constexpr int EPB = 1; };
+
+// cache field slots (SoA, field f at cache + f*stride), per strategy
+enum CacheSlot : int {
+  // scalar/tensor: scalars first
+  C_LNJ = 0, C_JP = 1, C_C1 = 2, C_C2 = 3, C_C3 = 4, C_EF = 6,
+  // tensor: then F, Finv, S, Cinv
+  C_F = 8, C_FINV = 17, C_S = 26, C_CINV = 32, C_NT = 38,
+  // cachedF: displacement gradient G = F - I
+  C_G = 0, C_NG = 9
+};
+
+template <typename T>
+struct KArgs {
+  const T* x;          // input vector (3 per node), apply / unused by diag
+  T* loc;              // element-local output, (e*nn3 + m)*3 + c
+  const T* uk;         // linearization point in T (none/scalar), 3 per node
+  const double* ukd;   // linearization point in double (linearize only)
+  const T* geo;        // J0^-1 (9) + detw (1), SoA with stride geo_stride
+  const double* geod;  // same, double (linearize)
+  int64_t geo_stride;
+  int affine;          // geometry per element instead of per qp
+  T* cache;            // SoA fields
+  int64_t cache_stride;
+  int strategy;        // runtime strategy for linearize/diagonal
+  int nx, ny, nz, mx, my, mz;
+  int64_t nel;
+  int64_t e_begin;     // first element of the processed range (boundary/interior split)
+  int faces;           // Dirichlet faces bit mask (-x,+x,-y,+y,-z,+z)
+  unsigned long long* err;  // first failing e*nq3+q (atomicMin)
+  MatConst<T> mat;
+  MatConst<double> matd;
+  T Bm[81], Dm[81];
+  double Bd[81], Dd[81];
+  double qwd[9];  // 1D Gauss weights (affine geometry stores det J0 without them)
+};
+
+__device__ __forceinline__ bool node_constrained(int a, int b, int c, int mx, int my, int mz, int faces) {
+  return ((faces & 1) && a == 0) || ((faces & 2) && a == mx - 1) || ((faces & 4) && b == 0) ||
+         ((faces & 8) && b == my - 1) || ((faces & 16) && c == 0) || ((faces & 32) && c == mz - 1);
+}
+
+// ---- sum factorization on one element's shared arrays -----------------------
+// A, Bf: 9 arrays of N^3 each (per element). Thread owns point (i,j,k).
+
+// Forward: input field in A[0..2] (3 components, lexicographic a fastest),
+// output reference gradient g[c][d] = d u_c / d xi_d at qp (i,j,k).
+template <typename T, int N>
+__device__ __forceinline__ void sf_forward(T (*A)[N * N * N], T (*Bf)[N * N * N], const T* sB, const T* sD, int i,
+                                           int j, int k, T* g) {
+  constexpr int N2 = N * N;
+  const int pt = (k * N + j) * N + i;
+  // S1: x-sweep with B and D
+  {
+    T tb[3], td[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) tb[c] = td[c] = T(0);
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const T b = sB[i * N + a], d = sD[i * N + a];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T u = A[c][k * N2 + j * N + a];
+        tb[c] += b * u;
+        td[c] += d * u;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Bf[c][pt] = tb[c];
+      Bf[3 + c][pt] = td[c];
+    }
+  }
+  __syncthreads();
+  // S2: y-sweep: sBB = By tB, sBD = Dy tB, sDB = By tD
+  {
+    T bb[3], bd[3], db[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bb[c] = bd[c] = db[c] = T(0);
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      const T vb = sB[j * N + b], vd = sD[j * N + b];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T tb = Bf[c][k * N2 + b * N + i], td = Bf[3 + c][k * N2 + b * N + i];
+        bb[c] += vb * tb;
+        bd[c] += vd * tb;
+        db[c] += vb * td;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      A[c][pt] = bb[c];
+      A[3 + c][pt] = bd[c];
+      A[6 + c][pt] = db[c];
+    }
+  }
+  __syncthreads();
+  // S3: z-sweep: g0 = Bz sDB, g1 = Bz sBD, g2 = Dz sBB
+  {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) g[q] = T(0);
+#pragma unroll
+    for (int cc = 0; cc < N; ++cc) {
+      const T vb = sB[k * N + cc], vd = sD[k * N + cc];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int o = cc * N2 + j * N + i;
+        g[3 * c + 0] += vb * A[6 + c][o];
+        g[3 * c + 1] += vb * A[3 + c][o];
+        g[3 * c + 2] += vd * A[c][o];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Transposed: w(c,d) at qp (i,j,k) -> nodal out[c] at node (i,j,k):
+// out = sum_q grad_xi phi_node(q) . w(c,:)(q)  (sumfact.hpp:90-110)
+template <typename T, int N>
+__device__ __forceinline__ void sf_transpose(T (*A)[N * N * N], T (*Bf)[N * N * N], const T* sB, const T* sD, int i,
+                                             int j, int k, const T* w, T* out) {
+  constexpr int N2 = N * N;
+  const int pt = (k * N + j) * N + i;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) A[q][pt] = w[q];
+  __syncthreads();
+  // T1 (z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2   (node index k)
+  {
+    T a0[3], a1[3], a2[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a0[c] = a1[c] = a2[c] = T(0);
+#pragma unroll
+    for (int qc = 0; qc < N; ++qc) {
+      const T vb = sB[qc * N + k], vd = sD[qc * N + k];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int o = qc * N2 + j * N + i;
+        a0[c] += vb * A[3 * c + 0][o];
+        a1[c] += vb * A[3 * c + 1][o];
+        a2[c] += vd * A[3 * c + 2][o];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Bf[3 * c + 0][pt] = a0[c];
+      Bf[3 * c + 1][pt] = a1[c];
+      Bf[3 * c + 2][pt] = a2[c];
+    }
+  }
+  __syncthreads();
+  // T2 (y): Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2   (node index j)
+  {
+    T q0[3], q12[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) q0[c] = q12[c] = T(0);
+#pragma unroll
+    for (int qb = 0; qb < N; ++qb) {
+      const T vb = sB[qb * N + j], vd = sD[qb * N + j];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int o = k * N2 + qb * N + i;
+        q0[c] += vb * Bf[3 * c + 0][o];
+        q12[c] += vd * Bf[3 * c + 1][o] + vb * Bf[3 * c + 2][o];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      A[2 * c][pt] = q0[c];
+      A[2 * c + 1][pt] = q12[c];
+    }
+  }
+  __syncthreads();
+  // T3 (x): out = Dx^T Q0 + Bx^T Q12   (node index i)
+  {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[c] = T(0);
+#pragma unroll
+    for (int qa = 0; qa < N; ++qa) {
+      const T vb = sB[qa * N + i], vd = sD[qa * N + i];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int o = k * N2 + j * N + qa;
+        out[c] += vd * A[2 * c][o] + vb * A[2 * c + 1][o];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---- element addressing -------------------------------------------------------
+struct ElemPos {
+  int64_t e;
+  int ei, ej, ek;
+  int64_t node;  // global node of this thread's local node (i,j,k)
+  int ga, gb, gc;
+};
+
+template <int P>
+__device__ __forceinline__ ElemPos elem_pos(int64_t e, int nx, int ny, int mx, int my, int i, int j, int k) {
+  ElemPos r;
+  r.e = e;
+  r.ei = (int)(e % nx);
+  r.ej = (int)((e / nx) % ny);
+  r.ek = (int)(e / ((int64_t)nx * ny));
+  r.ga = r.ei * P + i;
+  r.gb = r.ej * P + j;
+  r.gc = r.ek * P + k;
+  r.node = ((int64_t)r.gc * my + r.gb) * mx + r.ga;
+  return r;
+}
+
+// Geometry factors at (e, q): J0^-1 and det(J0)*w_q (operator.hpp:492, 496-504).
+// Curved meshes store both per qp; affine meshes store them per element and
+// apply the tensor-product weight here (SURVEY §8(d) affine shortcut).
+template <typename T, typename A>
+__device__ __forceinline__ void load_geo(const A& a, const T* geo, bool valid, int64_t e, int64_t qidx, int i, int j,
+                                         int k, T* j0inv, T& detw) {
+  const int64_t gidx = valid ? (a.affine ? e : qidx) : 0;
+  const int64_t stride = a.geo_stride;
+#pragma unroll
+  for (int m = 0; m < 9; ++m) j0inv[m] = geo[m * stride + gidx];
+  detw = geo[9 * stride + gidx];
+  if (a.affine) detw = detw * T(a.qwd[i] * a.qwd[j] * a.qwd[k]);
+}
+
+// ---- apply kernel ---------------------------------------------------------------
+template <typename T, int P, int MODEL, int STRAT>
+__global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
+    apply_kernel(const KArgs<T> a) {
+  constexpr int N = P + 1, N3 = N * N * N, EPB = Tile<P>::EPB;
+  __shared__ T sB[N * N], sD[N * N];
+  __shared__ T bufA[EPB][9][N3], bufB[EPB][9][N3];
+  const int tid = threadIdx.x;
+  const int el = tid / N3, q = tid % N3;
+  const int i = q % N, j = (q / N) % N, k = q / (N * N);
+  if (tid < N * N) {
+    sB[tid] = a.Bm[tid];
+    sD[tid] = a.Dm[tid];
+  }
+  const int64_t e = (int64_t)blockIdx.x * EPB + el + a.e_begin;
+  const bool valid = e < a.nel;
+  const ElemPos ep = elem_pos<P>(valid ? e : a.e_begin, a.nx, a.ny, a.mx, a.my, i, j, k);
+  const bool fixed = node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
+  // gather input (Dirichlet columns masked, operator.hpp:604-605)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) bufA[el][c][q] = (valid && !fixed) ? a.x[3 * ep.node + c] : T(0);
+  __syncthreads();
+  T gx[9];
+  sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gx);
+
+  Bundle<T> cb;
+  const int64_t qidx = e * N3 + q;
+  if (STRAT == S_NONE || STRAT == S_SCALAR) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.uk[3 * ep.node + c] : T(0);
+    __syncthreads();
+    T gk[9];
+    sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
+    T j0inv[9], detw, g[9];
+    load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
+    mm(gk, j0inv, g);
+    const bool ok = make_strain(g, cb);
+    if (!ok && valid) atomicMin(a.err, (unsigned long long)qidx);
+    if (STRAT == S_NONE) {
+      cache_scalars<T, MODEL>(a.mat, cb);
+    } else {
+      const T* cs = a.cache;
+      const int64_t st = a.cache_stride, ix = valid ? qidx : 0;
+      if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + ix];
+      else {
+        cb.jp = cs[C_JP * st + ix];
+        cb.c1 = cs[C_C1 * st + ix];
+        cb.c2 = cs[C_C2 * st + ix];
+      }
+      if (MODEL == FIBER) {
+        cb.c3[0] = cs[(C_C3 + 0) * st + ix];
+        cb.c3[1] = cs[(C_C3 + 1) * st + ix];
+        cb.efib[0] = cs[(C_EF + 0) * st + ix];
+        cb.efib[1] = cs[(C_EF + 1) * st + ix];
+      }
+    }
+    second_pk<T, MODEL>(a.mat, cb);
+    T w[9], out[3];
+    tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, w);
+    sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
+    if (valid)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a.loc[qidx * 3 + c] = out[c];
+    return;
+  }
+  T j0inv[9], detw;
+  load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
+  const T* cs = a.cache;
+  const int64_t st = a.cache_stride, ix = valid ? qidx : 0;
+  if (STRAT == S_CACHEDF) {
+    T g[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) g[m] = cs[(C_G + m) * st + ix];
+    const bool ok = make_strain(g, cb);
+    if (!ok && valid) atomicMin(a.err, (unsigned long long)qidx);
+    cache_scalars<T, MODEL>(a.mat, cb);
+    second_pk<T, MODEL>(a.mat, cb);
+  } else {  // S_TENSOR
+    if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + ix];
+    else {
+      cb.jp = cs[C_JP * st + ix];
+      cb.c1 = cs[C_C1 * st + ix];
+      cb.c2 = cs[C_C2 * st + ix];
+    }
+    if (MODEL == FIBER) {
+      cb.c3[0] = cs[(C_C3 + 0) * st + ix];
+      cb.c3[1] = cs[(C_C3 + 1) * st + ix];
+      cb.efib[0] = cs[(C_EF + 0) * st + ix];
+      cb.efib[1] = cs[(C_EF + 1) * st + ix];
+    }
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+      cb.F[m] = cs[(C_F + m) * st + ix];
+      cb.Finv[m] = cs[(C_FINV + m) * st + ix];
+    }
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      cb.S[m] = cs[(C_S + m) * st + ix];
+      cb.Cinv[m] = cs[(C_CINV + m) * st + ix];
+    }
+  }
+  T w[9], out[3];
+  tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, w);
+  sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
+  if (valid)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a.loc[qidx * 3 + c] = out[c];
+}
+
+// ---- linearization kernel (double compute, T store), operator.hpp:643-770 ------
+template <typename T, int P, int MODEL>
+__global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
+    linearize_kernel(const KArgs<T> a) {
+  constexpr int N = P + 1, N3 = N * N * N, EPB = Tile<P>::EPB;
+  __shared__ double sB[N * N], sD[N * N];
+  __shared__ double bufA[EPB][9][N3], bufB[EPB][9][N3];
+  const int tid = threadIdx.x;
+  const int el = tid / N3, q = tid % N3;
+  const int i = q % N, j = (q / N) % N, k = q / (N * N);
+  if (tid < N * N) {
+    sB[tid] = a.Bd[tid];
+    sD[tid] = a.Dd[tid];
+  }
+  const int64_t e = (int64_t)blockIdx.x * EPB + el + a.e_begin;
+  const bool valid = e < a.nel;
+  const ElemPos ep = elem_pos<P>(valid ? e : a.e_begin, a.nx, a.ny, a.mx, a.my, i, j, k);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.ukd[3 * ep.node + c] : 0.0;
+  __syncthreads();
+  double gk[9];
+  sf_forward<double, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
+  if (!valid) return;
+  const int64_t qidx = e * N3 + q;
+  double j0inv[9], detw, g[9];
+  load_geo(a, a.geod, true, e, qidx, i, j, k, j0inv, detw);
+  mm(gk, j0inv, g);
+  const int64_t st = a.cache_stride;
+  if (a.strategy == S_CACHEDF) {
+#pragma unroll
+    for (int m = 0; m < 9; ++m) a.cache[(C_G + m) * st + qidx] = T(g[m]);
+  }
+  Bundle<double> cb;
+  if (!make_strain(g, cb)) {
+    atomicMin(a.err, (unsigned long long)qidx);
+    return;
+  }
+  if (a.strategy == S_CACHEDF || a.strategy == S_NONE) return;
+  // stored scalars, computed in double (operator.hpp:720-735)
+  cache_scalars<double, MODEL>(a.matd, cb);
+  if (MODEL == CNH) {
+    a.cache[C_LNJ * st + qidx] = T(cb.lnj);
+  } else {
+    a.cache[C_JP * st + qidx] = T(cb.jp);
+    a.cache[C_C1 * st + qidx] = T(cb.c1);
+    a.cache[C_C2 * st + qidx] = T(cb.c2);
+  }
+  if (MODEL == FIBER) {
+    a.cache[(C_C3 + 0) * st + qidx] = T(cb.c3[0]);
+    a.cache[(C_C3 + 1) * st + qidx] = T(cb.c3[1]);
+    a.cache[(C_EF + 0) * st + qidx] = T(cb.efib[0]);
+    a.cache[(C_EF + 1) * st + qidx] = T(cb.efib[1]);
+  }
+  if (a.strategy != S_TENSOR) return;
+  second_pk<double, MODEL>(a.matd, cb);
+#pragma unroll
+  for (int m = 0; m < 9; ++m) {
+    a.cache[(C_F + m) * st + qidx] = T(cb.F[m]);
+    a.cache[(C_FINV + m) * st + qidx] = T(cb.Finv[m]);
+  }
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    a.cache[(C_S + m) * st + qidx] = T(cb.S[m]);
+    a.cache[(C_CINV + m) * st + qidx] = T(cb.Cinv[m]);
+  }
+}
+
+// ---- diagonal kernel ----------------------------------------------------------------
+// diag(m=(a,b,c), comp) = sum_q sum_{d,d'} A^comp_{dd'}(q) dphi_m/dxi_d(q) dphi_m/dxi_d'(q)
+// with A^comp_{dd'} = d w_ref(comp,d) / d Gref(comp,d'), obtained from 9 unit
+// evaluations of the (linear) qp tangent; the quadratic form is contracted
+// by transposed sweeps with the elementwise products BB, BD, DD of the 1D
+// tables.  Same operator entries as the reference's 3(p+1)^3 local unit
+// applications (operator.hpp:824-866).
+template <typename T, int P, int MODEL>
+__global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
+    diagonal_kernel(const KArgs<T> a) {
+  constexpr int N = P + 1, N3 = N * N * N, N2 = N * N, EPB = Tile<P>::EPB;
+  __shared__ T sB[N * N], sD[N * N];
+  __shared__ T bufA[EPB][9][N3], bufB[EPB][9][N3];
+  const int tid = threadIdx.x;
+  const int el = tid / N3, q = tid % N3;
+  const int i = q % N, j = (q / N) % N, k = q / (N * N);
+  if (tid < N * N) {
+    sB[tid] = a.Bm[tid];
+    sD[tid] = a.Dm[tid];
+  }
+  const int64_t e = (int64_t)blockIdx.x * EPB + el + a.e_begin;
+  const bool valid = e < a.nel;
+  const ElemPos ep = elem_pos<P>(valid ? e : a.e_begin, a.nx, a.ny, a.mx, a.my, i, j, k);
+  const int64_t qidx = e * N3 + q;
+  const int64_t st = a.cache_stride, ix = valid ? qidx : 0;
+  const T* cs = a.cache;
+  Bundle<T> cb;
+  T j0inv[9], detw;
+  load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
+  if (a.strategy == S_NONE || a.strategy == S_SCALAR) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.uk[3 * ep.node + c] : T(0);
+    __syncthreads();
+    T gk[9], g[9];
+    sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
+    mm(gk, j0inv, g);
+    make_strain(g, cb);
+    if (a.strategy == S_NONE) cache_scalars<T, MODEL>(a.mat, cb);
+  } else if (a.strategy == S_CACHEDF) {
+    T g[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) g[m] = cs[(C_G + m) * st + ix];
+    make_strain(g, cb);
+    cache_scalars<T, MODEL>(a.mat, cb);
+  } else {
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+      cb.F[m] = cs[(C_F + m) * st + ix];
+      cb.Finv[m] = cs[(C_FINV + m) * st + ix];
+    }
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      cb.S[m] = cs[(C_S + m) * st + ix];
+      cb.Cinv[m] = cs[(C_CINV + m) * st + ix];
+    }
+  }
+  if (a.strategy == S_SCALAR || a.strategy == S_TENSOR) {
+    if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + ix];
+    else {
+      cb.jp = cs[C_JP * st + ix];
+      cb.c1 = cs[C_C1 * st + ix];
+      cb.c2 = cs[C_C2 * st + ix];
+    }
+    if (MODEL == FIBER) {
+      cb.c3[0] = cs[(C_C3 + 0) * st + ix];
+      cb.c3[1] = cs[(C_C3 + 1) * st + ix];
+      cb.efib[0] = cs[(C_EF + 0) * st + ix];
+      cb.efib[1] = cs[(C_EF + 1) * st + ix];
+    }
+  }
+  if (a.strategy != S_TENSOR) second_pk<T, MODEL>(a.mat, cb);
+
+  // A^c_{dd'}: 27 values per qp, as symmetric quadratic-form coefficients
+  // coef[c][pair], pairs (00,11,22,01,02,12) with off-diagonals A_dd'+A_d'd.
+  T coef[3][6];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    T A[3][3];
+#pragma unroll
+    for (int dp = 0; dp < 3; ++dp) {
+      T gref[9], w[9];
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gref[m] = T(0);
+      gref[3 * c + dp] = T(1);
+      tangent_integrand<T, MODEL>(a.mat, cb, gref, j0inv, detw, w);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) A[d][dp] = w[3 * c + d];
+    }
+    coef[c][0] = A[0][0];
+    coef[c][1] = A[1][1];
+    coef[c][2] = A[2][2];
+    coef[c][3] = A[0][1] + A[1][0];
+    coef[c][4] = A[0][2] + A[2][0];
+    coef[c][5] = A[1][2] + A[2][1];
+  }
+  if (!valid) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int s = 0; s < 6; ++s) coef[c][s] = T(0);
+  }
+  // factor per axis for pair (d,d'): axis x gets D*D if d=d'=0, B*D if one of
+  // them is 0, else B*B; same for y (index 1) and z (index 2).
+  T out[3] = {T(0), T(0), T(0)};
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int d0 = s < 3 ? s : (s == 5 ? 1 : 0);
+    const int d1 = s < 3 ? s : (s == 3 ? 1 : 2);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bufA[el][c][q] = coef[c][s];
+    __syncthreads();
+    // z (node index k)
+    T t[3] = {T(0), T(0), T(0)};
+    const int nz_ = (d0 == 2) + (d1 == 2);
+    const int ny_ = (d0 == 1) + (d1 == 1);
+    const int nx_ = (d0 == 0) + (d1 == 0);
+#pragma unroll
+    for (int qc = 0; qc < N; ++qc) {
+      const T b = sB[qc * N + k], d = sD[qc * N + k];
+      const T f = nz_ == 2 ? d * d : (nz_ == 1 ? b * d : b * b);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) t[c] += f * bufA[el][c][qc * N2 + j * N + i];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bufB[el][c][q] = t[c];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c) t[c] = T(0);
+#pragma unroll
+    for (int qb = 0; qb < N; ++qb) {
+      const T b = sB[qb * N + j], d = sD[qb * N + j];
+      const T f = ny_ == 2 ? d * d : (ny_ == 1 ? b * d : b * b);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) t[c] += f * bufB[el][c][k * N2 + qb * N + i];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bufA[el][3 + c][q] = t[c];
+    __syncthreads();
+#pragma unroll
+    for (int qa = 0; qa < N; ++qa) {
+      const T b = sB[qa * N + i], d = sD[qa * N + i];
+      const T f = nx_ == 2 ? d * d : (nx_ == 1 ? b * d : b * b);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[c] += f * bufA[el][3 + c][k * N2 + j * N + qa];
+    }
+    __syncthreads();
+  }
+  if (valid)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a.loc[qidx * 3 + c] = out[c];
+}
+
+}  // namespace emfgpu

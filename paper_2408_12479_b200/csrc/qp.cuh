@@ -1,0 +1,336 @@
+// Quadrature-point material kernels (device).  B200-native restatement of the
+// reference's per-point algebra — NOT a translation of its lane-batched C++:
+// one CUDA thread owns one quadrature point, all 3x3 tensors live in
+// registers, the fourth-order tangent is never formed.
+//
+// Semantics follow (stable formulation, material domain):
+//   make_strain            proj/include/elastmf/constitutive.hpp:43-57
+//   compute_cache          constitutive.hpp:326-377
+//   fiber_invariants       constitutive.hpp:117-149
+//   second_pk_base         constitutive.hpp:197-238
+//   tangent_material       constitutive.hpp:381-419
+//   integrand              proj/include/elastmf/operator.hpp:495-504
+//   ln_plus_one/fast_jpow  proj/include/elastmf/fastscalar.hpp:44-89
+// Numerics: nvcc contracts a*b+c into FMA (the reference forbids contraction,
+// proj/CMakeLists.txt:11-13), so results match the oracle to round-off
+// (rel-L2 ~1e-15 fp64), not bitwise.  The ln series is evaluated in Horner
+// form in y^2 (same 16 terms, same |x|>0.5 log1p switch).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace emfgpu {
+
+enum Model : int { CNH = 0, INH = 1, FIBER = 2 };
+enum Strategy : int { S_NONE = 0, S_SCALAR = 1, S_TENSOR = 2, S_CACHEDF = 3 };
+
+// Material constants in the operator's number type, rounded from double the
+// way the reference does (N(scalar_of<N>(p.x)), e.g. constitutive.hpp:200).
+template <typename T>
+struct MatConst {
+  T mu, lam, half_k, kappa, k2, two_k1;
+  T h[2][6];   // structure tensors H4, H6 (material.cpp:50-82)
+  T m1[2][3];  // mean fibre directions
+};
+
+template <typename T>
+__device__ __forceinline__ T dlog1p(T x);
+template <>
+__device__ __forceinline__ double dlog1p<double>(double x) { return log1p(x); }
+template <>
+__device__ __forceinline__ float dlog1p<float>(float x) { return log1pf(x); }
+template <typename T>
+__device__ __forceinline__ T dexp(T x);
+template <>
+__device__ __forceinline__ double dexp<double>(double x) { return exp(x); }
+template <>
+__device__ __forceinline__ float dexp<float>(float x) { return expf(x); }
+
+// SymTensor order (11,22,33,12,13,23), tensor.hpp:93-100.
+__host__ __device__ constexpr int sidx(int i, int j) { return i == j ? i : 2 + i + j; }
+
+template <typename T>
+__device__ __forceinline__ T det3(const T* t) {
+  return (t[0] * (t[4] * t[8] - t[5] * t[7]) - t[1] * (t[3] * t[8] - t[5] * t[6])) +
+         t[2] * (t[3] * t[7] - t[4] * t[6]);
+}
+
+// det(I+G)-1 without forming I+G (tensor.hpp:199-208).
+template <typename T>
+__device__ __forceinline__ T det_minus_one(const T* g) {
+  const T tr = (g[0] + g[4]) + g[8];
+  const T minors = ((g[0] * g[4] - g[1] * g[3]) + (g[0] * g[8] - g[2] * g[6])) + (g[4] * g[8] - g[5] * g[7]);
+  return (det3(g) + minors) + tr;
+}
+
+// Adjugate / determinant (tensor.hpp:212-231).
+template <typename T>
+__device__ __forceinline__ void inverse3(const T* t, T* r) {
+  const T inv = T(1) / det3(t);
+  r[0] = (t[4] * t[8] - t[5] * t[7]) * inv;
+  r[1] = (t[2] * t[7] - t[1] * t[8]) * inv;
+  r[2] = (t[1] * t[5] - t[2] * t[4]) * inv;
+  r[3] = (t[5] * t[6] - t[3] * t[8]) * inv;
+  r[4] = (t[0] * t[8] - t[2] * t[6]) * inv;
+  r[5] = (t[2] * t[3] - t[0] * t[5]) * inv;
+  r[6] = (t[3] * t[7] - t[4] * t[6]) * inv;
+  r[7] = (t[1] * t[6] - t[0] * t[7]) * inv;
+  r[8] = (t[0] * t[4] - t[1] * t[3]) * inv;
+}
+
+// r = x * y (general x general)
+template <typename T>
+__device__ __forceinline__ void mm(const T* x, const T* y, T* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) r[3 * i + j] = (x[3 * i] * y[j] + x[3 * i + 1] * y[3 + j]) + x[3 * i + 2] * y[6 + j];
+}
+// r = x * y^T (general x general^T)
+template <typename T>
+__device__ __forceinline__ void mm_bt(const T* x, const T* y, T* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      r[3 * i + j] = (x[3 * i] * y[3 * j] + x[3 * i + 1] * y[3 * j + 1]) + x[3 * i + 2] * y[3 * j + 2];
+}
+// r = x * ys (general x symmetric)
+template <typename T>
+__device__ __forceinline__ void mm_ts(const T* x, const T* ys, T* r) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      r[3 * i + j] = (x[3 * i] * ys[sidx(0, j)] + x[3 * i + 1] * ys[sidx(1, j)]) + x[3 * i + 2] * ys[sidx(2, j)];
+}
+// symmetric part of xs * y, only the 6 unique entries (tensor.hpp:155-166 of matmul)
+template <typename T>
+__device__ __forceinline__ void sym_mm_st(const T* xs, const T* y, T* s) {
+  T r[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      r[3 * i + j] = (xs[sidx(i, 0)] * y[j] + xs[sidx(i, 1)] * y[3 + j]) + xs[sidx(i, 2)] * y[6 + j];
+  s[0] = r[0];
+  s[1] = r[4];
+  s[2] = r[8];
+  s[3] = T(0.5) * (r[1] + r[3]);
+  s[4] = T(0.5) * (r[2] + r[6]);
+  s[5] = T(0.5) * (r[5] + r[7]);
+}
+template <typename T>
+__device__ __forceinline__ void sym_part(const T* t, T* s) {
+  s[0] = t[0];
+  s[1] = t[4];
+  s[2] = t[8];
+  s[3] = T(0.5) * (t[1] + t[3]);
+  s[4] = T(0.5) * (t[2] + t[6]);
+  s[5] = T(0.5) * (t[5] + t[7]);
+}
+template <typename T>
+__device__ __forceinline__ T ddot_s(const T* x, const T* y) {
+  return ((x[0] * y[0] + x[1] * y[1]) + x[2] * y[2]) + T(2) * ((x[3] * y[3] + x[4] * y[4]) + x[5] * y[5]);
+}
+
+// ln(1+x): 2 sum_{n<16} y^(2n+1)/(2n+1), y = x/(2+x); log1p for |x|>0.5
+// (fastscalar.hpp:44-71).  Horner in y^2 instead of the stored powers.
+template <typename T>
+__device__ __forceinline__ T ln_plus_one(T x) {
+  if (fabs(x) > T(0.5)) return dlog1p(x);
+  const T y = x / (T(2) + x);
+  const T y2 = y * y;
+  T s = T(1.0 / 31.0);
+#pragma unroll
+  for (int n = 14; n >= 0; --n) s = s * y2 + T(1.0 / (2 * n + 1));
+  return T(2) * (y * s);
+}
+
+// J^(-2/3) by the reference's 3-step Newton recurrence (fastscalar.hpp:77-89).
+template <typename T>
+__device__ __forceinline__ T fast_jpow(T jm1) {
+  const T third = T(1) / T(3);
+  const T four_thirds = T(4) / T(3);
+  const T alpha = ((jm1 + T(2)) * jm1 + T(1)) * third;
+  T beta = four_thirds - alpha;
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const T b2 = beta * beta;
+    beta = four_thirds * beta - alpha * (b2 * b2);
+  }
+  return beta;
+}
+
+// Everything the tangent needs at one point (QpCache, constitutive.hpp:79-93,
+// material cell).  E/jm1 are kept for second_pk.
+template <typename T>
+struct Bundle {
+  T F[9], Finv[9], Cinv[6], S[6], E[6];
+  T jm1, lnj, jp, c1, c2, c3[2], efib[2];
+};
+
+// Stable kinematics from the displacement gradient g (constitutive.hpp:48-57).
+// Returns false when det(F) <= 0.
+template <typename T>
+__device__ __forceinline__ bool make_strain(const T* g, Bundle<T>& c) {
+  c.jm1 = det_minus_one(g);
+  if (!(c.jm1 > T(-1))) return false;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const T q = (g[i] * g[j] + g[3 + i] * g[3 + j]) + g[6 + i] * g[6 + j];
+      c.E[sidx(i, j)] = T(0.5) * ((g[3 * i + j] + g[3 * j + i]) + q);
+    }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) c.F[i] = g[i];
+  c.F[0] = T(1) + g[0];
+  c.F[4] = T(1) + g[4];
+  c.F[8] = T(1) + g[8];
+  inverse3(c.F, c.Finv);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j)
+      c.Cinv[sidx(i, j)] =
+          (c.Finv[3 * i] * c.Finv[3 * j] + c.Finv[3 * i + 1] * c.Finv[3 * j + 1]) + c.Finv[3 * i + 2] * c.Finv[3 * j + 2];
+  return true;
+}
+
+// Scalars of compute_cache (constitutive.hpp:335-366).
+template <typename T, int MODEL>
+__device__ __forceinline__ void cache_scalars(const MatConst<T>& m, Bundle<T>& c) {
+  const T i1 = T(3) + T(2) * ((c.E[0] + c.E[1]) + c.E[2]);
+  c.lnj = MODEL == CNH ? ln_plus_one(c.jm1) : T(0);  // lnJ enters only cNH's material tangent
+  c.jp = MODEL == CNH ? T(1) : fast_jpow(c.jm1);
+  if (MODEL != CNH) {
+    const T jac = T(1) + c.jm1;
+    c.c1 = m.half_k * (c.jm1 * (c.jm1 + T(2))) - ((m.mu / T(3)) * c.jp) * i1;
+    c.c2 = (((T(2) * m.mu) / T(9)) * c.jp) * i1 + (m.kappa * jac) * jac;
+  }
+  if (MODEL == FIBER) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      T mm6[6];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j) mm6[sidx(i, j)] = m.m1[f][i] * m.m1[f][j];
+      c.efib[f] = T(2) * ddot_s(m.h[f], c.E);
+      const T gate = T(2) * ddot_s(mm6, c.E);
+      const T z = (m.k2 * c.efib[f]) * c.efib[f];
+      c.c3[f] = gate > T(0) ? dexp(z) * m.two_k1 : T(0);  // tension-only gate, stable form
+    }
+  }
+}
+
+// S = second_pk_base (+ fibre terms), constitutive.hpp:197-238, 368-371.
+template <typename T, int MODEL>
+__device__ __forceinline__ void second_pk(const MatConst<T>& m, Bundle<T>& c) {
+  T inner[6];
+  if (MODEL == CNH) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) inner[k] = (T(2) * m.mu) * c.E[k];
+    const T v = (T(2) * m.lam) * c.lnj;
+    inner[0] += v;
+    inner[1] += v;
+    inner[2] += v;
+  } else {
+    const T vol = m.half_k * (c.jm1 * (c.jm1 + T(2)));
+    const T tre3 = ((c.E[0] + c.E[1]) + c.E[2]) * (T(1) / T(3));
+    const T s = (T(2) * m.mu) * c.jp;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) inner[k] = s * c.E[k];
+    const T d = vol - s * tre3;
+    inner[0] += d;
+    inner[1] += d;
+    inner[2] += d;
+  }
+  T full[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) full[3 * i + j] = inner[sidx(i, j)];
+  sym_mm_st(c.Cinv, full, c.S);
+  if (MODEL == FIBER) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const T coef = c.c3[f] * c.efib[f];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) c.S[k] += coef * m.h[f][k];
+    }
+  }
+}
+
+// D_u S in direction dg (constitutive.hpp:381-419).
+template <typename T, int MODEL>
+__device__ __forceinline__ void tangent_material(const MatConst<T>& m, const Bundle<T>& c, const T* dg, T* r) {
+  T a[9], sac[6];
+  mm(c.Finv, dg, a);
+  const T w = (a[0] + a[4]) + a[8];
+  {
+    T ac[9];
+    mm_ts(a, c.Cinv, ac);
+    sym_part(ac, sac);
+  }
+  if (MODEL == CNH) {
+    const T f1 = T(2) * (m.mu - (T(2) * m.lam) * c.lnj);
+    const T f2 = (T(2) * m.lam) * w;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) r[k] = f1 * sac[k] + f2 * c.Cinv[k];
+    return;
+  }
+  T q = c.F[0] * dg[0];
+#pragma unroll
+  for (int i = 1; i < 9; ++i) q += c.F[i] * dg[i];
+  const T ttmj = ((T(2) * m.mu) / T(3)) * c.jp;
+  const T m2c1 = T(-2) * c.c1;
+  const T f2 = c.c2 * w - ttmj * q;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) r[k] = m2c1 * sac[k] + f2 * c.Cinv[k];
+  const T dgl = (-ttmj) * w;
+  r[0] += dgl;
+  r[1] += dgl;
+  r[2] += dgl;
+  if (MODEL == FIBER) {
+    T dch[6];
+    // sym(F^T dg)
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i; j < 3; ++j) {
+        const T xij = (c.F[i] * dg[j] + c.F[3 + i] * dg[3 + j]) + c.F[6 + i] * dg[6 + j];
+        const T xji = (c.F[j] * dg[i] + c.F[3 + j] * dg[3 + i]) + c.F[6 + j] * dg[6 + i];
+        dch[sidx(i, j)] = i == j ? xij : T(0.5) * (xij + xji);
+      }
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const T hdc = T(2) * ddot_s(m.h[f], dch);
+      const T coef = (c.c3[f] * ((((T(2) * m.k2) * c.efib[f]) * c.efib[f]) + T(1))) * hdc;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r[k] += coef * m.h[f][k];
+    }
+  }
+}
+
+// w_ref = detw * (dg S + F D_uS) J0^-T  (operator.hpp:502-504), dg = Gref J0^-1.
+template <typename T, int MODEL>
+__device__ __forceinline__ void tangent_integrand(const MatConst<T>& m, const Bundle<T>& c, const T* gref,
+                                                  const T* j0inv, T detw, T* wref) {
+  T dg[9], ds[6], wm[9];
+  mm(gref, j0inv, dg);
+  tangent_material<T, MODEL>(m, c, dg, ds);
+  {
+    T t1[9], t2[9];
+    mm_ts(dg, c.S, t1);
+    mm_ts(c.F, ds, t2);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wm[k] = t1[k] + t2[k];
+  }
+  mm_bt(wm, j0inv, wref);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) wref[k] *= detw;
+}
+
+}  // namespace emfgpu

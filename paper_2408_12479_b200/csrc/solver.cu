@@ -1,0 +1,206 @@
+// hp-multigrid ingredients on the device (fp32 or fp64 levels):
+//   lattice transfers          TransferOp / lattice_sweep, mesh.hpp:190-289
+//   Chebyshev-Jacobi updates   ChebyshevSmoother::smooth, solver.hpp:330-361
+//   deterministic dot          dot_d, solver.hpp:95-100 (fixed-order tree)
+#include "internal.h"
+
+namespace emfgpu {
+
+// One axis of a separable lattice transfer on an interleaved 3-component
+// vector.  Forward (prolongate / interpolate_down): out[d] = sum_s w[d,s]
+// in[src_elem[d]*p_src + s].  Transposed (restrict): each source-lattice
+// index t gathers w[d,s] in[d] over the destinations d that touch it, in
+// ascending d — the order in which the reference's scatter adds them
+// (mesh.hpp:228-236) — through a CSR built on the host.
+template <typename T>
+__global__ void lattice_sweep_kernel(const T* __restrict__ in, T* __restrict__ out, const int* __restrict__ src_elem,
+                                     const double* __restrict__ w, const int* __restrict__ t_ptr,
+                                     const int* __restrict__ t_d, const int* __restrict__ t_s, int stencil,
+                                     int p_src, int transpose, int axis, int in0, int in1, int in2, int out_na) {
+  const int o0 = axis == 0 ? out_na : in0, o1 = axis == 1 ? out_na : in1, o2 = axis == 2 ? out_na : in2;
+  const int64_t total = (int64_t)o0 * o1 * o2 * 3;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int comp = (int)(idx % 3);
+  const int64_t node = idx / 3;
+  const int a = (int)(node % o0), b = (int)((node / o0) % o1), c = (int)(node / ((int64_t)o0 * o1));
+  const int pos = axis == 0 ? a : (axis == 1 ? b : c);
+  auto in_at = [&](int t) -> T {
+    const int aa = axis == 0 ? t : a, bb = axis == 1 ? t : b, cc = axis == 2 ? t : c;
+    return in[(((int64_t)cc * in1 + bb) * in0 + aa) * 3 + comp];
+  };
+  T acc = T(0);
+  if (!transpose) {
+    const int base = src_elem[pos] * p_src;
+    for (int s = 0; s < stencil; ++s) acc += T(w[pos * stencil + s]) * in_at(base + s);
+  } else {
+    for (int r = t_ptr[pos]; r < t_ptr[pos + 1]; ++r) acc += T(w[t_d[r] * stencil + t_s[r]]) * in_at(t_d[r]);
+  }
+  out[idx] = acc;
+}
+
+template <typename T>
+void launch_transfer_axis(const T* in, T* out, const int* src_elem, const double* w, const int* t_ptr,
+                          const int* t_d, const int* t_s, int stencil, int p_src, int transpose, int axis, int in0,
+                          int in1, int in2, int out_na, cudaStream_t s) {
+  const int o0 = axis == 0 ? out_na : in0, o1 = axis == 1 ? out_na : in1, o2 = axis == 2 ? out_na : in2;
+  const int64_t total = (int64_t)o0 * o1 * o2 * 3;
+  lattice_sweep_kernel<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+      in, out, src_elem, w, t_ptr, t_d, t_s, stencil, p_src, transpose, axis, in0, in1, in2, out_na);
+}
+template void launch_transfer_axis<double>(const double*, double*, const int*, const double*, const int*, const int*,
+                                           const int*, int, int, int, int, int, int, int, int, cudaStream_t);
+template void launch_transfer_axis<float>(const float*, float*, const int*, const double*, const int*, const int*,
+                                          const int*, int, int, int, int, int, int, int, int, cudaStream_t);
+
+// ---- Chebyshev (solver.hpp:330-361) ------------------------------------------
+template <typename T>
+__global__ void cheb_first_kernel(T* __restrict__ x, T* __restrict__ r, T* __restrict__ d, const T* __restrict__ b,
+                                  const T* __restrict__ inv_diag, T inv_theta, int zero_start, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // zero start: r = b, x = 0; else r holds A x on entry
+  const T ri = zero_start ? b[i] : b[i] - r[i];
+  const T di = (inv_theta * inv_diag[i]) * ri;
+  r[i] = ri;
+  d[i] = di;
+  x[i] = zero_start ? di : x[i] + di;
+}
+
+template <typename T>
+__global__ void cheb_step_kernel(T* __restrict__ x, T* __restrict__ r, T* __restrict__ d, const T* __restrict__ ad,
+                                 const T* __restrict__ inv_diag, T f1, T f2, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const T ri = r[i] - ad[i];
+  const T di = f1 * d[i] + (f2 * inv_diag[i]) * ri;
+  r[i] = ri;
+  d[i] = di;
+  x[i] += di;
+}
+
+template <typename T>
+__global__ void inv_kernel(const T* __restrict__ d, T* __restrict__ inv, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) inv[i] = T(1) / d[i];
+}
+
+template <typename T>
+void launch_cheb_first(T* x, T* r, T* d, const T* b, const T* inv_diag, double inv_theta, int zero_start, int64_t n,
+                       cudaStream_t s) {
+  cheb_first_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, r, d, b, inv_diag, T(inv_theta), zero_start, n);
+}
+template <typename T>
+void launch_cheb_step(T* x, T* r, T* d, const T* ad, const T* inv_diag, double f1, double f2, int64_t n,
+                      cudaStream_t s) {
+  cheb_step_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, r, d, ad, inv_diag, T(f1), T(f2), n);
+}
+template <typename T>
+void launch_inv(const T* d, T* inv, int64_t n, cudaStream_t s) {
+  inv_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d, inv, n);
+}
+template void launch_cheb_first<double>(double*, double*, double*, const double*, const double*, double, int, int64_t,
+                                        cudaStream_t);
+template void launch_cheb_first<float>(float*, float*, float*, const float*, const float*, double, int, int64_t,
+                                       cudaStream_t);
+template void launch_cheb_step<double>(double*, double*, double*, const double*, const double*, double, double,
+                                       int64_t, cudaStream_t);
+template void launch_cheb_step<float>(float*, float*, float*, const float*, const float*, double, double, int64_t,
+                                      cudaStream_t);
+template void launch_inv<double>(const double*, double*, int64_t, cudaStream_t);
+template void launch_inv<float>(const float*, float*, int64_t, cudaStream_t);
+
+// ---- deterministic dot: fixed grid, fixed per-thread ranges, tree in smem ----
+constexpr int kDotBlocks = 592, kDotThreads = 256;
+
+template <typename T>
+__global__ void dot_partial_kernel(const T* __restrict__ a, const T* __restrict__ b, int64_t n, double* partial) {
+  __shared__ double sm[kDotThreads];
+  const int64_t gt = (int64_t)blockIdx.x * kDotThreads + threadIdx.x;
+  const int64_t stride = (int64_t)kDotBlocks * kDotThreads;
+  double s = 0.0;
+  for (int64_t i = gt; i < n; i += stride) s += double(a[i]) * double(b[i]);
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kDotThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sm[0];
+}
+
+__global__ void dot_final_kernel(const double* partial, double* out) {
+  __shared__ double sm[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < kDotBlocks; i += 1024) s += partial[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
+template <typename T>
+void launch_dot(const T* a, const T* b, int64_t n, double* partial, double* out, cudaStream_t s) {
+  dot_partial_kernel<T><<<kDotBlocks, kDotThreads, 0, s>>>(a, b, n, partial);
+  dot_final_kernel<<<1, 1024, 0, s>>>(partial, out);
+}
+template void launch_dot<double>(const double*, const double*, int64_t, double*, double*, cudaStream_t);
+template void launch_dot<float>(const float*, const float*, int64_t, double*, double*, cudaStream_t);
+int dot_partial_count() { return kDotBlocks; }
+
+// ---- Lanczos vector kernels (solver.hpp:271-300) -------------------------------
+template <typename T>
+__global__ void scale_to_T_kernel(const double* __restrict__ s, const double* __restrict__ v, T* __restrict__ t,
+                                  int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) t[i] = T(s[i] * v[i]);
+}
+template <typename T>
+__global__ void scale_from_T_kernel(const double* __restrict__ s, const T* __restrict__ at, double* __restrict__ w,
+                                    int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] = s[i] * double(at[i]);
+}
+template <typename T>
+__global__ void dinv_sqrt_kernel(const T* __restrict__ d, double* __restrict__ s, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) s[i] = 1.0 / sqrt(fmax(1e-300, double(d[i])));
+}
+__global__ void axpy_d_kernel(double a, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] -= a * x[i];
+}
+__global__ void scal_d_kernel(const double* __restrict__ x, double inv, double* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] / inv;
+}
+
+template <typename T>
+void launch_scale_to_T(const double* s, const double* v, T* t, int64_t n, cudaStream_t st) {
+  scale_to_T_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, v, t, n);
+}
+template <typename T>
+void launch_scale_from_T(const double* s, const T* at, double* w, int64_t n, cudaStream_t st) {
+  scale_from_T_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, at, w, n);
+}
+template <typename T>
+void launch_dinv_sqrt(const T* d, double* s, int64_t n, cudaStream_t st) {
+  dinv_sqrt_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d, s, n);
+}
+void launch_axpy_minus(double a, const double* x, double* y, int64_t n, cudaStream_t st) {
+  axpy_d_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, x, y, n);
+}
+void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st) {
+  scal_d_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, b, y, n);
+}
+template void launch_scale_to_T<double>(const double*, const double*, double*, int64_t, cudaStream_t);
+template void launch_scale_to_T<float>(const double*, const double*, float*, int64_t, cudaStream_t);
+template void launch_scale_from_T<double>(const double*, const double*, double*, int64_t, cudaStream_t);
+template void launch_scale_from_T<float>(const double*, const float*, double*, int64_t, cudaStream_t);
+template void launch_dinv_sqrt<double>(const double*, double*, int64_t, cudaStream_t);
+template void launch_dinv_sqrt<float>(const float*, double*, int64_t, cudaStream_t);
+
+}  // namespace emfgpu

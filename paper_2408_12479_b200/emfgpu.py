@@ -1,0 +1,415 @@
+"""Python binding of libemfgpu.so (include/emfgpu.h) with the reference's
+operator vocabulary (proj/include/elastmf/operator.hpp:49-204, mesh.hpp,
+solver.hpp).  This is the host mirror used by tests and bench.py; C++ callers
+use include/emfgpu/operator.hpp instead.  Device memory is anything exposing
+``data_ptr()`` (torch tensors) or a raw integer address.
+
+There is no CPU fallback: if the CUDA library or a device is missing, every
+constructor raises :class:`EmfGpuError`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libemfgpu.so")
+
+MODELS = {"cnh": 0, "inh": 1, "fiber": 2}
+STRATEGIES = {"none": 0, "scalar": 1, "tensor": 2, "cachedF": 3}
+MAPS = {"reference": 0, "shear_x": 1, "coords": 2}
+STATUS = {0: "OK", 1: "ERR_CONFIG", 2: "ERR_NUMERICAL", 3: "ERR_IO", 4: "ERR_INVALID", 5: "ERR_STALE",
+          6: "ERR_CUDA"}
+
+
+class EmfGpuError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"emfgpu {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class NonPositiveJacobian(EmfGpuError):
+    """det F <= 0 at (element, qpoint) (errors.hpp:31-38)."""
+
+    def __init__(self, code, msg, element, qpoint):
+        super().__init__(code, msg)
+        self.element = element
+        self.qpoint = qpoint
+
+
+class StaleCache(EmfGpuError):
+    pass
+
+
+class LevelDesc(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("p", C.c_int),
+                ("extent", C.c_double * 3), ("map", C.c_int), ("map_param", C.c_double * 4),
+                ("coords", C.c_void_p), ("dirichlet_faces", C.c_int), ("device", C.c_int),
+                ("z_offset", C.c_int)]
+
+
+class Material(C.Structure):
+    _fields_ = [("mu", C.c_double), ("lambda_", C.c_double), ("kappa_b", C.c_double), ("k1", C.c_double),
+                ("k2", C.c_double), ("a", C.c_double), ("b", C.c_double), ("phi", C.c_double),
+                ("e1", C.c_double * 3), ("e2", C.c_double * 3), ("e3", C.c_double * 3)]
+
+
+@dataclass
+class MaterialParams:
+    """MaterialParams (material.hpp:36-50). Defaults are the BASELINE configs'
+    (cNH mu=1, lambda=10; kappa_b for iNH/fiber; fibre k1=2, k2=5, +-40 deg)."""
+    mu: float = 1.0
+    lam: float = 10.0
+    kappa_b: float = 1000.0
+    k1: float = 2.0
+    k2: float = 5.0
+    a: float = 3.62
+    b: float = 34.3
+    phi: float = float(np.deg2rad(40.0))
+    e1: tuple = (1.0, 0.0, 0.0)
+    e2: tuple = (0.0, 1.0, 0.0)
+    e3: tuple = (0.0, 0.0, 1.0)
+
+    def to_c(self) -> Material:
+        m = Material()
+        m.mu, m.lambda_, m.kappa_b, m.k1, m.k2, m.a, m.b, m.phi = (
+            self.mu, self.lam, self.kappa_b, self.k1, self.k2, self.a, self.b, self.phi)
+        m.e1[:] = self.e1
+        m.e2[:] = self.e2
+        m.e3[:] = self.e3
+        return m
+
+    def as_array(self) -> np.ndarray:
+        """The 17-double layout used by oracle/ (mu, lambda, kappa, k1, k2, a, b, phi, e1, e2, e3)."""
+        return np.array([self.mu, self.lam, self.kappa_b, self.k1, self.k2, self.a, self.b, self.phi,
+                         *self.e1, *self.e2, *self.e3], dtype=np.float64)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EmfGpuError(6, f"{LIB_PATH} missing — run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, st = C.c_void_p, C.c_int64, C.c_int
+        sig = {
+            "emfgpu_version": (C.c_char_p, []),
+            "emfgpu_global_last_error": (C.c_char_p, []),
+            "emfgpu_level_create": (st, [C.POINTER(LevelDesc), C.POINTER(vp)]),
+            "emfgpu_level_destroy": (None, [vp]),
+            "emfgpu_level_n_dofs": (i64, [vp]),
+            "emfgpu_level_n_elements": (i64, [vp]),
+            "emfgpu_level_affine": (C.c_int, [vp]),
+            "emfgpu_level_jacobians": (st, [vp, vp]),
+            "emfgpu_level_coords": (st, [vp, vp]),
+            "emfgpu_level_last_error": (C.c_char_p, [vp]),
+            "emfgpu_op_create": (st, [vp, C.c_int, C.POINTER(Material), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+            "emfgpu_op_destroy": (None, [vp]),
+            "emfgpu_op_n_dofs": (i64, [vp]),
+            "emfgpu_op_precision": (C.c_int, [vp]),
+            "emfgpu_op_last_error": (C.c_char_p, [vp]),
+            "emfgpu_op_update_linearization_host": (st, [vp, vp, C.POINTER(i64), C.POINTER(C.c_int)]),
+            "emfgpu_op_update_linearization": (st, [vp, vp, C.POINTER(i64), C.POINTER(C.c_int), vp]),
+            "emfgpu_op_linearized": (C.c_int, [vp]),
+            "emfgpu_op_checksum": (C.c_uint64, [vp]),
+            "emfgpu_op_apply": (st, [vp, vp, vp, vp]),
+            "emfgpu_op_apply_host": (st, [vp, vp, vp]),
+            "emfgpu_op_check": (st, [vp, C.POINTER(i64), C.POINTER(C.c_int)]),
+            "emfgpu_op_compute_diagonal": (st, [vp, vp, C.POINTER(i64), vp]),
+            "emfgpu_op_compute_diagonal_host": (st, [vp, vp, C.POINTER(i64)]),
+            "emfgpu_op_ledger": (st, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double)]),
+            "emfgpu_op_apply_elements": (st, [vp, vp, C.c_int, C.c_int, vp]),
+            "emfgpu_op_apply_nodes": (st, [vp, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
+            "emfgpu_op_local_buffer": (vp, [vp]),
+            "emfgpu_op_face_values": (i64, [vp]),
+            "emfgpu_op_pack_face": (st, [vp, C.c_int, C.c_int, vp, vp]),
+            "emfgpu_transfer_create": (st, [vp, vp, C.POINTER(vp)]),
+            "emfgpu_transfer_destroy": (None, [vp]),
+            "emfgpu_transfer_apply": (st, [vp, C.c_int, C.c_int, vp, vp, vp]),
+            "emfgpu_cheb_create": (st, [vp, vp, C.c_double, C.c_int, C.c_double, C.c_double, C.POINTER(vp)]),
+            "emfgpu_cheb_destroy": (None, [vp]),
+            "emfgpu_cheb_smooth": (st, [vp, vp, vp, C.c_int, vp]),
+            "emfgpu_op_estimate_eigenvalues": (st, [vp, vp, C.c_int, C.c_uint64, C.POINTER(C.c_double),
+                                                    C.POINTER(C.c_double)]),
+            "emfgpu_dot": (st, [C.c_int, vp, vp, i64, C.POINTER(C.c_double), vp]),
+            "emfgpu_bench_fma_peak": (st, [C.c_int, C.c_double, C.POINTER(C.c_double)]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+class FeLevel:
+    """FeLevel(HexMesh, degree, DeformMap) + set_dirichlet (mesh.hpp:71-138);
+    EXT: nx != ny != nz boxes, per-axis extents, the cfg2 shear map, or any
+    node-coordinate array."""
+
+    def __init__(self, nx, ny=None, nz=None, p=2, extent=(1.0, 1.0, 1.0), map="reference",
+                 map_param=(0.0,), coords=None, dirichlet_faces=1, device=0, z_offset=0):
+        ny = nx if ny is None else ny
+        nz = nx if nz is None else nz
+        d = LevelDesc()
+        d.nx, d.ny, d.nz, d.p = nx, ny, nz, p
+        d.extent[:] = extent
+        d.map = MAPS["coords"] if coords is not None else MAPS[map]
+        mp = list(map_param) + [0.0] * (4 - len(map_param))
+        d.map_param[:] = mp
+        self._coords = None if coords is None else np.ascontiguousarray(coords, np.float64)
+        d.coords = None if coords is None else self._coords.ctypes.data
+        d.dirichlet_faces = dirichlet_faces
+        d.device = device
+        d.z_offset = z_offset
+        h = C.c_void_p()
+        st = lib().emfgpu_level_create(C.byref(d), C.byref(h))
+        if st:
+            raise EmfGpuError(st, lib().emfgpu_global_last_error().decode())
+        self.h = h.value
+        self.nx, self.ny, self.nz, self.p = nx, ny, nz, p
+        self.faces = dirichlet_faces
+        self.n_dofs = lib().emfgpu_level_n_dofs(self.h)
+        self.n_elements = lib().emfgpu_level_n_elements(self.h)
+        self.affine = bool(lib().emfgpu_level_affine(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().emfgpu_level_destroy(self.h)
+            self.h = None
+
+    def dof_count(self):
+        return self.n_dofs
+
+    def jacobians(self) -> np.ndarray:
+        out = np.empty(self.n_elements * (self.p + 1) ** 3 * 9)
+        _check(lib().emfgpu_level_jacobians(self.h, out.ctypes.data))
+        return out
+
+    def node_coords(self) -> np.ndarray:
+        out = np.empty(self.n_dofs)
+        _check(lib().emfgpu_level_coords(self.h, out.ctypes.data))
+        return out
+
+
+def _check(st, msg=""):
+    if st:
+        raise EmfGpuError(st, msg or lib().emfgpu_global_last_error().decode())
+
+
+@dataclass
+class ByteLedger:
+    storage_per_qp: int
+    traffic_per_qp: int
+    traffic_per_dof: float
+
+
+class ElasticOperator:
+    """ElasticOperator<Number> (operator.hpp:49-204) on one B200.
+
+    precision=64 -> Number=double, 32 -> float.  Host methods take/return
+    numpy arrays (parity path: PCIe copies inside); ``*_device`` methods take
+    device tensors and a stream and do not synchronise."""
+
+    def __init__(self, level: FeLevel, model="cnh", params: MaterialParams | None = None, strategy="none",
+                 precision=64, domain=0):
+        self.level = level
+        self.params = params or MaterialParams()
+        self.model, self.strategy, self.precision = model, strategy, precision
+        self.dtype = np.float64 if precision == 64 else np.float32
+        self._mat = self.params.to_c()
+        h = C.c_void_p()
+        st = lib().emfgpu_op_create(level.h, MODELS[model], C.byref(self._mat), domain, STRATEGIES[strategy],
+                                    precision, C.byref(h))
+        if st:
+            raise EmfGpuError(st, lib().emfgpu_global_last_error().decode())
+        self.h = h.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().emfgpu_op_destroy(self.h)
+            self.h = None
+
+    def _raise(self, st, e=None, q=None):
+        msg = lib().emfgpu_op_last_error(self.h).decode()
+        if st == 2 and e is not None and e.value >= 0 and "det(F)" in msg:
+            raise NonPositiveJacobian(st, msg, e.value, q.value)
+        if st == 5:
+            raise StaleCache(st, msg)
+        raise EmfGpuError(st, msg)
+
+    def n_dofs(self):
+        return lib().emfgpu_op_n_dofs(self.h)
+
+    def linearized(self):
+        return bool(lib().emfgpu_op_linearized(self.h))
+
+    def checksum(self):
+        return lib().emfgpu_op_checksum(self.h)
+
+    def update_linearization(self, u_k):
+        u = np.ascontiguousarray(u_k, np.float64)
+        e, q = C.c_int64(-1), C.c_int(-1)
+        st = lib().emfgpu_op_update_linearization_host(self.h, u.ctypes.data, C.byref(e), C.byref(q))
+        if st:
+            self._raise(st, e, q)
+
+    def update_linearization_device(self, d_u_k, stream=None):
+        e, q = C.c_int64(-1), C.c_int(-1)
+        st = lib().emfgpu_op_update_linearization(self.h, _ptr(d_u_k), C.byref(e), C.byref(q), _stream(stream))
+        if st:
+            self._raise(st, e, q)
+
+    def apply_tangent(self, du) -> np.ndarray:
+        x = np.ascontiguousarray(du, self.dtype)
+        y = np.empty_like(x)
+        st = lib().emfgpu_op_apply_host(self.h, x.ctypes.data, y.ctypes.data)
+        if st:
+            self._raise(st, C.c_int64(-1), C.c_int(-1))
+        return y
+
+    def apply_tangent_device(self, d_x, d_y, stream=None):
+        st = lib().emfgpu_op_apply(self.h, _ptr(d_x), _ptr(d_y), _stream(stream))
+        if st:
+            self._raise(st)
+
+    def check(self):
+        e, q = C.c_int64(-1), C.c_int(-1)
+        st = lib().emfgpu_op_check(self.h, C.byref(e), C.byref(q))
+        if st:
+            self._raise(st, e, q)
+
+    def compute_diagonal(self):
+        """Returns (diag, n_nonpositive) (operator.hpp:106-107 returns the index list)."""
+        d = np.empty(self.n_dofs(), self.dtype)
+        nb = C.c_int64(0)
+        st = lib().emfgpu_op_compute_diagonal_host(self.h, d.ctypes.data, C.byref(nb))
+        if st:
+            self._raise(st)
+        return d, nb.value
+
+    def compute_diagonal_device(self, d_diag, stream=None):
+        nb = C.c_int64(0)
+        st = lib().emfgpu_op_compute_diagonal(self.h, _ptr(d_diag), C.byref(nb), _stream(stream))
+        if st:
+            self._raise(st)
+        return nb.value
+
+    def byte_ledger(self) -> ByteLedger:
+        s, t, d = C.c_int(), C.c_int(), C.c_double()
+        _check(lib().emfgpu_op_ledger(self.h, C.byref(s), C.byref(t), C.byref(d)))
+        return ByteLedger(s.value, t.value, d.value)
+
+    # split apply for z slabs
+    def apply_elements(self, d_x, k0, k1, stream=None):
+        st = lib().emfgpu_op_apply_elements(self.h, _ptr(d_x), k0, k1, _stream(stream))
+        if st:
+            self._raise(st)
+
+    def apply_nodes(self, d_x, d_y, c0, c1, ghost_lo=None, ghost_hi=None, stream=None):
+        st = lib().emfgpu_op_apply_nodes(self.h, _ptr(d_x), _ptr(d_y), c0, c1, _ptr(ghost_lo), _ptr(ghost_hi),
+                                         _stream(stream))
+        if st:
+            self._raise(st)
+
+    def face_values(self):
+        return lib().emfgpu_op_face_values(self.h)
+
+    def pack_face(self, k, side, d_face, stream=None):
+        st = lib().emfgpu_op_pack_face(self.h, k, side, _ptr(d_face), _stream(stream))
+        if st:
+            self._raise(st)
+
+    def estimate_eigenvalues(self, d_diag, iterations=20, seed=0x9E3779B97F4A7C15):
+        lo, hi = C.c_double(), C.c_double()
+        st = lib().emfgpu_op_estimate_eigenvalues(self.h, _ptr(d_diag), iterations, seed, C.byref(lo), C.byref(hi))
+        if st:
+            self._raise(st)
+        return lo.value, hi.value
+
+
+class TransferOp:
+    """TransferOp(fine, coarse) (mesh.hpp:157-182) on device vectors."""
+
+    def __init__(self, fine: FeLevel, coarse: FeLevel):
+        h = C.c_void_p()
+        _check(lib().emfgpu_transfer_create(fine.h, coarse.h, C.byref(h)))
+        self.h = h.value
+        self.fine, self.coarse = fine, coarse
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().emfgpu_transfer_destroy(self.h)
+            self.h = None
+
+    def _run(self, kind, precision, d_in, d_out, stream):
+        _check(lib().emfgpu_transfer_apply(self.h, kind, precision, _ptr(d_in), _ptr(d_out), _stream(stream)))
+
+    def prolongate(self, d_coarse, d_fine, precision=64, stream=None):
+        self._run(0, precision, d_coarse, d_fine, stream)
+
+    def restrict_(self, d_fine, d_coarse, precision=64, stream=None):
+        self._run(1, precision, d_fine, d_coarse, stream)
+
+    def interpolate_down(self, d_fine, d_coarse, precision=64, stream=None):
+        self._run(2, precision, d_fine, d_coarse, stream)
+
+
+class ChebyshevSmoother:
+    """ChebyshevSmoother<Number> (solver.hpp:312-362): setup at construction."""
+
+    def __init__(self, op: ElasticOperator, d_diag, lmax_est, degree=6, range_factor=15.0, safety=1.2):
+        h = C.c_void_p()
+        st = lib().emfgpu_cheb_create(op.h, _ptr(d_diag), lmax_est, degree, range_factor, safety, C.byref(h))
+        if st:
+            op._raise(st)
+        self.h = h.value
+        self.op = op
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().emfgpu_cheb_destroy(self.h)
+            self.h = None
+
+    def smooth(self, d_x, d_b, zero_start=True, stream=None):
+        st = lib().emfgpu_cheb_smooth(self.h, _ptr(d_x), _ptr(d_b), int(zero_start), _stream(stream))
+        if st:
+            self.op._raise(st)
+
+
+def dot(d_a, d_b, n, precision=64, stream=None) -> float:
+    out = C.c_double()
+    _check(lib().emfgpu_dot(precision, _ptr(d_a), _ptr(d_b), n, C.byref(out), _stream(stream)))
+    return out.value
+
+
+def fma_peak_tflops(precision=64, seconds=0.5) -> float:
+    out = C.c_double()
+    _check(lib().emfgpu_bench_fma_peak(precision, seconds, C.byref(out)))
+    return out.value

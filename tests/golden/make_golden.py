@@ -1,0 +1,111 @@
+"""Generates tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref,
+compiled from /root/reference/proj by oracle/Makefile).  Run here (needs
+/root/reference to build oracle/_ref); the fixtures travel to the GPU box.
+
+The reference ships no golden vectors; these are outputs of the
+reference itself on the seeded inputs of paper_2408_12479_b200/inputs.py.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import refbind as R  # noqa: E402
+from paper_2408_12479_b200 import inputs as I  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def cfg0():
+    """BASELINE configs[0]: 8^3 Q2 cNH mu=1 lambda=10, fp64 (and fp32), none."""
+    L = R.RefLevel(1, 3, 2, 0.0, 1)
+    u0 = I.make_u0(8, 8, 8, 2)
+    v = I.make_v(L.ndofs)
+    prm = R.material_params(mu=1.0, lam=10.0)
+    out = {}  # u0/v are regenerated from the seeds by inputs.py
+    for prec in (64, 32):
+        op = R.RefOperator(L, "cnh", prm, "none", prec)
+        op.update_linearization(u0)
+        out[f"y{prec}"] = op.apply(v.astype(op.dtype))
+        out[f"diag{prec}"] = op.diagonal()[0]
+    np.savez_compressed(os.path.join(OUT, "cfg0.npz"), **out)
+    print("cfg0 |y64| =", np.linalg.norm(out["y64"]), "|diag64| =", np.linalg.norm(out["diag64"]))
+
+
+# small cases: (name, n, p, model, deform amplitude, u0 amplitude)
+SMALL = [
+    ("cnh_p1_n4_curved", 4, 1, "cnh", 0.05, 0.05),
+    ("cnh_p3_n2_curved", 2, 3, "cnh", 0.05, 0.05),
+    ("inh_p2_n4_curved", 4, 2, "inh", 0.05, 0.05),
+    ("inh_p4_n2_affine", 2, 4, "inh", 0.0, 0.05),
+    ("fiber_p2_n2_curved", 2, 2, "fiber", 0.05, 0.05),
+    ("fiber_p3_n2_affine", 2, 3, "fiber", 0.0, 0.05),
+]
+KAPPA = 50.0
+
+
+def small():
+    for name, n, p, model, damp, uamp in SMALL:
+        lev = {2: 1, 4: 2}[n]
+        L = R.RefLevel(1, lev, p, damp, 1)
+        prm = R.material_params(mu=1.0, lam=10.0, kappa=KAPPA)
+        u0 = I.make_u0(n, n, n, p, amp=uamp)
+        v = I.make_v(L.ndofs)
+        out = {"u0": u0, "v": v, "coords": L.coords(), "params": prm}
+        for prec in (64, 32):
+            for strat in ("none", "scalar", "tensor"):
+                if prec == 64 and strat != "none":
+                    continue  # fp64 strategies are bitwise identical in the reference
+                op = R.RefOperator(L, model, prm, strat, prec)
+                op.update_linearization(u0)
+                out[f"y{prec}_{strat}"] = op.apply(v.astype(op.dtype))
+            op = R.RefOperator(L, model, prm, "none", prec)
+            op.update_linearization(u0)
+            out[f"diag{prec}"] = op.diagonal()[0]
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+        print(name, L.ndofs)
+
+
+def transfers():
+    """TransferOp (mesh.hpp:157-289): p-steps 4->2->1 and an h-step 4->2."""
+    out = {}
+    for tag, (fl, fp, cl, cp) in {"p42": (1, 4, 1, 2), "p21": (1, 2, 1, 1), "h21": (2, 1, 1, 1)}.items():
+        F = R.RefLevel(1, fl, fp, 0.05, 1)
+        Cc = R.RefLevel(1, cl, cp, 0.05, 1)
+        xc = I.make_v(Cc.ndofs, 7)
+        xf = I.make_v(F.ndofs, 8)
+        out[f"{tag}_xc"] = xc
+        out[f"{tag}_xf"] = xf
+        out[f"{tag}_prolongate"] = R.transfer(F, Cc, "prolongate", xc)
+        out[f"{tag}_restrict"] = R.transfer(F, Cc, "restrict", xf)
+        out[f"{tag}_interpolate_down"] = R.transfer(F, Cc, "interpolate_down", xf)
+    np.savez_compressed(os.path.join(OUT, "transfers.npz"), **out)
+
+
+def smoother():
+    """Lanczos estimate + Chebyshev smoothing (solver.hpp:262-361) on a 4^3 Q2
+    iNH (kappa=50) level at u0 = 0 (SPD), fp32 and fp64."""
+    L = R.RefLevel(1, 2, 2, 0.0, 1)
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=KAPPA)
+    u0 = np.zeros(L.ndofs)
+    out = {}
+    for prec in (64, 32):
+        op = R.RefOperator(L, "inh", prm, "none", prec)
+        op.update_linearization(u0)
+        d = op.diagonal()[0]
+        lmin, lmax = op.estimate_eigenvalues(d)
+        b = I.make_v(L.ndofs, 9).astype(op.dtype)
+        x1 = op.chebyshev(d, lmax, b, np.zeros_like(b), degree=5)
+        x2 = op.chebyshev(d, lmax, b, x1, degree=5, zero_start=False)
+        out.update({f"diag{prec}": d, f"lmin{prec}": lmin, f"lmax{prec}": lmax, f"b{prec}": b,
+                    f"x1_{prec}": x1, f"x2_{prec}": x2})
+    np.savez_compressed(os.path.join(OUT, "smoother.npz"), **out)
+
+
+if __name__ == "__main__":
+    cfg0()
+    small()
+    transfers()
+    smoother()

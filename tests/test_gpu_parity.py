@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden fixtures from oracle/_ref) and the bit-exact C oracle.
+Tolerances (north star): rel-L2 <= 1e-12 in fp64, <= 1e-5 in fp32."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2408_12479_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {64: 1e-12, 32: 1e-5}
+SMALL = ["cnh_p1_n4_curved", "cnh_p3_n2_curved", "inh_p2_n4_curved", "inh_p4_n2_affine",
+         "fiber_p2_n2_curved", "fiber_p3_n2_affine"]
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2408_12479_b200 import emfgpu
+    return emfgpu
+
+
+def params_from(arr, G):
+    return G.MaterialParams(mu=arr[0], lam=arr[1], kappa_b=arr[2], k1=arr[3], k2=arr[4], a=arr[5], b=arr[6],
+                            phi=arr[7], e1=tuple(arr[8:11]), e2=tuple(arr[11:14]), e3=tuple(arr[14:17]))
+
+
+def test_cfg0_vs_reference(G):
+    g = np.load(os.path.join(GOLD, "cfg0.npz"))
+    lev = G.FeLevel(8, p=2, dirichlet_faces=1)
+    assert lev.affine
+    u0 = I.make_u0(8, 8, 8, 2)
+    v = I.make_v(lev.n_dofs)
+    for prec in (64, 32):
+        op = G.ElasticOperator(lev, "cnh", G.MaterialParams(mu=1.0, lam=10.0), "none", prec)
+        op.update_linearization(u0)
+        y = op.apply_tangent(v)
+        assert rel(y, g[f"y{prec}"]) <= TOL[prec]
+        assert rel(y, g["y64"]) <= TOL[prec]
+        mask = I.dirichlet_mask(8, 8, 8, 2, 1)
+        assert np.array_equal(y[mask], v.astype(op.dtype)[mask])  # identity rows, operator.hpp:617-620
+        y2 = op.apply_tangent(v)
+        assert np.array_equal(y, y2)  # run-to-run bitwise determinism
+        d, nb = op.compute_diagonal()
+        assert nb == 0 and rel(d, g[f"diag{prec}"]) <= TOL[prec]
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("strategy", ["none", "scalar", "tensor", "cachedF"])
+def test_small_vs_reference(G, name, prec, strategy):
+    g = np.load(os.path.join(GOLD, f"{name}.npz"))
+    model, pp, nn = name.split("_")[:3]
+    p, n = int(pp[1:]), int(nn[1:])
+    lev = G.FeLevel(n, p=p, coords=g["coords"], dirichlet_faces=1)
+    op = G.ElasticOperator(lev, model, params_from(g["params"], G), strategy, prec)
+    op.update_linearization(g["u0"])
+    y = op.apply_tangent(g["v"])
+    key = f"y{prec}_{strategy if (prec == 32 and strategy != 'cachedF') else 'none'}"
+    assert rel(y, g[key]) <= TOL[prec], rel(y, g[key])
+    d, nb = op.compute_diagonal()
+    assert rel(d, g[f"diag{prec}"]) <= TOL[prec], rel(d, g[f"diag{prec}"])
+
+
+def test_geometry_matches_reference_jacobians(G):
+    from oracle import orcbind as O
+    g = np.load(os.path.join(GOLD, "inh_p2_n4_curved.npz"))
+    lev = G.FeLevel(4, p=2, coords=g["coords"])
+    assert not lev.affine
+    orc = O.OracleOperator(4, 4, 4, 2, g["coords"], 1, "inh", g["params"])
+    assert rel(lev.jacobians(), orc.jacobians()) <= 1e-14
+
+
+def test_cfg1_full_size_known_answers(G):
+    """BASELINE configs[1] at full size (32^3 Q3, 2 738 019 DoFs) against the
+    reference's known answers and the oracle."""
+    lev = G.FeLevel(32, p=3)
+    u0 = I.make_u0(32, 32, 32, 3)
+    v = I.make_v(lev.n_dofs)
+    assert np.isclose(np.linalg.norm(u0), 28.816069046240159, rtol=1e-13)
+    ys = {}
+    for prec in (64, 32):
+        for strategy in ("none", "cachedF", "scalar", "tensor"):
+            op = G.ElasticOperator(lev, "cnh", G.MaterialParams(mu=1.0, lam=10.0), strategy, prec)
+            op.update_linearization(u0)
+            ys[(prec, strategy)] = op.apply_tangent(v)
+    y = ys[(64, "none")]
+    assert np.isclose(np.linalg.norm(y), 892.45567630658536, rtol=1e-12)
+    node = (48 * 97 + 48) * 97 + 48
+    assert y[3 * node:3 * node + 3] == pytest.approx(
+        [-0.21301797238610545, -0.00067067958362078579, -0.2998014835832995], rel=1e-10, abs=1e-13)
+    for (prec, strategy), yy in ys.items():
+        assert rel(yy, y) <= TOL[prec], (prec, strategy, rel(yy, y))
+    from oracle import orcbind as O
+    orc = O.OracleOperator(32, 32, 32, 3, model="cnh", params=np.array(
+        [1.0, 10.0, 1000.0, 2.0, 5.0, 3.62, 34.3, 0.7, 1, 0, 0, 0, 1, 0, 0, 0, 1]))
+    orc.update_linearization(u0)
+    assert rel(y, orc.apply(v)) <= 1e-12
+
+
+def test_nonpositive_jacobian_first_point_matches_oracle(G):
+    from oracle import orcbind as O
+    lev = G.FeLevel(2, p=2)
+    u = np.zeros(lev.n_dofs)
+    u[3 * 40] = -5.0
+    orc = O.OracleOperator(2, 2, 2, 2)
+    with pytest.raises(O.OracleError) as eo:
+        orc.update_linearization(u)
+    op = G.ElasticOperator(lev, "cnh")
+    with pytest.raises(G.NonPositiveJacobian) as eg:
+        op.update_linearization(u)
+    assert f"element={eg.value.element} qpoint={eg.value.qpoint}" in str(eo.value)
+
+
+def test_stale_cache(G):
+    op = G.ElasticOperator(G.FeLevel(2, p=2), "cnh")
+    with pytest.raises(G.StaleCache):
+        op.apply_tangent(np.zeros(op.n_dofs()))
+
+
+def test_transfers_vs_reference(G):
+    import torch
+    g = np.load(os.path.join(GOLD, "transfers.npz"))
+    dims = {"p42": ((2, 4), (2, 2)), "p21": ((2, 2), (2, 1)), "h21": ((4, 1), (2, 1))}
+    for tag, ((nf, pf), (nc, pc)) in dims.items():
+        F = G.FeLevel(nf, p=pf, map_param=(0.05,))
+        Cl = G.FeLevel(nc, p=pc, map_param=(0.05,))
+        t = G.TransferOp(F, Cl)
+        for prec, dt in ((64, torch.float64), (32, torch.float32)):
+            xc = torch.tensor(g[f"{tag}_xc"], dtype=dt, device="cuda")
+            xf = torch.tensor(g[f"{tag}_xf"], dtype=dt, device="cuda")
+            of = torch.empty(F.n_dofs, dtype=dt, device="cuda")
+            oc = torch.empty(Cl.n_dofs, dtype=dt, device="cuda")
+            t.prolongate(xc, of, prec)
+            torch.cuda.synchronize()
+            assert rel(of.cpu().numpy(), g[f"{tag}_prolongate"]) <= TOL[prec]
+            t.restrict_(xf, oc, prec)
+            torch.cuda.synchronize()
+            assert rel(oc.cpu().numpy(), g[f"{tag}_restrict"]) <= TOL[prec]
+            t.interpolate_down(xf, oc, prec)
+            torch.cuda.synchronize()
+            assert rel(oc.cpu().numpy(), g[f"{tag}_interpolate_down"]) <= TOL[prec]
+
+
+def test_smoother_and_eigenvalues_vs_reference(G):
+    import torch
+    g = np.load(os.path.join(GOLD, "smoother.npz"))
+    lev = G.FeLevel(4, p=2)
+    for prec, dt in ((64, torch.float64), (32, torch.float32)):
+        op = G.ElasticOperator(lev, "inh", G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0), "none", prec)
+        op.update_linearization(np.zeros(lev.n_dofs))
+        d = torch.empty(lev.n_dofs, dtype=dt, device="cuda")
+        assert op.compute_diagonal_device(d) == 0
+        assert rel(d.cpu().numpy(), g[f"diag{prec}"]) <= TOL[prec]
+        lmin, lmax = op.estimate_eigenvalues(d)
+        assert abs(lmax - float(g[f"lmax{prec}"])) <= 1e-6 * abs(float(g[f"lmax{prec}"]))
+        sm = G.ChebyshevSmoother(op, d, float(g[f"lmax{prec}"]), degree=5)
+        b = torch.tensor(g[f"b{prec}"], dtype=dt, device="cuda")
+        x = torch.zeros_like(b)
+        sm.smooth(x, b, zero_start=True)
+        torch.cuda.synchronize()
+        assert rel(x.cpu().numpy(), g[f"x1_{prec}"]) <= 10 * TOL[prec]
+        sm.smooth(x, b, zero_start=False)
+        torch.cuda.synchronize()
+        assert rel(x.cpu().numpy(), g[f"x2_{prec}"]) <= 10 * TOL[prec]
+
+
+def test_split_apply_and_slab_emulation(G):
+    """apply == element phase + node phase; and a 2-slab decomposition with
+    ghost faces reproduces the single-level result BITWISE (same colour-order
+    sums on the interface plane)."""
+    import torch
+    n, p = 4, 2
+    lev = G.FeLevel(n, p=p, dirichlet_faces=1 | 16)
+    u0 = I.make_u0(n, n, n, p, faces=1 | 16)
+    v = I.make_v(lev.n_dofs)
+    op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+    op.update_linearization(u0)
+    y_full = op.apply_tangent(v)
+    X, Y, Z = I.lattice_positions(n, n, n, p)
+    coords = np.stack([X, Y, Z], 1).ravel()
+    m = n * p + 1
+    plane = 3 * m * m
+    ys = []
+    halves = [(0, 1), (1, 4)]  # odd split: exercises the colour parity offset
+    ops, xs, faces = [], [], []
+    for r, (k0, k1) in enumerate(halves):
+        c0, c1 = k0 * p, k1 * p
+        sl = slice(c0 * plane, (c1 + 1) * plane)
+        lv = G.FeLevel(n, n, k1 - k0, p=p, coords=coords[sl], dirichlet_faces=1 | (16 if r == 0 else 0),
+                       z_offset=k0)
+        o = G.ElasticOperator(lv, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+        o.update_linearization(u0[sl])
+        x = torch.tensor(v[sl], device="cuda")
+        o.apply_elements(x, 0, k1 - k0)
+        ops.append(o)
+        xs.append(x)
+    f_lo = torch.empty(ops[0].face_values(), dtype=torch.float64, device="cuda")
+    f_hi = torch.empty(ops[1].face_values(), dtype=torch.float64, device="cuda")
+    ops[0].pack_face(0, 1, f_lo)  # top layer of rank 0, upper face -> rank 1's ghost_lo
+    ops[1].pack_face(0, 0, f_hi)  # bottom layer of rank 1, lower face -> rank 0's ghost_hi
+    for r, o in enumerate(ops):
+        yv = torch.empty_like(xs[r])
+        mz = (halves[r][1] - halves[r][0]) * p + 1
+        o.apply_nodes(xs[r], yv, 0, mz - 1, ghost_lo=f_lo if r == 1 else None, ghost_hi=f_hi if r == 0 else None)
+        torch.cuda.synchronize()
+        ys.append(yv.cpu().numpy())
+    y_split = np.concatenate([ys[0], ys[1][plane:]])
+    assert np.array_equal(ys[0][-plane:], ys[1][:plane])
+    assert np.array_equal(y_split, y_full)

@@ -1,0 +1,151 @@
+"""CPU tests: the C restatement (oracle/emf_oracle.c) against the reference's
+own outputs (golden fixtures from oracle/_ref) and the reference's known
+constants.  The oracle must be BIT-EXACT to the reference; that is what makes
+it a valid checker for the CUDA path."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import orcbind as O
+from paper_2408_12479_b200 import inputs as I
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SMALL = ["cnh_p1_n4_curved", "cnh_p3_n2_curved", "inh_p2_n4_curved", "inh_p4_n2_affine",
+         "fiber_p2_n2_curved", "fiber_p3_n2_affine"]
+MODEL = {"cnh": "cnh", "inh": "inh", "fiber": "fiber"}
+
+
+def _case(name):
+    model, pp, nn, _ = name.split("_")
+    return model, int(pp[1:]), int(nn[1:])
+
+
+def test_inputs_reproduce_survey_known_answers():
+    # ||u0||, ||v|| of cfg0 and cfg1 (reference generator).
+    u0 = I.make_u0(8, 8, 8, 2)
+    v = I.make_v(u0.size)
+    assert np.isclose(np.linalg.norm(u0), 1.9603902670929043, rtol=1e-14)
+    assert np.isclose(np.linalg.norm(v), 70.098428167379268, rtol=1e-14)
+    assert v[:3].tolist() == pytest.approx([0.13312315034456179, 0.49156351452540226, 0.94200550717359244],
+                                           rel=1e-15)
+
+
+def test_splitmix64_matches_scalar_definition():
+    # solver.hpp:209-219, written out with Python ints
+    def sm(state):
+        state = (state + 0x9E3779B97F4A7C15) & (2**64 - 1)
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+        return state, z ^ (z >> 31)
+    s, ref = 7, []
+    for _ in range(50):
+        s, z = sm(s)
+        ref.append(z)
+    assert I.splitmix64_stream(7, 50).tolist() == ref
+
+
+def test_oracle_cfg0_bitexact_vs_reference_golden():
+    g = np.load(os.path.join(GOLD, "cfg0.npz"))
+    u0 = I.make_u0(8, 8, 8, 2)
+    v = I.make_v(u0.size)
+    prm = np.array([1.0, 10.0, 1000.0, 2.0, 5.0, 3.62, 34.3, np.deg2rad(40), 1, 0, 0, 0, 1, 0, 0, 0, 1])
+    for prec in (64, 32):
+        op = O.OracleOperator(8, 8, 8, 2, model="cnh", params=prm, strategy="none", precision=prec)
+        op.update_linearization(u0)
+        y = op.apply(v.astype(op.dtype))
+        assert np.array_equal(y, g[f"y{prec}"])
+        d, nb = op.diagonal()
+        assert np.array_equal(d, g[f"diag{prec}"]) and nb == 0
+    # SURVEY §8(c) known answers
+    assert np.isclose(np.linalg.norm(g["y64"]), 240.93765195277956, rtol=1e-14)
+    node = (8 * 17 + 8) * 17 + 8
+    assert g["y64"][3 * node:3 * node + 3] == pytest.approx(
+        [-1.2687094083128543, 1.607692006743817, 0.13302019928913428], rel=1e-13)
+    assert np.isclose(np.linalg.norm(g["diag64"]), 298.73218954820248, rtol=1e-14)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_small_bitexact_vs_reference_golden(name):
+    g = np.load(os.path.join(GOLD, f"{name}.npz"))
+    model, p, n = _case(name)
+    for prec in (64, 32):
+        strategies = ("none",) if prec == 64 else ("none", "scalar", "tensor")
+        for strat in strategies:
+            op = O.OracleOperator(n, n, n, p, g["coords"], 1, model, g["params"], strat, prec)
+            op.update_linearization(g["u0"])
+            y = op.apply(g["v"].astype(op.dtype))
+            assert np.array_equal(y, g[f"y{prec}_{strat}"]), (prec, strat)
+        op = O.OracleOperator(n, n, n, p, g["coords"], 1, model, g["params"], "none", prec)
+        op.update_linearization(g["u0"])
+        assert np.array_equal(op.diagonal()[0], g[f"diag{prec}"])
+
+
+def test_oracle_strategies_bitwise_equal_fp64():
+    # acceptance.cpp:256-307: strategies agree (observed spread 0.0 in fp64)
+    g = np.load(os.path.join(GOLD, "inh_p2_n4_curved.npz"))
+    ys = []
+    for strat in ("none", "scalar", "tensor"):
+        op = O.OracleOperator(4, 4, 4, 2, g["coords"], 1, "inh", g["params"], strat, 64)
+        op.update_linearization(g["u0"])
+        ys.append(op.apply(g["v"]))
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
+
+
+def test_oracle_transfers_bitexact():
+    g = np.load(os.path.join(GOLD, "transfers.npz"))
+    dims = {"p42": ((2, 2, 2, 4), (2, 2, 2, 2)), "p21": ((2, 2, 2, 2), (2, 2, 2, 1)),
+            "h21": ((4, 4, 4, 1), (2, 2, 2, 1))}
+    for tag, (fd, cd) in dims.items():
+        assert np.array_equal(O.transfer(fd, cd, "prolongate", g[f"{tag}_xc"]), g[f"{tag}_prolongate"])
+        assert np.array_equal(O.transfer(fd, cd, "restrict", g[f"{tag}_xf"]), g[f"{tag}_restrict"])
+        assert np.array_equal(O.transfer(fd, cd, "interpolate_down", g[f"{tag}_xf"]), g[f"{tag}_interpolate_down"])
+
+
+def test_oracle_smoother_and_lanczos_bitexact():
+    g = np.load(os.path.join(GOLD, "smoother.npz"))
+    prm = np.array([1.0, 10.0, 50.0, 2.0, 5.0, 3.62, 34.3, np.deg2rad(40), 1, 0, 0, 0, 1, 0, 0, 0, 1])
+    for prec in (64, 32):
+        op = O.OracleOperator(4, 4, 4, 2, model="inh", params=prm, precision=prec)
+        op.update_linearization(np.zeros(op.n))
+        d, _ = op.diagonal()
+        assert np.array_equal(d, g[f"diag{prec}"])
+        lmin, lmax = op.estimate_eigenvalues(d)
+        assert (lmin, lmax) == (float(g[f"lmin{prec}"]), float(g[f"lmax{prec}"]))
+        x1 = op.chebyshev(d, lmax, g[f"b{prec}"], np.zeros(op.n), degree=5)
+        assert np.array_equal(x1, g[f"x1_{prec}"])
+        x2 = op.chebyshev(d, lmax, g[f"b{prec}"], x1, degree=5, zero_start=False)
+        assert np.array_equal(x2, g[f"x2_{prec}"])
+
+
+def test_oracle_structure_tensors_acceptance_constants():
+    # acceptance.cpp:44-54: (H11, H22, H33) = (0.9168, 0.0759, 0.0073) +- 5e-5
+    prm = np.array([62.1, 3042.9, 3084.3, 1.4, 22.1, 3.62, 34.3, 27.47 * np.pi / 180, 1, 0, 0, 0, 1, 0, 0, 0, 1])
+    st = O.structure_tensors(prm)
+    assert abs(st[18] - 0.9168) <= 5e-5 and abs(st[19] - 0.0759) <= 5e-5 and abs(st[20] - 0.0073) <= 5e-5
+
+
+def test_oracle_nonpositive_jacobian_reports_first_point():
+    op = O.OracleOperator(2, 2, 2, 2)
+    u = np.zeros(op.n)
+    u[3 * 40] = -5.0  # an interior node pushed through its neighbours
+    with pytest.raises(O.OracleError) as ei:
+        op.update_linearization(u)
+    assert ei.value.code == 3 and "element=" in str(ei.value)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(O.HERE), "oracle", "_ref", "libemfref.so")),
+                    reason="oracle/_ref not built")
+def test_oracle_vs_live_reference_box_and_curved():
+    from oracle import refbind as R
+    L = R.RefLevel(1, 2, 3, 0.05, 1)
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=100.0)
+    u0 = I.make_u0(4, 4, 4, 3, amp=0.05)
+    v = I.make_v(L.ndofs, 3)
+    for model in ("cnh", "inh", "fiber"):
+        ref = R.RefOperator(L, model, prm, "tensor", 32)
+        ref.update_linearization(u0)
+        orc = O.OracleOperator(4, 4, 4, 3, L.coords(), 1, model, prm, "tensor", 32)
+        orc.update_linearization(u0)
+        assert np.array_equal(ref.apply(v.astype(np.float32)), orc.apply(v.astype(np.float32)))
