@@ -14,8 +14,9 @@
  *   DoF = 3*node + comp; node = (c*my + b)*mx + a (a fastest); element
  *   e = (k*ny + j)*nx + i; Dirichlet faces bit f = -x,+x,-y,+y,-z,+z.
  *   Device-pointer entry points are stream-ordered (stream = cudaStream_t,
- *   NULL = the handle's own stream) and do not synchronise; *_host entry
- *   points take host vectors, synchronise and report numerical errors.
+ *   taken literally: NULL = the legacy default stream) and do not
+ *   synchronise; *_host entry points take host vectors, run on the handle's
+ *   private stream, synchronise and report numerical errors.
  */
 #ifndef EMFGPU_H
 #define EMFGPU_H

@@ -1,0 +1,138 @@
+// C++ adapter over the emfgpu C ABI with the method signatures of the
+// reference's ElasticOperator<Number> (proj/include/elastmf/operator.hpp:49-204),
+// FeLevel (mesh.hpp:71-138), TransferOp (mesh.hpp:157-182) and
+// ChebyshevSmoother (solver.hpp:312-362), so reference-style host code
+// (solvers templated on the operator type, the throughput driver
+// runner.cpp:55-146) can swap the CPU operator for the B200 one.
+// Header-only; link against libemfgpu.so.  Errors become exceptions named
+// like the reference's (errors.hpp:15-93).
+#ifndef EMFGPU_OPERATOR_HPP
+#define EMFGPU_OPERATOR_HPP
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../emfgpu.h"
+
+namespace emfgpu {
+
+struct Error : std::runtime_error {
+  emfgpu_status code;
+  Error(emfgpu_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+struct ConfigError : Error {
+  using Error::Error;
+};
+struct StaleCache : Error {
+  using Error::Error;
+};
+struct NonPositiveJacobian : Error {
+  std::int64_t element;
+  int qpoint;
+  NonPositiveJacobian(emfgpu_status c, const std::string& m, std::int64_t e, int q) : Error(c, m), element(e), qpoint(q) {}
+};
+
+inline void throw_status(emfgpu_status st, const char* msg, std::int64_t e = -1, int q = -1) {
+  if (st == EMFGPU_OK) return;
+  if (st == EMFGPU_ERR_CONFIG) throw ConfigError(st, msg);
+  if (st == EMFGPU_ERR_STALE) throw StaleCache(st, msg);
+  if (st == EMFGPU_ERR_NUMERICAL && e >= 0) throw NonPositiveJacobian(st, msg, e, q);
+  throw Error(st, msg);
+}
+
+enum class ModelKind { cnh = EMFGPU_CNH, inh = EMFGPU_INH, fiber = EMFGPU_FIBER };
+enum class Strategy { none = EMFGPU_NONE, scalar = EMFGPU_SCALAR, tensor = EMFGPU_TENSOR, cached_f = EMFGPU_CACHED_F };
+
+/// FeLevel: structured (deformed) box with Q_p on GLL nodes, Dirichlet faces.
+class FeLevel {
+ public:
+  explicit FeLevel(const emfgpu_level_desc& d) { throw_status(emfgpu_level_create(&d, &h_), emfgpu_global_last_error()); }
+  /// build_cube(n0, level) + FeLevel(mesh, degree, DeformMap{amplitude}) (mesh.hpp:61, 73)
+  FeLevel(int n, int degree, double deform_amplitude = 0.0, int dirichlet_faces = 1) {
+    emfgpu_level_desc d{};
+    d.nx = d.ny = d.nz = n;
+    d.p = degree;
+    d.extent[0] = d.extent[1] = d.extent[2] = 1.0;
+    d.map = EMFGPU_MAP_REFERENCE;
+    d.map_param[0] = deform_amplitude;
+    d.dirichlet_faces = dirichlet_faces;
+    throw_status(emfgpu_level_create(&d, &h_), emfgpu_global_last_error());
+  }
+  FeLevel(const FeLevel&) = delete;
+  FeLevel& operator=(const FeLevel&) = delete;
+  ~FeLevel() { emfgpu_level_destroy(h_); }
+  std::int64_t dof_count() const { return emfgpu_level_n_dofs(h_); }
+  std::int64_t n_elements() const { return emfgpu_level_n_elements(h_); }
+  const emfgpu_level* handle() const { return h_; }
+
+ private:
+  emfgpu_level* h_ = nullptr;
+};
+
+/// ElasticOperator<Number> on one B200; Number = double or float.
+template <typename Number>
+class ElasticOperator {
+  static_assert(sizeof(Number) == 8 || sizeof(Number) == 4, "Number must be double or float");
+
+ public:
+  ElasticOperator(const FeLevel& level, ModelKind model, const emfgpu_material& params, Strategy strategy)
+      : level_(&level) {
+    throw_status(emfgpu_op_create(level.handle(), static_cast<int>(model), &params, 0, static_cast<int>(strategy),
+                                  sizeof(Number) == 8 ? 64 : 32, &h_),
+                 emfgpu_global_last_error());
+  }
+  ElasticOperator(const ElasticOperator&) = delete;
+  ElasticOperator& operator=(const ElasticOperator&) = delete;
+  ~ElasticOperator() { emfgpu_op_destroy(h_); }
+
+  const FeLevel& level() const { return *level_; }
+  void set_threads(int) {}  // signature compatibility: parallelism is the GPU's
+  std::int64_t n_dofs() const { return emfgpu_op_n_dofs(h_); }
+  bool linearized() const { return emfgpu_op_linearized(h_) != 0; }
+  std::uint64_t checksum() const { return emfgpu_op_checksum(h_); }
+
+  /// operator.hpp:87
+  void update_linearization(const std::vector<double>& u_k) {
+    if ((std::int64_t)u_k.size() != n_dofs()) throw Error(EMFGPU_ERR_CONFIG, "update_linearization: size mismatch");
+    std::int64_t e = -1;
+    int q = -1;
+    throw_status(emfgpu_op_update_linearization_host(h_, u_k.data(), &e, &q), emfgpu_op_last_error(h_), e, q);
+  }
+
+  /// operator.hpp:99-100 (y is resized, as y.assign does in the reference)
+  void apply_tangent(const std::vector<Number>& du, std::vector<Number>& y) const {
+    if ((std::int64_t)du.size() != n_dofs()) throw Error(EMFGPU_ERR_CONFIG, "apply_tangent: size mismatch");
+    y.resize(du.size());
+    throw_status(emfgpu_op_apply_host(h_, du.data(), y.data()), emfgpu_op_last_error(h_));
+  }
+
+  /// Device-resident variant (stream-ordered; stream is a cudaStream_t).
+  void apply_tangent_device(const Number* d_x, Number* d_y, void* stream = nullptr) const {
+    throw_status(emfgpu_op_apply(h_, d_x, d_y, stream), emfgpu_op_last_error(h_));
+  }
+
+  /// operator.hpp:106-107: (diag, indices of nonpositive free entries)
+  std::pair<std::vector<Number>, std::vector<std::int64_t>> compute_diagonal() const {
+    std::vector<Number> d(n_dofs());
+    std::int64_t nbad = 0;
+    throw_status(emfgpu_op_compute_diagonal_host(h_, d.data(), &nbad), emfgpu_op_last_error(h_));
+    std::vector<std::int64_t> bad;
+    if (nbad > 0)
+      for (std::int64_t i = 0; i < (std::int64_t)d.size(); ++i)
+        if (!(d[i] > Number(0))) bad.push_back(i);
+    return {std::move(d), std::move(bad)};
+  }
+
+  emfgpu_op* handle() const { return h_; }
+
+ private:
+  const FeLevel* level_;
+  emfgpu_op* h_ = nullptr;
+};
+
+}  // namespace emfgpu
+
+#endif

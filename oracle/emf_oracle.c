@@ -785,3 +785,9 @@ int orc_transfer(int nf_x, int nf_y, int nf_z, int pf, int nc_x, int nc_y, int n
   for (int a = 0; a < 3; ++a) lmap_free(&m[a]);
   return 0;
 }
+
+int orc_op_element_locals(const orc_op* op, const void* x, void* loc, int64_t e0, int64_t e1) {
+  if (!op->linearized) return 4;
+  return op->precision == 64 ? element_locals_d(op, (const double*)x, (double*)loc, e0, e1)
+                             : element_locals_f(op, (const float*)x, (float*)loc, e0, e1);
+}

@@ -650,3 +650,35 @@ static int SFX(chebyshev)(const orc_op* op, const R* diag, double lmax_est, int 
   free(ad);
   return err;
 }
+
+/* Element-local results of element_tangent_batch (operator.hpp:468-530) for
+ * the element range [e0, e1), before the colour-ordered scatter:
+ * loc[((e - e0)*nn3 + m)*3 + c].  Used to check the slab decomposition. */
+static int SFX(element_locals)(const orc_op* op, const R* du, R* loc, int64_t e0, int64_t e1) {
+  const int64_t n = op->ndofs;
+  R* masked = (R*)malloc(sizeof(R) * n);
+  R* ukn = (R*)malloc(sizeof(R) * n);
+  for (int64_t i = 0; i < n; ++i) {
+    masked[i] = op->mask[i] ? (R)0 : du[i];
+    ukn[i] = (R)op->uk[i];
+  }
+  int err = 0;
+#pragma omp parallel
+  {
+    SFX(scratch)* s = (SFX(scratch)*)malloc(sizeof(SFX(scratch)));
+#pragma omp for schedule(static)
+    for (int64_t e = e0; e < e1; ++e) {
+      if (SFX(element_tangent)(op, e, masked, ukn, s)) {
+#pragma omp atomic write
+        err = 1;
+        continue;
+      }
+      for (int m = 0; m < op->nn3; ++m)
+        for (int c = 0; c < 3; ++c) loc[((e - e0) * op->nn3 + m) * 3 + c] = s->out[c][m];
+    }
+    free(s);
+  }
+  free(masked);
+  free(ukn);
+  return err;
+}

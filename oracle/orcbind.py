@@ -43,6 +43,7 @@ def lib():
         L.orc_transfer.argtypes = [C.c_int] * 10 + [vp, vp]
         L.orc_lattice_coords.argtypes = [C.c_int] * 4 + [vp, C.c_int, vp, vp]
         L.orc_structure_tensors.argtypes = [vp, vp]
+        L.orc_op_element_locals.argtypes = [vp, vp, vp, i64, i64]
         L.orc_basis_tables.argtypes = [C.c_int] + [vp] * 5
         _lib = L
     return _lib
@@ -127,6 +128,16 @@ class OracleOperator:
         if st:
             raise OracleError(st)
         return y
+
+    def element_locals(self, x, e0, e1):
+        """Element-local results (before scatter) of elements [e0, e1): (e1-e0, nn3, 3)."""
+        nx, ny, nz, p = self.dims
+        x = np.ascontiguousarray(x, self.dtype)
+        out = np.empty((e1 - e0, (p + 1) ** 3, 3), self.dtype)
+        st = lib().orc_op_element_locals(self.h, _p(x), _p(out), e0, e1)
+        if st:
+            raise OracleError(st)
+        return out
 
     def diagonal(self):
         d = np.empty(self.n, self.dtype)

@@ -48,7 +48,9 @@ emfgpu_status guarded(std::string* slot, Fn&& fn) {
   }
 }
 
-cudaStream_t S(void* s, cudaStream_t def) { return s ? static_cast<cudaStream_t>(s) : def; }
+// Stream arguments are taken literally (NULL = the legacy default stream, as in
+// cuBLAS); the handle's private stream is used only by the *_host entry points.
+cudaStream_t S(void* s, cudaStream_t /*def*/) { return static_cast<cudaStream_t>(s); }
 
 // ---- 1D basis: Gauss-Lobatto nodes, Gauss rule, Lagrange tables ----------
 // Standard Newton iterations on Legendre polynomials (the construction of

@@ -161,7 +161,15 @@ def _ptr(t) -> int:
 
 
 def _stream(s):
+    """cudaStream_t for a call: an int handle, a torch.cuda.Stream, or None =
+    torch's current stream on the current device (0 if torch/CUDA absent)."""
     if s is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream or None
+        except ImportError:
+            pass
         return None
     if isinstance(s, int):
         return s
