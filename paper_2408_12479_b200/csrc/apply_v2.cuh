@@ -1,0 +1,441 @@
+// Tangent-apply element phase, v2 (the production kernel).
+//
+// Differences from the first version (kernels.cuh:apply_kernel), each driven
+// by the round-1 ncu profile (profiles/r01_ncu_apply_fp64_none.txt: fp64 pipe
+// 33%, stalls long-scoreboard > wait > short-scoreboard > MIO throttle):
+//  * persistent CTAs (one wave, occupancy-sized) loop over element groups and
+//    prefetch the NEXT group's x / u_k / affine geometry into a second shared
+//    staging buffer with cp.async while the current group computes;
+//  * sum factorization by pencil workers: a worker owns one (component, line)
+//    pencil and performs the full 1D contraction in registers, so every
+//    shared load feeds n FMAs and the 1D tables are compile-time-indexed
+//    kernel parameters (constant-bank operands, no shared loads);
+//  * power-of-two n uses an XOR-swizzled element layout that makes all three
+//    pencil orientations and the per-point accesses bank-conflict free;
+//  * element-local results are stored component-major, loc[(e*3 + c)*n^3 + m],
+//    as contiguous vector stores.
+// The quadrature-point algebra is unchanged (qp.cuh), so is the result up to
+// summation order inside the sweeps.
+#pragma once
+#include "kernels.cuh"
+
+namespace emfgpu {
+
+// Per-element array layout: a + SY*b + SZ*c with padded strides chosen (by
+// exhaustive search over small paddings) so that the three pencil
+// orientations and the per-point accesses of a half-warp hit at most 2 banks
+// per 8-byte word, while every pencil access stays base + compile-time offset.
+template <int N>
+struct Lay;
+template <>
+struct Lay<2> { static constexpr int N = 2, N2 = 4, N3 = 8, SY = 2, SZ = 4, SIZE = 8; };
+template <>
+struct Lay<3> { static constexpr int N = 3, N2 = 9, N3 = 27, SY = 3, SZ = 12, SIZE = 36; };
+template <>
+struct Lay<4> { static constexpr int N = 4, N2 = 16, N3 = 64, SY = 4, SZ = 18, SIZE = 72; };
+template <>
+struct Lay<5> { static constexpr int N = 5, N2 = 25, N3 = 125, SY = 5, SZ = 25, SIZE = 125; };
+template <int N>
+__device__ __forceinline__ constexpr int lat(int a, int b, int c) {
+  return a + Lay<N>::SY * b + Lay<N>::SZ * c;
+}
+
+// Element coordinates and this thread's node for element e (< 2^31) with
+// precomputed-multiplier divisions (no 64-bit division in the hot loop).
+template <int P, typename A>
+__device__ __forceinline__ ElemPos elem_pos_fast(int64_t e64, const A& a, int i, int j, int k) {
+  const uint32_t e = (uint32_t)e64;
+  const uint32_t ek = a.fd_nxy.div(e);
+  const uint32_t r = e - ek * a.fd_nxy.d;
+  const uint32_t ej = a.fd_nx.div(r);
+  ElemPos p;
+  p.e = e64;
+  p.ei = (int)(r - ej * a.fd_nx.d);
+  p.ej = (int)ej;
+  p.ek = (int)ek;
+  p.ga = p.ei * P + i;
+  p.gb = p.ej * P + j;
+  p.gc = p.ek * P + k;
+  p.node = ((int64_t)p.gc * a.my + p.gb) * a.mx + p.ga;
+  return p;
+}
+
+template <int P>
+struct TileV2;
+template <>
+struct TileV2<1> { static constexpr int EPB = 16, MINB = 4; };
+template <>
+struct TileV2<2> { static constexpr int EPB = 4, MINB = 4; };
+template <>
+struct TileV2<3> { static constexpr int EPB = 2, MINB = 4; };
+template <>
+struct TileV2<4> { static constexpr int EPB = 1, MINB = 4; };
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_T(T* smem, const T* gmem) {
+  if constexpr (sizeof(T) == 8)
+    cp_async8(smem, gmem);
+  else
+    cp_async4(smem, gmem);
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
+}
+
+// ---- pencil sweeps ------------------------------------------------------------
+// Arguments are base pointers of consecutive per-element arrays of N3 values
+// (array t at base + t*N3) with Lay<N>::at addressing.  `w` is the worker
+// index inside the element (0 .. N3-1); a worker with w < 3*N2 owns
+// (component c, line l).  M[row*N + col] are compile-time-indexed tables.
+
+// Forward x-sweep: in[c] -> tB[c] = Bx in, tD[c] = Dx in.
+template <typename T, int N>
+__device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+    const int c = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
+    T u[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) u[a] = in[c * L::SIZE + lat<N>(a, j, k)];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      T sb = Bm[q * N] * u[0], sd = Dm[q * N] * u[0];
+#pragma unroll
+      for (int a = 1; a < N; ++a) {
+        sb += Bm[q * N + a] * u[a];
+        sd += Dm[q * N + a] * u[a];
+      }
+      tb[c * L::SIZE + lat<N>(q, j, k)] = sb;
+      td[c * L::SIZE + lat<N>(q, j, k)] = sd;
+    }
+  }
+}
+
+// Forward y-sweep: sBB = By tB, sBD = Dy tB, sDB = By tD.
+template <typename T, int N>
+__device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T* sdb,
+                                     const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+    const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
+    T ub[N], ud[N];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      ub[b] = tb[c * L::SIZE + lat<N>(i, b, k)];
+      ud[b] = td[c * L::SIZE + lat<N>(i, b, k)];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      T s1 = Bm[q * N] * ub[0], s2 = Dm[q * N] * ub[0], s3 = Bm[q * N] * ud[0];
+#pragma unroll
+      for (int b = 1; b < N; ++b) {
+        s1 += Bm[q * N + b] * ub[b];
+        s2 += Dm[q * N + b] * ub[b];
+        s3 += Bm[q * N + b] * ud[b];
+      }
+      sbb[c * L::SIZE + lat<N>(i, q, k)] = s1;
+      sbd[c * L::SIZE + lat<N>(i, q, k)] = s2;
+      sdb[c * L::SIZE + lat<N>(i, q, k)] = s3;
+    }
+  }
+}
+
+// Forward z-sweep: g[c][0] = Bz sDB, g[c][1] = Bz sBD, g[c][2] = Dz sBB.
+template <typename T, int N>
+__device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T* g, const T* Bm,
+                                     const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+    const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
+    T u0[N], u1[N], u2[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      u0[k] = sdb[c * L::SIZE + lat<N>(i, j, k)];
+      u1[k] = sbd[c * L::SIZE + lat<N>(i, j, k)];
+      u2[k] = sbb[c * L::SIZE + lat<N>(i, j, k)];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      T g0 = Bm[q * N] * u0[0], g1 = Bm[q * N] * u1[0], g2 = Dm[q * N] * u2[0];
+#pragma unroll
+      for (int k = 1; k < N; ++k) {
+        g0 += Bm[q * N + k] * u0[k];
+        g1 += Bm[q * N + k] * u1[k];
+        g2 += Dm[q * N + k] * u2[k];
+      }
+      g[(3 * c + 0) * L::SIZE + lat<N>(i, j, q)] = g0;
+      g[(3 * c + 1) * L::SIZE + lat<N>(i, j, q)] = g1;
+      g[(3 * c + 2) * L::SIZE + lat<N>(i, j, q)] = g2;
+    }
+  }
+}
+
+// Transposed z-sweep (node index along z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2.
+template <typename T, int N>
+__device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+    const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
+    T u0[N], u1[N], u2[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      u0[q] = wv[(3 * c + 0) * L::SIZE + lat<N>(i, j, q)];
+      u1[q] = wv[(3 * c + 1) * L::SIZE + lat<N>(i, j, q)];
+      u2[q] = wv[(3 * c + 2) * L::SIZE + lat<N>(i, j, q)];
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      T a0 = Bm[k] * u0[0], a1 = Bm[k] * u1[0], a2 = Dm[k] * u2[0];
+#pragma unroll
+      for (int q = 1; q < N; ++q) {
+        a0 += Bm[q * N + k] * u0[q];
+        a1 += Bm[q * N + k] * u1[q];
+        a2 += Dm[q * N + k] * u2[q];
+      }
+      av[(3 * c + 0) * L::SIZE + lat<N>(i, j, k)] = a0;
+      av[(3 * c + 1) * L::SIZE + lat<N>(i, j, k)] = a1;
+      av[(3 * c + 2) * L::SIZE + lat<N>(i, j, k)] = a2;
+    }
+  }
+}
+
+// Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
+template <typename T, int N>
+__device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+    const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
+    T u0[N], u1[N], u2[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      u0[q] = av[(3 * c + 0) * L::SIZE + lat<N>(i, q, k)];
+      u1[q] = av[(3 * c + 1) * L::SIZE + lat<N>(i, q, k)];
+      u2[q] = av[(3 * c + 2) * L::SIZE + lat<N>(i, q, k)];
+    }
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      T q0 = Bm[b] * u0[0], q12 = Dm[b] * u1[0] + Bm[b] * u2[0];
+#pragma unroll
+      for (int q = 1; q < N; ++q) {
+        q0 += Bm[q * N + b] * u0[q];
+        q12 += Dm[q * N + b] * u1[q] + Bm[q * N + b] * u2[q];
+      }
+      qv[(2 * c + 0) * L::SIZE + lat<N>(i, b, k)] = q0;
+      qv[(2 * c + 1) * L::SIZE + lat<N>(i, b, k)] = q12;
+    }
+  }
+}
+
+// Transposed x-sweep: out = Dx^T Q0 + Bx^T Q12, written as N contiguous
+// values of loc[(e*3 + c)*N3 + lexicographic m] (component-major).
+template <typename T, int N>
+__device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+    const int c = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
+    T u0[N], u1[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      u0[q] = qv[(2 * c + 0) * L::SIZE + lat<N>(q, j, k)];
+      u1[q] = qv[(2 * c + 1) * L::SIZE + lat<N>(q, j, k)];
+    }
+    T o[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      T s = Dm[a] * u0[0] + Bm[a] * u1[0];
+#pragma unroll
+      for (int q = 1; q < N; ++q) s += Dm[q * N + a] * u0[q] + Bm[q * N + a] * u1[q];
+      o[a] = s;
+    }
+    T* dst = loc_e + c * L::N3 + (k * N + j) * N;
+#pragma unroll
+    for (int a = 0; a < N; ++a) dst[a] = o[a];
+  }
+}
+
+// ---- the kernel -------------------------------------------------------------------
+template <typename T, int P, int MODEL, int STRAT>
+struct ApplyV2Smem {
+  static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
+  static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR);
+  static constexpr int NST = kUk ? 6 : 3;  // staged fields: x (3) [+ u_k (3)]
+  static constexpr int SZ = Lay<N>::SIZE;
+  T stage[2][EPB][NST][SZ];
+  T geo[2][EPB][10];
+  T r1[EPB][9][SZ];
+  T r2[EPB][9][SZ];
+};
+
+// fp64 kernels keep 3 CTAs/SM (<= 168 registers, no spills): measured faster
+// than 4 CTAs/SM with spills (profiles/r01_*: 0.195 vs 0.207 ms at cfg1).
+template <typename T, int P>
+constexpr int minb_v2() {
+  return sizeof(T) == 8 ? (TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB) : TileV2<P>::MINB;
+}
+
+template <typename T, int P, int MODEL, int STRAT>
+__global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P>()))
+    apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
+  using SM = ApplyV2Smem<T, P, MODEL, STRAT>;
+  constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
+  constexpr bool kUk = SM::kUk;
+  constexpr int SZ = Lay<N>::SIZE;
+  __shared__ __align__(16) SM sm;
+  const int tid = threadIdx.x;
+  const int el = tid / N3, q = tid % N3;
+  const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
+  const int qs = lat<N>(qi, qj, qk);  // padded slot of this thread's point
+  const int64_t stride = gridDim.x;
+
+  // issue the cp.async copies of group g into staging buffer b
+  auto prefetch = [&](int64_t g, int b) {
+    const int64_t e = g * EPB + el + a.e_begin;
+    if (e < a.nel) {
+      const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][c][qs], a.x + 3 * ep.node + c);
+      if constexpr (kUk) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][3 + c][qs], a.uk + 3 * ep.node + c);
+      }
+      if (a.affine && q < 10) cp_async_T(&sm.geo[b][el][q], a.geo + q * a.geo_stride + e);
+    }
+    cp_async_commit();
+  };
+
+  int64_t g = blockIdx.x;
+  int buf = 0;
+  if (g < ngroups) prefetch(g, 0);
+  for (; g < ngroups; g += stride, buf ^= 1) {
+    const bool more = g + stride < ngroups;
+    if (more)
+      prefetch(g + stride, buf ^ 1);
+    else
+      cp_async_commit();
+    cp_async_wait<1>();
+    const int64_t e = g * EPB + el + a.e_begin;
+    const bool valid = e < a.nel;
+    const ElemPos ep = elem_pos_fast<P>(valid ? e : a.e_begin, a, qi, qj, qk);
+    // Dirichlet columns are masked (operator.hpp:604-605); zero the stale
+    // staging values of padding elements.
+    if (!valid || node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces)) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) sm.stage[buf][el][c][qs] = T(0);
+    }
+    // per-qp geometry / cache loads are issued before the sweeps
+    const int64_t qidx = (valid ? e : a.e_begin) * N3 + q;
+    T j0inv[9], detw;
+    if (!a.affine) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];
+      detw = a.geo[9 * a.geo_stride + qidx];
+    }
+    __syncthreads();
+
+    T* const R1 = &sm.r1[el][0][0];  // 9 arrays of SZ, contiguous
+    T* const R2 = &sm.r2[el][0][0];
+    // ---- gradient of x at the qps
+    fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, a.Dm, q);
+    __syncthreads();
+    fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, a.Dm, q);
+    __syncthreads();
+    fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, a.Dm, q);
+    __syncthreads();
+    T gx[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
+    if (a.affine) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) j0inv[m] = sm.geo[buf][el][m];
+      detw = sm.geo[buf][el][9] * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+    }
+    Bundle<T> cb;
+    const T* cs = a.cache;
+    const int64_t st = a.cache_stride;
+    if constexpr (kUk) {
+      __syncthreads();
+      fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, a.Dm, q);
+      __syncthreads();
+      fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, a.Dm, q);
+      __syncthreads();
+      fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, a.Dm, q);
+      __syncthreads();
+      T gk[9], gg[9];
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+      mm(gk, j0inv, gg);
+      if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
+      if constexpr (STRAT == S_NONE) {
+        cache_scalars<T, MODEL>(a.mat, cb);
+      } else {
+        if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
+        else {
+          cb.jp = cs[C_JP * st + qidx];
+          cb.c1 = cs[C_C1 * st + qidx];
+          cb.c2 = cs[C_C2 * st + qidx];
+        }
+        if (MODEL == FIBER) {
+          cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
+          cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
+          cb.efib[0] = cs[(C_EF + 0) * st + qidx];
+          cb.efib[1] = cs[(C_EF + 1) * st + qidx];
+        }
+      }
+      second_pk<T, MODEL>(a.mat, cb);
+    } else if constexpr (STRAT == S_CACHEDF) {
+      T gg[9];
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gg[m] = cs[(C_G + m) * st + qidx];
+      if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
+      cache_scalars<T, MODEL>(a.mat, cb);
+      second_pk<T, MODEL>(a.mat, cb);
+    } else {  // S_TENSOR
+      if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
+      else {
+        cb.jp = cs[C_JP * st + qidx];
+        cb.c1 = cs[C_C1 * st + qidx];
+        cb.c2 = cs[C_C2 * st + qidx];
+      }
+      if (MODEL == FIBER) {
+        cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
+        cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
+        cb.efib[0] = cs[(C_EF + 0) * st + qidx];
+        cb.efib[1] = cs[(C_EF + 1) * st + qidx];
+      }
+#pragma unroll
+      for (int m = 0; m < 9; ++m) {
+        cb.F[m] = cs[(C_F + m) * st + qidx];
+        cb.Finv[m] = cs[(C_FINV + m) * st + qidx];
+      }
+#pragma unroll
+      for (int m = 0; m < 6; ++m) {
+        cb.S[m] = cs[(C_S + m) * st + qidx];
+        cb.Cinv[m] = cs[(C_CINV + m) * st + qidx];
+      }
+    }
+    T wv[9];
+    tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, wv);
+    // ---- test with the gradients of the basis functions
+#pragma unroll
+    for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];
+    __syncthreads();
+    tr_z<T, N>(R1, R2, a.Bm, a.Dm, q);
+    __syncthreads();
+    tr_y<T, N>(R2, R1, a.Bm, a.Dm, q);
+    __syncthreads();
+    if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, a.Bm, a.Dm, q);
+    __syncthreads();  // staging buffer `buf` and r1/r2 are reused next
+  }
+}
+
+}  // namespace emfgpu

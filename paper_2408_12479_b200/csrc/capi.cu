@@ -212,6 +212,8 @@ KArgs<T> kargs(const emfgpu_op* op) {
     a.Dd[t] = L->D[t];
   }
   for (int t = 0; t < n; ++t) a.qwd[t] = L->qwts[t];
+  a.fd_nx = FastDiv::make((uint32_t)L->nx);
+  a.fd_nxy = FastDiv::make((uint32_t)(L->nx * L->ny));
   return a;
 }
 
@@ -550,6 +552,13 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_err);
   if (op->h_err) cudaFreeHost(op->h_err);
   if (op->stream) cudaStreamDestroy(op->stream);
+  if (op->s_h2d) cudaStreamDestroy(op->s_h2d);
+  if (op->s_d2h) cudaStreamDestroy(op->s_d2h);
+  if (op->ev_start) cudaEventDestroy(op->ev_start);
+  for (int i = 0; i < emfgpu_op::kMaxChunks; ++i) {
+    if (op->ev_h2d[i]) cudaEventDestroy(op->ev_h2d[i]);
+    if (op->ev_comp[i]) cudaEventDestroy(op->ev_comp[i]);
+  }
   delete op;
 }
 
@@ -609,6 +618,66 @@ emfgpu_status emfgpu_op_apply(emfgpu_op* op, const void* d_x, void* d_y, void* s
   });
 }
 
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Host-vector apply.  With page-locked x and y the lattice is cut into z
+// chunks of element layers and three streams overlap (i) H2D of the next
+// chunk's node planes, (ii) the element + node phases of the current chunk,
+// (iii) D2H of the node planes the previous chunks finalised.  PCIe copies run
+// on both copy engines concurrently; the result is bitwise the one-shot apply.
+static void apply_host_pipelined(emfgpu_op* op, const void* x, void* y) {
+  const emfgpu_level* L = op->L;
+  const size_t plane = nsize(op) * 3 * (size_t)L->mx * L->my;
+  const char* hx = static_cast<const char*>(x);
+  char* hy = static_cast<char*>(y);
+  char* dx = static_cast<char*>(op->d_x);
+  char* dy = static_cast<char*>(op->d_y);
+  if (!op->s_h2d) {
+    CK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&op->ev_start, cudaEventDisableTiming));
+    for (int i = 0; i < emfgpu_op::kMaxChunks; ++i) {
+      CK(cudaEventCreateWithFlags(&op->ev_h2d[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&op->ev_comp[i], cudaEventDisableTiming));
+    }
+  }
+  const int nch = std::min(emfgpu_op::kMaxChunks, std::max(1, L->nz / 4));
+  const int per = (L->nz + nch - 1) / nch;
+  CK(cudaEventRecord(op->ev_start, op->stream));
+  CK(cudaStreamWaitEvent(op->s_h2d, op->ev_start, 0));
+  int done_hi = -1;  // highest node plane copied in so far
+  for (int i = 0; i < nch; ++i) {
+    const int k1 = std::min(L->nz, (i + 1) * per);
+    const int hi = k1 * L->p;
+    if (hi > done_hi) {
+      CK(cudaMemcpyAsync(dx + (done_hi + 1) * plane, hx + (done_hi + 1) * plane, (hi - done_hi) * plane,
+                         cudaMemcpyHostToDevice, op->s_h2d));
+      done_hi = hi;
+    }
+    CK(cudaEventRecord(op->ev_h2d[i], op->s_h2d));
+  }
+  for (int i = 0; i < nch; ++i) {
+    const int k0 = i * per, k1 = std::min(L->nz, (i + 1) * per);
+    if (k0 >= k1) break;
+    const int c0 = k0 * L->p, c1 = (k1 == L->nz) ? L->mz - 1 : k1 * L->p - 1;
+    CK(cudaStreamWaitEvent(op->stream, op->ev_h2d[i], 0));
+    apply_elements(op, op->d_x, k0, k1, op->stream);
+    apply_nodes(op, op->d_x, op->d_y, c0, c1, nullptr, nullptr, 0, op->stream);
+    CK(cudaEventRecord(op->ev_comp[i], op->stream));
+    CK(cudaStreamWaitEvent(op->s_d2h, op->ev_comp[i], 0));
+    CK(cudaMemcpyAsync(hy + c0 * plane, dy + c0 * plane, (c1 - c0 + 1) * plane, cudaMemcpyDeviceToHost,
+                       op->s_d2h));
+  }
+  CK(cudaStreamSynchronize(op->s_d2h));
+}
+
 emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y) {
   if (!op || !x || !y) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
@@ -617,10 +686,14 @@ emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y) {
     const size_t bytes = nsize(op) * op->L->ndofs;
     if (!op->d_x) CK(cudaMalloc(&op->d_x, bytes));
     if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
-    CK(cudaMemcpyAsync(op->d_x, x, bytes, cudaMemcpyHostToDevice, op->stream));
-    apply_elements(op, op->d_x, 0, op->L->nz, op->stream);
-    apply_nodes(op, op->d_x, op->d_y, 0, op->L->mz - 1, nullptr, nullptr, 0, op->stream);
-    CK(cudaMemcpyAsync(y, op->d_y, bytes, cudaMemcpyDeviceToHost, op->stream));
+    if (op->L->nz >= 8 && is_pinned(x) && is_pinned(y)) {
+      apply_host_pipelined(op, x, y);
+    } else {
+      CK(cudaMemcpyAsync(op->d_x, x, bytes, cudaMemcpyHostToDevice, op->stream));
+      apply_elements(op, op->d_x, 0, op->L->nz, op->stream);
+      apply_nodes(op, op->d_x, op->d_y, 0, op->L->mz - 1, nullptr, nullptr, 0, op->stream);
+      CK(cudaMemcpyAsync(y, op->d_y, bytes, cudaMemcpyDeviceToHost, op->stream));
+    }
     check_err(op, op->stream, nullptr, nullptr, "apply_tangent");
   });
 }

@@ -80,16 +80,21 @@ __global__ void node_gather_kernel(const T* __restrict__ loc, const T* __restric
     for (int tj = 0; tj < nj; ++tj)
       for (int ti = 0; ti < ni; ++ti) {
         int64_t off;
+        T v0, v1, v2;
         if (k < 0 || k >= nz) {
           src = k < 0 ? ghost_lo : ghost_hi;
           if (!src) continue;
           off = ((((int64_t)je[tj] * nx + ie[ti]) * N2) + jl[tj] * N + il[ti]) * 3;
-        } else {
-          src = loc;
+          v0 = src[off];
+          v1 = src[off + 1];
+          v2 = src[off + 2];
+        } else {  // element-local results, component-major loc[(e*3 + c)*N3 + m]
           const int64_t e = ((int64_t)k * ny + je[tj]) * nx + ie[ti];
-          off = (e * N3 + (kl[tk] * N + jl[tj]) * N + il[ti]) * 3;
+          off = e * 3 * N3 + (kl[tk] * N + jl[tj]) * N + il[ti];
+          v0 = loc[off];
+          v1 = loc[off + N3];
+          v2 = loc[off + 2 * N3];
         }
-        const T v0 = src[off], v1 = src[off + 1], v2 = src[off + 2];
         if (first) {
           s0 = v0;
           s1 = v1;
@@ -119,7 +124,8 @@ void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, cons
 }
 
 // Face of element layer k: lower (side 0, local c=0) or upper (side 1, c=p)
-// node plane of each element's local results, ((j*nx+i)*N2 + b*N + a)*3 + comp.
+// node plane of each element's local results (read from the component-major
+// loc[(e*3 + c)*N3 + m]), packed as ((j*nx+i)*N2 + b*N + a)*3 + comp.
 template <typename T>
 __global__ void pack_face_kernel(const T* __restrict__ loc, T* __restrict__ face, int nx, int ny, int p, int k,
                                  int side) {
@@ -133,7 +139,7 @@ __global__ void pack_face_kernel(const T* __restrict__ loc, T* __restrict__ face
   const int64_t ij = fn / N2;
   const int64_t e = (int64_t)k * nx * ny + ij;
   const int lc = side ? p : 0;
-  face[idx] = loc[(e * N3 + lc * N2 + m2) * 3 + comp];
+  face[idx] = loc[(e * 3 + comp) * N3 + lc * N2 + m2];
 }
 
 template <typename T>

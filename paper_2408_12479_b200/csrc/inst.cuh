@@ -1,20 +1,33 @@
 // Explicit instantiation of the element kernels for one (Number, degree).
 // Included by inst_<t><p>.cu with EMF_T and EMF_P defined, so the 8 units
 // compile in parallel.
+#include <algorithm>
+
+#include "apply_v2.cuh"
 #include "internal.h"
 
 namespace emfgpu {
 
 template <int MODEL, int STRAT>
 static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
-  constexpr int N = EMF_P + 1, EPB = Tile<EMF_P>::EPB;
+  constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P>::EPB, THREADS = EPB * N * N * N;
   const int64_t cnt = e1 - e0;
   if (cnt <= 0) return;
+  // persistent grid: one wave at the kernel's occupancy
+  static int per_sm = 0, sms = 0;
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT>, THREADS, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
   KArgs<EMF_T> b = a;
   b.e_begin = e0;
   b.nel = e1;
-  const int64_t blocks = (cnt + EPB - 1) / EPB;
-  apply_kernel<EMF_T, EMF_P, MODEL, STRAT><<<(unsigned)blocks, EPB * N * N * N, 0, s>>>(b);
+  const int64_t groups = (cnt + EPB - 1) / EPB;
+  const int64_t grid = std::min<int64_t>(groups, (int64_t)sms * per_sm);
+  apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT><<<(unsigned)grid, THREADS, 0, s>>>(b, groups);
 }
 
 template <>

@@ -96,6 +96,10 @@ struct emfgpu_op {
   unsigned long long* d_err = nullptr;
   unsigned long long* h_err = nullptr;  // pinned
   cudaStream_t stream = nullptr;
+  // pipelined host-vector apply: copy streams + per-chunk events
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  static constexpr int kMaxChunks = 16;
+  cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr;
   bool linearized = false;
   uint64_t checksum = 0;
   std::string last_error;

@@ -45,10 +45,32 @@ enum CacheSlot : int {
   C_G = 0, C_NG = 9
 };
 
+// n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method,
+// Hacker's Delight 10-9): q = (umulhi(n, m) + n) >> l.
+struct FastDiv {
+  uint32_t d, m;
+  int l;
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#ifdef __CUDA_ARCH__
+    return (__umulhi(n, m) + n) >> l;
+#else
+    return (uint32_t)((((uint64_t)n * m) >> 32) + n) >> l;
+#endif
+  }
+  static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.l = 0;
+    while ((1ull << f.l) < d) ++f.l;
+    f.m = (uint32_t)(((1ull << 32) * ((1ull << f.l) - d)) / d + 1);
+    return f;
+  }
+};
+
 template <typename T>
 struct KArgs {
   const T* x;          // input vector (3 per node), apply / unused by diag
-  T* loc;              // element-local output, (e*nn3 + m)*3 + c
+  T* loc;              // element-local output, component-major (e*3 + c)*nn3 + m
   const T* uk;         // linearization point in T (none/scalar), 3 per node
   const double* ukd;   // linearization point in double (linearize only)
   const T* geo;        // J0^-1 (9) + detw (1), SoA with stride geo_stride
@@ -68,6 +90,7 @@ struct KArgs {
   T Bm[81], Dm[81];
   double Bd[81], Dd[81];
   double qwd[9];  // 1D Gauss weights (affine geometry stores det J0 without them)
+  FastDiv fd_nx, fd_nxy;
 };
 
 __device__ __forceinline__ bool node_constrained(int a, int b, int c, int mx, int my, int mz, int faces) {
@@ -259,114 +282,7 @@ __device__ __forceinline__ void load_geo(const A& a, const T* geo, bool valid, i
   if (a.affine) detw = detw * T(a.qwd[i] * a.qwd[j] * a.qwd[k]);
 }
 
-// ---- apply kernel ---------------------------------------------------------------
-template <typename T, int P, int MODEL, int STRAT>
-__global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
-    apply_kernel(const KArgs<T> a) {
-  constexpr int N = P + 1, N3 = N * N * N, EPB = Tile<P>::EPB;
-  __shared__ T sB[N * N], sD[N * N];
-  __shared__ T bufA[EPB][9][N3], bufB[EPB][9][N3];
-  const int tid = threadIdx.x;
-  const int el = tid / N3, q = tid % N3;
-  const int i = q % N, j = (q / N) % N, k = q / (N * N);
-  if (tid < N * N) {
-    sB[tid] = a.Bm[tid];
-    sD[tid] = a.Dm[tid];
-  }
-  const int64_t e = (int64_t)blockIdx.x * EPB + el + a.e_begin;
-  const bool valid = e < a.nel;
-  const ElemPos ep = elem_pos<P>(valid ? e : a.e_begin, a.nx, a.ny, a.mx, a.my, i, j, k);
-  const bool fixed = node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
-  // gather input (Dirichlet columns masked, operator.hpp:604-605)
-#pragma unroll
-  for (int c = 0; c < 3; ++c) bufA[el][c][q] = (valid && !fixed) ? a.x[3 * ep.node + c] : T(0);
-  __syncthreads();
-  T gx[9];
-  sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gx);
-
-  Bundle<T> cb;
-  const int64_t qidx = e * N3 + q;
-  if (STRAT == S_NONE || STRAT == S_SCALAR) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.uk[3 * ep.node + c] : T(0);
-    __syncthreads();
-    T gk[9];
-    sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
-    T j0inv[9], detw, g[9];
-    load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
-    mm(gk, j0inv, g);
-    const bool ok = make_strain(g, cb);
-    if (!ok && valid) atomicMin(a.err, (unsigned long long)qidx);
-    if (STRAT == S_NONE) {
-      cache_scalars<T, MODEL>(a.mat, cb);
-    } else {
-      const T* cs = a.cache;
-      const int64_t st = a.cache_stride, ix = valid ? qidx : 0;
-      if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + ix];
-      else {
-        cb.jp = cs[C_JP * st + ix];
-        cb.c1 = cs[C_C1 * st + ix];
-        cb.c2 = cs[C_C2 * st + ix];
-      }
-      if (MODEL == FIBER) {
-        cb.c3[0] = cs[(C_C3 + 0) * st + ix];
-        cb.c3[1] = cs[(C_C3 + 1) * st + ix];
-        cb.efib[0] = cs[(C_EF + 0) * st + ix];
-        cb.efib[1] = cs[(C_EF + 1) * st + ix];
-      }
-    }
-    second_pk<T, MODEL>(a.mat, cb);
-    T w[9], out[3];
-    tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, w);
-    sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
-    if (valid)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) a.loc[qidx * 3 + c] = out[c];
-    return;
-  }
-  T j0inv[9], detw;
-  load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
-  const T* cs = a.cache;
-  const int64_t st = a.cache_stride, ix = valid ? qidx : 0;
-  if (STRAT == S_CACHEDF) {
-    T g[9];
-#pragma unroll
-    for (int m = 0; m < 9; ++m) g[m] = cs[(C_G + m) * st + ix];
-    const bool ok = make_strain(g, cb);
-    if (!ok && valid) atomicMin(a.err, (unsigned long long)qidx);
-    cache_scalars<T, MODEL>(a.mat, cb);
-    second_pk<T, MODEL>(a.mat, cb);
-  } else {  // S_TENSOR
-    if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + ix];
-    else {
-      cb.jp = cs[C_JP * st + ix];
-      cb.c1 = cs[C_C1 * st + ix];
-      cb.c2 = cs[C_C2 * st + ix];
-    }
-    if (MODEL == FIBER) {
-      cb.c3[0] = cs[(C_C3 + 0) * st + ix];
-      cb.c3[1] = cs[(C_C3 + 1) * st + ix];
-      cb.efib[0] = cs[(C_EF + 0) * st + ix];
-      cb.efib[1] = cs[(C_EF + 1) * st + ix];
-    }
-#pragma unroll
-    for (int m = 0; m < 9; ++m) {
-      cb.F[m] = cs[(C_F + m) * st + ix];
-      cb.Finv[m] = cs[(C_FINV + m) * st + ix];
-    }
-#pragma unroll
-    for (int m = 0; m < 6; ++m) {
-      cb.S[m] = cs[(C_S + m) * st + ix];
-      cb.Cinv[m] = cs[(C_CINV + m) * st + ix];
-    }
-  }
-  T w[9], out[3];
-  tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, w);
-  sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
-  if (valid)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) a.loc[qidx * 3 + c] = out[c];
-}
+// The apply kernel itself is apply_v2.cuh:apply_v2_kernel.
 
 // ---- linearization kernel (double compute, T store), operator.hpp:643-770 ------
 template <typename T, int P, int MODEL>
@@ -584,7 +500,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   }
   if (valid)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.loc[qidx * 3 + c] = out[c];
+    for (int c = 0; c < 3; ++c) a.loc[(e * 3 + c) * N3 + q] = out[c];
 }
 
 }  // namespace emfgpu

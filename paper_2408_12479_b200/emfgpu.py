@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libemfgpu.so")
+LIB_PATH = os.environ.get("EMFGPU_LIB") or os.path.join(HERE, "lib", "libemfgpu.so")
 
 MODELS = {"cnh": 0, "inh": 1, "fiber": 2}
 STRATEGIES = {"none": 0, "scalar": 1, "tensor": 2, "cachedF": 3}
