@@ -65,7 +65,10 @@ typedef struct emfgpu_level_desc {
   int dirichlet_faces;   /* bit mask, clamped to zero */
   int device;            /* CUDA device ordinal */
   int z_offset;          /* global index of element layer 0 (z slabs; colour parity) */
+  int flags;             /* EMFGPU_LEVEL_* bits: disable geometry fast paths (testing) */
 } emfgpu_level_desc;
+#define EMFGPU_LEVEL_NO_CARTESIAN 1 /* use the general J0^-1 products even if J0 is diagonal */
+#define EMFGPU_LEVEL_NO_AFFINE 2    /* store geometry per quadrature point even if affine */
 
 /* MaterialParams, material.hpp:36-50 (phi in radians; e1,e2,e3 frame). */
 typedef struct emfgpu_material {
@@ -88,6 +91,7 @@ void emfgpu_level_destroy(emfgpu_level* l);
 int64_t emfgpu_level_n_dofs(const emfgpu_level* l);          /* FeLevel::dof_count */
 int64_t emfgpu_level_n_elements(const emfgpu_level* l);
 int emfgpu_level_affine(const emfgpu_level* l);              /* 1: geometry stored per element */
+int emfgpu_level_cartesian(const emfgpu_level* l);           /* 1: affine, J0 diagonal (axis-aligned) fast path */
 /* Reference->material Jacobians J0 (9 per qp, element-major, row = comp),
  * FeLevel::jacobians (mesh.hpp:97-99). host_out holds nel*(p+1)^3*9. */
 emfgpu_status emfgpu_level_jacobians(const emfgpu_level* l, double* host_out);

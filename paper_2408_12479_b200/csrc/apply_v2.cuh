@@ -264,7 +264,7 @@ __device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T
 }
 
 // ---- the kernel -------------------------------------------------------------------
-template <typename T, int P, int MODEL, int STRAT>
+template <typename T, int P, int MODEL, int STRAT, bool CART>
 struct ApplyV2Smem {
   static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
   static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR);
@@ -283,16 +283,35 @@ constexpr int minb_v2() {
   return sizeof(T) == 8 ? (TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB) : TileV2<P>::MINB;
 }
 
-template <typename T, int P, int MODEL, int STRAT>
+template <typename T, int P, int MODEL, int STRAT, bool CART>
 __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P>()))
     apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
-  using SM = ApplyV2Smem<T, P, MODEL, STRAT>;
+  using SM = ApplyV2Smem<T, P, MODEL, STRAT, CART>;
+  // CART: affine elements with a diagonal J0^-1 (axis-aligned boxes): the
+  // geometry factors reduce to 3 scalings per direction.
+  const T* const Dfx = a.Dm;
+  const T* const Dfy = a.Dm;
+  const T* const Dfz = a.Dm;
+  const T* const Btx = a.Bm;
+  const T* const Dtx = a.Dm;
+  const T* const Bty = a.Bm;
+  const T* const Dty = a.Dm;
+  const T* const Btz = a.Bm;
+  const T* const Dtz = a.Dm;
   constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
   constexpr bool kUk = SM::kUk;
   constexpr int SZ = Lay<N>::SIZE;
   __shared__ __align__(16) SM sm;
   const int tid = threadIdx.x;
   const int el = tid / N3, q = tid % N3;
+  // Elements of a CTA only share data through their own slices, so when an
+  // element spans whole warps it synchronises on its own named barrier.
+  auto esync = [&]() {
+    if constexpr (N3 % 32 == 0 && EPB > 1)
+      asm volatile("bar.sync %0, %1;\n" ::"r"(el + 1), "n"(N3) : "memory");
+    else
+      __syncthreads();
+  };
   const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
   const int qs = lat<N>(qi, qj, qk);  // padded slot of this thread's point
   const int64_t stride = gridDim.x;
@@ -335,26 +354,31 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     // per-qp geometry / cache loads are issued before the sweeps
     const int64_t qidx = (valid ? e : a.e_begin) * N3 + q;
     T j0inv[9], detw;
-    if (!a.affine) {
+    if (!CART && !a.affine) {
 #pragma unroll
       for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];
       detw = a.geo[9 * a.geo_stride + qidx];
     }
-    __syncthreads();
+    esync();
 
     T* const R1 = &sm.r1[el][0][0];  // 9 arrays of SZ, contiguous
     T* const R2 = &sm.r2[el][0][0];
     // ---- gradient of x at the qps
-    fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, a.Dm, q);
-    __syncthreads();
-    fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, a.Dm, q);
-    __syncthreads();
-    fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, a.Dm, q);
-    __syncthreads();
+    fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+    esync();
+    fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+    esync();
+    fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+    esync();
     T gx[9];
 #pragma unroll
     for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
-    if (a.affine) {
+    if (CART) {  // diagonal J0^-1 (entries 0, 4, 8)
+      j0inv[0] = sm.geo[buf][el][0];
+      j0inv[4] = sm.geo[buf][el][4];
+      j0inv[8] = sm.geo[buf][el][8];
+      detw = sm.geo[buf][el][9] * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+    } else if (a.affine) {
 #pragma unroll
       for (int m = 0; m < 9; ++m) j0inv[m] = sm.geo[buf][el][m];
       detw = sm.geo[buf][el][9] * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
@@ -363,17 +387,22 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     const T* cs = a.cache;
     const int64_t st = a.cache_stride;
     if constexpr (kUk) {
-      __syncthreads();
-      fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, a.Dm, q);
-      __syncthreads();
-      fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, a.Dm, q);
-      __syncthreads();
-      fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, a.Dm, q);
-      __syncthreads();
+      esync();
+      fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+      esync();
+      fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+      esync();
+      fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+      esync();
       T gk[9], gg[9];
 #pragma unroll
       for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
-      mm(gk, j0inv, gg);
+      if constexpr (CART) {
+#pragma unroll
+        for (int m = 0; m < 9; ++m) gg[m] = gk[m] * j0inv[4 * (m % 3)];
+      } else {
+        mm(gk, j0inv, gg);
+      }
       if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
       if constexpr (STRAT == S_NONE) {
         cache_scalars<T, MODEL>(a.mat, cb);
@@ -424,17 +453,30 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       }
     }
     T wv[9];
-    tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, wv);
+    if constexpr (CART) {
+      T dg[9], wm[9];
+#pragma unroll
+      for (int m = 0; m < 9; ++m) dg[m] = gx[m] * j0inv[4 * (m % 3)];
+      tangent_wm<T, MODEL>(a.mat, cb, dg, wm);
+      const T s0 = detw * j0inv[0], s1 = detw * j0inv[4], s2 = detw * j0inv[8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        wv[3 * c + 0] = wm[3 * c + 0] * s0;
+        wv[3 * c + 1] = wm[3 * c + 1] * s1;
+        wv[3 * c + 2] = wm[3 * c + 2] * s2;
+      }
+    } else
+      tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, wv);
     // ---- test with the gradients of the basis functions
 #pragma unroll
     for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];
-    __syncthreads();
-    tr_z<T, N>(R1, R2, a.Bm, a.Dm, q);
-    __syncthreads();
-    tr_y<T, N>(R2, R1, a.Bm, a.Dm, q);
-    __syncthreads();
-    if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, a.Bm, a.Dm, q);
-    __syncthreads();  // staging buffer `buf` and r1/r2 are reused next
+    esync();
+    tr_z<T, N>(R1, R2, Btz, Dtz, q);
+    esync();
+    tr_y<T, N>(R2, R1, Bty, Dty, q);
+    esync();
+    if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
+    esync();  // staging buffer `buf` and r1/r2 are reused next
   }
 }
 

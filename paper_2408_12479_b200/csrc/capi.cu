@@ -212,6 +212,7 @@ KArgs<T> kargs(const emfgpu_op* op) {
     a.Dd[t] = L->D[t];
   }
   for (int t = 0; t < n; ++t) a.qwd[t] = L->qwts[t];
+  a.cartesian = L->cartesian;
   a.fd_nx = FastDiv::make((uint32_t)L->nx);
   a.fd_nxy = FastDiv::make((uint32_t)(L->nx * L->ny));
   return a;
@@ -416,7 +417,7 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
       cudaFree(geo_q);
       throw ApiError(EMFGPU_ERR_NUMERICAL, "level: mapping Jacobian not positive at a quadrature point");
     }
-    L->affine = hf[0] ? 0 : 1;
+    L->affine = (hf[0] || (d->flags & EMFGPU_LEVEL_NO_AFFINE)) ? 0 : 1;
     if (L->affine) {
       CK(cudaMalloc(&L->d_geo, sizeof(double) * L->nel * 10));
       launch_geo_compact(geo_q, L->d_geo, L->nel, (int)L->nq3, 0);
@@ -424,6 +425,16 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
       CK(cudaDeviceSynchronize());
       cudaFree(geo_q);
       L->geo_stride = L->nel;
+      // axis-aligned affine elements: J0^-1 diagonal in every element
+      std::vector<double> h(10 * L->nel);
+      CK(cudaMemcpy(h.data(), L->d_geo, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+      bool cart = !(d->flags & EMFGPU_LEVEL_NO_CARTESIAN);
+      for (int64_t e = 0; e < L->nel && cart; ++e) {
+        const double sc = std::max(std::abs(h[e]), std::max(std::abs(h[4 * L->nel + e]), std::abs(h[8 * L->nel + e])));
+        for (int m : {1, 2, 3, 5, 6, 7})
+          if (std::abs(h[m * L->nel + e]) > 1e-11 * sc) cart = false;
+      }
+      L->cartesian = cart ? 1 : 0;
     } else {
       L->d_geo = geo_q;  // fields 0..9 used, stride nqp
       L->geo_stride = nqp;
@@ -455,6 +466,7 @@ void emfgpu_level_destroy(emfgpu_level* l) {
 int64_t emfgpu_level_n_dofs(const emfgpu_level* l) { return l ? l->ndofs : 0; }
 int64_t emfgpu_level_n_elements(const emfgpu_level* l) { return l ? l->nel : 0; }
 int emfgpu_level_affine(const emfgpu_level* l) { return l ? l->affine : 0; }
+int emfgpu_level_cartesian(const emfgpu_level* l) { return l ? l->cartesian : 0; }
 const char* emfgpu_level_last_error(const emfgpu_level* l) { return l ? l->last_error.c_str() : ""; }
 
 emfgpu_status emfgpu_level_jacobians(const emfgpu_level* l, double* host_out) {

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1)) geom
     scale = fmax(scale, fabs(j0q0[el][m]));
     dev = fmax(dev, fabs(J[m] - j0q0[el][m]));
   }
-  if (dev > 1e-13 * scale) atomicExch(a.nonaffine, 1);
+  if (dev > 1e-11 * scale) atomicExch(a.nonaffine, 1);  // GLL-sweep rounding reaches ~1e-13
 #pragma unroll
   for (int m = 0; m < 9; ++m) a.geo[m * a.stride + qi] = inv[m];
   a.geo[9 * a.stride + qi] = det * ((a.qw[i] * a.qw[j]) * a.qw[k]);

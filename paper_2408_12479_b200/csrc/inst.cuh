@@ -8,7 +8,7 @@
 
 namespace emfgpu {
 
-template <int MODEL, int STRAT>
+template <int MODEL, int STRAT, bool CART>
 static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
   constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P>::EPB, THREADS = EPB * N * N * N;
   const int64_t cnt = e1 - e0;
@@ -19,7 +19,7 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT>, THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>, THREADS, 0);
     if (per_sm < 1) per_sm = 1;
   }
   KArgs<EMF_T> b = a;
@@ -27,14 +27,17 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   b.nel = e1;
   const int64_t groups = (cnt + EPB - 1) / EPB;
   const int64_t grid = std::min<int64_t>(groups, (int64_t)sms * per_sm);
-  apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT><<<(unsigned)grid, THREADS, 0, s>>>(b, groups);
+  apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART><<<(unsigned)grid, THREADS, 0, s>>>(b, groups);
 }
 
 template <>
 void launch_apply<EMF_T, EMF_P>(int model, int strategy, const KArgs<EMF_T>& a, int64_t e0, int64_t e1,
                                cudaStream_t s) {
-#define EMF_CASE(M, S) \
-  if (model == M && strategy == S) return apply_one<M, S>(a, e0, e1, s);
+#define EMF_CASE(M, S)                                                  \
+  if (model == M && strategy == S) {                                    \
+    if (a.cartesian) return apply_one<M, S, true>(a, e0, e1, s);        \
+    return apply_one<M, S, false>(a, e0, e1, s);                        \
+  }
   EMF_CASE(CNH, S_NONE) EMF_CASE(CNH, S_SCALAR) EMF_CASE(CNH, S_TENSOR) EMF_CASE(CNH, S_CACHEDF)
   EMF_CASE(INH, S_NONE) EMF_CASE(INH, S_SCALAR) EMF_CASE(INH, S_TENSOR) EMF_CASE(INH, S_CACHEDF)
   EMF_CASE(FIBER, S_NONE) EMF_CASE(FIBER, S_SCALAR) EMF_CASE(FIBER, S_TENSOR) EMF_CASE(FIBER, S_CACHEDF)

@@ -68,7 +68,7 @@ void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st
 struct emfgpu_level {
   int nx = 0, ny = 0, nz = 0, p = 0, mx = 0, my = 0, mz = 0;
   int64_t nnodes = 0, ndofs = 0, nel = 0, nq3 = 0;
-  int faces = 0, device = 0, affine = 0, z_offset = 0;
+  int faces = 0, device = 0, affine = 0, z_offset = 0, cartesian = 0;
   double extent[3] = {1, 1, 1};
   // basis tables (host): GLL nodes, Gauss points/weights, B/D (row = qp)
   std::vector<double> nodes, qpts, qwts, B, D;

@@ -77,6 +77,7 @@ struct KArgs {
   const double* geod;  // same, double (linearize)
   int64_t geo_stride;
   int affine;          // geometry per element instead of per qp
+  int cartesian;       // affine with diagonal J0 in every element (axis-aligned boxes)
   T* cache;            // SoA fields
   int64_t cache_stride;
   int strategy;        // runtime strategy for linearize/diagonal
@@ -87,8 +88,8 @@ struct KArgs {
   unsigned long long* err;  // first failing e*nq3+q (atomicMin)
   MatConst<T> mat;
   MatConst<double> matd;
-  T Bm[81], Dm[81];
-  double Bd[81], Dd[81];
+  T Bm[25], Dm[25];    // 1D tables, row = quadrature point (P <= 4)
+  double Bd[25], Dd[25];
   double qwd[9];  // 1D Gauss weights (affine geometry stores det J0 without them)
   FastDiv fd_nx, fd_nxy;
 };

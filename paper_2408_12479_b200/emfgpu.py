@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("EMFGPU_LIB") or os.path.join(HERE, "lib", "libemfgpu.
 MODELS = {"cnh": 0, "inh": 1, "fiber": 2}
 STRATEGIES = {"none": 0, "scalar": 1, "tensor": 2, "cachedF": 3}
 MAPS = {"reference": 0, "shear_x": 1, "coords": 2}
+NO_CARTESIAN, NO_AFFINE = 1, 2
 STATUS = {0: "OK", 1: "ERR_CONFIG", 2: "ERR_NUMERICAL", 3: "ERR_IO", 4: "ERR_INVALID", 5: "ERR_STALE",
           6: "ERR_CUDA"}
 
@@ -48,7 +49,7 @@ class LevelDesc(C.Structure):
     _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("p", C.c_int),
                 ("extent", C.c_double * 3), ("map", C.c_int), ("map_param", C.c_double * 4),
                 ("coords", C.c_void_p), ("dirichlet_faces", C.c_int), ("device", C.c_int),
-                ("z_offset", C.c_int)]
+                ("z_offset", C.c_int), ("flags", C.c_int)]
 
 
 class Material(C.Structure):
@@ -106,6 +107,7 @@ def lib():
             "emfgpu_level_n_dofs": (i64, [vp]),
             "emfgpu_level_n_elements": (i64, [vp]),
             "emfgpu_level_affine": (C.c_int, [vp]),
+            "emfgpu_level_cartesian": (C.c_int, [vp]),
             "emfgpu_level_jacobians": (st, [vp, vp]),
             "emfgpu_level_coords": (st, [vp, vp]),
             "emfgpu_level_last_error": (C.c_char_p, [vp]),
@@ -182,7 +184,7 @@ class FeLevel:
     node-coordinate array."""
 
     def __init__(self, nx, ny=None, nz=None, p=2, extent=(1.0, 1.0, 1.0), map="reference",
-                 map_param=(0.0,), coords=None, dirichlet_faces=1, device=0, z_offset=0):
+                 map_param=(0.0,), coords=None, dirichlet_faces=1, device=0, z_offset=0, flags=0):
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         d = LevelDesc()
@@ -196,6 +198,7 @@ class FeLevel:
         d.dirichlet_faces = dirichlet_faces
         d.device = device
         d.z_offset = z_offset
+        d.flags = flags
         h = C.c_void_p()
         st = lib().emfgpu_level_create(C.byref(d), C.byref(h))
         if st:
@@ -206,10 +209,11 @@ class FeLevel:
         self.n_dofs = lib().emfgpu_level_n_dofs(self.h)
         self.n_elements = lib().emfgpu_level_n_elements(self.h)
         self.affine = bool(lib().emfgpu_level_affine(self.h))
+        self.cartesian = bool(lib().emfgpu_level_cartesian(self.h))
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().emfgpu_level_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_level_destroy(self.h)
             self.h = None
 
     def dof_count(self):
@@ -260,8 +264,8 @@ class ElasticOperator:
         self.h = h.value
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().emfgpu_op_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_op_destroy(self.h)
             self.h = None
 
     def _raise(self, st, e=None, q=None):
@@ -372,8 +376,8 @@ class TransferOp:
         self.fine, self.coarse = fine, coarse
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().emfgpu_transfer_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_transfer_destroy(self.h)
             self.h = None
 
     def _run(self, kind, precision, d_in, d_out, stream):
@@ -401,8 +405,8 @@ class ChebyshevSmoother:
         self.op = op
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().emfgpu_cheb_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_cheb_destroy(self.h)
             self.h = None
 
     def smooth(self, d_x, d_b, zero_start=True, stream=None):

@@ -32,10 +32,11 @@ def params_from(arr, G):
                             phi=arr[7], e1=tuple(arr[8:11]), e2=tuple(arr[11:14]), e3=tuple(arr[14:17]))
 
 
-def test_cfg0_vs_reference(G):
+@pytest.mark.parametrize("flags", [0, 1, 3])  # Cartesian fast path / affine / per-qp geometry
+def test_cfg0_vs_reference(G, flags):
     g = np.load(os.path.join(GOLD, "cfg0.npz"))
-    lev = G.FeLevel(8, p=2, dirichlet_faces=1)
-    assert lev.affine
+    lev = G.FeLevel(8, p=2, dirichlet_faces=1, flags=flags)
+    assert lev.affine == (flags & 2 == 0) and lev.cartesian == (flags == 0)
     u0 = I.make_u0(8, 8, 8, 2)
     v = I.make_v(lev.n_dofs)
     for prec in (64, 32):
@@ -78,10 +79,12 @@ def test_geometry_matches_reference_jacobians(G):
     assert rel(lev.jacobians(), orc.jacobians()) <= 1e-14
 
 
-def test_cfg1_full_size_known_answers(G):
+@pytest.mark.parametrize("flags", [0, 1])
+def test_cfg1_full_size_known_answers(G, flags):
     """BASELINE configs[1] at full size (32^3 Q3, 2 738 019 DoFs) against the
     reference's known answers and the oracle."""
-    lev = G.FeLevel(32, p=3)
+    lev = G.FeLevel(32, p=3, flags=flags)
+    assert lev.cartesian == (flags == 0)
     u0 = I.make_u0(32, 32, 32, 3)
     v = I.make_v(lev.n_dofs)
     assert np.isclose(np.linalg.norm(u0), 28.816069046240159, rtol=1e-13)
@@ -196,6 +199,7 @@ def test_split_apply_and_slab_emulation(G):
         sl = slice(c0 * plane, (c1 + 1) * plane)
         lv = G.FeLevel(n, n, k1 - k0, p=p, coords=coords[sl], dirichlet_faces=1 | (16 if r == 0 else 0),
                        z_offset=k0)
+        assert lv.cartesian
         o = G.ElasticOperator(lv, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
         o.update_linearization(u0[sl])
         x = torch.tensor(v[sl], device="cuda")

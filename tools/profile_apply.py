@@ -16,6 +16,7 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 model = sys.argv[4] if len(sys.argv) > 4 else "cnh"
 n, p = (32, 3) if len(sys.argv) <= 5 else (int(sys.argv[5]), int(sys.argv[6]))
 lev = G.FeLevel(n, p=p)
+print("affine", lev.affine, "cartesian", lev.cartesian)
 op = G.ElasticOperator(lev, model, G.MaterialParams(mu=1.0, lam=10.0, kappa_b=1000.0), strat, prec)
 op.update_linearization(I.make_u0(n, n, n, p))
 dt = torch.float64 if prec == 64 else torch.float32
