@@ -175,6 +175,43 @@ emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, 
  * vectors of Number (dot_d, solver.hpp:95-100). */
 emfgpu_status emfgpu_dot(int precision, const void* d_a, const void* d_b, int64_t n, double* out, void* stream);
 
+/* ---- hp-multigrid preconditioner (MgHierarchy<Prec>, solver.hpp:437-581) ---
+ * Ladder p -> p/2 -> ... -> 1 on the fine mesh, then uniform h-coarsening
+ * (all of nx, ny, nz halved) while every count stays >= coarse_n (the
+ * reference's n0, build_cube(n0, l)).  Coarse levels regenerate the fine
+ * level's map.  Smoother: Chebyshev-Jacobi on every level; coarsest level:
+ * Jacobi-PCG to coarse_rtol (the reference's CoarseSolver CG path). */
+typedef struct emfgpu_mg emfgpu_mg;
+typedef struct emfgpu_mg_config {
+  int degree;            /* operator applications per smoothing pass (default 6) */
+  double range_factor;   /* lambda_min = lambda_max / range_factor (15) */
+  double safety;         /* lambda_max = safety * Lanczos estimate (1.2) */
+  int eig_iterations;    /* Lanczos steps (20) */
+  uint64_t seed;         /* Lanczos start vector seed (0x9e3779b97f4a7c15) */
+  double coarse_rtol;    /* coarse CG relative tolerance (1e-4) */
+  int coarse_maxit;      /* coarse CG iteration cap (500) */
+  int coarse_n;          /* smallest element count per axis of the h-ladder (1) */
+  int precision;         /* level precision: 32 (MgHierarchy<float>, default) or 64 */
+} emfgpu_mg_config;
+void emfgpu_mg_default_config(emfgpu_mg_config* cfg);
+emfgpu_status emfgpu_mg_create(const emfgpu_level* fine, int model, const emfgpu_material* params, int strategy,
+                               const emfgpu_mg_config* cfg, emfgpu_mg** out);
+void emfgpu_mg_destroy(emfgpu_mg* mg);
+int emfgpu_mg_n_levels(const emfgpu_mg* mg);
+emfgpu_status emfgpu_mg_level_info(const emfgpu_mg* mg, int level, int* nx, int* ny, int* nz, int* p,
+                                   int64_t* n_dofs);
+const char* emfgpu_mg_last_error(const emfgpu_mg* mg);
+/* MgHierarchy::update_linearization (solver.hpp:490-509): interpolate u_k down
+ * the ladder, relinearize, diagonal, Lanczos, smoother setup. d_u: device fp64. */
+emfgpu_status emfgpu_mg_update_linearization(emfgpu_mg* mg, const double* d_u_fine, void* stream);
+/* MgHierarchy::precondition (solver.hpp:512-520): z = V-cycle(r), fp64 in/out. */
+emfgpu_status emfgpu_mg_precondition(emfgpu_mg* mg, const double* d_r, double* d_z, void* stream);
+/* Preconditioned CG in fp64 (BASELINE cfg4 outer solve; the reference's outer
+ * solver is FGMRES, solver.hpp:120-203): x0 = 0, stop at ||r|| <= rtol ||b||.
+ * mg may be NULL (unpreconditioned).  history (host, maxit+1) optional. */
+emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double rtol,
+                               int maxit, int* iterations, double* history, void* stream);
+
 /* FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured by a register-resident
  * FMA loop over one wave of CTAs for `seconds`: the FP64/FP32 roofline
  * denominator (bench.py). */

@@ -791,3 +791,240 @@ int orc_op_element_locals(const orc_op* op, const void* x, void* loc, int64_t e0
   return op->precision == 64 ? element_locals_d(op, (const double*)x, (double*)loc, e0, e1)
                              : element_locals_f(op, (const float*)x, (float*)loc, e0, e1);
 }
+
+/* ---- hp-multigrid V-cycle (solver.hpp:437-581), float levels --------------
+ * Ladder p -> p/2 -> ... -> 1 on the fine mesh, then n0<<l cubes for
+ * l = lmax-1..0 at p = 1 (solver.hpp:450-459).  Coarse solver: the
+ * reference's Jacobi-PCG path (solver.hpp:393-424; coarse_direct_limit = 0). */
+#define ORC_MAXLEV 16
+typedef struct {
+  int nlev, n[ORC_MAXLEV], p[ORC_MAXLEV], faces, degree, eig_it;
+  double range_factor, safety, lmax[ORC_MAXLEV];
+  uint64_t seed;
+  orc_op* ops[ORC_MAXLEV];
+  float* diag[ORC_MAXLEV];
+  float* x[ORC_MAXLEV];
+  float* b[ORC_MAXLEV];
+} orc_mg;
+
+static void zero_mask_f(const orc_op* op, float* v) {
+  for (int64_t i = 0; i < op->ndofs; ++i)
+    if (op->mask[i]) v[i] = 0.0f;
+}
+
+static double dotf(const float* a, const float* b, int64_t n) {
+  double s = 0;
+  for (int64_t i = 0; i < n; ++i) s += (double)a[i] * (double)b[i];
+  return s;
+}
+
+orc_mg* orc_mg_create(int n0, int lmax, int p, double deform_amp, int faces, int model, const double* prm,
+                      int strategy, int degree, double range_factor, double safety, int eig_it) {
+  orc_mg* m = (orc_mg*)calloc(1, sizeof(orc_mg));
+  int pp = p, k = 0;
+  m->n[k] = n0 << lmax;
+  m->p[k++] = pp;
+  while (pp > 1) {
+    pp /= 2;
+    m->n[k] = n0 << lmax;
+    m->p[k++] = pp;
+  }
+  for (int l = lmax - 1; l >= 0; --l) {
+    m->n[k] = n0 << l;
+    m->p[k++] = 1;
+  }
+  m->nlev = k;
+  m->faces = faces;
+  m->degree = degree;
+  m->range_factor = range_factor;
+  m->safety = safety;
+  m->eig_it = eig_it;
+  m->seed = 0x9e3779b97f4a7c15ull;
+  const double ext[3] = {1.0, 1.0, 1.0}, mp[2] = {deform_amp, 1.0};
+  for (int l = 0; l < m->nlev; ++l) {
+    const int n = m->n[l], q = m->p[l];
+    double* coords = (double*)malloc(sizeof(double) * 3 * (size_t)(n * q + 1) * (n * q + 1) * (n * q + 1));
+    orc_lattice_coords(n, n, n, q, ext, 0, mp, coords);
+    m->ops[l] = orc_op_create(n, n, n, q, coords, faces, model, prm, strategy, 32);
+    free(coords);
+    const int64_t nd = m->ops[l]->ndofs;
+    m->diag[l] = (float*)malloc(sizeof(float) * nd);
+    m->x[l] = (float*)calloc(nd, sizeof(float));
+    m->b[l] = (float*)calloc(nd, sizeof(float));
+  }
+  return m;
+}
+
+void orc_mg_destroy(orc_mg* m) {
+  for (int l = 0; l < m->nlev; ++l) {
+    orc_op_destroy(m->ops[l]);
+    free(m->diag[l]);
+    free(m->x[l]);
+    free(m->b[l]);
+  }
+  free(m);
+}
+
+int orc_mg_n_levels(const orc_mg* m) { return m->nlev; }
+
+static void dims4(const orc_mg* m, int l, int* d) { d[0] = d[1] = d[2] = m->n[l]; d[3] = m->p[l]; }
+
+/* MgHierarchy::update_linearization, solver.hpp:490-509 */
+int orc_mg_update(orc_mg* m, const double* u_fine) {
+  const int64_t n0 = m->ops[0]->ndofs;
+  double* u = (double*)malloc(sizeof(double) * n0);
+  memcpy(u, u_fine, sizeof(double) * n0);
+  int err = 0;
+  for (int l = 0; l < m->nlev; ++l) {
+    orc_op* op = m->ops[l];
+    if (l > 0) {
+      int fd[4], cd[4];
+      dims4(m, l - 1, fd);
+      dims4(m, l, cd);
+      double* uc = (double*)malloc(sizeof(double) * op->ndofs);
+      orc_transfer(fd[0], fd[1], fd[2], fd[3], cd[0], cd[1], cd[2], cd[3], 2, 64, u, uc);
+      for (int64_t i = 0; i < op->ndofs; ++i)
+        if (op->mask[i]) uc[i] = 0.0; /* dirichlet_set_values (zero) */
+      free(u);
+      u = uc;
+    }
+    if ((err = orc_op_linearize(op, u, NULL, NULL))) break;
+    int64_t nb;
+    if ((err = orc_op_diagonal(op, m->diag[l], &nb))) break;
+    double lmin;
+    if ((err = orc_op_estimate_eigenvalues(op, m->diag[l], m->eig_it, m->seed, &lmin, &m->lmax[l]))) break;
+  }
+  free(u);
+  return err;
+}
+
+/* CoarseSolver::solve (Jacobi-PCG path), solver.hpp:393-424 */
+static int coarse_cg(const orc_op* op, const float* diag, const float* b, float* x) {
+  const int64_t n = op->ndofs;
+  float *r = (float*)malloc(sizeof(float) * n), *z = (float*)malloc(sizeof(float) * n),
+        *pv = (float*)malloc(sizeof(float) * n), *ap = (float*)malloc(sizeof(float) * n),
+        *inv = (float*)malloc(sizeof(float) * n);
+  int err = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    x[i] = 0.0f;
+    r[i] = b[i];
+    inv[i] = 1.0f / diag[i];
+  }
+  const double bnorm = sqrt(dotf(b, b, n));
+  if (bnorm != 0) {
+    for (int64_t i = 0; i < n; ++i) z[i] = inv[i] * r[i];
+    memcpy(pv, z, sizeof(float) * n);
+    double rz = dotf(r, z, n);
+    int it;
+    for (it = 0; it < 500; ++it) {
+      err |= orc_op_apply(op, pv, ap);
+      const double alpha = rz / dotf(pv, ap, n);
+      for (int64_t i = 0; i < n; ++i) {
+        x[i] += (float)alpha * pv[i];
+        r[i] -= (float)alpha * ap[i];
+      }
+      if (sqrt(dotf(r, r, n)) <= 1e-4 * bnorm) break;
+      for (int64_t i = 0; i < n; ++i) z[i] = inv[i] * r[i];
+      const double rz_new = dotf(r, z, n);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = 0; i < n; ++i) pv[i] = z[i] + (float)beta * pv[i];
+    }
+    if (it == 500) err = 5;
+  }
+  free(r);
+  free(z);
+  free(pv);
+  free(ap);
+  free(inv);
+  return err;
+}
+
+/* MgHierarchy::v_cycle, solver.hpp:544-569 */
+static int v_cycle(orc_mg* m, int l, const float* b) {
+  orc_op* op = m->ops[l];
+  const int64_t n = op->ndofs;
+  float* x = m->x[l];
+  for (int64_t i = 0; i < n; ++i) x[i] = 0.0f;
+  if (l + 1 == m->nlev) return coarse_cg(op, m->diag[l], b, x);
+  int err = orc_op_chebyshev(op, m->diag[l], m->lmax[l], m->degree, m->range_factor, m->safety, b, x, 1);
+  float* t = (float*)malloc(sizeof(float) * n);
+  err |= orc_op_apply(op, x, t);
+  for (int64_t i = 0; i < n; ++i) t[i] = b[i] - t[i];
+  zero_mask_f(op, t);
+  int fd[4], cd[4];
+  dims4(m, l, fd);
+  dims4(m, l + 1, cd);
+  float* bc = m->b[l + 1];
+  orc_transfer(fd[0], fd[1], fd[2], fd[3], cd[0], cd[1], cd[2], cd[3], 1, 32, t, bc);
+  zero_mask_f(m->ops[l + 1], bc);
+  err |= v_cycle(m, l + 1, bc);
+  orc_transfer(fd[0], fd[1], fd[2], fd[3], cd[0], cd[1], cd[2], cd[3], 0, 32, m->x[l + 1], t);
+  zero_mask_f(op, t);
+  for (int64_t i = 0; i < n; ++i) x[i] += t[i];
+  err |= orc_op_chebyshev(op, m->diag[l], m->lmax[l], m->degree, m->range_factor, m->safety, b, x, 0);
+  free(t);
+  return err;
+}
+
+/* MgHierarchy::precondition, solver.hpp:512-520 */
+int orc_mg_precondition(orc_mg* m, const double* r, double* z) {
+  const int64_t n = m->ops[0]->ndofs;
+  float* b0 = m->b[0];
+  for (int64_t i = 0; i < n; ++i) b0[i] = (float)r[i];
+  zero_mask_f(m->ops[0], b0);
+  const int err = v_cycle(m, 0, b0);
+  for (int64_t i = 0; i < n; ++i) z[i] = (double)m->x[0][i];
+  return err;
+}
+
+/* Outer PCG in double (see ref_driver.cpp ref_pcg_solve). */
+int orc_pcg_solve(const orc_op* op, orc_mg* m, const double* b, double* x, double rtol, int maxit, int* iters,
+                  double* history) {
+  const int64_t n = op->ndofs;
+  double *r = (double*)malloc(sizeof(double) * n), *z = (double*)malloc(sizeof(double) * n),
+         *pv = (double*)malloc(sizeof(double) * n), *ap = (double*)malloc(sizeof(double) * n);
+  int err = 0, it = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    x[i] = 0.0;
+    r[i] = b[i];
+  }
+  const double bnorm = sqrt(dot_d(b, b, n));
+  if (history) history[0] = 1.0;
+  if (bnorm != 0) {
+    if (m)
+      err |= orc_mg_precondition(m, r, z);
+    else
+      memcpy(z, r, sizeof(double) * n);
+    memcpy(pv, z, sizeof(double) * n);
+    double rz = dot_d(r, z, n);
+    for (it = 0; it < maxit; ++it) {
+      err |= orc_op_apply(op, pv, ap);
+      const double alpha = rz / dot_d(pv, ap, n);
+      for (int64_t i = 0; i < n; ++i) {
+        x[i] += alpha * pv[i];
+        r[i] -= alpha * ap[i];
+      }
+      const double rel = sqrt(dot_d(r, r, n)) / bnorm;
+      if (history) history[it + 1] = rel;
+      if (rel <= rtol) {
+        ++it;
+        break;
+      }
+      if (m)
+        err |= orc_mg_precondition(m, r, z);
+      else
+        memcpy(z, r, sizeof(double) * n);
+      const double rz_new = dot_d(r, z, n);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = 0; i < n; ++i) pv[i] = z[i] + beta * pv[i];
+    }
+  }
+  *iters = it;
+  free(r);
+  free(z);
+  free(pv);
+  free(ap);
+  return err;
+}

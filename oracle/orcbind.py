@@ -175,3 +175,55 @@ def transfer(fine_dims, coarse_dims, kind, vec, precision=64):
     out = np.empty(3 * (d[0] * d[3] + 1) * (d[1] * d[3] + 1) * (d[2] * d[3] + 1), dt)
     lib().orc_transfer(*fine_dims, *coarse_dims, k, precision, _p(vec), _p(out))
     return out
+
+
+class OracleMg:
+    """C restatement of MgHierarchy<float> (emf_oracle.c), cube levels."""
+
+    def __init__(self, n0, lmax, p, model="inh", params=None, strategy="none", degree=6, range_factor=15.0,
+                 safety=1.2, eig_iterations=20, deform_amp=0.0, faces=1):
+        L = lib()
+        L.orc_mg_create.restype = C.c_void_p
+        L.orc_mg_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                    C.c_int, C.c_double, C.c_double, C.c_int]
+        L.orc_mg_destroy.argtypes = [C.c_void_p]
+        L.orc_mg_n_levels.argtypes = [C.c_void_p]
+        L.orc_mg_update.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_mg_precondition.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_pcg_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                    C.POINTER(C.c_int), C.c_void_p]
+        from oracle.refbind import material_params
+        self.params = material_params() if params is None else np.asarray(params, np.float64)
+        self.h = L.orc_mg_create(n0, lmax, p, deform_amp, faces, MODELS[model], _p(self.params),
+                                 STRATEGIES[strategy], degree, range_factor, safety, eig_iterations)
+        self.n_levels = L.orc_mg_n_levels(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_mg_destroy(self.h)
+
+    def update_linearization(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        st = lib().orc_mg_update(self.h, _p(u))
+        if st:
+            raise OracleError(st)
+
+    def precondition(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        st = lib().orc_mg_precondition(self.h, _p(r), _p(z))
+        if st:
+            raise OracleError(st)
+        return z
+
+
+def pcg_solve(op: OracleOperator, mg, b, rtol=1e-8, maxit=200):
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.empty_like(b)
+    it = C.c_int()
+    hist = np.zeros(maxit + 1)
+    st = lib().orc_pcg_solve(op.h, mg.h if mg is not None else None, _p(b), _p(x), rtol, maxit, C.byref(it),
+                             _p(hist))
+    if st:
+        raise OracleError(st)
+    return x, it.value, hist[:it.value + 1]

@@ -418,3 +418,119 @@ int ref_chebyshev(void* o, const void* diag, double lmax_est, int degree,
 }
 
 }  // extern "C"
+
+// ---- hp-multigrid (solver.hpp:437-581) and an outer PCG composed from
+// reference primitives (SURVEY §8(c) gap 4: the reference has no outer CG;
+// cfg4 asks for one).  The V-cycle, smoothers, transfers, Lanczos and coarse
+// solver are the reference's own MgHierarchy<float>.
+namespace {
+struct RefMg {
+  std::unique_ptr<MgHierarchy<float>> mg;
+  const FeLevel* fe = nullptr;
+};
+}  // namespace
+
+extern "C" {
+
+// coarse_direct_limit: DoF threshold below which the reference factorises the
+// coarsest level densely (default 2000); 0 forces its Jacobi-PCG path.
+void* ref_mg_create(void* l, int model, const double* params, int strategy, int degree, double range_factor,
+                    double safety, int eig_iterations, double deform_amp, int dirichlet_faces,
+                    int64_t coarse_direct_limit) {
+  RefLevel* L = static_cast<RefLevel*>(l);
+  RefMg* m = new RefMg;
+  int st = guarded([&] {
+    const Formulation form{Stability::stable, Domain::material};
+    const Strategy s = strategy == 0 ? Strategy::none : strategy == 1 ? Strategy::scalar : Strategy::tensor;
+    const ModelKind mk = model == 0 ? ModelKind::cnh : model == 1 ? ModelKind::inh : ModelKind::fiber;
+    SmootherConfig sc;
+    sc.degree = degree;
+    sc.range_factor = range_factor;
+    sc.safety = safety;
+    sc.eig_iterations = eig_iterations;
+    std::array<bool, 6> faces{};
+    for (int f = 0; f < 6; ++f) faces[f] = (dirichlet_faces >> f) & 1;
+    m->fe = L->fe.get();
+    m->mg = std::make_unique<MgHierarchy<float>>(*L->fe, faces, mk, params_from(params), form, s, KernelConfig{},
+                                                 sc, DeformMap{deform_amp}, coarse_direct_limit);
+  });
+  if (st != 0) {
+    delete m;
+    return nullptr;
+  }
+  return m;
+}
+
+void ref_mg_destroy(void* m) { delete static_cast<RefMg*>(m); }
+int ref_mg_n_levels(void* m) { return static_cast<RefMg*>(m)->mg->n_levels(); }
+
+int ref_mg_update_linearization(void* m, const double* u) {
+  RefMg* M = static_cast<RefMg*>(m);
+  return guarded([&] {
+    std::vector<double> uk(u, u + M->fe->dof_count());
+    M->mg->update_linearization(uk);
+  });
+}
+
+int ref_mg_precondition(void* m, const double* r, double* z) {
+  RefMg* M = static_cast<RefMg*>(m);
+  return guarded([&] {
+    const int64_t n = M->fe->dof_count();
+    std::vector<double> rv(r, r + n), zv;
+    M->mg->precondition(rv, zv);
+    std::memcpy(z, zv.data(), n * sizeof(double));
+  });
+}
+
+// Preconditioned CG in double (dot_d accumulation, solver.hpp:95-106) with the
+// reference operator and (optionally) the reference V-cycle; x starts at 0.
+// Stops when ||r|| <= rtol ||b||; returns iterations and the residual history.
+int ref_pcg_solve(void* o, void* m, const double* b, double* x, double rtol, int maxit, int* iters,
+                  double* history) {
+  RefOp* op = static_cast<RefOp*>(o);
+  RefMg* M = static_cast<RefMg*>(m);
+  return guarded([&] {
+    const int64_t n = op->n;
+    std::vector<double> bv(b, b + n), xv(n, 0.0), r = bv, z(n), p(n), ap(n);
+    auto prec = [&](const std::vector<double>& rr, std::vector<double>& zz) {
+      if (M)
+        M->mg->precondition(rr, zz);
+      else
+        zz = rr;
+    };
+    const double bnorm = norm_d(bv);
+    int it = 0;
+    if (history) history[0] = 1.0;
+    if (bnorm == 0) {
+      *iters = 0;
+      std::memset(x, 0, n * sizeof(double));
+      return;
+    }
+    prec(r, z);
+    p = z;
+    double rz = dot_d(r, z);
+    for (it = 0; it < maxit; ++it) {
+      op->d->apply_tangent(p, ap);
+      const double alpha = rz / dot_d(p, ap);
+      for (int64_t i = 0; i < n; ++i) {
+        xv[i] += alpha * p[i];
+        r[i] -= alpha * ap[i];
+      }
+      const double rel = norm_d(r) / bnorm;
+      if (history) history[it + 1] = rel;
+      if (rel <= rtol) {
+        ++it;
+        break;
+      }
+      prec(r, z);
+      const double rz_new = dot_d(r, z);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    }
+    *iters = it;
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+}  // extern "C"

@@ -184,3 +184,51 @@ def structure_tensors(params):
     out = np.empty(21)
     _check(lib().ref_structure_tensors(_p(np.asarray(params, np.float64)), _p(out)))
     return out
+
+
+class RefMg:
+    """The reference's MgHierarchy<float> (solver.hpp:437-581) on a cube level."""
+
+    def __init__(self, level: RefLevel, model, params, strategy="none", degree=6, range_factor=15.0, safety=1.2,
+                 eig_iterations=20, deform_amp=0.0, faces=1, coarse_direct_limit=0):
+        L = lib()
+        L.ref_mg_create.restype = C.c_void_p
+        L.ref_mg_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                    C.c_int, C.c_double, C.c_int, C.c_int64]
+        L.ref_mg_destroy.argtypes = [C.c_void_p]
+        L.ref_mg_n_levels.argtypes = [C.c_void_p]
+        L.ref_mg_update_linearization.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_mg_precondition.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_pcg_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                    C.POINTER(C.c_int), C.c_void_p]
+        self.params = np.asarray(params, np.float64)
+        self.level = level
+        self.h = L.ref_mg_create(level.h, MODELS[model], _p(self.params), STRATEGIES[strategy], degree, range_factor,
+                                 safety, eig_iterations, deform_amp, faces, coarse_direct_limit)
+        if not self.h:
+            raise RefError(1, L.ref_last_error().decode())
+        self.n_levels = L.ref_mg_n_levels(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_mg_destroy(self.h)
+
+    def update_linearization(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        _check(lib().ref_mg_update_linearization(self.h, _p(u)))
+
+    def precondition(self, r):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        _check(lib().ref_mg_precondition(self.h, _p(r), _p(z)))
+        return z
+
+
+def pcg_solve(op: RefOperator, mg, b, rtol=1e-8, maxit=200):
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.empty_like(b)
+    it = C.c_int()
+    hist = np.zeros(maxit + 1)
+    _check(lib().ref_pcg_solve(op.h, mg.h if mg is not None else None, _p(b), _p(x), rtol, maxit, C.byref(it),
+                               _p(hist)))
+    return x, it.value, hist[:it.value + 1]

@@ -327,7 +327,8 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
 #pragma unroll
         for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][3 + c][qs], a.uk + 3 * ep.node + c);
       }
-      if (a.affine && q < 10) cp_async_T(&sm.geo[b][el][q], a.geo + q * a.geo_stride + e);
+      if (a.affine)
+        for (int f = q; f < 10; f += N3) cp_async_T(&sm.geo[b][el][f], a.geo + f * a.geo_stride + e);
     }
     cp_async_commit();
   };

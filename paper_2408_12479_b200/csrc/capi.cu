@@ -352,6 +352,8 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
     L->nq3 = n * n * n;
     L->faces = d->dirichlet_faces;
     L->z_offset = d->z_offset;
+    L->desc = *d;
+    L->desc.coords = nullptr;
     for (int a = 0; a < 3; ++a) L->extent[a] = d->extent[a] > 0 ? d->extent[a] : 1.0;
     L->nodes = lobatto_nodes(n);
     gauss_rule(n, L->qpts, L->qwts);
@@ -1176,3 +1178,380 @@ emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, 
   });
 }
 
+
+// ============================================================================
+// hp-multigrid hierarchy (MgHierarchy, solver.hpp:437-581) and outer PCG
+// ============================================================================
+struct emfgpu_mg {
+  emfgpu_mg_config cfg{};
+  const emfgpu_level* fine = nullptr;
+  std::vector<emfgpu_level*> owned;
+  std::vector<const emfgpu_level*> lv;
+  std::vector<emfgpu_op*> ops;
+  std::vector<emfgpu_transfer*> tr;  // tr[l]: lv[l] (fine) <-> lv[l+1] (coarse)
+  std::vector<emfgpu_cheb*> cheb;
+  std::vector<void*> diag, x, b, t;
+  std::vector<double*> u;
+  void *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr, *cg_ap = nullptr, *cg_inv = nullptr;
+  double* dbuf = nullptr;
+  double* hdot = nullptr;  // pinned
+  int coarse_iterations = 0;
+  std::string last_error;
+};
+
+namespace {
+
+double mg_dot_sync(double* dbuf, double* hdot, cudaStream_t s) {
+  CK(cudaMemcpyAsync(hdot, dbuf, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return *hdot;
+}
+
+template <typename T>
+double devdot(emfgpu_mg* m, const T* a, const T* b, int64_t n, cudaStream_t s) {
+  launch_dot<T>(a, b, n, m->dbuf + 1, m->dbuf, s);
+  return mg_dot_sync(m->dbuf, m->hdot, s);
+}
+
+template <typename T>
+void op_apply_T(emfgpu_op* op, const T* x, T* y, cudaStream_t s) {
+  apply_elements(op, x, 0, op->L->nz, s);
+  apply_nodes(op, x, y, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+}
+
+template <typename T>
+void mask0(const emfgpu_level* L, T* v, cudaStream_t s) {
+  launch_mask_zero<T>(v, L->nnodes, L->mx, L->my, L->mz, L->faces, s);
+}
+
+// CoarseSolver::solve, Jacobi-PCG path (solver.hpp:393-424)
+template <typename T>
+void coarse_cg(emfgpu_mg* m, int l, cudaStream_t s) {
+  emfgpu_op* op = m->ops[l];
+  const int64_t n = op->L->ndofs;
+  T* x = static_cast<T*>(m->x[l]);
+  const T* b = static_cast<const T*>(m->b[l]);
+  T *r = static_cast<T*>(m->cg_r), *z = static_cast<T*>(m->cg_z), *p = static_cast<T*>(m->cg_p),
+    *ap = static_cast<T*>(m->cg_ap);
+  const T* inv = static_cast<const T*>(m->cg_inv);
+  CK(cudaMemsetAsync(x, 0, sizeof(T) * n, s));
+  CK(cudaMemcpyAsync(r, b, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  const double bnorm = std::sqrt(devdot<T>(m, b, b, n, s));
+  m->coarse_iterations = 0;
+  if (bnorm == 0) return;
+  launch_jacobi<T>(inv, r, z, n, s);
+  CK(cudaMemcpyAsync(p, z, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+  double rz = devdot<T>(m, r, z, n, s);
+  for (int it = 0; it < m->cfg.coarse_maxit; ++it) {
+    op_apply_T<T>(op, p, ap, s);
+    const double alpha = rz / devdot<T>(m, p, ap, n, s);
+    launch_cg_xr<T>(x, r, p, ap, alpha, n, s);
+    m->coarse_iterations = it + 1;
+    if (std::sqrt(devdot<T>(m, r, r, n, s)) <= m->cfg.coarse_rtol * bnorm) return;
+    launch_jacobi<T>(inv, r, z, n, s);
+    const double rz_new = devdot<T>(m, r, z, n, s);
+    const double beta = rz_new / rz;
+    rz = rz_new;
+    launch_cg_p<T>(p, z, beta, n, s);
+  }
+  throw ApiError(EMFGPU_ERR_NUMERICAL, "coarse CG: no convergence");
+}
+
+// MgHierarchy::v_cycle (solver.hpp:544-569)
+template <typename T>
+void v_cycle(emfgpu_mg* m, int l, cudaStream_t s) {
+  const emfgpu_level* L = m->lv[l];
+  const int64_t n = L->ndofs;
+  T* x = static_cast<T*>(m->x[l]);
+  T* b = static_cast<T*>(m->b[l]);
+  T* t = static_cast<T*>(m->t[l]);
+  if (l + 1 == (int)m->lv.size()) {
+    coarse_cg<T>(m, l, s);
+    return;
+  }
+  CK(cudaMemsetAsync(x, 0, sizeof(T) * n, s));
+  cheb_run<T>(m->cheb[l], x, b, 1, s);
+  op_apply_T<T>(m->ops[l], x, t, s);
+  launch_bminus<T>(b, t, n, s);
+  mask0<T>(L, t, s);
+  T* bc = static_cast<T*>(m->b[l + 1]);
+  transfer_run<T>(m->tr[l], 1, t, bc, s);
+  mask0<T>(m->lv[l + 1], bc, s);
+  v_cycle<T>(m, l + 1, s);
+  transfer_run<T>(m->tr[l], 0, static_cast<const T*>(m->x[l + 1]), t, s);
+  mask0<T>(L, t, s);
+  launch_add<T>(t, x, n, s);
+  cheb_run<T>(m->cheb[l], x, b, 0, s);
+}
+
+template <typename T>
+void mg_precondition(emfgpu_mg* m, const double* r, double* z, cudaStream_t s) {
+  const emfgpu_level* L = m->lv[0];
+  T* b0 = static_cast<T*>(m->b[0]);
+  launch_cast<double, T>(r, b0, L->ndofs, s);
+  mask0<T>(L, b0, s);
+  v_cycle<T>(m, 0, s);
+  launch_cast<T, double>(static_cast<const T*>(m->x[0]), z, L->ndofs, s);
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
+  const int nl = (int)m->lv.size();
+  CK(cudaMemcpyAsync(m->u[0], d_u, sizeof(double) * m->lv[0]->ndofs, cudaMemcpyDeviceToDevice, s));
+  for (int l = 0; l < nl; ++l) {
+    emfgpu_op* op = m->ops[l];
+    if (l > 0) {
+      transfer_run<double>(m->tr[l - 1], 2, m->u[l - 1], m->u[l], s);
+      mask0<double>(m->lv[l], m->u[l], s);  // dirichlet_set_values (zero)
+    }
+    CK(cudaMemcpyAsync(op->d_ukd, m->u[l], sizeof(double) * m->lv[l]->ndofs, cudaMemcpyDeviceToDevice, s));
+    int64_t be = -1;
+    int bq = -1;
+    linearize_impl(op, &be, &bq, s);
+    int64_t nbad = 0;
+    diagonal_impl(op, m->diag[l], &nbad, s);
+    double lmin = 0, lmax = 0;
+    lanczos<T>(op, static_cast<const T*>(m->diag[l]), m->cfg.eig_iterations, m->cfg.seed, &lmin, &lmax, s);
+    if (l + 1 < nl) {
+      if (m->cheb[l]) emfgpu_cheb_destroy(m->cheb[l]);
+      m->cheb[l] = nullptr;
+      if (emfgpu_cheb_create(op, m->diag[l], lmax, m->cfg.degree, m->cfg.range_factor, m->cfg.safety,
+                             &m->cheb[l]) != EMFGPU_OK)
+        throw ApiError(EMFGPU_ERR_CUDA, "mg: smoother setup failed");
+    } else {
+      launch_inv<T>(static_cast<const T*>(m->diag[l]), static_cast<T*>(m->cg_inv), m->lv[l]->ndofs, s);
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+void emfgpu_mg_default_config(emfgpu_mg_config* c) {
+  if (!c) return;
+  c->degree = 6;
+  c->range_factor = 15.0;
+  c->safety = 1.2;
+  c->eig_iterations = 20;
+  c->seed = 0x9e3779b97f4a7c15ull;
+  c->coarse_rtol = 1e-4;
+  c->coarse_maxit = 500;
+  c->coarse_n = 1;
+  c->precision = 32;
+}
+
+void emfgpu_mg_destroy(emfgpu_mg* m) {
+  if (!m) return;
+  for (auto* c : m->cheb) emfgpu_cheb_destroy(c);
+  for (auto* t : m->tr) emfgpu_transfer_destroy(t);
+  for (auto* o : m->ops) emfgpu_op_destroy(o);
+  for (auto* L : m->owned) emfgpu_level_destroy(L);
+  for (auto* v : m->diag) cudaFree(v);
+  for (auto* v : m->x) cudaFree(v);
+  for (auto* v : m->b) cudaFree(v);
+  for (auto* v : m->t) cudaFree(v);
+  for (auto* v : m->u) cudaFree(v);
+  cudaFree(m->cg_r);
+  cudaFree(m->cg_z);
+  cudaFree(m->cg_p);
+  cudaFree(m->cg_ap);
+  cudaFree(m->cg_inv);
+  cudaFree(m->dbuf);
+  if (m->hdot) cudaFreeHost(m->hdot);
+  delete m;
+}
+
+emfgpu_status emfgpu_mg_create(const emfgpu_level* fine, int model, const emfgpu_material* params, int strategy,
+                               const emfgpu_mg_config* cfg, emfgpu_mg** out) {
+  if (!fine || !params || !out) return EMFGPU_ERR_INVALID;
+  *out = nullptr;
+  auto* m = new emfgpu_mg;
+  if (cfg)
+    m->cfg = *cfg;
+  else
+    emfgpu_mg_default_config(&m->cfg);
+  emfgpu_status st = guarded(nullptr, [&] {
+    if (fine->desc.map == EMFGPU_MAP_COORDS)
+      throw ApiError(EMFGPU_ERR_CONFIG, "mg: coarse levels need a generated map (reference / shear_x)");
+    if (fine->z_offset != 0) throw ApiError(EMFGPU_ERR_CONFIG, "mg: slab levels are not supported");
+    if (m->cfg.precision != 32 && m->cfg.precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "mg: precision");
+    CK(cudaSetDevice(fine->device));
+    m->fine = fine;
+    m->lv.push_back(fine);
+    // ladder p -> p/2 -> ... -> 1, then uniform h-coarsening (solver.hpp:447-459)
+    emfgpu_level_desc d = fine->desc;
+    d.coords = nullptr;
+    int p = fine->p;
+    auto add_level = [&](const emfgpu_level_desc& dd) {
+      emfgpu_level* L = nullptr;
+      const emfgpu_status s2 = emfgpu_level_create(&dd, &L);
+      if (s2 != EMFGPU_OK) throw ApiError(s2, std::string("mg: level: ") + emfgpu_global_last_error());
+      m->owned.push_back(L);
+      m->lv.push_back(L);
+    };
+    while (p > 1) {
+      p /= 2;
+      d.p = p;
+      add_level(d);
+    }
+    const int cn = std::max(1, m->cfg.coarse_n);
+    while (d.nx % 2 == 0 && d.ny % 2 == 0 && d.nz % 2 == 0 && d.nx / 2 >= cn && d.ny / 2 >= cn &&
+           d.nz / 2 >= cn) {
+      d.nx /= 2;
+      d.ny /= 2;
+      d.nz /= 2;
+      add_level(d);
+    }
+    const int nl = (int)m->lv.size();
+    const size_t ts = m->cfg.precision == 64 ? 8 : 4;
+    for (int l = 0; l < nl; ++l) {
+      emfgpu_op* op = nullptr;
+      const emfgpu_status s2 = emfgpu_op_create(m->lv[l], model, params, 0, strategy, m->cfg.precision, &op);
+      if (s2 != EMFGPU_OK) throw ApiError(s2, std::string("mg: operator: ") + emfgpu_global_last_error());
+      m->ops.push_back(op);
+      if (l + 1 < nl) {
+        emfgpu_transfer* t = nullptr;
+        const emfgpu_status s3 = emfgpu_transfer_create(m->lv[l], m->lv[l + 1], &t);
+        if (s3 != EMFGPU_OK) throw ApiError(s3, "mg: transfer");
+        m->tr.push_back(t);
+      }
+      const int64_t n = m->lv[l]->ndofs;
+      void *dg, *x, *b, *t;
+      double* u;
+      CK(cudaMalloc(&dg, ts * n));
+      CK(cudaMalloc(&x, ts * n));
+      CK(cudaMalloc(&b, ts * n));
+      CK(cudaMalloc(&t, ts * n));
+      CK(cudaMalloc(&u, sizeof(double) * n));
+      m->diag.push_back(dg);
+      m->x.push_back(x);
+      m->b.push_back(b);
+      m->t.push_back(t);
+      m->u.push_back(u);
+    }
+    m->cheb.assign(nl, nullptr);
+    const int64_t nc = m->lv.back()->ndofs;
+    CK(cudaMalloc(&m->cg_r, ts * nc));
+    CK(cudaMalloc(&m->cg_z, ts * nc));
+    CK(cudaMalloc(&m->cg_p, ts * nc));
+    CK(cudaMalloc(&m->cg_ap, ts * nc));
+    CK(cudaMalloc(&m->cg_inv, ts * nc));
+    CK(cudaMalloc(&m->dbuf, sizeof(double) * (dot_partial_count() + 1)));
+    CK(cudaMallocHost(&m->hdot, sizeof(double)));
+  });
+  if (st != EMFGPU_OK) {
+    emfgpu_mg_destroy(m);
+    return st;
+  }
+  *out = m;
+  return EMFGPU_OK;
+}
+
+int emfgpu_mg_n_levels(const emfgpu_mg* m) { return m ? (int)m->lv.size() : 0; }
+
+emfgpu_status emfgpu_mg_level_info(const emfgpu_mg* m, int l, int* nx, int* ny, int* nz, int* p, int64_t* ndofs) {
+  if (!m || l < 0 || l >= (int)m->lv.size()) return EMFGPU_ERR_INVALID;
+  const emfgpu_level* L = m->lv[l];
+  if (nx) *nx = L->nx;
+  if (ny) *ny = L->ny;
+  if (nz) *nz = L->nz;
+  if (p) *p = L->p;
+  if (ndofs) *ndofs = L->ndofs;
+  return EMFGPU_OK;
+}
+
+const char* emfgpu_mg_last_error(const emfgpu_mg* m) { return m ? m->last_error.c_str() : ""; }
+
+emfgpu_status emfgpu_mg_update_linearization(emfgpu_mg* m, const double* d_u_fine, void* stream) {
+  if (!m || !d_u_fine) return EMFGPU_ERR_INVALID;
+  return guarded(&m->last_error, [&] {
+    CK(cudaSetDevice(m->fine->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (m->cfg.precision == 64)
+      mg_linearize<double>(m, d_u_fine, s);
+    else
+      mg_linearize<float>(m, d_u_fine, s);
+  });
+}
+
+emfgpu_status emfgpu_mg_precondition(emfgpu_mg* m, const double* d_r, double* d_z, void* stream) {
+  if (!m || !d_r || !d_z) return EMFGPU_ERR_INVALID;
+  return guarded(&m->last_error, [&] {
+    if (!m->ops[0]->linearized) throw ApiError(EMFGPU_ERR_STALE, "mg: update_linearization has not run");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (m->cfg.precision == 64)
+      mg_precondition<double>(m, d_r, d_z, s);
+    else
+      mg_precondition<float>(m, d_r, d_z, s);
+  });
+}
+
+// Preconditioned CG in double on device vectors (x starts at 0).  Stops when
+// ||r|| <= rtol ||b||.  history (host, maxit+1, optional) gets ||r_k||/||b||.
+emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double rtol, int maxit,
+                               int* iterations, double* history, void* stream) {
+  if (!op || !d_b || !d_x) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    if (op->precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "pcg: the outer operator must be fp64");
+    require_linearized(op, "pcg");
+    CK(cudaSetDevice(op->L->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t n = op->L->ndofs;
+    double *r, *z, *p, *ap, *dbuf, *hdot;
+    CK(cudaMalloc(&r, sizeof(double) * n));
+    CK(cudaMalloc(&z, sizeof(double) * n));
+    CK(cudaMalloc(&p, sizeof(double) * n));
+    CK(cudaMalloc(&ap, sizeof(double) * n));
+    CK(cudaMalloc(&dbuf, sizeof(double) * (dot_partial_count() + 1)));
+    CK(cudaMallocHost(&hdot, sizeof(double)));
+    auto dot = [&](const double* a, const double* b) {
+      launch_dot<double>(a, b, n, dbuf + 1, dbuf, s);
+      return mg_dot_sync(dbuf, hdot, s);
+    };
+    auto prec = [&](const double* rr, double* zz) {
+      if (mg) {
+        if (mg->cfg.precision == 64)
+          mg_precondition<double>(mg, rr, zz, s);
+        else
+          mg_precondition<float>(mg, rr, zz, s);
+      } else {
+        CK(cudaMemcpyAsync(zz, rr, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      }
+    };
+    CK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, s));
+    CK(cudaMemcpyAsync(r, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    const double bnorm = std::sqrt(dot(d_b, d_b));
+    if (history) history[0] = 1.0;
+    int it = 0;
+    if (bnorm != 0) {
+      prec(r, z);
+      CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      double rz = dot(r, z);
+      for (it = 0; it < maxit; ++it) {
+        op_apply_T<double>(op, p, ap, s);
+        const double alpha = rz / dot(p, ap);
+        launch_cg_xr<double>(d_x, r, p, ap, alpha, n, s);
+        const double rel = std::sqrt(dot(r, r)) / bnorm;
+        if (history) history[it + 1] = rel;
+        if (rel <= rtol) {
+          ++it;
+          break;
+        }
+        prec(r, z);
+        const double rz_new = dot(r, z);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        launch_cg_p<double>(p, z, beta, n, s);
+      }
+    }
+    if (iterations) *iterations = it;
+    CK(cudaStreamSynchronize(s));
+    cudaFree(r);
+    cudaFree(z);
+    cudaFree(p);
+    cudaFree(ap);
+    cudaFree(dbuf);
+    cudaFreeHost(hdot);
+  });
+}

@@ -62,6 +62,20 @@ template <typename T>
 void launch_dinv_sqrt(const T* d, double* s, int64_t n, cudaStream_t st);
 void launch_axpy_minus(double a, const double* x, double* y, int64_t n, cudaStream_t st);
 void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st);
+template <typename T>
+void launch_mask_zero(T* v, int64_t nnodes, int mx, int my, int mz, int faces, cudaStream_t s);
+template <typename Ti, typename To>
+void launch_cast(const Ti* in, To* out, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_bminus(const T* b, T* t, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_add(const T* x, T* y, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_cg_xr(T* x, T* r, const T* p, const T* ap, double alpha, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_cg_p(T* p, const T* z, double beta, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_jacobi(const T* inv, const T* r, T* z, int64_t n, cudaStream_t s);
 
 }  // namespace emfgpu
 
@@ -76,6 +90,7 @@ struct emfgpu_level {
   double* d_geo = nullptr;     // SoA, 10 fields: J0^-1 (9), det J0 * w_q (or det J0 if affine)
   float* d_geo_f = nullptr;
   int64_t geo_stride = 0;
+  emfgpu_level_desc desc{};  // creation parameters (coords pointer cleared), for hierarchies
   std::string last_error;
 };
 

@@ -204,3 +204,104 @@ template void launch_dinv_sqrt<double>(const double*, double*, int64_t, cudaStre
 template void launch_dinv_sqrt<float>(const float*, double*, int64_t, cudaStream_t);
 
 }  // namespace emfgpu
+
+// ---- multigrid / Krylov vector kernels ----------------------------------------
+namespace emfgpu {
+
+// v = 0 on Dirichlet DoFs (FeLevel::dirichlet_set_zero, mesh.hpp:115-119)
+template <typename T>
+__global__ void mask_zero_kernel(T* v, int64_t nnodes, int mx, int my, int mz, int faces) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnodes) return;
+  const int a = (int)(i % mx), b = (int)((i / mx) % my), c = (int)(i / ((int64_t)mx * my));
+  if (node_constrained(a, b, c, mx, my, mz, faces)) v[3 * i] = v[3 * i + 1] = v[3 * i + 2] = T(0);
+}
+template <typename T>
+void launch_mask_zero(T* v, int64_t nnodes, int mx, int my, int mz, int faces, cudaStream_t s) {
+  if (faces) mask_zero_kernel<T><<<(unsigned)((nnodes + 255) / 256), 256, 0, s>>>(v, nnodes, mx, my, mz, faces);
+}
+template void launch_mask_zero<double>(double*, int64_t, int, int, int, int, cudaStream_t);
+template void launch_mask_zero<float>(float*, int64_t, int, int, int, int, cudaStream_t);
+
+template <typename Ti, typename To>
+__global__ void cast_kernel(const Ti* __restrict__ in, To* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = To(in[i]);
+}
+template <typename Ti, typename To>
+void launch_cast(const Ti* in, To* out, int64_t n, cudaStream_t s) {
+  cast_kernel<Ti, To><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, n);
+}
+template void launch_cast<double, float>(const double*, float*, int64_t, cudaStream_t);
+template void launch_cast<float, double>(const float*, double*, int64_t, cudaStream_t);
+template void launch_cast<double, double>(const double*, double*, int64_t, cudaStream_t);
+
+// t = b - t (residual from t = A x)
+template <typename T>
+__global__ void bminus_kernel(const T* __restrict__ b, T* __restrict__ t, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) t[i] = b[i] - t[i];
+}
+template <typename T>
+void launch_bminus(const T* b, T* t, int64_t n, cudaStream_t s) {
+  bminus_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(b, t, n);
+}
+template void launch_bminus<double>(const double*, double*, int64_t, cudaStream_t);
+template void launch_bminus<float>(const float*, float*, int64_t, cudaStream_t);
+
+// y += x
+template <typename T>
+__global__ void add_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += x[i];
+}
+template <typename T>
+void launch_add(const T* x, T* y, int64_t n, cudaStream_t s) {
+  add_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, y, n);
+}
+template void launch_add<double>(const double*, double*, int64_t, cudaStream_t);
+template void launch_add<float>(const float*, float*, int64_t, cudaStream_t);
+
+// CG update: x += T(alpha) p ; r -= T(alpha) ap  (solver.hpp:410-413)
+template <typename T>
+__global__ void cg_xr_kernel(T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+                             const T* __restrict__ ap, T alpha, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  x[i] += alpha * p[i];
+  r[i] -= alpha * ap[i];
+}
+template <typename T>
+void launch_cg_xr(T* x, T* r, const T* p, const T* ap, double alpha, int64_t n, cudaStream_t s) {
+  cg_xr_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, r, p, ap, T(alpha), n);
+}
+template void launch_cg_xr<double>(double*, double*, const double*, const double*, double, int64_t, cudaStream_t);
+template void launch_cg_xr<float>(float*, float*, const float*, const float*, double, int64_t, cudaStream_t);
+
+// p = z + T(beta) p
+template <typename T>
+__global__ void cg_p_kernel(T* __restrict__ p, const T* __restrict__ z, T beta, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = z[i] + beta * p[i];
+}
+template <typename T>
+void launch_cg_p(T* p, const T* z, double beta, int64_t n, cudaStream_t s) {
+  cg_p_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, z, T(beta), n);
+}
+template void launch_cg_p<double>(double*, const double*, double, int64_t, cudaStream_t);
+template void launch_cg_p<float>(float*, const float*, double, int64_t, cudaStream_t);
+
+// z = inv * r (Jacobi)
+template <typename T>
+__global__ void jacobi_kernel(const T* __restrict__ inv, const T* __restrict__ r, T* __restrict__ z, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) z[i] = inv[i] * r[i];
+}
+template <typename T>
+void launch_jacobi(const T* inv, const T* r, T* z, int64_t n, cudaStream_t s) {
+  jacobi_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(inv, r, z, n);
+}
+template void launch_jacobi<double>(const double*, const double*, double*, int64_t, cudaStream_t);
+template void launch_jacobi<float>(const float*, const float*, float*, int64_t, cudaStream_t);
+
+}  // namespace emfgpu

@@ -425,3 +425,85 @@ def fma_peak_tflops(precision=64, seconds=0.5) -> float:
     out = C.c_double()
     _check(lib().emfgpu_bench_fma_peak(precision, seconds, C.byref(out)))
     return out.value
+
+
+class MgConfig(C.Structure):
+    _fields_ = [("degree", C.c_int), ("range_factor", C.c_double), ("safety", C.c_double),
+                ("eig_iterations", C.c_int), ("seed", C.c_uint64), ("coarse_rtol", C.c_double),
+                ("coarse_maxit", C.c_int), ("coarse_n", C.c_int), ("precision", C.c_int)]
+
+
+class MgHierarchy:
+    """MgHierarchy<Prec> (solver.hpp:437-581) on the device: Chebyshev-Jacobi
+    smoothed V-cycle over the p/h ladder of `fine`, fp32 levels by default."""
+
+    def __init__(self, fine: FeLevel, model="inh", params: MaterialParams | None = None, strategy="none",
+                 degree=6, range_factor=15.0, safety=1.2, eig_iterations=20, coarse_rtol=1e-4, coarse_maxit=500,
+                 coarse_n=1, precision=32, seed=0x9E3779B97F4A7C15):
+        L = lib()
+        for name, (res, args) in {
+            "emfgpu_mg_default_config": (None, [C.POINTER(MgConfig)]),
+            "emfgpu_mg_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Material), C.c_int, C.POINTER(MgConfig),
+                                           C.POINTER(C.c_void_p)]),
+            "emfgpu_mg_destroy": (None, [C.c_void_p]),
+            "emfgpu_mg_n_levels": (C.c_int, [C.c_void_p]),
+            "emfgpu_mg_level_info": (C.c_int, [C.c_void_p, C.c_int] + [C.POINTER(C.c_int)] * 4 +
+                                     [C.POINTER(C.c_int64)]),
+            "emfgpu_mg_last_error": (C.c_char_p, [C.c_void_p]),
+            "emfgpu_mg_update_linearization": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+            "emfgpu_mg_precondition": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+            "emfgpu_pcg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                           C.POINTER(C.c_int), C.c_void_p, C.c_void_p]),
+        }.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        cfg = MgConfig()
+        L.emfgpu_mg_default_config(C.byref(cfg))
+        cfg.degree, cfg.range_factor, cfg.safety, cfg.eig_iterations = degree, range_factor, safety, eig_iterations
+        cfg.seed, cfg.coarse_rtol, cfg.coarse_maxit, cfg.coarse_n, cfg.precision = (seed, coarse_rtol, coarse_maxit,
+                                                                                   coarse_n, precision)
+        self.params = params or MaterialParams()
+        self._mat = self.params.to_c()
+        h = C.c_void_p()
+        st = L.emfgpu_mg_create(fine.h, MODELS[model], C.byref(self._mat), STRATEGIES[strategy], C.byref(cfg),
+                                C.byref(h))
+        if st:
+            raise EmfGpuError(st, L.emfgpu_global_last_error().decode())
+        self.h = h.value
+        self.fine = fine
+        self.n_levels = L.emfgpu_mg_n_levels(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_mg_destroy(self.h)
+            self.h = None
+
+    def levels(self):
+        out = []
+        for l in range(self.n_levels):
+            v = [C.c_int() for _ in range(4)]
+            nd = C.c_int64()
+            lib().emfgpu_mg_level_info(self.h, l, *[C.byref(x) for x in v], C.byref(nd))
+            out.append((v[0].value, v[1].value, v[2].value, v[3].value, nd.value))
+        return out
+
+    def _chk(self, st):
+        if st:
+            raise EmfGpuError(st, lib().emfgpu_mg_last_error(self.h).decode())
+
+    def update_linearization(self, d_u, stream=None):
+        self._chk(lib().emfgpu_mg_update_linearization(self.h, _ptr(d_u), _stream(stream)))
+
+    def precondition(self, d_r, d_z, stream=None):
+        self._chk(lib().emfgpu_mg_precondition(self.h, _ptr(d_r), _ptr(d_z), _stream(stream)))
+
+
+def pcg_solve(op: ElasticOperator, mg: MgHierarchy | None, d_b, d_x, rtol=1e-8, maxit=200, stream=None):
+    """Returns (iterations, relative residual history)."""
+    it = C.c_int()
+    hist = np.zeros(maxit + 1)
+    st = lib().emfgpu_pcg_solve(op.h, mg.h if mg is not None else None, _ptr(d_b), _ptr(d_x), rtol, maxit,
+                                C.byref(it), hist.ctypes.data, _stream(stream))
+    if st:
+        op._raise(st)
+    return it.value, hist[:it.value + 1]

@@ -104,7 +104,36 @@ def smoother():
     np.savez_compressed(os.path.join(OUT, "smoother.npz"), **out)
 
 
+def multigrid():
+    """MgHierarchy<float> V-cycle and an outer PCG (reference operator + the
+    reference V-cycle, coarse Jacobi-PCG path) on the well-posed cfg4 variant
+    (SURVEY §8(c') F4): iNH kappa/mu = 50, u0 = 0, affine cube."""
+    out = {}
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=KAPPA)
+    for tag, (lmax, p) in {"q2": (2, 2), "q4": (2, 4)}.items():
+        n = 1 << lmax
+        L = R.RefLevel(1, lmax, p, 0.0, 1)
+        u0 = np.zeros(L.ndofs)
+        mg = R.RefMg(L, "inh", prm, degree=5, coarse_direct_limit=0)
+        mg.update_linearization(u0)
+        r = I.make_v(L.ndofs, 11)
+        out[f"{tag}_r"] = r
+        out[f"{tag}_z"] = mg.precondition(r)
+        op = R.RefOperator(L, "inh", prm, "none", 64)
+        op.update_linearization(u0)
+        b = I.make_v(L.ndofs, 12)
+        b[I.dirichlet_mask(n, n, n, p, 1)] = 0.0
+        x, its, hist = R.pcg_solve(op, mg, b, 1e-8, 200)
+        out[f"{tag}_b"] = b
+        out[f"{tag}_x"] = x
+        out[f"{tag}_its"] = its
+        out[f"{tag}_hist"] = hist
+        print("mg", tag, mg.n_levels, "levels, pcg", its, "its")
+    np.savez_compressed(os.path.join(OUT, "multigrid.npz"), **out)
+
+
 if __name__ == "__main__":
+    multigrid()
     cfg0()
     small()
     transfers()

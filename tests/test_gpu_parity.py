@@ -70,6 +70,26 @@ def test_small_vs_reference(G, name, prec, strategy):
     assert rel(d, g[f"diag{prec}"]) <= TOL[prec], rel(d, g[f"diag{prec}"])
 
 
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("flags", [0, 1, 3])
+def test_affine_paths_all_degrees_vs_oracle(G, p, flags):
+    """Every degree through the diagonal-affine, general-affine and per-qp
+    geometry paths (element groups smaller than the 10 geometry factors)."""
+    from oracle import orcbind as O
+    n = 3
+    lev = G.FeLevel(n, p=p, flags=flags)
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    u0 = I.make_u0(n, n, n, p)
+    v = I.make_v(lev.n_dofs, 5)
+    orc = O.OracleOperator(n, n, n, p, lev.node_coords(), 1, "inh", prm.as_array(), "none", 64)
+    orc.update_linearization(u0)
+    yo = orc.apply(v)
+    for prec in (64, 32):
+        op = G.ElasticOperator(lev, "inh", prm, "none", prec)
+        op.update_linearization(u0)
+        assert rel(op.apply_tangent(v), yo) <= {64: 1e-12, 32: 1e-5}[prec]
+
+
 def test_geometry_matches_reference_jacobians(G):
     from oracle import orcbind as O
     g = np.load(os.path.join(GOLD, "inh_p2_n4_curved.npz"))
@@ -219,3 +239,32 @@ def test_split_apply_and_slab_emulation(G):
     y_split = np.concatenate([ys[0], ys[1][plane:]])
     assert np.array_equal(ys[0][-plane:], ys[1][:plane])
     assert np.array_equal(y_split, y_full)
+
+
+@pytest.mark.parametrize("tag,lmax,p", [("q2", 2, 2), ("q4", 2, 4)])
+def test_multigrid_vcycle_and_pcg_vs_reference(G, tag, lmax, p):
+    """fp32 hp-multigrid V-cycle (ladder, smoothers, transfers, Lanczos, coarse
+    CG) and the fp64 outer PCG against the reference's MgHierarchy<float> on
+    the well-posed cfg4 variant: CG iteration counts within +-1."""
+    import torch
+    g = np.load(os.path.join(GOLD, "multigrid.npz"))
+    n = 1 << lmax
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    lev = G.FeLevel(n, p=p)
+    mg = G.MgHierarchy(lev, "inh", prm, degree=5, coarse_n=1, precision=32)
+    assert mg.n_levels == {2: 4, 4: 5}[p]
+    u0 = torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda")
+    mg.update_linearization(u0)
+    r = torch.tensor(g[f"{tag}_r"], device="cuda")
+    z = torch.empty_like(r)
+    mg.precondition(r, z)
+    torch.cuda.synchronize()
+    assert rel(z.cpu().numpy(), g[f"{tag}_z"]) <= 1e-3
+    op = G.ElasticOperator(lev, "inh", prm, "none", 64)
+    op.update_linearization(np.zeros(lev.n_dofs))
+    b = torch.tensor(g[f"{tag}_b"], device="cuda")
+    x = torch.empty_like(b)
+    its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 200)
+    assert abs(its - int(g[f"{tag}_its"])) <= 1, (its, int(g[f"{tag}_its"]))
+    assert hist[-1] <= 1e-8
+    assert rel(x.cpu().numpy(), g[f"{tag}_x"]) <= 1e-6

@@ -149,3 +149,19 @@ def test_oracle_vs_live_reference_box_and_curved():
         orc = O.OracleOperator(4, 4, 4, 3, L.coords(), 1, model, prm, "tensor", 32)
         orc.update_linearization(u0)
         assert np.array_equal(ref.apply(v.astype(np.float32)), orc.apply(v.astype(np.float32)))
+
+
+def test_oracle_multigrid_and_pcg_bitexact():
+    """The C V-cycle / coarse CG / outer PCG against the reference's own
+    MgHierarchy<float> + PCG composed from reference primitives."""
+    g = np.load(os.path.join(GOLD, "multigrid.npz"))
+    prm = np.array([1.0, 10.0, 50.0, 2.0, 5.0, 3.62, 34.3, np.deg2rad(40), 1, 0, 0, 0, 1, 0, 0, 0, 1])
+    for tag, (lmax, p) in {"q2": (2, 2), "q4": (2, 4)}.items():
+        n = 1 << lmax
+        mg = O.OracleMg(1, lmax, p, "inh", prm, degree=5)
+        mg.update_linearization(np.zeros(g[f"{tag}_r"].size))
+        assert np.array_equal(mg.precondition(g[f"{tag}_r"]), g[f"{tag}_z"])
+        op = O.OracleOperator(n, n, n, p, model="inh", params=prm)
+        op.update_linearization(np.zeros(op.n))
+        x, its, hist = O.pcg_solve(op, mg, g[f"{tag}_b"], 1e-8, 200)
+        assert its == int(g[f"{tag}_its"]) and np.array_equal(x, g[f"{tag}_x"])
