@@ -40,23 +40,29 @@ MU, LAM = 1.0, 10.0
 # Algorithmic work per element: reference sweep structure
 # (8 forward + 9 transpose sweeps per component, u_k swept again when the
 # strategy reads it) + counted qp flops of the reference material pipeline.
-QP_FLOPS = {"cnh": {"none": 782, "scalar": 714, "tensor": 386, "cachedF": 746}}
+QP_FLOPS = {"cnh": {"none": 782, "scalar": 714, "tensor": 386, "cachedF": 746},
+            "inh": {"none": 852, "scalar": 748, "tensor": 408, "cachedF": 816},
+            "fiber": {"none": 1063, "scalar": 887, "tensor": 521, "cachedF": 1027}}
+# ledger apply traffic per qp, material domain, fp64, u_k row removed (ledger.cpp:22-76;
+# fibre scalar/tensor without the per-qp H4/H6 of a global frame)
+LEDGER = {"cnh": {"none": 72, "scalar": 80, "tensor": 320, "cachedF": 144},
+          "inh": {"none": 72, "scalar": 96, "tensor": 336, "cachedF": 144},
+          "fiber": {"none": 72, "scalar": 128, "tensor": 368, "cachedF": 144}}
 
 
-def flops_per_element(strategy, n=P + 1):
+def flops_per_element(strategy, n=P + 1, model="cnh"):
     reads_uk = strategy in ("none", "scalar")
     sf = (75 if reads_uk else 51) * n ** 3 * (2 * n - 1) + 9 * n ** 3
-    return sf + n ** 3 * QP_FLOPS["cnh"][strategy]
+    return sf + n ** 3 * QP_FLOPS[model][strategy]
 
 
-def bytes_per_apply(strategy, prec, ndofs, nel, affine=True):
+def bytes_per_apply(strategy, prec, ndofs, nel, n=P + 1, model="cnh"):
     """Algorithmic bytes (SURVEY.md §8(d) ledger minus the u_k row, u_k per DoF;
     geometry per qp is the yardstick even when stored per element)."""
     s = prec // 8
-    nq = nel * (P + 1) ** 3
-    ledger = {"none": 72, "scalar": 80, "tensor": 320, "cachedF": 144}[strategy]  # cNH, material, fp64
+    nq = nel * n ** 3
     k = 3 if strategy in ("none", "scalar") else 2
-    return ledger * s / 8 * nq + k * s * ndofs
+    return LEDGER[model][strategy] * s / 8 * nq + k * s * ndofs
 
 
 def read_peaks():
@@ -360,11 +366,92 @@ def run_gpu(args):
         "gpu_launches": launches,
         "clocks": sampler.summary() if sampler else None,
     }
+    if world == 1 and not args.no_extra:
+        line["workloads"] = run_extra_workloads(args, flush, fp64_peak, hbm)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_extra_workloads(args, flush, fp64_peak, hbm):
+    """BASELINE configs 2 and 4 on one GPU (variants documented in
+    paper_2408_12479_b200/workloads.py).  Reported beside the headline."""
+    import torch
+    from paper_2408_12479_b200 import emfgpu as G
+    from paper_2408_12479_b200 import workloads as W
+    out = {}
+    # cfg2: literal inputs must be rejected like the reference does
+    w = W.cfg2(literal=True)
+    lev = w.level()
+    op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
+    try:
+        op.update_linearization(w.u0())
+        out["cfg2_literal"] = {"admissible": True}
+    except G.NonPositiveJacobian as ex:
+        out["cfg2_literal"] = {"admissible": False, "first_bad_element": ex.element, "first_bad_qpoint": ex.qpoint}
+    del op
+    w = W.cfg2(literal=False)
+    u0, v = w.u0(), w.v()
+    rec2 = {"mesh": "64^3 Q4, x' = x + 0.1 sin(2 pi y) e_x (curved, per-qp J0)", "ndofs": lev.n_dofs,
+            "noise": w.noise, "affine": lev.affine}
+    for prec, strat in ((64, "none"), (64, "tensor"), (32, "none")):
+        op = G.ElasticOperator(lev, w.model, w.material(), strat, prec)
+        op.update_linearization(u0)
+        dt = torch.float64 if prec == 64 else torch.float32
+        x = torch.tensor(v, dtype=dt, device="cuda")
+        y = torch.empty_like(x)
+        for _ in range(3):
+            op.apply_tangent_device(x, y)
+        ms = []
+        for _ in range(max(3, args.steps // 4)):
+            flush.fill_(1.0)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+            op.apply_elements(x, 0, lev.nz)
+            e1.record()
+            op.apply_nodes(x, y, 0, lev.nz * lev.p)
+            e2.record()
+            ms.append((e0, e1, e2))
+        torch.cuda.synchronize()
+        t_all = sum(a.elapsed_time(c) for a, b, c in ms) / len(ms)
+        t_el = sum(a.elapsed_time(b) for a, b, c in ms) / len(ms)
+        fl = flops_per_element(strat, 5, "inh") * lev.n_elements
+        by = bytes_per_apply(strat, prec, lev.n_dofs, lev.n_elements, 5, "inh")
+        rec2[f"fp{prec}_{strat}"] = {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all,
+                                     "ms_element_kernel": t_el,
+                                     "fma_frac": fl / (t_el * 1e-3) / 1e12 / (fp64_peak if prec == 64 else
+                                                                                2 * fp64_peak),
+                                     "hbm_frac": by / (t_el * 1e-3) / 1e9 / hbm}
+        del op, x, y
+    out["cfg2"] = rec2
+    del lev
+    # cfg4 (well-posed variant): fp64 PCG + fp32 hp-MG V-cycle
+    w = W.cfg4(wellposed=True)
+    lev = w.level()
+    t0 = time.perf_counter()
+    op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
+    u0 = np.zeros(lev.n_dofs)
+    op.update_linearization(u0)
+    mg = G.MgHierarchy(lev, w.model, w.material(), degree=5, coarse_n=6, precision=32)
+    mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    b = torch.tensor(W.rhs(w), device="cuda")
+    x = torch.empty_like(b)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 300)
+    torch.cuda.synchronize()
+    t_solve = time.perf_counter() - t0
+    out["cfg4_wellposed"] = {"ndofs": lev.n_dofs, "levels": mg.levels(), "cg_iterations": its,
+                             "final_rel_residual": float(hist[-1]), "solve_s": t_solve,
+                             "ms_per_iteration": 1e3 * t_solve / max(its, 1), "setup_s": t_setup,
+                             "settings": "iNH kappa/mu=50, u0=0, affine 48^3 Q4; fp64 PCG rtol 1e-8; fp32 V-cycle "
+                                         "Q4->Q2->Q1->24^3->12^3->6^3, Chebyshev-Jacobi degree 5, coarse "
+                                         "Jacobi-PCG 1e-4"}
+    return out
 
 
 def main():
@@ -375,6 +462,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 / cfg4 workloads")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
