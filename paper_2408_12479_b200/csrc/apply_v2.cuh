@@ -99,10 +99,10 @@ __device__ __forceinline__ void cp_async_wait() {
 // (component c, line l).  M[row*N + col] are compile-time-indexed tables.
 
 // Forward x-sweep: in[c] -> tB[c] = Bx in, tD[c] = Dx in.
-template <typename T, int N>
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, const T* Dm, int w) {
   using L = Lay<N>;
-  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
     T u[N];
 #pragma unroll
@@ -122,11 +122,11 @@ __device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, con
 }
 
 // Forward y-sweep: sBB = By tB, sBD = Dy tB, sDB = By tD.
-template <typename T, int N>
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T* sdb,
                                      const T* Bm, const T* Dm, int w) {
   using L = Lay<N>;
-  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T ub[N], ud[N];
 #pragma unroll
@@ -151,11 +151,11 @@ __device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T
 }
 
 // Forward z-sweep: g[c][0] = Bz sDB, g[c][1] = Bz sBD, g[c][2] = Dz sBB.
-template <typename T, int N>
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T* g, const T* Bm,
                                      const T* Dm, int w) {
   using L = Lay<N>;
-  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T u0[N], u1[N], u2[N];
 #pragma unroll
@@ -181,10 +181,10 @@ __device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T
 }
 
 // Transposed z-sweep (node index along z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2.
-template <typename T, int N>
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* Dm, int w) {
   using L = Lay<N>;
-  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T u0[N], u1[N], u2[N];
 #pragma unroll
@@ -210,10 +210,10 @@ __device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* D
 }
 
 // Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
-template <typename T, int N>
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* Dm, int w) {
   using L = Lay<N>;
-  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T u0[N], u1[N], u2[N];
 #pragma unroll
@@ -238,10 +238,10 @@ __device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* D
 
 // Transposed x-sweep: out = Dx^T Q0 + Bx^T Q12, written as N contiguous
 // values of loc[(e*3 + c)*N3 + lexicographic m] (component-major).
-template <typename T, int N>
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T* Dm, int w) {
   using L = Lay<N>;
-  for (int wk = w; wk < 3 * L::N2; wk += (3 * L::N2 <= L::N3 ? 3 * L::N2 : L::N3)) {
+  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
     T u0[N], u1[N];
 #pragma unroll

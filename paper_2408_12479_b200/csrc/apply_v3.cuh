@@ -1,0 +1,255 @@
+// Tangent-apply element phase, v3: one warp per element (Q2, Q3).
+//
+// Each warp streams its own sequence of elements (persistent), so there is no
+// CTA-wide barrier anywhere: phases are separated by __syncwarp() and warps of
+// the same SM sit in different phases (sweeps vs quadrature-point algebra),
+// which keeps the FP64 pipe and the shared-memory pipe busy at the same time.
+// The next element's x / u_k / affine geometry are prefetched with cp.async
+// into the warp's single staging buffer as soon as the current element has
+// consumed it (after the first x-sweep of u_k).  A lane owns N3/32 quadrature
+// points (2 for Q3, 1 for Q2) and up to 2 sweep pencils.
+// Sweeps, layout, geometry paths and qp algebra are those of apply_v2.cuh.
+#pragma once
+#include "apply_v2.cuh"
+
+namespace emfgpu {
+
+template <typename T, int P, int MODEL, int STRAT>
+struct ApplyV3Warp {
+  static constexpr int N = P + 1, SZ = Lay<N>::SIZE;
+  static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR);
+  static constexpr int NST = kUk ? 6 : 3;
+  T stage[NST][SZ];
+  T geo[10];
+  T r1[9][SZ];
+  T r2[9][SZ];
+};
+
+constexpr int kV3Warps = 4;
+
+template <typename T>
+constexpr int minb_v3() {
+  return sizeof(T) == 8 ? 3 : 4;
+}
+
+template <typename T, int P, int MODEL, int STRAT, bool CART>
+__global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(const KArgs<T> a) {
+  using WS = ApplyV3Warp<T, P, MODEL, STRAT>;
+  constexpr int N = P + 1, N3 = N * N * N, SZ = Lay<N>::SIZE;
+  constexpr int QPL = (N3 + 31) / 32;  // quadrature points per lane
+  constexpr bool kUk = WS::kUk;
+  extern __shared__ __align__(16) unsigned char v3_smem[];  // kV3Warps * sizeof(WS), dynamic
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WS& sm = reinterpret_cast<WS*>(v3_smem)[warp];
+  T* const R1 = &sm.r1[0][0];
+  T* const R2 = &sm.r2[0][0];
+  const int64_t wstride = (int64_t)gridDim.x * kV3Warps;
+  const T* Bm = a.Bm;
+  const T* Dm = a.Dm;
+
+  // cp.async of element e's inputs into the staging buffer; `which` selects
+  // x (1), u_k (2) or both (3)
+  auto prefetch = [&](int64_t e, int which) {
+    if (e < a.nel) {
+#pragma unroll
+      for (int r = 0; r < QPL; ++r) {
+        const int q = lane + 32 * r;
+        if (q < N3) {
+          const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
+          const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
+          const int qs = lat<N>(qi, qj, qk);
+          if (which & 1)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[c][qs], a.x + 3 * ep.node + c);
+          if constexpr (kUk)
+            if (which & 2)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[3 + c][qs], a.uk + 3 * ep.node + c);
+        }
+      }
+      if ((which & 1) && a.affine && lane < 10) cp_async_T(&sm.geo[lane], a.geo + lane * a.geo_stride + e);
+    }
+    cp_async_commit();
+  };
+
+  int64_t e = (int64_t)blockIdx.x * kV3Warps + warp + a.e_begin;
+  prefetch(e, 3);
+  for (; e < a.nel; e += wstride) {
+    cp_async_wait<0>();
+    __syncwarp();
+    // Dirichlet columns of x are masked (operator.hpp:604-605)
+#pragma unroll
+    for (int r = 0; r < QPL; ++r) {
+      const int q = lane + 32 * r;
+      if (q < N3) {
+        const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
+        const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
+        if (node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces)) {
+          const int qs = lat<N>(qi, qj, qk);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) sm.stage[c][qs] = T(0);
+        }
+      }
+    }
+    // affine geometry to registers now: the staging buffer is refilled with
+    // the next element's data before the quadrature-point phase
+    T j0d[3], g9[9], det0 = T(0);
+    if (CART || a.affine) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) g9[m] = sm.geo[m];
+      j0d[0] = g9[0];
+      j0d[1] = g9[4];
+      j0d[2] = g9[8];
+      det0 = sm.geo[9];
+    }
+    __syncwarp();
+    // ---- gradient of x
+    fw_x<T, N, 32>(&sm.stage[0][0], R2, R2 + 3 * SZ, Bm, Dm, lane);
+    __syncwarp();
+    if constexpr (!kUk) prefetch(e + wstride, 1);
+    fw_y<T, N, 32>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, Bm, Dm, lane);
+    __syncwarp();
+    fw_z<T, N, 32>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, Bm, Dm, lane);
+    __syncwarp();
+    T gx[QPL][9];
+#pragma unroll
+    for (int r = 0; r < QPL; ++r) {
+      const int q = lane + 32 * r;
+      const int qs = q < N3 ? lat<N>(q % N, (q / N) % N, q / (N * N)) : 0;
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gx[r][m] = R2[m * SZ + qs];
+    }
+    if constexpr (kUk) {
+      __syncwarp();
+      fw_x<T, N, 32>(&sm.stage[3][0], R2, R2 + 3 * SZ, Bm, Dm, lane);
+      __syncwarp();
+      prefetch(e + wstride, 3);  // the staging buffer is free from here on
+      fw_y<T, N, 32>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, Bm, Dm, lane);
+      __syncwarp();
+      fw_z<T, N, 32>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, Bm, Dm, lane);
+      __syncwarp();
+    }
+    // ---- quadrature-point phase.  fp64: the points of a lane one after the
+    // other (interleaving them exceeds the register budget); fp32: unrolled so
+    // the two points' instruction streams interleave.
+    const T* cs = a.cache;
+    const int64_t st = a.cache_stride;
+    auto qp_point = [&](int r) {
+      const int q = lane + 32 * r;
+      if (q >= N3) return;
+      T gxr[9];
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gxr[m] = gx[0][m];
+      if constexpr (QPL > 1)
+        if (r == 1)
+#pragma unroll
+          for (int m = 0; m < 9; ++m) gxr[m] = gx[QPL > 1 ? 1 : 0][m];
+      const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
+      const int qs = lat<N>(qi, qj, qk);
+      const int64_t qidx = e * N3 + q;
+      T j0inv[9], detw;
+      if (CART) {
+        detw = det0 * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+      } else if (a.affine) {
+#pragma unroll
+        for (int m = 0; m < 9; ++m) j0inv[m] = g9[m];
+        detw = det0 * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+      } else {
+#pragma unroll
+        for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];
+        detw = a.geo[9 * a.geo_stride + qidx];
+      }
+      Bundle<T> cb;
+      if constexpr (kUk) {
+        T gk[9], gg[9];
+#pragma unroll
+        for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+        if constexpr (CART) {
+#pragma unroll
+          for (int m = 0; m < 9; ++m) gg[m] = gk[m] * j0d[m % 3];
+        } else {
+          mm(gk, j0inv, gg);
+        }
+        if (!make_strain(gg, cb)) atomicMin(a.err, (unsigned long long)qidx);
+        if constexpr (STRAT == S_NONE) {
+          cache_scalars<T, MODEL>(a.mat, cb);
+        } else {
+          if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
+          else {
+            cb.jp = cs[C_JP * st + qidx];
+            cb.c1 = cs[C_C1 * st + qidx];
+            cb.c2 = cs[C_C2 * st + qidx];
+          }
+          if (MODEL == FIBER) {
+            cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
+            cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
+            cb.efib[0] = cs[(C_EF + 0) * st + qidx];
+            cb.efib[1] = cs[(C_EF + 1) * st + qidx];
+          }
+        }
+        second_pk<T, MODEL>(a.mat, cb);
+      } else if constexpr (STRAT == S_CACHEDF) {
+        T gg[9];
+#pragma unroll
+        for (int m = 0; m < 9; ++m) gg[m] = cs[(C_G + m) * st + qidx];
+        if (!make_strain(gg, cb)) atomicMin(a.err, (unsigned long long)qidx);
+        cache_scalars<T, MODEL>(a.mat, cb);
+        second_pk<T, MODEL>(a.mat, cb);
+      } else {  // S_TENSOR
+        if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
+        else {
+          cb.jp = cs[C_JP * st + qidx];
+          cb.c1 = cs[C_C1 * st + qidx];
+          cb.c2 = cs[C_C2 * st + qidx];
+        }
+        if (MODEL == FIBER) {
+          cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
+          cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
+          cb.efib[0] = cs[(C_EF + 0) * st + qidx];
+          cb.efib[1] = cs[(C_EF + 1) * st + qidx];
+        }
+#pragma unroll
+        for (int m = 0; m < 9; ++m) {
+          cb.F[m] = cs[(C_F + m) * st + qidx];
+          cb.Finv[m] = cs[(C_FINV + m) * st + qidx];
+        }
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+          cb.S[m] = cs[(C_S + m) * st + qidx];
+          cb.Cinv[m] = cs[(C_CINV + m) * st + qidx];
+        }
+      }
+      T wv[9];
+      if constexpr (CART) {
+        T dg[9], wm[9];
+#pragma unroll
+        for (int m = 0; m < 9; ++m) dg[m] = gxr[m] * j0d[m % 3];
+        tangent_wm<T, MODEL>(a.mat, cb, dg, wm);
+#pragma unroll
+        for (int m = 0; m < 9; ++m) wv[m] = wm[m] * (detw * j0d[m % 3]);
+      } else {
+        tangent_integrand<T, MODEL>(a.mat, cb, gxr, j0inv, detw, wv);
+      }
+#pragma unroll
+      for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];
+    };
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int r = 0; r < QPL; ++r) qp_point(r);
+    } else {
+#pragma unroll 1
+      for (int r = 0; r < QPL; ++r) qp_point(r);
+    }
+    __syncwarp();
+    // ---- test with the gradients of the basis functions
+    tr_z<T, N, 32>(R1, R2, Bm, Dm, lane);
+    __syncwarp();
+    tr_y<T, N, 32>(R2, R1, Bm, Dm, lane);
+    __syncwarp();
+    tr_x<T, N, 32>(R1, a.loc + e * 3 * N3, Bm, Dm, lane);
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace emfgpu

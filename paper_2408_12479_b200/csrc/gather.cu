@@ -49,48 +49,47 @@ __device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bo
   return 1;
 }
 
-template <typename T>
-__global__ void node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
-                                   const T* __restrict__ ghost_hi, const T* x, T* y,
-                                   int nx, int ny, int nz, int p, int faces, int kpar, int c0, int c1) {
-  const int mx = nx * p + 1, my = ny * p + 1, mz = nz * p + 1;
-  const int64_t plane = (int64_t)mx * my;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + (int64_t)c0 * plane;
-  if (idx >= (int64_t)(c1 + 1) * plane) return;
-  const int a = (int)(idx % mx);
-  const int b = (int)((idx / mx) % my);
-  const int c = (int)(idx / plane);
+// One thread per lattice node; 3-D grid (x: 32 nodes along a, y: 8 along b,
+// z: node planes) so no index division is needed.
+template <typename T, int P>
+__global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
+                                                          const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
+                                                          int ny, int nz, int faces, int kpar, int c0) {
+  constexpr int N = P + 1, N3 = N * N * N, N2 = N * N;
+  const int mx = nx * P + 1, my = ny * P + 1, mz = nz * P + 1;
+  const int a = blockIdx.x * 32 + threadIdx.x;
+  const int b = blockIdx.y * 8 + threadIdx.y;
+  const int c = blockIdx.z + c0;
+  if (a >= mx || b >= my) return;
+  const int64_t idx = ((int64_t)c * my + b) * mx + a;
   if (node_constrained(a, b, c, mx, my, mz, faces)) {
     y[3 * idx] = x[3 * idx];
     y[3 * idx + 1] = x[3 * idx + 1];
     y[3 * idx + 2] = x[3 * idx + 2];
     return;
   }
-  const int N = p + 1, N3 = N * N * N, N2 = N * N;
   int ie[2], il[2], je[2], jl[2], ke[2], kl[2];
-  const int ni = axis_candidates(a, p, nx, 0, false, ie, il);
-  const int nj = axis_candidates(b, p, ny, 0, false, je, jl);
+  const int ni = axis_candidates(a, P, nx, 0, false, ie, il);
+  const int nj = axis_candidates(b, P, ny, 0, false, je, jl);
   const bool ghosts = ghost_lo != nullptr || ghost_hi != nullptr;
-  int nk = axis_candidates(c, p, nz, kpar, ghosts, ke, kl);
+  const int nk = axis_candidates(c, P, nz, kpar, ghosts, ke, kl);
   T s0 = T(0), s1 = T(0), s2 = T(0);
   bool first = true;
   for (int tk = 0; tk < nk; ++tk) {
     const int k = ke[tk];
-    const T* src;
     for (int tj = 0; tj < nj; ++tj)
       for (int ti = 0; ti < ni; ++ti) {
-        int64_t off;
         T v0, v1, v2;
         if (k < 0 || k >= nz) {
-          src = k < 0 ? ghost_lo : ghost_hi;
+          const T* src = k < 0 ? ghost_lo : ghost_hi;
           if (!src) continue;
-          off = ((((int64_t)je[tj] * nx + ie[ti]) * N2) + jl[tj] * N + il[ti]) * 3;
+          const int64_t off = ((((int64_t)je[tj] * nx + ie[ti]) * N2) + jl[tj] * N + il[ti]) * 3;
           v0 = src[off];
           v1 = src[off + 1];
           v2 = src[off + 2];
         } else {  // element-local results, component-major loc[(e*3 + c)*N3 + m]
           const int64_t e = ((int64_t)k * ny + je[tj]) * nx + ie[ti];
-          off = e * 3 * N3 + (kl[tk] * N + jl[tj]) * N + il[ti];
+          const int64_t off = e * 3 * N3 + (kl[tk] * N + jl[tj]) * N + il[ti];
           v0 = loc[off];
           v1 = loc[off + N3];
           v2 = loc[off + 2 * N3];
@@ -115,12 +114,20 @@ __global__ void node_gather_kernel(const T* __restrict__ loc, const T* __restric
 template <typename T>
 void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny, int nz,
                         int p, int faces, int kpar, int c0, int c1, cudaStream_t s) {
-  const int64_t plane = (int64_t)(nx * p + 1) * (ny * p + 1);
-  const int64_t cnt = (int64_t)(c1 - c0 + 1) * plane;
-  if (cnt <= 0) return;
-  const int bs = 256;
-  node_gather_kernel<T><<<(unsigned)((cnt + bs - 1) / bs), bs, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, p,
-                                                                        faces, kpar, c0, c1);
+  if (c1 < c0) return;
+  const int mx = nx * p + 1, my = ny * p + 1;
+  const dim3 grid((mx + 31) / 32, (my + 7) / 8, c1 - c0 + 1), block(32, 8);
+  switch (p) {
+#define EMF_G(PP)                                                                                             \
+  case PP:                                                                                                    \
+    node_gather_kernel<T, PP><<<grid, block, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, faces, kpar, c0); \
+    break;
+    EMF_G(1)
+    EMF_G(2)
+    EMF_G(3)
+    EMF_G(4)
+#undef EMF_G
+  }
 }
 
 // Face of element layer k: lower (side 0, local c=0) or upper (side 1, c=p)

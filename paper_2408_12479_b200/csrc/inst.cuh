@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "apply_v2.cuh"
+#include "apply_v3.cuh"
 #include "internal.h"
 
 namespace emfgpu {
@@ -13,6 +14,33 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P>::EPB, THREADS = EPB * N * N * N;
   const int64_t cnt = e1 - e0;
   if (cnt <= 0) return;
+  // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):
+  // warp-per-element (v3) for fp32 and for the fp64 strategies without u_k
+  // sweeps; 2 elements per CTA with named barriers (v2) for fp64 none/scalar.
+  constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) &&
+                       (sizeof(EMF_T) == 4 || STRAT == S_CACHEDF || STRAT == S_TENSOR);
+  if constexpr (kV3) {
+    // warp-per-element kernel (apply_v3.cuh)
+    constexpr size_t smem = sizeof(ApplyV3Warp<EMF_T, EMF_P, MODEL, STRAT>) * kV3Warps;
+    static int per_sm3 = 0, sms3 = 0;
+    if (per_sm3 == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms3, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>,
+                                                    32 * kV3Warps, smem);
+      if (per_sm3 < 1) per_sm3 = 1;
+    }
+    KArgs<EMF_T> b = a;
+    b.e_begin = e0;
+    b.nel = e1;
+    const int64_t blocks = (cnt + kV3Warps - 1) / kV3Warps;
+    const int64_t grid = std::min<int64_t>(blocks, (int64_t)sms3 * per_sm3);
+    apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART><<<(unsigned)grid, 32 * kV3Warps, smem, s>>>(b);
+    return;
+  }
   // persistent grid: one wave at the kernel's occupancy
   static int per_sm = 0, sms = 0;
   if (per_sm == 0) {
