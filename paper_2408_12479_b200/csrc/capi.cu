@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -157,6 +158,10 @@ MatConst<T> mat_const(const emfgpu_material& p, const double h[2][6], const doub
   m.kappa = T(p.kappa_b);
   m.k2 = T(p.k2);
   m.two_k1 = T(2.0 * p.k1);
+  // the reference evaluates mu/3, 2mu/9, 2mu/3 in Number (constitutive.hpp:349-352, 404)
+  m.mu_3 = T(p.mu) / T(3);
+  m.two_mu_9 = (T(2) * T(p.mu)) / T(9);
+  m.two_mu_3 = (T(2) * T(p.mu)) / T(3);
   for (int f = 0; f < 2; ++f) {
     for (int k = 0; k < 6; ++k) m.h[f][k] = T(h[f][k]);
     for (int k = 0; k < 3; ++k) m.m1[f][k] = T(m1[f][k]);
@@ -662,7 +667,12 @@ static void apply_host_pipelined(emfgpu_op* op, const void* x, void* y) {
       CK(cudaEventCreateWithFlags(&op->ev_comp[i], cudaEventDisableTiming));
     }
   }
-  const int nch = std::min(emfgpu_op::kMaxChunks, std::max(1, L->nz / 4));
+  static const int env_chunks = [] {
+    const char* e = std::getenv("EMFGPU_E2E_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int want = env_chunks > 0 ? env_chunks : std::max(1, L->nz / 4);
+  const int nch = std::min(std::min(emfgpu_op::kMaxChunks, L->nz), want);
   const int per = (L->nz + nch - 1) / nch;
   CK(cudaEventRecord(op->ev_start, op->stream));
   CK(cudaStreamWaitEvent(op->s_h2d, op->ev_start, 0));

@@ -29,6 +29,7 @@ enum Strategy : int { S_NONE = 0, S_SCALAR = 1, S_TENSOR = 2, S_CACHEDF = 3 };
 template <typename T>
 struct MatConst {
   T mu, lam, half_k, kappa, k2, two_k1;
+  T mu_3, two_mu_9, two_mu_3;  // mu/3, 2 mu/9, 2 mu/3 (host-rounded once, not divided per point)
   T h[2][6];   // structure tensors H4, H6 (material.cpp:50-82)
   T m1[2][3];  // mean fibre directions
 };
@@ -45,6 +46,31 @@ template <>
 __device__ __forceinline__ double dexp<double>(double x) { return exp(x); }
 template <>
 __device__ __forceinline__ float dexp<float>(float x) { return expf(x); }
+
+// Reciprocal without the IEEE-division slow path: MUFU approximation refined
+// by Newton steps (2 for fp64: ~full precision; |1/x - rcp(x)| <= 1 ulp class).
+// Used for 1/det(F) and y = x/(2+x), whose arguments are bounded away from
+// 0 and infinity on admissible states.
+template <typename T>
+__device__ __forceinline__ T fast_rcp(T x);
+template <>
+__device__ __forceinline__ double fast_rcp<double>(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+template <>
+__device__ __forceinline__ float fast_rcp<float>(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  const float e = fmaf(-x, r, 1.0f);
+  return fmaf(r, e, r);
+}
 
 // SymTensor order (11,22,33,12,13,23), tensor.hpp:93-100.
 __host__ __device__ constexpr int sidx(int i, int j) { return i == j ? i : 2 + i + j; }
@@ -66,7 +92,7 @@ __device__ __forceinline__ T det_minus_one(const T* g) {
 // Adjugate / determinant (tensor.hpp:212-231).
 template <typename T>
 __device__ __forceinline__ void inverse3(const T* t, T* r) {
-  const T inv = T(1) / det3(t);
+  const T inv = fast_rcp(det3(t));
   r[0] = (t[4] * t[8] - t[5] * t[7]) * inv;
   r[1] = (t[2] * t[7] - t[1] * t[8]) * inv;
   r[2] = (t[1] * t[5] - t[2] * t[4]) * inv;
@@ -139,7 +165,7 @@ __device__ __forceinline__ T ddot_s(const T* x, const T* y) {
 template <typename T>
 __device__ __forceinline__ T ln_plus_one(T x) {
   if (fabs(x) > T(0.5)) return dlog1p(x);
-  const T y = x / (T(2) + x);
+  const T y = x * fast_rcp(T(2) + x);
   const T y2 = y * y;
   T s = T(1.0 / 31.0);
 #pragma unroll
@@ -206,8 +232,8 @@ __device__ __forceinline__ void cache_scalars(const MatConst<T>& m, Bundle<T>& c
   c.jp = MODEL == CNH ? T(1) : fast_jpow(c.jm1);
   if (MODEL != CNH) {
     const T jac = T(1) + c.jm1;
-    c.c1 = m.half_k * (c.jm1 * (c.jm1 + T(2))) - ((m.mu / T(3)) * c.jp) * i1;
-    c.c2 = (((T(2) * m.mu) / T(9)) * c.jp) * i1 + (m.kappa * jac) * jac;
+    c.c1 = m.half_k * (c.jm1 * (c.jm1 + T(2))) - (m.mu_3 * c.jp) * i1;
+    c.c2 = (m.two_mu_9 * c.jp) * i1 + (m.kappa * jac) * jac;
   }
   if (MODEL == FIBER) {
 #pragma unroll
@@ -284,7 +310,7 @@ __device__ __forceinline__ void tangent_material(const MatConst<T>& m, const Bun
   T q = c.F[0] * dg[0];
 #pragma unroll
   for (int i = 1; i < 9; ++i) q += c.F[i] * dg[i];
-  const T ttmj = ((T(2) * m.mu) / T(3)) * c.jp;
+  const T ttmj = m.two_mu_3 * c.jp;
   const T m2c1 = T(-2) * c.c1;
   const T f2 = c.c2 * w - ttmj * q;
 #pragma unroll
@@ -345,7 +371,7 @@ __device__ __forceinline__ void tangent_wm(const MatConst<T>& m, const Bundle<T>
       T q = c.F[0] * dg[0];
 #pragma unroll
       for (int i = 1; i < 9; ++i) q += c.F[i] * dg[i];
-      const T t = ((T(2) * m.mu) / T(3)) * c.jp;
+      const T t = m.two_mu_3 * c.jp;
       h = -c.c1;
       g2 = c.c2 * trA - t * q;
     }
@@ -357,7 +383,7 @@ __device__ __forceinline__ void tangent_wm(const MatConst<T>& m, const Bundle<T>
 #pragma unroll
       for (int j = 0; j < 3; ++j) wm[3 * i + j] += h * AF[3 * j + i] + g2 * c.Finv[3 * j + i];
     if constexpr (MODEL == INH) {
-      const T tw = -(((T(2) * m.mu) / T(3)) * c.jp) * trA;
+      const T tw = -(m.two_mu_3 * c.jp) * trA;
 #pragma unroll
       for (int k = 0; k < 9; ++k) wm[k] += tw * c.F[k];
     }
