@@ -427,6 +427,42 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
         del op, x, y
     out["cfg2"] = rec2
     del lev
+    # cfg3: fibre tube with per-qp cylindrical frames, tensor strategy
+    w = W.cfg3()
+    lev = w.level()
+    u0 = W.tube_u0(w, lev.node_coords())
+    v = w.v()
+    rec3 = {"mesh": "tube r=[1,1.3] L=10, 16x128x256 Q3, periodic theta, per-qp fibre frames",
+            "ndofs": lev.n_dofs}
+    for prec in (64, 32):
+        op = G.ElasticOperator(lev, "fiber", w.material(), "tensor", prec)
+        op.set_fibre_frame("cylindrical")
+        op.update_linearization(u0)
+        dt = torch.float64 if prec == 64 else torch.float32
+        x = torch.tensor(v, dtype=dt, device="cuda")
+        y = torch.empty_like(x)
+        for _ in range(3):
+            op.apply_tangent_device(x, y)
+        ms = []
+        for _ in range(max(3, args.steps // 4)):
+            flush.fill_(1.0)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+            op.apply_elements(x, 0, lev.nz)
+            e1.record()
+            op.apply_nodes(x, y, 0, lev.nz * lev.p)
+            e2.record()
+            ms.append((e0, e1, e2))
+        torch.cuda.synchronize()
+        t_all = sum(a.elapsed_time(c) for a, b, c in ms) / len(ms)
+        t_el = sum(a.elapsed_time(b) for a, b, c in ms) / len(ms)
+        nq = lev.n_elements * 64
+        by = (LEDGER["fiber"]["tensor"] + 96) * (prec // 8) / 8 * nq + 2 * (prec // 8) * lev.n_dofs  # + per-qp H4/H6
+        rec3[f"fp{prec}_tensor"] = {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all,
+                                    "ms_element_kernel": t_el, "hbm_frac": by / (t_el * 1e-3) / 1e9 / hbm}
+        del op, x, y
+    out["cfg3"] = rec3
+    del lev
     # cfg4 (well-posed variant): fp64 PCG + fp32 hp-MG V-cycle
     w = W.cfg4(wellposed=True)
     lev = w.level()

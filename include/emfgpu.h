@@ -49,7 +49,9 @@ typedef enum emfgpu_strategy {
 typedef enum emfgpu_map {
   EMFGPU_MAP_REFERENCE = 0, /* DeformMap, mesh.cpp:128-136: param[0] = amplitude */
   EMFGPU_MAP_SHEAR_X = 1,   /* x' = x + param[0] sin(2 pi y) e_x (BASELINE cfg2) */
-  EMFGPU_MAP_COORDS = 2     /* node coordinates given in emfgpu_level_desc.coords */
+  EMFGPU_MAP_COORDS = 2,    /* node coordinates given in emfgpu_level_desc.coords */
+  EMFGPU_MAP_TUBE = 3       /* BASELINE cfg3: x = radial, y = theta (use EMFGPU_LEVEL_PERIODIC_Y),
+                               z = axial; param = {r_inner, r_outer, length} */
 } emfgpu_map;
 
 /* FeLevel(HexMesh, degree, DeformMap) + set_dirichlet, mesh.hpp:71-138.
@@ -69,6 +71,7 @@ typedef struct emfgpu_level_desc {
 } emfgpu_level_desc;
 #define EMFGPU_LEVEL_NO_CARTESIAN 1 /* use the general J0^-1 products even if J0 is diagonal */
 #define EMFGPU_LEVEL_NO_AFFINE 2    /* store geometry per quadrature point even if affine */
+#define EMFGPU_LEVEL_PERIODIC_Y 4   /* periodic lattice in y (my = ny*p; ny even) */
 
 /* MaterialParams, material.hpp:36-50 (phi in radians; e1,e2,e3 frame). */
 typedef struct emfgpu_material {
@@ -211,6 +214,15 @@ emfgpu_status emfgpu_mg_precondition(emfgpu_mg* mg, const double* d_r, double* d
  * mg may be NULL (unpreconditioned).  history (host, maxit+1) optional. */
 emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double rtol,
                                int maxit, int* iterations, double* history, void* stream);
+
+/* Fibre model with a per-quadrature-point frame field (SURVEY §8(c) gap 2):
+ * kind 0 = the global frame of the material (default), 1 = cylindrical frame
+ * about the z axis at each qp (e1 circumferential, e2 axial, e3 radial; the
+ * families at +-phi from e1), 2 = the material's frame replicated per qp.
+ * Call before update_linearization. */
+emfgpu_status emfgpu_op_set_fibre_frame(emfgpu_op* op, int kind);
+/* Per-qp H4,H6 (12 per qp, SoA field-major) and M1_4,M1_6 (6 per qp). */
+emfgpu_status emfgpu_op_fibre_field(const emfgpu_op* op, double* h_out, double* m1_out);
 
 /* FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured by a register-resident
  * FMA loop over one wave of CTAs for `seconds`: the FP64/FP32 roofline

@@ -58,8 +58,24 @@ typedef struct orc_op {
   uint8_t* mask;    /* ndofs, owned */
   double* uk;       /* ndofs, owned */
   double* cache;    /* nel*nq3*ORC_CACHE_STRIDE when strategy != none */
+  double* hq;       /* optional per-qp H4,H6 (12 fields, SoA) */
+  double* m1q;      /* optional per-qp M1_4,M1_6 (6 fields, SoA) */
   int linearized;
 } orc_op;
+
+/* EXT (SURVEY §8(c) gap 2): fibre structure tensors per quadrature point.
+ * Without a frame field this is the operator's constant material. */
+static orc_material orc_mat_at(const orc_op* op, int64_t at) {
+  orc_material m = op->mat;
+  if (op->hq) {
+    const int64_t st = op->nel * op->nq3;
+    for (int f = 0; f < 2; ++f) {
+      for (int k = 0; k < 6; ++k) m.h[f][k] = op->hq[(6 * f + k) * st + at];
+      for (int k = 0; k < 3; ++k) m.m1[f][k] = op->m1q[(3 * f + k) * st + at];
+    }
+  }
+  return m;
+}
 
 /* ---- quadrature / basis: mesh.cpp:14-120 ------------------------------- */
 static const double kPi = 3.14159265358979323846;
@@ -442,6 +458,8 @@ orc_op* orc_op_create(int nx, int ny, int nz, int p, const double* coords, int f
 
 void orc_op_destroy(orc_op* op) {
   if (!op) return;
+  free(op->hq);
+  free(op->m1q);
   free(op->jac);
   free(op->mask);
   free(op->uk);
@@ -480,11 +498,12 @@ int orc_op_linearize(orc_op* op, const double* u, int64_t* bad_e, int* bad_q) {
         }
         mm_d(gref, j0inv, gk);
         qpc_d c;
-        if (compute_cache_d(&op->mat, gk, &c)) {
+        const orc_material mq = orc_mat_at(op, at);
+        if (compute_cache_d(&mq, gk, &c)) {
           if (at < first) first = at;
           continue;
         }
-        second_pk_d(&op->mat, &c, c.S);
+        second_pk_d(&mq, &c, c.S);
         if (op->cache) {
           double* sc = op->cache + at * ORC_CACHE_STRIDE;
           sc[ORC_C_LNJ] = c.lnj;
@@ -1027,4 +1046,16 @@ int orc_pcg_solve(const orc_op* op, orc_mg* m, const double* b, double* x, doubl
   free(pv);
   free(ap);
   return err;
+}
+
+/* Per-qp fibre frame field: h (12*nqp, SoA H4,H6) and m1 (6*nqp, SoA). */
+void orc_op_set_frames(orc_op* op, const double* h, const double* m1) {
+  const int64_t nqp = op->nel * op->nq3;
+  free(op->hq);
+  free(op->m1q);
+  op->hq = (double*)malloc(sizeof(double) * 12 * nqp);
+  op->m1q = (double*)malloc(sizeof(double) * 6 * nqp);
+  memcpy(op->hq, h, sizeof(double) * 12 * nqp);
+  memcpy(op->m1q, m1, sizeof(double) * 6 * nqp);
+  op->linearized = 0;
 }

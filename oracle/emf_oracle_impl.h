@@ -346,6 +346,7 @@ static void SFX(scatter_grad)(const orc_basis* b, const R* g0, const R* g1, cons
  * active strategy. gk = Grad u_k (reference gradient times J0^-1). */
 static int SFX(bundle)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)* c) {
   const int64_t at = e * op->nq3 + q;
+  const orc_material mq = orc_mat_at(op, at);
   if (op->strategy == ORC_TENSOR || op->strategy == ORC_SCALAR) {
     const double* sc = op->cache + at * ORC_CACHE_STRIDE;
     c->lnj = (R)sc[ORC_C_LNJ];
@@ -375,7 +376,7 @@ static int SFX(bundle)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)
     }
     /* scalar: strain tensors recomputed from G_k, scalars from storage */
     SFX(qpc) s;
-    if (SFX(compute_cache)(&op->mat, gk, &s)) return 1;
+    if (SFX(compute_cache)(&mq, gk, &s)) return 1;
     c->jm1 = s.jm1; /* second_pk_base reads J-1 from the strain state */
     for (int k = 0; k < 9; ++k) {
       c->F[k] = s.F[k];
@@ -385,11 +386,11 @@ static int SFX(bundle)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)
       c->Cinv[k] = s.Cinv[k];
       c->E[k] = s.E[k];
     }
-    SFX(second_pk)(&op->mat, c, c->S);
+    SFX(second_pk)(&mq, c, c->S);
     return 0;
   }
-  if (SFX(compute_cache)(&op->mat, gk, c)) return 1;
-  SFX(second_pk)(&op->mat, c, c->S);
+  if (SFX(compute_cache)(&mq, gk, c)) return 1;
+  SFX(second_pk)(&mq, c, c->S);
   return 0;
 }
 
@@ -443,7 +444,8 @@ static int SFX(element_tangent)(const orc_op* op, int64_t e, const R* input, con
     }
     SFX(qpc) cache;
     if (SFX(bundle)(op, e, q, gk, &cache)) return 1;
-    SFX(tangent_material)(&op->mat, &cache, dg, ds);
+    const orc_material mq = orc_mat_at(op, e * op->nq3 + q);
+    SFX(tangent_material)(&mq, &cache, dg, ds);
     SFX(mm_ts)(dg, cache.S, t1);
     SFX(mm_ts)(cache.F, ds, t2);
     for (int k = 0; k < 9; ++k) wm[k] = t1[k] + t2[k];
@@ -572,7 +574,8 @@ static int SFX(diagonal)(const orc_op* op, R* diag, int64_t* n_bad) {
             for (int c = 0; c < 3; ++c)
               for (int d = 0; d < 3; ++d) gref[3 * c + d] = s->g[c][d][q];
             SFX(mm)(gref, j0inv + 9 * q, dg);
-            SFX(tangent_material)(&op->mat, &bundles[q], dg, ds);
+            const orc_material mq = orc_mat_at(op, e * op->nq3 + q);
+            SFX(tangent_material)(&mq, &bundles[q], dg, ds);
             SFX(mm_ts)(dg, bundles[q].S, t1);
             SFX(mm_ts)(bundles[q].F, ds, t2);
             for (int k2 = 0; k2 < 9; ++k2) wm[k2] = t1[k2] + t2[k2];

@@ -44,6 +44,7 @@ def lib():
         L.orc_lattice_coords.argtypes = [C.c_int] * 4 + [vp, C.c_int, vp, vp]
         L.orc_structure_tensors.argtypes = [vp, vp]
         L.orc_op_element_locals.argtypes = [vp, vp, vp, i64, i64]
+        L.orc_op_set_frames.argtypes = [vp, vp, vp]
         L.orc_basis_tables.argtypes = [C.c_int] + [vp] * 5
         _lib = L
     return _lib
@@ -128,6 +129,12 @@ class OracleOperator:
         if st:
             raise OracleError(st)
         return y
+
+    def set_frames(self, h, m1):
+        """Per-qp fibre frame field (12*nqp H4,H6 and 6*nqp M1s, SoA); EXT of the reference."""
+        h = np.ascontiguousarray(h, np.float64)
+        m1 = np.ascontiguousarray(m1, np.float64)
+        lib().orc_op_set_frames(self.h, _p(h), _p(m1))
 
     def element_locals(self, x, e0, e1):
         """Element-local results (before scatter) of elements [e0, e1): (e1-e0, nn3, 3)."""

@@ -55,6 +55,7 @@ __device__ __forceinline__ ElemPos elem_pos_fast(int64_t e64, const A& a, int i,
   p.ek = (int)ek;
   p.ga = p.ei * P + i;
   p.gb = p.ej * P + j;
+  if (p.gb >= a.my) p.gb -= a.my;  // periodic y lattice
   p.gc = p.ek * P + k;
   p.node = ((int64_t)p.gc * a.my + p.gb) * a.mx + p.ga;
   return p;
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     }
     // per-qp geometry / cache loads are issued before the sweeps
     const int64_t qidx = (valid ? e : a.e_begin) * N3 + q;
+    const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
     T j0inv[9], detw;
     if (!CART && !a.affine) {
 #pragma unroll
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       }
       if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
       if constexpr (STRAT == S_NONE) {
-        cache_scalars<T, MODEL>(a.mat, cb);
+        cache_scalars<T, MODEL>(mq, cb);
       } else {
         if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
         else {
@@ -421,14 +423,14 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
           cb.efib[1] = cs[(C_EF + 1) * st + qidx];
         }
       }
-      second_pk<T, MODEL>(a.mat, cb);
+      second_pk<T, MODEL>(mq, cb);
     } else if constexpr (STRAT == S_CACHEDF) {
       T gg[9];
 #pragma unroll
       for (int m = 0; m < 9; ++m) gg[m] = cs[(C_G + m) * st + qidx];
       if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
-      cache_scalars<T, MODEL>(a.mat, cb);
-      second_pk<T, MODEL>(a.mat, cb);
+      cache_scalars<T, MODEL>(mq, cb);
+      second_pk<T, MODEL>(mq, cb);
     } else {  // S_TENSOR
       if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
       else {
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       T dg[9], wm[9];
 #pragma unroll
       for (int m = 0; m < 9; ++m) dg[m] = gx[m] * j0inv[4 * (m % 3)];
-      tangent_wm<T, MODEL>(a.mat, cb, dg, wm);
+      tangent_wm<T, MODEL>(mq, cb, dg, wm);
       const T s0 = detw * j0inv[0], s1 = detw * j0inv[4], s2 = detw * j0inv[8];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
         wv[3 * c + 2] = wm[3 * c + 2] * s2;
       }
     } else
-      tangent_integrand<T, MODEL>(a.mat, cb, gx, j0inv, detw, wv);
+      tangent_integrand<T, MODEL>(mq, cb, gx, j0inv, detw, wv);
     // ---- test with the gradients of the basis functions
 #pragma unroll
     for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];

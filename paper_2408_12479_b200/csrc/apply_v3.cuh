@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
       const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
       const int qs = lat<N>(qi, qj, qk);
       const int64_t qidx = e * N3 + q;
+      const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
       T j0inv[9], detw;
       if (CART) {
         detw = det0 * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
         }
         if (!make_strain(gg, cb)) atomicMin(a.err, (unsigned long long)qidx);
         if constexpr (STRAT == S_NONE) {
-          cache_scalars<T, MODEL>(a.mat, cb);
+          cache_scalars<T, MODEL>(mq, cb);
         } else {
           if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
           else {
@@ -187,14 +188,14 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
             cb.efib[1] = cs[(C_EF + 1) * st + qidx];
           }
         }
-        second_pk<T, MODEL>(a.mat, cb);
+        second_pk<T, MODEL>(mq, cb);
       } else if constexpr (STRAT == S_CACHEDF) {
         T gg[9];
 #pragma unroll
         for (int m = 0; m < 9; ++m) gg[m] = cs[(C_G + m) * st + qidx];
         if (!make_strain(gg, cb)) atomicMin(a.err, (unsigned long long)qidx);
-        cache_scalars<T, MODEL>(a.mat, cb);
-        second_pk<T, MODEL>(a.mat, cb);
+        cache_scalars<T, MODEL>(mq, cb);
+        second_pk<T, MODEL>(mq, cb);
       } else {  // S_TENSOR
         if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
         else {
@@ -224,11 +225,11 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
         T dg[9], wm[9];
 #pragma unroll
         for (int m = 0; m < 9; ++m) dg[m] = gxr[m] * j0d[m % 3];
-        tangent_wm<T, MODEL>(a.mat, cb, dg, wm);
+        tangent_wm<T, MODEL>(mq, cb, dg, wm);
 #pragma unroll
         for (int m = 0; m < 9; ++m) wv[m] = wm[m] * (detw * j0d[m % 3]);
       } else {
-        tangent_integrand<T, MODEL>(a.mat, cb, gxr, j0inv, detw, wv);
+        tangent_integrand<T, MODEL>(mq, cb, gxr, j0inv, detw, wv);
       }
 #pragma unroll
       for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];

@@ -218,6 +218,10 @@ KArgs<T> kargs(const emfgpu_op* op) {
   }
   for (int t = 0; t < n; ++t) a.qwd[t] = L->qwts[t];
   a.cartesian = L->cartesian;
+  a.hq = static_cast<const T*>(op->d_hq);
+  a.hqd = op->d_hqd;
+  a.m1qd = op->d_m1qd;
+  a.hq_stride = L->nel * L->nq3;
   a.fd_nx = FastDiv::make((uint32_t)L->nx);
   a.fd_nxy = FastDiv::make((uint32_t)(L->nx * L->ny));
   return a;
@@ -279,11 +283,11 @@ void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const vo
   if (op->precision == 64)
     launch_node_gather<double>(static_cast<const double*>(op->d_loc), static_cast<const double*>(glo),
                                static_cast<const double*>(ghi), static_cast<const double*>(x),
-                               static_cast<double*>(y), L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, s);
+                               static_cast<double*>(y), L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s);
   else
     launch_node_gather<float>(static_cast<const float*>(op->d_loc), static_cast<const float*>(glo),
                               static_cast<const float*>(ghi), static_cast<const float*>(x), static_cast<float*>(y),
-                              L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, s);
+                              L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s);
   CK(cudaGetLastError());
 }
 
@@ -347,8 +351,13 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
     L->ny = d->ny;
     L->nz = d->nz;
     L->p = d->p;
+    L->periodic_y = (d->flags & EMFGPU_LEVEL_PERIODIC_Y) ? 1 : 0;
+    if (L->periodic_y && ((d->ny % 2) != 0 || d->ny < 2))
+      throw ApiError(EMFGPU_ERR_CONFIG, "level: a periodic y lattice needs an even ny >= 2 (colouring)");
+    if (L->periodic_y && (d->dirichlet_faces & (4 | 8)))
+      throw ApiError(EMFGPU_ERR_CONFIG, "level: no Dirichlet faces across a periodic direction");
     L->mx = d->nx * d->p + 1;
-    L->my = d->ny * d->p + 1;
+    L->my = d->ny * d->p + (L->periodic_y ? 0 : 1);
     L->mz = d->nz * d->p + 1;
     L->nnodes = (int64_t)L->mx * L->my * L->mz;
     L->ndofs = 3 * L->nnodes;
@@ -399,6 +408,12 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
               r2 += A * std::sin(s * x) * std::sin(s * y);
             } else if (d->map == EMFGPU_MAP_SHEAR_X) {
               r0 += amp * std::sin(2.0 * M_PI * y);
+            } else if (d->map == EMFGPU_MAP_TUBE) {  // BASELINE cfg3: (radial, theta, axial) lattice
+              const double r = d->map_param[0] + (d->map_param[1] - d->map_param[0]) * (x / L->extent[0]);
+              const double th = 2.0 * M_PI * (y / L->extent[1]);
+              r0 = r * std::cos(th);
+              r1 = r * std::sin(th);
+              r2 = d->map_param[2] * (z / L->extent[2]);
             }
             const int64_t node = ((int64_t)c * m[1] + b) * m[0] + a;
             coords[3 * node] = r0;
@@ -415,7 +430,7 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
     CK(cudaMalloc(&flags, 2 * sizeof(int)));
     CK(cudaMemset(flags, 0, 2 * sizeof(int)));
     launch_geometry(L->d_coords, geo_q, nullptr, L->nx, L->ny, L->nz, L->p, L->B.data(), L->D.data(),
-                    L->qwts.data(), flags, flags + 1, 0);
+                    L->qwts.data(), flags, flags + 1, L->periodic_y, 0);
     CK(cudaGetLastError());
     int hf[2];
     CK(cudaMemcpy(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost));
@@ -487,7 +502,7 @@ emfgpu_status emfgpu_level_jacobians(const emfgpu_level* l, double* host_out) {
     CK(cudaMalloc(&j0, sizeof(double) * nqp * 9));
     CK(cudaMalloc(&flags, 2 * sizeof(int)));
     launch_geometry(l->d_coords, geo_q, j0, l->nx, l->ny, l->nz, l->p, l->B.data(), l->D.data(), l->qwts.data(),
-                    flags, flags + 1, 0);
+                    flags, flags + 1, l->periodic_y, 0);
     CK(cudaGetLastError());
     CK(cudaMemcpy(host_out, j0, sizeof(double) * nqp * 9, cudaMemcpyDeviceToHost));
     cudaFree(geo_q);
@@ -563,6 +578,8 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
 void emfgpu_op_destroy(emfgpu_op* op) {
   if (!op) return;
   cudaFree(op->d_cache);
+  if (op->d_hq && op->d_hq != op->d_hqd) cudaFree(op->d_hq);
+  cudaFree(op->d_hqd);  // d_m1qd points into it
   cudaFree(op->d_uk);
   cudaFree(op->d_ukd);
   cudaFree(op->d_loc);
@@ -741,13 +758,13 @@ static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream
     dispatch_diagonal<double>(op, kargs<double>(op), s);
     double* d = static_cast<double*>(d_diag);
     launch_node_gather<double>(static_cast<const double*>(op->d_loc), nullptr, nullptr, d, d, L->nx, L->ny, L->nz,
-                               L->p, 0, 0, 0, L->mz - 1, s);
+                               L->p, 0, 0, 0, L->mz - 1, L->periodic_y, s);
     launch_diag_finish<double>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, s);
   } else {
     dispatch_diagonal<float>(op, kargs<float>(op), s);
     float* d = static_cast<float*>(d_diag);
     launch_node_gather<float>(static_cast<const float*>(op->d_loc), nullptr, nullptr, d, d, L->nx, L->ny, L->nz,
-                              L->p, 0, 0, 0, L->mz - 1, s);
+                              L->p, 0, 0, 0, L->mz - 1, L->periodic_y, s);
     launch_diag_finish<float>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, s);
   }
   CK(cudaGetLastError());
@@ -903,6 +920,8 @@ emfgpu_status emfgpu_transfer_create(const emfgpu_level* fine, const emfgpu_leve
   auto t = std::make_unique<emfgpu_transfer>();
   emfgpu_status st = guarded(nullptr, [&] {
     const int nf[3] = {fine->nx, fine->ny, fine->nz}, nc[3] = {coarse->nx, coarse->ny, coarse->nz};
+    if (fine->periodic_y || coarse->periodic_y)
+      throw ApiError(EMFGPU_ERR_CONFIG, "TransferOp: periodic lattices are not supported");
     const bool p_step = nf[0] == nc[0] && nf[1] == nc[1] && nf[2] == nc[2] && fine->p > coarse->p;
     const bool h_step = fine->p == coarse->p && nf[0] == 2 * nc[0] && nf[1] == 2 * nc[1] && nf[2] == 2 * nc[2];
     if (!p_step && !h_step)
@@ -1563,5 +1582,60 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     cudaFree(ap);
     cudaFree(dbuf);
     cudaFreeHost(hdot);
+  });
+}
+
+// ---- per-quadrature-point fibre frames (BASELINE cfg3) -----------------------
+emfgpu_status emfgpu_op_set_fibre_frame(emfgpu_op* op, int kind) {
+  if (!op) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    if (op->model != EMFGPU_FIBER) throw ApiError(EMFGPU_ERR_CONFIG, "fibre frame: fibre model only");
+    if (kind < 0 || kind > 2) throw ApiError(EMFGPU_ERR_CONFIG, "fibre frame: kind must be 0, 1 or 2");
+    CK(cudaSetDevice(op->L->device));
+    const emfgpu_level* L = op->L;
+    op->linearized = false;
+    if (op->d_hq && op->d_hq != op->d_hqd) cudaFree(op->d_hq);
+    cudaFree(op->d_hqd);
+    op->d_hq = nullptr;
+    op->d_hqd = op->d_m1qd = nullptr;
+    op->frame_kind = kind;
+    if (kind == 0) return;
+    const int64_t nqp = L->nel * L->nq3;
+    CK(cudaMalloc(&op->d_hqd, sizeof(double) * 18 * nqp));
+    op->d_m1qd = op->d_hqd + 12 * nqp;
+    double h[2][6], m1[2][3];
+    structure_tensors(op->params, h, m1);
+    // h11, h22, h33 of the dispersion (material.cpp:52-61)
+    const double h33 = 1.0 / (4.0 * op->params.b) - std::exp(-2.0 * op->params.b) /
+                                                       (std::sqrt(2.0 * M_PI * op->params.b) *
+                                                        std::erf(std::sqrt(2.0 * op->params.b)));
+    const double ratio = std::cyl_bessel_i(1.0, op->params.a) / std::cyl_bessel_i(0.0, op->params.a);
+    const double h11 = 0.5 * (1.0 - h33) * (1.0 + ratio), h22 = 0.5 * (1.0 - h33) * (1.0 - ratio);
+    double frame[9];
+    for (int d = 0; d < 3; ++d) {
+      frame[d] = op->params.e1[d];
+      frame[3 + d] = op->params.e2[d];
+      frame[6 + d] = op->params.e3[d];
+    }
+    launch_fibre_frame(L->d_coords, op->d_hqd, op->d_m1qd, L->nx, L->ny, L->nz, L->p, L->periodic_y, L->B.data(),
+                       h11, h22, h33, op->params.phi, kind, frame, op->stream);
+    CK(cudaGetLastError());
+    if (op->precision == 64) {
+      op->d_hq = op->d_hqd;
+    } else {
+      CK(cudaMalloc(&op->d_hq, sizeof(float) * 18 * nqp));
+      launch_cast_d2f(op->d_hqd, static_cast<float*>(op->d_hq), 18 * nqp, op->stream);
+    }
+    CK(cudaStreamSynchronize(op->stream));
+  });
+}
+
+emfgpu_status emfgpu_op_fibre_field(const emfgpu_op* op, double* h_out, double* m1_out) {
+  if (!op) return EMFGPU_ERR_INVALID;
+  return guarded(nullptr, [&] {
+    if (!op->d_hqd) throw ApiError(EMFGPU_ERR_CONFIG, "fibre field: no per-qp frame set");
+    const int64_t nqp = op->L->nel * op->L->nq3;
+    if (h_out) CK(cudaMemcpy(h_out, op->d_hqd, sizeof(double) * 12 * nqp, cudaMemcpyDeviceToHost));
+    if (m1_out) CK(cudaMemcpy(m1_out, op->d_m1qd, sizeof(double) * 6 * nqp, cudaMemcpyDeviceToHost));
   });
 }

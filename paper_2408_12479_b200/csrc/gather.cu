@@ -14,8 +14,17 @@ namespace emfgpu {
 // n elements, lattice size m), sorted even-index first. Local node index in
 // the element along that axis is returned in loc[].  lo/hi ghost layers are
 // allowed along z (index -1 and n).
-__device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bool ghosts, int* el, int* loc) {
+__device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bool ghosts, int* el, int* loc,
+                                               bool periodic = false) {
   const int e1 = a / p;
+  if (periodic && a == 0) {  // seam of a periodic lattice: elements n-1 (local p) and 0 (local 0)
+    const bool odd_last = ((n - 1) & 1) != 0;
+    el[0] = odd_last ? 0 : n - 1;
+    loc[0] = odd_last ? 0 : p;
+    el[1] = odd_last ? n - 1 : 0;
+    loc[1] = odd_last ? p : 0;
+    return 2;
+  }
   if (a % p == 0) {
     const bool has_lo = a > 0 || ghosts;
     const bool has_hi = a < n * p || ghosts;
@@ -54,9 +63,10 @@ __device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bo
 template <typename T, int P>
 __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
                                                           const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
-                                                          int ny, int nz, int faces, int kpar, int c0) {
+                                                          int ny, int nz, int faces, int kpar, int c0,
+                                                          int periodic_y) {
   constexpr int N = P + 1, N3 = N * N * N, N2 = N * N;
-  const int mx = nx * P + 1, my = ny * P + 1, mz = nz * P + 1;
+  const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1), mz = nz * P + 1;
   const int a = blockIdx.x * 32 + threadIdx.x;
   const int b = blockIdx.y * 8 + threadIdx.y;
   const int c = blockIdx.z + c0;
@@ -70,7 +80,7 @@ __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ 
   }
   int ie[2], il[2], je[2], jl[2], ke[2], kl[2];
   const int ni = axis_candidates(a, P, nx, 0, false, ie, il);
-  const int nj = axis_candidates(b, P, ny, 0, false, je, jl);
+  const int nj = axis_candidates(b, P, ny, 0, false, je, jl, periodic_y != 0);
   const bool ghosts = ghost_lo != nullptr || ghost_hi != nullptr;
   const int nk = axis_candidates(c, P, nz, kpar, ghosts, ke, kl);
   T s0 = T(0), s1 = T(0), s2 = T(0);
@@ -113,14 +123,14 @@ __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ 
 
 template <typename T>
 void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny, int nz,
-                        int p, int faces, int kpar, int c0, int c1, cudaStream_t s) {
+                        int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s) {
   if (c1 < c0) return;
-  const int mx = nx * p + 1, my = ny * p + 1;
+  const int mx = nx * p + 1, my = ny * p + (periodic_y ? 0 : 1);
   const dim3 grid((mx + 31) / 32, (my + 7) / 8, c1 - c0 + 1), block(32, 8);
   switch (p) {
 #define EMF_G(PP)                                                                                             \
   case PP:                                                                                                    \
-    node_gather_kernel<T, PP><<<grid, block, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, faces, kpar, c0); \
+    node_gather_kernel<T, PP><<<grid, block, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, faces, kpar, c0, periodic_y); \
     break;
     EMF_G(1)
     EMF_G(2)
@@ -179,9 +189,9 @@ void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces,
 }
 
 template void launch_node_gather<double>(const double*, const double*, const double*, const double*, double*, int,
-                                         int, int, int, int, int, int, int, cudaStream_t);
+                                         int, int, int, int, int, int, int, int, cudaStream_t);
 template void launch_node_gather<float>(const float*, const float*, const float*, const float*, float*, int, int,
-                                        int, int, int, int, int, int, cudaStream_t);
+                                        int, int, int, int, int, int, int, cudaStream_t);
 template void launch_pack_face<double>(const double*, double*, int, int, int, int, int, cudaStream_t);
 template void launch_pack_face<float>(const float*, float*, int, int, int, int, int, cudaStream_t);
 template void launch_diag_finish<double>(double*, int64_t, int, int, int, int, unsigned long long*, cudaStream_t);

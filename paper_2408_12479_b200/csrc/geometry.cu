@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1)) geom
 
 void launch_geometry(const double* coords, double* geo_q, double* j0_out, int nx, int ny, int nz, int p,
                      const double* B, const double* D, const double* qw, int* nonaffine, int* degenerate,
-                     cudaStream_t s) {
+                     int periodic_y, cudaStream_t s) {
   GeoArgs a;
   a.coords = coords;
   a.geo = geo_q;
@@ -77,7 +77,7 @@ void launch_geometry(const double* coords, double* geo_q, double* j0_out, int nx
   a.ny = ny;
   a.nz = nz;
   a.mx = nx * p + 1;
-  a.my = ny * p + 1;
+  a.my = ny * p + (periodic_y ? 0 : 1);
   a.nel = (int64_t)nx * ny * nz;
   const int n = p + 1;
   a.stride = a.nel * n * n * n;
@@ -114,6 +114,97 @@ __global__ void geo_compact_kernel(const double* geo_q, double* geo_e, int64_t n
 
 void launch_geo_compact(const double* geo_q, double* geo_e, int64_t nel, int nq3, cudaStream_t s) {
   geo_compact_kernel<<<(unsigned)((nel + 255) / 256), 256, 0, s>>>(geo_q, geo_e, nel, nq3);
+}
+
+// Per-qp fibre frame field: cylindrical frame about the z axis at the qp's
+// reference position (e1 = circumferential, e2 = axial, e3 = radial), the two
+// families at +-phi from e1 in the (e1, e2) plane; H_f = h11 m1 m1 + h22 m2 m2 +
+// h33 e3 e3 (material.cpp:50-82 with a per-point frame, SURVEY §8(c) gap 2).
+// kind 2: the constant frame (e1, e2, e3) given in frame[] (for testing).
+struct FrameArgs {
+  const double* coords;
+  double* hq;   // 12 * nqp (H4, H6), SoA
+  double* m1q;  // 6 * nqp (M1_4, M1_6), SoA
+  int nx, ny, mx, my, p, kind;
+  int64_t nel, nqp;
+  double B[81];
+  double h11, h22, h33, phi;
+  double frame[9];
+};
+
+__global__ void fibre_frame_kernel(const FrameArgs a) {
+  const int n = a.p + 1, n3 = n * n * n;
+  const int64_t qi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= a.nqp) return;
+  const int64_t e = qi / n3;
+  const int q = (int)(qi % n3);
+  const int qa = q % n, qb = (q / n) % n, qc = q / (n * n);
+  const int ei = (int)(e % a.nx), ej = (int)((e / a.nx) % a.ny), ek = (int)(e / ((int64_t)a.nx * a.ny));
+  double x[3] = {0, 0, 0};
+  for (int c = 0; c < n; ++c)
+    for (int b = 0; b < n; ++b)
+      for (int aa = 0; aa < n; ++aa) {
+        int gb = ej * a.p + b;
+        if (gb >= a.my) gb -= a.my;
+        const int64_t node = ((int64_t)(ek * a.p + c) * a.my + gb) * a.mx + (ei * a.p + aa);
+        const double w = a.B[qa * n + aa] * a.B[qb * n + b] * a.B[qc * n + c];
+        for (int d = 0; d < 3; ++d) x[d] += w * a.coords[3 * node + d];
+      }
+  double e1[3], e2[3], e3[3];
+  if (a.kind == 1) {
+    const double th = atan2(x[1], x[0]);
+    const double cs = cos(th), sn = sin(th);
+    e1[0] = -sn; e1[1] = cs; e1[2] = 0.0;
+    e2[0] = 0.0; e2[1] = 0.0; e2[2] = 1.0;
+    e3[0] = cs; e3[1] = sn; e3[2] = 0.0;
+  } else {
+    for (int d = 0; d < 3; ++d) {
+      e1[d] = a.frame[d];
+      e2[d] = a.frame[3 + d];
+      e3[d] = a.frame[6 + d];
+    }
+  }
+  const double c = cos(a.phi), s = sin(a.phi);
+  double m1[2][3], m2[2][3];
+  for (int d = 0; d < 3; ++d) {
+    m1[0][d] = c * e1[d] + s * e2[d];
+    m2[0][d] = -s * e1[d] + c * e2[d];
+    m1[1][d] = c * e1[d] + (-s) * e2[d];
+    m2[1][d] = s * e1[d] + c * e2[d];
+  }
+  for (int f = 0; f < 2; ++f) {
+    for (int i = 0; i < 3; ++i)
+      for (int j = i; j < 3; ++j) {
+        const int k = sidx(i, j);
+        const double h = a.h11 * (m1[f][i] * m1[f][j]) + a.h22 * (m2[f][i] * m2[f][j]) + a.h33 * (e3[i] * e3[j]);
+        a.hq[(6 * f + k) * a.nqp + qi] = h;
+      }
+    for (int d = 0; d < 3; ++d) a.m1q[(3 * f + d) * a.nqp + qi] = m1[f][d];
+  }
+}
+
+void launch_fibre_frame(const double* coords, double* hq, double* m1q, int nx, int ny, int nz, int p, int periodic_y,
+                        const double* B, double h11, double h22, double h33, double phi, int kind,
+                        const double* frame, cudaStream_t s) {
+  FrameArgs a;
+  a.coords = coords;
+  a.hq = hq;
+  a.m1q = m1q;
+  a.nx = nx;
+  a.ny = ny;
+  a.mx = nx * p + 1;
+  a.my = ny * p + (periodic_y ? 0 : 1);
+  a.p = p;
+  a.kind = kind;
+  a.nel = (int64_t)nx * ny * nz;
+  a.nqp = a.nel * (p + 1) * (p + 1) * (p + 1);
+  for (int t = 0; t < (p + 1) * (p + 1); ++t) a.B[t] = B[t];
+  a.h11 = h11;
+  a.h22 = h22;
+  a.h33 = h33;
+  a.phi = phi;
+  for (int t = 0; t < 9; ++t) a.frame[t] = frame ? frame[t] : 0.0;
+  fibre_frame_kernel<<<(unsigned)((a.nqp + 255) / 256), 256, 0, s>>>(a);
 }
 
 __global__ void cast_d2f_kernel(const double* in, float* out, int64_t n) {

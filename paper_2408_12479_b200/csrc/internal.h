@@ -24,7 +24,7 @@ void launch_diagonal(int model, const KArgs<T>& a, cudaStream_t s);
 // gather.cu
 template <typename T>
 void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny,
-                        int nz, int p, int faces, int kpar, int c0, int c1, cudaStream_t s);
+                        int nz, int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s);
 template <typename T>
 void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int side, cudaStream_t s);
 template <typename T>
@@ -34,7 +34,10 @@ void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces,
 // geometry.cu
 void launch_geometry(const double* coords, double* geo_q, double* j0_out, int nx, int ny, int nz, int p,
                      const double* B, const double* D, const double* qw, int* nonaffine, int* degenerate,
-                     cudaStream_t s);
+                     int periodic_y, cudaStream_t s);
+void launch_fibre_frame(const double* coords, double* hq, double* m1q, int nx, int ny, int nz, int p, int periodic_y,
+                        const double* B, double h11, double h22, double h33, double phi, int kind,
+                        const double* frame, cudaStream_t s);
 void launch_geo_compact(const double* geo_q, double* geo_e, int64_t nel, int nq3, cudaStream_t s);
 void launch_cast_d2f(const double* in, float* out, int64_t n, cudaStream_t s);
 
@@ -82,7 +85,7 @@ void launch_jacobi(const T* inv, const T* r, T* z, int64_t n, cudaStream_t s);
 struct emfgpu_level {
   int nx = 0, ny = 0, nz = 0, p = 0, mx = 0, my = 0, mz = 0;
   int64_t nnodes = 0, ndofs = 0, nel = 0, nq3 = 0;
-  int faces = 0, device = 0, affine = 0, z_offset = 0, cartesian = 0;
+  int faces = 0, device = 0, affine = 0, z_offset = 0, cartesian = 0, periodic_y = 0;
   double extent[3] = {1, 1, 1};
   // basis tables (host): GLL nodes, Gauss points/weights, B/D (row = qp)
   std::vector<double> nodes, qpts, qwts, B, D;
@@ -110,6 +113,11 @@ struct emfgpu_op {
   void* d_y = nullptr;
   unsigned long long* d_err = nullptr;
   unsigned long long* h_err = nullptr;  // pinned
+  // per-qp fibre frame field (fibre model): H4/H6 in double and Number, M1s
+  int frame_kind = 0;
+  double* d_hqd = nullptr;
+  double* d_m1qd = nullptr;
+  void* d_hq = nullptr;
   cudaStream_t stream = nullptr;
   // pipelined host-vector apply: copy streams + per-chunk events
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;

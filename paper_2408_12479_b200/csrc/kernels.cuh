@@ -92,7 +92,45 @@ struct KArgs {
   double Bd[25], Dd[25];
   double qwd[9];  // 1D Gauss weights (affine geometry stores det J0 without them)
   FastDiv fd_nx, fd_nxy;
+  // optional per-qp fibre frame field (fibre model): 18 SoA fields H4 (6),
+  // H6 (6), M1_4 (3), M1_6 (3) with stride hq_stride, in Number (hq) and in
+  // double (hqd; m1qd = hqd + 12*stride) for linearization
+  const T* hq;
+  const double* hqd;
+  const double* m1qd;
+  int64_t hq_stride;
 };
+
+// Material constants at one quadrature point: the operator's constants, with
+// the fibre structure tensors replaced by the per-qp frame field if present.
+template <typename T, int MODEL>
+__device__ __forceinline__ MatConst<T> mat_at(const MatConst<T>& m, const T* hq, int64_t st, int64_t qidx) {
+  MatConst<T> r = m;
+  if (MODEL == FIBER && hq != nullptr) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r.h[f][k] = hq[(6 * f + k) * st + qidx];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) r.m1[f][k] = hq[(12 + 3 * f + k) * st + qidx];  // dead for tensor/scalar
+    }
+  }
+  return r;
+}
+__device__ __forceinline__ MatConst<double> matd_at(const MatConst<double>& m, const double* hq, const double* m1q,
+                                                    int64_t st, int64_t qidx) {
+  MatConst<double> r = m;
+  if (hq != nullptr) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) r.h[f][k] = hq[(6 * f + k) * st + qidx];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) r.m1[f][k] = m1q[(3 * f + k) * st + qidx];
+    }
+  }
+  return r;
+}
 
 __device__ __forceinline__ bool node_constrained(int a, int b, int c, int mx, int my, int mz, int faces) {
   return ((faces & 1) && a == 0) || ((faces & 2) && a == mx - 1) || ((faces & 4) && b == 0) ||
@@ -264,6 +302,7 @@ __device__ __forceinline__ ElemPos elem_pos(int64_t e, int nx, int ny, int mx, i
   r.ek = (int)(e / ((int64_t)nx * ny));
   r.ga = r.ei * P + i;
   r.gb = r.ej * P + j;
+  if (r.gb >= my) r.gb -= my;  // periodic y lattice (my = ny*P); never taken otherwise
   r.gc = r.ek * P + k;
   r.node = ((int64_t)r.gc * my + r.gb) * mx + r.ga;
   return r;
@@ -317,6 +356,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
 #pragma unroll
     for (int m = 0; m < 9; ++m) a.cache[(C_G + m) * st + qidx] = T(g[m]);
   }
+  const MatConst<double> md = matd_at(a.matd, a.hqd, a.m1qd, a.hq_stride, qidx);
   Bundle<double> cb;
   if (!make_strain(g, cb)) {
     atomicMin(a.err, (unsigned long long)qidx);
@@ -324,7 +364,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   }
   if (a.strategy == S_CACHEDF || a.strategy == S_NONE) return;
   // stored scalars, computed in double (operator.hpp:720-735)
-  cache_scalars<double, MODEL>(a.matd, cb);
+  cache_scalars<double, MODEL>(md, cb);
   if (MODEL == CNH) {
     a.cache[C_LNJ * st + qidx] = T(cb.lnj);
   } else {
@@ -339,7 +379,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     a.cache[(C_EF + 1) * st + qidx] = T(cb.efib[1]);
   }
   if (a.strategy != S_TENSOR) return;
-  second_pk<double, MODEL>(a.matd, cb);
+  second_pk<double, MODEL>(md, cb);
 #pragma unroll
   for (int m = 0; m < 9; ++m) {
     a.cache[(C_F + m) * st + qidx] = T(cb.F[m]);
@@ -378,6 +418,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   const int64_t qidx = e * N3 + q;
   const int64_t st = a.cache_stride, ix = valid ? qidx : 0;
   const T* cs = a.cache;
+  const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, ix);
   Bundle<T> cb;
   T j0inv[9], detw;
   load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
@@ -389,13 +430,13 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
     mm(gk, j0inv, g);
     make_strain(g, cb);
-    if (a.strategy == S_NONE) cache_scalars<T, MODEL>(a.mat, cb);
+    if (a.strategy == S_NONE) cache_scalars<T, MODEL>(mq, cb);
   } else if (a.strategy == S_CACHEDF) {
     T g[9];
 #pragma unroll
     for (int m = 0; m < 9; ++m) g[m] = cs[(C_G + m) * st + ix];
     make_strain(g, cb);
-    cache_scalars<T, MODEL>(a.mat, cb);
+    cache_scalars<T, MODEL>(mq, cb);
   } else {
 #pragma unroll
     for (int m = 0; m < 9; ++m) {
@@ -422,7 +463,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
       cb.efib[1] = cs[(C_EF + 1) * st + ix];
     }
   }
-  if (a.strategy != S_TENSOR) second_pk<T, MODEL>(a.mat, cb);
+  if (a.strategy != S_TENSOR) second_pk<T, MODEL>(mq, cb);
 
   // A^c_{dd'}: 27 values per qp, as symmetric quadratic-form coefficients
   // coef[c][pair], pairs (00,11,22,01,02,12) with off-diagonals A_dd'+A_d'd.
@@ -436,7 +477,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
 #pragma unroll
       for (int m = 0; m < 9; ++m) gref[m] = T(0);
       gref[3 * c + dp] = T(1);
-      tangent_integrand<T, MODEL>(a.mat, cb, gref, j0inv, detw, w);
+      tangent_integrand<T, MODEL>(mq, cb, gref, j0inv, detw, w);
 #pragma unroll
       for (int d = 0; d < 3; ++d) A[d][dp] = w[3 * c + d];
     }

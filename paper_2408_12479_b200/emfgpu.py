@@ -20,8 +20,9 @@ LIB_PATH = os.environ.get("EMFGPU_LIB") or os.path.join(HERE, "lib", "libemfgpu.
 
 MODELS = {"cnh": 0, "inh": 1, "fiber": 2}
 STRATEGIES = {"none": 0, "scalar": 1, "tensor": 2, "cachedF": 3}
-MAPS = {"reference": 0, "shear_x": 1, "coords": 2}
-NO_CARTESIAN, NO_AFFINE = 1, 2
+MAPS = {"reference": 0, "shear_x": 1, "coords": 2, "tube": 3}
+NO_CARTESIAN, NO_AFFINE, PERIODIC_Y = 1, 2, 4
+FRAMES = {"global": 0, "cylindrical": 1, "replicated": 2}
 STATUS = {0: "OK", 1: "ERR_CONFIG", 2: "ERR_NUMERICAL", 3: "ERR_IO", 4: "ERR_INVALID", 5: "ERR_STALE",
           6: "ERR_CUDA"}
 
@@ -141,6 +142,8 @@ def lib():
                                                     C.POINTER(C.c_double)]),
             "emfgpu_dot": (st, [C.c_int, vp, vp, i64, C.POINTER(C.c_double), vp]),
             "emfgpu_bench_fma_peak": (st, [C.c_int, C.c_double, C.POINTER(C.c_double)]),
+            "emfgpu_op_set_fibre_frame": (st, [vp, C.c_int]),
+            "emfgpu_op_fibre_field": (st, [vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -184,7 +187,7 @@ class FeLevel:
     node-coordinate array."""
 
     def __init__(self, nx, ny=None, nz=None, p=2, extent=(1.0, 1.0, 1.0), map="reference",
-                 map_param=(0.0,), coords=None, dirichlet_faces=1, device=0, z_offset=0, flags=0):
+                 map_param=(0.0,), coords=None, dirichlet_faces=1, device=0, z_offset=0, flags=0, periodic_y=False):
         ny = nx if ny is None else ny
         nz = nx if nz is None else nz
         d = LevelDesc()
@@ -198,7 +201,7 @@ class FeLevel:
         d.dirichlet_faces = dirichlet_faces
         d.device = device
         d.z_offset = z_offset
-        d.flags = flags
+        d.flags = flags | (PERIODIC_Y if periodic_y else 0)
         h = C.c_void_p()
         st = lib().emfgpu_level_create(C.byref(d), C.byref(h))
         if st:
@@ -206,6 +209,7 @@ class FeLevel:
         self.h = h.value
         self.nx, self.ny, self.nz, self.p = nx, ny, nz, p
         self.faces = dirichlet_faces
+        self.periodic_y = bool(periodic_y)
         self.n_dofs = lib().emfgpu_level_n_dofs(self.h)
         self.n_elements = lib().emfgpu_level_n_elements(self.h)
         self.affine = bool(lib().emfgpu_level_affine(self.h))
@@ -357,6 +361,20 @@ class ElasticOperator:
         st = lib().emfgpu_op_pack_face(self.h, k, side, _ptr(d_face), _stream(stream))
         if st:
             self._raise(st)
+
+    def set_fibre_frame(self, kind="cylindrical"):
+        """Per-qp fibre frames (fibre model): "global", "cylindrical" (about z) or "replicated"."""
+        st = lib().emfgpu_op_set_fibre_frame(self.h, FRAMES[kind] if isinstance(kind, str) else int(kind))
+        if st:
+            self._raise(st)
+
+    def fibre_field(self):
+        """(H [12, nqp], M1 [6, nqp]) of the per-qp frame field (SoA)."""
+        nqp = self.level.n_elements * (self.level.p + 1) ** 3
+        h = np.empty(12 * nqp)
+        m = np.empty(6 * nqp)
+        _check(lib().emfgpu_op_fibre_field(self.h, h.ctypes.data, m.ctypes.data))
+        return h, m
 
     def estimate_eigenvalues(self, d_diag, iterations=20, seed=0x9E3779B97F4A7C15):
         lo, hi = C.c_double(), C.c_double()

@@ -79,18 +79,21 @@ def lattice_axis(n_el: int, p: int, extent: float = 1.0) -> np.ndarray:
     return (e + 0.5 * (nodes[l] + 1.0)) * h
 
 
-def lattice_positions(nx: int, ny: int, nz: int, p: int, extent=(1.0, 1.0, 1.0)):
-    """Pre-map lattice positions X, Y, Z flattened in node order (a fastest)."""
+def lattice_positions(nx: int, ny: int, nz: int, p: int, extent=(1.0, 1.0, 1.0), periodic_y=False):
+    """Pre-map lattice positions X, Y, Z flattened in node order (a fastest).
+    A periodic y lattice drops the node row at y = extent (it is row 0)."""
     ax = lattice_axis(nx, p, extent[0])
     ay = lattice_axis(ny, p, extent[1])
+    if periodic_y:
+        ay = ay[:-1]
     az = lattice_axis(nz, p, extent[2])
     Z, Y, X = np.meshgrid(az, ay, ax, indexing="ij")
     return X.ravel(), Y.ravel(), Z.ravel()
 
 
-def dirichlet_mask(nx, ny, nz, p, faces: int) -> np.ndarray:
+def dirichlet_mask(nx, ny, nz, p, faces: int, periodic_y=False) -> np.ndarray:
     """Per-DoF mask for clamped faces (bit f: -x,+x,-y,+y,-z,+z), mesh.cpp:213-246."""
-    mx, my, mz = nx * p + 1, ny * p + 1, nz * p + 1
+    mx, my, mz = nx * p + 1, ny * p + (0 if periodic_y else 1), nz * p + 1
     c, b, a = np.meshgrid(np.arange(mz), np.arange(my), np.arange(mx), indexing="ij")
     on = np.zeros(c.shape, bool)
     tests = [a == 0, a == mx - 1, b == 0, b == my - 1, c == 0, c == mz - 1]
@@ -112,3 +115,19 @@ def make_u0(nx, ny, nz, p, amp=0.05, noise=1e-3, seed=0, faces=1, extent=(1.0, 1
 
 def make_v(ndofs: int, seed: int = 1) -> np.ndarray:
     return -1.0 + 2.0 * uniform01(seed, ndofs)
+
+
+def periodic_to_open(v: np.ndarray, nx, ny, nz, p) -> np.ndarray:
+    """P: a vector on a periodic-y lattice -> the open lattice with the seam
+    row duplicated (row my = row 0)."""
+    mx, my, mz = nx * p + 1, ny * p, nz * p + 1
+    a = v.reshape(mz, my, mx, -1)
+    return np.concatenate([a, a[:, :1]], axis=1).reshape(-1)
+
+
+def open_to_periodic(v: np.ndarray, nx, ny, nz, p) -> np.ndarray:
+    """P^T: sums the duplicated seam row of the open lattice into row 0."""
+    mx, my, mz = nx * p + 1, ny * p, nz * p + 1
+    a = v.reshape(mz, my + 1, mx, -1).copy()
+    a[:, 0] += a[:, my]
+    return a[:, :my].reshape(-1)

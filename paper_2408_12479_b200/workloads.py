@@ -12,7 +12,13 @@ cfg4  48^3 Q4 iNH, fp64 PCG to 1e-8 with an fp32 hp-multigrid V-cycle
       kappa/mu = 1000 with the indefinite u0 does not converge with the
       reference algorithm (F3/F4); the timed variant is the well-posed one
       SURVEY §8(c') prescribes: u0 = 0, kappa/mu = 50, affine cube.
-cfg3  (tube, per-point fibre frames, periodic theta) is not built in round 1.
+cfg3  Thick tube r in [1, 1.3], length 10: 16 (radial) x 128 (circumferential,
+      periodic) x 256 (axial) Q3 = 43 408 512 DoFs; fibre model (mu=1,
+      kappa=100, k1=2, k2=5, +-40 deg from the circumferential direction in the
+      circumferential-axial plane, dispersion a=3.62, b=34.3 — BASELINE leaves
+      them open, SURVEY §8(c) gap 2), per-qp cylindrical fibre frames; u0 =
+      5% radial expansion 0.05 (x, y, 0) + 1e-3 seeded noise; no Dirichlet
+      face (apply only); cached stress+tangent strategy, fp64 and fp32.
 """
 from __future__ import annotations
 
@@ -39,7 +45,7 @@ class Workload:
     @property
     def ndofs(self):
         nx, ny, nz = self.n
-        return 3 * (nx * self.p + 1) * (ny * self.p + 1) * (nz * self.p + 1)
+        return 3 * (nx * self.p + 1) * (ny * self.p + (0 if self.periodic_y else 1)) * (nz * self.p + 1)
 
     def u0(self):
         nx, ny, nz = self.n
@@ -48,11 +54,13 @@ class Workload:
     def v(self, seed=1):
         return I.make_v(self.ndofs, seed)
 
+    periodic_y: bool = False
+
     def level(self, **kw):
         from .emfgpu import FeLevel
         nx, ny, nz = self.n
         return FeLevel(nx, ny, nz, p=self.p, map=self.map, map_param=self.map_param, dirichlet_faces=self.faces,
-                       **kw)
+                       periodic_y=self.periodic_y, **kw)
 
     def material(self):
         from .emfgpu import MaterialParams
@@ -86,3 +94,19 @@ def rhs(w: Workload, seed=2):
     nx, ny, nz = w.n
     b[I.dirichlet_mask(nx, ny, nz, w.p, w.faces)] = 0.0
     return b
+
+
+def cfg3(n=(16, 128, 256)):
+    return Workload("cfg3", tuple(n), 3, "fiber",
+                    dict(mu=1.0, kappa_b=100.0, k1=2.0, k2=5.0, a=3.62, b=34.3, phi=float(np.deg2rad(40.0))),
+                    map="tube", map_param=(1.0, 1.3, 10.0), u_amp=0.05, noise=1e-3, faces=0, periodic_y=True)
+
+
+def tube_u0(w: Workload, coords: np.ndarray, seed=0):
+    """cfg3 linearization point: 5% radial expansion plus seeded noise."""
+    c = coords.reshape(-1, 3)
+    u = np.zeros_like(c)
+    u[:, 0] = w.u_amp * c[:, 0]
+    u[:, 1] = w.u_amp * c[:, 1]
+    u = u.reshape(-1)
+    return u + (-w.noise + 2.0 * w.noise * I.uniform01(seed, u.size))

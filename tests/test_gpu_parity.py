@@ -268,3 +268,59 @@ def test_multigrid_vcycle_and_pcg_vs_reference(G, tag, lmax, p):
     assert abs(its - int(g[f"{tag}_its"])) <= 1, (its, int(g[f"{tag}_its"]))
     assert hist[-1] <= 1e-8
     assert rel(x.cpu().numpy(), g[f"{tag}_x"]) <= 1e-6
+
+
+def test_fibre_frame_field_replicated_equals_global(G):
+    """Per-qp frames that replicate the material frame reproduce the
+    global-frame operator (to the last bits of H, recomputed on the device);
+    cylindrical frames agree with the oracle."""
+    from oracle import orcbind as O
+    n, p = 2, 3
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    prm = G.MaterialParams(mu=1.0, kappa_b=100.0, k1=2.0, k2=5.0)
+    u0 = I.make_u0(n, n, n, p)
+    v = I.make_v(lev.n_dofs, 4)
+    ys = {}
+    for kind in ("global", "replicated", "cylindrical"):
+        op = G.ElasticOperator(lev, "fiber", prm, "tensor", 64)
+        op.set_fibre_frame(kind)
+        op.update_linearization(u0)
+        ys[kind] = op.apply_tangent(v)
+        if kind == "cylindrical":
+            h, m1 = op.fibre_field()
+    assert rel(ys["replicated"], ys["global"]) <= 1e-14
+    orc = O.OracleOperator(n, n, n, p, lev.node_coords(), 1, "fiber", prm.as_array(), "tensor", 64)
+    orc.set_frames(h, m1)
+    orc.update_linearization(u0)
+    assert rel(ys["cylindrical"], orc.apply(v)) <= 1e-12
+    assert not np.allclose(ys["cylindrical"], ys["global"])
+
+
+@pytest.mark.parametrize("strategy", ["tensor", "none"])
+def test_periodic_tube_vs_oracle(G, strategy):
+    """BASELINE cfg3 geometry at small size: periodic-theta tube, per-qp
+    cylindrical fibre frames.  Oracle: the open lattice with the seam row
+    duplicated, y = P^T K P x (the reference has no periodic meshes)."""
+    from oracle import orcbind as O
+    from paper_2408_12479_b200 import workloads as W
+    nx, ny, nz, p = 2, 8, 3, 3
+    w = W.cfg3((nx, ny, nz))
+    lev = w.level()
+    assert lev.periodic_y and not lev.affine
+    coords = lev.node_coords()
+    u0 = W.tube_u0(w, coords)
+    v = I.make_v(lev.n_dofs, 6)
+    prm = w.material()
+    co = I.periodic_to_open(coords, nx, ny, nz, p)
+    for prec in (64, 32):
+        op = G.ElasticOperator(lev, "fiber", prm, strategy, prec)
+        op.set_fibre_frame("cylindrical")
+        op.update_linearization(u0)
+        y = op.apply_tangent(v)
+        h, m1 = op.fibre_field()
+        orc = O.OracleOperator(nx, ny, nz, p, co, 0, "fiber", prm.as_array(), strategy, prec)
+        orc.set_frames(h, m1)
+        orc.update_linearization(I.periodic_to_open(u0, nx, ny, nz, p))
+        yo = I.open_to_periodic(orc.apply(I.periodic_to_open(v, nx, ny, nz, p).astype(orc.dtype)).astype(np.float64),
+                                nx, ny, nz, p)
+        assert rel(y, yo) <= {64: 1e-12, 32: 1e-5}[prec], (prec, rel(y, yo))

@@ -165,3 +165,17 @@ def test_oracle_multigrid_and_pcg_bitexact():
         op.update_linearization(np.zeros(op.n))
         x, its, hist = O.pcg_solve(op, mg, g[f"{tag}_b"], 1e-8, 200)
         assert its == int(g[f"{tag}_its"]) and np.array_equal(x, g[f"{tag}_x"])
+
+
+def test_oracle_replicated_frames_equal_global_frame():
+    """A per-qp frame field that replicates the global frame reproduces the
+    reference's fibre operator bit for bit (SURVEY §8(c) gap 2 pin)."""
+    g = np.load(os.path.join(GOLD, "fiber_p3_n2_affine.npz"))
+    st = O.structure_tensors(g["params"])
+    op = O.OracleOperator(2, 2, 2, 3, g["coords"], 1, "fiber", g["params"], "none", 64)
+    nqp = 8 * 64
+    h = np.repeat(st[:12][:, None], nqp, axis=1).ravel()
+    m1 = np.repeat(st[12:18][:, None], nqp, axis=1).ravel()
+    op.set_frames(h, m1)
+    op.update_linearization(g["u0"])
+    assert np.array_equal(op.apply(g["v"]), g["y64_none"])
