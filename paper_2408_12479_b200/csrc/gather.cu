@@ -59,7 +59,46 @@ __device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bo
 }
 
 // One thread per lattice node; 3-D grid (x: 32 nodes along a, y: 8 along b,
-// z: node planes) so no index division is needed.
+// z: node planes) so no index division is needed.  Per axis a node has two
+// candidate-element slots ordered even index first (a non-shared node uses
+// only the first); the 2x2x2 slot product is visited z-major, which is the
+// reference's colour order, with predicated loads and a running sum that
+// starts at 0 exactly like y = 0; y += ... in operator.hpp:606, 439.
+struct AxisSlots {
+  int e[2], l[2];
+  bool v[2];
+};
+
+template <int P>
+__device__ __forceinline__ AxisSlots axis_slots(int a, int n, int par, bool lo_ok, bool hi_ok, bool periodic) {
+  AxisSlots s;
+  const int q = a / P, r = a - q * P;
+  if (r != 0) {
+    s.e[0] = q;
+    s.l[0] = r;
+    s.v[0] = true;
+    s.e[1] = q;
+    s.l[1] = 0;
+    s.v[1] = false;
+    return s;
+  }
+  int elo = q - 1, ehi = q;
+  bool vlo = q > 0 || lo_ok, vhi = q < n || hi_ok;
+  if (periodic && q == 0) {
+    elo = n - 1;
+    vlo = true;
+  }
+  // the even (global) element index first
+  const bool swap = ((elo + par) & 1) != 0;
+  s.e[0] = swap ? ehi : elo;
+  s.l[0] = swap ? 0 : P;
+  s.v[0] = swap ? vhi : vlo;
+  s.e[1] = swap ? elo : ehi;
+  s.l[1] = swap ? P : 0;
+  s.v[1] = swap ? vlo : vhi;
+  return s;
+}
+
 template <typename T, int P>
 __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
                                                           const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
@@ -78,44 +117,36 @@ __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ 
     y[3 * idx + 2] = x[3 * idx + 2];
     return;
   }
-  int ie[2], il[2], je[2], jl[2], ke[2], kl[2];
-  const int ni = axis_candidates(a, P, nx, 0, false, ie, il);
-  const int nj = axis_candidates(b, P, ny, 0, false, je, jl, periodic_y != 0);
-  const bool ghosts = ghost_lo != nullptr || ghost_hi != nullptr;
-  const int nk = axis_candidates(c, P, nz, kpar, ghosts, ke, kl);
+  const AxisSlots sx = axis_slots<P>(a, nx, 0, false, false, false);
+  const AxisSlots sy = axis_slots<P>(b, ny, 0, false, false, periodic_y != 0);
+  const AxisSlots sz = axis_slots<P>(c, nz, kpar, ghost_lo != nullptr, ghost_hi != nullptr, false);
   T s0 = T(0), s1 = T(0), s2 = T(0);
-  bool first = true;
-  for (int tk = 0; tk < nk; ++tk) {
-    const int k = ke[tk];
-    for (int tj = 0; tj < nj; ++tj)
-      for (int ti = 0; ti < ni; ++ti) {
+#pragma unroll
+  for (int tk = 0; tk < 2; ++tk)
+#pragma unroll
+    for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+      for (int ti = 0; ti < 2; ++ti) {
+        if (!(sz.v[tk] && sy.v[tj] && sx.v[ti])) continue;
+        const int k = sz.e[tk];
         T v0, v1, v2;
         if (k < 0 || k >= nz) {
           const T* src = k < 0 ? ghost_lo : ghost_hi;
-          if (!src) continue;
-          const int64_t off = ((((int64_t)je[tj] * nx + ie[ti]) * N2) + jl[tj] * N + il[ti]) * 3;
+          const int64_t off = ((((int64_t)sy.e[tj] * nx + sx.e[ti]) * N2) + sy.l[tj] * N + sx.l[ti]) * 3;
           v0 = src[off];
           v1 = src[off + 1];
           v2 = src[off + 2];
         } else {  // element-local results, component-major loc[(e*3 + c)*N3 + m]
-          const int64_t e = ((int64_t)k * ny + je[tj]) * nx + ie[ti];
-          const int64_t off = e * 3 * N3 + (kl[tk] * N + jl[tj]) * N + il[ti];
+          const int64_t e = ((int64_t)k * ny + sy.e[tj]) * nx + sx.e[ti];
+          const int64_t off = e * 3 * N3 + (sz.l[tk] * N + sy.l[tj]) * N + sx.l[ti];
           v0 = loc[off];
           v1 = loc[off + N3];
           v2 = loc[off + 2 * N3];
         }
-        if (first) {
-          s0 = v0;
-          s1 = v1;
-          s2 = v2;
-          first = false;
-        } else {
-          s0 += v0;
-          s1 += v1;
-          s2 += v2;
-        }
+        s0 += v0;
+        s1 += v1;
+        s2 += v2;
       }
-  }
   y[3 * idx] = s0;
   y[3 * idx + 1] = s1;
   y[3 * idx + 2] = s2;

@@ -121,8 +121,12 @@ struct emfgpu_op {
   cudaStream_t stream = nullptr;
   // pipelined host-vector apply: copy streams + per-chunk events
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  static constexpr int kMaxChunks = 16;
-  cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr;
+  static constexpr int kMaxChunks = 32;
+  cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
+  cudaGraphExec_t gexec = nullptr;  // captured pipeline for (g_x, g_y, g_nch)
+  const void* g_x = nullptr;
+  void* g_y = nullptr;
+  int g_nch = 0;
   bool linearized = false;
   uint64_t checksum = 0;
   std::string last_error;
