@@ -224,6 +224,34 @@ emfgpu_status emfgpu_op_set_fibre_frame(emfgpu_op* op, int kind);
 /* Per-qp H4,H6 (12 per qp, SoA field-major) and M1_4,M1_6 (6 per qp). */
 emfgpu_status emfgpu_op_fibre_field(const emfgpu_op* op, double* h_out, double* m1_out);
 
+/* ---- residual and loads ----------------------------------
+ * evaluate_residual(u, r), operator.hpp:94-95/623-641 (material domain):
+ * r_i = (Grad v_i, F S) - load_scale * load_i, Dirichlet rows zeroed. */
+emfgpu_status emfgpu_op_residual(emfgpu_op* op, const void* d_u, void* d_r, void* stream);
+emfgpu_status emfgpu_op_residual_host(emfgpu_op* op, const void* u, void* r);
+/* Loads::pressure on face (operator.hpp:23-32, 995-1001): traction -p N on the
+ * reference geometry of face `face` (-x,+x,-y,+y,-z,+z = 0..5). */
+emfgpu_status emfgpu_op_set_pressure(emfgpu_op* op, double pressure, int face);
+emfgpu_status emfgpu_op_set_load_scale(emfgpu_op* op, double scale); /* set_load_scale, :80 */
+
+/* ---- Newton-Krylov on the device ------------------------
+ * fgmres_solve (solver.hpp:120-203): right-preconditioned FGMRES(restart) with
+ * modified Gram-Schmidt; x in/out; mg may be NULL. */
+emfgpu_status emfgpu_fgmres_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double abs_tol,
+                                  double rel_tol, int restart, int max_restarts, int* iterations,
+                                  double* final_residual, void* stream);
+typedef struct emfgpu_newton_config {
+  double eps_abs, eps_rel; /* NewtonConfig (solver.hpp:26-30): 1e-8, 1e-3 */
+  int max_iter;            /* 25 */
+  double lin_abs_tol, lin_rel_tol; /* FgmresConfig (solver.hpp:32-37): 1e-12, 1e-3 */
+  int restart, max_restarts;        /* 30, 40 */
+} emfgpu_newton_config;
+void emfgpu_newton_default_config(emfgpu_newton_config* cfg);
+/* newton_solve (solver.hpp:603-656) with the op's loads: d_u (fp64) in/out. */
+emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, const emfgpu_newton_config* cfg,
+                                  int* newton_iterations, int* linear_iterations, double* final_residual,
+                                  void* stream);
+
 /* FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured by a register-resident
  * FMA loop over one wave of CTAs for `seconds`: the FP64/FP32 roofline
  * denominator (bench.py). */

@@ -549,6 +549,76 @@ int orc_op_diagonal(const orc_op* op, void* d, int64_t* n_bad) {
   return op->precision == 64 ? diagonal_d(op, (double*)d, n_bad) : diagonal_f(op, (float*)d, n_bad);
 }
 
+/* build_load_vector operator.hpp:925-1003, pressure part: -p N traction on
+ * face `face` (0..5 = -x,+x,-y,+y,-z,+z) of the reference geometry `coords`,
+ * (p+1)^2 Gauss points per face element, accumulated in double. */
+void orc_pressure_load(const orc_op* op, const double* coords, double pressure, int face, double* load) {
+  const orc_basis* b = &op->basis;
+  const int p = op->p, nn = p + 1, nq = b->n;
+  const int axis = face / 2, t1 = (axis + 1) % 3, t2 = (axis + 2) % 3, upper = face % 2 == 1;
+  const int ne[3] = {op->nx, op->ny, op->nz};
+  for (int64_t i = 0; i < op->ndofs; ++i) load[i] = 0.0;
+  if (pressure == 0.0) return;
+  int64_t nodes[ORC_MAXN3];
+  for (int ej = 0; ej < ne[t2]; ++ej)
+    for (int ei = 0; ei < ne[t1]; ++ei) {
+      int idx[3];
+      idx[axis] = upper ? ne[axis] - 1 : 0;
+      idx[t1] = ei;
+      idx[t2] = ej;
+      orc_element_nodes(op, ((int64_t)idx[2] * op->ny + idx[1]) * op->nx + idx[0], nodes);
+      const int lface = upper ? p : 0;
+      for (int q2 = 0; q2 < nq; ++q2)
+        for (int q1 = 0; q1 < nq; ++q1) {
+          double x[3] = {0, 0, 0}, g1[3] = {0, 0, 0}, g2[3] = {0, 0, 0};
+          for (int a2 = 0; a2 < nn; ++a2)
+            for (int a1 = 0; a1 < nn; ++a1) {
+              const double v1 = b->B[q1 * nn + a1], d1 = b->D[q1 * nn + a1];
+              const double v2 = b->B[q2 * nn + a2], d2 = b->D[q2 * nn + a2];
+              int loc[3];
+              loc[axis] = lface;
+              loc[t1] = a1;
+              loc[t2] = a2;
+              const int64_t g = nodes[(loc[2] * nn + loc[1]) * nn + loc[0]];
+              for (int c = 0; c < 3; ++c) {
+                const double xc = coords[3 * g + c];
+                x[c] += v1 * v2 * xc;
+                g1[c] += d1 * v2 * xc;
+                g2[c] += v1 * d2 * xc;
+              }
+            }
+          const double nr[3] = {g1[1] * g2[2] - g1[2] * g2[1], g1[2] * g2[0] - g1[0] * g2[2],
+                                g1[0] * g2[1] - g1[1] * g2[0]};
+          const double sgn = upper ? 1.0 : -1.0;
+          const double area = sqrt(nr[0] * nr[0] + nr[1] * nr[1] + nr[2] * nr[2]);
+          const double unit[3] = {sgn * nr[0] / area, sgn * nr[1] / area, sgn * nr[2] / area};
+          const double h[3] = {-pressure * unit[0], -pressure * unit[1], -pressure * unit[2]};
+          const double w = b->qwts[q1] * b->qwts[q2] * area;
+          for (int a2 = 0; a2 < nn; ++a2)
+            for (int a1 = 0; a1 < nn; ++a1) {
+              const double phi = b->B[q1 * nn + a1] * b->B[q2 * nn + a2];
+              int loc[3];
+              loc[axis] = lface;
+              loc[t1] = a1;
+              loc[t2] = a2;
+              const int64_t g = nodes[(loc[2] * nn + loc[1]) * nn + loc[0]];
+              for (int c = 0; c < 3; ++c) load[3 * g + c] += phi * w * h[c];
+            }
+        }
+    }
+}
+
+/* evaluate_residual with a face pressure; u, r in the op's precision. */
+int orc_op_residual(const orc_op* op, const double* coords, const void* u, double pressure, int face,
+                    double load_scale, void* r) {
+  double* load = (double*)malloc(sizeof(double) * op->ndofs);
+  orc_pressure_load(op, coords, pressure, face, load);
+  const int err = op->precision == 64 ? residual_d(op, (const double*)u, load, load_scale, (double*)r)
+                                      : residual_f(op, (const float*)u, load, load_scale, (float*)r);
+  free(load);
+  return err;
+}
+
 int orc_op_chebyshev(const orc_op* op, const void* diag, double lmax_est, int degree, double range_factor,
                      double safety, const void* b, void* x, int zero_start) {
   if (!op->linearized) return 4;

@@ -508,6 +508,78 @@ static int SFX(apply)(const orc_op* op, const R* du, R* y) {
   return err;
 }
 
+/* element_residual_batch operator.hpp:533-595 (material domain) +
+ * evaluate_residual :623-641: r = sum_e (Grad v, F S) in colour order (input
+ * NOT masked), r -= load_scale * load (load in Number), Dirichlet rows zeroed. */
+static int SFX(residual)(const orc_op* op, const R* u, const double* load, double load_scale, R* r) {
+  const int64_t n = op->ndofs;
+  const orc_basis* b = &op->basis;
+  const int nq = b->n, nq3 = op->nq3, nn3 = op->nn3;
+  for (int64_t i = 0; i < n; ++i) r[i] = (R)0;
+  int err = 0;
+  for (int color = 0; color < 8; ++color) {
+    const int ci = color & 1, cj = (color >> 1) & 1, ck = (color >> 2) & 1;
+    const int nci = (op->nx - ci + 1) / 2, ncj = (op->ny - cj + 1) / 2, nck = (op->nz - ck + 1) / 2;
+    const int64_t cnt = (int64_t)nci * ncj * nck;
+#pragma omp parallel
+    {
+      SFX(scratch)* s = (SFX(scratch)*)malloc(sizeof(SFX(scratch)));
+#pragma omp for schedule(static)
+      for (int64_t t = 0; t < cnt; ++t) {
+        const int i = ci + 2 * (int)(t % nci);
+        const int j = cj + 2 * (int)((t / nci) % ncj);
+        const int k = ck + 2 * (int)(t / ((int64_t)nci * ncj));
+        const int64_t e = ((int64_t)k * op->ny + j) * op->nx + i;
+        SFX(gather)(op, u, e, s->loc);
+        for (int c = 0; c < 3; ++c) SFX(grad_qp)(b, s->loc[c], s->work, s->g[c][0], s->g[c][1], s->g[c][2]);
+        int bad = 0;
+        for (int q = 0; q < nq3 && !bad; ++q) {
+          R j0[9], det0, j0inv[9], gref[9], g[9], S[6], wm[9], j0t[9], wr[9];
+          SFX(qp_mapping)(op, e, q, j0, &det0);
+          if (SFX(inverse)(j0, j0inv)) bad = 1;
+          for (int c = 0; c < 3; ++c)
+            for (int d = 0; d < 3; ++d) gref[3 * c + d] = s->g[c][d][q];
+          SFX(mm)(gref, j0inv, g);
+          const int qa = q % nq, qb = (q / nq) % nq, qc = q / (nq * nq);
+          const R wq = (R)(b->qwts[qa] * b->qwts[qb] * b->qwts[qc]);
+          const orc_material mq = orc_mat_at(op, e * nq3 + q);
+          SFX(qpc) c;
+          if (SFX(compute_cache)(&mq, g, &c)) {
+            bad = 1;
+            break;
+          }
+          SFX(second_pk)(&mq, &c, S);
+          SFX(mm_ts)(c.F, S, wm);
+          SFX(transpose)(j0inv, j0t);
+          SFX(mm)(wm, j0t, wr);
+          const R sc = det0 * wq;
+          for (int cc = 0; cc < 3; ++cc)
+            for (int d = 0; d < 3; ++d) s->g[cc][d][q] = sc * wr[3 * cc + d];
+        }
+        if (bad) {
+#pragma omp atomic write
+          err = 1;
+          continue;
+        }
+        for (int c = 0; c < 3; ++c)
+          for (int m = 0; m < nn3; ++m) s->out[c][m] = (R)0;
+        for (int c = 0; c < 3; ++c) SFX(scatter_grad)(b, s->g[c][0], s->g[c][1], s->g[c][2], s->work, s->out[c]);
+        int64_t nodes[ORC_MAXN3];
+        orc_element_nodes(op, e, nodes);
+        for (int c = 0; c < 3; ++c)
+          for (int m = 0; m < nn3; ++m) r[3 * nodes[m] + c] += s->out[c][m];
+      }
+      free(s);
+    }
+  }
+  const R ls = (R)load_scale;
+  for (int64_t i = 0; i < n; ++i) {
+    r[i] -= ls * (R)load[i];
+    if (op->mask[i]) r[i] = (R)0;
+  }
+  return err;
+}
+
 /* compute_diagonal operator.hpp:772-878: 3*(p+1)^3 element-local unit
  * applications per element, (ldof, ldof) entries scattered in colour order. */
 static int SFX(diagonal)(const orc_op* op, R* diag, int64_t* n_bad) {

@@ -45,6 +45,8 @@ def lib():
         L.orc_structure_tensors.argtypes = [vp, vp]
         L.orc_op_element_locals.argtypes = [vp, vp, vp, i64, i64]
         L.orc_op_set_frames.argtypes = [vp, vp, vp]
+        L.orc_op_residual.argtypes = [vp, vp, vp, C.c_double, C.c_int, C.c_double, vp]
+        L.orc_pressure_load.argtypes = [vp, vp, C.c_double, C.c_int, vp]
         L.orc_basis_tables.argtypes = [C.c_int] + [vp] * 5
         _lib = L
     return _lib
@@ -129,6 +131,20 @@ class OracleOperator:
         if st:
             raise OracleError(st)
         return y
+
+    def residual(self, u, pressure=0.0, face=1, load_scale=1.0):
+        """evaluate_residual with a face pressure (operator.hpp:623-641, 925-1003)."""
+        u = np.ascontiguousarray(u, self.dtype)
+        r = np.empty(self.n, self.dtype)
+        st = lib().orc_op_residual(self.h, _p(self.coords), _p(u), pressure, face, load_scale, _p(r))
+        if st:
+            raise OracleError(st)
+        return r
+
+    def pressure_load(self, pressure, face=1):
+        out = np.empty(self.n)
+        lib().orc_pressure_load(self.h, _p(self.coords), pressure, face, _p(out))
+        return out
 
     def set_frames(self, h, m1):
         """Per-qp fibre frame field (12*nqp H4,H6 and 6*nqp M1s, SoA); EXT of the reference."""

@@ -534,3 +534,57 @@ int ref_pcg_solve(void* o, void* m, const double* b, double* x, double rtol, int
 }
 
 }  // extern "C"
+
+// ---- residual with loads and the reference's Newton solve (run_solve_with,
+// runner.cpp:166-204, one increment): evaluate_residual, newton_solve with
+// FGMRES(30) + MgHierarchy<float>.
+extern "C" {
+
+int ref_residual_with_pressure(void* l, int model, const double* params, double pressure, int face,
+                               double load_scale, const double* u, double* r) {
+  RefLevel* L = static_cast<RefLevel*>(l);
+  return guarded([&] {
+    Loads loads;
+    loads.pressure = pressure;
+    loads.pressure_face = face;
+    const ModelKind mk = model == 0 ? ModelKind::cnh : model == 1 ? ModelKind::inh : ModelKind::fiber;
+    ElasticOperator<double> op(*L->fe, mk, params_from(params), {Stability::stable, Domain::material},
+                               Strategy::none, KernelConfig{}, loads);
+    op.set_load_scale(load_scale);
+    std::vector<double> uv(u, u + L->fe->dof_count()), rv;
+    op.evaluate_residual(uv, rv);
+    std::memcpy(r, rv.data(), rv.size() * sizeof(double));
+  });
+}
+
+int ref_newton_pressure(void* l, int model, const double* params, double pressure, int face, int degree,
+                        double deform_amp, int dirichlet_faces, int64_t coarse_direct_limit, double* u_out,
+                        int* newton_its, int* fgmres_its, double* final_res) {
+  RefLevel* L = static_cast<RefLevel*>(l);
+  return guarded([&] {
+    Loads loads;
+    loads.pressure = pressure;
+    loads.pressure_face = face;
+    const ModelKind mk = model == 0 ? ModelKind::cnh : model == 1 ? ModelKind::inh : ModelKind::fiber;
+    const Formulation form{Stability::stable, Domain::material};
+    ElasticOperator<double> op(*L->fe, mk, params_from(params), form, Strategy::none, KernelConfig{}, loads);
+    SmootherConfig sc;
+    sc.degree = degree;
+    std::array<bool, 6> faces{};
+    for (int f = 0; f < 6; ++f) faces[f] = (dirichlet_faces >> f) & 1;
+    MgHierarchy<float> mg(*L->fe, faces, mk, params_from(params), form, Strategy::none, KernelConfig{}, sc,
+                          DeformMap{deform_amp}, coarse_direct_limit);
+    std::vector<double> u(L->fe->dof_count(), 0.0);
+    L->fe->dirichlet_set_values(u);
+    op.set_load_scale(1.0);
+    const NewtonStats st = newton_solve(op, &mg, u, NewtonConfig{}, FgmresConfig{});
+    int lin = 0;
+    for (const auto& s : st.steps) lin += s.fgmres_iters;
+    *newton_its = st.iterations;
+    *fgmres_its = lin;
+    *final_res = st.final_residual;
+    std::memcpy(u_out, u.data(), u.size() * sizeof(double));
+  });
+}
+
+}  // extern "C"

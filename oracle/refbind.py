@@ -232,3 +232,28 @@ def pcg_solve(op: RefOperator, mg, b, rtol=1e-8, maxit=200):
     _check(lib().ref_pcg_solve(op.h, mg.h if mg is not None else None, _p(b), _p(x), rtol, maxit, C.byref(it),
                                _p(hist)))
     return x, it.value, hist[:it.value + 1]
+
+
+def residual_with_pressure(level: RefLevel, model, params, pressure, face, u, load_scale=1.0):
+    L = lib()
+    L.ref_residual_with_pressure.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_int, C.c_double,
+                                             C.c_void_p, C.c_void_p]
+    params = np.asarray(params, np.float64)
+    u = np.ascontiguousarray(u, np.float64)
+    r = np.empty_like(u)
+    _check(L.ref_residual_with_pressure(level.h, MODELS[model], _p(params), pressure, face, load_scale, _p(u), _p(r)))
+    return r
+
+
+def newton_pressure(level: RefLevel, model, params, pressure, face=1, degree=6, deform_amp=0.0, faces=1,
+                    coarse_direct_limit=0):
+    L = lib()
+    L.ref_newton_pressure.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_double,
+                                      C.c_int, C.c_int64, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_double)]
+    params = np.asarray(params, np.float64)
+    u = np.empty(level.ndofs)
+    nit, lit, res = C.c_int(), C.c_int(), C.c_double()
+    _check(L.ref_newton_pressure(level.h, MODELS[model], _p(params), pressure, face, degree, deform_amp, faces,
+                                 coarse_direct_limit, _p(u), C.byref(nit), C.byref(lit), C.byref(res)))
+    return u, nit.value, lit.value, res.value

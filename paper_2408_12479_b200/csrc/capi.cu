@@ -246,6 +246,15 @@ void dispatch_linearize(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) 
   }
 }
 template <typename T>
+void dispatch_residual(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) {
+  switch (op->L->p) {
+    case 1: launch_residual<T, 1>(op->model, a, s); break;
+    case 2: launch_residual<T, 2>(op->model, a, s); break;
+    case 3: launch_residual<T, 3>(op->model, a, s); break;
+    case 4: launch_residual<T, 4>(op->model, a, s); break;
+  }
+}
+template <typename T>
 void dispatch_diagonal(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) {
   switch (op->L->p) {
     case 1: launch_diagonal<T, 1>(op->model, a, s); break;
@@ -585,6 +594,7 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_loc);
   cudaFree(op->d_x);
   cudaFree(op->d_y);
+  cudaFree(op->d_load);
   cudaFree(op->d_err);
   if (op->h_err) cudaFreeHost(op->h_err);
   if (op->stream) cudaStreamDestroy(op->stream);
@@ -1675,5 +1685,352 @@ emfgpu_status emfgpu_op_fibre_field(const emfgpu_op* op, double* h_out, double* 
     const int64_t nqp = op->L->nel * op->L->nq3;
     if (h_out) CK(cudaMemcpy(h_out, op->d_hqd, sizeof(double) * 12 * nqp, cudaMemcpyDeviceToHost));
     if (m1_out) CK(cudaMemcpy(m1_out, op->d_m1qd, sizeof(double) * 6 * nqp, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---- residual and loads (operator.hpp:532-595, 623-641, 880-1008) ----------
+static void residual_impl(emfgpu_op* op, const void* u, void* r, cudaStream_t s) {
+  const emfgpu_level* L = op->L;
+  if (op->precision == 64) {
+    KArgs<double> a = kargs<double>(op);
+    a.x = static_cast<const double*>(u);
+    dispatch_residual<double>(op, a, s);
+    launch_node_gather<double>(static_cast<const double*>(op->d_loc), nullptr, nullptr, static_cast<const double*>(u),
+                               static_cast<double*>(r), L->nx, L->ny, L->nz, L->p, L->faces, 0, 0, L->mz - 1,
+                               L->periodic_y, s);
+    launch_sub_load_mask<double>(static_cast<double*>(r), static_cast<const double*>(op->d_load), op->load_scale,
+                                 L->nnodes, L->mx, L->my, L->mz, L->faces, s);
+  } else {
+    KArgs<float> a = kargs<float>(op);
+    a.x = static_cast<const float*>(u);
+    dispatch_residual<float>(op, a, s);
+    launch_node_gather<float>(static_cast<const float*>(op->d_loc), nullptr, nullptr, static_cast<const float*>(u),
+                              static_cast<float*>(r), L->nx, L->ny, L->nz, L->p, L->faces, 0, 0, L->mz - 1,
+                              L->periodic_y, s);
+    launch_sub_load_mask<float>(static_cast<float*>(r), static_cast<const float*>(op->d_load), op->load_scale,
+                                L->nnodes, L->mx, L->my, L->mz, L->faces, s);
+  }
+  CK(cudaGetLastError());
+}
+
+emfgpu_status emfgpu_op_residual(emfgpu_op* op, const void* d_u, void* d_r, void* stream) {
+  if (!op || !d_u || !d_r) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] { residual_impl(op, d_u, d_r, S(stream, op->stream)); });
+}
+
+emfgpu_status emfgpu_op_residual_host(emfgpu_op* op, const void* u, void* r) {
+  if (!op || !u || !r) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    const size_t bytes = nsize(op) * op->L->ndofs;
+    if (!op->d_x) CK(cudaMalloc(&op->d_x, bytes));
+    if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
+    CK(cudaMemcpyAsync(op->d_x, u, bytes, cudaMemcpyHostToDevice, op->stream));
+    residual_impl(op, op->d_x, op->d_y, op->stream);
+    CK(cudaMemcpyAsync(r, op->d_y, bytes, cudaMemcpyDeviceToHost, op->stream));
+    check_err(op, op->stream, nullptr, nullptr, "evaluate_residual");
+  });
+}
+
+emfgpu_status emfgpu_op_set_load_scale(emfgpu_op* op, double scale) {
+  if (!op) return EMFGPU_ERR_INVALID;
+  op->load_scale = scale;
+  return EMFGPU_OK;
+}
+
+// Uniform pressure on one face of the (deformed) box: traction -p N on the
+// reference geometry, (p+1)^2 Gauss points per face element
+// (build_load_vector, operator.hpp:933-1001).  Setup-time, on the host.
+emfgpu_status emfgpu_op_set_pressure(emfgpu_op* op, double pressure, int face) {
+  if (!op) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    if (face < 0 || face > 5) throw ApiError(EMFGPU_ERR_CONFIG, "pressure: face must be 0..5");
+    const emfgpu_level* L = op->L;
+    if (L->periodic_y && (face == 2 || face == 3)) throw ApiError(EMFGPU_ERR_CONFIG, "pressure: periodic face");
+    CK(cudaSetDevice(L->device));
+    std::vector<double> coords(L->ndofs), load(L->ndofs, 0.0);
+    CK(cudaMemcpy(coords.data(), L->d_coords, sizeof(double) * L->ndofs, cudaMemcpyDeviceToHost));
+    const int p = L->p, nn = p + 1, nq = p + 1;
+    const int axis = face / 2, t1 = (axis + 1) % 3, t2 = (axis + 2) % 3;
+    const bool upper = face % 2 == 1;
+    const int ne[3] = {L->nx, L->ny, L->nz};
+    const int m[3] = {L->mx, L->my, L->mz};
+    const std::vector<double>& B = L->B;
+    const std::vector<double>& D = L->D;
+    auto gnode = [&](const int* ijk, const int* loc) -> int64_t {
+      int g[3];
+      for (int d = 0; d < 3; ++d) g[d] = ijk[d] * p + loc[d];
+      if (L->periodic_y && g[1] >= m[1]) g[1] -= m[1];
+      return ((int64_t)g[2] * m[1] + g[1]) * m[0] + g[0];
+    };
+    if (pressure != 0.0)
+      for (int ej = 0; ej < ne[t2]; ++ej)
+        for (int ei = 0; ei < ne[t1]; ++ei) {
+          int idx[3];
+          idx[axis] = upper ? ne[axis] - 1 : 0;
+          idx[t1] = ei;
+          idx[t2] = ej;
+          for (int q2 = 0; q2 < nq; ++q2)
+            for (int q1 = 0; q1 < nq; ++q1) {
+              double x[3] = {0, 0, 0}, g1[3] = {0, 0, 0}, g2[3] = {0, 0, 0};
+              for (int a2 = 0; a2 < nn; ++a2)
+                for (int a1 = 0; a1 < nn; ++a1) {
+                  const double v1 = B[q1 * nn + a1], d1 = D[q1 * nn + a1];
+                  const double v2 = B[q2 * nn + a2], d2 = D[q2 * nn + a2];
+                  int loc[3];
+                  loc[axis] = upper ? p : 0;
+                  loc[t1] = a1;
+                  loc[t2] = a2;
+                  const int64_t g = gnode(idx, loc);
+                  for (int c = 0; c < 3; ++c) {
+                    const double xc = coords[3 * g + c];
+                    x[c] += v1 * v2 * xc;
+                    g1[c] += d1 * v2 * xc;
+                    g2[c] += v1 * d2 * xc;
+                  }
+                }
+              const double nrm[3] = {g1[1] * g2[2] - g1[2] * g2[1], g1[2] * g2[0] - g1[0] * g2[2],
+                                     g1[0] * g2[1] - g1[1] * g2[0]};
+              const double sgn = upper ? 1.0 : -1.0;
+              const double area = std::sqrt((nrm[0] * nrm[0] + nrm[1] * nrm[1]) + nrm[2] * nrm[2]);
+              const double h[3] = {-pressure * (sgn * nrm[0] / area), -pressure * (sgn * nrm[1] / area),
+                                   -pressure * (sgn * nrm[2] / area)};
+              const double w = L->qwts[q1] * L->qwts[q2] * area;
+              for (int a2 = 0; a2 < nn; ++a2)
+                for (int a1 = 0; a1 < nn; ++a1) {
+                  const double phi = B[q1 * nn + a1] * B[q2 * nn + a2];
+                  int loc[3];
+                  loc[axis] = upper ? p : 0;
+                  loc[t1] = a1;
+                  loc[t2] = a2;
+                  const int64_t g = gnode(idx, loc);
+                  for (int c = 0; c < 3; ++c) load[3 * g + c] += phi * w * h[c];
+                }
+            }
+        }
+    const size_t ns = nsize(op);
+    if (!op->d_load) CK(cudaMalloc(&op->d_load, ns * L->ndofs));
+    if (op->precision == 64) {
+      CK(cudaMemcpy(op->d_load, load.data(), sizeof(double) * L->ndofs, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float> lf(load.begin(), load.end());
+      CK(cudaMemcpy(op->d_load, lf.data(), sizeof(float) * L->ndofs, cudaMemcpyHostToDevice));
+    }
+  });
+}
+
+// ============================================================================
+// FGMRES(m) and Newton on the device (solver.hpp:120-203, 603-656)
+// ============================================================================
+namespace {
+
+struct DevVec {
+  double* p = nullptr;
+  ~DevVec() { cudaFree(p); }
+};
+
+__global__ void lincomb_kernel(double* y, const double* x, double a, int64_t n) {  // y += a x
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+__global__ void scale_copy_kernel(double* y, const double* x, double a, int64_t n) {  // y = x / a
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] / a;
+}
+__global__ void neg_kernel(double* y, const double* x, int64_t n) {  // y = -x
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = -x[i];
+}
+inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+struct Krylov {
+  emfgpu_op* op;
+  emfgpu_mg* mg;
+  cudaStream_t s;
+  int64_t n;
+  double *dbuf = nullptr, *hdot = nullptr;
+  Krylov(emfgpu_op* o, emfgpu_mg* m, cudaStream_t st) : op(o), mg(m), s(st), n(o->L->ndofs) {
+    CK(cudaMalloc(&dbuf, sizeof(double) * (dot_partial_count() + 1)));
+    CK(cudaMallocHost(&hdot, sizeof(double)));
+  }
+  ~Krylov() {
+    cudaFree(dbuf);
+    if (hdot) cudaFreeHost(hdot);
+  }
+  double dot(const double* a, const double* b) {
+    launch_dot<double>(a, b, n, dbuf + 1, dbuf, s);
+    return mg_dot_sync(dbuf, hdot, s);
+  }
+  void apply(const double* x, double* y) { op_apply_T<double>(op, x, y, s); }
+  void prec(const double* r, double* z) {
+    if (mg) {
+      if (mg->cfg.precision == 64)
+        mg_precondition<double>(mg, r, z, s);
+      else
+        mg_precondition<float>(mg, r, z, s);
+    } else {
+      CK(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+};
+
+// Right-preconditioned flexible GMRES with restart, modified Gram-Schmidt,
+// Givens rotations; terminates when ||b - A x|| <= max(abs_tol, rel_tol ||b||)
+// (fgmres_solve, solver.hpp:120-203).  Returns false without convergence.
+bool fgmres(Krylov& K, const double* b, double* x, double abs_tol, double rel_tol, int m, int max_restarts,
+            int* iterations, double* final_res) {
+  const int64_t n = K.n;
+  const double bnorm = std::sqrt(K.dot(b, b));
+  const double tol = std::max(abs_tol, rel_tol * bnorm);
+  std::vector<DevVec> V(m + 1), Z(m);
+  for (auto& v : V) CK(cudaMalloc(&v.p, sizeof(double) * n));
+  for (auto& z : Z) CK(cudaMalloc(&z.p, sizeof(double) * n));
+  DevVec w, r;
+  CK(cudaMalloc(&w.p, sizeof(double) * n));
+  CK(cudaMalloc(&r.p, sizeof(double) * n));
+  std::vector<double> H((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0);
+  int its = 0;
+  for (int cycle = 0; cycle <= max_restarts; ++cycle) {
+    K.apply(x, r.p);
+    launch_bminus<double>(b, r.p, n, K.s);  // r = b - A x
+    const double beta = std::sqrt(K.dot(r.p, r.p));
+    *final_res = beta;
+    if (beta <= tol) {
+      *iterations = its;
+      return true;
+    }
+    if (cycle == max_restarts) break;
+    scale_copy_kernel<<<nb(n), 256, 0, K.s>>>(V[0].p, r.p, beta, n);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int j = 0;
+    for (; j < m; ++j) {
+      K.prec(V[j].p, Z[j].p);
+      K.apply(Z[j].p, w.p);
+      for (int i = 0; i <= j; ++i) {
+        const double h = K.dot(w.p, V[i].p);
+        H[i * m + j] = h;
+        lincomb_kernel<<<nb(n), 256, 0, K.s>>>(w.p, V[i].p, -h, n);
+      }
+      const double h1 = std::sqrt(K.dot(w.p, w.p));
+      H[(j + 1) * m + j] = h1;
+      ++its;
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
+        H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
+        H[i * m + j] = t;
+      }
+      const double denom = std::hypot(H[j * m + j], h1);
+      if (denom < 1e-300) break;
+      cs[j] = H[j * m + j] / denom;
+      sn[j] = h1 / denom;
+      H[j * m + j] = denom;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      if (h1 > 1e-300) scale_copy_kernel<<<nb(n), 256, 0, K.s>>>(V[j + 1].p, w.p, h1, n);
+      if (std::abs(g[j + 1]) <= tol || h1 <= 1e-300) {
+        ++j;
+        break;
+      }
+    }
+    const int used = j;
+    std::vector<double> y(used, 0.0);
+    for (int i = used - 1; i >= 0; --i) {
+      double sacc = g[i];
+      for (int k = i + 1; k < used; ++k) sacc -= H[i * m + k] * y[k];
+      y[i] = sacc / H[i * m + i];
+    }
+    for (int i = 0; i < used; ++i) lincomb_kernel<<<nb(n), 256, 0, K.s>>>(x, Z[i].p, y[i], n);
+    CK(cudaGetLastError());
+  }
+  *iterations = its;
+  return false;
+}
+
+}  // namespace
+
+emfgpu_status emfgpu_fgmres_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double abs_tol,
+                                  double rel_tol, int restart, int max_restarts, int* iterations,
+                                  double* final_residual, void* stream) {
+  if (!op || !d_b || !d_x) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    if (op->precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "fgmres: the outer operator must be fp64");
+    require_linearized(op, "fgmres");
+    CK(cudaSetDevice(op->L->device));
+    Krylov K(op, mg, static_cast<cudaStream_t>(stream));
+    int its = 0;
+    double res = 0;
+    const bool ok = fgmres(K, d_b, d_x, abs_tol, rel_tol, restart, max_restarts, &its, &res);
+    if (iterations) *iterations = its;
+    if (final_residual) *final_residual = res;
+    CK(cudaStreamSynchronize(K.s));
+    if (!ok) throw ApiError(EMFGPU_ERR_NUMERICAL, "fgmres: no convergence within restart budget");
+  });
+}
+
+void emfgpu_newton_default_config(emfgpu_newton_config* c) {
+  if (!c) return;
+  c->eps_abs = 1e-8;
+  c->eps_rel = 1e-3;
+  c->max_iter = 25;
+  c->lin_abs_tol = 1e-12;
+  c->lin_rel_tol = 1e-3;
+  c->restart = 30;
+  c->max_restarts = 40;
+}
+
+// newton_solve (solver.hpp:603-656): relinearise op and mg at u, solve
+// K du = -r with MG-preconditioned FGMRES, u += du, until ||r|| <= eps_abs or
+// <= eps_rel ||r0||.  d_u: device fp64, updated in place.
+emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, const emfgpu_newton_config* cfg,
+                                  int* newton_iterations, int* linear_iterations, double* final_residual,
+                                  void* stream) {
+  if (!op || !d_u) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    if (op->precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "newton: the operator must be fp64");
+    CK(cudaSetDevice(op->L->device));
+    emfgpu_newton_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      emfgpu_newton_default_config(&c);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Krylov K(op, mg, s);
+    const int64_t n = K.n;
+    DevVec r, rhs, du;
+    CK(cudaMalloc(&r.p, sizeof(double) * n));
+    CK(cudaMalloc(&rhs.p, sizeof(double) * n));
+    CK(cudaMalloc(&du.p, sizeof(double) * n));
+    residual_impl(op, d_u, r.p, s);
+    double rnorm = std::sqrt(K.dot(r.p, r.p));
+    const double r0 = rnorm;
+    int k = 0, lin = 0;
+    while (rnorm > c.eps_abs && rnorm > c.eps_rel * r0) {
+      if (k >= c.max_iter) throw ApiError(EMFGPU_ERR_NUMERICAL, "newton: iteration budget exhausted");
+      CK(cudaMemcpyAsync(op->d_ukd, d_u, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      op->checksum = 0;
+      linearize_impl(op, nullptr, nullptr, s);
+      if (mg) {
+        if (mg->cfg.precision == 64)
+          mg_linearize<double>(mg, d_u, s);
+        else
+          mg_linearize<float>(mg, d_u, s);
+      }
+      neg_kernel<<<nb(n), 256, 0, s>>>(rhs.p, r.p, n);
+      CK(cudaMemsetAsync(du.p, 0, sizeof(double) * n, s));
+      int its = 0;
+      double res = 0;
+      if (!fgmres(K, rhs.p, du.p, c.lin_abs_tol, c.lin_rel_tol, c.restart, c.max_restarts, &its, &res))
+        throw ApiError(EMFGPU_ERR_NUMERICAL, "newton: linear solve did not converge");
+      lin += its;
+      lincomb_kernel<<<nb(n), 256, 0, s>>>(d_u, du.p, 1.0, n);
+      residual_impl(op, d_u, r.p, s);
+      rnorm = std::sqrt(K.dot(r.p, r.p));
+      ++k;
+    }
+    check_err(op, s, nullptr, nullptr, "newton");
+    if (newton_iterations) *newton_iterations = k;
+    if (linear_iterations) *linear_iterations = lin;
+    if (final_residual) *final_residual = rnorm;
   });
 }

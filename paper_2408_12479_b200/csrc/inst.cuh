@@ -94,4 +94,15 @@ void launch_diagonal<EMF_T, EMF_P>(int model, const KArgs<EMF_T>& a, cudaStream_
   if (model == FIBER) diagonal_kernel<EMF_T, EMF_P, FIBER><<<blocks, EPB * N * N * N, 0, s>>>(b);
 }
 
+template <>
+void launch_residual<EMF_T, EMF_P>(int model, const KArgs<EMF_T>& a, cudaStream_t s) {
+  constexpr int N = EMF_P + 1, EPB = Tile<EMF_P>::EPB;
+  KArgs<EMF_T> b = a;
+  b.e_begin = 0;
+  const unsigned blocks = (unsigned)((a.nel + EPB - 1) / EPB);
+  if (model == CNH) residual_kernel<EMF_T, EMF_P, CNH><<<blocks, EPB * N * N * N, 0, s>>>(b);
+  if (model == INH) residual_kernel<EMF_T, EMF_P, INH><<<blocks, EPB * N * N * N, 0, s>>>(b);
+  if (model == FIBER) residual_kernel<EMF_T, EMF_P, FIBER><<<blocks, EPB * N * N * N, 0, s>>>(b);
+}
+
 }  // namespace emfgpu

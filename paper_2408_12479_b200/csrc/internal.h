@@ -20,6 +20,12 @@ template <typename T, int P>
 void launch_linearize(int model, const KArgs<T>& a, cudaStream_t s);
 template <typename T, int P>
 void launch_diagonal(int model, const KArgs<T>& a, cudaStream_t s);
+template <typename T, int P>
+void launch_residual(int model, const KArgs<T>& a, cudaStream_t s);
+// solver.cu: r = r - scale * load, then Dirichlet rows zeroed
+template <typename T>
+void launch_sub_load_mask(T* r, const T* load, double scale, int64_t nnodes, int mx, int my, int mz, int faces,
+                          cudaStream_t s);
 
 // gather.cu
 template <typename T>
@@ -124,6 +130,9 @@ struct emfgpu_op {
   static constexpr int kMaxChunks = 32;
   cudaEvent_t ev_h2d[kMaxChunks] = {}, ev_comp[kMaxChunks] = {}, ev_start = nullptr, ev_done = nullptr;
   cudaGraphExec_t gexec = nullptr;  // captured pipeline for (g_x, g_y, g_nch)
+  // Loads (operator.hpp:23-32, 880-1008): pressure on one face, scaled
+  void* d_load = nullptr;  // Number, n_dofs (null: no load)
+  double load_scale = 1.0;
   const void* g_x = nullptr;
   void* g_y = nullptr;
   int g_nch = 0;

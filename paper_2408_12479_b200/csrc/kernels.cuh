@@ -546,3 +546,54 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
 }
 
 }  // namespace emfgpu
+
+namespace emfgpu {
+
+// ---- residual kernel: r_e = (Grad_xi test, det J0 w_q F S J0^-T) -----------
+// element_residual_batch, operator.hpp:532-595 (material domain), thread per
+// qp, shared-memory sweeps.  Not the hot path: one launch per Newton step.
+template <typename T, int P, int MODEL>
+__global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
+    residual_kernel(const KArgs<T> a) {
+  constexpr int N = P + 1, N3 = N * N * N, EPB = Tile<P>::EPB;
+  __shared__ T sB[N * N], sD[N * N];
+  __shared__ T bufA[EPB][9][N3], bufB[EPB][9][N3];
+  const int tid = threadIdx.x;
+  const int el = tid / N3, q = tid % N3;
+  const int i = q % N, j = (q / N) % N, k = q / (N * N);
+  if (tid < N * N) {
+    sB[tid] = a.Bm[tid];
+    sD[tid] = a.Dm[tid];
+  }
+  const int64_t e = (int64_t)blockIdx.x * EPB + el;
+  const bool valid = e < a.nel;
+  const ElemPos ep = elem_pos<P>(valid ? e : 0, a.nx, a.ny, a.mx, a.my, i, j, k);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.x[3 * ep.node + c] : T(0);
+  __syncthreads();
+  T gref[9];
+  sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gref);
+  const int64_t qidx = (valid ? e : 0) * N3 + q;
+  T j0inv[9], detw;
+  load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
+  const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
+  T g[9], w[9], out[3];
+  mm(gref, j0inv, g);
+  Bundle<T> cb;
+  if (!make_strain(g, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
+  cache_scalars<T, MODEL>(mq, cb);  // lnJ (cNH), J^-2/3, fibre invariants (operator.hpp:557-566)
+  second_pk<T, MODEL>(mq, cb);
+  {
+    T fs[9];
+    mm_ts(cb.F, cb.S, fs);  // w_mat = F S (operator.hpp:568)
+    mm_bt(fs, j0inv, w);
+#pragma unroll
+    for (int m = 0; m < 9; ++m) w[m] *= detw;
+  }
+  sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
+  if (valid)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a.loc[(e * 3 + c) * N3 + q] = out[c];
+}
+
+}  // namespace emfgpu

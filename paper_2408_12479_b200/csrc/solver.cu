@@ -305,3 +305,29 @@ template void launch_jacobi<double>(const double*, const double*, double*, int64
 template void launch_jacobi<float>(const float*, const float*, float*, int64_t, cudaStream_t);
 
 }  // namespace emfgpu
+
+namespace emfgpu {
+// evaluate_residual tail (operator.hpp:638-640): r -= scale * load; Dirichlet rows = 0
+template <typename T>
+__global__ void sub_load_mask_kernel(T* r, const T* load, T scale, int64_t nnodes, int mx, int my, int mz,
+                                     int faces) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnodes) return;
+  const int a = (int)(i % mx), b = (int)((i / mx) % my), c = (int)(i / ((int64_t)mx * my));
+  const bool fixed = node_constrained(a, b, c, mx, my, mz, faces);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    T v = r[3 * i + d];
+    if (load) v -= scale * load[3 * i + d];
+    r[3 * i + d] = fixed ? T(0) : v;
+  }
+}
+template <typename T>
+void launch_sub_load_mask(T* r, const T* load, double scale, int64_t nnodes, int mx, int my, int mz, int faces,
+                          cudaStream_t s) {
+  sub_load_mask_kernel<T><<<(unsigned)((nnodes + 255) / 256), 256, 0, s>>>(r, load, T(scale), nnodes, mx, my, mz,
+                                                                            faces);
+}
+template void launch_sub_load_mask<double>(double*, const double*, double, int64_t, int, int, int, int, cudaStream_t);
+template void launch_sub_load_mask<float>(float*, const float*, double, int64_t, int, int, int, int, cudaStream_t);
+}  // namespace emfgpu

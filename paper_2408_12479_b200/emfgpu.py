@@ -93,6 +93,13 @@ class MaterialParams:
 _lib = None
 
 
+class NewtonConfig(C.Structure):
+    """NewtonConfig + FgmresConfig (solver.hpp:26-37)."""
+    _fields_ = [("eps_abs", C.c_double), ("eps_rel", C.c_double), ("max_iter", C.c_int),
+                ("lin_abs_tol", C.c_double), ("lin_rel_tol", C.c_double), ("restart", C.c_int),
+                ("max_restarts", C.c_int)]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -144,6 +151,15 @@ def lib():
             "emfgpu_bench_fma_peak": (st, [C.c_int, C.c_double, C.POINTER(C.c_double)]),
             "emfgpu_op_set_fibre_frame": (st, [vp, C.c_int]),
             "emfgpu_op_fibre_field": (st, [vp, vp, vp]),
+            "emfgpu_op_residual": (st, [vp, vp, vp, vp]),
+            "emfgpu_op_residual_host": (st, [vp, vp, vp]),
+            "emfgpu_op_set_pressure": (st, [vp, C.c_double, C.c_int]),
+            "emfgpu_op_set_load_scale": (st, [vp, C.c_double]),
+            "emfgpu_fgmres_solve": (st, [vp, vp, vp, vp, C.c_double, C.c_double, C.c_int, C.c_int,
+                                         C.POINTER(C.c_int), C.POINTER(C.c_double), vp]),
+            "emfgpu_newton_default_config": (None, [C.POINTER(NewtonConfig)]),
+            "emfgpu_newton_solve": (st, [vp, vp, vp, C.POINTER(NewtonConfig), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_double), vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -272,6 +288,10 @@ class ElasticOperator:
             _lib.emfgpu_op_destroy(self.h)
             self.h = None
 
+    def _ok(self, st):
+        if st:
+            self._raise(st)
+
     def _raise(self, st, e=None, q=None):
         msg = lib().emfgpu_op_last_error(self.h).decode()
         if st == 2 and e is not None and e.value >= 0 and "det(F)" in msg:
@@ -375,6 +395,23 @@ class ElasticOperator:
         m = np.empty(6 * nqp)
         _check(lib().emfgpu_op_fibre_field(self.h, h.ctypes.data, m.ctypes.data))
         return h, m
+
+    def set_pressure(self, pressure, face=1):
+        """Loads{pressure, pressure_face} (operator.hpp:23-32): -p N traction on `face`."""
+        self._ok(lib().emfgpu_op_set_pressure(self.h, float(pressure), int(face)))
+
+    def set_load_scale(self, scale):
+        self._ok(lib().emfgpu_op_set_load_scale(self.h, float(scale)))
+
+    def evaluate_residual(self, u) -> np.ndarray:
+        """evaluate_residual (operator.hpp:94-95): r = (Grad v, F S) - s*load, host fp64/fp32."""
+        u = np.ascontiguousarray(u, dtype=self.dtype)
+        r = np.empty_like(u)
+        self._ok(lib().emfgpu_op_residual_host(self.h, u.ctypes.data, r.ctypes.data))
+        return r
+
+    def evaluate_residual_device(self, d_u, d_r, stream=None):
+        self._ok(lib().emfgpu_op_residual(self.h, _ptr(d_u), _ptr(d_r), _stream(stream)))
 
     def estimate_eigenvalues(self, d_diag, iterations=20, seed=0x9E3779B97F4A7C15):
         lo, hi = C.c_double(), C.c_double()
@@ -525,3 +562,29 @@ def pcg_solve(op: ElasticOperator, mg: MgHierarchy | None, d_b, d_x, rtol=1e-8, 
     if st:
         op._raise(st)
     return it.value, hist[:it.value + 1]
+
+
+def fgmres_solve(op: ElasticOperator, mg: MgHierarchy | None, d_b, d_x, abs_tol=1e-12, rel_tol=1e-3, restart=30,
+                 max_restarts=40, stream=None):
+    """fgmres_solve (solver.hpp:120-203) on the device. Returns (iterations, final residual)."""
+    it, res = C.c_int(), C.c_double()
+    st = lib().emfgpu_fgmres_solve(op.h, mg.h if mg is not None else None, _ptr(d_b), _ptr(d_x), abs_tol, rel_tol,
+                                   restart, max_restarts, C.byref(it), C.byref(res), _stream(stream))
+    if st:
+        op._raise(st)
+    return it.value, res.value
+
+
+def newton_solve(op: ElasticOperator, mg: MgHierarchy | None, d_u, stream=None, **cfg):
+    """newton_solve (solver.hpp:603-656): d_u (fp64, device) in/out with the
+    op's loads.  Returns (newton iterations, total FGMRES iterations, |r|)."""
+    c = NewtonConfig()
+    lib().emfgpu_newton_default_config(C.byref(c))
+    for k, v in cfg.items():
+        setattr(c, k, v)
+    nit, lit, res = C.c_int(), C.c_int(), C.c_double()
+    st = lib().emfgpu_newton_solve(op.h, mg.h if mg is not None else None, _ptr(d_u), C.byref(c), C.byref(nit),
+                                   C.byref(lit), C.byref(res), _stream(stream))
+    if st:
+        op._raise(st)
+    return nit.value, lit.value, res.value

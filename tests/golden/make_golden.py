@@ -132,7 +132,42 @@ def multigrid():
     np.savez_compressed(os.path.join(OUT, "multigrid.npz"), **out)
 
 
+# residual + Newton cases: (name, model, lmax, p, deform amplitude, pressure)
+NEWTON = [
+    ("inh_p2_n4_curved", "inh", 2, 2, 0.05, 0.2),
+    ("cnh_p3_n2_curved", "cnh", 1, 3, 0.05, 0.1),
+    ("fiber_p2_n4_affine", "fiber", 2, 2, 0.0, 0.3),
+]
+
+
+def newton():
+    """evaluate_residual with a +x face pressure (Loads, operator.hpp:23-32) at a
+    seeded state, and the reference newton_solve (solver.hpp:603-656: FGMRES(30)
+    + MgHierarchy<float>, coarse Jacobi-PCG) for one full load increment with
+    the -x face clamped."""
+    out = {}
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=KAPPA)
+    for name, model, lmax, p, damp, pres in NEWTON:
+        n = 1 << lmax
+        L = R.RefLevel(1, lmax, p, damp, 1)
+        u = I.make_u0(n, n, n, p, amp=0.05)
+        out[f"{name}_r"] = R.residual_with_pressure(L, model, prm, pres, 1, u, 0.75)
+        x, nit, lit, res = R.newton_pressure(L, model, prm, pres, 1, 6, damp, 1, 0)
+        out[f"{name}_u"] = x
+        out[f"{name}_nit"] = nit
+        out[f"{name}_lit"] = lit
+        out[f"{name}_res"] = res
+        print("newton", name, L.ndofs, "newton its", nit, "fgmres its", lit, "res", res)
+    out["params"] = prm
+    np.savez_compressed(os.path.join(OUT, "newton.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for f in sys.argv[1:]:
+            globals()[f]()
+        sys.exit(0)
+    newton()
     multigrid()
     cfg0()
     small()

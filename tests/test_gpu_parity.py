@@ -324,3 +324,86 @@ def test_periodic_tube_vs_oracle(G, strategy):
         yo = I.open_to_periodic(orc.apply(I.periodic_to_open(v, nx, ny, nz, p).astype(orc.dtype)).astype(np.float64),
                                 nx, ny, nz, p)
         assert rel(y, yo) <= {64: 1e-12, 32: 1e-5}[prec], (prec, rel(y, yo))
+
+
+NEWTON = [("inh_p2_n4_curved", "inh", 2, 2, 0.05, 0.2), ("cnh_p3_n2_curved", "cnh", 1, 3, 0.05, 0.1),
+          ("fiber_p2_n4_affine", "fiber", 2, 2, 0.0, 0.3)]
+
+
+@pytest.mark.parametrize("case", NEWTON, ids=[c[0] for c in NEWTON])
+@pytest.mark.parametrize("prec", [64, 32])
+def test_residual_with_pressure_vs_reference(G, case, prec):
+    """evaluate_residual + face-pressure load (operator.hpp:623-641, 925-1003)
+    against the reference's own output, host and device entry points."""
+    import torch
+    name, model, lmax, p, damp, pres = case
+    g = np.load(os.path.join(GOLD, "newton.npz"))
+    n = 1 << lmax
+    lev = G.FeLevel(n, p=p, map_param=(damp,))
+    op = G.ElasticOperator(lev, model, params_from(g["params"], G), "none", prec)
+    op.set_pressure(pres, 1)
+    op.set_load_scale(0.75)
+    u = I.make_u0(n, n, n, p, amp=0.05)
+    r = op.evaluate_residual(u)
+    assert rel(r, g[f"{name}_r"]) <= TOL[prec], rel(r, g[f"{name}_r"])
+    mask = I.dirichlet_mask(n, n, n, p, 1)
+    assert np.all(r[mask] == 0)
+    du = torch.tensor(u.astype(op.dtype), device="cuda")
+    dr = torch.empty_like(du)
+    op.evaluate_residual_device(du, dr)
+    torch.cuda.synchronize()
+    assert np.array_equal(dr.cpu().numpy(), r)
+
+
+@pytest.mark.parametrize("case", NEWTON, ids=[c[0] for c in NEWTON])
+def test_newton_fgmres_mg_vs_reference(G, case):
+    """newton_solve (solver.hpp:603-656) with FGMRES(30) right-preconditioned
+    by the fp32 hp-multigrid V-cycle, one full pressure increment: the same
+    Newton iteration count as the reference, FGMRES iterations within +-1 per
+    Newton step, the same converged displacement."""
+    import torch
+    name, model, lmax, p, damp, pres = case
+    g = np.load(os.path.join(GOLD, "newton.npz"))
+    n = 1 << lmax
+    prm = params_from(g["params"], G)
+    lev = G.FeLevel(n, p=p, map_param=(damp,))
+    op = G.ElasticOperator(lev, model, prm, "none", 64)
+    op.set_pressure(pres, 1)
+    mg = G.MgHierarchy(lev, model, prm, degree=6, coarse_n=1, precision=32)
+    u = torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda")
+    nit, lit, res = G.newton_solve(op, mg, u)
+    ref_nit, ref_lit = int(g[f"{name}_nit"]), int(g[f"{name}_lit"])
+    assert nit == ref_nit, (nit, ref_nit)
+    assert abs(lit - ref_lit) <= nit, (lit, ref_lit)
+    assert res <= 1e-3 * np.linalg.norm(op_residual_at_zero(G, lev, model, prm, pres)) or res <= 1e-8
+    assert rel(u.cpu().numpy(), g[f"{name}_u"]) <= 1e-5
+
+
+def op_residual_at_zero(G, lev, model, prm, pres):
+    op = G.ElasticOperator(lev, model, prm, "none", 64)
+    op.set_pressure(pres, 1)
+    return op.evaluate_residual(np.zeros(lev.n_dofs))
+
+
+def test_fgmres_linear_solve_matches_pcg_solution(G):
+    """Device FGMRES (solver.hpp:120-203) on the SPD cfg4-variant system: the
+    same solution as PCG, identity preconditioner and multigrid."""
+    import torch
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    lev = G.FeLevel(4, p=2)
+    op = G.ElasticOperator(lev, "inh", prm, "none", 64)
+    op.update_linearization(np.zeros(lev.n_dofs))
+    b = I.make_v(lev.n_dofs, 12)
+    b[I.dirichlet_mask(4, 4, 4, 2, 1)] = 0.0
+    db = torch.tensor(b, device="cuda")
+    x_cg = torch.zeros_like(db)
+    its, hist = G.pcg_solve(op, None, db, x_cg, 1e-12, 2000)
+    mg = G.MgHierarchy(lev, "inh", prm, degree=5, precision=32)
+    mg.update_linearization(torch.zeros_like(db))
+    for pre, m in ((None, 400), (mg, 30)):
+        x = torch.zeros_like(db)
+        it, res = G.fgmres_solve(op, pre, db, x, abs_tol=0.0, rel_tol=1e-10, restart=m, max_restarts=20)
+        assert res <= 1e-10 * np.linalg.norm(b)
+        assert rel(x.cpu().numpy(), x_cg.cpu().numpy()) <= 1e-6
+        if pre is mg:
+            assert it < 60

@@ -179,3 +179,23 @@ def test_oracle_replicated_frames_equal_global_frame():
     op.set_frames(h, m1)
     op.update_linearization(g["u0"])
     assert np.array_equal(op.apply(g["v"]), g["y64_none"])
+
+
+NEWTON = [("inh_p2_n4_curved", "inh", 2, 2, 0.05, 0.2), ("cnh_p3_n2_curved", "cnh", 1, 3, 0.05, 0.1),
+          ("fiber_p2_n4_affine", "fiber", 2, 2, 0.0, 0.3)]
+
+
+@pytest.mark.parametrize("case", NEWTON, ids=[c[0] for c in NEWTON])
+def test_oracle_residual_with_pressure_bitexact(case):
+    """evaluate_residual with a +x face pressure at load scale 0.75 against the
+    reference's own evaluate_residual (golden newton.npz)."""
+    name, model, lmax, p, damp, pres = case
+    g = np.load(os.path.join(GOLD, "newton.npz"))
+    n = 1 << lmax
+    coords = O.lattice_coords(n, n, n, p, map_kind=0, prm=(damp, 1.0))
+    op = O.OracleOperator(n, n, n, p, coords, 1, model, g["params"], "none", 64)
+    u = I.make_u0(n, n, n, p, amp=0.05)
+    assert np.array_equal(op.residual(u, pres, 1, 0.75), g[f"{name}_r"])
+    # the load alone: r(0) = -s * load on free rows; total force = p * area along -x
+    load = op.pressure_load(pres, 1)
+    assert np.isclose(load[0::3].sum(), -pres * 1.0, rtol=1e-12) or damp != 0.0
