@@ -33,7 +33,10 @@ enum { ORC_NONE = 0, ORC_SCALAR = 1, ORC_TENSOR = 2 };
 enum {
   ORC_C_LNJ = 0, ORC_C_JM1, ORC_C_JP, ORC_C_C1, ORC_C_C2, ORC_C_C3, ORC_C_IS = ORC_C_C3 + 2,
   ORC_C_EF = ORC_C_IS + 2, ORC_C_F = ORC_C_EF + 2, ORC_C_FINV = ORC_C_F + 9, ORC_C_S = ORC_C_FINV + 9,
-  ORC_C_CINV = ORC_C_S + 6, ORC_CACHE_STRIDE = ORC_C_CINV + 6
+  ORC_C_CINV = ORC_C_S + 6,
+  /* spatial domain (operator.hpp:139-143): 1/J, J_t, tau, b, F H_i F^T */
+  ORC_C_INVJ = ORC_C_CINV + 6, ORC_C_JT = ORC_C_INVJ + 1, ORC_C_TAU = ORC_C_JT + 9, ORC_C_B = ORC_C_TAU + 6,
+  ORC_C_FH = ORC_C_B + 6, ORC_CACHE_STRIDE = ORC_C_FH + 12
 };
 
 typedef struct {
@@ -54,6 +57,7 @@ typedef struct orc_op {
   orc_basis basis;
   orc_material mat;
   int strategy, precision;
+  int spatial; /* Domain::spatial (material.hpp:18) */
   double* jac;      /* nel*nq3*9, owned */
   uint8_t* mask;    /* ndofs, owned */
   double* uk;       /* ndofs, owned */
@@ -468,6 +472,11 @@ void orc_op_destroy(orc_op* op) {
 }
 
 int64_t orc_op_ndofs(const orc_op* op) { return op->ndofs; }
+/* Formulation::domain (material.hpp:18-23): 0 material, 1 spatial; before linearize. */
+void orc_op_set_domain(orc_op* op, int spatial) {
+  op->spatial = spatial;
+  op->linearized = 0;
+}
 void orc_op_jacobians(const orc_op* op, double* out) { memcpy(out, op->jac, sizeof(double) * op->nel * op->nq3 * 9); }
 void orc_op_mask(const orc_op* op, uint8_t* out) { memcpy(out, op->mask, op->ndofs); }
 
@@ -477,7 +486,8 @@ int orc_op_linearize(orc_op* op, const double* u, int64_t* bad_e, int* bad_q) {
   memcpy(op->uk, u, sizeof(double) * op->ndofs);
   free(op->cache);
   op->cache = NULL;
-  if (op->strategy != ORC_NONE) op->cache = (double*)calloc(op->nel * op->nq3 * ORC_CACHE_STRIDE, sizeof(double));
+  if (op->strategy != ORC_NONE || op->spatial)
+    op->cache = (double*)calloc(op->nel * op->nq3 * ORC_CACHE_STRIDE, sizeof(double));
   int64_t first = INT64_MAX;
 #pragma omp parallel
   {
@@ -504,6 +514,25 @@ int orc_op_linearize(orc_op* op, const double* u, int64_t* bad_e, int* bad_q) {
           continue;
         }
         second_pk_d(&mq, &c, c.S);
+        if (op->spatial) {
+          /* operator.hpp:736-744: 1/J and J_t = J0 + Grad_xi u_k, det J_t > 0 */
+          double* sc = op->cache + at * ORC_CACHE_STRIDE;
+          double jt[9];
+          for (int k = 0; k < 9; ++k) jt[k] = J0[k] + gref[k];
+          if (!(det_d(jt) > 0)) {
+            if (at < first) first = at;
+            continue;
+          }
+          spatial_cell_d(&mq, &c);
+          sc[ORC_C_INVJ] = 1.0 / c.jac;
+          for (int k = 0; k < 9; ++k) sc[ORC_C_JT + k] = jt[k];
+          for (int k = 0; k < 6; ++k) {
+            sc[ORC_C_TAU + k] = c.tau[k];
+            sc[ORC_C_B + k] = c.b[k];
+            sc[ORC_C_FH + k] = c.fh[0][k];
+            sc[ORC_C_FH + 6 + k] = c.fh[1][k];
+          }
+        }
         if (op->cache) {
           double* sc = op->cache + at * ORC_CACHE_STRIDE;
           sc[ORC_C_LNJ] = c.lnj;

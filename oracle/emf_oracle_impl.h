@@ -135,6 +135,7 @@ static inline R SFX(fast_jpow)(R jm1) {
 typedef struct {
   R jm1, jac, lnj, jp, c1, c2, c3[2], istar[2], efib[2];
   R F[9], Finv[9], S[6], Cinv[6], E[6], i1;
+  R bt[6], b[6], tau[6], fh[2][6]; /* spatial cell: Green-Euler bt, b = F F^T, tau, F H_i F^T */
 } SFX(qpc);
 
 /* make_strain (stable) constitutive.hpp:43-57 + compute_cache :326-377,
@@ -156,6 +157,15 @@ static int SFX(compute_cache)(const orc_material* mat, const R* g, SFX(qpc)* c) 
       for (int j = i; j < 3; ++j) {
         const R q = (g[i] * g[j] + g[3 + i] * g[3 + j]) + g[6 + i] * g[6 + j];
         c->E[SFX(sidx)(i, j)] = half * ((g[3 * i + j] + g[3 * j + i]) + q);
+      }
+  }
+  /* green_euler_stable tensor.hpp:259-270 */
+  {
+    const R half = (R)0.5;
+    for (int i = 0; i < 3; ++i)
+      for (int j = i; j < 3; ++j) {
+        const R q = (g[3 * i] * g[3 * j] + g[3 * i + 1] * g[3 * j + 1]) + g[3 * i + 2] * g[3 * j + 2];
+        c->bt[SFX(sidx)(i, j)] = half * ((g[3 * i + j] + g[3 * j + i]) + q);
       }
   }
   if (SFX(inverse)(Fm, c->Finv)) return 2;
@@ -229,6 +239,88 @@ static void SFX(second_pk)(const orc_material* mat, const SFX(qpc)* c, R* S) {
       const R coef = c->c3[f] * c->efib[f];
       for (int k = 0; k < 6; ++k) S[k] += coef * (R)mat->h[f][k];
     }
+}
+
+/* Spatial cell of compute_cache (constitutive.hpp:371-376): b = 2 bt + I,
+ * tau = kirchhoff_base (:240-283, stable) + sum c3 E_i F H_i F^T with
+ * push_forward (tensor.hpp:332-341).  Reads bt, jm1, F, lnj, jp, c3, efib. */
+static void SFX(spatial_cell)(const orc_material* mat, SFX(qpc)* c) {
+  const R mu = (R)mat->mu;
+  for (int k = 0; k < 6; ++k) c->b[k] = (R)2 * c->bt[k];
+  c->b[0] += (R)1;
+  c->b[1] += (R)1;
+  c->b[2] += (R)1;
+  if (mat->model == 0) {
+    const R lam = (R)mat->lambda;
+    for (int k = 0; k < 6; ++k) c->tau[k] = ((R)2 * mu) * c->bt[k];
+    const R v = ((R)2 * lam) * c->lnj;
+    c->tau[0] += v;
+    c->tau[1] += v;
+    c->tau[2] += v;
+  } else {
+    const R half_k = (R)(0.5 * mat->kappa);
+    const R vol = half_k * (c->jm1 * (c->jm1 + (R)2));
+    const R trb3 = ((c->bt[0] + c->bt[1]) + c->bt[2]) * ((R)1 / (R)3);
+    const R s2 = ((R)2 * mu) * c->jp;
+    for (int k = 0; k < 6; ++k) c->tau[k] = s2 * c->bt[k];
+    const R v = vol - s2 * trb3;
+    c->tau[0] += v;
+    c->tau[1] += v;
+    c->tau[2] += v;
+  }
+  for (int f = 0; f < 2; ++f)
+    for (int k = 0; k < 6; ++k) c->fh[f][k] = (R)0;
+  if (mat->model == 2)
+    for (int f = 0; f < 2; ++f) {
+      R h[6], fhm[9];
+      for (int k = 0; k < 6; ++k) h[k] = (R)mat->h[f][k];
+      SFX(mm_ts)(c->F, h, fhm);
+      for (int i = 0; i < 3; ++i)
+        for (int j = i; j < 3; ++j)
+          c->fh[f][SFX(sidx)(i, j)] =
+              (fhm[3 * i] * c->F[3 * j] + fhm[3 * i + 1] * c->F[3 * j + 1]) + fhm[3 * i + 2] * c->F[3 * j + 2];
+      const R coef = c->c3[f] * c->efib[f];
+      for (int k = 0; k < 6; ++k) c->tau[k] += coef * c->fh[f][k];
+    }
+}
+
+/* tangent_spatial constitutive.hpp:421-463: J c : (grad du)^S + (grad du) tau. */
+static void SFX(tangent_spatial)(const orc_material* mat, const SFX(qpc)* c, const R* dgrad, R* out) {
+  const R mu = (R)mat->mu;
+  R xs[6], jc[6], gt[9];
+  SFX(sym_part)(dgrad, xs);
+  const R trx = (dgrad[0] + dgrad[4]) + dgrad[8];
+  if (mat->model == 0) {
+    const R lam = (R)mat->lambda;
+    const R f = (R)2 * (mu - ((R)2 * lam) * c->lnj);
+    for (int k = 0; k < 6; ++k) jc[k] = f * xs[k];
+    const R v = ((R)2 * lam) * trx;
+    jc[0] += v;
+    jc[1] += v;
+    jc[2] += v;
+  } else {
+    const R bx = SFX(ddot_s)(c->b, xs);
+    const R ttmj = (((R)2 * mu) / (R)3) * c->jp;
+    const R f0 = -ttmj * trx;
+    for (int k = 0; k < 6; ++k) jc[k] = f0 * c->b[k];
+    const R m2c1 = (R)-2 * c->c1;
+    for (int k = 0; k < 6; ++k) jc[k] += m2c1 * xs[k];
+    const R v = c->c2 * trx - ttmj * bx;
+    jc[0] += v;
+    jc[1] += v;
+    jc[2] += v;
+    if (mat->model == 2) {
+      const R k2 = (R)mat->k2;
+      for (int f = 0; f < 2; ++f) {
+        const R fhx = SFX(ddot_s)(c->fh[f], xs);
+        const R coef = (((R)2 * c->c3[f]) * ((((R)2 * k2) * c->efib[f]) * c->efib[f] + (R)1)) * fhx;
+        for (int k = 0; k < 6; ++k) jc[k] += coef * c->fh[f][k];
+      }
+    }
+  }
+  SFX(mm_ts)(dgrad, c->tau, gt);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) out[3 * i + j] = jc[SFX(sidx)(i, j)] + gt[3 * i + j];
 }
 
 /* tangent_material constitutive.hpp:381-419 */
@@ -344,7 +436,9 @@ static void SFX(scatter_grad)(const orc_basis* b, const R* g0, const R* g1, cons
 
 /* qp_cache_for_apply operator.hpp:390-434: builds the bundle at (e,q) for the
  * active strategy. gk = Grad u_k (reference gradient times J0^-1). */
+static int SFX(bundle_spatial)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)* c);
 static int SFX(bundle)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)* c) {
+  if (op->spatial) return SFX(bundle_spatial)(op, e, q, gk, c);
   const int64_t at = e * op->nq3 + q;
   const orc_material mq = orc_mat_at(op, at);
   if (op->strategy == ORC_TENSOR || op->strategy == ORC_SCALAR) {
@@ -394,6 +488,51 @@ static int SFX(bundle)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)
   return 0;
 }
 
+/* qp_cache_for_apply, spatial cell (operator.hpp:393-434, 362-370):
+ * none recomputes, scalar loads the scalars and rebuilds b, tau, F H F^T from
+ * G_k, tensor loads tau, b, F H F^T. */
+static int SFX(bundle_spatial)(const orc_op* op, int64_t e, int q, const R* gk, SFX(qpc)* c) {
+  const int64_t at = e * op->nq3 + q;
+  const orc_material mq = orc_mat_at(op, at);
+  if (op->strategy == ORC_NONE) {
+    if (SFX(compute_cache)(&mq, gk, c)) return 1;
+    SFX(spatial_cell)(&mq, c);
+    return 0;
+  }
+  const double* sc = op->cache + at * ORC_CACHE_STRIDE;
+  c->lnj = (R)sc[ORC_C_LNJ];
+  if (op->mat.model != 0) {
+    c->jm1 = (R)sc[ORC_C_JM1];
+    c->jp = (R)sc[ORC_C_JP];
+    c->c1 = (R)sc[ORC_C_C1];
+    c->c2 = (R)sc[ORC_C_C2];
+  } else {
+    c->jm1 = c->c1 = c->c2 = (R)0;
+    c->jp = (R)1;
+  }
+  for (int f = 0; f < 2; ++f) {
+    c->c3[f] = op->mat.model == 2 ? (R)sc[ORC_C_C3 + f] : (R)0;
+    c->istar[f] = op->mat.model == 2 ? (R)sc[ORC_C_IS + f] : (R)0;
+    c->efib[f] = op->mat.model == 2 ? (R)sc[ORC_C_EF + f] : (R)0;
+  }
+  if (op->strategy == ORC_TENSOR) {
+    for (int k = 0; k < 6; ++k) {
+      c->tau[k] = (R)sc[ORC_C_TAU + k];
+      c->b[k] = op->mat.model != 0 ? (R)sc[ORC_C_B + k] : (R)0;
+      c->fh[0][k] = op->mat.model == 2 ? (R)sc[ORC_C_FH + k] : (R)0;
+      c->fh[1][k] = op->mat.model == 2 ? (R)sc[ORC_C_FH + 6 + k] : (R)0;
+    }
+    return 0;
+  }
+  SFX(qpc) s;
+  if (SFX(compute_cache)(&mq, gk, &s)) return 1;
+  c->jm1 = s.jm1; /* kirchhoff_base reads J-1 from the strain state */
+  for (int k = 0; k < 9; ++k) c->F[k] = s.F[k];
+  for (int k = 0; k < 6; ++k) c->bt[k] = s.bt[k];
+  SFX(spatial_cell)(&mq, c);
+  return 0;
+}
+
 /* Per-element scratch for one element. */
 typedef struct {
   R loc[3][ORC_MAXN3], uk[3][ORC_MAXN3], out[3][ORC_MAXN3];
@@ -432,6 +571,35 @@ static int SFX(element_tangent)(const orc_op* op, int64_t e, const R* input, con
     R j0[9], det0, j0inv[9], gref[9], dg[9], gk[9], ds[6], t1[9], t2[9], wm[9], j0t[9], wr[9];
     const int qa = q % nq, qb = (q / nq) % nq, qc = q / (nq * nq);
     const R wq = (R)(b->qwts[qa] * b->qwts[qb] * b->qwts[qc]);
+    if (op->spatial) {
+      /* operator.hpp:506-519: grad du = Grad_xi du J_t^-1, w = (1/J) det J_t w_q (.) J_t^-T */
+      const double* sc = op->cache + (e * nq3 + q) * ORC_CACHE_STRIDE;
+      R jt[9], jtinv[9], wsp[9];
+      for (int k = 0; k < 9; ++k) jt[k] = (R)sc[ORC_C_JT + k];
+      if (SFX(inverse)(jt, jtinv)) return 2;
+      const R detjt = SFX(det)(jt);
+      const R invj = (R)sc[ORC_C_INVJ];
+      for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d) gref[3 * c + d] = s->g[c][d][q];
+      SFX(mm)(gref, jtinv, dg);
+      if (need_uk) {
+        SFX(qp_mapping)(op, e, q, j0, &det0);
+        if (SFX(inverse)(j0, j0inv)) return 2;
+        for (int c = 0; c < 3; ++c)
+          for (int d = 0; d < 3; ++d) gref[3 * c + d] = s->gk[c][d][q];
+        SFX(mm)(gref, j0inv, gk);
+      }
+      SFX(qpc) cache;
+      if (SFX(bundle)(op, e, q, gk, &cache)) return 1;
+      const orc_material mq = orc_mat_at(op, e * op->nq3 + q);
+      SFX(tangent_spatial)(&mq, &cache, dg, wsp);
+      SFX(transpose)(jtinv, j0t);
+      SFX(mm)(wsp, j0t, wr);
+      const R sc2 = (invj * detjt) * wq;
+      for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d) s->g[c][d][q] = sc2 * wr[3 * c + d];
+      continue;
+    }
     SFX(qp_mapping)(op, e, q, j0, &det0);
     if (SFX(inverse)(j0, j0inv)) return 2;
     for (int c = 0; c < 3; ++c)
@@ -548,6 +716,23 @@ static int SFX(residual)(const orc_op* op, const R* u, const double* load, doubl
             bad = 1;
             break;
           }
+          if (op->spatial) {
+            /* operator.hpp:572-588: J_t = J0 + Grad_xi u, w = (1/J) det J_t w_q tau J_t^-T */
+            R jt[9], jtinv[9], tf[9];
+            for (int k = 0; k < 9; ++k) jt[k] = j0[k] + gref[k];
+            if (SFX(inverse)(jt, jtinv)) bad = 1;
+            const R detjt = SFX(det)(jt);
+            const R invj = (R)1 / c.jac;
+            SFX(spatial_cell)(&mq, &c);
+            for (int i2 = 0; i2 < 3; ++i2)
+              for (int j2 = 0; j2 < 3; ++j2) tf[3 * i2 + j2] = c.tau[SFX(sidx)(i2, j2)];
+            SFX(transpose)(jtinv, j0t);
+            SFX(mm)(tf, j0t, wr);
+            const R sc2 = (invj * detjt) * wq;
+            for (int cc = 0; cc < 3; ++cc)
+              for (int d = 0; d < 3; ++d) s->g[cc][d][q] = sc2 * wr[3 * cc + d];
+            continue;
+          }
           SFX(second_pk)(&mq, &c, S);
           SFX(mm_ts)(c.F, S, wm);
           SFX(transpose)(j0inv, j0t);
@@ -604,6 +789,7 @@ static int SFX(diagonal)(const orc_op* op, R* diag, int64_t* n_bad) {
       SFX(qpc)* bundles = (SFX(qpc)*)malloc(sizeof(SFX(qpc)) * ORC_MAXN3);
       R* j0inv = (R*)malloc(sizeof(R) * 9 * ORC_MAXN3);
       R* det0w = (R*)malloc(sizeof(R) * ORC_MAXN3);
+      R* jts = (R*)malloc(sizeof(R) * 9 * ORC_MAXN3);
 #pragma omp for schedule(static)
       for (int64_t t = 0; t < cnt; ++t) {
         const int i = ci + 2 * (int)(t % nci);
@@ -630,6 +816,13 @@ static int SFX(diagonal)(const orc_op* op, R* diag, int64_t* n_bad) {
           }
           if (SFX(bundle)(op, e, q, gk, &bundles[q])) bad = 1;
           det0w[q] = det0 * wq;
+          if (op->spatial) {
+            const double* sc = op->cache + (e * nq3 + q) * ORC_CACHE_STRIDE;
+            R jt[9];
+            for (int k = 0; k < 9; ++k) jt[k] = (R)sc[ORC_C_JT + k];
+            if (SFX(inverse)(jt, jts + 9 * q)) bad = 1;
+            det0w[q] = ((R)sc[ORC_C_INVJ] * SFX(det)(jt)) * wq;
+          }
         }
         if (bad) {
 #pragma omp atomic write
@@ -645,8 +838,17 @@ static int SFX(diagonal)(const orc_op* op, R* diag, int64_t* n_bad) {
             R gref[9], dg[9], ds[6], t1[9], t2[9], wm[9], jt[9], wr[9];
             for (int c = 0; c < 3; ++c)
               for (int d = 0; d < 3; ++d) gref[3 * c + d] = s->g[c][d][q];
-            SFX(mm)(gref, j0inv + 9 * q, dg);
             const orc_material mq = orc_mat_at(op, e * op->nq3 + q);
+            if (op->spatial) {
+              SFX(mm)(gref, jts + 9 * q, dg);
+              SFX(tangent_spatial)(&mq, &bundles[q], dg, wm);
+              SFX(transpose)(jts + 9 * q, jt);
+              SFX(mm)(wm, jt, wr);
+              for (int c = 0; c < 3; ++c)
+                for (int d = 0; d < 3; ++d) s->g[c][d][q] = det0w[q] * wr[3 * c + d];
+              continue;
+            }
+            SFX(mm)(gref, j0inv + 9 * q, dg);
             SFX(tangent_material)(&mq, &bundles[q], dg, ds);
             SFX(mm_ts)(dg, bundles[q].S, t1);
             SFX(mm_ts)(bundles[q].F, ds, t2);
@@ -666,6 +868,7 @@ static int SFX(diagonal)(const orc_op* op, R* diag, int64_t* n_bad) {
       free(bundles);
       free(j0inv);
       free(det0w);
+      free(jts);
     }
   }
   int64_t nb = 0;

@@ -45,6 +45,7 @@ def lib():
         L.orc_structure_tensors.argtypes = [vp, vp]
         L.orc_op_element_locals.argtypes = [vp, vp, vp, i64, i64]
         L.orc_op_set_frames.argtypes = [vp, vp, vp]
+        L.orc_op_set_domain.argtypes = [vp, C.c_int]
         L.orc_op_residual.argtypes = [vp, vp, vp, C.c_double, C.c_int, C.c_double, vp]
         L.orc_pressure_load.argtypes = [vp, vp, C.c_double, C.c_int, vp]
         L.orc_basis_tables.argtypes = [C.c_int] + [vp] * 5
@@ -84,10 +85,10 @@ def structure_tensors(params):
 
 
 class OracleOperator:
-    """Mirror of ElasticOperator<Number> (operator.hpp:49-204), material domain."""
+    """Mirror of ElasticOperator<Number> (operator.hpp:49-204); domain 0 material, 1 spatial."""
 
     def __init__(self, nx, ny, nz, p, coords=None, faces=1, model="cnh", params=None,
-                 strategy="none", precision=64):
+                 strategy="none", precision=64, domain=0):
         from oracle.refbind import material_params
         if coords is None:
             coords = lattice_coords(nx, ny, nz, p)
@@ -100,6 +101,7 @@ class OracleOperator:
                                      STRATEGIES[strategy], precision)
         if not self.h:
             raise OracleError(1, "create")
+        lib().orc_op_set_domain(self.h, int(domain))
         self.n = lib().orc_op_ndofs(self.h)
 
     def __del__(self):

@@ -162,11 +162,39 @@ def newton():
     np.savez_compressed(os.path.join(OUT, "newton.npz"), **out)
 
 
+SPATIAL = [("cnh_p3_n2_curved", "cnh", 1, 3, 0.05), ("inh_p2_n4_curved", "inh", 2, 2, 0.05),
+           ("fiber_p2_n2_curved", "fiber", 1, 2, 0.05), ("inh_p4_n2_affine", "inh", 1, 4, 0.0)]
+
+
+def spatial():
+    """Spatial-domain (Omega_t) operator, Formulation{stable, spatial}
+    (operator.hpp:506-519, constitutive.hpp:421-463): apply for every strategy
+    and precision, diagonal, residual."""
+    out = {}
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=KAPPA)
+    for name, model, lmax, p, damp in SPATIAL:
+        n = 1 << lmax
+        L = R.RefLevel(1, lmax, p, damp, 1)
+        u0 = I.make_u0(n, n, n, p, amp=0.05)
+        v = I.make_v(L.ndofs)
+        for prec in (64, 32):
+            for strat in ("none", "scalar", "tensor"):
+                op = R.RefOperator(L, model, prm, strat, prec, domain=1)
+                op.update_linearization(u0)
+                out[f"{name}_y{prec}_{strat}"] = op.apply(v.astype(op.dtype))
+            out[f"{name}_diag{prec}"] = op.diagonal()[0]
+            out[f"{name}_r{prec}"] = op.residual(u0.astype(op.dtype))
+        print("spatial", name, L.ndofs)
+    out["params"] = prm
+    np.savez_compressed(os.path.join(OUT, "spatial.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for f in sys.argv[1:]:
             globals()[f]()
         sys.exit(0)
+    spatial()
     newton()
     multigrid()
     cfg0()

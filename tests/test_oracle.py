@@ -199,3 +199,27 @@ def test_oracle_residual_with_pressure_bitexact(case):
     # the load alone: r(0) = -s * load on free rows; total force = p * area along -x
     load = op.pressure_load(pres, 1)
     assert np.isclose(load[0::3].sum(), -pres * 1.0, rtol=1e-12) or damp != 0.0
+
+
+SPATIAL = [("cnh_p3_n2_curved", "cnh", 1, 3, 0.05), ("inh_p2_n4_curved", "inh", 2, 2, 0.05),
+           ("fiber_p2_n2_curved", "fiber", 1, 2, 0.05), ("inh_p4_n2_affine", "inh", 1, 4, 0.0)]
+
+
+@pytest.mark.parametrize("case", SPATIAL, ids=[c[0] for c in SPATIAL])
+def test_oracle_spatial_domain_bitexact(case):
+    """Spatial (Omega_t) formulation: apply (3 strategies x 2 precisions),
+    diagonal and residual bit-exact to the reference (golden spatial.npz)."""
+    name, model, lmax, p, damp = case
+    g = np.load(os.path.join(GOLD, "spatial.npz"))
+    n = 1 << lmax
+    coords = O.lattice_coords(n, n, n, p, map_kind=0, prm=(damp, 1.0))
+    u0 = I.make_u0(n, n, n, p, amp=0.05)
+    v = I.make_v(u0.size)
+    for prec in (64, 32):
+        dt = np.float64 if prec == 64 else np.float32
+        for strat in ("none", "scalar", "tensor"):
+            op = O.OracleOperator(n, n, n, p, coords, 1, model, g["params"], strat, prec, domain=1)
+            op.update_linearization(u0)
+            assert np.array_equal(op.apply(v.astype(dt)), g[f"{name}_y{prec}_{strat}"]), (prec, strat)
+        assert np.array_equal(op.diagonal()[0], g[f"{name}_diag{prec}"])
+        assert np.array_equal(op.residual(u0.astype(dt)), g[f"{name}_r{prec}"])
