@@ -238,12 +238,15 @@ def run_gpu(args):
     head = None
     launches = 0
     order = [(64, "none"), (64, "cachedF"), (64, "scalar"), (64, "tensor"),
-             (32, "none"), (32, "cachedF"), (32, "scalar"), (32, "tensor")]
+             (32, "none"), (32, "cachedF"), (32, "scalar"), (32, "tensor"),
+             (64, "spatial_none"), (64, "spatial_tensor"), (32, "spatial_none"), (32, "spatial_tensor")]
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.__enter__()
     for prec, strat in order:
-        op = G.ElasticOperator(lev, "cnh", params, strat, prec)
+        spatial = strat.startswith("spatial_")
+        op = G.ElasticOperator(lev, "cnh", params, strat.replace("spatial_", ""), prec,
+                               domain="spatial" if spatial else "material")
         op.update_linearization(u0)
         dt = torch.float64 if prec == 64 else torch.float32
         sop = SlabOperator(op, part, dt)
@@ -275,6 +278,8 @@ def run_gpu(args):
             by = bytes_per_apply(strat, prec, lev.n_dofs, part.nel_local)
             rec["element_kernel_tflops"] = fl / (ms_elem * 1e-3) / 1e12
             rec["element_kernel_gbs"] = by / (ms_elem * 1e-3) / 1e9
+        else:  # spatial: bytes from the operator's own ledger (J_t, 1/J, caches, vectors)
+            rec["element_kernel_gbs"] = op.byte_ledger().traffic_per_dof * lev.n_dofs / (ms_elem * 1e-3) / 1e9
         variants[f"fp{prec}_{strat}"] = rec
         if (prec, strat) == (64, "none"):
             head = (op, sop, x, y, rec)
@@ -335,7 +340,8 @@ def run_gpu(args):
     hbm = peaks.get("hbm_gbs", 6650.0)
     for k, r in variants.items():
         pk = fp64_peak if k.startswith("fp64") else fp32_peak
-        r["fma_frac"] = r["element_kernel_tflops"] / pk
+        if "element_kernel_tflops" in r:
+            r["fma_frac"] = r["element_kernel_tflops"] / pk
         r["hbm_frac"] = r["element_kernel_gbs"] / hbm
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")

@@ -102,7 +102,9 @@ emfgpu_status emfgpu_level_coords(const emfgpu_level* l, double* host_out); /* n
 const char* emfgpu_level_last_error(const emfgpu_level* l);
 
 /* ---- operator (ElasticOperator<Number>, operator.hpp:49-204) ---------------
- * domain: 0 material (spatial is not supported yet -> EMFGPU_ERR_CONFIG).
+ * domain: 0 material, 1 spatial (Formulation::domain, material.hpp:18-23; the
+ * spatial form integrates on Omega_t with per-qp J_t and 1/J, operator.hpp:506-519;
+ * cachedF is material-only -> EMFGPU_ERR_CONFIG).
  * precision: 64 (double) or 32 (float): the Number template argument. */
 emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_material* params, int domain,
                                int strategy, int precision, emfgpu_op** out);
@@ -225,7 +227,7 @@ emfgpu_status emfgpu_op_set_fibre_frame(emfgpu_op* op, int kind);
 emfgpu_status emfgpu_op_fibre_field(const emfgpu_op* op, double* h_out, double* m1_out);
 
 /* ---- residual and loads ----------------------------------
- * evaluate_residual(u, r), operator.hpp:94-95/623-641 (material domain):
+ * evaluate_residual(u, r), operator.hpp:94-95/623-641 (both domains):
  * r_i = (Grad v_i, F S) - load_scale * load_i, Dirichlet rows zeroed. */
 emfgpu_status emfgpu_op_residual(emfgpu_op* op, const void* d_u, void* d_r, void* stream);
 emfgpu_status emfgpu_op_residual_host(emfgpu_op* op, const void* u, void* r);

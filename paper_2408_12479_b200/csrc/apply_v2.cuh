@@ -268,7 +268,7 @@ __device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 struct ApplyV2Smem {
   static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
-  static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR);
+  static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR);
   static constexpr int NST = kUk ? 6 : 3;  // staged fields: x (3) [+ u_k (3)]
   static constexpr int SZ = Lay<N>::SIZE;
   T stage[2][EPB][NST][SZ];
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
 #pragma unroll
         for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][3 + c][qs], a.uk + 3 * ep.node + c);
       }
-      if (a.affine)
+      if (a.affine && (!is_spatial(STRAT) || kUk))
         for (int f = q; f < 10; f += N3) cp_async_T(&sm.geo[b][el][f], a.geo + f * a.geo_stride + e);
     }
     cp_async_commit();
@@ -357,10 +357,18 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     const int64_t qidx = (valid ? e : a.e_begin) * N3 + q;
     const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
     T j0inv[9], detw;
-    if (!CART && !a.affine) {
+    if ((!is_spatial(STRAT) || kUk) && !CART && !a.affine) {
 #pragma unroll
       for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];
       detw = a.geo[9 * a.geo_stride + qidx];
+    }
+    const T* cs = a.cache;
+    const int64_t st = a.cache_stride;
+    T sj[10];  // spatial: J_t (9) and 1/J, loaded before the sweeps
+    if constexpr (is_spatial(STRAT)) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) sj[m] = cs[(C_JT + m) * st + qidx];
+      sj[9] = cs[C_INVJ * st + qidx];
     }
     esync();
 
@@ -387,8 +395,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       detw = sm.geo[buf][el][9] * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
     }
     Bundle<T> cb;
-    const T* cs = a.cache;
-    const int64_t st = a.cache_stride;
+    SpCell<T> sp;
     if constexpr (kUk) {
       esync();
       fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
@@ -406,24 +413,17 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       } else {
         mm(gk, j0inv, gg);
       }
-      if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
-      if constexpr (STRAT == S_NONE) {
-        cache_scalars<T, MODEL>(mq, cb);
+      if constexpr (is_spatial(STRAT)) {
+        if (!spatial_bundle<T, MODEL>(STRAT - S_SP_NONE, mq, gg, cs, st, qidx, cb, sp) && valid)
+          atomicMin(a.err, (unsigned long long)qidx);
       } else {
-        if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
-        else {
-          cb.jp = cs[C_JP * st + qidx];
-          cb.c1 = cs[C_C1 * st + qidx];
-          cb.c2 = cs[C_C2 * st + qidx];
-        }
-        if (MODEL == FIBER) {
-          cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
-          cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
-          cb.efib[0] = cs[(C_EF + 0) * st + qidx];
-          cb.efib[1] = cs[(C_EF + 1) * st + qidx];
-        }
+        if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
+        if constexpr (STRAT == S_NONE) cache_scalars<T, MODEL>(mq, cb);
+        else load_scalars<T, MODEL>(cs, st, qidx, cb);
+        second_pk<T, MODEL>(mq, cb);
       }
-      second_pk<T, MODEL>(mq, cb);
+    } else if constexpr (STRAT == S_SP_TENSOR) {
+      spatial_bundle<T, MODEL>(S_TENSOR, mq, nullptr, cs, st, qidx, cb, sp);
     } else if constexpr (STRAT == S_CACHEDF) {
       T gg[9];
 #pragma unroll
@@ -456,7 +456,12 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       }
     }
     T wv[9];
-    if constexpr (CART) {
+    if constexpr (is_spatial(STRAT)) {
+      T jtinv[9];
+      inverse3(sj, jtinv);
+      const T ssc = (sj[9] * det3(sj)) * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+      spatial_integrand<T, MODEL>(mq, cb, sp, gx, jtinv, ssc, wv);
+    } else if constexpr (CART) {
       T dg[9], wm[9];
 #pragma unroll
       for (int m = 0; m < 9; ++m) dg[m] = gx[m] * j0inv[4 * (m % 3)];

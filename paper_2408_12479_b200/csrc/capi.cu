@@ -224,16 +224,19 @@ KArgs<T> kargs(const emfgpu_op* op) {
   a.hq_stride = L->nel * L->nq3;
   a.fd_nx = FastDiv::make((uint32_t)L->nx);
   a.fd_nxy = FastDiv::make((uint32_t)(L->nx * L->ny));
+  a.spatial = op->domain;
+  a.coords = L->d_coords;
   return a;
 }
 
 template <typename T>
 void dispatch_apply(const emfgpu_op* op, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
+  const int ks = op->domain ? S_SP_NONE + op->strategy : op->strategy;  // element-kernel strategy code
   switch (op->L->p) {
-    case 1: launch_apply<T, 1>(op->model, op->strategy, a, e0, e1, s); break;
-    case 2: launch_apply<T, 2>(op->model, op->strategy, a, e0, e1, s); break;
-    case 3: launch_apply<T, 3>(op->model, op->strategy, a, e0, e1, s); break;
-    case 4: launch_apply<T, 4>(op->model, op->strategy, a, e0, e1, s); break;
+    case 1: launch_apply<T, 1>(op->model, ks, a, e0, e1, s); break;
+    case 2: launch_apply<T, 2>(op->model, ks, a, e0, e1, s); break;
+    case 3: launch_apply<T, 3>(op->model, ks, a, e0, e1, s); break;
+    case 4: launch_apply<T, 4>(op->model, ks, a, e0, e1, s); break;
   }
 }
 template <typename T>
@@ -536,8 +539,10 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
   auto op = std::make_unique<emfgpu_op>();
   emfgpu_status st = guarded(nullptr, [&] {
     if (model < 0 || model > 2) throw ApiError(EMFGPU_ERR_CONFIG, "op: unknown model");
-    if (domain != 0) throw ApiError(EMFGPU_ERR_CONFIG, "op: spatial domain not supported (material only)");
+    if (domain != 0 && domain != 1) throw ApiError(EMFGPU_ERR_CONFIG, "op: domain must be 0 (material) or 1 (spatial)");
     if (strategy < 0 || strategy > 3) throw ApiError(EMFGPU_ERR_CONFIG, "op: unknown strategy");
+    if (domain == 1 && strategy == EMFGPU_CACHED_F)
+      throw ApiError(EMFGPU_ERR_CONFIG, "op: the cachedF strategy is material-domain only");
     if (precision != 64 && precision != 32) throw ApiError(EMFGPU_ERR_CONFIG, "op: precision must be 64 or 32");
     // MaterialParams::validate, material.cpp:36-48
     if (!(params->mu > 0)) throw ApiError(EMFGPU_ERR_CONFIG, "MaterialParams: mu must be positive");
@@ -557,6 +562,7 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
     op->L = l;
     op->model = model;
     op->strategy = strategy;
+    op->domain = domain;
     op->precision = precision;
     op->params = *params;
     double h[2][6] = {}, m1[2][3] = {};
@@ -571,7 +577,8 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
     CK(cudaMallocHost(&op->h_err, sizeof(unsigned long long)));
     CK(cudaMalloc(&op->d_ukd, sizeof(double) * l->ndofs));
     if (strategy == EMFGPU_NONE || strategy == EMFGPU_SCALAR) CK(cudaMalloc(&op->d_uk, ns * l->ndofs));
-    const int nf = strategy == EMFGPU_TENSOR ? C_NT : strategy == EMFGPU_SCALAR ? 8 : strategy == EMFGPU_CACHED_F ? C_NG : 0;
+    int nf = strategy == EMFGPU_TENSOR ? C_NT : strategy == EMFGPU_SCALAR ? 8 : strategy == EMFGPU_CACHED_F ? C_NG : 0;
+    if (domain == 1) nf = strategy == EMFGPU_TENSOR ? C_NSP : C_JT + 9;  // J_t, 1/J always (operator.hpp:690-691)
     op->n_cache_fields = nf;
     op->cache_stride = l->nel * l->nq3;
     if (nf) CK(cudaMalloc(&op->d_cache, ns * nf * op->cache_stride));
@@ -851,13 +858,20 @@ emfgpu_status emfgpu_op_ledger(const emfgpu_op* op, int* storage, int* traffic, 
   if (op->strategy == EMFGPU_SCALAR || op->strategy == EMFGPU_TENSOR)
     fields = (op->model == 0 ? 1 : 3) + (op->model == 2 ? 4 : 0);
   if (op->strategy == EMFGPU_TENSOR) fields += 30;
-  const int geo = L->affine ? 0 : 10 * s;
+  bool need_geo = true;
+  if (op->domain == 1) {  // ledger.cpp:27-70 spatial rows: J_t + 1/J always, tau/b/FHF^T for tensor
+    fields = 10;
+    if (op->strategy != EMFGPU_NONE) fields += (op->model == 0 ? 1 : 3) + (op->model == 2 ? 4 : 0);
+    if (op->strategy == EMFGPU_TENSOR) fields += 6 + (op->model != 0 ? 6 : 0) + (op->model == 2 ? 12 : 0);
+    need_geo = op->strategy != EMFGPU_TENSOR;  // J0 only maps Grad u_k
+  }
+  const int geo = (L->affine || !need_geo) ? 0 : 10 * s;
   if (storage) *storage = geo + fields * s;
   if (traffic) *traffic = geo + fields * s;
   if (per_dof) {
     const bool uk = op->strategy == EMFGPU_NONE || op->strategy == EMFGPU_SCALAR;
     const double qp = (double)(geo + fields * s) * L->nel * L->nq3;
-    const double el = L->affine ? 10.0 * s * L->nel : 0.0;
+    const double el = (L->affine && need_geo) ? 10.0 * s * L->nel : 0.0;
     *per_dof = (qp + el) / L->ndofs + (uk ? 3 : 2) * s;
   }
   return EMFGPU_OK;

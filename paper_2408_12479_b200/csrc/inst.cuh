@@ -17,7 +17,7 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):
   // warp-per-element (v3) for fp32 and for the fp64 strategies without u_k
   // sweeps; 2 elements per CTA with named barriers (v2) for fp64 none/scalar.
-  constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) &&
+  constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) && !is_spatial(STRAT) &&
                        (sizeof(EMF_T) == 4 || STRAT == S_CACHEDF || STRAT == S_TENSOR);
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
@@ -70,6 +70,12 @@ void launch_apply<EMF_T, EMF_P>(int model, int strategy, const KArgs<EMF_T>& a, 
   EMF_CASE(INH, S_NONE) EMF_CASE(INH, S_SCALAR) EMF_CASE(INH, S_TENSOR) EMF_CASE(INH, S_CACHEDF)
   EMF_CASE(FIBER, S_NONE) EMF_CASE(FIBER, S_SCALAR) EMF_CASE(FIBER, S_TENSOR) EMF_CASE(FIBER, S_CACHEDF)
 #undef EMF_CASE
+#define EMF_SP(M, S) \
+  if (model == M && strategy == S) return apply_one<M, S, false>(a, e0, e1, s);
+  EMF_SP(CNH, S_SP_NONE) EMF_SP(CNH, S_SP_SCALAR) EMF_SP(CNH, S_SP_TENSOR)
+  EMF_SP(INH, S_SP_NONE) EMF_SP(INH, S_SP_SCALAR) EMF_SP(INH, S_SP_TENSOR)
+  EMF_SP(FIBER, S_SP_NONE) EMF_SP(FIBER, S_SP_SCALAR) EMF_SP(FIBER, S_SP_TENSOR)
+#undef EMF_SP
 }
 
 template <>

@@ -106,6 +106,7 @@ struct emfgpu_level {
 struct emfgpu_op {
   const emfgpu_level* L = nullptr;
   int model = 0, strategy = 0, precision = 64;
+  int domain = 0;  // 0 material, 1 spatial (Formulation::domain, material.hpp:18-23)
   emfgpu_material params{};
   emfgpu::MatConst<double> matd{};
   emfgpu::MatConst<float> matf{};

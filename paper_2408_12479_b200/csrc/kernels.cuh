@@ -42,7 +42,10 @@ enum CacheSlot : int {
   // tensor: then F, Finv, S, Cinv
   C_F = 8, C_FINV = 17, C_S = 26, C_CINV = 32, C_NT = 38,
   // cachedF: displacement gradient G = F - I
-  C_G = 0, C_NG = 9
+  C_G = 0, C_NG = 9,
+  // spatial formulation (operator.hpp:139-143): scalars as above, then 1/J,
+  // J_t (9; all strategies), tau, b, F H4 F^T, F H6 F^T (tensor)
+  C_INVJ = 8, C_JT = 9, C_TAU = 18, C_B = 24, C_FH = 30, C_NSP = 42
 };
 
 // n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method,
@@ -99,7 +102,66 @@ struct KArgs {
   const double* hqd;
   const double* m1qd;
   int64_t hq_stride;
+  int spatial;           // Formulation::domain == spatial (linearize / diagonal / residual)
+  const double* coords;  // node coordinates (spatial linearization: J_t = J0 + Grad_xi u_k)
 };
+
+// Stored scalars of the scalar/tensor strategies (load_scalar_fields,
+// operator.hpp:327-343).
+template <typename T, int MODEL>
+__device__ __forceinline__ void load_scalars(const T* cs, int64_t st, int64_t qidx, Bundle<T>& cb) {
+  if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
+  else {
+    cb.jp = cs[C_JP * st + qidx];
+    cb.c1 = cs[C_C1 * st + qidx];
+    cb.c2 = cs[C_C2 * st + qidx];
+  }
+  if (MODEL == FIBER) {
+    cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
+    cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
+    cb.efib[0] = cs[(C_EF + 0) * st + qidx];
+    cb.efib[1] = cs[(C_EF + 1) * st + qidx];
+  }
+}
+
+// Spatial linearization bundle at one point (qp_cache_for_apply spatial cell,
+// operator.hpp:393-434): strat S_NONE recomputes from gg = Grad u_k, S_SCALAR
+// loads the scalars and rebuilds b, tau, F H F^T from gg, S_TENSOR loads all.
+// Returns false when det(F) <= 0.
+template <typename T, int MODEL>
+__device__ __forceinline__ bool spatial_bundle(int strat, const MatConst<T>& mq, const T* gg, const T* cs, int64_t st,
+                                               int64_t qidx, Bundle<T>& cb, SpCell<T>& sp) {
+  if (strat == S_TENSOR) {
+    load_scalars<T, MODEL>(cs, st, qidx, cb);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      sp.tau[k] = cs[(C_TAU + k) * st + qidx];
+      if (MODEL != CNH) sp.b[k] = cs[(C_B + k) * st + qidx];
+      if (MODEL == FIBER) {
+        sp.fh[0][k] = cs[(C_FH + k) * st + qidx];
+        sp.fh[1][k] = cs[(C_FH + 6 + k) * st + qidx];
+      }
+    }
+    return true;
+  }
+  const bool ok = make_strain(gg, cb);
+  T bt[6];
+  green_euler(gg, bt);
+  if (strat == S_NONE) cache_scalars<T, MODEL>(mq, cb);
+  else load_scalars<T, MODEL>(cs, st, qidx, cb);
+  spatial_cell<T, MODEL>(mq, cb, bt, sp);
+  return ok;
+}
+
+// J_t^-1 and (1/J) det J_t w_q at one point from the spatial cache.
+template <typename T>
+__device__ __forceinline__ void spatial_geo(const T* cs, int64_t st, int64_t qidx, T wq, T* jtinv, T& s) {
+  T jt[9];
+#pragma unroll
+  for (int m = 0; m < 9; ++m) jt[m] = cs[(C_JT + m) * st + qidx];
+  inverse3(jt, jtinv);
+  s = (cs[C_INVJ * st + qidx] * det3(jt)) * wq;
+}
 
 // Material constants at one quadrature point: the operator's constants, with
 // the fibre structure tensors replaced by the per-qp frame field if present.
@@ -344,8 +406,15 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
 #pragma unroll
   for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.ukd[3 * ep.node + c] : 0.0;
   __syncthreads();
-  double gk[9];
+  double gk[9], j0[9];
   sf_forward<double, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
+  if (a.spatial) {  // J0 by the geometry kernel's isoparametric sweep (mesh.cpp:162-186)
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.coords[3 * ep.node + c] : 0.0;
+    __syncthreads();
+    sf_forward<double, N>(bufA[el], bufB[el], sB, sD, i, j, k, j0);
+  }
   if (!valid) return;
   const int64_t qidx = e * N3 + q;
   double j0inv[9], detw, g[9];
@@ -361,6 +430,19 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   if (!make_strain(g, cb)) {
     atomicMin(a.err, (unsigned long long)qidx);
     return;
+  }
+  if (a.spatial) {
+    // 1/J and J_t = J0 + Grad_xi u_k with det J_t > 0 (operator.hpp:736-744)
+    double jt[9];
+#pragma unroll
+    for (int m = 0; m < 9; ++m) jt[m] = j0[m] + gk[m];
+    if (!(det3(jt) > 0.0)) {
+      atomicMin(a.err, (unsigned long long)qidx);
+      return;
+    }
+    a.cache[C_INVJ * st + qidx] = T(1.0 / (1.0 + cb.jm1));
+#pragma unroll
+    for (int m = 0; m < 9; ++m) a.cache[(C_JT + m) * st + qidx] = T(jt[m]);
   }
   if (a.strategy == S_CACHEDF || a.strategy == S_NONE) return;
   // stored scalars, computed in double (operator.hpp:720-735)
@@ -379,6 +461,22 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     a.cache[(C_EF + 1) * st + qidx] = T(cb.efib[1]);
   }
   if (a.strategy != S_TENSOR) return;
+  if (a.spatial) {  // tau, b, F H_i F^T (operator.hpp:756-765)
+    double bt[6];
+    green_euler(g, bt);
+    SpCell<double> sp;
+    spatial_cell<double, MODEL>(md, cb, bt, sp);
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      a.cache[(C_TAU + m) * st + qidx] = T(sp.tau[m]);
+      if (MODEL != CNH) a.cache[(C_B + m) * st + qidx] = T(sp.b[m]);
+      if (MODEL == FIBER) {
+        a.cache[(C_FH + m) * st + qidx] = T(sp.fh[0][m]);
+        a.cache[(C_FH + 6 + m) * st + qidx] = T(sp.fh[1][m]);
+      }
+    }
+    return;
+  }
   second_pk<double, MODEL>(md, cb);
 #pragma unroll
   for (int m = 0; m < 9; ++m) {
@@ -422,7 +520,21 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   Bundle<T> cb;
   T j0inv[9], detw;
   load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
-  if (a.strategy == S_NONE || a.strategy == S_SCALAR) {
+  SpCell<T> sp;
+  T jtinv[9], ssc = T(0);
+  if (a.spatial) {
+    T g[9];
+    if (a.strategy == S_NONE || a.strategy == S_SCALAR) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.uk[3 * ep.node + c] : T(0);
+      __syncthreads();
+      T gk[9];
+      sf_forward<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, gk);
+      mm(gk, j0inv, g);
+    }
+    spatial_geo(cs, st, ix, T(a.qwd[i] * a.qwd[j] * a.qwd[k]), jtinv, ssc);
+    spatial_bundle<T, MODEL>(a.strategy, mq, g, cs, st, ix, cb, sp);
+  } else if (a.strategy == S_NONE || a.strategy == S_SCALAR) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) bufA[el][c][q] = valid ? a.uk[3 * ep.node + c] : T(0);
     __syncthreads();
@@ -449,21 +561,10 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
       cb.Cinv[m] = cs[(C_CINV + m) * st + ix];
     }
   }
-  if (a.strategy == S_SCALAR || a.strategy == S_TENSOR) {
-    if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + ix];
-    else {
-      cb.jp = cs[C_JP * st + ix];
-      cb.c1 = cs[C_C1 * st + ix];
-      cb.c2 = cs[C_C2 * st + ix];
-    }
-    if (MODEL == FIBER) {
-      cb.c3[0] = cs[(C_C3 + 0) * st + ix];
-      cb.c3[1] = cs[(C_C3 + 1) * st + ix];
-      cb.efib[0] = cs[(C_EF + 0) * st + ix];
-      cb.efib[1] = cs[(C_EF + 1) * st + ix];
-    }
+  if (!a.spatial) {
+    if (a.strategy == S_SCALAR || a.strategy == S_TENSOR) load_scalars<T, MODEL>(cs, st, ix, cb);
+    if (a.strategy != S_TENSOR) second_pk<T, MODEL>(mq, cb);
   }
-  if (a.strategy != S_TENSOR) second_pk<T, MODEL>(mq, cb);
 
   // A^c_{dd'}: 27 values per qp, as symmetric quadratic-form coefficients
   // coef[c][pair], pairs (00,11,22,01,02,12) with off-diagonals A_dd'+A_d'd.
@@ -477,7 +578,10 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
 #pragma unroll
       for (int m = 0; m < 9; ++m) gref[m] = T(0);
       gref[3 * c + dp] = T(1);
-      tangent_integrand<T, MODEL>(mq, cb, gref, j0inv, detw, w);
+      if (a.spatial)
+        spatial_integrand<T, MODEL>(mq, cb, sp, gref, jtinv, ssc, w);
+      else
+        tangent_integrand<T, MODEL>(mq, cb, gref, j0inv, detw, w);
 #pragma unroll
       for (int d = 0; d < 3; ++d) A[d][dp] = w[3 * c + d];
     }
@@ -582,8 +686,29 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   Bundle<T> cb;
   if (!make_strain(g, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
   cache_scalars<T, MODEL>(mq, cb);  // lnJ (cNH), J^-2/3, fibre invariants (operator.hpp:557-566)
-  second_pk<T, MODEL>(mq, cb);
-  {
+  if (a.spatial) {
+    // J_t = J0 + Grad_xi u, w = (1/J) det J_t w_q tau J_t^-T (operator.hpp:572-588);
+    // J0 recovered from the stored J0^-1
+    T j0[9], jt[9], jtinv[9], bt[6], tf[9];
+    inverse3(j0inv, j0);
+#pragma unroll
+    for (int m = 0; m < 9; ++m) jt[m] = j0[m] + gref[m];
+    inverse3(jt, jtinv);
+    const T detjt = det3(jt);
+    const T invj = T(1) / (T(1) + cb.jm1);
+    green_euler(g, bt);
+    SpCell<T> sp;
+    spatial_cell<T, MODEL>(mq, cb, bt, sp);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tf[3 * r + c] = sp.tau[sidx(r, c)];
+    mm_bt(tf, jtinv, w);
+    const T sc = (invj * detjt) * T(a.qwd[i] * a.qwd[j] * a.qwd[k]);
+#pragma unroll
+    for (int m = 0; m < 9; ++m) w[m] *= sc;
+  } else {
+    second_pk<T, MODEL>(mq, cb);
     T fs[9];
     mm_ts(cb.F, cb.S, fs);  // w_mat = F S (operator.hpp:568)
     mm_bt(fs, j0inv, w);

@@ -23,6 +23,9 @@ namespace emfgpu {
 
 enum Model : int { CNH = 0, INH = 1, FIBER = 2 };
 enum Strategy : int { S_NONE = 0, S_SCALAR = 1, S_TENSOR = 2, S_CACHEDF = 3 };
+// element-kernel strategy codes of the spatial (Omega_t) formulation
+enum SpatialStrategy : int { S_SP_NONE = 4, S_SP_SCALAR = 5, S_SP_TENSOR = 6 };
+__host__ __device__ constexpr bool is_spatial(int strat) { return strat >= S_SP_NONE; }
 
 // Material constants in the operator's number type, rounded from double the
 // way the reference does (N(scalar_of<N>(p.x)), e.g. constitutive.hpp:200).
@@ -400,6 +403,126 @@ __device__ __forceinline__ void tangent_integrand(const MatConst<T>& m, const Bu
   mm_bt(wm, j0inv, wref);
 #pragma unroll
   for (int k = 0; k < 9; ++k) wref[k] *= detw;
+}
+
+// ---- spatial (Omega_t) formulation -------------------------------------------
+// Spatial cell of QpCache (constitutive.hpp:91-92): b = F F^T, tau, F H_i F^T.
+template <typename T>
+struct SpCell {
+  T b[6], tau[6], fh[2][6];
+};
+
+// Green-Euler strain bt = (G + G^T + G G^T)/2 (tensor.hpp:259-270).
+template <typename T>
+__device__ __forceinline__ void green_euler(const T* g, T* bt) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const T q = (g[3 * i] * g[3 * j] + g[3 * i + 1] * g[3 * j + 1]) + g[3 * i + 2] * g[3 * j + 2];
+      bt[sidx(i, j)] = T(0.5) * ((g[3 * i + j] + g[3 * j + i]) + q);
+    }
+}
+
+// b = 2 bt + I, tau = kirchhoff_base (constitutive.hpp:240-283, stable) plus
+// the fibre terms c3 E_i F H_i F^T (push_forward, tensor.hpp:332-341).
+// Reads c.F, c.jm1, c.lnj (cNH), c.jp, c.c3, c.efib.
+template <typename T, int MODEL>
+__device__ __forceinline__ void spatial_cell(const MatConst<T>& m, const Bundle<T>& c, const T* bt, SpCell<T>& sp) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) sp.b[k] = T(2) * bt[k];
+  sp.b[0] += T(1);
+  sp.b[1] += T(1);
+  sp.b[2] += T(1);
+  if (MODEL == CNH) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sp.tau[k] = (T(2) * m.mu) * bt[k];
+    const T v = (T(2) * m.lam) * c.lnj;
+    sp.tau[0] += v;
+    sp.tau[1] += v;
+    sp.tau[2] += v;
+  } else {
+    const T vol = m.half_k * (c.jm1 * (c.jm1 + T(2)));
+    const T trb3 = ((bt[0] + bt[1]) + bt[2]) * (T(1) / T(3));
+    const T s2 = (T(2) * m.mu) * c.jp;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sp.tau[k] = s2 * bt[k];
+    const T v = vol - s2 * trb3;
+    sp.tau[0] += v;
+    sp.tau[1] += v;
+    sp.tau[2] += v;
+  }
+  if (MODEL == FIBER) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      T fhm[9];
+      mm_ts(c.F, m.h[f], fhm);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j)
+          sp.fh[f][sidx(i, j)] = (fhm[3 * i] * c.F[3 * j] + fhm[3 * i + 1] * c.F[3 * j + 1]) + fhm[3 * i + 2] * c.F[3 * j + 2];
+      const T coef = c.c3[f] * c.efib[f];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) sp.tau[k] += coef * sp.fh[f][k];
+    }
+  }
+}
+
+// tangent_spatial (constitutive.hpp:421-463): J c : (grad du)^S + (grad du) tau.
+template <typename T, int MODEL>
+__device__ __forceinline__ void tangent_spatial(const MatConst<T>& m, const Bundle<T>& c, const SpCell<T>& sp,
+                                                const T* dgrad, T* out) {
+  T xs[6], jc[6];
+  sym_part(dgrad, xs);
+  const T trx = (dgrad[0] + dgrad[4]) + dgrad[8];
+  if (MODEL == CNH) {
+    const T f = T(2) * (m.mu - (T(2) * m.lam) * c.lnj);
+    const T v = (T(2) * m.lam) * trx;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) jc[k] = f * xs[k];
+    jc[0] += v;
+    jc[1] += v;
+    jc[2] += v;
+  } else {
+    const T bx = ddot_s(sp.b, xs);
+    const T ttmj = m.two_mu_3 * c.jp;
+    const T f0 = -ttmj * trx;
+    const T m2c1 = T(-2) * c.c1;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) jc[k] = f0 * sp.b[k] + m2c1 * xs[k];
+    const T v = c.c2 * trx - ttmj * bx;
+    jc[0] += v;
+    jc[1] += v;
+    jc[2] += v;
+    if (MODEL == FIBER) {
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const T fhx = ddot_s(sp.fh[f], xs);
+        const T coef = ((T(2) * c.c3[f]) * ((((T(2) * m.k2) * c.efib[f]) * c.efib[f]) + T(1))) * fhx;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) jc[k] += coef * sp.fh[f][k];
+      }
+    }
+  }
+  mm_ts(dgrad, sp.tau, out);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) out[3 * i + j] += jc[sidx(i, j)];
+}
+
+// w_ref = s (tangent_spatial(Gref J_t^-1)) J_t^-T with s = (1/J) det J_t w_q
+// (operator.hpp:506-519).
+template <typename T, int MODEL>
+__device__ __forceinline__ void spatial_integrand(const MatConst<T>& m, const Bundle<T>& c, const SpCell<T>& sp,
+                                                  const T* gref, const T* jtinv, T s, T* wref) {
+  T dgrad[9], ws[9];
+  mm(gref, jtinv, dgrad);
+  tangent_spatial<T, MODEL>(m, c, sp, dgrad, ws);
+  mm_bt(ws, jtinv, wref);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) wref[k] *= s;
 }
 
 }  // namespace emfgpu

@@ -273,7 +273,9 @@ class ElasticOperator:
                  precision=64, domain=0):
         self.level = level
         self.params = params or MaterialParams()
-        self.model, self.strategy, self.precision = model, strategy, precision
+        if isinstance(domain, str):
+            domain = {"material": 0, "spatial": 1}[domain]
+        self.model, self.strategy, self.precision, self.domain = model, strategy, precision, domain
         self.dtype = np.float64 if precision == 64 else np.float32
         self._mat = self.params.to_c()
         h = C.c_void_p()

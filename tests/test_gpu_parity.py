@@ -407,3 +407,35 @@ def test_fgmres_linear_solve_matches_pcg_solution(G):
         assert rel(x.cpu().numpy(), x_cg.cpu().numpy()) <= 1e-6
         if pre is mg:
             assert it < 60
+
+
+SPATIAL = [("cnh_p3_n2_curved", "cnh", 1, 3, 0.05), ("inh_p2_n4_curved", "inh", 2, 2, 0.05),
+           ("fiber_p2_n2_curved", "fiber", 1, 2, 0.05), ("inh_p4_n2_affine", "inh", 1, 4, 0.0)]
+
+
+@pytest.mark.parametrize("case", SPATIAL, ids=[c[0] for c in SPATIAL])
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("strategy", ["none", "scalar", "tensor"])
+def test_spatial_domain_vs_reference(G, case, prec, strategy):
+    """Spatial (Omega_t) formulation (operator.hpp:506-519, constitutive.hpp:
+    421-463): tangent apply, diagonal and residual against the reference."""
+    name, model, lmax, p, damp = case
+    g = np.load(os.path.join(GOLD, "spatial.npz"))
+    n = 1 << lmax
+    lev = G.FeLevel(n, p=p, map_param=(damp,))
+    op = G.ElasticOperator(lev, model, params_from(g["params"], G), strategy, prec, domain="spatial")
+    u0 = I.make_u0(n, n, n, p, amp=0.05)
+    op.update_linearization(u0)
+    y = op.apply_tangent(I.make_v(lev.n_dofs))
+    ref = g[f"{name}_y{prec}_{strategy}"]
+    assert rel(y, ref) <= TOL[prec], rel(y, ref)
+    d, nb = op.compute_diagonal()
+    assert nb == 0 and rel(d, g[f"{name}_diag{prec}"]) <= TOL[prec]
+    r = op.evaluate_residual(u0)
+    assert rel(r, g[f"{name}_r{prec}"]) <= TOL[prec], rel(r, g[f"{name}_r{prec}"])
+
+
+def test_spatial_cachedf_rejected(G):
+    lev = G.FeLevel(2, p=2)
+    with pytest.raises(G.EmfGpuError):
+        G.ElasticOperator(lev, "cnh", G.MaterialParams(), "cachedF", 64, domain="spatial")
