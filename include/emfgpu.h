@@ -197,6 +197,8 @@ typedef struct emfgpu_mg_config {
   int coarse_maxit;      /* coarse CG iteration cap (500) */
   int coarse_n;          /* smallest element count per axis of the h-ladder (1) */
   int precision;         /* level precision: 32 (MgHierarchy<float>, default) or 64 */
+  int64_t coarse_direct_limit; /* dense coarse solve below this many DoFs (2000, solver.hpp:444;
+                                  0 = always the Jacobi-PCG path) */
 } emfgpu_mg_config;
 void emfgpu_mg_default_config(emfgpu_mg_config* cfg);
 emfgpu_status emfgpu_mg_create(const emfgpu_level* fine, int model, const emfgpu_material* params, int strategy,

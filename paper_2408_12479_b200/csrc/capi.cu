@@ -1282,6 +1282,11 @@ struct emfgpu_mg {
   double* dbuf = nullptr;
   double* hdot = nullptr;  // pinned
   int coarse_iterations = 0;
+  // dense coarse solve (CoarseSolver dense path): assembled matrix and [I | A^-1]
+  bool dense = false;
+  double* d_A = nullptr;
+  double* d_M = nullptr;
+  int* d_sing = nullptr;
   std::string last_error;
 };
 
@@ -1352,7 +1357,10 @@ void v_cycle(emfgpu_mg* m, int l, cudaStream_t s) {
   T* b = static_cast<T*>(m->b[l]);
   T* t = static_cast<T*>(m->t[l]);
   if (l + 1 == (int)m->lv.size()) {
-    coarse_cg<T>(m, l, s);
+    if (m->dense)
+      launch_coarse_gemv<T>(m->d_M, b, x, (int)n, s);
+    else
+      coarse_cg<T>(m, l, s);
     return;
   }
   CK(cudaMemsetAsync(x, 0, sizeof(T) * n, s));
@@ -1381,6 +1389,35 @@ void mg_precondition(emfgpu_mg* m, const double* r, double* z, cudaStream_t s) {
   CK(cudaGetLastError());
 }
 
+// CoarseSolver::prepare, dense path (solver.hpp:369-383): the coarse tangent
+// assembled by probing (3 (2p+1)^3 applies, columns identical to the
+// reference's unit-vector applies), then inverted in double.
+template <typename T>
+void dense_coarse(emfgpu_mg* m, int l, cudaStream_t s) {
+  emfgpu_op* op = m->ops[l];
+  const emfgpu_level* L = m->lv[l];
+  const int64_t n = L->ndofs;
+  const int sp = 2 * L->p + 1;
+  T* x = static_cast<T*>(m->cg_p);
+  T* y = static_cast<T*>(m->cg_ap);
+  CK(cudaMemsetAsync(m->d_A, 0, sizeof(double) * n * n, s));
+  for (int cc = 0; cc < sp; ++cc)
+    for (int cb = 0; cb < sp; ++cb)
+      for (int ca = 0; ca < sp; ++ca)
+        for (int comp = 0; comp < 3; ++comp) {
+          launch_probe_fill<T>(x, L->mx, L->my, L->mz, sp, ca, cb, cc, comp, s);
+          op_apply_T<T>(op, x, y, s);
+          launch_probe_extract<T>(y, m->d_A, n, L->mx, L->my, L->mz, L->p, sp, ca, cb, cc, comp, s);
+        }
+  CK(cudaMemsetAsync(m->d_sing, 0, sizeof(int), s));
+  launch_dense_invert(m->d_A, m->d_M, (int)n, m->d_sing, s);
+  CK(cudaGetLastError());
+  int sing = 0;
+  CK(cudaMemcpyAsync(&sing, m->d_sing, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (sing) throw ApiError(EMFGPU_ERR_NUMERICAL, "DenseLU: zero pivot (singular coarse matrix)");
+}
+
 template <typename T>
 void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
   const int nl = (int)m->lv.size();
@@ -1405,6 +1442,8 @@ void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
       if (emfgpu_cheb_create(op, m->diag[l], lmax, m->cfg.degree, m->cfg.range_factor, m->cfg.safety,
                              &m->cheb[l]) != EMFGPU_OK)
         throw ApiError(EMFGPU_ERR_CUDA, "mg: smoother setup failed");
+    } else if (m->dense) {
+      dense_coarse<T>(m, l, s);
     } else {
       launch_inv<T>(static_cast<const T*>(m->diag[l]), static_cast<T*>(m->cg_inv), m->lv[l]->ndofs, s);
     }
@@ -1424,6 +1463,7 @@ void emfgpu_mg_default_config(emfgpu_mg_config* c) {
   c->coarse_rtol = 1e-4;
   c->coarse_maxit = 500;
   c->coarse_n = 1;
+  c->coarse_direct_limit = 2000;
   c->precision = 32;
 }
 
@@ -1443,6 +1483,9 @@ void emfgpu_mg_destroy(emfgpu_mg* m) {
   cudaFree(m->cg_p);
   cudaFree(m->cg_ap);
   cudaFree(m->cg_inv);
+  cudaFree(m->d_A);
+  cudaFree(m->d_M);
+  cudaFree(m->d_sing);
   cudaFree(m->dbuf);
   if (m->hdot) cudaFreeHost(m->hdot);
   delete m;
@@ -1525,6 +1568,12 @@ emfgpu_status emfgpu_mg_create(const emfgpu_level* fine, int model, const emfgpu
     CK(cudaMalloc(&m->cg_inv, ts * nc));
     CK(cudaMalloc(&m->dbuf, sizeof(double) * (dot_partial_count() + 1)));
     CK(cudaMallocHost(&m->hdot, sizeof(double)));
+    m->dense = nc < m->cfg.coarse_direct_limit;  // CoarseSolver::prepare, solver.hpp:373
+    if (m->dense) {
+      CK(cudaMalloc(&m->d_A, sizeof(double) * nc * nc));
+      CK(cudaMalloc(&m->d_M, sizeof(double) * 2 * nc * nc));
+      CK(cudaMalloc(&m->d_sing, sizeof(int)));
+    }
   });
   if (st != EMFGPU_OK) {
     emfgpu_mg_destroy(m);

@@ -37,6 +37,16 @@ template <typename T>
 void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces, unsigned long long* nbad,
                         cudaStream_t s);
 
+// coarse.cu: dense coarse solve (probing assembly, Gauss-Jordan inverse, GEMV)
+template <typename T>
+void launch_probe_fill(T* x, int mx, int my, int mz, int s, int ca, int cb, int cc, int comp, cudaStream_t st);
+template <typename T>
+void launch_probe_extract(const T* y, double* A, int64_t n, int mx, int my, int mz, int p, int s, int ca, int cb,
+                          int cc, int comp, cudaStream_t st);
+void launch_dense_invert(const double* A, double* M, int n, int* d_singular, cudaStream_t st);
+template <typename T>
+void launch_coarse_gemv(const double* M, const T* b, T* x, int n, cudaStream_t st);
+
 // geometry.cu
 void launch_geometry(const double* coords, double* geo_q, double* j0_out, int nx, int ny, int nz, int p,
                      const double* B, const double* D, const double* qw, int* nonaffine, int* degenerate,

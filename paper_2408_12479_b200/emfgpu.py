@@ -487,7 +487,8 @@ def fma_peak_tflops(precision=64, seconds=0.5) -> float:
 class MgConfig(C.Structure):
     _fields_ = [("degree", C.c_int), ("range_factor", C.c_double), ("safety", C.c_double),
                 ("eig_iterations", C.c_int), ("seed", C.c_uint64), ("coarse_rtol", C.c_double),
-                ("coarse_maxit", C.c_int), ("coarse_n", C.c_int), ("precision", C.c_int)]
+                ("coarse_maxit", C.c_int), ("coarse_n", C.c_int), ("precision", C.c_int),
+                ("coarse_direct_limit", C.c_int64)]
 
 
 class MgHierarchy:
@@ -496,7 +497,7 @@ class MgHierarchy:
 
     def __init__(self, fine: FeLevel, model="inh", params: MaterialParams | None = None, strategy="none",
                  degree=6, range_factor=15.0, safety=1.2, eig_iterations=20, coarse_rtol=1e-4, coarse_maxit=500,
-                 coarse_n=1, precision=32, seed=0x9E3779B97F4A7C15):
+                 coarse_n=1, precision=32, seed=0x9E3779B97F4A7C15, coarse_direct_limit=2000):
         L = lib()
         for name, (res, args) in {
             "emfgpu_mg_default_config": (None, [C.POINTER(MgConfig)]),
@@ -519,6 +520,7 @@ class MgHierarchy:
         cfg.degree, cfg.range_factor, cfg.safety, cfg.eig_iterations = degree, range_factor, safety, eig_iterations
         cfg.seed, cfg.coarse_rtol, cfg.coarse_maxit, cfg.coarse_n, cfg.precision = (seed, coarse_rtol, coarse_maxit,
                                                                                    coarse_n, precision)
+        cfg.coarse_direct_limit = coarse_direct_limit
         self.params = params or MaterialParams()
         self._mat = self.params.to_c()
         h = C.c_void_p()

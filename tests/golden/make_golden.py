@@ -129,6 +129,14 @@ def multigrid():
         out[f"{tag}_its"] = its
         out[f"{tag}_hist"] = hist
         print("mg", tag, mg.n_levels, "levels, pcg", its, "its")
+        # the reference's default configuration: dense LU coarse solve (limit 2000)
+        mgd = R.RefMg(L, "inh", prm, degree=5, coarse_direct_limit=2000)
+        mgd.update_linearization(u0)
+        out[f"{tag}_dense_z"] = mgd.precondition(r)
+        x, its, hist = R.pcg_solve(op, mgd, b, 1e-8, 200)
+        out[f"{tag}_dense_x"] = x
+        out[f"{tag}_dense_its"] = its
+        print("mg dense", tag, "pcg", its, "its")
     np.savez_compressed(os.path.join(OUT, "multigrid.npz"), **out)
 
 

@@ -251,7 +251,7 @@ def test_multigrid_vcycle_and_pcg_vs_reference(G, tag, lmax, p):
     n = 1 << lmax
     prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
     lev = G.FeLevel(n, p=p)
-    mg = G.MgHierarchy(lev, "inh", prm, degree=5, coarse_n=1, precision=32)
+    mg = G.MgHierarchy(lev, "inh", prm, degree=5, coarse_n=1, precision=32, coarse_direct_limit=0)
     assert mg.n_levels == {2: 4, 4: 5}[p]
     u0 = torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda")
     mg.update_linearization(u0)
@@ -369,7 +369,7 @@ def test_newton_fgmres_mg_vs_reference(G, case):
     lev = G.FeLevel(n, p=p, map_param=(damp,))
     op = G.ElasticOperator(lev, model, prm, "none", 64)
     op.set_pressure(pres, 1)
-    mg = G.MgHierarchy(lev, model, prm, degree=6, coarse_n=1, precision=32)
+    mg = G.MgHierarchy(lev, model, prm, degree=6, coarse_n=1, precision=32, coarse_direct_limit=0)
     u = torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda")
     nit, lit, res = G.newton_solve(op, mg, u)
     ref_nit, ref_lit = int(g[f"{name}_nit"]), int(g[f"{name}_lit"])
@@ -439,3 +439,49 @@ def test_spatial_cachedf_rejected(G):
     lev = G.FeLevel(2, p=2)
     with pytest.raises(G.EmfGpuError):
         G.ElasticOperator(lev, "cnh", G.MaterialParams(), "cachedF", 64, domain="spatial")
+
+
+@pytest.mark.parametrize("tag,lmax,p", [("q2", 2, 2), ("q4", 2, 4)])
+def test_multigrid_dense_coarse_vs_reference(G, tag, lmax, p):
+    """The reference's default hierarchy (coarse_direct_limit 2000 -> dense LU
+    coarse solve, solver.hpp:369-401): device probing assembly + Gauss-Jordan
+    inverse; V-cycle and outer PCG iteration counts against the reference."""
+    import torch
+    g = np.load(os.path.join(GOLD, "multigrid.npz"))
+    n = 1 << lmax
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    lev = G.FeLevel(n, p=p)
+    mg = G.MgHierarchy(lev, "inh", prm, degree=5, precision=32)
+    mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+    r = torch.tensor(g[f"{tag}_r"], device="cuda")
+    z = torch.empty_like(r)
+    mg.precondition(r, z)
+    torch.cuda.synchronize()
+    assert rel(z.cpu().numpy(), g[f"{tag}_dense_z"]) <= 1e-4, rel(z.cpu().numpy(), g[f"{tag}_dense_z"])
+    op = G.ElasticOperator(lev, "inh", prm, "none", 64)
+    op.update_linearization(np.zeros(lev.n_dofs))
+    b = torch.tensor(g[f"{tag}_b"], device="cuda")
+    x = torch.empty_like(b)
+    its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 200)
+    assert abs(its - int(g[f"{tag}_dense_its"])) <= 1
+    assert rel(x.cpu().numpy(), g[f"{tag}_dense_x"]) <= 1e-6
+
+
+def test_dense_coarse_matches_cg_coarse(G):
+    """Dense coarse solve and a tightly converged coarse CG agree (the coarse
+    operator assembled by probing is the operator)."""
+    import torch
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    lev = G.FeLevel(4, p=1)
+    u0 = torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda")
+    r = torch.tensor(I.make_v(lev.n_dofs, 5), device="cuda")
+    zs = []
+    for lim, rtol in ((2000, 1e-4), (0, 1e-13)):
+        mg = G.MgHierarchy(lev, "inh", prm, degree=5, precision=64, coarse_n=4, coarse_direct_limit=lim,
+                           coarse_rtol=rtol, coarse_maxit=5000)
+        assert mg.n_levels == 1
+        mg.update_linearization(u0)
+        z = torch.empty_like(r)
+        mg.precondition(r, z)
+        zs.append(z.cpu().numpy())
+    assert rel(zs[0], zs[1]) <= 1e-10
