@@ -491,8 +491,8 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
                              "final_rel_residual": float(hist[-1]), "solve_s": t_solve,
                              "ms_per_iteration": 1e3 * t_solve / max(its, 1), "setup_s": t_setup,
                              "settings": "iNH kappa/mu=50, u0=0, affine 48^3 Q4; fp64 PCG rtol 1e-8; fp32 V-cycle "
-                                         "Q4->Q2->Q1->24^3->12^3->6^3, Chebyshev-Jacobi degree 5, coarse "
-                                         "Jacobi-PCG 1e-4"}
+                                         "Q4->Q2->Q1->24^3->12^3->6^3, Chebyshev-Jacobi degree 5, dense coarse "
+                                         "solve (1029 DoFs < coarse_direct_limit 2000, as the reference)"}
     return out
 
 
