@@ -256,6 +256,18 @@ emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, con
                                   int* newton_iterations, int* linear_iterations, double* final_residual,
                                   void* stream);
 
+/* ---- forward-stability lab ------------------------------
+ * run_sweep (stability.hpp, stability.cpp:163-251) on the device: per scale,
+ * samples_per_scale seeded gradient/direction pairs (SweepRng streams), every
+ * cell evaluated in fp64 and fp32 with the reference formulas (no FMA
+ * contraction).  Outputs n_scales * 32 cells, scale-major, then model (cNH,
+ * iNH, fibre, SVK), formulation (standard-material, stable-material,
+ * standard-spatial, stable-spatial), quantity (stress, tangent) — the
+ * reference's write_csv order.  Scales must be positive and increasing. */
+#define EMFGPU_SWEEP_CELLS 32
+emfgpu_status emfgpu_stability_sweep(const double* scales, int n_scales, int samples_per_scale, uint64_t seed,
+                                     const emfgpu_material* params, double* max_rel_error, int64_t* count_invalid);
+
 /* FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured by a register-resident
  * FMA loop over one wave of CTAs for `seconds`: the FP64/FP32 roofline
  * denominator (bench.py). */

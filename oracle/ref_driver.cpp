@@ -23,6 +23,7 @@
 
 #include "elastmf/operator.hpp"
 #include "elastmf/solver.hpp"
+#include "elastmf/stability.hpp"
 
 using namespace emf;
 
@@ -588,3 +589,20 @@ int ref_newton_pressure(void* l, int model, const double* params, double pressur
 }
 
 }  // extern "C"
+
+// ---- the reference's forward-stability sweep (stability.cpp:163-251) ----
+extern "C" int ref_stability_sweep(const double* scales, int n_scales, int samples, uint64_t seed,
+                                   const double* params, double* max_rel_error, int64_t* count_invalid) {
+  return guarded([&] {
+    SweepConfig cfg;
+    cfg.scales.assign(scales, scales + n_scales);
+    cfg.samples_per_scale = samples;
+    cfg.seed = seed;
+    cfg.params = params_from(params);
+    const std::vector<SweepRecord> recs = run_sweep(cfg);
+    for (std::size_t i = 0; i < recs.size(); ++i) {
+      max_rel_error[i] = recs[i].max_rel_error;
+      count_invalid[i] = recs[i].count_invalid;
+    }
+  });
+}

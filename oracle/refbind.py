@@ -257,3 +257,16 @@ def newton_pressure(level: RefLevel, model, params, pressure, face=1, degree=6, 
     _check(L.ref_newton_pressure(level.h, MODELS[model], _p(params), pressure, face, degree, deform_amp, faces,
                                  coarse_direct_limit, _p(u), C.byref(nit), C.byref(lit), C.byref(res)))
     return u, nit.value, lit.value, res.value
+
+
+def stability_sweep(scales, samples=1000, seed=42, params=None):
+    """run_sweep of the reference (stability.cpp:163-251): (n_scales, 32) max
+    relative errors and invalid counts in write_csv order."""
+    L = lib()
+    L.ref_stability_sweep.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+    scales = np.ascontiguousarray(scales, np.float64)
+    params = material_params() if params is None else np.asarray(params, np.float64)
+    err = np.empty(scales.size * 32)
+    inv = np.empty(scales.size * 32, np.int64)
+    _check(L.ref_stability_sweep(_p(scales), scales.size, samples, seed, _p(params), _p(err), _p(inv)))
+    return err.reshape(-1, 32), inv.reshape(-1, 32)

@@ -2097,3 +2097,23 @@ emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, con
     if (final_residual) *final_residual = rnorm;
   });
 }
+
+// ---- stability lab -------------------------------------------------------------
+emfgpu_status emfgpu_stability_sweep(const double* scales, int n_scales, int samples_per_scale, uint64_t seed,
+                                     const emfgpu_material* params, double* max_rel_error, int64_t* count_invalid) {
+  if (!scales || !params || !max_rel_error || !count_invalid) return EMFGPU_ERR_INVALID;
+  return guarded(nullptr, [&] {
+    // run_sweep argument checks (stability.cpp:164-170)
+    if (n_scales <= 0 || samples_per_scale < 0) throw ApiError(EMFGPU_ERR_CONFIG, "run_sweep: empty sweep axes");
+    for (int i = 0; i < n_scales; ++i)
+      if (!(scales[i] > 0) || (i > 0 && !(scales[i] > scales[i - 1])))
+        throw ApiError(EMFGPU_ERR_CONFIG, "run_sweep: scales must be positive and increasing");
+    double h[2][6] = {}, m1[2][3] = {};
+    structure_tensors(*params, h, m1);
+    try {
+      run_stability_sweep(scales, n_scales, samples_per_scale, seed, *params, h, m1, max_rel_error, count_invalid);
+    } catch (const std::runtime_error& e) {
+      throw ApiError(EMFGPU_ERR_CUDA, e.what());
+    }
+  });
+}

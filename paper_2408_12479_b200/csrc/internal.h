@@ -47,6 +47,10 @@ void launch_dense_invert(const double* A, double* M, int n, int* d_singular, cud
 template <typename T>
 void launch_coarse_gemv(const double* M, const T* b, T* x, int n, cudaStream_t st);
 
+// stability.cu
+void run_stability_sweep(const double* scales, int n_scales, int samples, uint64_t seed, const emfgpu_material& p,
+                         const double h[2][6], const double m1[2][3], double* max_rel_error, int64_t* count_invalid);
+
 // geometry.cu
 void launch_geometry(const double* coords, double* geo_q, double* j0_out, int nx, int ny, int nz, int p,
                      const double* B, const double* D, const double* qw, int* nonaffine, int* degenerate,

@@ -158,6 +158,7 @@ def lib():
             "emfgpu_fgmres_solve": (st, [vp, vp, vp, vp, C.c_double, C.c_double, C.c_int, C.c_int,
                                          C.POINTER(C.c_int), C.POINTER(C.c_double), vp]),
             "emfgpu_newton_default_config": (None, [C.POINTER(NewtonConfig)]),
+            "emfgpu_stability_sweep": (st, [vp, C.c_int, C.c_int, C.c_uint64, C.POINTER(Material), vp, vp]),
             "emfgpu_newton_solve": (st, [vp, vp, vp, C.POINTER(NewtonConfig), C.POINTER(C.c_int),
                                          C.POINTER(C.c_int), C.POINTER(C.c_double), vp]),
         }
@@ -592,3 +593,35 @@ def newton_solve(op: ElasticOperator, mg: MgHierarchy | None, d_u, stream=None, 
     if st:
         op._raise(st)
     return nit.value, lit.value, res.value
+
+
+SWEEP_MODELS = ("cNH", "iNH", "fiber", "svk")
+SWEEP_FORMULATIONS = ("standard-material", "stable-material", "standard-spatial", "stable-spatial")
+SWEEP_QUANTITIES = ("stress", "tangent")
+
+
+def stability_sweep(scales, samples_per_scale=1000, seed=42, params: MaterialParams | None = None):
+    """run_sweep (stability.hpp / stability.cpp:163-251) on the device.
+    Returns (max_rel_error, count_invalid), each (n_scales, 32) in the
+    reference's write_csv cell order (model, formulation, quantity)."""
+    scales = np.ascontiguousarray(scales, np.float64)
+    mat = (params or MaterialParams(mu=62.1, lam=3042.9, kappa_b=3084.3, k1=1.4, k2=22.1, a=3.62, b=34.3,
+                                    phi=27.47 * np.pi / 180.0)).to_c()
+    err = np.empty(scales.size * 32)
+    inv = np.empty(scales.size * 32, np.int64)
+    _check(lib().emfgpu_stability_sweep(scales.ctypes.data, scales.size, samples_per_scale, seed, C.byref(mat),
+                                        err.ctypes.data, inv.ctypes.data))
+    return err.reshape(-1, 32), inv.reshape(-1, 32)
+
+
+def write_sweep_csv(scales, err, inv, path):
+    """write_csv (stability.cpp:253-265) layout."""
+    with open(path, "w") as f:
+        f.write("scale,model,formulation,quantity,max_rel_error,count_invalid\n")
+        for i, s in enumerate(scales):
+            c = 0
+            for m in SWEEP_MODELS:
+                for fm in SWEEP_FORMULATIONS:
+                    for q in SWEEP_QUANTITIES:
+                        f.write(f"{s:.9e},{m},{fm},{q},{err[i, c]:.9e},{inv[i, c]}\n")
+                        c += 1

@@ -197,11 +197,24 @@ def spatial():
     np.savez_compressed(os.path.join(OUT, "spatial.npz"), **out)
 
 
+def stability():
+    """The reference's forward-stability sweep (stability.cpp:163-251) on 40
+    log-spaced scales in [1e-8, 1e2], 200 samples each, seed 42, default
+    MaterialParams (material.hpp:36-47)."""
+    scales = np.logspace(-8, 2, 40)
+    prm = R.material_params(mu=62.1, lam=3042.9, kappa=3084.3, k1=1.4, k2=22.1, a=3.62, b=34.3,
+                            phi=27.47 * 3.14159265358979323846 / 180.0)
+    err, inv = R.stability_sweep(scales, 200, 42, prm)
+    np.savez_compressed(os.path.join(OUT, "stability.npz"), scales=scales, err=err, inv=inv)
+    print("stability", err.shape, int(inv.sum()))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for f in sys.argv[1:]:
             globals()[f]()
         sys.exit(0)
+    stability()
     spatial()
     newton()
     multigrid()

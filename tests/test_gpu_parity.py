@@ -485,3 +485,28 @@ def test_dense_coarse_matches_cg_coarse(G):
         mg.precondition(r, z)
         zs.append(z.cpu().numpy())
     assert rel(zs[0], zs[1]) <= 1e-10
+
+
+def test_stability_sweep_vs_reference(G):
+    """Forward-stability lab (stability.cpp:163-251) on the device against the
+    reference's run_sweep: identical invalid counts; bit-identical maxima for
+    every cell whose formulas use no libm transcendental (SVK, iNH — the TU is
+    built without FMA contraction and replays the reference's operation
+    order); cells that call exp (fibre) or log (cNH) differ only by glibc vs
+    CUDA libm ulps on the worst sample."""
+    g = np.load(os.path.join(GOLD, "stability.npz"))
+    prm = G.MaterialParams(mu=62.1, lam=3042.9, kappa_b=3084.3, k1=1.4, k2=22.1, a=3.62, b=34.3,
+                           phi=27.47 * np.pi / 180.0)
+    err, inv = G.stability_sweep(g["scales"], 200, 42, prm)
+    assert np.array_equal(inv, g["inv"])
+    ref = g["err"]
+    names = [(m, f, q) for m in G.SWEEP_MODELS for f in G.SWEEP_FORMULATIONS for q in G.SWEEP_QUANTITIES]
+    for c, (m, f, q) in enumerate(names):
+        if m in ("svk", "iNH"):
+            assert np.array_equal(err[:, c], ref[:, c]), (m, f, q)
+        else:
+            np.testing.assert_allclose(err[:, c], ref[:, c], rtol=0.25, atol=0)
+    assert (err == ref).mean() > 0.9
+    # ordering/validation contract
+    with pytest.raises(G.EmfGpuError):
+        G.stability_sweep([1e-3, 1e-4], 10)
