@@ -268,6 +268,12 @@ emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, con
 emfgpu_status emfgpu_stability_sweep(const double* scales, int n_scales, int samples_per_scale, uint64_t seed,
                                      const emfgpu_material* params, double* max_rel_error, int64_t* count_invalid);
 
+/* Host-vector Newton solve (u in/out on the host, one upload and one download):
+ * the signature of newton_solve(op, &mg, u, ...) for reference-style drivers
+ * (runner.cpp:166-204). */
+emfgpu_status emfgpu_newton_solve_host(emfgpu_op* op, emfgpu_mg* mg, double* u, const emfgpu_newton_config* cfg,
+                                       int* newton_iterations, int* linear_iterations, double* final_residual);
+
 /* FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured by a register-resident
  * FMA loop over one wave of CTAs for `seconds`: the FP64/FP32 roofline
  * denominator (bench.py). */

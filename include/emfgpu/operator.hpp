@@ -44,6 +44,13 @@ inline void throw_status(emfgpu_status st, const char* msg, std::int64_t e = -1,
 }
 
 enum class ModelKind { cnh = EMFGPU_CNH, inh = EMFGPU_INH, fiber = EMFGPU_FIBER };
+/// Formulation::domain (material.hpp:18); the stability is always "stable".
+enum class Domain { material = 0, spatial = 1 };
+/// Loads (operator.hpp:23-32): uniform pressure on one face (-x,+x,-y,+y,-z,+z = 0..5).
+struct Loads {
+  double pressure = 0.0;
+  int pressure_face = 1;
+};
 enum class Strategy { none = EMFGPU_NONE, scalar = EMFGPU_SCALAR, tensor = EMFGPU_TENSOR, cached_f = EMFGPU_CACHED_F };
 
 /// FeLevel: structured (deformed) box with Q_p on GLL nodes, Dirichlet faces.
@@ -79,10 +86,16 @@ class ElasticOperator {
 
  public:
   ElasticOperator(const FeLevel& level, ModelKind model, const emfgpu_material& params, Strategy strategy)
+      : ElasticOperator(level, model, params, Domain::material, strategy, Loads{}) {}
+  /// operator.hpp:55-70: (level, model, params, formulation, strategy, loads)
+  ElasticOperator(const FeLevel& level, ModelKind model, const emfgpu_material& params, Domain domain,
+                  Strategy strategy, const Loads& loads = {})
       : level_(&level) {
-    throw_status(emfgpu_op_create(level.handle(), static_cast<int>(model), &params, 0, static_cast<int>(strategy),
-                                  sizeof(Number) == 8 ? 64 : 32, &h_),
+    throw_status(emfgpu_op_create(level.handle(), static_cast<int>(model), &params, static_cast<int>(domain),
+                                  static_cast<int>(strategy), sizeof(Number) == 8 ? 64 : 32, &h_),
                  emfgpu_global_last_error());
+    if (loads.pressure != 0.0)
+      throw_status(emfgpu_op_set_pressure(h_, loads.pressure, loads.pressure_face), emfgpu_op_last_error(h_));
   }
   ElasticOperator(const ElasticOperator&) = delete;
   ElasticOperator& operator=(const ElasticOperator&) = delete;
@@ -109,6 +122,15 @@ class ElasticOperator {
     throw_status(emfgpu_op_apply_host(h_, du.data(), y.data()), emfgpu_op_last_error(h_));
   }
 
+  /// operator.hpp:94-95: r = (Grad v, P(u)) - load_scale * load, Dirichlet rows zero
+  void evaluate_residual(const std::vector<Number>& u, std::vector<Number>& r) const {
+    if ((std::int64_t)u.size() != n_dofs()) throw Error(EMFGPU_ERR_CONFIG, "evaluate_residual: size mismatch");
+    r.resize(u.size());
+    throw_status(emfgpu_op_residual_host(h_, u.data(), r.data()), emfgpu_op_last_error(h_));
+  }
+  /// operator.hpp:80
+  void set_load_scale(double s) { throw_status(emfgpu_op_set_load_scale(h_, s), emfgpu_op_last_error(h_)); }
+
   /// Device-resident variant (stream-ordered; stream is a cudaStream_t).
   void apply_tangent_device(const Number* d_x, Number* d_y, void* stream = nullptr) const {
     throw_status(emfgpu_op_apply(h_, d_x, d_y, stream), emfgpu_op_last_error(h_));
@@ -132,6 +154,48 @@ class ElasticOperator {
   const FeLevel* level_;
   emfgpu_op* h_ = nullptr;
 };
+
+/// MgHierarchy<Prec> (solver.hpp:437-581) on the device; Prec = float (default) or double.
+class MgHierarchy {
+ public:
+  MgHierarchy(const FeLevel& fine, ModelKind model, const emfgpu_material& params, Strategy strategy,
+              const emfgpu_mg_config* cfg = nullptr) {
+    emfgpu_mg_config c;
+    emfgpu_mg_default_config(&c);
+    if (cfg) c = *cfg;
+    throw_status(emfgpu_mg_create(fine.handle(), static_cast<int>(model), &params, static_cast<int>(strategy), &c,
+                                  &h_),
+                 emfgpu_global_last_error());
+  }
+  MgHierarchy(const MgHierarchy&) = delete;
+  MgHierarchy& operator=(const MgHierarchy&) = delete;
+  ~MgHierarchy() { emfgpu_mg_destroy(h_); }
+  int n_levels() const { return emfgpu_mg_n_levels(h_); }
+  emfgpu_mg* handle() const { return h_; }
+
+ private:
+  emfgpu_mg* h_ = nullptr;
+};
+
+struct NewtonStats {
+  int iterations = 0;
+  int linear_iterations = 0;
+  double final_residual = 0.0;
+};
+
+/// newton_solve (solver.hpp:603-656): u in/out, FGMRES(30) right-preconditioned
+/// by the hierarchy's V-cycle (or unpreconditioned when mg is null).
+inline NewtonStats newton_solve(ElasticOperator<double>& op, MgHierarchy* mg, std::vector<double>& u,
+                                const emfgpu_newton_config* cfg = nullptr) {
+  emfgpu_newton_config c;
+  emfgpu_newton_default_config(&c);
+  if (cfg) c = *cfg;
+  NewtonStats st;
+  throw_status(emfgpu_newton_solve_host(op.handle(), mg ? mg->handle() : nullptr, u.data(), &c, &st.iterations,
+                                        &st.linear_iterations, &st.final_residual),
+               emfgpu_op_last_error(op.handle()));
+  return st;
+}
 
 }  // namespace emfgpu
 

@@ -2117,3 +2117,23 @@ emfgpu_status emfgpu_stability_sweep(const double* scales, int n_scales, int sam
     }
   });
 }
+
+emfgpu_status emfgpu_newton_solve_host(emfgpu_op* op, emfgpu_mg* mg, double* u, const emfgpu_newton_config* cfg,
+                                       int* newton_iterations, int* linear_iterations, double* final_residual) {
+  if (!op || !u) return EMFGPU_ERR_INVALID;
+  double* d_u = nullptr;
+  emfgpu_status st = guarded(&op->last_error, [&] {
+    CK(cudaSetDevice(op->L->device));
+    CK(cudaMalloc(&d_u, sizeof(double) * op->L->ndofs));
+    CK(cudaMemcpy(d_u, u, sizeof(double) * op->L->ndofs, cudaMemcpyHostToDevice));
+  });
+  if (st == EMFGPU_OK) {
+    st = emfgpu_newton_solve(op, mg, d_u, cfg, newton_iterations, linear_iterations, final_residual, op->stream);
+    if (st == EMFGPU_OK)
+      st = guarded(&op->last_error, [&] {
+        CK(cudaMemcpy(u, d_u, sizeof(double) * op->L->ndofs, cudaMemcpyDeviceToHost));
+      });
+  }
+  cudaFree(d_u);
+  return st;
+}
