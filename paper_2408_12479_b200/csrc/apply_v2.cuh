@@ -317,11 +317,17 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   const int qs = lat<N>(qi, qj, qk);  // padded slot of this thread's point
   const int64_t stride = gridDim.x;
 
-  // issue the cp.async copies of group g into staging buffer b
-  auto prefetch = [&](int64_t g, int b) {
+  // per-thread tensor-product weight of this thread's point (operator.hpp:492)
+  const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+  // issue the cp.async copies of group g into staging buffer b; returns true
+  // when this thread's staged x value must be zeroed (Dirichlet node or
+  // padding element), decided here where the lattice position is at hand
+  auto prefetch = [&](int64_t g, int b) -> bool {
     const int64_t e = g * EPB + el + a.e_begin;
+    bool zero = true;
     if (e < a.nel) {
       const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
+      zero = node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
 #pragma unroll
       for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][c][qs], a.x + 3 * ep.node + c);
       if constexpr (kUk) {
@@ -332,24 +338,27 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
         for (int f = q; f < 10; f += N3) cp_async_T(&sm.geo[b][el][f], a.geo + f * a.geo_stride + e);
     }
     cp_async_commit();
+    return zero;
   };
 
   int64_t g = blockIdx.x;
   int buf = 0;
-  if (g < ngroups) prefetch(g, 0);
+  bool zero_cur = true, zero_next = true;
+  if (g < ngroups) zero_cur = prefetch(g, 0);
   for (; g < ngroups; g += stride, buf ^= 1) {
     const bool more = g + stride < ngroups;
     if (more)
-      prefetch(g + stride, buf ^ 1);
+      zero_next = prefetch(g + stride, buf ^ 1);
     else
       cp_async_commit();
     cp_async_wait<1>();
     const int64_t e = g * EPB + el + a.e_begin;
     const bool valid = e < a.nel;
-    const ElemPos ep = elem_pos_fast<P>(valid ? e : a.e_begin, a, qi, qj, qk);
     // Dirichlet columns are masked (operator.hpp:604-605); zero the stale
     // staging values of padding elements.
-    if (!valid || node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces)) {
+    const bool zero_me = zero_cur;
+    zero_cur = zero_next;
+    if (zero_me) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) sm.stage[buf][el][c][qs] = T(0);
     }
@@ -388,11 +397,11 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       j0inv[0] = sm.geo[buf][el][0];
       j0inv[4] = sm.geo[buf][el][4];
       j0inv[8] = sm.geo[buf][el][8];
-      detw = sm.geo[buf][el][9] * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+      detw = sm.geo[buf][el][9] * wq3;
     } else if (a.affine) {
 #pragma unroll
       for (int m = 0; m < 9; ++m) j0inv[m] = sm.geo[buf][el][m];
-      detw = sm.geo[buf][el][9] * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+      detw = sm.geo[buf][el][9] * wq3;
     }
     Bundle<T> cb;
     SpCell<T> sp;
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     if constexpr (is_spatial(STRAT)) {
       T jtinv[9];
       inverse3(sj, jtinv);
-      const T ssc = (sj[9] * det3(sj)) * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+      const T ssc = (sj[9] * det3(sj)) * wq3;
       spatial_integrand<T, MODEL>(mq, cb, sp, gx, jtinv, ssc, wv);
     } else if constexpr (CART) {
       T dg[9], wm[9];

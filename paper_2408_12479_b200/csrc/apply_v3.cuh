@@ -49,7 +49,10 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
 
   // cp.async of element e's inputs into the staging buffer; `which` selects
   // x (1), u_k (2) or both (3)
-  auto prefetch = [&](int64_t e, int which) {
+  // returns, per point r of this lane (bit r), whether its staged x value
+  // must be zeroed (Dirichlet node); only meaningful when x is fetched
+  auto prefetch = [&](int64_t e, int which) -> unsigned {
+    unsigned zero = 0;
     if (e < a.nel) {
 #pragma unroll
       for (int r = 0; r < QPL; ++r) {
@@ -57,6 +60,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
         if (q < N3) {
           const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
           const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
+          if (node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces)) zero |= 1u << r;
           const int qs = lat<N>(qi, qj, qk);
           if (which & 1)
 #pragma unroll
@@ -70,10 +74,17 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
       if ((which & 1) && a.affine && lane < 10) cp_async_T(&sm.geo[lane], a.geo + lane * a.geo_stride + e);
     }
     cp_async_commit();
+    return zero;
   };
 
+  T wq3[QPL];  // tensor-product weights of this lane's points (operator.hpp:492), fp32 path
+#pragma unroll
+  for (int r = 0; r < QPL; ++r) {
+    const int q = lane + 32 * r < N3 ? lane + 32 * r : 0;
+    wq3[r] = T(a.qwd[q % N] * a.qwd[(q / N) % N] * a.qwd[q / (N * N)]);
+  }
   int64_t e = (int64_t)blockIdx.x * kV3Warps + warp + a.e_begin;
-  prefetch(e, 3);
+  unsigned zero_cur = prefetch(e, 3);
   for (; e < a.nel; e += wstride) {
     cp_async_wait<0>();
     __syncwarp();
@@ -81,14 +92,10 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
 #pragma unroll
     for (int r = 0; r < QPL; ++r) {
       const int q = lane + 32 * r;
-      if (q < N3) {
-        const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
-        const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
-        if (node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces)) {
-          const int qs = lat<N>(qi, qj, qk);
+      if (q < N3 && ((zero_cur >> r) & 1u)) {
+        const int qs = lat<N>(q % N, (q / N) % N, q / (N * N));
 #pragma unroll
-          for (int c = 0; c < 3; ++c) sm.stage[c][qs] = T(0);
-        }
+        for (int c = 0; c < 3; ++c) sm.stage[c][qs] = T(0);
       }
     }
     // affine geometry to registers now: the staging buffer is refilled with
@@ -106,7 +113,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
     // ---- gradient of x
     fw_x<T, N, 32>(&sm.stage[0][0], R2, R2 + 3 * SZ, Bm, Dm, lane);
     __syncwarp();
-    if constexpr (!kUk) prefetch(e + wstride, 1);
+    if constexpr (!kUk) zero_cur = prefetch(e + wstride, 1);
     fw_y<T, N, 32>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, Bm, Dm, lane);
     __syncwarp();
     fw_z<T, N, 32>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, Bm, Dm, lane);
@@ -123,7 +130,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
       __syncwarp();
       fw_x<T, N, 32>(&sm.stage[3][0], R2, R2 + 3 * SZ, Bm, Dm, lane);
       __syncwarp();
-      prefetch(e + wstride, 3);  // the staging buffer is free from here on
+      zero_cur = prefetch(e + wstride, 3);  // the staging buffer is free from here on
       fw_y<T, N, 32>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, Bm, Dm, lane);
       __syncwarp();
       fw_z<T, N, 32>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, Bm, Dm, lane);
@@ -147,14 +154,17 @@ __global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(c
       const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
       const int qs = lat<N>(qi, qj, qk);
       const int64_t qidx = e * N3 + q;
+      // fp32: hoisted per-lane weights; fp64 (sequential points, register-bound): recomputed
+      const T wqr = sizeof(T) == 8 ? T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk])
+                                   : ((QPL > 1 && r == 1) ? wq3[QPL > 1 ? 1 : 0] : wq3[0]);
       const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
       T j0inv[9], detw;
       if (CART) {
-        detw = det0 * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+        detw = det0 * wqr;
       } else if (a.affine) {
 #pragma unroll
         for (int m = 0; m < 9; ++m) j0inv[m] = g9[m];
-        detw = det0 * T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+        detw = det0 * wqr;
       } else {
 #pragma unroll
         for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];

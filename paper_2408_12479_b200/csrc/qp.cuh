@@ -165,15 +165,21 @@ __device__ __forceinline__ T ddot_s(const T* x, const T* y) {
 
 // ln(1+x): 2 sum_{n<16} y^(2n+1)/(2n+1), y = x/(2+x); log1p for |x|>0.5
 // (fastscalar.hpp:44-71).  Horner in y^2 instead of the stored powers.
+// Two interleaved Horner chains in y^4 (even / odd powers of y^2) halve the
+// dependent-FMA depth of the 16-term sum.
 template <typename T>
 __device__ __forceinline__ T ln_plus_one(T x) {
   if (fabs(x) > T(0.5)) return dlog1p(x);
   const T y = x * fast_rcp(T(2) + x);
   const T y2 = y * y;
-  T s = T(1.0 / 31.0);
+  const T y4 = y2 * y2;
+  T se = T(1.0 / 29.0), so = T(1.0 / 31.0);  // coefficients 1/(2n+1), n even / odd
 #pragma unroll
-  for (int n = 14; n >= 0; --n) s = s * y2 + T(1.0 / (2 * n + 1));
-  return T(2) * (y * s);
+  for (int m = 6; m >= 0; --m) {
+    se = se * y4 + T(1.0 / (4 * m + 1));
+    so = so * y4 + T(1.0 / (4 * m + 3));
+  }
+  return T(2) * (y * (se + y2 * so));
 }
 
 // J^(-2/3) by the reference's 3-step Newton recurrence (fastscalar.hpp:77-89).
