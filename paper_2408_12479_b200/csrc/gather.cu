@@ -6,6 +6,7 @@
 // i parity); summing in exactly that order here reproduces the reference's
 // association of the scatter sums, with no atomics and no colour passes.
 // Dirichlet rows return the input (operator.hpp:617-620).
+#include "gather.cuh"
 #include "internal.h"
 
 namespace emfgpu {
@@ -58,98 +59,17 @@ __device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bo
   return 1;
 }
 
-// One thread per lattice node; 3-D grid (x: 32 nodes along a, y: 8 along b,
-// z: node planes) so no index division is needed.  Per axis a node has two
-// candidate-element slots ordered even index first (a non-shared node uses
-// only the first); the 2x2x2 slot product is visited z-major, which is the
-// reference's colour order, with predicated loads and a running sum that
-// starts at 0 exactly like y = 0; y += ... in operator.hpp:606, 439.
-struct AxisSlots {
-  int e[2], l[2];
-  bool v[2];
-};
-
-template <int P>
-__device__ __forceinline__ AxisSlots axis_slots(int a, int n, int par, bool lo_ok, bool hi_ok, bool periodic) {
-  AxisSlots s;
-  const int q = a / P, r = a - q * P;
-  if (r != 0) {
-    s.e[0] = q;
-    s.l[0] = r;
-    s.v[0] = true;
-    s.e[1] = q;
-    s.l[1] = 0;
-    s.v[1] = false;
-    return s;
-  }
-  int elo = q - 1, ehi = q;
-  bool vlo = q > 0 || lo_ok, vhi = q < n || hi_ok;
-  if (periodic && q == 0) {
-    elo = n - 1;
-    vlo = true;
-  }
-  // the even (global) element index first
-  const bool swap = ((elo + par) & 1) != 0;
-  s.e[0] = swap ? ehi : elo;
-  s.l[0] = swap ? 0 : P;
-  s.v[0] = swap ? vhi : vlo;
-  s.e[1] = swap ? elo : ehi;
-  s.l[1] = swap ? P : 0;
-  s.v[1] = swap ? vlo : vhi;
-  return s;
-}
-
 template <typename T, int P>
 __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
                                                           const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
                                                           int ny, int nz, int faces, int kpar, int c0,
                                                           int periodic_y) {
-  constexpr int N = P + 1, N3 = N * N * N, N2 = N * N;
-  const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1), mz = nz * P + 1;
+  const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1);
   const int a = blockIdx.x * 32 + threadIdx.x;
   const int b = blockIdx.y * 8 + threadIdx.y;
   const int c = blockIdx.z + c0;
   if (a >= mx || b >= my) return;
-  const int64_t idx = ((int64_t)c * my + b) * mx + a;
-  if (node_constrained(a, b, c, mx, my, mz, faces)) {
-    y[3 * idx] = x[3 * idx];
-    y[3 * idx + 1] = x[3 * idx + 1];
-    y[3 * idx + 2] = x[3 * idx + 2];
-    return;
-  }
-  const AxisSlots sx = axis_slots<P>(a, nx, 0, false, false, false);
-  const AxisSlots sy = axis_slots<P>(b, ny, 0, false, false, periodic_y != 0);
-  const AxisSlots sz = axis_slots<P>(c, nz, kpar, ghost_lo != nullptr, ghost_hi != nullptr, false);
-  T s0 = T(0), s1 = T(0), s2 = T(0);
-#pragma unroll
-  for (int tk = 0; tk < 2; ++tk)
-#pragma unroll
-    for (int tj = 0; tj < 2; ++tj)
-#pragma unroll
-      for (int ti = 0; ti < 2; ++ti) {
-        if (!(sz.v[tk] && sy.v[tj] && sx.v[ti])) continue;
-        const int k = sz.e[tk];
-        T v0, v1, v2;
-        if (k < 0 || k >= nz) {
-          const T* src = k < 0 ? ghost_lo : ghost_hi;
-          const int64_t off = ((((int64_t)sy.e[tj] * nx + sx.e[ti]) * N2) + sy.l[tj] * N + sx.l[ti]) * 3;
-          v0 = src[off];
-          v1 = src[off + 1];
-          v2 = src[off + 2];
-        } else {  // element-local results, component-major loc[(e*3 + c)*N3 + m]
-          const int64_t e = ((int64_t)k * ny + sy.e[tj]) * nx + sx.e[ti];
-          const int64_t off = e * 3 * N3 + (sz.l[tk] * N + sy.l[tj]) * N + sx.l[ti];
-          v0 = loc[off];
-          v1 = loc[off + N3];
-          v2 = loc[off + 2 * N3];
-        }
-        s0 += v0;
-        s1 += v1;
-        s2 += v2;
-      }
-  y[3 * idx] = s0;
-  y[3 * idx + 1] = s1;
-  y[3 * idx + 2] = s2;
+  assemble_node<T, P>(loc, ghost_lo, ghost_hi, x, y, a, b, c, nx, ny, nz, faces, kpar, periodic_y);
 }
 
 template <typename T>

@@ -510,3 +510,34 @@ def test_stability_sweep_vs_reference(G):
     # ordering/validation contract
     with pytest.raises(G.EmfGpuError):
         G.stability_sweep([1e-3, 1e-4], 10)
+
+
+def test_pinned_host_apply_pipeline_bitwise(G):
+    """The pipelined host-vector apply (pinned buffers: z-chunked copies
+    overlapped with per-chunk element/node launches, graph-captured from the
+    second call on) returns exactly the device-resident apply, repeatedly."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2408_12479_b200 import emfgpu as G, inputs as I
+for (n, p, model, strat) in ((16, 3, "cnh", "none"), (8, 4, "inh", "scalar"), (16, 2, "fiber", "none"), (16, 3, "cnh", "tensor")):
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    op = G.ElasticOperator(lev, model, prm, strat, 64)
+    op.update_linearization(I.make_u0(n, n, n, p, amp=0.05))
+    v = I.make_v(lev.n_dofs)
+    hx = torch.tensor(v).pin_memory(); hy = torch.empty_like(hx).pin_memory()
+    dx = hx.cuda(); dy = torch.empty_like(dx)
+    op.apply_tangent_device(dx, dy); torch.cuda.synchronize()
+    ref = dy.cpu().numpy()
+    for it in range(4):
+        hy.fill_(float("nan"))
+        assert G.lib().emfgpu_op_apply_host(op.h, hx.data_ptr(), hy.data_ptr()) == 0
+        assert np.array_equal(hy.numpy(), ref), (n, p, model, strat, it)
+print("ok")
+'''
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
