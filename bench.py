@@ -361,7 +361,7 @@ def run_gpu(args):
                    "l2": "flushed (256 MiB write) before every timed apply", "parallelism": f"z-slab x{world}"},
         "roofline": {"bound": "fp64_fma", "achieved": rec["element_kernel_tflops"], "peak": fp64_peak,
                      "unit": "TFLOP/s", "frac": rec["element_kernel_tflops"] / fp64_peak, "traffic": traffic,
-                     "kernel": "apply_kernel<double,3,CNH,S_NONE> (element phase)",
+                     "kernel": "apply_v2_kernel<double,3,CNH,S_NONE,CART> (element phase)",
                      "peak_source": "measured FMA loop on this GPU (emfgpu_bench_fma_peak)",
                      "flops_per_launch": flops_per_element("none") * part.nel_local,
                      "hbm_achieved_gbs": rec["element_kernel_gbs"], "hbm_peak_gbs": hbm,
