@@ -277,15 +277,20 @@ struct ApplyV2Smem {
   T r2[EPB][9][SZ];
 };
 
-// fp64 kernels keep 3 CTAs/SM (<= 168 registers, no spills): measured faster
-// than 4 CTAs/SM with spills (profiles/r01_*: 0.195 vs 0.207 ms at cfg1).
-template <typename T, int P>
+// CTAs per SM for the launch bounds.  fp64 keeps 3 CTAs/SM (<= 168 registers)
+// except for the variants that ptxas fits into 128 registers without spills,
+// which measured faster at 4 CTAs/SM (cfg1: headline fp64 none 0.1676 ->
+// 0.1654 ms, spatial tensor 0.1205 -> 0.1148 ms); fp32 always 4.
+template <typename T, int P, int MODEL, int STRAT, bool CART>
 constexpr int minb_v2() {
-  return sizeof(T) == 8 ? (TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB) : TileV2<P>::MINB;
+  if (sizeof(T) == 4) return TileV2<P>::MINB;
+  if (P == 3 && MODEL == CNH && ((STRAT == S_NONE && CART) || STRAT == S_SP_NONE || STRAT == S_SP_TENSOR)) return 4;
+  if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
+  return TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB;
 }
 
 template <typename T, int P, int MODEL, int STRAT, bool CART>
-__global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P>()))
+__global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P, MODEL, STRAT, CART>()))
     apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
   using SM = ApplyV2Smem<T, P, MODEL, STRAT, CART>;
   // CART: affine elements with a diagonal J0^-1 (axis-aligned boxes): the

@@ -27,13 +27,15 @@ struct ApplyV3Warp {
 
 constexpr int kV3Warps = 4;
 
-template <typename T>
+// CTAs per SM for the launch bounds: fp32 4, fp64 3 (4 measured slower even
+// where it fits without spills: cfg1 fp64 tensor 0.1251 -> 0.1382 ms).
+template <typename T, int MODEL, int STRAT>
 constexpr int minb_v3() {
-  return sizeof(T) == 8 ? 3 : 4;
+  return sizeof(T) == 4 ? 4 : 3;
 }
 
 template <typename T, int P, int MODEL, int STRAT, bool CART>
-__global__ void __launch_bounds__(32 * kV3Warps, minb_v3<T>()) apply_v3_kernel(const KArgs<T> a) {
+__global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) apply_v3_kernel(const KArgs<T> a) {
   using WS = ApplyV3Warp<T, P, MODEL, STRAT>;
   constexpr int N = P + 1, N3 = N * N * N, SZ = Lay<N>::SIZE;
   constexpr int QPL = (N3 + 31) / 32;  // quadrature points per lane
