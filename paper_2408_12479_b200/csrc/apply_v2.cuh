@@ -181,6 +181,97 @@ __device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T
   }
 }
 
+// Forward sweeps of NV staged vectors at once, in place.  Array (v, c) of a
+// stage lives at base + (v*3 + c)*SIZE.  A pencil's positions belong to one
+// worker in every stage, so outputs overwrite consumed inputs:
+//   x: S -> S (B-sweep), T (D-sweep)
+//   y: S, T -> S (BB), T (BD), U (DB)
+//   z: U, T, S -> U (d/dx), T (d/dy), S (d/dz)
+// With NV = 2 (x and u_k) 2*3N^2 pencils keep every lane busy for N = 4
+// (96 pencils = 3 warp-rounds of 32, vs 4 half-empty rounds one vector at a time).
+template <typename T, int N, int NV, int STRIDE>
+__device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
+    const int vc = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
+    T* const s = S + vc * L::SIZE;
+    T* const t = Tt + vc * L::SIZE;
+    T u[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) u[a] = s[lat<N>(a, j, k)];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      T sb = Bm[q * N] * u[0], sd = Dm[q * N] * u[0];
+#pragma unroll
+      for (int a = 1; a < N; ++a) {
+        sb += Bm[q * N + a] * u[a];
+        sd += Dm[q * N + a] * u[a];
+      }
+      s[lat<N>(q, j, k)] = sb;
+      t[lat<N>(q, j, k)] = sd;
+    }
+  }
+}
+template <typename T, int N, int NV, int STRIDE>
+__device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
+    const int vc = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
+    T* const s = S + vc * L::SIZE;
+    T* const t = Tt + vc * L::SIZE;
+    T* const u = U + vc * L::SIZE;
+    T ub[N], ud[N];
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      ub[b] = s[lat<N>(i, b, k)];
+      ud[b] = t[lat<N>(i, b, k)];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      T s1 = Bm[q * N] * ub[0], s2 = Dm[q * N] * ub[0], s3 = Bm[q * N] * ud[0];
+#pragma unroll
+      for (int b = 1; b < N; ++b) {
+        s1 += Bm[q * N + b] * ub[b];
+        s2 += Dm[q * N + b] * ub[b];
+        s3 += Bm[q * N + b] * ud[b];
+      }
+      s[lat<N>(i, q, k)] = s1;
+      t[lat<N>(i, q, k)] = s2;
+      u[lat<N>(i, q, k)] = s3;
+    }
+  }
+}
+template <typename T, int N, int NV, int STRIDE>
+__device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w) {
+  using L = Lay<N>;
+  for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
+    const int vc = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
+    T* const s = S + vc * L::SIZE;
+    T* const t = Tt + vc * L::SIZE;
+    T* const u = U + vc * L::SIZE;
+    T u0[N], u1[N], u2[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      u0[k] = u[lat<N>(i, j, k)];
+      u1[k] = t[lat<N>(i, j, k)];
+      u2[k] = s[lat<N>(i, j, k)];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      T g0 = Bm[q * N] * u0[0], g1 = Bm[q * N] * u1[0], g2 = Dm[q * N] * u2[0];
+#pragma unroll
+      for (int k = 1; k < N; ++k) {
+        g0 += Bm[q * N + k] * u0[k];
+        g1 += Bm[q * N + k] * u1[k];
+        g2 += Dm[q * N + k] * u2[k];
+      }
+      u[lat<N>(i, j, q)] = g0;
+      t[lat<N>(i, j, q)] = g1;
+      s[lat<N>(i, j, q)] = g2;
+    }
+  }
+}
+
 // Transposed z-sweep (node index along z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* Dm, int w) {
@@ -388,16 +479,41 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
 
     T* const R1 = &sm.r1[el][0][0];  // 9 arrays of SZ, contiguous
     T* const R2 = &sm.r2[el][0][0];
-    // ---- gradient of x at the qps
-    fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
-    esync();
-    fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
-    esync();
-    fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
-    esync();
     T gx[9];
+    T* const S = &sm.stage[buf][el][0][0];  // kUk: x (arrays 0-2), u_k (3-5)
+    // gradient of staged vector v at this thread's point after the in-place
+    // sweeps: d/dx in R1, d/dy in R2, d/dz in the stage (read late: registers)
+    auto grad_at = [&](int v, T* g) {
 #pragma unroll
-    for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
+      for (int c = 0; c < 3; ++c) {
+        g[3 * c + 0] = R1[(3 * v + c) * SZ + qs];
+        g[3 * c + 1] = R2[(3 * v + c) * SZ + qs];
+        g[3 * c + 2] = S[(3 * v + c) * SZ + qs];
+      }
+    };
+    // fp32: x and u_k swept together (full lanes); fp64 keeps one vector per
+    // sweep, whose shorter live ranges fit its 128/168-register budget
+    // (measured: fused sweeps cost fp64 none 0.165 -> 0.175 ms, gave fp32 -3%)
+    constexpr bool kFused = kUk && sizeof(T) == 4;
+    if constexpr (kFused) {
+      // ---- gradients of x and u_k at the qps, both vectors per sweep, in place
+      fwc_x<T, N, 2, N3>(S, R2, a.Bm, Dfx, q);
+      esync();
+      fwc_y<T, N, 2, N3>(S, R2, R1, a.Bm, Dfy, q);
+      esync();
+      fwc_z<T, N, 2, N3>(S, R2, R1, a.Bm, Dfz, q);
+      esync();
+    } else {
+      // ---- gradient of x at the qps
+      fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+      esync();
+      fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+      esync();
+      fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+      esync();
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
+    }
     if (CART) {  // diagonal J0^-1 (entries 0, 4, 8)
       j0inv[0] = sm.geo[buf][el][0];
       j0inv[4] = sm.geo[buf][el][4];
@@ -411,16 +527,20 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     Bundle<T> cb;
     SpCell<T> sp;
     if constexpr (kUk) {
-      esync();
-      fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
-      esync();
-      fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
-      esync();
-      fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
-      esync();
       T gk[9], gg[9];
+      if constexpr (kFused) {
+        grad_at(1, gk);
+      } else {
+        esync();
+        fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+        esync();
+        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+        esync();
+        fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+        esync();
 #pragma unroll
-      for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+        for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+      }
       if constexpr (CART) {
 #pragma unroll
         for (int m = 0; m < 9; ++m) gg[m] = gk[m] * j0inv[4 * (m % 3)];
@@ -469,6 +589,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
         cb.Cinv[m] = cs[(C_CINV + m) * st + qidx];
       }
     }
+    if constexpr (kFused) grad_at(0, gx);
     T wv[9];
     if constexpr (is_spatial(STRAT)) {
       T jtinv[9];

@@ -112,6 +112,31 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
       det0 = sm.geo[9];
     }
     __syncwarp();
+    // fp32 with u_k: x and u_k swept together in place (apply_v2.cuh fwc_*),
+    // 3 full 32-lane rounds per stage instead of 4 half-empty ones; the
+    // staging buffer then holds d/dz until the points have read it
+    constexpr bool kFused = kUk && sizeof(T) == 4;
+    T* const S = &sm.stage[0][0];
+    T gx[QPL][9];
+    if constexpr (kFused) {
+      fwc_x<T, N, 2, 32>(S, R2, Bm, Dm, lane);
+      __syncwarp();
+      fwc_y<T, N, 2, 32>(S, R2, R1, Bm, Dm, lane);
+      __syncwarp();
+      fwc_z<T, N, 2, 32>(S, R2, R1, Bm, Dm, lane);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < QPL; ++r) {
+        const int q = lane + 32 * r;
+        const int qs = q < N3 ? lat<N>(q % N, (q / N) % N, q / (N * N)) : 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          gx[r][3 * c + 0] = R1[c * SZ + qs];
+          gx[r][3 * c + 1] = R2[c * SZ + qs];
+          gx[r][3 * c + 2] = S[c * SZ + qs];
+        }
+      }
+    } else {
     // ---- gradient of x
     fw_x<T, N, 32>(&sm.stage[0][0], R2, R2 + 3 * SZ, Bm, Dm, lane);
     __syncwarp();
@@ -120,7 +145,6 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
     __syncwarp();
     fw_z<T, N, 32>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, Bm, Dm, lane);
     __syncwarp();
-    T gx[QPL][9];
 #pragma unroll
     for (int r = 0; r < QPL; ++r) {
       const int q = lane + 32 * r;
@@ -128,7 +152,8 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
 #pragma unroll
       for (int m = 0; m < 9; ++m) gx[r][m] = R2[m * SZ + qs];
     }
-    if constexpr (kUk) {
+    }
+    if constexpr (kUk && !kFused) {
       __syncwarp();
       fw_x<T, N, 32>(&sm.stage[3][0], R2, R2 + 3 * SZ, Bm, Dm, lane);
       __syncwarp();
@@ -175,8 +200,17 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
       Bundle<T> cb;
       if constexpr (kUk) {
         T gk[9], gg[9];
+        if constexpr (kFused) {
 #pragma unroll
-        for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+          for (int c = 0; c < 3; ++c) {
+            gk[3 * c + 0] = R1[(3 + c) * SZ + qs];
+            gk[3 * c + 1] = R2[(3 + c) * SZ + qs];
+            gk[3 * c + 2] = S[(3 + c) * SZ + qs];
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+        }
         if constexpr (CART) {
 #pragma unroll
           for (int m = 0; m < 9; ++m) gg[m] = gk[m] * j0d[m % 3];
@@ -254,6 +288,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
       for (int r = 0; r < QPL; ++r) qp_point(r);
     }
     __syncwarp();
+    if constexpr (kFused) zero_cur = prefetch(e + wstride, 3);  // the staging buffer is free from here on
     // ---- test with the gradients of the basis functions
     tr_z<T, N, 32>(R1, R2, Bm, Dm, lane);
     __syncwarp();

@@ -92,7 +92,21 @@ __device__ __forceinline__ T det_minus_one(const T* g) {
   return (det3(g) + minors) + tr;
 }
 
-// Adjugate / determinant (tensor.hpp:212-231).
+// Adjugate / determinant (tensor.hpp:212-231); inverse3_det takes det(t) when
+// it is already known (F: det F = 1 + (J-1), same value to rounding).
+template <typename T>
+__device__ __forceinline__ void inverse3_det(const T* t, T det, T* r) {
+  const T inv = fast_rcp(det);
+  r[0] = (t[4] * t[8] - t[5] * t[7]) * inv;
+  r[1] = (t[2] * t[7] - t[1] * t[8]) * inv;
+  r[2] = (t[1] * t[5] - t[2] * t[4]) * inv;
+  r[3] = (t[5] * t[6] - t[3] * t[8]) * inv;
+  r[4] = (t[0] * t[8] - t[2] * t[6]) * inv;
+  r[5] = (t[2] * t[3] - t[0] * t[5]) * inv;
+  r[6] = (t[3] * t[7] - t[4] * t[6]) * inv;
+  r[7] = (t[1] * t[6] - t[0] * t[7]) * inv;
+  r[8] = (t[0] * t[4] - t[1] * t[3]) * inv;
+}
 template <typename T>
 __device__ __forceinline__ void inverse3(const T* t, T* r) {
   const T inv = fast_rcp(det3(t));
@@ -167,17 +181,31 @@ __device__ __forceinline__ T ddot_s(const T* x, const T* y) {
 // (fastscalar.hpp:44-71).  Horner in y^2 instead of the stored powers.
 // Two interleaved Horner chains in y^4 (even / odd powers of y^2) halve the
 // dependent-FMA depth of the 16-term sum.
+// For y^2 < 1/64 the terms past n = 9 sum to less than y^20 / 21 < 2^-64
+// relative to the leading term, so 10 terms give the same double.
 template <typename T>
 __device__ __forceinline__ T ln_plus_one(T x) {
   if (fabs(x) > T(0.5)) return dlog1p(x);
   const T y = x * fast_rcp(T(2) + x);
   const T y2 = y * y;
   const T y4 = y2 * y2;
-  T se = T(1.0 / 29.0), so = T(1.0 / 31.0);  // coefficients 1/(2n+1), n even / odd
+  T se, so;  // coefficients 1/(2n+1), n even / odd
+  if (y2 < T(1.0 / 64.0)) {
+    se = T(1.0 / 17.0);
+    so = T(1.0 / 19.0);
 #pragma unroll
-  for (int m = 6; m >= 0; --m) {
-    se = se * y4 + T(1.0 / (4 * m + 1));
-    so = so * y4 + T(1.0 / (4 * m + 3));
+    for (int m = 3; m >= 0; --m) {
+      se = se * y4 + T(1.0 / (4 * m + 1));
+      so = so * y4 + T(1.0 / (4 * m + 3));
+    }
+  } else {
+    se = T(1.0 / 29.0);
+    so = T(1.0 / 31.0);
+#pragma unroll
+    for (int m = 6; m >= 0; --m) {
+      se = se * y4 + T(1.0 / (4 * m + 1));
+      so = so * y4 + T(1.0 / (4 * m + 3));
+    }
   }
   return T(2) * (y * (se + y2 * so));
 }
@@ -223,7 +251,7 @@ __device__ __forceinline__ bool make_strain(const T* g, Bundle<T>& c) {
   c.F[0] = T(1) + g[0];
   c.F[4] = T(1) + g[4];
   c.F[8] = T(1) + g[8];
-  inverse3(c.F, c.Finv);
+  inverse3_det(c.F, T(1) + c.jm1, c.Finv);
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
