@@ -17,7 +17,7 @@ namespace emfgpu {
 template <typename T, int P, int MODEL, int STRAT>
 struct ApplyV3Warp {
   static constexpr int N = P + 1, SZ = Lay<N>::SIZE;
-  static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR);
+  static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR);
   static constexpr int NST = kUk ? 6 : 3;
   T stage[NST][SZ];
   T geo[10];
@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
               for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[3 + c][qs], a.uk + 3 * ep.node + c);
         }
       }
-      if ((which & 1) && a.affine && lane < 10) cp_async_T(&sm.geo[lane], a.geo + lane * a.geo_stride + e);
+      if ((which & 1) && a.affine && (!is_spatial(STRAT) || kUk) && lane < 10)
+        cp_async_T(&sm.geo[lane], a.geo + lane * a.geo_stride + e);
     }
     cp_async_commit();
     return zero;
@@ -192,13 +193,35 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
 #pragma unroll
         for (int m = 0; m < 9; ++m) j0inv[m] = g9[m];
         detw = det0 * wqr;
-      } else {
+      } else if (!is_spatial(STRAT) || kUk) {
 #pragma unroll
         for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];
         detw = a.geo[9 * a.geo_stride + qidx];
       }
       Bundle<T> cb;
-      if constexpr (kUk) {
+      SpCell<T> sp;
+      if constexpr (is_spatial(STRAT)) {
+        // spatial formulation (operator.hpp:506-519): bundle from G_k (none,
+        // scalar) or the stored spatial cell (tensor), test with J_t^-1
+        T gg[9];
+        if constexpr (kUk) {
+          T gk[9];
+          if constexpr (kFused) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              gk[3 * c + 0] = R1[(3 + c) * SZ + qs];
+              gk[3 * c + 1] = R2[(3 + c) * SZ + qs];
+              gk[3 * c + 2] = S[(3 + c) * SZ + qs];
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+          }
+          mm(gk, j0inv, gg);
+        }
+        if (!spatial_bundle<T, MODEL>(STRAT - S_SP_NONE, mq, gg, cs, st, qidx, cb, sp))
+          atomicMin(a.err, (unsigned long long)qidx);
+      } else if constexpr (kUk) {
         T gk[9], gg[9];
         if constexpr (kFused) {
 #pragma unroll
@@ -267,7 +290,14 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
         }
       }
       T wv[9];
-      if constexpr (CART) {
+      if constexpr (is_spatial(STRAT)) {
+        T jt[9], jtinv[9];
+#pragma unroll
+        for (int m = 0; m < 9; ++m) jt[m] = cs[(C_JT + m) * st + qidx];
+        inverse3(jt, jtinv);
+        const T ssc = (cs[C_INVJ * st + qidx] * det3(jt)) * wqr;
+        spatial_integrand<T, MODEL>(mq, cb, sp, gxr, jtinv, ssc, wv);
+      } else if constexpr (CART) {
         T dg[9], wm[9];
 #pragma unroll
         for (int m = 0; m < 9; ++m) dg[m] = gxr[m] * j0d[m % 3];

@@ -17,7 +17,7 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):
   // warp-per-element (v3) for fp32 and for the fp64 strategies without u_k
   // sweeps; 2 elements per CTA with named barriers (v2) for fp64 none/scalar.
-  constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) && !is_spatial(STRAT) &&
+  constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) &&
                        (sizeof(EMF_T) == 4 || STRAT == S_CACHEDF || STRAT == S_TENSOR);
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
