@@ -43,11 +43,16 @@ MU, LAM = 1.0, 10.0
 QP_FLOPS = {"cnh": {"none": 782, "scalar": 714, "tensor": 386, "cachedF": 746},
             "inh": {"none": 852, "scalar": 748, "tensor": 408, "cachedF": 816},
             "fiber": {"none": 1063, "scalar": 887, "tensor": 521, "cachedF": 1027}}
-# ledger apply traffic per qp, material domain, fp64, u_k row removed (ledger.cpp:22-76;
-# fibre scalar/tensor without the per-qp H4/H6 of a global frame)
-LEDGER = {"cnh": {"none": 72, "scalar": 80, "tensor": 320, "cachedF": 144},
-          "inh": {"none": 72, "scalar": 96, "tensor": 336, "cachedF": 144},
-          "fiber": {"none": 72, "scalar": 128, "tensor": 368, "cachedF": 144}}
+# ledger apply traffic per qp (paper_2408_12479_b200/ledger.py, the reference's
+# ledger.cpp:22-76 restated and tested), with the u_k row removed (u_k counted
+# per DoF) and, for the fibre model with one global frame, without the per-qp
+# H4/H6 rows; cachedF (ours): J0 + G.
+def ledger_qp_bytes(model, strategy, domain="material"):
+    from paper_2408_12479_b200 import ledger as LG
+    if strategy == "cachedF":
+        return 144
+    rows = [r for r in LG.cell_ledger(model, domain, strategy) if r[2] and r[0] not in ("u_k", "H4", "H6")]
+    return sum(b for _, b, _ in rows)
 
 
 def flops_per_element(strategy, n=P + 1, model="cnh"):
@@ -62,7 +67,7 @@ def bytes_per_apply(strategy, prec, ndofs, nel, n=P + 1, model="cnh"):
     s = prec // 8
     nq = nel * n ** 3
     k = 3 if strategy in ("none", "scalar") else 2
-    return LEDGER[model][strategy] * s / 8 * nq + k * s * ndofs
+    return ledger_qp_bytes(model, strategy) * s / 8 * nq + k * s * ndofs
 
 
 def read_peaks():
@@ -463,7 +468,7 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
         t_all = sum(a.elapsed_time(c) for a, b, c in ms) / len(ms)
         t_el = sum(a.elapsed_time(b) for a, b, c in ms) / len(ms)
         nq = lev.n_elements * 64
-        by = (LEDGER["fiber"]["tensor"] + 96) * (prec // 8) / 8 * nq + 2 * (prec // 8) * lev.n_dofs  # + per-qp H4/H6
+        by = (ledger_qp_bytes("fiber", "tensor") + 96) * (prec // 8) / 8 * nq + 2 * (prec // 8) * lev.n_dofs  # + per-qp H4/H6
         rec3[f"fp{prec}_tensor"] = {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all,
                                     "ms_element_kernel": t_el, "hbm_frac": by / (t_el * 1e-3) / 1e9 / hbm}
         del op, x, y

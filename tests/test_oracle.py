@@ -223,3 +223,20 @@ def test_oracle_spatial_domain_bitexact(case):
             assert np.array_equal(op.apply(v.astype(dt)), g[f"{name}_y{prec}_{strat}"]), (prec, strat)
         assert np.array_equal(op.diagonal()[0], g[f"{name}_diag{prec}"])
         assert np.array_equal(op.residual(u0.astype(dt)), g[f"{name}_r{prec}"])
+
+
+def test_ledger_restatement_matches_reference():
+    """paper_2408_12479_b200/ledger.py == the reference's cell_ledger
+    (ledger.cpp:22-76) for every (model, domain, strategy): storage and
+    traffic bytes per quadrature point (golden ledger.json from oracle/_ref)."""
+    import json
+    from paper_2408_12479_b200 import ledger as LG
+    g = json.load(open(os.path.join(GOLD, "ledger.json")))
+    for key, (storage, traffic) in g.items():
+        model, dom, strat = key.split("/")
+        d = "material" if dom == "0" else "spatial"
+        assert LG.storage_bytes(model, d, strat) == storage, key
+        assert LG.traffic_bytes(model, d, strat) == traffic, key
+    # the acceptance table (acceptance.cpp:65-78), material scalar / tensor storage
+    assert [LG.storage_bytes(m, "material", s) for m in ("cnh", "inh", "fiber") for s in ("scalar", "tensor")] == \
+        [104, 320, 128, 344, 272, 488]
