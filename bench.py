@@ -283,8 +283,12 @@ def run_gpu(args):
             by = bytes_per_apply(strat, prec, lev.n_dofs, part.nel_local)
             rec["element_kernel_tflops"] = fl / (ms_elem * 1e-3) / 1e12
             rec["element_kernel_gbs"] = by / (ms_elem * 1e-3) / 1e9
-        else:  # spatial: bytes from the operator's own ledger (J_t, 1/J, caches, vectors)
-            rec["element_kernel_gbs"] = op.byte_ledger().traffic_per_dof * lev.n_dofs / (ms_elem * 1e-3) / 1e9
+        else:  # spatial: the reference ledger's spatial rows (J0, J_t, 1/J, caches), vectors per DoF
+            st = strat.replace("spatial_", "")
+            k = 3 if st in ("none", "scalar") else 2
+            by = ledger_qp_bytes("cnh", st, "spatial") * (prec // 8) / 8 * part.nel_local * (P + 1) ** 3 + \
+                k * (prec // 8) * lev.n_dofs
+            rec["element_kernel_gbs"] = by / (ms_elem * 1e-3) / 1e9
         variants[f"fp{prec}_{strat}"] = rec
         if (prec, strat) == (64, "none"):
             head = (op, sop, x, y, rec)
