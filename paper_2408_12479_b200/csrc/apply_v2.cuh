@@ -25,9 +25,10 @@ namespace emfgpu {
 // exhaustive search over small paddings) so that the three pencil
 // orientations and the per-point accesses of a half-warp hit at most 2 banks
 // per 8-byte word, while every pencil access stays base + compile-time offset.
-// Q3: SZ = 21, SIZE = 80 (was 18 / 72) measured 7% faster in fp32 (cfg1 fp32
-// none 0.104 -> 0.097 ms) and neutral in fp64, where the y-pencils keep a
-// 2-way conflict with any SY = 4 layout (ncu: 8.3M excess of 29M wavefronts).
+// Q3: SZ = 20, SIZE = 80 (was 18 / 72), picked by a measured sweep over
+// (SZ, SIZE) (tools/layout_sweep.sh): SZ = 4 mod 16 makes the y-pencils'
+// 64-bit half-warp accesses conflict-free; cfg1 element phase fp64 none
+// 0.1648 -> 0.1625 ms, fp64 scalar -3%, fp32 none 0.104 -> 0.096 ms.
 template <int N>
 struct Lay;
 template <>
@@ -35,7 +36,7 @@ struct Lay<2> { static constexpr int N = 2, N2 = 4, N3 = 8, SY = 2, SZ = 4, SIZE
 template <>
 struct Lay<3> { static constexpr int N = 3, N2 = 9, N3 = 27, SY = 3, SZ = 12, SIZE = 36; };
 template <>
-struct Lay<4> { static constexpr int N = 4, N2 = 16, N3 = 64, SY = 4, SZ = 21, SIZE = 80; };
+struct Lay<4> { static constexpr int N = 4, N2 = 16, N3 = 64, SY = 4, SZ = 20, SIZE = 80; };
 template <>
 struct Lay<5> { static constexpr int N = 5, N2 = 25, N3 = 125, SY = 5, SZ = 25, SIZE = 125; };
 template <int N>
