@@ -618,3 +618,83 @@ def test_multigrid_zero_rhs_and_beats_plain_cg(G):
     its_mg, _ = G.pcg_solve(op, mg, b, torch.empty_like(b), 1e-8, 500)
     its_cg, _ = G.pcg_solve(op, None, b, torch.empty_like(b), 1e-8, 2000)
     assert its_mg < its_cg / 4, (its_mg, its_cg)
+
+
+# ---- BASELINE configs 2 and 3 at full size: size-independent properties
+
+def _device_props(G, op, n, free_mask, seed=21):
+    import torch
+    dt = torch.float64 if op.precision == 64 else torch.float32
+    v = torch.tensor(I.make_v(n, seed), dtype=dt, device="cuda")
+    w = torch.tensor(I.make_v(n, seed + 1), dtype=dt, device="cuda")
+    if free_mask is not None:
+        fm = torch.tensor(free_mask, device="cuda")
+        v *= fm
+        w *= fm
+    kv, kw, kvw = torch.empty_like(v), torch.empty_like(v), torch.empty_like(v)
+    op.apply_tangent_device(v, kv)
+    op.apply_tangent_device(w, kw)
+    op.apply_tangent_device(0.75 * v - 1.25 * w, kvw)
+    torch.cuda.synchronize()
+    lin = (torch.linalg.norm((kvw - (0.75 * kv - 1.25 * kw)).double()) / torch.linalg.norm(kvw.double())).item()
+    sym = abs((torch.dot(w.double(), kv.double()) - torch.dot(v.double(), kw.double())).item()) / abs(
+        torch.dot(w.double(), kv.double()).item())
+    return lin, sym, kv
+
+
+def test_cfg2_full_size_properties(G):
+    """cfg2 (64^3 Q4 iNH on the curved map, 50.9M DoFs, scaled-noise u0):
+    the literal noise is rejected at the reference's first (e, q); linear,
+    symmetric on the free DoFs, strategies and precisions agree."""
+    from paper_2408_12479_b200 import workloads as W
+    lit = W.cfg2(literal=True)
+    lev = lit.level()
+    op = G.ElasticOperator(lev, "inh", lit.material(), "none", 64)
+    with pytest.raises(G.NonPositiveJacobian) as ex:
+        op.update_linearization(lit.u0())
+    assert (ex.value.element, ex.value.qpoint) == (1, 46)
+    w = W.cfg2()
+    u0 = w.u0()
+    free = ~I.dirichlet_mask(64, 64, 64, 4, 1)
+    kvs = {}
+    for strat, prec in (("none", 64), ("tensor", 64), ("none", 32)):
+        op = G.ElasticOperator(lev, "inh", w.material(), strat, prec)
+        op.update_linearization(u0)
+        lin, sym, kv = _device_props(G, op, lev.n_dofs, free)
+        assert lin <= {64: 1e-13, 32: 1e-5}[prec], (strat, prec, lin)
+        assert sym <= {64: 1e-10, 32: 1e-4}[prec], (strat, prec, sym)
+        kvs[(strat, prec)] = kv.double().cpu().numpy()
+        del op
+    assert rel(kvs[("tensor", 64)], kvs[("none", 64)]) <= 1e-12
+    assert rel(kvs[("none", 32)], kvs[("none", 64)]) <= 1e-5
+
+
+def test_cfg3_full_size_properties(G):
+    """cfg3 (periodic tube 16x128x256 Q3, 43.4M DoFs, per-qp cylindrical fibre
+    frames, no Dirichlet face): linear and symmetric, fp64 tensor == none,
+    fp32 within 1e-5; rigid translations are in the kernel of the tangent
+    (no Dirichlet face, periodic seam handled)."""
+    import torch
+    from paper_2408_12479_b200 import workloads as W
+    w = W.cfg3()
+    lev = w.level()
+    u0 = W.tube_u0(w, lev.node_coords())
+    kvs = {}
+    for strat, prec in (("tensor", 64), ("none", 64), ("tensor", 32)):
+        op = G.ElasticOperator(lev, "fiber", w.material(), strat, prec)
+        op.set_fibre_frame("cylindrical")
+        op.update_linearization(u0)
+        lin, sym, kv = _device_props(G, op, lev.n_dofs, None)
+        assert lin <= {64: 1e-13, 32: 1e-5}[prec], (strat, prec, lin)
+        assert sym <= {64: 1e-10, 32: 1e-4}[prec], (strat, prec, sym)
+        kvs[(strat, prec)] = kv.double().cpu().numpy()
+        if (strat, prec) == ("tensor", 64):
+            t = torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda")
+            t[0::3] = 1.0  # rigid x-translation
+            kt = torch.empty_like(t)
+            op.apply_tangent_device(t, kt)
+            torch.cuda.synchronize()
+            assert torch.linalg.norm(kt).item() <= 1e-9 * np.linalg.norm(kvs[(strat, prec)])
+        del op
+    assert rel(kvs[("none", 64)], kvs[("tensor", 64)]) <= 1e-12
+    assert rel(kvs[("tensor", 32)], kvs[("tensor", 64)]) <= 1e-5
