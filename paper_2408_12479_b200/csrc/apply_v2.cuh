@@ -29,16 +29,19 @@ namespace emfgpu {
 // (SZ, SIZE) (tools/layout_sweep.sh): SZ = 4 mod 16 makes the y-pencils'
 // 64-bit half-warp accesses conflict-free; cfg1 element phase fp64 none
 // 0.1648 -> 0.1625 ms, fp64 scalar -3%, fp32 none 0.104 -> 0.096 ms.
-template <int N>
+template <int N, int ES = 8>  // ES: element size in bytes (array stride may differ)
 struct Lay;
-template <>
-struct Lay<2> { static constexpr int N = 2, N2 = 4, N3 = 8, SY = 2, SZ = 4, SIZE = 8; };
-template <>
-struct Lay<3> { static constexpr int N = 3, N2 = 9, N3 = 27, SY = 3, SZ = 12, SIZE = 36; };
-template <>
-struct Lay<4> { static constexpr int N = 4, N2 = 16, N3 = 64, SY = 4, SZ = 20, SIZE = 80; };
-template <>
-struct Lay<5> { static constexpr int N = 5, N2 = 25, N3 = 125, SY = 5, SZ = 25, SIZE = 125; };
+template <int ES>
+struct Lay<2, ES> { static constexpr int N = 2, N2 = 4, N3 = 8, SY = 2, SZ = 4, SIZE = 8; };
+template <int ES>
+struct Lay<3, ES> { static constexpr int N = 3, N2 = 9, N3 = 27, SY = 3, SZ = 12, SIZE = 36; };
+// fp64: SIZE = 82 (41 16-byte units, odd) with the j-c-k pencil order of the
+// x-sweeps puts the two components of a quarter-warp's LDS.128 on disjoint
+// bank groups; fp32 keeps 80 (float4 alignment of every pencil).
+template <int ES>
+struct Lay<4, ES> { static constexpr int N = 4, N2 = 16, N3 = 64, SY = 4, SZ = 20, SIZE = ES == 8 ? 82 : 80; };
+template <int ES>
+struct Lay<5, ES> { static constexpr int N = 5, N2 = 25, N3 = 125, SY = 5, SZ = 25, SIZE = 125; };
 template <int N>
 __device__ __forceinline__ constexpr int lat(int a, int b, int c) {
   return a + Lay<N>::SY * b + Lay<N>::SZ * c;
@@ -106,9 +109,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // Forward x-sweep: in[c] -> tB[c] = Bx in, tD[c] = Dx in.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
-    const int c = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
+    // fp64: pencil order j, c, k (j fastest) so a quarter-warp spans two
+    // components (SIZE 82); fp32: component-major (measured better)
+    const int j = sizeof(T) == 8 ? wk % N : (wk % L::N2) % N;
+    const int c = sizeof(T) == 8 ? (wk / N) % 3 : wk / L::N2;
+    const int k = sizeof(T) == 8 ? wk / (3 * N) : (wk % L::N2) / N;
     T u[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) u[a] = in[c * L::SIZE + lat<N>(a, j, k)];
@@ -130,7 +137,7 @@ __device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, con
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T* sdb,
                                      const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T ub[N], ud[N];
@@ -159,7 +166,7 @@ __device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T* g, const T* Bm,
                                      const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T u0[N], u1[N], u2[N];
@@ -195,7 +202,7 @@ __device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T
 // (96 pencils = 3 warp-rounds of 32, vs 4 half-empty rounds one vector at a time).
 template <typename T, int N, int NV, int STRIDE>
 __device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
     const int vc = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
     T* const s = S + vc * L::SIZE;
@@ -218,7 +225,7 @@ __device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int
 }
 template <typename T, int N, int NV, int STRIDE>
 __device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
     const int vc = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T* const s = S + vc * L::SIZE;
@@ -247,7 +254,7 @@ __device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* D
 }
 template <typename T, int N, int NV, int STRIDE>
 __device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
     const int vc = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T* const s = S + vc * L::SIZE;
@@ -279,7 +286,7 @@ __device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* D
 // Transposed z-sweep (node index along z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T u0[N], u1[N], u2[N];
@@ -308,7 +315,7 @@ __device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* D
 // Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T u0[N], u1[N], u2[N];
@@ -336,9 +343,11 @@ __device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* D
 // values of loc[(e*3 + c)*N3 + lexicographic m] (component-major).
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
 __device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T* Dm, int w) {
-  using L = Lay<N>;
+  using L = Lay<N, sizeof(T)>;
   for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
-    const int c = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
+    const int j = sizeof(T) == 8 ? wk % N : (wk % L::N2) % N;  // pencil order as fw_x
+    const int c = sizeof(T) == 8 ? (wk / N) % 3 : wk / L::N2;
+    const int k = sizeof(T) == 8 ? wk / (3 * N) : (wk % L::N2) / N;
     T u0[N], u1[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
@@ -365,7 +374,7 @@ struct ApplyV2Smem {
   static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
   static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR);
   static constexpr int NST = kUk ? 6 : 3;  // staged fields: x (3) [+ u_k (3)]
-  static constexpr int SZ = Lay<N>::SIZE;
+  static constexpr int SZ = Lay<N, sizeof(T)>::SIZE;
   T stage[2][EPB][NST][SZ];
   T geo[2][EPB][10];
   T r1[EPB][9][SZ];
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   const T* const Dtz = a.Dm;
   constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
   constexpr bool kUk = SM::kUk;
-  constexpr int SZ = Lay<N>::SIZE;
+  constexpr int SZ = Lay<N, sizeof(T)>::SIZE;
   __shared__ __align__(16) SM sm;
   const int tid = threadIdx.x;
   const int el = tid / N3, q = tid % N3;

@@ -16,7 +16,7 @@ namespace emfgpu {
 
 template <typename T, int P, int MODEL, int STRAT>
 struct ApplyV3Warp {
-  static constexpr int N = P + 1, SZ = Lay<N>::SIZE;
+  static constexpr int N = P + 1, SZ = Lay<N, sizeof(T)>::SIZE;
   static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR);
   static constexpr int NST = kUk ? 6 : 3;
   T stage[NST][SZ];
@@ -37,7 +37,7 @@ constexpr int minb_v3() {
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) apply_v3_kernel(const KArgs<T> a) {
   using WS = ApplyV3Warp<T, P, MODEL, STRAT>;
-  constexpr int N = P + 1, N3 = N * N * N, SZ = Lay<N>::SIZE;
+  constexpr int N = P + 1, N3 = N * N * N, SZ = Lay<N, sizeof(T)>::SIZE;
   constexpr int QPL = (N3 + 31) / 32;  // quadrature points per lane
   constexpr bool kUk = WS::kUk;
   extern __shared__ __align__(16) unsigned char v3_smem[];  // kV3Warps * sizeof(WS), dynamic
