@@ -602,6 +602,7 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_x);
   cudaFree(op->d_y);
   cudaFree(op->d_load);
+  cudaFree(op->lz_buf);
   cudaFree(op->d_err);
   if (op->h_err) cudaFreeHost(op->h_err);
   if (op->stream) cudaStreamDestroy(op->stream);
@@ -1184,71 +1185,63 @@ double tridiag_extreme(const std::vector<double>& al, const std::vector<double>&
 template <typename T>
 static void lanczos(emfgpu_op* op, const T* diag, int iterations, uint64_t seed, double* lmin, double* lmax,
                     cudaStream_t s) {
+  // estimate_eigenvalues (solver.hpp:262-308): Lanczos on D^-1/2 A D^-1/2 with
+  // full (modified Gram-Schmidt) reorthogonalisation.  Device resident: the
+  // seeded start vector is generated on the device, the MGS coefficients
+  // never leave it, and one host read per step fetches beta (break test).
   const int64_t n = op->L->ndofs;
   const int maxit = (int)std::min<int64_t>(iterations, n);
-  // start vector: splitmix64 uniform01 - 0.5 (solver.hpp:274-277), normalised
-  std::vector<double> hv(n);
-  uint64_t state = seed;
-  for (auto& x : hv) {
-    state += 0x9e3779b97f4a7c15ull;
-    uint64_t z = state;
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    z ^= z >> 31;
-    x = (double)(z >> 11) * 0x1.0p-53 - 0.5;
+  const int nd = dot_partial_count() + 1;
+  const size_t need = sizeof(double) * ((size_t)n * (std::max(1, maxit) + 2) + (size_t)nd + 2 * (size_t)maxit + 2) +
+                      2 * sizeof(T) * (size_t)n + 64;
+  if (op->lz_bytes < need) {
+    cudaFree(op->lz_buf);
+    op->lz_buf = nullptr;
+    op->lz_bytes = 0;
+    CK(cudaMalloc(&op->lz_buf, need));
+    op->lz_bytes = need;
   }
-  double nv = 0;
-  for (double x : hv) nv += x * x;
-  nv = std::sqrt(nv);
-  for (auto& x : hv) x /= nv;
-  double *dis, *basis, *w, *dbuf;
-  T *t, *at;
-  CK(cudaMalloc(&dis, sizeof(double) * n));
-  CK(cudaMalloc(&basis, sizeof(double) * n * std::max(1, maxit)));
-  CK(cudaMalloc(&w, sizeof(double) * n));
-  CK(cudaMalloc(&dbuf, sizeof(double) * (dot_partial_count() + 1)));
-  CK(cudaMalloc(&t, sizeof(T) * n));
-  CK(cudaMalloc(&at, sizeof(T) * n));
-  CK(cudaMemcpyAsync(basis, hv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  double* basis = op->lz_buf;
+  double* dis = basis + (size_t)n * std::max(1, maxit);
+  double* w = dis + n;
+  double* dbuf = w + n;          // dot partials + result
+  double* coef = dbuf + nd;      // alpha_j, beta_j
+  T* t = reinterpret_cast<T*>(coef + 2 * (size_t)maxit + 2);
+  T* at = t + n;
+  launch_lanczos_start(basis, n, (unsigned long long)seed, s);
+  launch_dot<double>(basis, basis, n, dbuf + 1, dbuf, s);
+  launch_div_sqrt_dev(dbuf, basis, basis, n, s);
   launch_dinv_sqrt<T>(diag, dis, n, s);
-  auto dot = [&](const double* x, const double* y) {
-    launch_dot<double>(x, y, n, dbuf + 1, dbuf, s);
-    double r;
-    CK(cudaMemcpyAsync(&r, dbuf, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return r;
-  };
   std::vector<double> alpha, beta;
-  double beta_prev = 0.0;
+  double hb = 0.0;
   for (int j = 0; j < maxit; ++j) {
     double* v = basis + (size_t)j * n;
     launch_scale_to_T<T>(dis, v, t, n, s);
     apply_elements(op, t, 0, op->L->nz, s);
     apply_nodes(op, t, at, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
     launch_scale_from_T<T>(dis, at, w, n, s);
-    if (j > 0) launch_axpy_minus(beta_prev, basis + (size_t)(j - 1) * n, w, n, s);
-    const double a = dot(w, v);
-    alpha.push_back(a);
-    launch_axpy_minus(a, v, w, n, s);
+    if (j > 0) launch_axpy_minus(hb, basis + (size_t)(j - 1) * n, w, n, s);
+    launch_dot<double>(w, v, n, dbuf + 1, coef + 2 * j, s);  // alpha_j
+    launch_axpy_dev(coef + 2 * j, v, w, n, s);
     for (int qb = 0; qb <= j; ++qb) {
       const double* q = basis + (size_t)qb * n;
-      launch_axpy_minus(dot(w, q), q, w, n, s);
+      launch_dot<double>(w, q, n, dbuf + 1, dbuf, s);
+      launch_axpy_dev(dbuf, q, w, n, s);
     }
-    const double b = std::sqrt(dot(w, w));
+    launch_dot<double>(w, w, n, dbuf + 1, coef + 2 * j + 1, s);  // beta_j^2
+    double ab[2];
+    CK(cudaMemcpyAsync(ab, coef + 2 * j, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    alpha.push_back(ab[0]);
+    const double b = std::sqrt(ab[1]);
     if (j + 1 < maxit) beta.push_back(b);
     if (b < 1e-12) break;
     if (j + 1 < maxit) launch_div(w, b, basis + (size_t)(j + 1) * n, n, s);
-    beta_prev = b;
+    hb = b;
   }
   beta.resize(alpha.empty() ? 0 : alpha.size() - 1);
   *lmax = tridiag_extreme(alpha, beta, true);
   *lmin = tridiag_extreme(alpha, beta, false);
-  cudaFree(dis);
-  cudaFree(basis);
-  cudaFree(w);
-  cudaFree(dbuf);
-  cudaFree(t);
-  cudaFree(at);
 }
 
 emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, int iterations, uint64_t seed,

@@ -84,6 +84,9 @@ void launch_scale_from_T(const double* s, const T* at, double* w, int64_t n, cud
 template <typename T>
 void launch_dinv_sqrt(const T* d, double* s, int64_t n, cudaStream_t st);
 void launch_axpy_minus(double a, const double* x, double* y, int64_t n, cudaStream_t st);
+void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st);
+void launch_axpy_dev(const double* c, const double* x, double* y, int64_t n, cudaStream_t st);
+void launch_div_sqrt_dev(const double* d, const double* x, double* y, int64_t n, cudaStream_t st);
 void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st);
 template <typename T>
 void launch_mask_zero(T* v, int64_t nnodes, int mx, int my, int mz, int faces, cudaStream_t s);
@@ -134,6 +137,9 @@ struct emfgpu_op {
   void* d_y = nullptr;
   unsigned long long* d_err = nullptr;
   unsigned long long* h_err = nullptr;  // pinned
+  // Lanczos work space (estimate_eigenvalues), kept across relinearizations
+  double* lz_buf = nullptr;
+  size_t lz_bytes = 0;
   // per-qp fibre frame field (fibre model): H4/H6 in double and Number, M1s
   int frame_kind = 0;
   double* d_hqd = nullptr;

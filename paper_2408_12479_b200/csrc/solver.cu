@@ -178,6 +178,39 @@ __global__ void scal_d_kernel(const double* __restrict__ x, double inv, double* 
   if (i < n) y[i] = x[i] / inv;
 }
 
+// Lanczos start vector (solver.hpp:274-277): element i of the sequential
+// splitmix64 stream is mix(seed + (i+1) gamma), so it is generated in parallel.
+__global__ void lanczos_start_kernel(double* __restrict__ v, int64_t n, unsigned long long seed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long z = seed + (unsigned long long)(i + 1) * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  v[i] = (double)(z >> 11) * 0x1.0p-53 - 0.5;
+}
+// y -= c[0] x with the coefficient read from device memory (no host round trip)
+__global__ void axpy_dev_kernel(const double* __restrict__ c, const double* __restrict__ x, double* __restrict__ y,
+                                int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] -= c[0] * x[i];
+}
+// y = x / sqrt(d[0])
+__global__ void div_sqrt_dev_kernel(const double* __restrict__ d, const double* __restrict__ x,
+                                    double* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] / sqrt(d[0]);
+}
+void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st) {
+  lanczos_start_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, seed);
+}
+void launch_axpy_dev(const double* c, const double* x, double* y, int64_t n, cudaStream_t st) {
+  axpy_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c, x, y, n);
+}
+void launch_div_sqrt_dev(const double* d, const double* x, double* y, int64_t n, cudaStream_t st) {
+  div_sqrt_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d, x, y, n);
+}
+
 template <typename T>
 void launch_scale_to_T(const double* s, const double* v, T* t, int64_t n, cudaStream_t st) {
   scale_to_T_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, v, t, n);
