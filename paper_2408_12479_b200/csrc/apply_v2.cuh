@@ -1,8 +1,7 @@
-// Tangent-apply element phase, v2 (the production kernel).
+// Tangent-apply element phase, v2: persistent CTAs, EPB elements per CTA.
 //
-// Differences from the first version (kernels.cuh:apply_kernel), each driven
-// by the round-1 ncu profile (profiles/r01_ncu_apply_fp64_none.txt: fp64 pipe
-// 33%, stalls long-scoreboard > wait > short-scoreboard > MIO throttle):
+// Design (each point driven by an ncu profile, see DESIGN.md §3 and
+// profiles/r01_*):
 //  * persistent CTAs (one wave, occupancy-sized) loop over element groups and
 //    prefetch the NEXT group's x / u_k / affine geometry into a second shared
 //    staging buffer with cp.async while the current group computes;
@@ -10,12 +9,12 @@
 //    pencil and performs the full 1D contraction in registers, so every
 //    shared load feeds n FMAs and the 1D tables are compile-time-indexed
 //    kernel parameters (constant-bank operands, no shared loads);
-//  * power-of-two n uses an XOR-swizzled element layout that makes all three
-//    pencil orientations and the per-point accesses bank-conflict free;
+//  * padded element arrays (Lay below) chosen by measurement so the pencil
+//    orientations and the per-point accesses avoid bank conflicts;
+//  * each element of a CTA synchronises on its own named barrier;
 //  * element-local results are stored component-major, loc[(e*3 + c)*n^3 + m],
-//    as contiguous vector stores.
-// The quadrature-point algebra is unchanged (qp.cuh), so is the result up to
-// summation order inside the sweeps.
+//    as contiguous vector stores, for the node phase (gather.cu).
+// The quadrature-point algebra is in qp.cuh.
 #pragma once
 #include "kernels.cuh"
 
