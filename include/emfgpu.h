@@ -127,7 +127,11 @@ uint64_t emfgpu_op_checksum(const emfgpu_op* op);            /* checksum(), FNV-
 /* apply_tangent(du, y), operator.hpp:99-100/597-621: y = K(u_k) du with the
  * Dirichlet identity.  x, y: device arrays of n_dofs Number values. */
 emfgpu_status emfgpu_op_apply(emfgpu_op* op, const void* d_x, void* d_y, void* stream);
-/* Same through host vectors (H2D, apply, D2H, synchronise, error check). */
+/* Same through host vectors (H2D, apply, D2H, synchronise, error check).
+ * With page-locked x and y (cudaHostAlloc / cudaHostRegister) and nz >= 8 the
+ * copies are pipelined with the compute in z-chunks on the copy engines and
+ * the whole sequence is replayed as a CUDA graph from the second call with
+ * the same buffers; pageable buffers take the plain copy-apply-copy path. */
 emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y);
 /* Numerical-error word of the stream-ordered calls (synchronises op's work). */
 emfgpu_status emfgpu_op_check(emfgpu_op* op, int64_t* bad_element, int* bad_qpoint);
