@@ -16,6 +16,9 @@
 //    as contiguous vector stores, for the node phase (gather.cu).
 // The quadrature-point algebra is in qp.cuh.
 #pragma once
+#include <climits>
+
+#include "gather.cuh"
 #include "kernels.cuh"
 
 namespace emfgpu {
@@ -367,6 +370,40 @@ __device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T
   }
 }
 
+// ---- fused node phase ---------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Node chunk c of the fused schedule: waits until the element layers of its
+// slab are finished, then assembles THREADS * k nodes exactly like
+// node_gather_kernel (gather.cuh), reading the element results through L2.
+template <typename T, int P, int THREADS>
+__device__ __forceinline__ void node_chunk(const KArgs<T>& a, int c, int tid) {
+  const FuseSched& f = a.fs;
+  const int s = (int)f.fd_cps.div((uint32_t)c);
+  const int j = c - s * f.chunks_per_slab;
+  if (tid == 0) {
+    const unsigned need = (unsigned)(a.nx * a.ny);
+    while (ld_acquire_gpu(&f.ctr[2 + s]) < need) __nanosleep(64);
+    if (s > 0)
+      while (ld_acquire_gpu(&f.ctr[1 + s]) < need) __nanosleep(64);
+  }
+  __syncthreads();
+  const int mxy = a.mx * a.my;
+  const int total = (s == a.nz - 1 ? P + 1 : P) * mxy;
+  const int end = min(total, (j + 1) * f.chunk_nodes);
+  for (int idx = j * f.chunk_nodes + tid; idx < end; idx += THREADS) {
+    const int pl = (int)f.fd_mxy.div((uint32_t)idx);
+    const int rem = idx - pl * mxy;
+    const int b = (int)f.fd_mx.div((uint32_t)rem);
+    assemble_node<T, P, true>(a.loc, nullptr, nullptr, a.x, static_cast<T*>(f.y), rem - b * a.mx, b, s * P + pl,
+                              a.nx, a.ny, a.nz, a.faces, 0, f.periodic_y);
+  }
+}
+
 // ---- the kernel -------------------------------------------------------------------
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 struct ApplyV2Smem {
@@ -392,7 +429,7 @@ constexpr int minb_v2() {
   return TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB;
 }
 
-template <typename T, int P, int MODEL, int STRAT, bool CART>
+template <typename T, int P, int MODEL, int STRAT, bool CART, bool FUSE = false>
 __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P, MODEL, STRAT, CART>()))
     apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
   using SM = ApplyV2Smem<T, P, MODEL, STRAT, CART>;
@@ -449,23 +486,12 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     return zero;
   };
 
-  int64_t g = blockIdx.x;
-  int buf = 0;
-  bool zero_cur = true, zero_next = true;
-  if (g < ngroups) zero_cur = prefetch(g, 0);
-  for (; g < ngroups; g += stride, buf ^= 1) {
-    const bool more = g + stride < ngroups;
-    if (more)
-      zero_next = prefetch(g + stride, buf ^ 1);
-    else
-      cp_async_commit();
-    cp_async_wait<1>();
+  // element group g, staged in buffer buf (its cp.async group complete)
+  auto compute = [&](int64_t g, int buf, bool zero_me) {
     const int64_t e = g * EPB + el + a.e_begin;
     const bool valid = e < a.nel;
     // Dirichlet columns are masked (operator.hpp:604-605); zero the stale
     // staging values of padding elements.
-    const bool zero_me = zero_cur;
-    zero_cur = zero_next;
     if (zero_me) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) sm.stage[buf][el][c][qs] = T(0);
@@ -632,6 +658,88 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     esync();
     if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
     esync();  // staging buffer `buf` and r1/r2 are reused next
+    if constexpr (FUSE) {
+      // publish the element to the node chunks of its layer: the element's
+      // stores are ordered before the count by the barrier and the fence
+      if (q == 0 && valid) {
+        __threadfence();
+        atomicAdd(&a.fs.ctr[2 + a.fd_nxy.div((uint32_t)e)], 1u);
+      }
+    }
+  };
+
+  if constexpr (!FUSE) {
+    int64_t g = blockIdx.x;
+    int buf = 0;
+    bool zero_cur = true, zero_next = true;
+    if (g < ngroups) zero_cur = prefetch(g, 0);
+    for (; g < ngroups; g += stride, buf ^= 1) {
+      const bool more = g + stride < ngroups;
+      if (more)
+        zero_next = prefetch(g + stride, buf ^ 1);
+      else
+        cp_async_commit();
+      cp_async_wait<1>();
+      const bool zero_me = zero_cur;
+      zero_cur = zero_next;
+      compute(g, buf, zero_me);
+    }
+  } else {
+    // Ticket-scheduled element groups and node chunks.  Invariants that make
+    // the spin-wait of a node chunk deadlock-free without co-residency:
+    //  (1) a node chunk with ticket t only depends on element groups with
+    //      tickets < t (host-built order);
+    //  (2) a CTA runs a node chunk only after computing every element group
+    //      it took before that chunk; the one ticket it may hold meanwhile
+    //      was taken after the chunk's.
+    // So every wait points to a smaller ticket held by a CTA that either
+    // computes it or waits on a still smaller one.
+    constexpr int END = INT_MIN;
+    __shared__ int s_tk[2];
+    unsigned* const ctr = a.fs.ctr;
+    auto code_of = [&](unsigned t) { return t < (unsigned)a.fs.ntasks ? a.fs.tasks[t] : END; };
+    if (tid == 0) s_tk[0] = code_of(atomicAdd(ctr, 1u));
+    __syncthreads();
+    int nxt = s_tk[0];
+    int par = 1, buf = 0;
+    int64_t cur = -1;  // staged element group, -1: none
+    bool zero_cur = true, zero_next = true;
+    while (cur >= 0 || nxt != END) {
+      if (nxt >= 0)
+        zero_next = prefetch(nxt, buf ^ 1);
+      else
+        cp_async_commit();
+      unsigned tk = 0;
+      if (tid == 0 && nxt != END) tk = atomicAdd(ctr, 1u);  // consumed after the compute
+      if (cur >= 0) {
+        cp_async_wait<1>();
+        compute(cur, buf, zero_cur);
+      }
+      if (tid == 0) s_tk[par] = nxt != END ? code_of(tk) : END;
+      __syncthreads();
+      const int nn = s_tk[par];
+      par ^= 1;
+      if (nxt >= 0) {
+        cur = nxt;
+        buf ^= 1;
+        zero_cur = zero_next;
+      } else {
+        cur = -1;
+        if (nxt != END) node_chunk<T, P, EPB * N3>(a, -(nxt + 1), tid);
+      }
+      nxt = nn;
+    }
+    cp_async_wait<0>();
+    // the last CTA out rewinds the counters for the next launch
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(&ctr[1], 1u) == gridDim.x - 1) {
+        ctr[0] = 0;
+        ctr[1] = 0;
+        for (int k = 0; k < a.nz; ++k) ctr[2 + k] = 0;
+        __threadfence();
+      }
+    }
   }
 }
 

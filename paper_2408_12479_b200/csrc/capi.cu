@@ -230,14 +230,15 @@ KArgs<T> kargs(const emfgpu_op* op) {
 }
 
 template <typename T>
-void dispatch_apply(const emfgpu_op* op, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
+bool dispatch_apply(const emfgpu_op* op, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
   const int ks = op->domain ? S_SP_NONE + op->strategy : op->strategy;  // element-kernel strategy code
   switch (op->L->p) {
-    case 1: launch_apply<T, 1>(op->model, ks, a, e0, e1, s); break;
-    case 2: launch_apply<T, 2>(op->model, ks, a, e0, e1, s); break;
-    case 3: launch_apply<T, 3>(op->model, ks, a, e0, e1, s); break;
-    case 4: launch_apply<T, 4>(op->model, ks, a, e0, e1, s); break;
+    case 1: return launch_apply<T, 1>(op->model, ks, a, e0, e1, s);
+    case 2: return launch_apply<T, 2>(op->model, ks, a, e0, e1, s);
+    case 3: return launch_apply<T, 3>(op->model, ks, a, e0, e1, s);
+    case 4: return launch_apply<T, 4>(op->model, ks, a, e0, e1, s);
   }
+  return false;
 }
 template <typename T>
 void dispatch_linearize(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) {
@@ -287,6 +288,112 @@ void apply_elements(emfgpu_op* op, const void* x, int k0, int k1, cudaStream_t s
     dispatch_apply<float>(op, a, e0, e1, s);
   }
   CK(cudaGetLastError());
+}
+
+// Ticket order of the fused apply (apply_v2.cuh, FUSE): element groups in
+// index order; the node chunks of slab s (planes [s p, s p + p), the last slab
+// also plane nz p) follow the group that finishes element layer s + lag, with
+// lag sized so the groups in flight (3 per CTA, at most 4 CTAs/SM) have
+// usually finished when a chunk is taken; the last slabs close the order.
+void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const void* glo, const void* ghi, int kpar,
+                 cudaStream_t s);
+
+// EMFGPU_FUSE: 1 fused node phase, 0 (default) element kernel + node gather,
+// 2 ticket-scheduled element kernel + node gather (measurement only)
+static int fuse_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = std::getenv("EMFGPU_FUSE");
+    mode = e ? std::atoi(e) : 0;
+  }
+  return mode;
+}
+
+static void ensure_fuse_sched(emfgpu_op* op) {
+  if (op->d_tasks) return;
+  const emfgpu_level* L = op->L;
+  const int p = L->p, n3 = (p + 1) * (p + 1) * (p + 1), epb = kV2Epb[p];
+  const int mode = fuse_mode();
+  const char* env_npt = std::getenv("EMFGPU_FUSE_NPT");
+  const char* env_lag = std::getenv("EMFGPU_FUSE_LAG");
+  const int threads = epb * n3, npt = env_npt ? std::max(1, std::atoi(env_npt)) : 4;
+  const int64_t nxy = (int64_t)L->nx * L->ny, mxy = (int64_t)L->mx * L->my;
+  const int64_t ngroups = (L->nel + epb - 1) / epb;
+  const int chunk = threads * npt;
+  const int cps = (int)(((p + 1) * mxy + chunk - 1) / chunk);
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t inflight = (int64_t)3 * sms * 4 * epb;
+  int lag = (int)std::min<int64_t>(L->nz, 1 + (inflight + nxy - 1) / nxy);
+  if (env_lag) lag = std::max(0, std::min(L->nz, std::atoi(env_lag)));
+  const int64_t ntasks = ngroups + (int64_t)L->nz * cps;
+  if (ntasks >= INT32_MAX || mxy * (p + 1) >= INT32_MAX || L->nel >= INT32_MAX)
+    throw ApiError(EMFGPU_ERR_CONFIG, "fused apply: mesh too large for 32-bit tickets");
+  std::vector<int> t;
+  t.reserve((size_t)ntasks);
+  int next_slab = 0;
+  auto push_slab = [&](int sl) {
+    for (int c = 0; c < cps; ++c) t.push_back(-(sl * cps + c) - 1);
+  };
+  for (int64_t g = 0; g < ngroups; ++g) {
+    t.push_back((int)g);
+    // element layers finished by this group: all with (k + 1) nxy <= (g + 1) epb
+    const int64_t done_layers = std::min<int64_t>(L->nz, ((g + 1) * epb) / nxy);
+    while (next_slab < L->nz && next_slab + lag < done_layers) push_slab(next_slab++);
+  }
+  while (next_slab < L->nz) push_slab(next_slab++);
+  if (mode == 2) {  // element tickets only (measurement mode)
+    t.resize((size_t)ngroups);
+    for (int64_t g = 0; g < ngroups; ++g) t[(size_t)g] = (int)g;
+  }
+  op->fs_ntasks = (int)t.size();
+  op->fs_chunk = chunk;
+  op->fs_cps = cps;
+  CK(cudaMalloc(&op->d_tasks, sizeof(int) * t.size()));
+  CK(cudaMemcpy(op->d_tasks, t.data(), sizeof(int) * t.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&op->d_ctr, sizeof(unsigned) * (2 + L->nz)));
+  CK(cudaMemset(op->d_ctr, 0, sizeof(unsigned) * (2 + L->nz)));
+}
+
+
+// Whole-lattice apply y = K x: the element kernel with the node phase fused
+// where the variant supports it, else the element kernel + node gather.
+// Either way the result is bitwise the same (same per-node summation order).
+void apply_full(emfgpu_op* op, const void* x, void* y, cudaStream_t s) {
+  const emfgpu_level* L = op->L;
+  if (fuse_mode() == 0) {
+    apply_elements(op, x, 0, L->nz, s);
+    apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, 0, s);
+    return;
+  }
+  ensure_fuse_sched(op);
+  auto fill = [&](auto& a) {
+    a.fs.tasks = op->d_tasks;
+    a.fs.ctr = op->d_ctr;
+    a.fs.y = y;
+    a.fs.ntasks = op->fs_ntasks;
+    a.fs.chunk_nodes = op->fs_chunk;
+    a.fs.chunks_per_slab = op->fs_cps;
+    a.fs.periodic_y = L->periodic_y;
+    a.fs.fd_cps = FastDiv::make((uint32_t)op->fs_cps);
+    a.fs.fd_mx = FastDiv::make((uint32_t)L->mx);
+    a.fs.fd_mxy = FastDiv::make((uint32_t)(L->mx * L->my));
+  };
+  bool fused;
+  if (op->precision == 64) {
+    KArgs<double> a = kargs<double>(op);
+    a.x = static_cast<const double*>(x);
+    fill(a);
+    fused = dispatch_apply<double>(op, a, 0, L->nel, s);
+  } else {
+    KArgs<float> a = kargs<float>(op);
+    a.x = static_cast<const float*>(x);
+    fill(a);
+    fused = dispatch_apply<float>(op, a, 0, L->nel, s);
+  }
+  CK(cudaGetLastError());
+  if (!fused || fuse_mode() == 2) apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, 0, s);
 }
 
 void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const void* glo, const void* ghi, int kpar,
@@ -599,6 +706,8 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_uk);
   cudaFree(op->d_ukd);
   cudaFree(op->d_loc);
+  cudaFree(op->d_tasks);
+  cudaFree(op->d_ctr);
   cudaFree(op->d_x);
   cudaFree(op->d_y);
   cudaFree(op->d_load);
@@ -669,8 +778,7 @@ emfgpu_status emfgpu_op_apply(emfgpu_op* op, const void* d_x, void* d_y, void* s
   return guarded(&op->last_error, [&] {
     require_linearized(op, "apply_tangent");
     cudaStream_t s = S(stream, op->stream);
-    apply_elements(op, d_x, 0, op->L->nz, s);
-    apply_nodes(op, d_x, d_y, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+    apply_full(op, d_x, d_y, s);
   });
 }
 
@@ -782,8 +890,7 @@ emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y) {
       apply_host_pipelined(op, x, y);
     } else {
       CK(cudaMemcpyAsync(op->d_x, x, bytes, cudaMemcpyHostToDevice, op->stream));
-      apply_elements(op, op->d_x, 0, op->L->nz, op->stream);
-      apply_nodes(op, op->d_x, op->d_y, 0, op->L->mz - 1, nullptr, nullptr, 0, op->stream);
+      apply_full(op, op->d_x, op->d_y, op->stream);
       CK(cudaMemcpyAsync(y, op->d_y, bytes, cudaMemcpyDeviceToHost, op->stream));
     }
     check_err(op, op->stream, nullptr, nullptr, "apply_tangent");
@@ -1106,13 +1213,11 @@ static void cheb_run(emfgpu_cheb* c, T* x, const T* b, int zero_start, cudaStrea
   T* ad = static_cast<T*>(c->ad);
   const T* inv = static_cast<const T*>(c->inv_diag);
   if (!zero_start) {
-    apply_elements(op, x, 0, op->L->nz, s);
-    apply_nodes(op, x, r, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+    apply_full(op, x, r, s);
   }
   launch_cheb_first<T>(x, r, d, b, inv, 1.0 / theta, zero_start, n, s);
   for (int k = 1; k < c->degree; ++k) {
-    apply_elements(op, d, 0, op->L->nz, s);
-    apply_nodes(op, d, ad, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+    apply_full(op, d, ad, s);
     const double rho_new = 1.0 / (2.0 * sigma1 - rho_old);
     launch_cheb_step<T>(x, r, d, ad, inv, rho_new * rho_old, 2.0 * rho_new / delta, n, s);
     rho_old = rho_new;
@@ -1217,8 +1322,7 @@ static void lanczos(emfgpu_op* op, const T* diag, int iterations, uint64_t seed,
   for (int j = 0; j < maxit; ++j) {
     double* v = basis + (size_t)j * n;
     launch_scale_to_T<T>(dis, v, t, n, s);
-    apply_elements(op, t, 0, op->L->nz, s);
-    apply_nodes(op, t, at, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+    apply_full(op, t, at, s);
     launch_scale_from_T<T>(dis, at, w, n, s);
     if (j > 0) launch_axpy_minus(hb, basis + (size_t)(j - 1) * n, w, n, s);
     launch_dot<double>(w, v, n, dbuf + 1, coef + 2 * j, s);  // alpha_j
@@ -1299,8 +1403,7 @@ double devdot(emfgpu_mg* m, const T* a, const T* b, int64_t n, cudaStream_t s) {
 
 template <typename T>
 void op_apply_T(emfgpu_op* op, const T* x, T* y, cudaStream_t s) {
-  apply_elements(op, x, 0, op->L->nz, s);
-  apply_nodes(op, x, y, 0, op->L->mz - 1, nullptr, nullptr, 0, s);
+  apply_full(op, x, y, s);
 }
 
 template <typename T>

@@ -1,0 +1,78 @@
+"""Fused node phase vs element kernel + node gather: bitwise equality and
+device time per apply (L2 flushed), for a list of configurations.
+python tools/fuse_ab.py [n p model strategy precision [amp]] ..."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2408_12479_b200 import emfgpu as G  # noqa: E402
+from paper_2408_12479_b200 import inputs as I  # noqa: E402
+
+CASES = [
+    (32, 3, "cnh", "none", 64, 0.0),
+    (32, 3, "cnh", "scalar", 64, 0.0),
+    (32, 3, "cnh", "none", 64, 0.05),
+    (24, 4, "inh", "none", 64, 0.1),
+    (32, 2, "cnh", "none", 64, 0.0),
+    (32, 1, "cnh", "none", 64, 0.0),
+]
+
+
+def timed(fn, flush, reps=15):
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fn()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def main():
+    cases = CASES
+    if len(sys.argv) > 1:
+        a = sys.argv[1:]
+        cases = [(int(a[0]), int(a[1]), a[2], a[3], int(a[4]), float(a[5]) if len(a) > 5 else 0.0)]
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    for n, p, model, strat, prec, amp in cases:
+        lev = G.FeLevel(n, p=p, map_param=(amp,), dirichlet_faces=1)
+        op = G.ElasticOperator(lev, model, G.MaterialParams(mu=1.0, lam=10.0, kappa_b=1000.0), strat, prec)
+        op.update_linearization(I.make_u0(n, n, n, p, noise=1e-3 * 8 / n))
+        dt = torch.float64 if prec == 64 else torch.float32
+        x = torch.tensor(I.make_v(lev.n_dofs), dtype=dt, device="cuda")
+        y1 = torch.empty_like(x)
+        y2 = torch.empty_like(x)
+        mz = n * p + 1
+
+        def fused():
+            op.apply_tangent_device(x, y1)
+
+        def split():
+            op.apply_elements(x, 0, n)
+            op.apply_nodes(x, y2, 0, mz - 1)
+
+        fused()
+        split()
+        torch.cuda.synchronize()
+        same = torch.equal(y1, y2)
+        for _ in range(3):  # repeated launches must rewind the schedule counters
+            fused()
+        torch.cuda.synchronize()
+        same = same and torch.equal(y1, y2)
+        tf, ts = timed(fused, flush), timed(split, flush)
+        print("n=%d p=%d %s %s fp%d amp=%g: bitwise %s  fused %.4f ms  split %.4f ms  (%.1f%%)  %.3e DoF/s" % (
+            n, p, model, strat, prec, amp, same, tf, ts, 100 * (ts - tf) / ts, lev.n_dofs / (tf * 1e-3)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
