@@ -16,9 +16,6 @@
 //    as contiguous vector stores, for the node phase (gather.cu).
 // The quadrature-point algebra is in qp.cuh.
 #pragma once
-#include <climits>
-
-#include "gather.cuh"
 #include "kernels.cuh"
 
 namespace emfgpu {
@@ -370,40 +367,6 @@ __device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T
   }
 }
 
-// ---- fused node phase ---------------------------------------------------------------
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Node chunk c of the fused schedule: waits until the element layers of its
-// slab are finished, then assembles THREADS * k nodes exactly like
-// node_gather_kernel (gather.cuh), reading the element results through L2.
-template <typename T, int P, int THREADS>
-__device__ __forceinline__ void node_chunk(const KArgs<T>& a, int c, int tid) {
-  const FuseSched& f = a.fs;
-  const int s = (int)f.fd_cps.div((uint32_t)c);
-  const int j = c - s * f.chunks_per_slab;
-  if (tid == 0) {
-    const unsigned need = (unsigned)(a.nx * a.ny);
-    while (ld_acquire_gpu(&f.ctr[2 + s]) < need) __nanosleep(64);
-    if (s > 0)
-      while (ld_acquire_gpu(&f.ctr[1 + s]) < need) __nanosleep(64);
-  }
-  __syncthreads();
-  const int mxy = a.mx * a.my;
-  const int total = (s == a.nz - 1 ? P + 1 : P) * mxy;
-  const int end = min(total, (j + 1) * f.chunk_nodes);
-  for (int idx = j * f.chunk_nodes + tid; idx < end; idx += THREADS) {
-    const int pl = (int)f.fd_mxy.div((uint32_t)idx);
-    const int rem = idx - pl * mxy;
-    const int b = (int)f.fd_mx.div((uint32_t)rem);
-    assemble_node<T, P, true>(a.loc, nullptr, nullptr, a.x, static_cast<T*>(f.y), rem - b * a.mx, b, s * P + pl,
-                              a.nx, a.ny, a.nz, a.faces, 0, f.periodic_y);
-  }
-}
-
 // ---- the kernel -------------------------------------------------------------------
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 struct ApplyV2Smem {
@@ -421,15 +384,32 @@ struct ApplyV2Smem {
 // except for the variants that ptxas fits into 128 registers without spills,
 // which measured faster at 4 CTAs/SM (cfg1: headline fp64 none 0.1676 ->
 // 0.1654 ms, spatial tensor 0.1205 -> 0.1148 ms); fp32 always 4.
+#ifndef EMF_MINB_V2D_FORCE
+#define EMF_MINB_V2D_FORCE 0
+#endif
+#ifndef EMF_MINB_Q4C
+#define EMF_MINB_Q4C 2
+#endif
+#ifndef EMF_MINB_FIBER_V2D
+#define EMF_MINB_FIBER_V2D 2
+#endif
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 constexpr int minb_v2() {
   if (sizeof(T) == 4) return TileV2<P>::MINB;
+  if (EMF_MINB_V2D_FORCE) return EMF_MINB_V2D_FORCE;  // experiments (tools/build_variant.sh)
   if (P == 3 && MODEL == CNH && ((STRAT == S_NONE && CART) || STRAT == S_SP_NONE || STRAT == S_SP_TENSOR)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
+  // Q4 curved fp64: 2 CTAs/SM (255 registers) beats 3 with spills
+  // (24^3 Q4 curved iNH none 0.241 -> 0.214 ms, tensor 0.220 -> 0.198 ms);
+  // on axis-aligned meshes 3 stays ahead (0.2028 vs 0.2058 ms)
+  if (P == 4 && !CART) return EMF_MINB_Q4C;
+  // fibre fp64 at Q3: 2 CTAs/SM, spill-free (32^3 curved none 0.278 -> 0.249 ms,
+  // scalar 0.261 -> 0.232 ms); Q2 stays at 3 (0.128 vs 0.136 ms)
+  if (MODEL == FIBER && P >= 3) return EMF_MINB_FIBER_V2D;
   return TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB;
 }
 
-template <typename T, int P, int MODEL, int STRAT, bool CART, bool FUSE = false>
+template <typename T, int P, int MODEL, int STRAT, bool CART>
 __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P, MODEL, STRAT, CART>()))
     apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
   using SM = ApplyV2Smem<T, P, MODEL, STRAT, CART>;
@@ -460,15 +440,23 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   };
   const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
   const int qs = lat<N>(qi, qj, qk);  // padded slot of this thread's point
-  const int64_t stride = gridDim.x;
 
   // per-thread tensor-product weight of this thread's point (operator.hpp:492)
   const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
-  // issue the cp.async copies of group g into staging buffer b; returns true
+  // Work units handed out by a ticket counter (dynamic load balance; the
+  // unit index is opaque to the compiler, which keeps it from building
+  // strength-reduced address induction variables that spilled on Q4).  When
+  // every element of the CTA synchronises on its own named barrier, each
+  // element is its own worker with its own ticket stream; otherwise a unit is
+  // a group of EPB elements.
+  constexpr bool kPerElem = N3 % 32 == 0 && EPB > 1;
+  const int64_t nunits = kPerElem ? a.nel - a.e_begin : ngroups;
+  auto elem_of = [&](int64_t u) -> int64_t { return (kPerElem ? u : u * EPB + el) + a.e_begin; };
+  // issue the cp.async copies of unit u into staging buffer b; returns true
   // when this thread's staged x value must be zeroed (Dirichlet node or
   // padding element), decided here where the lattice position is at hand
-  auto prefetch = [&](int64_t g, int b) -> bool {
-    const int64_t e = g * EPB + el + a.e_begin;
+  auto prefetch = [&](int64_t u, int b) -> bool {
+    const int64_t e = elem_of(u);
     bool zero = true;
     if (e < a.nel) {
       const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
@@ -486,9 +474,9 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     return zero;
   };
 
-  // element group g, staged in buffer buf (its cp.async group complete)
-  auto compute = [&](int64_t g, int buf, bool zero_me) {
-    const int64_t e = g * EPB + el + a.e_begin;
+  // unit u, staged in buffer buf (its cp.async group complete)
+  auto compute = [&](int64_t u, int buf, bool zero_me) {
+    const int64_t e = elem_of(u);
     const bool valid = e < a.nel;
     // Dirichlet columns are masked (operator.hpp:604-605); zero the stale
     // staging values of padding elements.
@@ -658,87 +646,52 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     esync();
     if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
     esync();  // staging buffer `buf` and r1/r2 are reused next
-    if constexpr (FUSE) {
-      // publish the element to the node chunks of its layer: the element's
-      // stores are ordered before the count by the barrier and the fence
-      if (q == 0 && valid) {
-        __threadfence();
-        atomicAdd(&a.fs.ctr[2 + a.fd_nxy.div((uint32_t)e)], 1u);
-      }
-    }
   };
 
-  if constexpr (!FUSE) {
-    int64_t g = blockIdx.x;
-    int buf = 0;
-    bool zero_cur = true, zero_next = true;
-    if (g < ngroups) zero_cur = prefetch(g, 0);
-    for (; g < ngroups; g += stride, buf ^= 1) {
-      const bool more = g + stride < ngroups;
-      if (more)
-        zero_next = prefetch(g + stride, buf ^ 1);
-      else
-        cp_async_commit();
+  // The first two units of a worker are static (no atomic round trip before
+  // the first element); later tickets come from a.tk[0], taken one unit ahead
+  // of need by the worker's leader and published through shared memory, read
+  // after the next compute's closing barrier.
+  __shared__ int64_t s_tk[EPB][2];
+  const int64_t nw = (int64_t)gridDim.x * (kPerElem ? EPB : 1);
+  const int64_t wid = kPerElem ? (int64_t)blockIdx.x * EPB + el : blockIdx.x;
+  const bool leader = kPerElem ? q == 0 : tid == 0;
+  const int slot = kPerElem ? el : 0;
+  int64_t cur = -1, nxt = wid, pend = wid + nw;  // cur: staged unit (-1: none)
+  int buf = 0, par = 0;
+  bool zero_cur = true, zero_next = true;
+  while (cur >= 0 || nxt < nunits) {
+    if (nxt < nunits)
+      zero_next = prefetch(nxt, buf ^ 1);
+    else
+      cp_async_commit();
+    if (leader) {
+      s_tk[slot][par] = pend;
+      if (pend < nunits) pend = 2 * nw + atomicAdd(a.tk, 1u);
+    }
+    if (cur >= 0) {
       cp_async_wait<1>();
-      const bool zero_me = zero_cur;
+      compute(cur, buf, zero_cur);  // ends with the worker's barrier
+    } else {
+      esync();
+    }
+    const int64_t nn = s_tk[slot][par];
+    par ^= 1;
+    if (nxt < nunits) {
+      cur = nxt;
+      buf ^= 1;
       zero_cur = zero_next;
-      compute(g, buf, zero_me);
+    } else {
+      cur = -1;
     }
-  } else {
-    // Ticket-scheduled element groups and node chunks.  Invariants that make
-    // the spin-wait of a node chunk deadlock-free without co-residency:
-    //  (1) a node chunk with ticket t only depends on element groups with
-    //      tickets < t (host-built order);
-    //  (2) a CTA runs a node chunk only after computing every element group
-    //      it took before that chunk; the one ticket it may hold meanwhile
-    //      was taken after the chunk's.
-    // So every wait points to a smaller ticket held by a CTA that either
-    // computes it or waits on a still smaller one.
-    constexpr int END = INT_MIN;
-    __shared__ int s_tk[2];
-    unsigned* const ctr = a.fs.ctr;
-    auto code_of = [&](unsigned t) { return t < (unsigned)a.fs.ntasks ? a.fs.tasks[t] : END; };
-    if (tid == 0) s_tk[0] = code_of(atomicAdd(ctr, 1u));
-    __syncthreads();
-    int nxt = s_tk[0];
-    int par = 1, buf = 0;
-    int64_t cur = -1;  // staged element group, -1: none
-    bool zero_cur = true, zero_next = true;
-    while (cur >= 0 || nxt != END) {
-      if (nxt >= 0)
-        zero_next = prefetch(nxt, buf ^ 1);
-      else
-        cp_async_commit();
-      unsigned tk = 0;
-      if (tid == 0 && nxt != END) tk = atomicAdd(ctr, 1u);  // consumed after the compute
-      if (cur >= 0) {
-        cp_async_wait<1>();
-        compute(cur, buf, zero_cur);
-      }
-      if (tid == 0) s_tk[par] = nxt != END ? code_of(tk) : END;
-      __syncthreads();
-      const int nn = s_tk[par];
-      par ^= 1;
-      if (nxt >= 0) {
-        cur = nxt;
-        buf ^= 1;
-        zero_cur = zero_next;
-      } else {
-        cur = -1;
-        if (nxt != END) node_chunk<T, P, EPB * N3>(a, -(nxt + 1), tid);
-      }
-      nxt = nn;
-    }
-    cp_async_wait<0>();
-    // the last CTA out rewinds the counters for the next launch
-    if (tid == 0) {
-      __threadfence();
-      if (atomicAdd(&ctr[1], 1u) == gridDim.x - 1) {
-        ctr[0] = 0;
-        ctr[1] = 0;
-        for (int k = 0; k < a.nz; ++k) ctr[2 + k] = 0;
-        __threadfence();
-      }
+    nxt = nn;
+  }
+  cp_async_wait<0>();
+  // the last worker out rewinds the counter for the next launch on this slot
+  if (leader) {
+    if (atomicAdd(a.tk + 1, 1u) == (unsigned)(nw - 1)) {
+      a.tk[0] = 0;
+      a.tk[1] = 0;
     }
   }
 }

@@ -226,19 +226,19 @@ KArgs<T> kargs(const emfgpu_op* op) {
   a.fd_nxy = FastDiv::make((uint32_t)(L->nx * L->ny));
   a.spatial = op->domain;
   a.coords = L->d_coords;
+  a.tk = op->d_ctr + 2 * (op->ticket_seq++ % emfgpu_op::kTicketSlots);
   return a;
 }
 
 template <typename T>
-bool dispatch_apply(const emfgpu_op* op, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
+void dispatch_apply(const emfgpu_op* op, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
   const int ks = op->domain ? S_SP_NONE + op->strategy : op->strategy;  // element-kernel strategy code
   switch (op->L->p) {
-    case 1: return launch_apply<T, 1>(op->model, ks, a, e0, e1, s);
-    case 2: return launch_apply<T, 2>(op->model, ks, a, e0, e1, s);
-    case 3: return launch_apply<T, 3>(op->model, ks, a, e0, e1, s);
-    case 4: return launch_apply<T, 4>(op->model, ks, a, e0, e1, s);
+    case 1: launch_apply<T, 1>(op->model, ks, a, e0, e1, s); break;
+    case 2: launch_apply<T, 2>(op->model, ks, a, e0, e1, s); break;
+    case 3: launch_apply<T, 3>(op->model, ks, a, e0, e1, s); break;
+    case 4: launch_apply<T, 4>(op->model, ks, a, e0, e1, s); break;
   }
-  return false;
 }
 template <typename T>
 void dispatch_linearize(const emfgpu_op* op, const KArgs<T>& a, cudaStream_t s) {
@@ -290,112 +290,6 @@ void apply_elements(emfgpu_op* op, const void* x, int k0, int k1, cudaStream_t s
   CK(cudaGetLastError());
 }
 
-// Ticket order of the fused apply (apply_v2.cuh, FUSE): element groups in
-// index order; the node chunks of slab s (planes [s p, s p + p), the last slab
-// also plane nz p) follow the group that finishes element layer s + lag, with
-// lag sized so the groups in flight (3 per CTA, at most 4 CTAs/SM) have
-// usually finished when a chunk is taken; the last slabs close the order.
-void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const void* glo, const void* ghi, int kpar,
-                 cudaStream_t s);
-
-// EMFGPU_FUSE: 1 fused node phase, 0 (default) element kernel + node gather,
-// 2 ticket-scheduled element kernel + node gather (measurement only)
-static int fuse_mode() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = std::getenv("EMFGPU_FUSE");
-    mode = e ? std::atoi(e) : 0;
-  }
-  return mode;
-}
-
-static void ensure_fuse_sched(emfgpu_op* op) {
-  if (op->d_tasks) return;
-  const emfgpu_level* L = op->L;
-  const int p = L->p, n3 = (p + 1) * (p + 1) * (p + 1), epb = kV2Epb[p];
-  const int mode = fuse_mode();
-  const char* env_npt = std::getenv("EMFGPU_FUSE_NPT");
-  const char* env_lag = std::getenv("EMFGPU_FUSE_LAG");
-  const int threads = epb * n3, npt = env_npt ? std::max(1, std::atoi(env_npt)) : 4;
-  const int64_t nxy = (int64_t)L->nx * L->ny, mxy = (int64_t)L->mx * L->my;
-  const int64_t ngroups = (L->nel + epb - 1) / epb;
-  const int chunk = threads * npt;
-  const int cps = (int)(((p + 1) * mxy + chunk - 1) / chunk);
-  int dev = 0, sms = 148;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t inflight = (int64_t)3 * sms * 4 * epb;
-  int lag = (int)std::min<int64_t>(L->nz, 1 + (inflight + nxy - 1) / nxy);
-  if (env_lag) lag = std::max(0, std::min(L->nz, std::atoi(env_lag)));
-  const int64_t ntasks = ngroups + (int64_t)L->nz * cps;
-  if (ntasks >= INT32_MAX || mxy * (p + 1) >= INT32_MAX || L->nel >= INT32_MAX)
-    throw ApiError(EMFGPU_ERR_CONFIG, "fused apply: mesh too large for 32-bit tickets");
-  std::vector<int> t;
-  t.reserve((size_t)ntasks);
-  int next_slab = 0;
-  auto push_slab = [&](int sl) {
-    for (int c = 0; c < cps; ++c) t.push_back(-(sl * cps + c) - 1);
-  };
-  for (int64_t g = 0; g < ngroups; ++g) {
-    t.push_back((int)g);
-    // element layers finished by this group: all with (k + 1) nxy <= (g + 1) epb
-    const int64_t done_layers = std::min<int64_t>(L->nz, ((g + 1) * epb) / nxy);
-    while (next_slab < L->nz && next_slab + lag < done_layers) push_slab(next_slab++);
-  }
-  while (next_slab < L->nz) push_slab(next_slab++);
-  if (mode == 2) {  // element tickets only (measurement mode)
-    t.resize((size_t)ngroups);
-    for (int64_t g = 0; g < ngroups; ++g) t[(size_t)g] = (int)g;
-  }
-  op->fs_ntasks = (int)t.size();
-  op->fs_chunk = chunk;
-  op->fs_cps = cps;
-  CK(cudaMalloc(&op->d_tasks, sizeof(int) * t.size()));
-  CK(cudaMemcpy(op->d_tasks, t.data(), sizeof(int) * t.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&op->d_ctr, sizeof(unsigned) * (2 + L->nz)));
-  CK(cudaMemset(op->d_ctr, 0, sizeof(unsigned) * (2 + L->nz)));
-}
-
-
-// Whole-lattice apply y = K x: the element kernel with the node phase fused
-// where the variant supports it, else the element kernel + node gather.
-// Either way the result is bitwise the same (same per-node summation order).
-void apply_full(emfgpu_op* op, const void* x, void* y, cudaStream_t s) {
-  const emfgpu_level* L = op->L;
-  if (fuse_mode() == 0) {
-    apply_elements(op, x, 0, L->nz, s);
-    apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, 0, s);
-    return;
-  }
-  ensure_fuse_sched(op);
-  auto fill = [&](auto& a) {
-    a.fs.tasks = op->d_tasks;
-    a.fs.ctr = op->d_ctr;
-    a.fs.y = y;
-    a.fs.ntasks = op->fs_ntasks;
-    a.fs.chunk_nodes = op->fs_chunk;
-    a.fs.chunks_per_slab = op->fs_cps;
-    a.fs.periodic_y = L->periodic_y;
-    a.fs.fd_cps = FastDiv::make((uint32_t)op->fs_cps);
-    a.fs.fd_mx = FastDiv::make((uint32_t)L->mx);
-    a.fs.fd_mxy = FastDiv::make((uint32_t)(L->mx * L->my));
-  };
-  bool fused;
-  if (op->precision == 64) {
-    KArgs<double> a = kargs<double>(op);
-    a.x = static_cast<const double*>(x);
-    fill(a);
-    fused = dispatch_apply<double>(op, a, 0, L->nel, s);
-  } else {
-    KArgs<float> a = kargs<float>(op);
-    a.x = static_cast<const float*>(x);
-    fill(a);
-    fused = dispatch_apply<float>(op, a, 0, L->nel, s);
-  }
-  CK(cudaGetLastError());
-  if (!fused || fuse_mode() == 2) apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, 0, s);
-}
-
 void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const void* glo, const void* ghi, int kpar,
                  cudaStream_t s) {
   const emfgpu_level* L = op->L;
@@ -408,6 +302,13 @@ void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const vo
                               static_cast<const float*>(ghi), static_cast<const float*>(x), static_cast<float*>(y),
                               L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s);
   CK(cudaGetLastError());
+}
+
+// Whole-lattice apply y = K x: element kernel + node gather.
+void apply_full(emfgpu_op* op, const void* x, void* y, cudaStream_t s) {
+  const emfgpu_level* L = op->L;
+  apply_elements(op, x, 0, L->nz, s);
+  apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, 0, s);
 }
 
 void check_err(emfgpu_op* op, cudaStream_t s, int64_t* be, int* bq, const char* what) {
@@ -679,6 +580,8 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
     const size_t ns = nsize(op.get());
     CK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&op->d_loc, ns * l->nel * l->nq3 * 3));
+    CK(cudaMalloc(&op->d_ctr, sizeof(unsigned) * 2 * emfgpu_op::kTicketSlots));
+    CK(cudaMemset(op->d_ctr, 0, sizeof(unsigned) * 2 * emfgpu_op::kTicketSlots));
     CK(cudaMalloc(&op->d_err, sizeof(unsigned long long)));
     CK(cudaMemset(op->d_err, 0xff, sizeof(unsigned long long)));
     CK(cudaMallocHost(&op->h_err, sizeof(unsigned long long)));
@@ -706,7 +609,6 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_uk);
   cudaFree(op->d_ukd);
   cudaFree(op->d_loc);
-  cudaFree(op->d_tasks);
   cudaFree(op->d_ctr);
   cudaFree(op->d_x);
   cudaFree(op->d_y);

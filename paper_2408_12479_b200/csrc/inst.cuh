@@ -11,13 +11,11 @@ namespace emfgpu {
 
 static_assert(TileV2<EMF_P>::EPB == kV2Epb[EMF_P], "internal.h kV2Epb out of date");
 
-// Returns true when the node phase ran fused into the element kernel
-// (a.fs.tasks set and the variant is the v2 kernel).
 template <int MODEL, int STRAT, bool CART>
-static bool apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
+static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
   constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P>::EPB, THREADS = EPB * N * N * N;
   const int64_t cnt = e1 - e0;
-  if (cnt <= 0) return false;
+  if (cnt <= 0) return;
   // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):
   // warp-per-element (v3) for fp32 and for the fp64 strategies without u_k
   // sweeps; 2 elements per CTA with named barriers (v2) for fp64 none/scalar.
@@ -43,27 +41,7 @@ static bool apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
     const int64_t blocks = (cnt + kV3Warps - 1) / kV3Warps;
     const int64_t grid = std::min<int64_t>(blocks, (int64_t)sms3 * per_sm3);
     apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART><<<(unsigned)grid, 32 * kV3Warps, smem, s>>>(b);
-    return false;
-  } else {
-    if (a.fs.tasks) {
-      // fused node phase: one wave at the fused kernel's occupancy (any grid
-      // is deadlock-free, see apply_v2.cuh; one wave is the fast one)
-      static int per_smf = 0, smsf = 0;
-      if (per_smf == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&smsf, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_smf,
-                                                      apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART, true>,
-                                                      THREADS, 0);
-        if (per_smf < 1) per_smf = 1;
-      }
-      KArgs<EMF_T> b = a;
-      b.e_begin = 0;
-      apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART, true><<<(unsigned)(smsf * per_smf), THREADS, 0, s>>>(
-          b, (a.nel + EPB - 1) / EPB);
-      return true;
-    }
+    return;
   }
   // persistent grid: one wave at the kernel's occupancy
   static int per_sm = 0, sms = 0;
@@ -80,11 +58,10 @@ static bool apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   const int64_t groups = (cnt + EPB - 1) / EPB;
   const int64_t grid = std::min<int64_t>(groups, (int64_t)sms * per_sm);
   apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART><<<(unsigned)grid, THREADS, 0, s>>>(b, groups);
-  return false;
 }
 
 template <>
-bool launch_apply<EMF_T, EMF_P>(int model, int strategy, const KArgs<EMF_T>& a, int64_t e0, int64_t e1,
+void launch_apply<EMF_T, EMF_P>(int model, int strategy, const KArgs<EMF_T>& a, int64_t e0, int64_t e1,
                                cudaStream_t s) {
 #define EMF_CASE(M, S)                                                  \
   if (model == M && strategy == S) {                                    \
@@ -101,7 +78,6 @@ bool launch_apply<EMF_T, EMF_P>(int model, int strategy, const KArgs<EMF_T>& a, 
   EMF_SP(INH, S_SP_NONE) EMF_SP(INH, S_SP_SCALAR) EMF_SP(INH, S_SP_TENSOR)
   EMF_SP(FIBER, S_SP_NONE) EMF_SP(FIBER, S_SP_SCALAR) EMF_SP(FIBER, S_SP_TENSOR)
 #undef EMF_SP
-  return false;
 }
 
 template <>

@@ -16,10 +16,9 @@ constexpr int kMaxP = 4;
 // elements per CTA of the v2 element kernel by degree (TileV2, apply_v2.cuh)
 constexpr int kV2Epb[5] = {0, 16, 4, 2, 1};
 
-// Per-(T,P) launchers, defined in inst_<t><p>.cu.  launch_apply returns true
-// when it also ran the node phase (fused schedule in a.fs).
+// Per-(T,P) launchers, defined in inst_<t><p>.cu.
 template <typename T, int P>
-bool launch_apply(int model, int strategy, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s);
+void launch_apply(int model, int strategy, const KArgs<T>& a, int64_t e0, int64_t e1, cudaStream_t s);
 template <typename T, int P>
 void launch_linearize(int model, const KArgs<T>& a, cudaStream_t s);
 template <typename T, int P>
@@ -161,10 +160,11 @@ struct emfgpu_op {
   const void* g_x = nullptr;
   void* g_y = nullptr;
   int g_nch = 0;
-  // fused node phase schedule (apply_v2 FUSE): ticket order and counters
-  int* d_tasks = nullptr;
+  // apply_v2 ticket counters: a ring of slots, one per launch, so launches
+  // of this operator on different streams never share a counter
+  static constexpr int kTicketSlots = 256;
   unsigned* d_ctr = nullptr;
-  int fs_ntasks = 0, fs_chunk = 0, fs_cps = 0;
+  mutable unsigned ticket_seq = 0;
   bool linearized = false;
   uint64_t checksum = 0;
   std::string last_error;

@@ -70,23 +70,6 @@ struct FastDiv {
   }
 };
 
-// Fused node phase (apply_v2 with FUSE): the element kernel also assembles
-// the lattice nodes, slab by slab, once the element layers a slab depends on
-// are finished.  Work is handed out by a ticket counter in the order of
-// `tasks` (element groups in index order, the node chunks of slab s inserted
-// after the groups of layer s + lag), so a node chunk only ever waits for
-// element groups with smaller tickets (see apply_v2.cuh for the argument).
-struct FuseSched {
-  const int* tasks;     // per ticket: g >= 0 element group g, -(c+1) node chunk c
-  unsigned* ctr;        // [0] ticket, [1] CTAs exited, [2 + k] finished elements of layer k
-  void* y;              // output vector (Number)
-  int ntasks;
-  int chunk_nodes;      // nodes per chunk (threads * nodes per thread)
-  int chunks_per_slab;  // slab s: node planes [s p, s p + p) (the last slab also holds plane nz p)
-  int periodic_y;
-  FastDiv fd_cps, fd_mx, fd_mxy;
-};
-
 template <typename T>
 struct KArgs {
   const T* x;          // input vector (3 per node), apply / unused by diag
@@ -121,7 +104,7 @@ struct KArgs {
   int64_t hq_stride;
   int spatial;           // Formulation::domain == spatial (linearize / diagonal / residual)
   const double* coords;  // node coordinates (spatial linearization: J_t = J0 + Grad_xi u_k)
-  FuseSched fs;          // fused node phase (tasks == nullptr: element phase only)
+  unsigned* tk;          // apply_v2 ticket counter slot: [0] next ticket, [1] workers done
 };
 
 // Stored scalars of the scalar/tensor strategies (load_scalar_fields,

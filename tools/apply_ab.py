@@ -1,6 +1,8 @@
-"""Fused node phase vs element kernel + node gather: bitwise equality and
-device time per apply (L2 flushed), for a list of configurations.
-python tools/fuse_ab.py [n p model strategy precision [amp]] ..."""
+"""Device apply (emfgpu_op_apply) vs the split-phase entry points
+(apply_elements + apply_nodes): bitwise equality and device time per apply
+(L2 flushed), for a list of configurations.  With EMFGPU_LIB pointing at a
+variant build (tools/build_variant.sh) it is the launch-bound A/B harness.
+python tools/apply_ab.py [n p model strategy precision [amp]]"""
 import os
 import sys
 
@@ -54,23 +56,23 @@ def main():
         y2 = torch.empty_like(x)
         mz = n * p + 1
 
-        def fused():
+        def whole():
             op.apply_tangent_device(x, y1)
 
         def split():
             op.apply_elements(x, 0, n)
             op.apply_nodes(x, y2, 0, mz - 1)
 
-        fused()
+        whole()
         split()
         torch.cuda.synchronize()
         same = torch.equal(y1, y2)
-        for _ in range(3):  # repeated launches must rewind the schedule counters
-            fused()
+        for _ in range(3):  # repeated launches must rewind the ticket counters
+            whole()
         torch.cuda.synchronize()
         same = same and torch.equal(y1, y2)
-        tf, ts = timed(fused, flush), timed(split, flush)
-        print("n=%d p=%d %s %s fp%d amp=%g: bitwise %s  fused %.4f ms  split %.4f ms  (%.1f%%)  %.3e DoF/s" % (
+        tf, ts = timed(whole, flush), timed(split, flush)
+        print("n=%d p=%d %s %s fp%d amp=%g: bitwise %s  apply %.4f ms  split %.4f ms  (%.1f%%)  %.3e DoF/s" % (
             n, p, model, strat, prec, amp, same, tf, ts, 100 * (ts - tf) / ts, lev.n_dofs / (tf * 1e-3)), flush=True)
 
 
