@@ -106,10 +106,21 @@ __device__ __forceinline__ void cp_async_wait() {
 // (component c, line l).  M[row*N + col] are compile-time-indexed tables.
 
 // Forward x-sweep: in[c] -> tB[c] = Bx in, tD[c] = Dx in.
-template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
-__device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, const T* Dm, int w) {
+// Dense pencil mapping (NE > 1): the NE elements of a CTA share one pencil
+// index space, pencil wk of element wk / (3 N^2); SI / SO are the element
+// strides of the input / output arrays.  The CTA's threads then run the
+// NE * 3N^2 pencils back to back, so only the warps that own pencils issue
+// sweep instructions (Q3: 3 of 4 warps instead of 4 half-used ones).
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
+          int SI = 0, int SO = 0>
+__device__ __forceinline__ void fw_x(const T* in0, T* tb0, T* td0, const T* Bm, const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
+  for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
+    const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
+    const int wk = wp - e_l * 3 * L::N2;
+    const T* const in = in0 + e_l * SI;
+    T* const tb = tb0 + e_l * SO;
+    T* const td = td0 + e_l * SO;
     // fp64: pencil order j, c, k (j fastest) so a quarter-warp spans two
     // components (SIZE 82); fp32: component-major (measured better)
     const int j = sizeof(T) == 8 ? wk % N : (wk % L::N2) % N;
@@ -133,11 +144,19 @@ __device__ __forceinline__ void fw_x(const T* in, T* tb, T* td, const T* Bm, con
 }
 
 // Forward y-sweep: sBB = By tB, sBD = Dy tB, sDB = By tD.
-template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
-__device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T* sdb,
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
+          int SR = 0>
+__device__ __forceinline__ void fw_y(const T* tb0, const T* td0, T* sbb0, T* sbd0, T* sdb0,
                                      const T* Bm, const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
+  for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
+    const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
+    const int wk = wp - e_l * 3 * L::N2;
+    const T* const tb = tb0 + e_l * SR;
+    const T* const td = td0 + e_l * SR;
+    T* const sbb = sbb0 + e_l * SR;
+    T* const sbd = sbd0 + e_l * SR;
+    T* const sdb = sdb0 + e_l * SR;
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T ub[N], ud[N];
 #pragma unroll
@@ -162,11 +181,18 @@ __device__ __forceinline__ void fw_y(const T* tb, const T* td, T* sbb, T* sbd, T
 }
 
 // Forward z-sweep: g[c][0] = Bz sDB, g[c][1] = Bz sBD, g[c][2] = Dz sBB.
-template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
-__device__ __forceinline__ void fw_z(const T* sbb, const T* sbd, const T* sdb, T* g, const T* Bm,
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
+          int SR = 0>
+__device__ __forceinline__ void fw_z(const T* sbb0, const T* sbd0, const T* sdb0, T* g0, const T* Bm,
                                      const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
+  for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
+    const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
+    const int wk = wp - e_l * 3 * L::N2;
+    const T* const sbb = sbb0 + e_l * SR;
+    const T* const sbd = sbd0 + e_l * SR;
+    const T* const sdb = sdb0 + e_l * SR;
+    T* const g = g0 + e_l * SR;
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T u0[N], u1[N], u2[N];
 #pragma unroll
@@ -283,10 +309,15 @@ __device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* D
 }
 
 // Transposed z-sweep (node index along z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2.
-template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
-__device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* Dm, int w) {
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
+          int SR = 0>
+__device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
+  for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
+    const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
+    const int wk = wp - e_l * 3 * L::N2;
+    const T* const wv = wv0 + e_l * SR;
+    T* const av = av0 + e_l * SR;
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T u0[N], u1[N], u2[N];
 #pragma unroll
@@ -312,10 +343,15 @@ __device__ __forceinline__ void tr_z(const T* wv, T* av, const T* Bm, const T* D
 }
 
 // Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
-template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
-__device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* Dm, int w) {
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
+          int SR = 0>
+__device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
+  for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
+    const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
+    const int wk = wp - e_l * 3 * L::N2;
+    const T* const av = av0 + e_l * SR;
+    T* const qv = qv0 + e_l * SR;
     const int c = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T u0[N], u1[N], u2[N];
 #pragma unroll
@@ -340,10 +376,16 @@ __device__ __forceinline__ void tr_y(const T* av, T* qv, const T* Bm, const T* D
 
 // Transposed x-sweep: out = Dx^T Q0 + Bx^T Q12, written as N contiguous
 // values of loc[(e*3 + c)*N3 + lexicographic m] (component-major).
-template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3)>
-__device__ __forceinline__ void tr_x(const T* qv, T* loc_e, const T* Bm, const T* Dm, int w) {
+template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
+          int SR = 0>
+__device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T* Dm, int w, int nvalid = 1) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < 3 * L::N2; wk += STRIDE) {
+  for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
+    const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
+    const int wk = wp - e_l * 3 * L::N2;
+    if (NE > 1 && e_l >= nvalid) break;
+    const T* const qv = qv0 + e_l * SR;
+    T* const loc_e = loc0 + e_l * 3 * L::N3;
     const int j = sizeof(T) == 8 ? wk % N : (wk % L::N2) % N;  // pencil order as fw_x
     const int c = sizeof(T) == 8 ? (wk / N) % 3 : wk / L::N2;
     const int k = sizeof(T) == 8 ? wk / (3 * N) : (wk % L::N2) / N;
@@ -384,6 +426,9 @@ struct ApplyV2Smem {
 // except for the variants that ptxas fits into 128 registers without spills,
 // which measured faster at 4 CTAs/SM (cfg1: headline fp64 none 0.1676 ->
 // 0.1654 ms, spatial tensor 0.1205 -> 0.1148 ms); fp32 always 4.
+#ifndef EMF_V2_DENSE
+#define EMF_V2_DENSE 1
+#endif
 #ifndef EMF_MINB_V2D_FORCE
 #define EMF_MINB_V2D_FORCE 0
 #endif
@@ -432,8 +477,12 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   const int el = tid / N3, q = tid % N3;
   // Elements of a CTA only share data through their own slices, so when an
   // element spans whole warps it synchronises on its own named barrier.
+  // Q3 (two 64-thread elements per CTA): dense pencil mapping over the CTA
+  // (see fw_x) with CTA-wide barriers; measured against per-element named
+  // barriers with 48 of 64 threads per element sweeping
+  constexpr bool kDense = EMF_V2_DENSE && N3 == 64 && EPB == 2;
   auto esync = [&]() {
-    if constexpr (N3 % 32 == 0 && EPB > 1)
+    if constexpr (N3 % 32 == 0 && EPB > 1 && !kDense)
       asm volatile("bar.sync %0, %1;\n" ::"r"(el + 1), "n"(N3) : "memory");
     else
       __syncthreads();
@@ -449,7 +498,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   // every element of the CTA synchronises on its own named barrier, each
   // element is its own worker with its own ticket stream; otherwise a unit is
   // a group of EPB elements.
-  constexpr bool kPerElem = N3 % 32 == 0 && EPB > 1;
+  constexpr bool kPerElem = N3 % 32 == 0 && EPB > 1 && !kDense;
   const int64_t nunits = kPerElem ? a.nel - a.e_begin : ngroups;
   auto elem_of = [&](int64_t u) -> int64_t { return (kPerElem ? u : u * EPB + el) + a.e_begin; };
   // issue the cp.async copies of unit u into staging buffer b; returns true
@@ -507,6 +556,27 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     T* const R2 = &sm.r2[el][0][0];
     T gx[9];
     T* const S = &sm.stage[buf][el][0][0];  // kUk: x (arrays 0-2), u_k (3-5)
+    // forward sweeps of staged vector arrays [f0, f0+3): gradients into R2
+    auto fwd_sweeps = [&](int f0) {
+      if constexpr (kDense) {
+        constexpr int SI = SM::NST * SZ, SR = 9 * SZ, TH = EPB * N3;
+        T* const R1a = &sm.r1[0][0][0];
+        T* const R2a = &sm.r2[0][0][0];
+        fw_x<T, N, TH, EPB, SI, SR>(&sm.stage[buf][0][f0][0], R2a, R2a + 3 * SZ, a.Bm, Dfx, tid);
+        esync();
+        fw_y<T, N, TH, EPB, SR>(R2a, R2a + 3 * SZ, R1a, R1a + 3 * SZ, R1a + 6 * SZ, a.Bm, Dfy, tid);
+        esync();
+        fw_z<T, N, TH, EPB, SR>(R1a, R1a + 3 * SZ, R1a + 6 * SZ, R2a, a.Bm, Dfz, tid);
+        esync();
+      } else {
+        fw_x<T, N>(&sm.stage[buf][el][f0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+        esync();
+        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+        esync();
+        fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+        esync();
+      }
+    };
     // gradient of staged vector v at this thread's point after the in-place
     // sweeps: d/dx in R1, d/dy in R2, d/dz in the stage (read late: registers)
     auto grad_at = [&](int v, T* g) {
@@ -531,12 +601,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
       esync();
     } else {
       // ---- gradient of x at the qps
-      fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
-      esync();
-      fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
-      esync();
-      fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
-      esync();
+      fwd_sweeps(0);
 #pragma unroll
       for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
     }
@@ -558,12 +623,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
         grad_at(1, gk);
       } else {
         esync();
-        fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
-        esync();
-        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
-        esync();
-        fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
-        esync();
+        fwd_sweeps(3);
 #pragma unroll
         for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
       }
@@ -640,11 +700,23 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
 #pragma unroll
     for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];
     esync();
-    tr_z<T, N>(R1, R2, Btz, Dtz, q);
-    esync();
-    tr_y<T, N>(R2, R1, Bty, Dty, q);
-    esync();
-    if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
+    if constexpr (kDense) {
+      constexpr int SR = 9 * SZ, TH = EPB * N3;
+      T* const R1a = &sm.r1[0][0][0];
+      T* const R2a = &sm.r2[0][0][0];
+      tr_z<T, N, TH, EPB, SR>(R1a, R2a, Btz, Dtz, tid);
+      esync();
+      tr_y<T, N, TH, EPB, SR>(R2a, R1a, Bty, Dty, tid);
+      esync();
+      const int64_t e0 = e - el;
+      tr_x<T, N, TH, EPB, SR>(R1a, a.loc + e0 * 3 * N3, Btx, Dtx, tid, (int)(a.nel - e0 < EPB ? a.nel - e0 : EPB));
+    } else {
+      tr_z<T, N>(R1, R2, Btz, Dtz, q);
+      esync();
+      tr_y<T, N>(R2, R1, Bty, Dty, q);
+      esync();
+      if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
+    }
     esync();  // staging buffer `buf` and r1/r2 are reused next
   };
 
