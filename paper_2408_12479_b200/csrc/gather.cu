@@ -6,6 +6,12 @@
 // i parity); summing in exactly that order here reproduces the reference's
 // association of the scatter sums, with no atomics and no colour passes.
 // Dirichlet rows return the input (operator.hpp:617-620).
+#include <cstdlib>
+
+#ifndef EMF_NODE_NPT
+#define EMF_NODE_NPT 1
+#endif
+
 #include "gather.cuh"
 #include "internal.h"
 
@@ -72,11 +78,57 @@ __global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ 
   assemble_node<T, P>(loc, ghost_lo, ghost_hi, x, y, a, b, c, nx, ny, nz, faces, kpar, periodic_y);
 }
 
+// Same assembly with the nodes of a plane flattened (a + mx b): every lane
+// of a warp owns a node, where the (32, 8) tiling of an mx = 3n+1 row leaves
+// a quarter of the warps almost empty (the kernel is issue-bound).
+template <typename T, int P, bool GHOSTS>
+__global__ void __launch_bounds__(256) node_gather_flat_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
+                                                               const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
+                                                               int ny, int nz, int faces, int kpar, int c0,
+                                                               int periodic_y, FastDiv fd_mx) {
+  const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1);
+  const int c = blockIdx.y + c0;
+#pragma unroll
+  for (int r = 0; r < EMF_NODE_NPT; ++r) {
+    const int idx = (blockIdx.x * EMF_NODE_NPT + r) * 256 + threadIdx.x;
+    if (idx >= mx * my) return;
+    const int b = (int)fd_mx.div((uint32_t)idx);
+    const int a = idx - b * mx;
+    assemble_node<T, P, false, GHOSTS>(loc, ghost_lo, ghost_hi, x, y, a, b, c, nx, ny, nz, faces, kpar, periodic_y);
+  }
+}
+
 template <typename T>
 void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny, int nz,
                         int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s) {
   if (c1 < c0) return;
   const int mx = nx * p + 1, my = ny * p + (periodic_y ? 0 : 1);
+  static int flat = -1;
+  if (flat < 0) {
+    const char* e = std::getenv("EMFGPU_NODE_FLAT");
+    flat = e ? std::atoi(e) : 1;
+  }
+  if (flat) {
+    const dim3 gridf((unsigned)(((int64_t)mx * my + 256 * EMF_NODE_NPT - 1) / (256 * EMF_NODE_NPT)), c1 - c0 + 1);
+    const FastDiv fd = FastDiv::make((uint32_t)mx);
+    switch (p) {
+#define EMF_F(PP)                                                                                       \
+  case PP:                                                                                              \
+    if (ghost_lo || ghost_hi)                                                                           \
+      node_gather_flat_kernel<T, PP, true><<<gridf, 256, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, \
+                                                                 faces, kpar, c0, periodic_y, fd);       \
+    else                                                                                                \
+      node_gather_flat_kernel<T, PP, false><<<gridf, 256, 0, s>>>(loc, nullptr, nullptr, x, y, nx, ny, nz, \
+                                                                  faces, kpar, c0, periodic_y, fd);      \
+    break;
+      EMF_F(1)
+      EMF_F(2)
+      EMF_F(3)
+      EMF_F(4)
+#undef EMF_F
+    }
+    return;
+  }
   const dim3 grid((mx + 31) / 32, (my + 7) / 8, c1 - c0 + 1), block(32, 8);
   switch (p) {
 #define EMF_G(PP)                                                                                             \

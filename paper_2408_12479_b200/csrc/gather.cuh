@@ -49,7 +49,7 @@ __device__ __forceinline__ AxisSlots axis_slots(int a, int n, int par, bool lo_o
 // y(node) = sum of the node's element contributions in colour order (or x on
 // Dirichlet rows).  CG = true reads the element results through L2 only
 // (written by other CTAs of the same launch).
-template <typename T, int P, bool CG = false>
+template <typename T, int P, bool CG = false, bool GHOSTS = true>
 __device__ __forceinline__ void assemble_node(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
                                               const T* __restrict__ ghost_hi, const T* x, T* y, int a, int b, int c,
                                               int nx, int ny, int nz, int faces, int kpar, int periodic_y) {
@@ -65,7 +65,7 @@ __device__ __forceinline__ void assemble_node(const T* __restrict__ loc, const T
   auto ld = [](const T* p) { return CG ? __ldcg(p) : *p; };
   const AxisSlots sx = axis_slots<P>(a, nx, 0, false, false, false);
   const AxisSlots sy = axis_slots<P>(b, ny, 0, false, false, periodic_y != 0);
-  const AxisSlots sz = axis_slots<P>(c, nz, kpar, ghost_lo != nullptr, ghost_hi != nullptr, false);
+  const AxisSlots sz = axis_slots<P>(c, nz, kpar, GHOSTS && ghost_lo != nullptr, GHOSTS && ghost_hi != nullptr, false);
   T s0 = T(0), s1 = T(0), s2 = T(0);
 #pragma unroll
   for (int tk = 0; tk < 2; ++tk)
@@ -76,7 +76,7 @@ __device__ __forceinline__ void assemble_node(const T* __restrict__ loc, const T
         if (!(sz.v[tk] && sy.v[tj] && sx.v[ti])) continue;
         const int k = sz.e[tk];
         T v0, v1, v2;
-        if (k < 0 || k >= nz) {
+        if (GHOSTS && (k < 0 || k >= nz)) {
           const T* src = k < 0 ? ghost_lo : ghost_hi;
           const int64_t off = ((((int64_t)sy.e[tj] * nx + sx.e[ti]) * N2) + sy.l[tj] * N + sx.l[ti]) * 3;
           v0 = src[off];

@@ -29,4 +29,7 @@ for it in range(25):
     if it >= 5:
         ts.append(e0.elapsed_time(e1))
 ts.sort()
-print(os.environ.get("EMFGPU_GATHER_NB", "1"), "node phase median %.4f ms min %.4f ms" % (ts[len(ts) // 2], ts[0]))
+import hashlib  # noqa: E402
+print("EMFGPU_NODE_FLAT=%s y sha1 %s node phase median %.4f ms min %.4f ms" % (
+    os.environ.get("EMFGPU_NODE_FLAT", "1"), hashlib.sha1(y.cpu().numpy().tobytes()).hexdigest()[:12],
+    ts[len(ts) // 2], ts[0]))
