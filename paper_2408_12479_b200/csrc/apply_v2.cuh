@@ -724,39 +724,36 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   // the first element); later tickets come from a.tk[0], taken one unit ahead
   // of need by the worker's leader and published through shared memory, read
   // after the next compute's closing barrier.
-  __shared__ int64_t s_tk[EPB][2];
-  const int64_t nw = (int64_t)gridDim.x * (kPerElem ? EPB : 1);
-  const int64_t wid = kPerElem ? (int64_t)blockIdx.x * EPB + el : blockIdx.x;
+  __shared__ int s_tk[EPB][2];
+  const int nw = (int)gridDim.x * (kPerElem ? EPB : 1);
+  const int wid = kPerElem ? (int)blockIdx.x * EPB + el : (int)blockIdx.x;
   const bool leader = kPerElem ? q == 0 : tid == 0;
   const int slot = kPerElem ? el : 0;
-  int64_t cur = -1, nxt = wid, pend = wid + nw;  // cur: staged unit (-1: none)
+  const int nu = (int)nunits;
+  int cur = wid, nxt = wid + nw;
+  unsigned praw = 0;  // raw ticket of the unit after nxt, used one iteration later
   int buf = 0, par = 0;
   bool zero_cur = true, zero_next = true;
-  while (cur >= 0 || nxt < nunits) {
-    if (nxt < nunits)
+  if (cur < nu) zero_cur = prefetch(cur, 0);
+  if (leader && nxt < nu) praw = atomicAdd(a.tk, 1u);
+  while (cur < nu) {
+    if (nxt < nu)
       zero_next = prefetch(nxt, buf ^ 1);
     else
       cp_async_commit();
     if (leader) {
-      s_tk[slot][par] = pend;
-      if (pend < nunits) pend = 2 * nw + atomicAdd(a.tk, 1u);
+      const int pt = nxt < nu ? 2 * nw + (int)praw : nu;
+      s_tk[slot][par] = pt;
+      if (pt < nu) praw = atomicAdd(a.tk, 1u);
     }
-    if (cur >= 0) {
-      cp_async_wait<1>();
-      compute(cur, buf, zero_cur);  // ends with the worker's barrier
-    } else {
-      esync();
-    }
-    const int64_t nn = s_tk[slot][par];
+    cp_async_wait<1>();
+    compute(cur, buf, zero_cur);  // ends with the worker's barrier
+    const int nn = s_tk[slot][par];
     par ^= 1;
-    if (nxt < nunits) {
-      cur = nxt;
-      buf ^= 1;
-      zero_cur = zero_next;
-    } else {
-      cur = -1;
-    }
+    cur = nxt;
     nxt = nn;
+    buf ^= 1;
+    zero_cur = zero_next;
   }
   cp_async_wait<0>();
   // the last worker out rewinds the counter for the next launch on this slot
