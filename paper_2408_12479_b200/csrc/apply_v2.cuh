@@ -2,16 +2,19 @@
 //
 // Design (each point driven by an ncu profile, see DESIGN.md §3 and
 // profiles/r01_*):
-//  * persistent CTAs (one wave, occupancy-sized) loop over element groups and
-//    prefetch the NEXT group's x / u_k / affine geometry into a second shared
-//    staging buffer with cp.async while the current group computes;
+//  * persistent CTAs (one wave, occupancy-sized) take element groups from a
+//    ticket counter and prefetch the NEXT group's x / u_k / affine geometry
+//    into a second shared staging buffer with cp.async while the current
+//    group computes;
 //  * sum factorization by pencil workers: a worker owns one (component, line)
 //    pencil and performs the full 1D contraction in registers, so every
 //    shared load feeds n FMAs and the 1D tables are compile-time-indexed
 //    kernel parameters (constant-bank operands, no shared loads);
 //  * padded element arrays (Lay below) chosen by measurement so the pencil
 //    orientations and the per-point accesses avoid bank conflicts;
-//  * each element of a CTA synchronises on its own named barrier;
+//  * Q3: the two elements of a CTA share one pencil index space (dense
+//    mapping, CTA-wide barriers); EMF_V2_DENSE=0 builds the older variant
+//    where each element synchronises on its own named barrier;
 //  * element-local results are stored component-major, loc[(e*3 + c)*n^3 + m],
 //    as contiguous vector stores, for the node phase (gather.cu).
 // The quadrature-point algebra is in qp.cuh.
