@@ -457,6 +457,22 @@ constexpr int minb_v2() {
   return TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB;
 }
 
+#ifndef EMF_V2_FRESH
+#define EMF_V2_FRESH -1
+#endif
+// Re-derive the thread's point inside the loop bodies (EMF_V2_FRESH_POS)?
+template <typename T, int P, int MODEL, int STRAT, bool CART>
+constexpr bool fresh_pos_v2() {
+  if (EMF_V2_FRESH >= 0) return EMF_V2_FRESH != 0;  // experiments (tools/build_variant.sh)
+  // measured with tools/v2_sweep.sh (profiles/r01_e2e_findings.md): a win only
+  // for these fp64 iNH variants (32^3 Q3 curved none 0.1956 -> 0.1854 ms,
+  // scalar 0.2202 -> 0.1997; 24^3 Q4 curved tensor 0.1875 -> 0.1813), a loss
+  // of 1-25% elsewhere (more recomputation, different load scheduling)
+  if (sizeof(T) == 8 && MODEL == INH && P == 3 && (STRAT == S_NONE || STRAT == S_SCALAR)) return true;
+  if (sizeof(T) == 8 && MODEL == INH && P == 4 && STRAT == S_TENSOR) return true;
+  return false;
+}
+
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P, MODEL, STRAT, CART>()))
     apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
@@ -490,11 +506,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     else
       __syncthreads();
   };
-  const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);
-  const int qs = lat<N>(qi, qj, qk);  // padded slot of this thread's point
 
-  // per-thread tensor-product weight of this thread's point (operator.hpp:492)
-  const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
   // Work units handed out by a ticket counter (dynamic load balance; the
   // unit index is opaque to the compiler, which keeps it from building
   // strength-reduced address induction variables that spilled on Q4).  When
@@ -502,13 +514,26 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   // element is its own worker with its own ticket stream; otherwise a unit is
   // a group of EPB elements.
   constexpr bool kPerElem = N3 % 32 == 0 && EPB > 1 && !kDense;
+  constexpr bool kFreshPos = fresh_pos_v2<T, P, MODEL, STRAT, CART>();
   const int64_t nunits = kPerElem ? a.nel - a.e_begin : ngroups;
-  auto elem_of = [&](int64_t u) -> int64_t { return (kPerElem ? u : u * EPB + el) + a.e_begin; };
+  // The thread's point (el, q, qi, qj, qk, qs) is re-derived from a fresh
+  // %tid.x read inside the loop bodies instead of being kept live across the
+  // loop: at 128 registers ptxas spilled these loop invariants and reloaded
+  // them every iteration (long-scoreboard stalls on the reloads).
+#define EMF_V2_FRESH_POS                                                       \
+  int tid_f = tid;                                                            \
+  if constexpr (kFreshPos) asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_f)); \
+  const int el = tid_f / N3, q = tid_f % N3;                                  \
+  const int qi = q % N, qj = (q / N) % N, qk = q / (N * N);                   \
+  const int qs = lat<N>(qi, qj, qk);                                          \
+  (void)qs;
+  auto elem_of = [&](int64_t u, int el_) -> int64_t { return (kPerElem ? u : u * EPB + el_) + a.e_begin; };
   // issue the cp.async copies of unit u into staging buffer b; returns true
   // when this thread's staged x value must be zeroed (Dirichlet node or
   // padding element), decided here where the lattice position is at hand
   auto prefetch = [&](int64_t u, int b) -> bool {
-    const int64_t e = elem_of(u);
+    EMF_V2_FRESH_POS
+    const int64_t e = elem_of(u, el);
     bool zero = true;
     if (e < a.nel) {
       const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
@@ -528,7 +553,10 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
 
   // unit u, staged in buffer buf (its cp.async group complete)
   auto compute = [&](int64_t u, int buf, bool zero_me) {
-    const int64_t e = elem_of(u);
+    EMF_V2_FRESH_POS
+    // tensor-product weight of this thread's point (operator.hpp:492)
+    const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
+    const int64_t e = elem_of(u, el);
     const bool valid = e < a.nel;
     // Dirichlet columns are masked (operator.hpp:604-605); zero the stale
     // staging values of padding elements.

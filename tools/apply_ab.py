@@ -44,11 +44,15 @@ def main():
     cases = CASES
     if len(sys.argv) > 1:
         a = sys.argv[1:]
-        cases = [(int(a[0]), int(a[1]), a[2], a[3], int(a[4]), float(a[5]) if len(a) > 5 else 0.0)]
+        cases = [(int(a[0]), int(a[1]), a[2], a[3], int(a[4]), float(a[5]) if len(a) > 5 else 0.0,
+                  a[6] if len(a) > 6 else "material")]
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
-    for n, p, model, strat, prec, amp in cases:
+    for case in cases:
+        n, p, model, strat, prec, amp = case[:6]
+        dom = case[6] if len(case) > 6 else "material"
         lev = G.FeLevel(n, p=p, map_param=(amp,), dirichlet_faces=1)
-        op = G.ElasticOperator(lev, model, G.MaterialParams(mu=1.0, lam=10.0, kappa_b=1000.0), strat, prec)
+        op = G.ElasticOperator(lev, model, G.MaterialParams(mu=1.0, lam=10.0, kappa_b=1000.0), strat, prec,
+                               domain=dom)
         op.update_linearization(I.make_u0(n, n, n, p, noise=1e-3 * 8 / n))
         dt = torch.float64 if prec == 64 else torch.float32
         x = torch.tensor(I.make_v(lev.n_dofs), dtype=dt, device="cuda")
@@ -72,8 +76,8 @@ def main():
         torch.cuda.synchronize()
         same = same and torch.equal(y1, y2)
         tf, ts = timed(whole, flush), timed(split, flush)
-        print("n=%d p=%d %s %s fp%d amp=%g: bitwise %s  apply %.4f ms  split %.4f ms  (%.1f%%)  %.3e DoF/s" % (
-            n, p, model, strat, prec, amp, same, tf, ts, 100 * (ts - tf) / ts, lev.n_dofs / (tf * 1e-3)), flush=True)
+        print("n=%d p=%d %s %s %s fp%d amp=%g: bitwise %s  apply %.4f ms  split %.4f ms  (%.1f%%)  %.3e DoF/s" % (
+            n, p, model, dom[:3], strat, prec, amp, same, tf, ts, 100 * (ts - tf) / ts, lev.n_dofs / (tf * 1e-3)), flush=True)
 
 
 if __name__ == "__main__":
