@@ -698,3 +698,39 @@ def test_cfg3_full_size_properties(G):
         del op
     assert rel(kvs[("none", 64)], kvs[("tensor", 64)]) <= 1e-12
     assert rel(kvs[("tensor", 32)], kvs[("tensor", 64)]) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,prec,strat", [(3, 64, "none"), (3, 32, "none"), (4, 64, "tensor"), (2, 64, "scalar")])
+def test_ticket_scheduler_ranges_streams_repeats(G, p, prec, strat):
+    """The element kernels hand out work by per-launch ticket counters (a ring
+    of slots per operator, rewound by the last worker out).  Element-range
+    launches on two streams at once, many back-to-back launches and the
+    whole-lattice apply all give bitwise the same result."""
+    import torch
+    n = 6
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), strat, prec)
+    op.update_linearization(I.make_u0(n, n, n, p))
+    dt = torch.float64 if prec == 64 else torch.float32
+    x = torch.tensor(I.make_v(lev.n_dofs), dtype=dt, device="cuda")
+    y_ref = torch.empty_like(x)
+    op.apply_tangent_device(x, y_ref)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    mz = n * p + 1
+    for _ in range(3):
+        # disjoint element layer ranges on two streams concurrently
+        with torch.cuda.stream(s1):
+            op.apply_elements(x, 0, 2, stream=s1.cuda_stream)
+        with torch.cuda.stream(s2):
+            op.apply_elements(x, 2, n, stream=s2.cuda_stream)
+        torch.cuda.synchronize()
+        y = torch.empty_like(x)
+        op.apply_nodes(x, y, 0, mz - 1)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref)
+    for _ in range(300):  # more launches than ticket slots
+        op.apply_tangent_device(x, y)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)

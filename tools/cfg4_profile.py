@@ -1,0 +1,28 @@
+"""cfg4 (well-posed variant) PCG + fp32 hp-MG solve, for an ncu launch list
+(python tools/cfg4_profile.py [iterations]); prints the solve time."""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2408_12479_b200 import emfgpu as G  # noqa: E402
+from paper_2408_12479_b200 import workloads as W  # noqa: E402
+
+its_max = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+w = W.cfg4(wellposed=True)
+lev = w.level()
+op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
+op.update_linearization(np.zeros(lev.n_dofs))
+mg = G.MgHierarchy(lev, w.model, w.material(), degree=5, coarse_n=6, precision=32)
+mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+b = torch.tensor(W.rhs(w), device="cuda")
+x = torch.empty_like(b)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+its, hist = G.pcg_solve(op, mg, b, x, 1e-8, its_max)
+torch.cuda.synchronize()
+print("its", its, "solve_s %.4f" % (time.perf_counter() - t0), "levels", mg.levels())
