@@ -755,6 +755,9 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   // the first element); later tickets come from a.tk[0], taken one unit ahead
   // of need by the worker's leader and published through shared memory, read
   // after the next compute's closing barrier.
+  // let a programmatically dependent node phase launch now: its CTAs take
+  // the SM slots this persistent grid frees at its end and wait there
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ int s_tk[EPB][2];
   const int nw = (int)gridDim.x * (kPerElem ? EPB : 1);
   const int wid = kPerElem ? (int)blockIdx.x * EPB + el : (int)blockIdx.x;

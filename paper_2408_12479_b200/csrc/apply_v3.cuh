@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
   // 0.218 / 0.177 ms vs static 0.206 / 0.165 ms fp64 / fp32 at 32^3 Q3;
   // cNH fp32 and fp64 cachedF gain 2-2.5% from tickets).
   constexpr bool kTk = MODEL != FIBER;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // see apply_v2_kernel
   const int nw = (int)gridDim.x * kV3Warps;
   const int nu = (int)(a.nel - a.e_begin);
   int cur = (int)blockIdx.x * kV3Warps + warp, nxt = cur + nw;

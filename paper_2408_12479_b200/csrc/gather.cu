@@ -8,9 +8,6 @@
 // Dirichlet rows return the input (operator.hpp:617-620).
 #include <cstdlib>
 
-#ifndef EMF_NODE_NPT
-#define EMF_NODE_NPT 1
-#endif
 
 #include "gather.cuh"
 #include "internal.h"
@@ -87,15 +84,25 @@ __global__ void __launch_bounds__(256) node_gather_flat_kernel(const T* __restri
                                                                int ny, int nz, int faces, int kpar, int c0,
                                                                int periodic_y, FastDiv fd_mx) {
   const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1);
+  const int idx = blockIdx.x * 256 + threadIdx.x;
   const int c = blockIdx.y + c0;
-#pragma unroll
-  for (int r = 0; r < EMF_NODE_NPT; ++r) {
-    const int idx = (blockIdx.x * EMF_NODE_NPT + r) * 256 + threadIdx.x;
-    if (idx >= mx * my) return;
-    const int b = (int)fd_mx.div((uint32_t)idx);
-    const int a = idx - b * mx;
-    assemble_node<T, P, false, GHOSTS>(loc, ghost_lo, ghost_hi, x, y, a, b, c, nx, ny, nz, faces, kpar, periodic_y);
+  // launched as a programmatic dependent of the element kernel: wait for that
+  // grid and its memory here, after the launch itself overlapped its tail
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (idx >= mx * my) return;
+  const int b = (int)fd_mx.div((uint32_t)idx);
+  const int a = idx - b * mx;
+  assemble_node<T, P, false, GHOSTS>(loc, ghost_lo, ghost_hi, x, y, a, b, c, nx, ny, nz, faces, kpar, periodic_y);
+}
+
+// Programmatic dependent launch of the node phase (EMFGPU_PDL=0 disables).
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("EMFGPU_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
   }
+  return on != 0;
 }
 
 template <typename T>
@@ -109,17 +116,26 @@ void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, cons
     flat = e ? std::atoi(e) : 1;
   }
   if (flat) {
-    const dim3 gridf((unsigned)(((int64_t)mx * my + 256 * EMF_NODE_NPT - 1) / (256 * EMF_NODE_NPT)), c1 - c0 + 1);
+    const dim3 gridf((unsigned)(((int64_t)mx * my + 255) / 256), c1 - c0 + 1);
     const FastDiv fd = FastDiv::make((uint32_t)mx);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = gridf;
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     switch (p) {
-#define EMF_F(PP)                                                                                       \
-  case PP:                                                                                              \
-    if (ghost_lo || ghost_hi)                                                                           \
-      node_gather_flat_kernel<T, PP, true><<<gridf, 256, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, \
-                                                                 faces, kpar, c0, periodic_y, fd);       \
-    else                                                                                                \
-      node_gather_flat_kernel<T, PP, false><<<gridf, 256, 0, s>>>(loc, nullptr, nullptr, x, y, nx, ny, nz, \
-                                                                  faces, kpar, c0, periodic_y, fd);      \
+#define EMF_F(PP)                                                                                           \
+  case PP:                                                                                                  \
+    if (ghost_lo || ghost_hi)                                                                               \
+      cudaLaunchKernelEx(&cfg, node_gather_flat_kernel<T, PP, true>, loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, \
+                         faces, kpar, c0, periodic_y, fd);                                                  \
+    else                                                                                                    \
+      cudaLaunchKernelEx(&cfg, node_gather_flat_kernel<T, PP, false>, loc, (const T*)nullptr,              \
+                         (const T*)nullptr, x, y, nx, ny, nz, faces, kpar, c0, periodic_y, fd);             \
     break;
       EMF_F(1)
       EMF_F(2)
