@@ -345,6 +345,19 @@ __device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T*
   }
 }
 
+// Array of (Q0 | Q12, component c) in the transposed-sweep buffer.  fp64:
+// the three components of one kind are adjacent arrays (stride SIZE = 41
+// 16-byte units, odd), so the j-c-k x-pencils of a quarter-warp's LDS.128 in
+// tr_x fall on distinct bank groups (measured 2-way conflicts with the
+// (Q0, Q12) pair adjacent: component stride 82 units); fp32 keeps the pairs.
+#ifndef EMF_QV_SPLIT
+#define EMF_QV_SPLIT 1
+#endif
+template <typename T>
+__device__ __forceinline__ constexpr int qv_arr(int t, int c) {
+  return (sizeof(T) == 8 && EMF_QV_SPLIT) ? t * 3 + c : 2 * c + t;
+}
+
 // Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
           int SR = 0>
@@ -371,8 +384,8 @@ __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T*
         q0 += Bm[q * N + b] * u0[q];
         q12 += Dm[q * N + b] * u1[q] + Bm[q * N + b] * u2[q];
       }
-      qv[(2 * c + 0) * L::SIZE + lat<N>(i, b, k)] = q0;
-      qv[(2 * c + 1) * L::SIZE + lat<N>(i, b, k)] = q12;
+      qv[qv_arr<T>(0, c) * L::SIZE + lat<N>(i, b, k)] = q0;
+      qv[qv_arr<T>(1, c) * L::SIZE + lat<N>(i, b, k)] = q12;
     }
   }
 }
@@ -395,8 +408,8 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T
     T u0[N], u1[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      u0[q] = qv[(2 * c + 0) * L::SIZE + lat<N>(q, j, k)];
-      u1[q] = qv[(2 * c + 1) * L::SIZE + lat<N>(q, j, k)];
+      u0[q] = qv[qv_arr<T>(0, c) * L::SIZE + lat<N>(q, j, k)];
+      u1[q] = qv[qv_arr<T>(1, c) * L::SIZE + lat<N>(q, j, k)];
     }
     T o[N];
 #pragma unroll
