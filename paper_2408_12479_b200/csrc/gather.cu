@@ -14,67 +14,6 @@
 
 namespace emfgpu {
 
-// Candidate elements along one axis for lattice coordinate a (element size p,
-// n elements, lattice size m), sorted even-index first. Local node index in
-// the element along that axis is returned in loc[].  lo/hi ghost layers are
-// allowed along z (index -1 and n).
-__device__ __forceinline__ int axis_candidates(int a, int p, int n, int gpar, bool ghosts, int* el, int* loc,
-                                               bool periodic = false) {
-  const int e1 = a / p;
-  if (periodic && a == 0) {  // seam of a periodic lattice: elements n-1 (local p) and 0 (local 0)
-    const bool odd_last = ((n - 1) & 1) != 0;
-    el[0] = odd_last ? 0 : n - 1;
-    loc[0] = odd_last ? 0 : p;
-    el[1] = odd_last ? n - 1 : 0;
-    loc[1] = odd_last ? p : 0;
-    return 2;
-  }
-  if (a % p == 0) {
-    const bool has_lo = a > 0 || ghosts;
-    const bool has_hi = a < n * p || ghosts;
-    int cnt = 0;
-    int c_el[2], c_loc[2];
-    if (has_lo) {
-      c_el[cnt] = e1 - 1;
-      c_loc[cnt] = p;
-      ++cnt;
-    }
-    if (has_hi) {
-      c_el[cnt] = e1;
-      c_loc[cnt] = 0;
-      ++cnt;
-    }
-    if (cnt == 2 && (((c_el[0] + gpar) & 1) != 0)) {  // odd first -> swap so even (global) goes first
-      el[0] = c_el[1];
-      loc[0] = c_loc[1];
-      el[1] = c_el[0];
-      loc[1] = c_loc[0];
-    } else {
-      for (int t = 0; t < cnt; ++t) {
-        el[t] = c_el[t];
-        loc[t] = c_loc[t];
-      }
-    }
-    return cnt;
-  }
-  el[0] = e1;
-  loc[0] = a - e1 * p;
-  return 1;
-}
-
-template <typename T, int P>
-__global__ void __launch_bounds__(256) node_gather_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
-                                                          const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
-                                                          int ny, int nz, int faces, int kpar, int c0,
-                                                          int periodic_y) {
-  const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1);
-  const int a = blockIdx.x * 32 + threadIdx.x;
-  const int b = blockIdx.y * 8 + threadIdx.y;
-  const int c = blockIdx.z + c0;
-  if (a >= mx || b >= my) return;
-  assemble_node<T, P>(loc, ghost_lo, ghost_hi, x, y, a, b, c, nx, ny, nz, faces, kpar, periodic_y);
-}
-
 // Same assembly with the nodes of a plane flattened (a + mx b): every lane
 // of a warp owns a node, where the (32, 8) tiling of an mx = 3n+1 row leaves
 // a quarter of the warps almost empty (the kernel is issue-bound).
@@ -110,12 +49,7 @@ void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, cons
                         int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s) {
   if (c1 < c0) return;
   const int mx = nx * p + 1, my = ny * p + (periodic_y ? 0 : 1);
-  static int flat = -1;
-  if (flat < 0) {
-    const char* e = std::getenv("EMFGPU_NODE_FLAT");
-    flat = e ? std::atoi(e) : 1;
-  }
-  if (flat) {
+  {
     const dim3 gridf((unsigned)(((int64_t)mx * my + 255) / 256), c1 - c0 + 1);
     const FastDiv fd = FastDiv::make((uint32_t)mx);
     cudaLaunchConfig_t cfg = {};
@@ -143,19 +77,6 @@ void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, cons
       EMF_F(4)
 #undef EMF_F
     }
-    return;
-  }
-  const dim3 grid((mx + 31) / 32, (my + 7) / 8, c1 - c0 + 1), block(32, 8);
-  switch (p) {
-#define EMF_G(PP)                                                                                             \
-  case PP:                                                                                                    \
-    node_gather_kernel<T, PP><<<grid, block, 0, s>>>(loc, ghost_lo, ghost_hi, x, y, nx, ny, nz, faces, kpar, c0, periodic_y); \
-    break;
-    EMF_G(1)
-    EMF_G(2)
-    EMF_G(3)
-    EMF_G(4)
-#undef EMF_G
   }
 }
 
