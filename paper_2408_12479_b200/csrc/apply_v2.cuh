@@ -70,16 +70,24 @@ __device__ __forceinline__ ElemPos elem_pos_fast(int64_t e64, const A& a, int i,
   return p;
 }
 
-template <int P>
+// Elements per CTA and CTAs per SM (fp32; fp64 see minb_v2) by degree and
+// element size in bytes.  EMF_Q4F_EPB=2 runs fp32 Q4 with 2 elements per CTA
+// on the dense pencil mapping (measured 1-4% slower than 1 element per CTA).
+#ifndef EMF_Q4F_EPB
+#define EMF_Q4F_EPB 1
+#endif
+template <int P, int ES = 8>
 struct TileV2;
+template <int ES>
+struct TileV2<1, ES> { static constexpr int EPB = 16, MINB = 4; };
+template <int ES>
+struct TileV2<2, ES> { static constexpr int EPB = 4, MINB = 4; };
+template <int ES>
+struct TileV2<3, ES> { static constexpr int EPB = 2, MINB = 4; };
 template <>
-struct TileV2<1> { static constexpr int EPB = 16, MINB = 4; };
+struct TileV2<4, 8> { static constexpr int EPB = 1, MINB = 4; };
 template <>
-struct TileV2<2> { static constexpr int EPB = 4, MINB = 4; };
-template <>
-struct TileV2<3> { static constexpr int EPB = 2, MINB = 4; };
-template <>
-struct TileV2<4> { static constexpr int EPB = 1, MINB = 4; };
+struct TileV2<4, 4> { static constexpr int EPB = EMF_Q4F_EPB, MINB = 4 / EMF_Q4F_EPB; };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -428,7 +436,7 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T
 // ---- the kernel -------------------------------------------------------------------
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 struct ApplyV2Smem {
-  static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
+  static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P, sizeof(T)>::EPB;
   static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR);
   static constexpr int NST = kUk ? 6 : 3;  // staged fields: x (3) [+ u_k (3)]
   static constexpr int SZ = Lay<N, sizeof(T)>::SIZE;
@@ -456,7 +464,7 @@ struct ApplyV2Smem {
 #endif
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 constexpr int minb_v2() {
-  if (sizeof(T) == 4) return TileV2<P>::MINB;
+  if (sizeof(T) == 4) return TileV2<P, 4>::MINB;
   if (EMF_MINB_V2D_FORCE) return EMF_MINB_V2D_FORCE;  // experiments (tools/build_variant.sh)
   if (P == 3 && MODEL == CNH && ((STRAT == S_NONE && CART) || STRAT == S_SP_NONE || STRAT == S_SP_TENSOR)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
@@ -487,7 +495,7 @@ constexpr bool fresh_pos_v2() {
 }
 
 template <typename T, int P, int MODEL, int STRAT, bool CART>
-__global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P, MODEL, STRAT, CART>()))
+__global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * (P + 1), (minb_v2<T, P, MODEL, STRAT, CART>()))
     apply_v2_kernel(const KArgs<T> a, int64_t ngroups) {
   using SM = ApplyV2Smem<T, P, MODEL, STRAT, CART>;
   // CART: affine elements with a diagonal J0^-1 (axis-aligned boxes): the
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   const T* const Dty = a.Dm;
   const T* const Btz = a.Bm;
   const T* const Dtz = a.Dm;
-  constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P>::EPB;
+  constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P, sizeof(T)>::EPB;
   constexpr bool kUk = SM::kUk;
   constexpr int SZ = Lay<N, sizeof(T)>::SIZE;
   __shared__ __align__(16) SM sm;
@@ -512,7 +520,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
   // Q3 (two 64-thread elements per CTA): dense pencil mapping over the CTA
   // (see fw_x) with CTA-wide barriers; measured against per-element named
   // barriers with 48 of 64 threads per element sweeping
-  constexpr bool kDense = EMF_V2_DENSE && N3 == 64 && EPB == 2;
+  constexpr bool kDense = EMF_V2_DENSE && (N3 == 64 || N3 == 125) && EPB == 2;
   auto esync = [&]() {
     if constexpr (N3 % 32 == 0 && EPB > 1 && !kDense)
       asm volatile("bar.sync %0, %1;\n" ::"r"(el + 1), "n"(N3) : "memory");
@@ -634,7 +642,7 @@ __global__ void __launch_bounds__(TileV2<P>::EPB*(P + 1) * (P + 1) * (P + 1), (m
     // fp32: x and u_k swept together (full lanes); fp64 keeps one vector per
     // sweep, whose shorter live ranges fit its 128/168-register budget
     // (measured: fused sweeps cost fp64 none 0.165 -> 0.175 ms, gave fp32 -3%)
-    constexpr bool kFused = kUk && sizeof(T) == 4;
+    constexpr bool kFused = kUk && sizeof(T) == 4 && !kDense;
     if constexpr (kFused) {
       // ---- gradients of x and u_k at the qps, both vectors per sweep, in place
       fwc_x<T, N, 2, N3>(S, R2, a.Bm, Dfx, q);

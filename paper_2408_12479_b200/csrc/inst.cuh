@@ -9,11 +9,10 @@
 
 namespace emfgpu {
 
-static_assert(TileV2<EMF_P>::EPB == kV2Epb[EMF_P], "internal.h kV2Epb out of date");
 
 template <int MODEL, int STRAT, bool CART>
 static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_t s) {
-  constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P>::EPB, THREADS = EPB * N * N * N;
+  constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P, sizeof(EMF_T)>::EPB, THREADS = EPB * N * N * N;
   const int64_t cnt = e1 - e0;
   if (cnt <= 0) return;
   // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):

@@ -13,8 +13,6 @@ namespace emfgpu {
 
 constexpr int kMaxP = 4;
 
-// elements per CTA of the v2 element kernel by degree (TileV2, apply_v2.cuh)
-constexpr int kV2Epb[5] = {0, 16, 4, 2, 1};
 
 // Per-(T,P) launchers, defined in inst_<t><p>.cu.
 template <typename T, int P>
