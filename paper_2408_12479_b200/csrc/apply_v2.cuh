@@ -450,6 +450,9 @@ struct ApplyV2Smem {
 // except for the variants that ptxas fits into 128 registers without spills,
 // which measured faster at 4 CTAs/SM (cfg1: headline fp64 none 0.1676 ->
 // 0.1654 ms, spatial tensor 0.1205 -> 0.1148 ms); fp32 always 4.
+#ifndef EMF_V2_PAIRSTAGE
+#define EMF_V2_PAIRSTAGE 1
+#endif
 #ifndef EMF_V2_DENSE
 #define EMF_V2_DENSE 1
 #endif
@@ -552,19 +555,45 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   // issue the cp.async copies of unit u into staging buffer b; returns true
   // when this thread's staged x value must be zeroed (Dirichlet node or
   // padding element), decided here where the lattice position is at hand
+  // The node a thread stages (sel, si, sj, sk): its own point, or with the
+  // dense Q3 mapping a row-paired one -- lanes 4m..4m+3 take a row of element
+  // 0 and the next 4 lanes the same row of element 1 (its x neighbour when
+  // nx is even), so a warp's 8-byte copies cover 4 lattice rows instead of 8
+  // (the copies' shared-memory wavefronts follow the global lines touched).
+  auto stage_pos = [&](int tid_, int& sel, int& si, int& sj, int& sk) {
+    if constexpr (kDense && N3 == 64 && EMF_V2_PAIRSTAGE) {
+      const int lane = tid_ & 31, row = (lane >> 3) + 4 * (tid_ >> 5);
+      sel = (lane >> 2) & 1;
+      si = lane & 3;
+      sj = row & 3;
+      sk = row >> 2;
+    } else {
+      sel = tid_ / N3;
+      const int q_ = tid_ % N3;
+      si = q_ % N;
+      sj = (q_ / N) % N;
+      sk = q_ / (N * N);
+    }
+  };
   auto prefetch = [&](int64_t u, int b) -> bool {
     EMF_V2_FRESH_POS
-    const int64_t e = elem_of(u, el);
+    int sel, si, sj, sk;
+    stage_pos(tid_f, sel, si, sj, sk);
+    const int sqs = lat<N>(si, sj, sk);
+    const int64_t es = elem_of(u, sel);
     bool zero = true;
-    if (e < a.nel) {
-      const ElemPos ep = elem_pos_fast<P>(e, a, qi, qj, qk);
+    if (es < a.nel) {
+      const ElemPos ep = elem_pos_fast<P>(es, a, si, sj, sk);
       zero = node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][c][qs], a.x + 3 * ep.node + c);
+      for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][sel][c][sqs], a.x + 3 * ep.node + c);
       if constexpr (kUk) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][el][3 + c][qs], a.uk + 3 * ep.node + c);
+        for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][sel][3 + c][sqs], a.uk + 3 * ep.node + c);
       }
+    }
+    const int64_t e = elem_of(u, el);
+    if (e < a.nel) {
       if (a.affine && (!is_spatial(STRAT) || kUk))
         for (int f = q; f < 10; f += N3) cp_async_T(&sm.geo[b][el][f], a.geo + f * a.geo_stride + e);
     }
@@ -582,8 +611,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // Dirichlet columns are masked (operator.hpp:604-605); zero the stale
     // staging values of padding elements.
     if (zero_me) {
+      int sel, si, sj, sk;
+      stage_pos(tid_f, sel, si, sj, sk);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) sm.stage[buf][el][c][qs] = T(0);
+      for (int c = 0; c < 3; ++c) sm.stage[buf][sel][c][lat<N>(si, sj, sk)] = T(0);
     }
     // per-qp geometry / cache loads are issued before the sweeps
     const int64_t qidx = (valid ? e : a.e_begin) * N3 + q;
