@@ -7,6 +7,13 @@
 #include "apply_v3.cuh"
 #include "internal.h"
 
+#ifndef EMF_F32V2
+#define EMF_F32V2 1
+#endif
+#ifndef EMF_V3_FP32
+#define EMF_V3_FP32 1
+#endif
+
 namespace emfgpu {
 
 
@@ -18,8 +25,15 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):
   // warp-per-element (v3) for fp32 and for the fp64 strategies without u_k
   // sweeps; 2 elements per CTA with named barriers (v2) for fp64 none/scalar.
+  // fp32 Q3 with u_k sweeps on curved meshes or in the spatial domain: the
+  // dense v2 kernel measured faster than v3 (32^3 curved iNH none 0.1301 ->
+  // 0.1219 ms, curved cNH 0.1239 -> 0.1198, spatial none 0.1179 -> 0.1157);
+  // axis-aligned material and Q2 stay on v3 (0.1116 vs 0.1138 ms).
+  constexpr bool kF32V2 = EMF_F32V2 && sizeof(EMF_T) == 4 && EMF_P == 3 &&
+                          (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR) &&
+                          (!CART || is_spatial(STRAT));
   constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) &&
-                       (sizeof(EMF_T) == 4 || STRAT == S_CACHEDF || STRAT == S_TENSOR);
+                       ((sizeof(EMF_T) == 4 && EMF_V3_FP32 && !kF32V2) || STRAT == S_CACHEDF || STRAT == S_TENSOR);
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
     constexpr size_t smem = sizeof(ApplyV3Warp<EMF_T, EMF_P, MODEL, STRAT>) * kV3Warps;
