@@ -7,11 +7,8 @@
 #include "apply_v3.cuh"
 #include "internal.h"
 
-#ifndef EMF_F32V2
-#define EMF_F32V2 1
-#endif
-#ifndef EMF_V3_FP32
-#define EMF_V3_FP32 1
+#ifndef EMF_V3_ENABLE
+#define EMF_V3_ENABLE 1
 #endif
 
 namespace emfgpu {
@@ -22,18 +19,16 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   constexpr int N = EMF_P + 1, EPB = TileV2<EMF_P, sizeof(EMF_T)>::EPB, THREADS = EPB * N * N * N;
   const int64_t cnt = e1 - e0;
   if (cnt <= 0) return;
-  // Kernel choice measured on B200 at cfg1 (profiles/r01_bench_v3_*.json):
-  // warp-per-element (v3) for fp32 and for the fp64 strategies without u_k
-  // sweeps; 2 elements per CTA with named barriers (v2) for fp64 none/scalar.
-  // fp32 Q3 with u_k sweeps on curved meshes or in the spatial domain: the
-  // dense v2 kernel measured faster than v3 (32^3 curved iNH none 0.1301 ->
-  // 0.1219 ms, curved cNH 0.1239 -> 0.1198, spatial none 0.1179 -> 0.1157);
-  // axis-aligned material and Q2 stay on v3 (0.1116 vs 0.1138 ms).
-  constexpr bool kF32V2 = EMF_F32V2 && sizeof(EMF_T) == 4 && EMF_P == 3 &&
-                          (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR) &&
-                          (!CART || is_spatial(STRAT));
-  constexpr bool kV3 = (EMF_P == 2 || EMF_P == 3) &&
-                       ((sizeof(EMF_T) == 4 && EMF_V3_FP32 && !kF32V2) || STRAT == S_CACHEDF || STRAT == S_TENSOR);
+  // Kernel choice measured on B200 (tools/apply_ab.py; profiles/r01_e2e_findings.md):
+  // the warp-per-element v3 for Q2 (fp32, and fp64 tensor / cachedF) and for
+  // fp32 Q3 none / scalar on axis-aligned meshes in the material domain; the
+  // dense v2 everywhere else (after the ticket loop and the dense Q3 mapping it
+  // beat v3 for Q3 tensor / cachedF in both precisions: fp32 curved iNH tensor
+  // 0.169 -> 0.114 ms, fibre 0.169 -> 0.120; fp64 iNH tensor 0.214 -> 0.163,
+  // cNH tensor 0.1445 -> 0.1384, cachedF 0.159 -> 0.151).
+  constexpr bool kTC = STRAT == S_CACHEDF || STRAT == S_TENSOR;
+  constexpr bool kF32V3 = sizeof(EMF_T) == 4 && CART && !is_spatial(STRAT) && (STRAT == S_NONE || STRAT == S_SCALAR);
+  constexpr bool kV3 = EMF_V3_ENABLE && (EMF_P == 2 ? (sizeof(EMF_T) == 4 || kTC) : (EMF_P == 3 && kF32V3));
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
     constexpr size_t smem = sizeof(ApplyV3Warp<EMF_T, EMF_P, MODEL, STRAT>) * kV3Warps;
