@@ -1286,6 +1286,14 @@ struct emfgpu_mg {
   double* d_A = nullptr;
   double* d_M = nullptr;
   int* d_sing = nullptr;
+  // V-cycle captured as a CUDA graph (dense coarse solve: no host syncs
+  // inside), keyed on the (r, z) buffers; dropped on relinearization, whose
+  // eigenvalue bounds are baked into the Chebyshev launches
+  cudaGraphExec_t vc_exec = nullptr;
+  const double* vc_r = nullptr;
+  double* vc_z = nullptr;
+  cudaStream_t vc_stream = nullptr;
+  cudaEvent_t vc_ev[2] = {nullptr, nullptr};
   std::string last_error;
 };
 
@@ -1486,6 +1494,10 @@ void emfgpu_mg_destroy(emfgpu_mg* m) {
   cudaFree(m->d_sing);
   cudaFree(m->dbuf);
   if (m->hdot) cudaFreeHost(m->hdot);
+  if (m->vc_exec) cudaGraphExecDestroy(m->vc_exec);
+  if (m->vc_stream) cudaStreamDestroy(m->vc_stream);
+  for (auto ev : m->vc_ev)
+    if (ev) cudaEventDestroy(ev);
   delete m;
 }
 
@@ -1596,11 +1608,19 @@ emfgpu_status emfgpu_mg_level_info(const emfgpu_mg* m, int l, int* nx, int* ny, 
 
 const char* emfgpu_mg_last_error(const emfgpu_mg* m) { return m ? m->last_error.c_str() : ""; }
 
+static void mg_drop_graph(emfgpu_mg* m) {
+  if (m->vc_exec) cudaGraphExecDestroy(m->vc_exec);
+  m->vc_exec = nullptr;
+  m->vc_r = nullptr;
+  m->vc_z = nullptr;
+}
+
 emfgpu_status emfgpu_mg_update_linearization(emfgpu_mg* m, const double* d_u_fine, void* stream) {
   if (!m || !d_u_fine) return EMFGPU_ERR_INVALID;
   return guarded(&m->last_error, [&] {
     CK(cudaSetDevice(m->fine->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    mg_drop_graph(m);
     if (m->cfg.precision == 64)
       mg_linearize<double>(m, d_u_fine, s);
     else
@@ -1608,15 +1628,67 @@ emfgpu_status emfgpu_mg_update_linearization(emfgpu_mg* m, const double* d_u_fin
   });
 }
 
+static bool mg_graphs_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("EMFGPU_MG_GRAPH");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on != 0;
+}
+
+// One V-cycle z = M^-1 r.  With the dense coarse solve the V-cycle has no
+// host synchronisation, so from the second call with the same buffers on it
+// is one graph launch (~100 kernels per cycle otherwise, most of them tiny on
+// the coarse levels, where the launch rate bounded the solve).
+static void mg_precondition_any(emfgpu_mg* m, const double* r, double* z, cudaStream_t s) {
+  auto run = [&](cudaStream_t st) {
+    if (m->cfg.precision == 64)
+      mg_precondition<double>(m, r, z, st);
+    else
+      mg_precondition<float>(m, r, z, st);
+  };
+  if (!m->dense || !mg_graphs_enabled()) {
+    run(s);
+    return;
+  }
+  if (!m->vc_stream) {
+    CK(cudaStreamCreateWithFlags(&m->vc_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&m->vc_ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&m->vc_ev[1], cudaEventDisableTiming));
+  }
+  const bool same = m->vc_r == r && m->vc_z == z;
+  if (same && !m->vc_exec) {
+    CK(cudaStreamBeginCapture(m->vc_stream, cudaStreamCaptureModeThreadLocal));
+    run(m->vc_stream);
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamEndCapture(m->vc_stream, &g));
+    const cudaError_t e = cudaGraphInstantiate(&m->vc_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      m->vc_exec = nullptr;
+      throw ApiError(EMFGPU_ERR_CUDA, std::string("V-cycle graph instantiate: ") + cudaGetErrorString(e));
+    }
+  }
+  if (same && m->vc_exec) {
+    CK(cudaEventRecord(m->vc_ev[0], s));
+    CK(cudaStreamWaitEvent(m->vc_stream, m->vc_ev[0], 0));
+    CK(cudaGraphLaunch(m->vc_exec, m->vc_stream));
+    CK(cudaEventRecord(m->vc_ev[1], m->vc_stream));
+    CK(cudaStreamWaitEvent(s, m->vc_ev[1], 0));
+    return;
+  }
+  mg_drop_graph(m);
+  m->vc_r = r;
+  m->vc_z = z;
+  run(s);
+}
+
 emfgpu_status emfgpu_mg_precondition(emfgpu_mg* m, const double* d_r, double* d_z, void* stream) {
   if (!m || !d_r || !d_z) return EMFGPU_ERR_INVALID;
   return guarded(&m->last_error, [&] {
     if (!m->ops[0]->linearized) throw ApiError(EMFGPU_ERR_STALE, "mg: update_linearization has not run");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (m->cfg.precision == 64)
-      mg_precondition<double>(m, d_r, d_z, s);
-    else
-      mg_precondition<float>(m, d_r, d_z, s);
+    mg_precondition_any(m, d_r, d_z, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1644,10 +1716,7 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     };
     auto prec = [&](const double* rr, double* zz) {
       if (mg) {
-        if (mg->cfg.precision == 64)
-          mg_precondition<double>(mg, rr, zz, s);
-        else
-          mg_precondition<float>(mg, rr, zz, s);
+        mg_precondition_any(mg, rr, zz, s);
       } else {
         CK(cudaMemcpyAsync(zz, rr, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
       }
@@ -1925,10 +1994,7 @@ struct Krylov {
   void apply(const double* x, double* y) { op_apply_T<double>(op, x, y, s); }
   void prec(const double* r, double* z) {
     if (mg) {
-      if (mg->cfg.precision == 64)
-        mg_precondition<double>(mg, r, z, s);
-      else
-        mg_precondition<float>(mg, r, z, s);
+      mg_precondition_any(mg, r, z, s);
     } else {
       CK(cudaMemcpyAsync(z, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     }
