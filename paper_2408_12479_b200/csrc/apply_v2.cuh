@@ -21,6 +21,10 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef EMF_MINB_F32Q4
+#define EMF_MINB_F32Q4 0  // fp32 Q4 CTAs/SM override (experiments)
+#endif
+
 namespace emfgpu {
 
 // Per-element array layout: a + SY*b + SZ*c with padded strides chosen (by
@@ -467,7 +471,7 @@ struct ApplyV2Smem {
 #endif
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 constexpr int minb_v2() {
-  if (sizeof(T) == 4) return TileV2<P, 4>::MINB;
+  if (sizeof(T) == 4) return (P == 4 && EMF_MINB_F32Q4) ? EMF_MINB_F32Q4 : TileV2<P, 4>::MINB;
   if (EMF_MINB_V2D_FORCE) return EMF_MINB_V2D_FORCE;  // experiments (tools/build_variant.sh)
   if (P == 3 && MODEL == CNH && ((STRAT == S_NONE && CART) || STRAT == S_SP_NONE || STRAT == S_SP_TENSOR)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
