@@ -290,17 +290,24 @@ void apply_elements(emfgpu_op* op, const void* x, int k0, int k1, cudaStream_t s
   CK(cudaGetLastError());
 }
 
+// set while capturing a conditional-graph body (no programmatic edges there)
+static thread_local bool tl_no_pdl = false;
+
+// pdl: launch as a programmatic dependent of the preceding element kernel
+// (off in the copy-overlapped host pipeline, where it measured 1% slower)
 void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const void* glo, const void* ghi, int kpar,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool pdl = true) {
   const emfgpu_level* L = op->L;
   if (op->precision == 64)
     launch_node_gather<double>(static_cast<const double*>(op->d_loc), static_cast<const double*>(glo),
                                static_cast<const double*>(ghi), static_cast<const double*>(x),
-                               static_cast<double*>(y), L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s);
+                               static_cast<double*>(y), L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s,
+                               pdl && !tl_no_pdl);
   else
     launch_node_gather<float>(static_cast<const float*>(op->d_loc), static_cast<const float*>(glo),
                               static_cast<const float*>(ghi), static_cast<const float*>(x), static_cast<float*>(y),
-                              L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s);
+                              L->nx, L->ny, L->nz, L->p, L->faces, kpar, c0, c1, L->periodic_y, s,
+                              pdl && !tl_no_pdl);
   CK(cudaGetLastError());
 }
 
@@ -758,7 +765,7 @@ static void apply_host_pipelined(emfgpu_op* op, const void* x, void* y) {
     const int c0 = k0 * L->p, c1 = (k1 == L->nz) ? L->mz - 1 : k1 * L->p - 1;
     CK(cudaStreamWaitEvent(op->stream, op->ev_h2d[i], 0));
     apply_elements(op, op->d_x, k0, k1, op->stream);
-    apply_nodes(op, op->d_x, op->d_y, c0, c1, nullptr, nullptr, 0, op->stream);
+    apply_nodes(op, op->d_x, op->d_y, c0, c1, nullptr, nullptr, 0, op->stream, false);
     CK(cudaEventRecord(op->ev_comp[i], op->stream));
     CK(cudaStreamWaitEvent(op->s_d2h, op->ev_comp[i], 0));
     CK(cudaMemcpyAsync(hy + c0 * plane, dy + c0 * plane, (c1 - c0 + 1) * plane, cudaMemcpyDeviceToHost,
@@ -1694,6 +1701,74 @@ emfgpu_status emfgpu_mg_precondition(emfgpu_mg* m, const double* d_r, double* d_
 
 // Preconditioned CG in double on device vectors (x starts at 0).  Stops when
 // ||r|| <= rtol ||b||.  history (host, maxit+1, optional) gets ||r_k||/||b||.
+static bool pcg_graph_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("EMFGPU_PCG_GRAPH");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on != 0;
+}
+
+// Run body(stream, h, 1) as the body of a conditional WHILE graph node, on s
+// (captured with the node phase's programmatic launches disabled: a
+// conditional body only takes kernel, memset, memcpy, child-graph and
+// conditional nodes).  Returns false, having enqueued nothing, when the graph
+// cannot be built; errors of the launch itself throw.
+template <typename F>
+static bool pcg_run_graph(cudaStream_t s, F&& body) {
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+  cudaGraphConditionalHandle h{};
+  cudaGraphNode_t node{};
+  cudaGraphNodeParams cp = {};
+  if (ok) ok = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  if (ok) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+  }
+  if (ok) {
+    cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+    ok = cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+         cudaSuccess;
+    if (ok) {
+      tl_no_pdl = true;
+      bool thrown = false;
+      try {
+        body(cs, h, 1);
+      } catch (...) {
+        thrown = true;
+      }
+      tl_no_pdl = false;
+      cudaGraph_t out = nullptr;
+      ok = cudaStreamEndCapture(cs, &out) == cudaSuccess && !thrown;
+    }
+  }
+  if (ok) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+    return false;
+  }
+  CK(cudaGraphLaunch(ge, s));
+  CK(cudaStreamSynchronize(s));
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return true;
+}
+
 emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double rtol, int maxit,
                                int* iterations, double* history, void* stream) {
   if (!op || !d_b || !d_x) return EMFGPU_ERR_INVALID;
@@ -1703,58 +1778,95 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     CK(cudaSetDevice(op->L->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t n = op->L->ndofs;
-    double *r, *z, *p, *ap, *dbuf, *hdot;
+    // Device-resident PCG: the scalars stay on the device (sc = {rz, pAp, rr,
+    // rz_new, ||b||}, ic = {iterations, done}) and, from the second iteration
+    // on, the whole loop is one CUDA graph with a conditional WHILE node whose
+    // condition the convergence-check kernel sets -- no host round trip per
+    // iteration.  Same arithmetic and order as the host loop it replaced.
+    double *r, *z, *p, *ap, *dbuf, *sc, *dhist;
+    int* ic;
     CK(cudaMalloc(&r, sizeof(double) * n));
     CK(cudaMalloc(&z, sizeof(double) * n));
     CK(cudaMalloc(&p, sizeof(double) * n));
     CK(cudaMalloc(&ap, sizeof(double) * n));
     CK(cudaMalloc(&dbuf, sizeof(double) * (dot_partial_count() + 1)));
-    CK(cudaMallocHost(&hdot, sizeof(double)));
-    auto dot = [&](const double* a, const double* b) {
-      launch_dot<double>(a, b, n, dbuf + 1, dbuf, s);
-      return mg_dot_sync(dbuf, hdot, s);
-    };
-    auto prec = [&](const double* rr, double* zz) {
-      if (mg) {
-        mg_precondition_any(mg, rr, zz, s);
-      } else {
-        CK(cudaMemcpyAsync(zz, rr, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMalloc(&sc, sizeof(double) * 8));
+    CK(cudaMalloc(&ic, sizeof(int) * 2));
+    CK(cudaMalloc(&dhist, sizeof(double) * (maxit + 1)));
+    struct Cleanup {
+      std::vector<void*> v;
+      ~Cleanup() {
+        for (void* q : v) cudaFree(q);
       }
+    } cleanup{{r, z, p, ap, dbuf, sc, ic, dhist}};
+    auto dot_to = [&](const double* a, const double* b, double* out, cudaStream_t st) {
+      launch_dot<double>(a, b, n, dbuf, out, st);
+    };
+    auto prec = [&](const double* rr, double* zz, cudaStream_t st) {
+      if (mg) {
+        if (mg->cfg.precision == 64)
+          mg_precondition<double>(mg, rr, zz, st);
+        else
+          mg_precondition<float>(mg, rr, zz, st);
+      } else {
+        CK(cudaMemcpyAsync(zz, rr, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      }
+    };
+    // apply, dots, x/r update, check: the tail of every iteration
+    auto tail = [&](cudaStream_t st, cudaGraphConditionalHandle h, int use_h) {
+      op_apply_T<double>(op, p, ap, st);
+      dot_to(p, ap, sc + 1, st);
+      launch_pcg_xr(d_x, r, p, ap, sc, n, st);
+      dot_to(r, r, sc + 2, st);
+      launch_pcg_check(sc, ic, dhist, rtol, maxit, h, use_h, st);
     };
     CK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, s));
+    CK(cudaMemsetAsync(ic, 0, sizeof(int) * 2, s));
     CK(cudaMemcpyAsync(r, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    const double bnorm = std::sqrt(dot(d_b, d_b));
-    if (history) history[0] = 1.0;
+    dot_to(d_b, d_b, sc + 4, s);
+    launch_pcg_sqrt(sc + 4, s);
+    double bnorm = 0;
+    CK(cudaMemcpyAsync(&bnorm, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     int it = 0;
-    if (bnorm != 0) {
-      prec(r, z);
+    if (history) history[0] = 1.0;
+    if (bnorm != 0 && maxit > 0) {
+      // first iteration eagerly (p = z, rz = (r, z))
+      prec(r, z, s);
       CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-      double rz = dot(r, z);
-      for (it = 0; it < maxit; ++it) {
-        op_apply_T<double>(op, p, ap, s);
-        const double alpha = rz / dot(p, ap);
-        launch_cg_xr<double>(d_x, r, p, ap, alpha, n, s);
-        const double rel = std::sqrt(dot(r, r)) / bnorm;
-        if (history) history[it + 1] = rel;
-        if (rel <= rtol) {
-          ++it;
-          break;
+      dot_to(r, z, sc + 0, s);
+      tail(s, cudaGraphConditionalHandle{}, 0);
+      int hic[2] = {0, 0};
+      CK(cudaMemcpyAsync(hic, ic, sizeof(hic), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      // later iterations: z = M r; rz_new = (r, z); p = z + beta p; rz = rz_new; tail
+      auto body = [&](cudaStream_t st, cudaGraphConditionalHandle h, int use_h) {
+        prec(r, z, st);
+        dot_to(r, z, sc + 3, st);
+        launch_pcg_p(p, z, sc, n, st);
+        launch_pcg_shift(sc, st);
+        tail(st, h, use_h);
+      };
+      if (!hic[1]) {
+        bool graphed = false;
+        // the V-cycle is capturable only without host syncs (dense coarse
+        // solve); the coarse-CG hierarchy keeps the host loop
+        if (pcg_graph_enabled() && (!mg || mg->dense)) graphed = pcg_run_graph(s, body);
+        if (!graphed) {
+          for (;;) {  // host loop (no graph): one sync per iteration
+            body(s, cudaGraphConditionalHandle{}, 0);
+            CK(cudaMemcpyAsync(hic, ic, sizeof(hic), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (hic[1]) break;
+          }
         }
-        prec(r, z);
-        const double rz_new = dot(r, z);
-        const double beta = rz_new / rz;
-        rz = rz_new;
-        launch_cg_p<double>(p, z, beta, n, s);
       }
+      CK(cudaMemcpyAsync(&it, ic, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (history && it > 0) CK(cudaMemcpy(history + 1, dhist + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
     }
     if (iterations) *iterations = it;
     CK(cudaStreamSynchronize(s));
-    cudaFree(r);
-    cudaFree(z);
-    cudaFree(p);
-    cudaFree(ap);
-    cudaFree(dbuf);
-    cudaFreeHost(hdot);
   });
 }
 

@@ -46,7 +46,7 @@ static bool pdl_enabled() {
 
 template <typename T>
 void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny, int nz,
-                        int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s) {
+                        int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s, bool pdl) {
   if (c1 < c0) return;
   const int mx = nx * p + 1, my = ny * p + (periodic_y ? 0 : 1);
   {
@@ -58,7 +58,7 @@ void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, cons
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     switch (p) {
@@ -129,9 +129,9 @@ void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces,
 }
 
 template void launch_node_gather<double>(const double*, const double*, const double*, const double*, double*, int,
-                                         int, int, int, int, int, int, int, int, cudaStream_t);
+                                         int, int, int, int, int, int, int, int, cudaStream_t, bool);
 template void launch_node_gather<float>(const float*, const float*, const float*, const float*, float*, int, int,
-                                        int, int, int, int, int, int, int, cudaStream_t);
+                                        int, int, int, int, int, int, int, cudaStream_t, bool);
 template void launch_pack_face<double>(const double*, double*, int, int, int, int, int, cudaStream_t);
 template void launch_pack_face<float>(const float*, float*, int, int, int, int, int, cudaStream_t);
 template void launch_diag_finish<double>(double*, int64_t, int, int, int, int, unsigned long long*, cudaStream_t);

@@ -31,7 +31,8 @@ void launch_sub_load_mask(T* r, const T* load, double scale, int64_t nnodes, int
 // gather.cu
 template <typename T>
 void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, const T* x, T* y, int nx, int ny,
-                        int nz, int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s);
+                        int nz, int p, int faces, int kpar, int c0, int c1, int periodic_y, cudaStream_t s,
+                        bool pdl = true);
 template <typename T>
 void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int side, cudaStream_t s);
 template <typename T>
@@ -101,6 +102,14 @@ template <typename T>
 void launch_cg_xr(T* x, T* r, const T* p, const T* ap, double alpha, int64_t n, cudaStream_t s);
 template <typename T>
 void launch_cg_p(T* p, const T* z, double beta, int64_t n, cudaStream_t s);
+// device-resident PCG (solver.cu)
+void launch_pcg_xr(double* x, double* r, const double* p, const double* ap, const double* sc, int64_t n,
+                   cudaStream_t s);
+void launch_pcg_p(double* p, const double* z, const double* sc, int64_t n, cudaStream_t s);
+void launch_pcg_shift(double* sc, cudaStream_t s);
+void launch_pcg_sqrt(double* v, cudaStream_t s);
+void launch_pcg_check(const double* sc, int* ic, double* hist, double rtol, int maxit, cudaGraphConditionalHandle h,
+                      int use_h, cudaStream_t s);
 template <typename T>
 void launch_jacobi(const T* inv, const T* r, T* z, int64_t n, cudaStream_t s);
 

@@ -324,6 +324,51 @@ void launch_cg_p(T* p, const T* z, double beta, int64_t n, cudaStream_t s) {
 template void launch_cg_p<double>(double*, const double*, double, int64_t, cudaStream_t);
 template void launch_cg_p<float>(float*, const float*, double, int64_t, cudaStream_t);
 
+// ---- device-resident PCG (capi.cu emfgpu_pcg_solve) -------------------------
+// Scalars live on the device: sc = {rz, p.Ap, r.r, rz_new, ||b||}, ic = {it, done}.
+// The arithmetic is the host loop's, in the same order (alpha = rz / pAp,
+// rel = sqrt(rr) / ||b||, beta = rz_new / rz), so iterates are identical.
+__global__ void pcg_xr_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                              const double* __restrict__ ap, const double* __restrict__ sc, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double alpha = sc[0] / sc[1];
+  x[i] += alpha * p[i];
+  r[i] -= alpha * ap[i];
+}
+__global__ void pcg_p_kernel(double* __restrict__ p, const double* __restrict__ z, const double* __restrict__ sc,
+                             int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double beta = sc[3] / sc[0];
+  p[i] = z[i] + beta * p[i];
+}
+__global__ void pcg_shift_kernel(double* sc) { sc[0] = sc[3]; }
+__global__ void pcg_sqrt_kernel(double* v) { *v = sqrt(*v); }
+__global__ void pcg_check_kernel(const double* __restrict__ sc, int* ic, double* hist, double rtol, int maxit,
+                                 cudaGraphConditionalHandle h, int use_h) {
+  const double rel = sqrt(sc[2]) / sc[4];
+  const int it = ic[0] + 1;
+  hist[it] = rel;
+  ic[0] = it;
+  const int stop = (rel <= rtol) || it >= maxit;
+  ic[1] = stop;
+  if (use_h) cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+void launch_pcg_xr(double* x, double* r, const double* p, const double* ap, const double* sc, int64_t n,
+                   cudaStream_t s) {
+  pcg_xr_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, r, p, ap, sc, n);
+}
+void launch_pcg_p(double* p, const double* z, const double* sc, int64_t n, cudaStream_t s) {
+  pcg_p_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, z, sc, n);
+}
+void launch_pcg_shift(double* sc, cudaStream_t s) { pcg_shift_kernel<<<1, 1, 0, s>>>(sc); }
+void launch_pcg_sqrt(double* v, cudaStream_t s) { pcg_sqrt_kernel<<<1, 1, 0, s>>>(v); }
+void launch_pcg_check(const double* sc, int* ic, double* hist, double rtol, int maxit, cudaGraphConditionalHandle h,
+                      int use_h, cudaStream_t s) {
+  pcg_check_kernel<<<1, 1, 0, s>>>(sc, ic, hist, rtol, maxit, h, use_h);
+}
+
 // z = inv * r (Jacobi)
 template <typename T>
 __global__ void jacobi_kernel(const T* __restrict__ inv, const T* __restrict__ r, T* __restrict__ z, int64_t n) {

@@ -103,6 +103,9 @@ class SlabOperator:
         s = self._stream()
         nzl = part.nz_local
         if part.world == 1:
+            if ev_mid is None and hasattr(e, "apply_tangent_device"):
+                e.apply_tangent_device(x, y, stream=s)  # one call: element + node phase
+                return
             e.apply_elements(x, 0, nzl, stream=s)
             if ev_mid is not None:
                 ev_mid.record()

@@ -734,3 +734,39 @@ def test_ticket_scheduler_ranges_streams_repeats(G, p, prec, strat):
         op.apply_tangent_device(x, y)
     torch.cuda.synchronize()
     assert torch.equal(y, y_ref)
+
+
+@pytest.mark.gpu
+def test_pcg_graph_loop_equals_host_loop(G):
+    """The device-resident PCG (conditional-WHILE CUDA graph around apply,
+    V-cycle and device scalars) gives bitwise the iterates, history and
+    iteration count of the host-driven loop (EMFGPU_PCG_GRAPH=0)."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, hashlib, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2408_12479_b200 import emfgpu as G, inputs as I
+n, p = 6, 2
+lev = G.FeLevel(n, p=p)
+prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+mg = G.MgHierarchy(lev, "inh", prm, degree=5, coarse_n=3, precision=32)
+mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+op = G.ElasticOperator(lev, "inh", prm, "none", 64)
+op.update_linearization(np.zeros(lev.n_dofs))
+b = torch.tensor(I.make_v(lev.n_dofs, 2), device="cuda")
+b[torch.tensor(I.dirichlet_mask(n, n, n, p, 1), device="cuda")] = 0
+x = torch.empty_like(b)
+its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 200)
+x2 = torch.empty_like(b)
+its2, hist2 = G.pcg_solve(op, None, b, x2, 1e-10, 3000)
+print(its, its2, hashlib.sha1(x.cpu().numpy().tobytes() + hist.tobytes() + x2.cpu().numpy().tobytes()).hexdigest())
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, EMFGPU_PCG_GRAPH=flag)
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, env=env)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(out.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs

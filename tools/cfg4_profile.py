@@ -21,8 +21,10 @@ mg = G.MgHierarchy(lev, w.model, w.material(), degree=5, coarse_n=6, precision=3
 mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
 b = torch.tensor(W.rhs(w), device="cuda")
 x = torch.empty_like(b)
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-its, hist = G.pcg_solve(op, mg, b, x, 1e-8, its_max)
-torch.cuda.synchronize()
-print("its", its, "solve_s %.4f" % (time.perf_counter() - t0), "levels", mg.levels())
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+for _ in range(reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    its, hist = G.pcg_solve(op, mg, b, x, 1e-8, its_max)
+    torch.cuda.synchronize()
+    print("its", its, "solve_s %.4f" % (time.perf_counter() - t0), "levels", mg.levels(), flush=True)
