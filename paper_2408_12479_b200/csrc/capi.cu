@@ -226,7 +226,7 @@ KArgs<T> kargs(const emfgpu_op* op) {
   a.fd_nxy = FastDiv::make((uint32_t)(L->nx * L->ny));
   a.spatial = op->domain;
   a.coords = L->d_coords;
-  a.tk = op->d_ctr + 2 * (op->ticket_seq++ % emfgpu_op::kTicketSlots);
+  a.tk = op->d_ctr + 2 * (op->ticket_seq.fetch_add(1, std::memory_order_relaxed) % emfgpu_op::kTicketSlots);
   return a;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -171,7 +172,7 @@ struct emfgpu_op {
   // of this operator on different streams never share a counter
   static constexpr int kTicketSlots = 256;
   unsigned* d_ctr = nullptr;
-  mutable unsigned ticket_seq = 0;
+  mutable std::atomic<unsigned> ticket_seq{0};  // host threads may launch concurrently
   bool linearized = false;
   uint64_t checksum = 0;
   std::string last_error;
