@@ -101,6 +101,10 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 template <typename T>
 __device__ __forceinline__ void cp_async_T(T* smem, const T* gmem) {
   if constexpr (sizeof(T) == 8)
@@ -586,14 +590,35 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     const int sqs = lat<N>(si, sj, sk);
     const int64_t es = elem_of(u, sel);
     bool zero = true;
+    // Q3: u_k comes from its per-element copy in the staging layout, as
+    // contiguous 16-byte copies (a warp moves 512 contiguous bytes) instead
+    // of 3 scattered 8-byte words per thread
+    constexpr bool kUkEl = kUk && P == 3;
+    const bool uk_el = kUkEl && a.uk_el != nullptr;
     if (es < a.nel) {
       const ElemPos ep = elem_pos_fast<P>(es, a, si, sj, sk);
       zero = node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
 #pragma unroll
       for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][sel][c][sqs], a.x + 3 * ep.node + c);
       if constexpr (kUk) {
+        if (!uk_el) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][sel][3 + c][sqs], a.uk + 3 * ep.node + c);
+          for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][sel][3 + c][sqs], a.uk + 3 * ep.node + c);
+        }
+      }
+    }
+    if constexpr (kUkEl) {
+      if (uk_el) {
+        constexpr int CH = 3 * SZ * (int)sizeof(T) / 16;  // 16-byte chunks per element
+        constexpr int NE = kPerElem ? 1 : EPB, NT = kPerElem ? N3 : EPB * N3;
+        const int t0 = kPerElem ? q : tid_f;
+        for (int ch = t0; ch < NE * CH; ch += NT) {
+          const int ee = kPerElem ? el : ch / CH, cc = ch - (kPerElem ? 0 : ee) * CH;
+          const int64_t e2 = elem_of(u, ee);
+          if (e2 < a.nel)
+            cp_async16(reinterpret_cast<char*>(&sm.stage[b][ee][3][0]) + 16 * cc,
+                       reinterpret_cast<const char*>(a.uk_el + e2 * 3 * SZ) + 16 * cc);
+        }
       }
     }
     const int64_t e = elem_of(u, el);

@@ -207,6 +207,38 @@ void launch_fibre_frame(const double* coords, double* hq, double* m1q, int nx, i
   fibre_frame_kernel<<<(unsigned)((a.nqp + 255) / 256), 256, 0, s>>>(a);
 }
 
+// u_k gathered per element into the element kernels' staging layout: slot
+// a + SY b + SZ c of array comp (apply_v2.cuh Lay<N>), padding slots zero.
+template <typename T, int N, int SY, int SZ_, int SIZE>
+__global__ void uk_elem_kernel(const T* __restrict__ uk, T* __restrict__ out, int64_t nel, int nx, int ny, int mx,
+                               int my) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nel * 3 * SIZE) return;
+  const int slot = (int)(i % SIZE);
+  const int64_t ec = i / SIZE;
+  const int comp = (int)(ec % 3);
+  const int64_t e = ec / 3;
+  const int lc = slot / SZ_, rem = slot - lc * SZ_, lb = rem / SY, la = rem - lb * SY;
+  T v = T(0);
+  if (la < N && lb < N && lc < N) {
+    const int64_t ei = e % nx, ej = (e / nx) % ny, ek = e / ((int64_t)nx * ny);
+    int gb = (int)ej * (N - 1) + lb;
+    if (gb >= my) gb -= my;  // periodic y lattice
+    const int64_t node = ((ek * (N - 1) + lc) * my + gb) * mx + ei * (N - 1) + la;
+    v = uk[3 * node + comp];
+  }
+  out[i] = v;
+}
+template <typename T>
+void launch_uk_elem(const T* uk, T* out, int64_t nel, int nx, int ny, int mx, int my, int size, cudaStream_t s) {
+  const int64_t tot = nel * 3 * size;
+  const unsigned blocks = (unsigned)((tot + 255) / 256);
+  if (size == 82) uk_elem_kernel<T, 4, 4, 20, 82><<<blocks, 256, 0, s>>>(uk, out, nel, nx, ny, mx, my);
+  else uk_elem_kernel<T, 4, 4, 20, 80><<<blocks, 256, 0, s>>>(uk, out, nel, nx, ny, mx, my);
+}
+template void launch_uk_elem<double>(const double*, double*, int64_t, int, int, int, int, int, cudaStream_t);
+template void launch_uk_elem<float>(const float*, float*, int64_t, int, int, int, int, int, cudaStream_t);
+
 __global__ void cast_d2f_kernel(const double* in, float* out, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (float)in[i];

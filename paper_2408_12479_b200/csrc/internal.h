@@ -103,6 +103,9 @@ template <typename T>
 void launch_cg_xr(T* x, T* r, const T* p, const T* ap, double alpha, int64_t n, cudaStream_t s);
 template <typename T>
 void launch_cg_p(T* p, const T* z, double beta, int64_t n, cudaStream_t s);
+// geometry.cu: u_k in the Q3 staging layout per element (size = Lay<4>::SIZE)
+template <typename T>
+void launch_uk_elem(const T* uk, T* out, int64_t nel, int nx, int ny, int mx, int my, int size, cudaStream_t s);
 // device-resident PCG (solver.cu)
 void launch_pcg_xr(double* x, double* r, const double* p, const double* ap, const double* sc, int64_t n,
                    cudaStream_t s);
@@ -172,6 +175,7 @@ struct emfgpu_op {
   // of this operator on different streams never share a counter
   static constexpr int kTicketSlots = 256;
   unsigned* d_ctr = nullptr;
+  void* d_uk_el = nullptr;  // Q3 none/scalar: u_k per element in the staging layout (KArgs::uk_el)
   mutable std::atomic<unsigned> ticket_seq{0};  // host threads may launch concurrently
   bool linearized = false;
   uint64_t checksum = 0;

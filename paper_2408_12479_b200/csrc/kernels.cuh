@@ -105,6 +105,7 @@ struct KArgs {
   int spatial;           // Formulation::domain == spatial (linearize / diagonal / residual)
   const double* coords;  // node coordinates (spatial linearization: J_t = J0 + Grad_xi u_k)
   unsigned* tk;          // apply_v2 ticket counter slot: [0] next ticket, [1] workers done
+  const T* uk_el;        // Q3: u_k per element in the staging layout [e][3][SIZE] (null: lattice gather)
 };
 
 // Stored scalars of the scalar/tensor strategies (load_scalar_fields,
