@@ -669,23 +669,28 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     T gx[9];
     T* const S = &sm.stage[buf][el][0][0];  // kUk: x (arrays 0-2), u_k (3-5)
     // forward sweeps of staged vector arrays [f0, f0+3): gradients into R2
-    auto fwd_sweeps = [&](int f0) {
+    // swap: the u_k pass runs R1 -> R2 -> R1 so that its first stage can
+    // start while the threads still read the x gradient from R2 (no barrier
+    // between the two passes); its gradient then ends in R1
+    auto fwd_sweeps = [&](int f0, bool swap) {
       if constexpr (kDense) {
         constexpr int SI = SM::NST * SZ, SR = 9 * SZ, TH = EPB * N3;
-        T* const R1a = &sm.r1[0][0][0];
-        T* const R2a = &sm.r2[0][0][0];
-        fw_x<T, N, TH, EPB, SI, SR>(&sm.stage[buf][0][f0][0], R2a, R2a + 3 * SZ, a.Bm, Dfx, tid);
+        T* const P1 = swap ? &sm.r2[0][0][0] : &sm.r1[0][0][0];
+        T* const P2 = swap ? &sm.r1[0][0][0] : &sm.r2[0][0][0];
+        fw_x<T, N, TH, EPB, SI, SR>(&sm.stage[buf][0][f0][0], P2, P2 + 3 * SZ, a.Bm, Dfx, tid);
         esync();
-        fw_y<T, N, TH, EPB, SR>(R2a, R2a + 3 * SZ, R1a, R1a + 3 * SZ, R1a + 6 * SZ, a.Bm, Dfy, tid);
+        fw_y<T, N, TH, EPB, SR>(P2, P2 + 3 * SZ, P1, P1 + 3 * SZ, P1 + 6 * SZ, a.Bm, Dfy, tid);
         esync();
-        fw_z<T, N, TH, EPB, SR>(R1a, R1a + 3 * SZ, R1a + 6 * SZ, R2a, a.Bm, Dfz, tid);
+        fw_z<T, N, TH, EPB, SR>(P1, P1 + 3 * SZ, P1 + 6 * SZ, P2, a.Bm, Dfz, tid);
         esync();
       } else {
-        fw_x<T, N>(&sm.stage[buf][el][f0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+        T* const P1 = swap ? R2 : R1;
+        T* const P2 = swap ? R1 : R2;
+        fw_x<T, N>(&sm.stage[buf][el][f0][0], P2, P2 + 3 * SZ, a.Bm, Dfx, q);
         esync();
-        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+        fw_y<T, N>(P2, P2 + 3 * SZ, P1, P1 + 3 * SZ, P1 + 6 * SZ, a.Bm, Dfy, q);
         esync();
-        fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+        fw_z<T, N>(P1, P1 + 3 * SZ, P1 + 6 * SZ, P2, a.Bm, Dfz, q);
         esync();
       }
     };
@@ -713,7 +718,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       esync();
     } else {
       // ---- gradient of x at the qps
-      fwd_sweeps(0);
+      fwd_sweeps(0, false);
 #pragma unroll
       for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
     }
@@ -734,10 +739,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       if constexpr (kFused) {
         grad_at(1, gk);
       } else {
-        esync();
-        fwd_sweeps(3);
+        fwd_sweeps(3, true);
 #pragma unroll
-        for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+        for (int m = 0; m < 9; ++m) gk[m] = R1[m * SZ + qs];
       }
       if constexpr (CART) {
 #pragma unroll
