@@ -833,7 +833,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       esync();
       if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
     }
-    esync();  // staging buffer `buf` and r1/r2 are reused next
+    // No closing barrier: before the next unit's first barrier a thread only
+    // zeroes its own staged words of the other buffer and issues the next
+    // prefetch into this unit's buffer, whose last readers (the x-sweeps, or
+    // the fp32 d/dz read) are behind several barriers already; r1/r2 are
+    // first written after that barrier.
   };
 
   // The first two units of a worker are static (no atomic round trip before
@@ -866,7 +870,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       if (pt < nu) praw = atomicAdd(a.tk, 1u);
     }
     cp_async_wait<1>();
-    compute(cur, buf, zero_cur);  // ends with the worker's barrier
+    compute(cur, buf, zero_cur);  // the published ticket is read after its barriers
     const int nn = s_tk[slot][par];
     par ^= 1;
     cur = nxt;
