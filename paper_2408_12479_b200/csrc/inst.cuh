@@ -7,6 +7,9 @@
 #include "apply_v3.cuh"
 #include "internal.h"
 
+#ifndef EMF_F32_V3CART
+#define EMF_F32_V3CART 1
+#endif
 #ifndef EMF_V3_ENABLE
 #define EMF_V3_ENABLE 1
 #endif
@@ -27,7 +30,8 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   // 0.169 -> 0.114 ms, fibre 0.169 -> 0.120; fp64 iNH tensor 0.214 -> 0.163,
   // cNH tensor 0.1445 -> 0.1384, cachedF 0.159 -> 0.151).
   constexpr bool kTC = STRAT == S_CACHEDF || STRAT == S_TENSOR;
-  constexpr bool kF32V3 = sizeof(EMF_T) == 4 && CART && !is_spatial(STRAT) && (STRAT == S_NONE || STRAT == S_SCALAR);
+  constexpr bool kF32V3 = EMF_F32_V3CART && sizeof(EMF_T) == 4 && CART && !is_spatial(STRAT) &&
+                          (STRAT == S_NONE || STRAT == S_SCALAR);
   constexpr bool kV3 = EMF_V3_ENABLE && (EMF_P == 2 ? (sizeof(EMF_T) == 4 || kTC) : (EMF_P == 3 && kF32V3));
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
