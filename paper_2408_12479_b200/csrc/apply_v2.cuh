@@ -478,6 +478,10 @@ constexpr int minb_v2() {
   if (sizeof(T) == 4) return (P == 4 && EMF_MINB_F32Q4) ? EMF_MINB_F32Q4 : TileV2<P, 4>::MINB;
   if (EMF_MINB_V2D_FORCE) return EMF_MINB_V2D_FORCE;  // experiments (tools/build_variant.sh)
   if (P == 3 && MODEL == CNH && ((STRAT == S_NONE && CART) || STRAT == S_SP_NONE || STRAT == S_SP_TENSOR)) return 4;
+  // re-measured after the ticket / dense-mapping / barrier work: cNH on
+  // axis-aligned meshes fits 128 registers for these too (scalar 0.1649 ->
+  // 0.1588 ms, tensor 0.1383 -> 0.1281, cachedF 0.1486 -> 0.1444)
+  if (P == 3 && MODEL == CNH && CART && (STRAT == S_SCALAR || STRAT == S_TENSOR || STRAT == S_CACHEDF)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
   // Q4 curved fp64: 2 CTAs/SM (255 registers) beats 3 with spills
   // (24^3 Q4 curved iNH none 0.241 -> 0.214 ms, tensor 0.220 -> 0.198 ms);
