@@ -21,6 +21,9 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef EMF_MINB_F32Q3
+#define EMF_MINB_F32Q3 0  // fp32 Q3 CTAs/SM override (experiments)
+#endif
 #ifndef EMF_MINB_F32Q4
 #define EMF_MINB_F32Q4 0  // fp32 Q4 CTAs/SM override (experiments)
 #endif
@@ -475,7 +478,15 @@ struct ApplyV2Smem {
 #endif
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 constexpr int minb_v2() {
-  if (sizeof(T) == 4) return (P == 4 && EMF_MINB_F32Q4) ? EMF_MINB_F32Q4 : TileV2<P, 4>::MINB;
+  if (sizeof(T) == 4) {
+    if (P == 4 && EMF_MINB_F32Q4) return EMF_MINB_F32Q4;
+    if (P == 3 && EMF_MINB_F32Q3) return EMF_MINB_F32Q3;
+    // 5 CTAs/SM measured faster for these cNH fp32 Q3 variants (tensor
+    // 0.0912 -> 0.0871 ms, spatial none 0.1137 -> 0.1076), slower for fibre
+    // tensor (0.1178 -> 0.1280) and no better elsewhere
+    if (P == 3 && MODEL == CNH && (STRAT == S_TENSOR || STRAT == S_SP_NONE)) return 5;
+    return TileV2<P, 4>::MINB;
+  }
   if (EMF_MINB_V2D_FORCE) return EMF_MINB_V2D_FORCE;  // experiments (tools/build_variant.sh)
   if (P == 3 && MODEL == CNH && ((STRAT == S_NONE && CART) || STRAT == S_SP_NONE || STRAT == S_SP_TENSOR)) return 4;
   // re-measured after the ticket / dense-mapping / barrier work: cNH on

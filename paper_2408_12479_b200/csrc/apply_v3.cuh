@@ -29,6 +29,9 @@ constexpr int kV3Warps = 4;
 
 // CTAs per SM for the launch bounds: fp32 4, fp64 3 (4 measured slower even
 // where it fits without spills: cfg1 fp64 tensor 0.1251 -> 0.1382 ms).
+#ifndef EMF_MINB_V3F
+#define EMF_MINB_V3F 0  // fp32 v3 CTAs/SM override (experiments)
+#endif
 #ifndef EMF_MINB_FIBER_V3F
 #define EMF_MINB_FIBER_V3F 4
 #endif
@@ -40,7 +43,7 @@ constexpr int minb_v3() {
   // fibre: fp64 2 CTAs/SM, spill-free (32^3 Q3 tensor 0.226 -> 0.208 ms);
   // fp32 keeps 4 (3 measured slower: 0.167 -> 0.187 ms)
   if (MODEL == FIBER) return sizeof(T) == 4 ? EMF_MINB_FIBER_V3F : EMF_MINB_FIBER_V3D;
-  return sizeof(T) == 4 ? 4 : 3;
+  return sizeof(T) == 4 ? (EMF_MINB_V3F ? EMF_MINB_V3F : 4) : 3;
 }
 
 template <typename T, int P, int MODEL, int STRAT, bool CART>
