@@ -5,6 +5,7 @@
 // proj/src/capi.cpp:26-41); no CPU fallback exists — without a CUDA device
 // every create call fails with EMFGPU_ERR_CUDA.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -640,6 +641,7 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_y);
   cudaFree(op->d_load);
   cudaFree(op->lz_buf);
+  cudaFree(op->pcg_buf);
   cudaFree(op->d_err);
   if (op->h_err) cudaFreeHost(op->h_err);
   if (op->stream) cudaStreamDestroy(op->stream);
@@ -1780,9 +1782,13 @@ static bool pcg_run_graph(cudaStream_t s, F&& body) {
       ok = cudaStreamEndCapture(cs, &out) == cudaSuccess && !thrown;
     }
   }
+  const auto t_cap = std::chrono::steady_clock::now();
   if (ok) ok = cudaGraphInstantiate(&ge, g, 0) == cudaSuccess;
+  const auto t_inst = std::chrono::steady_clock::now();
   if (!ok) {
-    cudaGetLastError();
+    const cudaError_t err = cudaGetLastError();
+    if (std::getenv("EMFGPU_DEBUG"))
+      std::fprintf(stderr, "emfgpu: PCG graph not built (%s), host loop\n", cudaGetErrorString(err));
     if (ge) cudaGraphExecDestroy(ge);
     if (g) cudaGraphDestroy(g);
     cudaStreamDestroy(cs);
@@ -1790,6 +1796,11 @@ static bool pcg_run_graph(cudaStream_t s, F&& body) {
   }
   CK(cudaGraphLaunch(ge, s));
   CK(cudaStreamSynchronize(s));
+  if (std::getenv("EMFGPU_DEBUG")) {
+    const auto t_run = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "emfgpu: PCG graph instantiate %.2f ms, run %.2f ms\n", ms(t_cap, t_inst), ms(t_inst, t_run));
+  }
   cudaGraphExecDestroy(ge);
   cudaGraphDestroy(g);
   cudaStreamDestroy(cs);
@@ -1810,22 +1821,25 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     // on, the whole loop is one CUDA graph with a conditional WHILE node whose
     // condition the convergence-check kernel sets -- no host round trip per
     // iteration.  Same arithmetic and order as the host loop it replaced.
-    double *r, *z, *p, *ap, *dbuf, *sc, *dhist;
-    int* ic;
-    CK(cudaMalloc(&r, sizeof(double) * n));
-    CK(cudaMalloc(&z, sizeof(double) * n));
-    CK(cudaMalloc(&p, sizeof(double) * n));
-    CK(cudaMalloc(&ap, sizeof(double) * n));
-    CK(cudaMalloc(&dbuf, sizeof(double) * (dot_partial_count() + 1)));
-    CK(cudaMalloc(&sc, sizeof(double) * 8));
-    CK(cudaMalloc(&ic, sizeof(int) * 2));
-    CK(cudaMalloc(&dhist, sizeof(double) * (maxit + 1)));
-    struct Cleanup {
-      std::vector<void*> v;
-      ~Cleanup() {
-        for (void* q : v) cudaFree(q);
-      }
-    } cleanup{{r, z, p, ap, dbuf, sc, ic, dhist}};
+    // work space cached on the operator (large cudaMalloc / cudaFree pairs
+    // per solve cost 0-200 ms of host time, measured)
+    const size_t need = sizeof(double) * (4 * (size_t)n + dot_partial_count() + 1 + 8 + (size_t)maxit + 1) + 16;
+    if (op->pcg_bytes < need) {
+      cudaFree(op->pcg_buf);
+      op->pcg_buf = nullptr;
+      op->pcg_bytes = 0;
+      CK(cudaMalloc(&op->pcg_buf, need));
+      op->pcg_bytes = need;
+    }
+    double* const base = static_cast<double*>(op->pcg_buf);
+    double* const r = base;
+    double* const z = r + n;
+    double* const p = z + n;
+    double* const ap = p + n;
+    double* const dbuf = ap + n;
+    double* const sc = dbuf + dot_partial_count() + 1;
+    double* const dhist = sc + 8;
+    int* const ic = reinterpret_cast<int*>(dhist + maxit + 1);
     auto dot_to = [&](const double* a, const double* b, double* out, cudaStream_t st) {
       launch_dot<double>(a, b, n, dbuf, out, st);
     };
