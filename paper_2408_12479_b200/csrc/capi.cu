@@ -642,6 +642,7 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->d_load);
   cudaFree(op->lz_buf);
   cudaFree(op->pcg_buf);
+  cudaFree(op->fgmres_buf);
   cudaFree(op->d_err);
   if (op->h_err) cudaFreeHost(op->h_err);
   if (op->stream) cudaStreamDestroy(op->stream);
@@ -2162,12 +2163,25 @@ bool fgmres(Krylov& K, const double* b, double* x, double abs_tol, double rel_to
   const int64_t n = K.n;
   const double bnorm = std::sqrt(K.dot(b, b));
   const double tol = std::max(abs_tol, rel_tol * bnorm);
-  std::vector<DevVec> V(m + 1), Z(m);
-  for (auto& v : V) CK(cudaMalloc(&v.p, sizeof(double) * n));
-  for (auto& z : Z) CK(cudaMalloc(&z.p, sizeof(double) * n));
-  DevVec w, r;
-  CK(cudaMalloc(&w.p, sizeof(double) * n));
-  CK(cudaMalloc(&r.p, sizeof(double) * n));
+  // Krylov basis, preconditioned directions, w and r: 2m + 3 vectors from
+  // one work space cached on the operator (a per-solve cudaMalloc / cudaFree
+  // of 2m + 3 vectors cost far more than the allocation of the PCG's 4)
+  struct Vec {
+    double* p;
+  };
+  const size_t need = sizeof(double) * (size_t)(2 * m + 3) * (size_t)n;
+  if (K.op->fgmres_bytes < need) {
+    cudaFree(K.op->fgmres_buf);
+    K.op->fgmres_buf = nullptr;
+    K.op->fgmres_bytes = 0;
+    CK(cudaMalloc(&K.op->fgmres_buf, need));
+    K.op->fgmres_bytes = need;
+  }
+  double* const wbase = static_cast<double*>(K.op->fgmres_buf);
+  std::vector<Vec> V(m + 1), Z(m);
+  for (int i = 0; i <= m; ++i) V[i].p = wbase + (size_t)i * n;
+  for (int i = 0; i < m; ++i) Z[i].p = wbase + (size_t)(m + 1 + i) * n;
+  Vec w{wbase + (size_t)(2 * m + 1) * n}, r{wbase + (size_t)(2 * m + 2) * n};
   std::vector<double> H((m + 1) * m, 0.0), cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0);
   int its = 0;
   for (int cycle = 0; cycle <= max_restarts; ++cycle) {

@@ -154,9 +154,11 @@ struct emfgpu_op {
   // Lanczos work space (estimate_eigenvalues), kept across relinearizations
   double* lz_buf = nullptr;
   size_t lz_bytes = 0;
-  // PCG work space (emfgpu_pcg_solve), kept across solves
+  // PCG / FGMRES work spaces, kept across solves
   void* pcg_buf = nullptr;
   size_t pcg_bytes = 0;
+  void* fgmres_buf = nullptr;
+  size_t fgmres_bytes = 0;
   // per-qp fibre frame field (fibre model): H4/H6 in double and Number, M1s
   int frame_kind = 0;
   double* d_hqd = nullptr;
