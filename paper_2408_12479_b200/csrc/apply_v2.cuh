@@ -5,7 +5,8 @@
 //  * persistent CTAs (one wave, occupancy-sized) take element groups from a
 //    ticket counter and prefetch the NEXT group's x / u_k / affine geometry
 //    into a second shared staging buffer with cp.async while the current
-//    group computes;
+//    group computes; 10 barriers per group (the u_k forward pass runs through
+//    swapped buffers, and a group has no closing barrier);
 //  * sum factorization by pencil workers: a worker owns one (component, line)
 //    pencil and performs the full 1D contraction in registers, so every
 //    shared load feeds n FMAs and the 1D tables are compile-time-indexed
@@ -859,9 +860,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
 
   // The first two units of a worker are static (no atomic round trip before
   // the first element); later tickets come from a.tk[0], taken one unit ahead
-  // of need by the worker's leader and published through shared memory, read
-  // after the next compute's closing barrier.
-  // let a programmatically dependent node phase launch now: its CTAs take
+  // of need by the worker's leader (its value used one unit later, so the
+  // atomic's round trip is never waited on) and published through shared
+  // memory, read after the barriers of the next compute.
+  // Let a programmatically dependent node phase launch now: its CTAs take
   // the SM slots this persistent grid frees at its end and wait there
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   __shared__ int s_tk[EPB][2];
