@@ -22,6 +22,9 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef EMF_CF_EARLY
+#define EMF_CF_EARLY 1  // cachedF: G loaded before the sweeps
+#endif
 #ifndef EMF_MINB_F32Q3
 #define EMF_MINB_F32Q3 0  // fp32 Q3 CTAs/SM override (experiments)
 #endif
@@ -680,6 +683,15 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       for (int m = 0; m < 9; ++m) sj[m] = cs[(C_JT + m) * st + qidx];
       sj[9] = cs[C_INVJ * st + qidx];
     }
+    // cachedF fp64: G = F - I loaded before the sweeps, its latency hidden
+    // behind them (cNH 0.1444 -> 0.1403 ms, curved iNH 0.2059 -> 0.1977;
+    // fp32 measured 2% slower, keeps the late load)
+    constexpr bool kCfEarly = STRAT == S_CACHEDF && EMF_CF_EARLY && sizeof(T) == 8;
+    T gcf[9];
+    if constexpr (kCfEarly) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gcf[m] = cs[(C_G + m) * st + qidx];
+    }
     esync();
 
     T* const R1 = &sm.r1[el][0][0];  // 9 arrays of SZ, contiguous
@@ -781,7 +793,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     } else if constexpr (STRAT == S_CACHEDF) {
       T gg[9];
 #pragma unroll
-      for (int m = 0; m < 9; ++m) gg[m] = cs[(C_G + m) * st + qidx];
+      for (int m = 0; m < 9; ++m) gg[m] = kCfEarly ? gcf[m] : cs[(C_G + m) * st + qidx];
       if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
       cache_scalars<T, MODEL>(mq, cb);
       second_pk<T, MODEL>(mq, cb);
