@@ -22,6 +22,12 @@
 #pragma once
 #include "kernels.cuh"
 
+#ifndef EMF_TEN_EARLY
+#define EMF_TEN_EARLY 1  // tensor: cached bundle loaded before the sweeps
+#endif
+#ifndef EMF_TEN_EARLY_F32
+#define EMF_TEN_EARLY_F32 1
+#endif
 #ifndef EMF_CF_EARLY
 #define EMF_CF_EARLY 1  // cachedF: G loaded before the sweeps
 #endif
@@ -687,6 +693,36 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // behind them (cNH 0.1444 -> 0.1403 ms, curved iNH 0.2059 -> 0.1977;
     // fp32 measured 2% slower, keeps the late load)
     constexpr bool kCfEarly = STRAT == S_CACHEDF && EMF_CF_EARLY && sizeof(T) == 8;
+    // tensor Q3: the cached bundle loaded before the sweeps, its latency
+    // hidden behind them (fp64 cNH 0.1281 -> 0.1219 ms, curved iNH 0.1628 ->
+    // 0.1567, fibre 0.2018 -> 0.1854; fp32 2-4%; Q4 iNH slower, 0.1772 -> 0.1874)
+    constexpr bool kTenEarly = STRAT == S_TENSOR && EMF_TEN_EARLY && P == 3 && (sizeof(T) == 8 || EMF_TEN_EARLY_F32);
+    auto load_tensor_bundle = [&](Bundle<T>& b) {
+      if (MODEL == CNH) b.lnj = cs[C_LNJ * st + qidx];
+      else {
+        b.jp = cs[C_JP * st + qidx];
+        b.c1 = cs[C_C1 * st + qidx];
+        b.c2 = cs[C_C2 * st + qidx];
+      }
+      if (MODEL == FIBER) {
+        b.c3[0] = cs[(C_C3 + 0) * st + qidx];
+        b.c3[1] = cs[(C_C3 + 1) * st + qidx];
+        b.efib[0] = cs[(C_EF + 0) * st + qidx];
+        b.efib[1] = cs[(C_EF + 1) * st + qidx];
+      }
+#pragma unroll
+      for (int m = 0; m < 9; ++m) {
+        b.F[m] = cs[(C_F + m) * st + qidx];
+        b.Finv[m] = cs[(C_FINV + m) * st + qidx];
+      }
+#pragma unroll
+      for (int m = 0; m < 6; ++m) {
+        b.S[m] = cs[(C_S + m) * st + qidx];
+        b.Cinv[m] = cs[(C_CINV + m) * st + qidx];
+      }
+    };
+    Bundle<T> cbe;
+    if constexpr (kTenEarly) load_tensor_bundle(cbe);
     T gcf[9];
     if constexpr (kCfEarly) {
 #pragma unroll
@@ -798,28 +834,8 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       cache_scalars<T, MODEL>(mq, cb);
       second_pk<T, MODEL>(mq, cb);
     } else {  // S_TENSOR
-      if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
-      else {
-        cb.jp = cs[C_JP * st + qidx];
-        cb.c1 = cs[C_C1 * st + qidx];
-        cb.c2 = cs[C_C2 * st + qidx];
-      }
-      if (MODEL == FIBER) {
-        cb.c3[0] = cs[(C_C3 + 0) * st + qidx];
-        cb.c3[1] = cs[(C_C3 + 1) * st + qidx];
-        cb.efib[0] = cs[(C_EF + 0) * st + qidx];
-        cb.efib[1] = cs[(C_EF + 1) * st + qidx];
-      }
-#pragma unroll
-      for (int m = 0; m < 9; ++m) {
-        cb.F[m] = cs[(C_F + m) * st + qidx];
-        cb.Finv[m] = cs[(C_FINV + m) * st + qidx];
-      }
-#pragma unroll
-      for (int m = 0; m < 6; ++m) {
-        cb.S[m] = cs[(C_S + m) * st + qidx];
-        cb.Cinv[m] = cs[(C_CINV + m) * st + qidx];
-      }
+      if constexpr (kTenEarly) cb = cbe;
+      else load_tensor_bundle(cb);
     }
     if constexpr (kFused) grad_at(0, gx);
     T wv[9];
