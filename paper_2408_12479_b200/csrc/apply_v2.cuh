@@ -25,6 +25,9 @@
 #ifndef EMF_TEN_EARLY
 #define EMF_TEN_EARLY 1  // tensor: cached bundle loaded before the sweeps
 #endif
+#ifndef EMF_SC_EARLY
+#define EMF_SC_EARLY 1
+#endif
 #ifndef EMF_TEN_EARLY_F32
 #define EMF_TEN_EARLY_F32 1
 #endif
@@ -723,6 +726,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     };
     Bundle<T> cbe;
     if constexpr (kTenEarly) load_tensor_bundle(cbe);
+    // scalar strategy: its 1-4 cached scalars loaded before the sweeps too
+    constexpr bool kScEarly = STRAT == S_SCALAR && EMF_SC_EARLY;
+    Bundle<T> cbs;
+    if constexpr (kScEarly) load_scalars<T, MODEL>(cs, st, qidx, cbs);
     T gcf[9];
     if constexpr (kCfEarly) {
 #pragma unroll
@@ -821,7 +828,17 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       } else {
         if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
         if constexpr (STRAT == S_NONE) cache_scalars<T, MODEL>(mq, cb);
-        else load_scalars<T, MODEL>(cs, st, qidx, cb);
+        else if constexpr (kScEarly) {
+          cb.lnj = cbs.lnj;
+          cb.jp = cbs.jp;
+          cb.c1 = cbs.c1;
+          cb.c2 = cbs.c2;
+          cb.c3[0] = cbs.c3[0];
+          cb.c3[1] = cbs.c3[1];
+          cb.efib[0] = cbs.efib[0];
+          cb.efib[1] = cbs.efib[1];
+        } else
+          load_scalars<T, MODEL>(cs, st, qidx, cb);
         second_pk<T, MODEL>(mq, cb);
       }
     } else if constexpr (STRAT == S_SP_TENSOR) {
