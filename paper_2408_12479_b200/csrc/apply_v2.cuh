@@ -25,6 +25,9 @@
 #ifndef EMF_TEN_EARLY
 #define EMF_TEN_EARLY 1  // tensor: cached bundle loaded before the sweeps
 #endif
+#ifndef EMF_SPT_EARLY
+#define EMF_SPT_EARLY 1
+#endif
 #ifndef EMF_SC_EARLY
 #define EMF_SC_EARLY 1
 #endif
@@ -726,6 +729,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     };
     Bundle<T> cbe;
     if constexpr (kTenEarly) load_tensor_bundle(cbe);
+    // spatial tensor: the cached spatial bundle loaded before the sweeps
+    constexpr bool kSpTenEarly = STRAT == S_SP_TENSOR && EMF_SPT_EARLY;
+    Bundle<T> cbst;
+    SpCell<T> spst;
+    if constexpr (kSpTenEarly) spatial_bundle<T, MODEL>(S_TENSOR, mq, nullptr, cs, st, qidx, cbst, spst);
     // scalar strategy: its 1-4 cached scalars loaded before the sweeps too
     constexpr bool kScEarly = STRAT == S_SCALAR && EMF_SC_EARLY;
     Bundle<T> cbs;
@@ -807,6 +815,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     }
     Bundle<T> cb;
     SpCell<T> sp;
+    if constexpr (kSpTenEarly) {
+      cb = cbst;
+      sp = spst;
+    }
     if constexpr (kUk) {
       T gk[9], gg[9];
       if constexpr (kFused) {
@@ -842,7 +854,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
         second_pk<T, MODEL>(mq, cb);
       }
     } else if constexpr (STRAT == S_SP_TENSOR) {
-      spatial_bundle<T, MODEL>(S_TENSOR, mq, nullptr, cs, st, qidx, cb, sp);
+      if constexpr (!kSpTenEarly) spatial_bundle<T, MODEL>(S_TENSOR, mq, nullptr, cs, st, qidx, cb, sp);
     } else if constexpr (STRAT == S_CACHEDF) {
       T gg[9];
 #pragma unroll
