@@ -142,6 +142,17 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
     // fp32 with u_k: x and u_k swept together in place (apply_v2.cuh fwc_*),
     // 3 full 32-lane rounds per stage instead of 4 half-empty ones; the
     // staging buffer then holds d/dz until the points have read it
+    // scalar strategy: this lane's cached scalars loaded before the sweeps
+    // (their latency hidden behind them, as in apply_v2)
+    constexpr bool kScEarly3 = STRAT == S_SCALAR && EMF_SC_EARLY;
+    Bundle<T> scb[QPL];
+    if constexpr (kScEarly3) {
+#pragma unroll
+      for (int r = 0; r < QPL; ++r) {
+        const int q = lane + 32 * r;
+        if (q < N3) load_scalars<T, MODEL>(a.cache, a.cache_stride, e * N3 + q, scb[r]);
+      }
+    }
     constexpr bool kFused = kUk && sizeof(T) == 4;
     T* const S = &sm.stage[0][0];
     T gx[QPL][9];
@@ -269,6 +280,16 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
         if (!make_strain(gg, cb)) atomicMin(a.err, (unsigned long long)qidx);
         if constexpr (STRAT == S_NONE) {
           cache_scalars<T, MODEL>(mq, cb);
+        } else if constexpr (kScEarly3) {
+          const Bundle<T>& sb = (QPL > 1 && r == 1) ? scb[QPL > 1 ? 1 : 0] : scb[0];
+          cb.lnj = sb.lnj;
+          cb.jp = sb.jp;
+          cb.c1 = sb.c1;
+          cb.c2 = sb.c2;
+          cb.c3[0] = sb.c3[0];
+          cb.c3[1] = sb.c3[1];
+          cb.efib[0] = sb.efib[0];
+          cb.efib[1] = sb.efib[1];
         } else {
           if (MODEL == CNH) cb.lnj = cs[C_LNJ * st + qidx];
           else {
