@@ -1,20 +1,28 @@
 """Benchmark of the matrix-free tangent apply y = K(u_k) v on B200.
 
-Contract (see DESIGN.md §5): one JSON line on rank 0.
-  * workload: BASELINE configs[1] — 32^3 affine cube, Q3, cNH (mu=1, lambda=10),
-    seeded u0/v (inputs.py).  At N GPUs: weak scaling, one 32^3 z-slab per GPU
-    (global mesh 32 x 32 x 32N), ghost faces exchanged with NCCL and
+Contract (DESIGN.md §4): one JSON line on rank 0.
+  * workload (the metric's config, BASELINE configs[2]): 64^3 Q4 hexahedra on
+    the curved map x' = x + 0.1 sin(2 pi y) e_x (per-qp J0 stored), iNH
+    (mu=1, kappa=1000), u0 amplitude 0.1 at pre-map coordinates with the
+    scaled noise 1e-3*8/64 (the literal 1e-3 noise is inadmissible: the
+    reference throws NonPositiveJacobian at (1, 46), reported under
+    "workloads"), v seeded U[-1,1].  At N GPUs: weak scaling, one 64^3 z-slab
+    per GPU (global mesh 64 x 64 x 64N), ghost faces exchanged with NCCL and
     overlapped with interior elements.
-  * a "step" = one tangent apply of the headline variant (fp64, on-the-fly
-    "none" strategy); the other 7 variants (fp64/fp32 x none/cachedF/scalar/
-    tensor) are timed the same way and reported under "variants".
-  * L2 is flushed (256 MiB write) before every timed apply; each apply is
-    timed with CUDA events on the operator's stream; max over ranks.
+  * a "step" = one tangent apply of the headline variant (fp64, strategy
+    none); the other cfg2 variants (fp64 tensor/scalar/cachedF, fp32
+    none/tensor) are timed the same way under "variants"; cfg1 (32^3 Q3 cNH,
+    12 variants) under "variants_cfg1" (N=1).
+  * L2 is flushed (256 MiB write) before every timed apply (the cfg2 inputs
+    are also larger than L2); each apply is timed with CUDA events on the
+    operator's stream; max over ranks.
   * value = global DoFs / apply time (reference definition, runner.cpp:131-132).
   * e2e = the same metric through the public host-vector call
     (emfgpu_op_apply_host: pinned H2D of v, apply, D2H of y, sync).
   * --impl reference: the reference's own CPU implementation (oracle/_ref,
-    ElasticOperator<double>, all host threads) on the same workload.
+    ElasticOperator<double>, all host threads) on the same cfg2 workload,
+    timed with runner.cpp:84-121's protocol (blocks of 1 apply, >= 1 s per
+    measurement, average of the best 3).
 """
 from __future__ import annotations
 
@@ -34,8 +42,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tangent-operator apply DoFs/s"
 UNIT = "DoF/s"
-N_EL, P = 32, 3
+# headline: BASELINE configs[2] (scaled-noise variant), per GPU
+C2_N, C2_P, C2_MODEL = 64, 4, "inh"
+C2_MU, C2_KAPPA, C2_SHEAR, C2_AMP = 1.0, 1000.0, 0.1, 0.1
+C2_NOISE = 1e-3 * 8.0 / C2_N
+# cfg1 sweep: BASELINE configs[1]
+C1_N, C1_P = 32, 3
 MU, LAM = 1.0, 10.0
+P = C1_P
 
 # Algorithmic work per element: reference sweep structure
 # (8 forward + 9 transpose sweeps per component, u_k swept again when the
@@ -68,14 +82,6 @@ def bytes_per_apply(strategy, prec, ndofs, nel, n=P + 1, model="cnh"):
     nq = nel * n ** 3
     k = 3 if strategy in ("none", "scalar") else 2
     return ledger_qp_bytes(model, strategy) * s / 8 * nq + k * s * ndofs
-
-
-def read_peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
-    except OSError:
-        return {}
 
 
 class ClockSampler:
@@ -130,6 +136,44 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def nominal_fma_tflops(prec, sm_mhz=None, sms=148):
+    """Nominal FMA-pipe peak: 64 FP64 / 128 FP32 FMA lanes per SM per clock
+    (2 flops each) at the maximum SM clock."""
+    mhz = sm_mhz or read_peaks().get("sm_max_mhz", 1965.0)
+    return sms * (64 if prec == 64 else 128) * 2 * mhz * 1e6 / 1e12
+
+
+def headline_config(world):
+    """The config dict of the headline line, identical in both arms."""
+    return {"workload": "cfg2 (BASELINE configs[2], scaled-noise variant): 64^3 Q4 per GPU, curved map "
+                        "x'=x+0.1 sin(2 pi y) e_x with per-qp J0, iNH mu=1 kappa=1000, u0 amp 0.1 at pre-map "
+                        "coords + noise 1e-3*8/64, v U[-1,1]; fp64, strategy none",
+            "global_mesh": [C2_N, C2_N, C2_N * world], "degree": C2_P, "ndofs": 3 * (C2_N * C2_P + 1) ** 2 * (
+                C2_N * world * C2_P + 1),
+            "l2": "flushed (256 MiB write) before every timed apply; inputs (x 407 MB) exceed L2",
+            "parallelism": f"z-slab x{world}"}
+
+
+def c2_material(G):
+    return G.MaterialParams(mu=C2_MU, lam=LAM, kappa_b=C2_KAPPA)
+
+
+def c2_inputs(part):
+    from paper_2408_12479_b200 import inputs as I
+    u0 = I.make_u0_planes(part.nx, part.ny, part.nz, part.p, part.c0, part.c1, amp=C2_AMP, noise=C2_NOISE,
+                          faces=part.faces, extent=(1.0, 1.0, float(part.world)))
+    v = I.make_v_planes(part.nx, part.ny, part.nz, part.p, part.c0, part.c1)
+    return u0, v
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -138,187 +182,253 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
+# the reference's CPU path (oracle/_ref = the unmodified reference, built from
+# its sources by oracle/Makefile)
+def ref_cfg2_operator(threads, precision=64):
+    """ElasticOperator<double> of the reference on the cfg2 level: build_cube
+    lattice + the shear map, J0 recomputed by the reference's own sweeps
+    (SURVEY §8(c) gap 1), linearized at the same seeded u0."""
+    from oracle import refbind as R
+    from paper_2408_12479_b200 import workloads as W
+    L0 = R.RefLevel(1, 6, C2_P, 0.0, 1)
+    c = L0.coords().reshape(-1, 3)
+    c[:, 0] += C2_SHEAR * np.sin(2.0 * np.pi * c[:, 1])
+    del L0
+    L = R.RefLevel(1, 6, C2_P, 0.0, 1, coords=c.reshape(-1))
+    del c
+    w = W.cfg2()
+    op = R.RefOperator(L, C2_MODEL, R.material_params(mu=C2_MU, lam=LAM, kappa=C2_KAPPA), "none", precision,
+                       threads=threads)
+    t0 = time.perf_counter()
+    op.update_linearization(w.u0())
+    t_lin = time.perf_counter() - t0
+    return L, op, w.v(), t_lin
+
+
+def runner_protocol(fn, measurements, min_seconds=1.0, average_best=3):
+    """runner.cpp:84-121: after one warm-up call (done by the caller), each
+    measurement repeats blocks of `fn` until min_seconds have passed (blocks
+    of 1 apply: repetitions_block=1, SURVEY §8(d) for cfg2-4); the best
+    `average_best` measurements (by rate) are averaged."""
+    runs = []
+    for _ in range(measurements):
+        reps, t0 = 0, time.perf_counter()
+        el = 0.0
+        while el < min_seconds:
+            fn()
+            reps += 1
+            el = time.perf_counter() - t0
+        runs.append((reps, el))
+    runs.sort(key=lambda r: -r[0] / r[1])
+    keep = runs[:min(average_best, len(runs))]
+    reps = sum(r for r, _ in keep)
+    secs = sum(s for _, s in keep)
+    return reps, secs, runs
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU ElasticOperator<double> (oracle/_ref),
-    same workload, all host threads; bounded sample per step."""
+    """--impl reference: the reference's CPU ElasticOperator<double>
+    (oracle/_ref), same cfg2 workload and config, all host threads,
+    runner.cpp's protocol with blocks of 1 apply."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     from oracle import refbind as R
-    from paper_2408_12479_b200 import inputs as I
     threads = os.cpu_count() or 1
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libemfref.so not built"}))
         return
-    L = R.RefLevel(1, 5, P, 0.0, 1)
-    u0 = I.make_u0(N_EL, N_EL, N_EL, P)
-    v = I.make_v(L.ndofs)
-    op = R.RefOperator(L, "cnh", R.material_params(mu=MU, lam=LAM), "none", 64, threads=threads)
-    t0 = time.perf_counter()
-    op.update_linearization(u0)
-    t_lin = time.perf_counter() - t0
-    for _ in range(args.warmup):
+    L, op, v, t_lin = ref_cfg2_operator(threads)
+    for _ in range(max(1, min(args.warmup, 1))):
         op.apply(v)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        op.apply(v)
-        times.append(time.perf_counter() - t0)
-    dt = sum(times) / len(times)
-    val = L.ndofs / dt
+    meas = max(3, min(args.steps, 10))
+    reps, secs, runs = runner_protocol(lambda: op.apply(v), meas)
+    val = L.ndofs * reps / secs
+    dt = secs / reps
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, SURVEY §8(c))",
-        "config": {"workload": "cfg1: 32^3 affine cube Q3 cNH mu=1 lambda=10, fp64, strategy none (reference CPU)",
-                   "ndofs": L.ndofs, "threads": threads, "update_linearization_s": t_lin},
+        "config": headline_config(world),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{args.steps} applies of the full cfg1 operator (ElasticOperator<double>)"},
+                         "sample": f"{meas} measurements of >=1 s of full cfg2 applies (64^3 Q4, {L.ndofs} DoFs; "
+                                   f"the reference's HexMesh is one cube, so at N>1 this is the per-GPU slab "
+                                   f"shape), best 3 averaged (runner.cpp:84-121, blocks of 1)"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference": {"update_linearization_s": t_lin, "threads": threads,
+                      "runs": [[r, s] for r, s in runs]},
     }))
 
 
 def cpu_baseline_sample(seconds=10.0):
     """Reference CPU path on the GPU box's host (rank 0, N=1): a bounded sample
-    of the same workload (oracle/_ref, all threads; falls back to the C port)."""
-    from paper_2408_12479_b200 import inputs as I
+    of the same cfg2 workload (oracle/_ref, all threads; the C port if the
+    reference is not built)."""
     threads = os.cpu_count() or 1
-    u0 = I.make_u0(N_EL, N_EL, N_EL, P)
-    v = I.make_v(u0.size)
     try:
         from oracle import refbind as R
         if not R.available():
             raise OSError
-        L = R.RefLevel(1, 5, P, 0.0, 1)
-        op = R.RefOperator(L, "cnh", R.material_params(mu=MU, lam=LAM), "none", 64, threads=threads)
+        L, op, v, t_lin = ref_cfg2_operator(threads)
+        n = L.ndofs
         kind = "reference"
     except OSError:
         from oracle import orcbind as O
-        op = O.OracleOperator(N_EL, N_EL, N_EL, P, model="cnh",
-                              params=np.array([MU, LAM, 1000, 2, 5, 3.62, 34.3, 0.7, 1, 0, 0, 0, 1, 0, 0, 0, 1]))
+        from paper_2408_12479_b200 import workloads as W
+        from paper_2408_12479_b200 import inputs as I
+        w = W.cfg2()
+        X, Y, Z = I.lattice_positions(C2_N, C2_N, C2_N, C2_P)
+        X = X + C2_SHEAR * np.sin(2.0 * np.pi * Y)
+        coords = np.stack([X, Y, Z], 1).ravel()
+        op = O.OracleOperator(C2_N, C2_N, C2_N, C2_P, coords, 1, "inh",
+                              np.array([C2_MU, LAM, C2_KAPPA, 2, 5, 3.62, 34.3, 0.7, 1, 0, 0, 0, 1, 0, 0, 0, 1]))
+        t0 = time.perf_counter()
+        op.update_linearization(w.u0())
+        t_lin = time.perf_counter() - t0
+        v = w.v()
+        n = v.size
         kind = "port"
-    op.update_linearization(u0)
+        threads = 1
     op.apply(v)
-    n, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < seconds or n < 2:
+    k, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds or k < 2:
         op.apply(v)
-        n += 1
-    dt = (time.perf_counter() - t0) / n
-    return {"value": u0.size / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{n} full cfg1 applies (ElasticOperator<double>, none, {threads} threads), "
-                      f"{dt * 1e3:.0f} ms each"}
+        k += 1
+    dt = (time.perf_counter() - t0) / k
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{k} full cfg2 applies (64^3 Q4 iNH, {n} DoFs, ElasticOperator<double>, none, "
+                      f"{threads} threads), {dt * 1e3:.0f} ms each; update_linearization {t_lin:.1f} s (serial)"}
 
 
 # ---------------------------------------------------------------------------
-def run_gpu(args):
+def time_variant(G, args, lev, part, sop_cls, u0, v, model, params, prec, strat, flush, world, dist, ev_elem=True,
+                 keep=False):
+    """Times one operator variant: `steps` whole applies (L2 flushed before
+    each, CUDA events on the stream), then the element kernel alone (N=1)."""
     import torch
-    import torch.distributed as dist
-    from paper_2408_12479_b200 import emfgpu as G
-    from paper_2408_12479_b200 import inputs as I
-    from paper_2408_12479_b200.slab import SlabPartition, SlabOperator
-
-    world, rank, local = dist_env()
-    if world != args.gpus:
-        world = max(world, 1)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    part = SlabPartition(N_EL, N_EL, N_EL * world, P, world, rank, faces=1)
-    params = G.MaterialParams(mu=MU, lam=LAM)
-    # global seeded inputs restricted to this slab's node planes
-    u0_g = I.make_u0(N_EL, N_EL, N_EL * world, P, extent=(1.0, 1.0, float(world)))
-    v_g = I.make_v(u0_g.size)
-    u0 = u0_g[part.dof_slice]
-    v = v_g[part.dof_slice]
-    del u0_g
-    lev = part.make_level(extent=(1.0, 1.0, float(world)), device=local)
-    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    spatial = strat.startswith("spatial_")
+    op = G.ElasticOperator(lev, model, params, strat.replace("spatial_", ""), prec,
+                           domain="spatial" if spatial else "material")
+    op.update_linearization(u0)
+    dt = torch.float64 if prec == 64 else torch.float32
+    sop = sop_cls(op, part, dt)
+    x = torch.tensor(v, dtype=dt, device="cuda")
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    variants = {}
-    head = None
-    launches = 0
-    order = [(64, "none"), (64, "cachedF"), (64, "scalar"), (64, "tensor"),
-             (32, "none"), (32, "cachedF"), (32, "scalar"), (32, "tensor"),
-             (64, "spatial_none"), (64, "spatial_tensor"), (32, "spatial_none"), (32, "spatial_tensor")]
+    for _ in range(args.warmup):
+        sop.apply(x, y)
+    barrier()
+    tot = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        # one GPU: the whole apply in one call (element kernel + node kernel
+        # as its programmatic dependent); the element kernel is timed alone below
+        sop.apply(x, y, ev_mid=None if world == 1 else ev[1])
+        ev[2].record(stream)
+        tot.append(ev)
+    barrier()
+    ms = [e[0].elapsed_time(e[2]) for e in tot]
+    if world == 1 and ev_elem:
+        el = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(stream)
+            op.apply_elements(x, 0, part.nz_local)
+            ev[1].record(stream)
+            el.append(ev)
+        barrier()
+        ms_el = [e[0].elapsed_time(e[1]) for e in el]
+    else:
+        ms_el = [e[0].elapsed_time(e[1]) for e in tot]
+    t = torch.tensor([sum(ms) / len(ms), sum(ms_el) / len(ms_el), min(ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step, ms_elem, ms_min = t.tolist()
+    rec = {"dofs_per_s": part.global_dofs / (ms_step * 1e-3), "ms_per_apply": ms_step, "ms_min": ms_min,
+           "ms_element_kernel": ms_elem}
+    kept = (op, sop, x, y) if keep else None
+    if not keep:
+        del op, sop, x, y
+    return rec, kept
+
+
+def add_roofline(rec, strat, prec, nel, ndofs, n, model, peaks):
+    """Per-variant roofline fields of the element kernel: algorithmic flops
+     against the nominal and the measured FMA peaks, ledger
+    bytes against the measured HBM copy bandwidth."""
+    t = rec["ms_element_kernel"] * 1e-3
+    st = strat.replace("spatial_", "")
+    if not strat.startswith("spatial_"):
+        fl = flops_per_element(st, n, model) * nel
+        rec["element_kernel_tflops"] = fl / t / 1e12
+        rec["fma_frac_nominal"] = rec["element_kernel_tflops"] / peaks[f"nominal{prec}"]
+        rec["fma_frac_measured"] = rec["element_kernel_tflops"] / peaks[f"measured{prec}"]
+        by = bytes_per_apply(st, prec, ndofs, nel, n, model)
+    else:
+        k = 3 if st in ("none", "scalar") else 2
+        by = ledger_qp_bytes(model, st, "spatial") * (prec // 8) / 8 * nel * n ** 3 + k * (prec // 8) * ndofs
+    rec["element_kernel_gbs"] = by / t / 1e9
+    rec["hbm_frac_yardstick"] = rec["element_kernel_gbs"] / peaks["hbm"]
+    return rec
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2408_12479_b200 import emfgpu as G
+    from paper_2408_12479_b200.slab import SlabPartition, SlabOperator
+
+    world, rank, local = dist_env()
+    world = max(world, 1)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    part = SlabPartition(C2_N, C2_N, C2_N * world, C2_P, world, rank, faces=1)
+    params = c2_material(G)
+    u0, v = c2_inputs(part)
+    lev = part.make_level(extent=(1.0, 1.0, float(world)), device=local, map="shear_x", map_param=(C2_SHEAR,))
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    peaks_file = read_peaks()
+    hbm = peaks_file.get("hbm_gbs", 6650.0)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.__enter__()
-    for prec, strat in order:
-        spatial = strat.startswith("spatial_")
-        op = G.ElasticOperator(lev, "cnh", params, strat.replace("spatial_", ""), prec,
-                               domain="spatial" if spatial else "material")
-        op.update_linearization(u0)
-        dt = torch.float64 if prec == 64 else torch.float32
-        sop = SlabOperator(op, part, dt)
-        x = torch.tensor(v, dtype=dt, device="cuda")
-        y = torch.empty_like(x)
-        stream = torch.cuda.current_stream()
-        for _ in range(args.warmup):
-            sop.apply(x, y)
-        barrier()
-        tot, elem_ms = [], []
-        for _ in range(args.steps):
-            flush.fill_(1.0)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            ev[0].record(stream)
-            # one GPU: the whole apply in one call (no event between the
-            # element and node kernels); the element kernel is timed alone below
-            sop.apply(x, y, ev_mid=None if world == 1 else ev[1])
-            ev[2].record(stream)
-            tot.append(ev)
-        barrier()
-        ms = [e[0].elapsed_time(e[2]) for e in tot]
-        if world == 1:
-            el = []
-            for _ in range(args.steps):
-                flush.fill_(1.0)
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                ev[0].record(stream)
-                op.apply_elements(x, 0, part.nz_local)
-                ev[1].record(stream)
-                el.append(ev)
-            barrier()
-            ms_el = [e[0].elapsed_time(e[1]) for e in el]
-        else:
-            ms_el = [e[0].elapsed_time(e[1]) for e in tot]
-        t = torch.tensor([sum(ms) / len(ms), sum(ms_el) / len(ms_el)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, ms_elem = t.tolist()
-        rec = {"dofs_per_s": part.global_dofs / (ms_step * 1e-3), "ms_per_apply": ms_step,
-               "ms_element_kernel": ms_elem}
-        if strat in ("none", "scalar", "tensor", "cachedF"):
-            fl = flops_per_element(strat) * part.nel_local
-            by = bytes_per_apply(strat, prec, lev.n_dofs, part.nel_local)
-            rec["element_kernel_tflops"] = fl / (ms_elem * 1e-3) / 1e12
-            rec["element_kernel_gbs"] = by / (ms_elem * 1e-3) / 1e9
-        else:  # spatial: the reference ledger's spatial rows (J0, J_t, 1/J, caches), vectors per DoF
-            st = strat.replace("spatial_", "")
-            k = 3 if st in ("none", "scalar") else 2
-            by = ledger_qp_bytes("cnh", st, "spatial") * (prec // 8) / 8 * part.nel_local * (P + 1) ** 3 + \
-                k * (prec // 8) * lev.n_dofs
-            rec["element_kernel_gbs"] = by / (ms_elem * 1e-3) / 1e9
-        variants[f"fp{prec}_{strat}"] = rec
-        if (prec, strat) == (64, "none"):
-            head = (op, sop, x, y, rec)
-            launches = sop.launches_per_apply * args.steps
-        else:
-            del op, sop
+    variants = {}
+    rec, kept = time_variant(G, args, lev, part, SlabOperator, u0, v, C2_MODEL, params, 64, "none", flush, world,
+                             dist, keep=True)
     if sampler:
         sampler.__exit__()
-    op, sop, x, y, rec = head
+    variants["fp64_none"] = rec
+    op, sop, x, y = kept
+    launches = sop.launches_per_apply * args.steps
 
     # e2e through the public host-vector API (pinned host buffers)
     hx = torch.tensor(v, dtype=torch.float64).pin_memory()
     hy = torch.empty_like(hx).pin_memory()
-    e2e_ms = None
     if world == 1:
-        import ctypes
         for _ in range(max(1, args.warmup)):
             G.lib().emfgpu_op_apply_host(op.h, hx.data_ptr(), hy.data_ptr())
         ts = []
@@ -330,12 +440,8 @@ def run_gpu(args):
             ts.append(time.perf_counter() - t0)
             assert st == 0
         e2e_ms = 1e3 * sum(ts) / len(ts)
-        e2e = {"value": lev.n_dofs / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hx.numel() * 8,
-               "d2h_bytes_per_step": hy.numel() * 8, "ms_per_step": e2e_ms,
-               "call": "emfgpu_op_apply_host (pinned host vectors)"}
+        call = "emfgpu_op_apply_host (pinned host vectors; H2D, apply, D2H pipelined in z-chunks)"
     else:
-        # multi-GPU e2e: each rank copies its slab of v in and its slab of y out
-        stream = torch.cuda.current_stream()
         ts = []
         dx = torch.empty_like(x)
         for _ in range(args.steps):
@@ -349,54 +455,84 @@ def run_gpu(args):
         tt = torch.tensor([sum(ts) / len(ts)], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item() * 1e3
-        e2e = {"value": part.global_dofs / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hx.numel() * 8,
-               "d2h_bytes_per_step": hy.numel() * 8, "ms_per_step": e2e_ms,
-               "call": "SlabOperator.apply with pinned H2D/D2H per rank"}
+        call = "SlabOperator.apply with pinned H2D/D2H per rank"
+    e2e = {"value": part.global_dofs / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hx.numel() * 8,
+           "d2h_bytes_per_step": hy.numel() * 8, "ms_per_step": e2e_ms, "call": call}
+    # evaluate_residual on the same operator (runner.cpp:85-105 times it too)
+    res_rec = None
+    if world == 1:
+        du = torch.tensor(u0, dtype=torch.float64, device="cuda")
+        r = torch.empty_like(du)
+        for _ in range(2):
+            op.evaluate_residual_device(du, r)
+        torch.cuda.synchronize()
+        evs = []
+        for _ in range(max(3, args.steps // 2)):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            op.evaluate_residual_device(du, r)
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        ms_r = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+        res_rec = {"dofs_per_s": lev.n_dofs / (ms_r * 1e-3), "ms": ms_r, "strategy": "none (fp64)"}
+        del du, r
+    del op, sop, x, y, kept
+
+    for prec, strat in ((64, "tensor"), (64, "scalar"), (64, "cachedF"), (32, "none"), (32, "tensor")):
+        rec, _ = time_variant(G, args, lev, part, SlabOperator, u0, v, C2_MODEL, params, prec, strat, flush, world,
+                              dist)
+        variants[f"fp{prec}_{strat}"] = rec
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    peaks = read_peaks()
-    fp64_peak = G.fma_peak_tflops(64, 0.5)
-    fp32_peak = G.fma_peak_tflops(32, 0.5)
-    hbm = peaks.get("hbm_gbs", 6650.0)
+    fp64_meas = G.fma_peak_tflops(64, 0.5)
+    fp32_meas = G.fma_peak_tflops(32, 0.5)
+    clocks = sampler.summary() if sampler else None
+    peaks = {"nominal64": nominal_fma_tflops(64), "nominal32": nominal_fma_tflops(32), "measured64": fp64_meas,
+             "measured32": fp32_meas, "hbm": hbm}
     for k, r in variants.items():
-        pk = fp64_peak if k.startswith("fp64") else fp32_peak
-        if "element_kernel_tflops" in r:
-            r["fma_frac"] = r["element_kernel_tflops"] / pk
-        r["hbm_frac"] = r["element_kernel_gbs"] / hbm
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("fp64_none_bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
+        prec, strat = (64 if k.startswith("fp64") else 32), k.split("_", 1)[1]
+        add_roofline(r, strat, prec, part.nel_local, lev.n_dofs, C2_P + 1, C2_MODEL, peaks)
+    traffic = load_traffic()
+    head = variants["fp64_none"]
+    tr = traffic.get("cfg2_fp64_none")
+    fl = flops_per_element("none", C2_P + 1, C2_MODEL) * part.nel_local
     line = {
-        "metric": METRIC, "value": rec["dofs_per_s"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": rec["ms_per_apply"], "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": head["dofs_per_s"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_apply"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded splitmix64 u0/v (SURVEY §8(c)), cfg1 mesh generated on device",
-        "config": {"workload": "cfg1: 32^3 affine unit cube per GPU (z-slabs), Q3, cNH mu=1 lambda=10, "
-                               "headline fp64 strategy none",
-                   "global_mesh": [N_EL, N_EL, N_EL * world], "ndofs": part.global_dofs,
-                   "l2": "flushed (256 MiB write) before every timed apply", "parallelism": f"z-slab x{world}"},
-        "roofline": {"bound": "fp64_fma", "achieved": rec["element_kernel_tflops"], "peak": fp64_peak,
-                     "unit": "TFLOP/s", "frac": rec["element_kernel_tflops"] / fp64_peak, "traffic": traffic,
-                     "kernel": "apply_v2_kernel<double,3,CNH,S_NONE,CART> (element phase)",
-                     "peak_source": "measured FMA loop on this GPU (emfgpu_bench_fma_peak)",
-                     "flops_per_launch": flops_per_element("none") * part.nel_local,
-                     "hbm_achieved_gbs": rec["element_kernel_gbs"], "hbm_peak_gbs": hbm,
-                     "hbm_frac": rec["element_kernel_gbs"] / hbm},
-        "fma_peaks_tflops": {"fp64": fp64_peak, "fp32": fp32_peak},
+        "data": "synthetic: seeded splitmix64 u0/v (SURVEY §8(c)), mesh and J0 generated for each slab",
+        "config": headline_config(world),
+        "roofline": {"bound": "fp64_fma", "achieved": head["element_kernel_tflops"], "peak": peaks["nominal64"],
+                     "unit": "TFLOP/s", "frac": head["element_kernel_tflops"] / peaks["nominal64"],
+                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                     "kernel": "apply_v2_kernel<double,4,INH,S_NONE,curved> (element phase)",
+                     "peak_source": "nominal FP64: 148 SMs x 64 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json "
+                                    "has no FP64 entry)",
+                     "peak_measured_fma_loop": fp64_meas,
+                     "frac_of_measured_fma_loop": head["element_kernel_tflops"] / fp64_meas,
+                     "flops_per_launch": fl, "flops_per_element": flops_per_element("none", C2_P + 1, C2_MODEL),
+                     "elements_per_launch": part.nel_local,
+                     "hbm_achieved_gbs_yardstick": head["element_kernel_gbs"], "hbm_peak_gbs": hbm,
+                     "traffic_source": tr.get("source") if tr else None,
+                     "traffic_frac_of_hbm": (tr["dram_bytes_per_launch"] / (head["ms_element_kernel"] * 1e-3) / 1e9
+                                             / hbm) if tr else None},
+        "fma_peaks_tflops": {"fp64_nominal": peaks["nominal64"], "fp32_nominal": peaks["nominal32"],
+                             "fp64_measured_fma_loop": fp64_meas, "fp32_measured_fma_loop": fp32_meas},
         "variants": variants,
         "e2e": e2e,
         "gpu_launches": launches,
-        "clocks": sampler.summary() if sampler else None,
+        "clocks": clocks,
     }
+    if res_rec:
+        line["residual"] = res_rec
     if world == 1 and not args.no_extra:
-        line["workloads"] = run_extra_workloads(args, flush, fp64_peak, hbm)
+        line["variants_cfg1"] = run_cfg1_sweep(args, flush, peaks)
+        line["workloads"] = run_extra_workloads(args, flush, peaks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
     print(json.dumps(line))
@@ -404,9 +540,32 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def run_extra_workloads(args, flush, fp64_peak, hbm):
-    """BASELINE configs 2 and 4 on one GPU (variants documented in
-    paper_2408_12479_b200/workloads.py).  Reported beside the headline."""
+def run_cfg1_sweep(args, flush, peaks):
+    """BASELINE configs[1] (32^3 affine cube Q3 cNH): fp64/fp32 x
+    none/cachedF/scalar/tensor + the spatial domain, one GPU."""
+    from paper_2408_12479_b200 import emfgpu as G
+    from paper_2408_12479_b200 import inputs as I
+    from paper_2408_12479_b200.slab import SlabPartition, SlabOperator
+    part = SlabPartition(C1_N, C1_N, C1_N, C1_P, 1, 0, faces=1)
+    lev = part.make_level()
+    u0 = I.make_u0(C1_N, C1_N, C1_N, C1_P)
+    v = I.make_v(u0.size)
+    params = G.MaterialParams(mu=MU, lam=LAM)
+    out = {}
+    order = [(64, "none"), (64, "cachedF"), (64, "scalar"), (64, "tensor"),
+             (32, "none"), (32, "cachedF"), (32, "scalar"), (32, "tensor"),
+             (64, "spatial_none"), (64, "spatial_tensor"), (32, "spatial_none"), (32, "spatial_tensor")]
+    for prec, strat in order:
+        rec, _ = time_variant(G, args, lev, part, SlabOperator, u0, v, "cnh", params, prec, strat, flush, 1, None)
+        out[f"fp{prec}_{strat}"] = add_roofline(rec, strat, prec, part.nel_local, lev.n_dofs, C1_P + 1, "cnh",
+                                                peaks)
+    return out
+
+
+def run_extra_workloads(args, flush, peaks):
+    """BASELINE configs 3 and 4 on one GPU (variants documented in
+    paper_2408_12479_b200/workloads.py), and the literal cfg2/cfg4 inputs'
+    rejection points."""
     import torch
     from paper_2408_12479_b200 import emfgpu as G
     from paper_2408_12479_b200 import workloads as W
@@ -435,6 +594,12 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
     torch.cuda.synchronize()
     t_solve = time.perf_counter() - t0
     smp.__exit__()
+    ref4 = None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "cfg4_full.json")) as f:
+            ref4 = json.load(f)
+    except (OSError, ValueError):
+        pass
     out["cfg4_wellposed"] = {"ndofs": lev.n_dofs, "levels": mg.levels(), "cg_iterations": its,
                              "final_rel_residual": float(hist[-1]), "solve_s": t_solve,
                              "ms_per_iteration": 1e3 * t_solve / max(its, 1), "setup_s": t_setup,
@@ -442,8 +607,26 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
                              "settings": "iNH kappa/mu=50, u0=0, affine 48^3 Q4; fp64 PCG rtol 1e-8; fp32 V-cycle "
                                          "Q4->Q2->Q1->24^3->12^3->6^3, Chebyshev-Jacobi degree 5, dense coarse "
                                          "solve (1029 DoFs < coarse_direct_limit 2000, as the reference)"}
+    if ref4:
+        out["cfg4_wellposed"].update({
+            "reference_iterations": ref4["iterations"], "reference_solve_s": ref4["solve_s"],
+            "reference_setup_s": ref4["setup_s"], "reference_threads": ref4["threads"],
+            "reference_note": "the reference's MgHierarchy<float> + fp64 PCG (oracle/ref_driver.cpp "
+                              "ref_pcg_solve) run once in the build container (tests/golden/cfg4_full.json)"})
+        out["cfg4_literal"] = ref4.get("literal")
     del op, mg, lev, b, x
-    # cfg2: literal inputs must be rejected like the reference does
+    # cfg4 literal: rejected like the reference
+    w = W.cfg4(wellposed=False)
+    lev = w.level()
+    op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
+    try:
+        op.update_linearization(w.u0())
+        lit = {"admissible": True}
+    except G.NonPositiveJacobian as ex:
+        lit = {"admissible": False, "first_bad_element": ex.element, "first_bad_qpoint": ex.qpoint}
+    out["cfg4_literal_gpu"] = lit
+    del op, lev
+    # cfg2 literal: rejected like the reference (first (e, q) = (1, 46))
     w = W.cfg2(literal=True)
     lev = w.level()
     op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
@@ -452,42 +635,7 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
         out["cfg2_literal"] = {"admissible": True}
     except G.NonPositiveJacobian as ex:
         out["cfg2_literal"] = {"admissible": False, "first_bad_element": ex.element, "first_bad_qpoint": ex.qpoint}
-    del op
-    w = W.cfg2(literal=False)
-    u0, v = w.u0(), w.v()
-    rec2 = {"mesh": "64^3 Q4, x' = x + 0.1 sin(2 pi y) e_x (curved, per-qp J0)", "ndofs": lev.n_dofs,
-            "noise": w.noise, "affine": lev.affine}
-    for prec, strat in ((64, "none"), (64, "tensor"), (32, "none")):
-        op = G.ElasticOperator(lev, w.model, w.material(), strat, prec)
-        op.update_linearization(u0)
-        dt = torch.float64 if prec == 64 else torch.float32
-        x = torch.tensor(v, dtype=dt, device="cuda")
-        y = torch.empty_like(x)
-        for _ in range(3):
-            op.apply_tangent_device(x, y)
-        ms = []
-        for _ in range(max(3, args.steps // 4)):
-            flush.fill_(1.0)
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record()
-            op.apply_elements(x, 0, lev.nz)
-            e1.record()
-            op.apply_nodes(x, y, 0, lev.nz * lev.p)
-            e2.record()
-            ms.append((e0, e1, e2))
-        torch.cuda.synchronize()
-        t_all = sum(a.elapsed_time(c) for a, b, c in ms) / len(ms)
-        t_el = sum(a.elapsed_time(b) for a, b, c in ms) / len(ms)
-        fl = flops_per_element(strat, 5, "inh") * lev.n_elements
-        by = bytes_per_apply(strat, prec, lev.n_dofs, lev.n_elements, 5, "inh")
-        rec2[f"fp{prec}_{strat}"] = {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all,
-                                     "ms_element_kernel": t_el,
-                                     "fma_frac": fl / (t_el * 1e-3) / 1e12 / (fp64_peak if prec == 64 else
-                                                                                2 * fp64_peak),
-                                     "hbm_frac": by / (t_el * 1e-3) / 1e9 / hbm}
-        del op, x, y
-    out["cfg2"] = rec2
-    del lev
+    del op, lev
     # cfg3: fibre tube with per-qp cylindrical frames, tensor strategy
     w = W.cfg3()
     lev = w.level()
@@ -518,9 +666,10 @@ def run_extra_workloads(args, flush, fp64_peak, hbm):
         t_all = sum(a.elapsed_time(c) for a, b, c in ms) / len(ms)
         t_el = sum(a.elapsed_time(b) for a, b, c in ms) / len(ms)
         nq = lev.n_elements * 64
-        by = (ledger_qp_bytes("fiber", "tensor") + 96) * (prec // 8) / 8 * nq + 2 * (prec // 8) * lev.n_dofs  # + per-qp H4/H6
+        by = (ledger_qp_bytes("fiber", "tensor") + 96) * (prec // 8) / 8 * nq + 2 * (prec // 8) * lev.n_dofs
         rec3[f"fp{prec}_tensor"] = {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all,
-                                    "ms_element_kernel": t_el, "hbm_frac": by / (t_el * 1e-3) / 1e9 / hbm}
+                                    "ms_element_kernel": t_el, "hbm_frac_yardstick": by / (t_el * 1e-3) / 1e9 /
+                                    peaks["hbm"]}
         del op, x, y
     out["cfg3"] = rec3
     del lev
@@ -535,7 +684,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 / cfg4 workloads")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 sweep and the cfg3 / cfg4 workloads")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -21,9 +21,10 @@ M1 = np.uint64(0xBF58476D1CE4E5B9)
 M2 = np.uint64(0x94D049BB133111EB)
 
 
-def splitmix64_stream(seed: int, n: int) -> np.ndarray:
-    """The first n outputs of splitmix64 started at ``state = seed``."""
-    k = np.arange(1, n + 1, dtype=np.uint64)
+def splitmix64_stream(seed: int, n: int, start: int = 0) -> np.ndarray:
+    """Outputs start .. start+n-1 of splitmix64 started at ``state = seed``
+    (output i is a pure function of i: state_i = seed + (i+1) * gamma)."""
+    k = np.arange(start + 1, start + n + 1, dtype=np.uint64)
     with np.errstate(over="ignore"):
         z = np.uint64(seed) + k * GAMMA
         z = (z ^ (z >> np.uint64(30))) * M1
@@ -32,9 +33,9 @@ def splitmix64_stream(seed: int, n: int) -> np.ndarray:
     return z
 
 
-def uniform01(seed: int, n: int) -> np.ndarray:
+def uniform01(seed: int, n: int, start: int = 0) -> np.ndarray:
     """solver.hpp:217-219: (splitmix64(state) >> 11) * 2^-53."""
-    return (splitmix64_stream(seed, n) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (splitmix64_stream(seed, n, start) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
 
 def gauss_lobatto(n: int) -> np.ndarray:
@@ -131,3 +132,31 @@ def open_to_periodic(v: np.ndarray, nx, ny, nz, p) -> np.ndarray:
     a = v.reshape(mz, my + 1, mx, -1).copy()
     a[:, 0] += a[:, my]
     return a[:, :my].reshape(-1)
+
+
+def make_u0_planes(nx, ny, nz, p, c0, c1, amp=0.05, noise=1e-3, seed=0, faces=1, extent=(1.0, 1.0, 1.0)):
+    """Node planes c0..c1 (inclusive) of make_u0(nx, ny, nz, p, ...), generated
+    without the rest of the global vector (z slabs of weak-scaled meshes)."""
+    ax = lattice_axis(nx, p, extent[0])
+    ay = lattice_axis(ny, p, extent[1])
+    az = lattice_axis(nz, p, extent[2])[c0:c1 + 1]
+    Z, Y, X = np.meshgrid(az, ay, ax, indexing="ij")
+    s = amp * np.sin(np.pi * X.ravel()) * np.sin(np.pi * Y.ravel()) * np.sin(np.pi * Z.ravel())
+    u = np.repeat(s, 3)
+    plane = 3 * (nx * p + 1) * (ny * p + 1)
+    if noise != 0.0:
+        u = u + (-noise + 2.0 * noise * uniform01(seed, u.size, c0 * plane))
+    mz = nz * p + 1
+    mask = dirichlet_mask(nx, ny, nz, p, faces & 0b001111)[: u.size]
+    if faces & 16 and c0 == 0:
+        mask[:plane] = True
+    if faces & 32 and c1 == mz - 1:
+        mask[-plane:] = True
+    u[mask] = 0.0
+    return u
+
+
+def make_v_planes(nx, ny, nz, p, c0, c1, seed: int = 1) -> np.ndarray:
+    """Node planes c0..c1 of make_v(global n_dofs, seed)."""
+    plane = 3 * (nx * p + 1) * (ny * p + 1)
+    return -1.0 + 2.0 * uniform01(seed, (c1 - c0 + 1) * plane, c0 * plane)

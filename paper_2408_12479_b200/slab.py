@@ -69,9 +69,21 @@ class SlabPartition:
         Z, Y, X = np.meshgrid(az, ay, ax, indexing="ij")
         return np.stack([X.ravel(), Y.ravel(), Z.ravel()], 1).ravel()
 
-    def make_level(self, extent=(1.0, 1.0, 1.0), device=0):
+    def make_level(self, extent=(1.0, 1.0, 1.0), device=0, map="reference", map_param=(0.0,)):
+        """This slab's FeLevel.  One rank: the level generator itself (the
+        map applied on the device-side generator, bitwise the workloads'
+        levels).  Several ranks: the global pre-map lattice restricted to the
+        slab's node planes, with the z-independent maps applied here."""
         from .emfgpu import FeLevel
-        return FeLevel(self.nx, self.ny, self.nz_local, p=self.p, coords=self.local_coords(extent),
+        if self.world == 1:
+            return FeLevel(self.nx, self.ny, self.nz, p=self.p, extent=extent, map=map, map_param=map_param,
+                           dirichlet_faces=self.local_faces, device=device)
+        c = self.local_coords(extent).reshape(-1, 3)
+        if map == "shear_x":  # BASELINE cfg2: x' = x + a sin(2 pi y) e_x
+            c[:, 0] += map_param[0] * np.sin(2.0 * np.pi * c[:, 1])
+        elif map != "reference" or map_param[0] != 0.0:
+            raise ValueError(f"slab levels support the shear_x map and the plain lattice, not {map}")
+        return FeLevel(self.nx, self.ny, self.nz_local, p=self.p, coords=c.reshape(-1),
                        dirichlet_faces=self.local_faces, device=device, z_offset=self.k0)
 
 

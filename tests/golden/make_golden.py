@@ -209,6 +209,158 @@ def stability():
     print("stability", err.shape, int(inv.sum()))
 
 
+def _shear_coords(L: "R.RefLevel", amp=0.1):
+    """BASELINE cfg2 map x' = x + amp sin(2 pi y) e_x applied to the reference's
+    own lattice (build_cube, mesh.cpp:138-160); SURVEY §8(c) gap 1: the level is
+    rebuilt with these coordinates and J0 recomputed by the reference's sweeps."""
+    c = L.coords().reshape(-1, 3).copy()
+    c[:, 0] += amp * np.sin(2.0 * np.pi * c[:, 1])
+    return c.reshape(-1)
+
+
+def _inh_params(kappa):
+    return R.material_params(mu=1.0, lam=10.0, kappa=kappa)
+
+
+def shear():
+    """cfg2-shaped operators at small size: shear map amplitude 0.1, iNH
+    kappa/mu = 1000, Q4, u0 = 0.1 sin sin sin at pre-map coordinates plus the
+    scaled noise 1e-3*8/n (workloads.cfg2); all reference strategies x
+    fp64/fp32 plus the diagonal.  2^3 and 4^3 elements."""
+    sys.path.insert(0, ROOT)
+    from paper_2408_12479_b200 import workloads as W
+    out = {}
+    for n, lev in ((2, 1), (4, 2)):
+        w = W.cfg2(n=n)
+        L0 = R.RefLevel(1, lev, 4, 0.0, 1)
+        coords = _shear_coords(L0)
+        L = R.RefLevel(1, lev, 4, 0.0, 1, coords=coords)
+        u0, v = w.u0(), w.v()
+        prm = _inh_params(1000.0)
+        tag = f"n{n}"
+        out[f"{tag}_coords"] = coords
+        out[f"{tag}_u0"] = u0
+        out[f"{tag}_v"] = v
+        for prec in (64, 32):
+            for strat in ("none", "scalar", "tensor"):
+                op = R.RefOperator(L, "inh", prm, strat, prec)
+                op.update_linearization(u0)
+                out[f"{tag}_y{prec}_{strat}"] = op.apply(v.astype(op.dtype))
+            op = R.RefOperator(L, "inh", prm, "none", prec)
+            op.update_linearization(u0)
+            d, bad, nbad = op.diagonal()
+            out[f"{tag}_diag{prec}"] = d
+            out[f"{tag}_diag{prec}_nbad"] = nbad
+            out[f"{tag}_diag{prec}_bad"] = bad
+        print("shear", tag, L.ndofs, "|y64| =", np.linalg.norm(out[f"{tag}_y64_none"]))
+    out["params"] = _inh_params(1000.0)
+    np.savez_compressed(os.path.join(OUT, "shear.npz"), **out)
+
+
+# sampled DoFs of the full-size known answers: seeded, plus the centre node
+def _sample_dofs(ndofs, m, count=2048, seed=5):
+    idx = np.unique((I.uniform01(seed, count) * ndofs).astype(np.int64))
+    c = m // 2
+    node = (c * m + c) * m + c
+    return np.unique(np.concatenate([idx, 3 * node + np.arange(3)]))
+
+
+def cfg2_full():
+    """BASELINE configs[2] at full size (64^3 Q4, 50 923 779 DoFs) through the
+    unmodified reference: the literal inputs' NonPositiveJacobian (first
+    element, qpoint) and, for the scaled-noise variant, norms and sampled
+    values of y = K(u0) v in fp64 and fp32 (tests/golden/cfg2_full.json)."""
+    import json
+    import time
+    sys.path.insert(0, ROOT)
+    from paper_2408_12479_b200 import workloads as W
+    n, m = 64, 64 * 4 + 1
+    L0 = R.RefLevel(1, 6, 4, 0.0, 1)
+    coords = _shear_coords(L0)
+    del L0
+    L = R.RefLevel(1, 6, 4, 0.0, 1, coords=coords)
+    del coords
+    prm = _inh_params(1000.0)
+    res = {"ndofs": int(L.ndofs), "threads": os.cpu_count()}
+    op = R.RefOperator(L, "inh", prm, "none", 64)
+    lit = W.cfg2(literal=True)
+    try:
+        op.update_linearization(lit.u0())
+        res["literal"] = {"admissible": True}
+    except R.RefError as ex:
+        res["literal"] = {"admissible": False, "message": str(ex)}
+    print("literal:", res["literal"])
+    w = W.cfg2()
+    u0, v = w.u0(), w.v()
+    t0 = time.perf_counter()
+    op.update_linearization(u0)
+    res["linearize_s"] = time.perf_counter() - t0
+    sd = _sample_dofs(L.ndofs, m)
+    res["sample_dofs"] = sd.tolist()
+    res["norm_u0"] = float(np.linalg.norm(u0))
+    res["norm_v"] = float(np.linalg.norm(v))
+    for prec in (64, 32):
+        if prec == 32:
+            op = R.RefOperator(L, "inh", prm, "none", 32)
+            op.update_linearization(u0)
+        t0 = time.perf_counter()
+        y = op.apply(v.astype(op.dtype))
+        res[f"apply{prec}_s"] = time.perf_counter() - t0
+        res[f"norm_y{prec}"] = float(np.linalg.norm(y.astype(np.float64)))
+        res[f"sum_y{prec}"] = float(np.sum(y.astype(np.float64)))
+        res[f"y{prec}_sample"] = [float(t) for t in y[sd]]
+        print(f"cfg2 fp{prec}: |y| = {res[f'norm_y{prec}']!r}  apply {res[f'apply{prec}_s']:.2f} s")
+    with open(os.path.join(OUT, "cfg2_full.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
+def cfg4_full():
+    """BASELINE configs[4] at full size (48^3 Q4, 21 567 171 DoFs) through the
+    reference: the literal inputs' NonPositiveJacobian, and on the well-posed
+    variant (kappa/mu = 50, u0 = 0, affine) the fp64 PCG preconditioned by the
+    reference's MgHierarchy<float> (Q4 -> Q2 -> Q1 -> 24^3 -> 12^3 -> 6^3,
+    Chebyshev degree 5, dense coarse LU below 2000 DoFs): iterations, residual
+    history and CPU times (tests/golden/cfg4_full.json)."""
+    import json
+    import time
+    sys.path.insert(0, ROOT)
+    from paper_2408_12479_b200 import workloads as W
+    res = {"threads": os.cpu_count()}
+    lit = W.cfg4(wellposed=False)
+    L0 = R.RefLevel(6, 3, 4, 0.0, 1)
+    Ls = R.RefLevel(6, 3, 4, 0.0, 1, coords=_shear_coords(L0))
+    op = R.RefOperator(Ls, "inh", _inh_params(1000.0), "none", 64)
+    try:
+        op.update_linearization(lit.u0())
+        res["literal"] = {"admissible": True}
+    except R.RefError as ex:
+        res["literal"] = {"admissible": False, "message": str(ex)}
+    print("literal:", res["literal"], flush=True)
+    del op, Ls
+    w = W.cfg4()
+    L = L0
+    prm = _inh_params(50.0)
+    res["ndofs"] = int(L.ndofs)
+    t0 = time.perf_counter()
+    op = R.RefOperator(L, "inh", prm, "none", 64)
+    op.update_linearization(np.zeros(L.ndofs))
+    mg = R.RefMg(L, "inh", prm, degree=5, coarse_direct_limit=2000)
+    mg.update_linearization(np.zeros(L.ndofs))
+    res["setup_s"] = time.perf_counter() - t0
+    res["mg_levels"] = mg.n_levels
+    print("setup", res["setup_s"], "levels", mg.n_levels, flush=True)
+    b = W.rhs(w)
+    t0 = time.perf_counter()
+    x, its, hist = R.pcg_solve(op, mg, b, 1e-8, 300)
+    res["solve_s"] = time.perf_counter() - t0
+    res["iterations"] = int(its)
+    res["history"] = [float(h) for h in hist]
+    res["norm_x"] = float(np.linalg.norm(x))
+    print("pcg", its, "its", res["solve_s"], "s", flush=True)
+    with open(os.path.join(OUT, "cfg4_full.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for f in sys.argv[1:]:
@@ -222,3 +374,4 @@ if __name__ == "__main__":
     small()
     transfers()
     smoother()
+    shear()

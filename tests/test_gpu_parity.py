@@ -770,3 +770,70 @@ print(its, its2, hashlib.sha1(x.cpu().numpy().tobytes() + hist.tobytes() + x2.cp
         assert out.returncode == 0, out.stderr[-2000:]
         outs.append(out.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1], outs
+
+
+# ---- BASELINE configs[2] shape against the reference itself (shear map)
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("strategy", ["none", "scalar", "tensor", "cachedF"])
+def test_shear_map_q4_inh_vs_reference(G, n, prec, strategy):
+    """cfg2's operator at small size: the device-generated shear map
+    x' = x + 0.1 sin(2 pi y) e_x (EMFGPU_MAP_SHEAR_X), iNH kappa/mu = 1000, Q4,
+    u0 amplitude 0.1 at pre-map coordinates + scaled noise, against the
+    unmodified reference on the same coordinates (tests/golden/shear.npz)."""
+    from paper_2408_12479_b200 import workloads as W
+    g = np.load(os.path.join(GOLD, "shear.npz"))
+    w = W.cfg2(n=n)
+    lev = w.level()
+    tag = f"n{n}"
+    assert rel(lev.node_coords(), g[f"{tag}_coords"]) <= 1e-15
+    assert np.array_equal(w.u0(), g[f"{tag}_u0"]) and np.array_equal(w.v(), g[f"{tag}_v"])
+    op = G.ElasticOperator(lev, "inh", params_from(g["params"], G), strategy, prec)
+    op.update_linearization(g[f"{tag}_u0"])
+    y = op.apply_tangent(g[f"{tag}_v"])
+    key = f"{tag}_y{prec}_{strategy if strategy != 'cachedF' else 'none'}"
+    assert rel(y, g[key]) <= TOL[prec], rel(y, g[key])
+    assert rel(y, g[f"{tag}_y64_none"]) <= TOL[prec]
+    if strategy == "none":
+        d, nb = op.compute_diagonal()
+        assert rel(d, g[f"{tag}_diag{prec}"]) <= TOL[prec]
+        assert nb == int(g[f"{tag}_diag{prec}_nbad"])
+
+
+def _cfg2_full():
+    import json
+    with open(os.path.join(GOLD, "cfg2_full.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("prec,strategy", [(64, "none"), (64, "tensor"), (64, "scalar"), (32, "none"),
+                                           (32, "tensor")])
+def test_cfg2_full_size_vs_reference(G, prec, strategy):
+    """BASELINE configs[2] at full size (64^3 Q4 curved iNH, 50 923 779 DoFs)
+    against the unmodified reference's known answers (tests/golden/
+    cfg2_full.json, make_golden.cfg2_full): ||y||_2 and y at 2051 sampled
+    DoFs (incl. the centre node) within 1e-12 (fp64) / 1e-5 (fp32)."""
+    import torch
+    from paper_2408_12479_b200 import workloads as W
+    ref = _cfg2_full()
+    w = W.cfg2()
+    lev = w.level()
+    assert lev.n_dofs == ref["ndofs"]
+    u0, v = w.u0(), w.v()
+    assert np.isclose(np.linalg.norm(u0), ref["norm_u0"], rtol=1e-14)
+    assert np.isclose(np.linalg.norm(v), ref["norm_v"], rtol=1e-14)
+    op = G.ElasticOperator(lev, "inh", w.material(), strategy, prec)
+    op.update_linearization(u0)
+    dt = torch.float64 if prec == 64 else torch.float32
+    x = torch.tensor(v, dtype=dt, device="cuda")
+    y = torch.empty_like(x)
+    op.apply_tangent_device(x, y)
+    torch.cuda.synchronize()
+    sd = torch.tensor(ref["sample_dofs"], device="cuda")
+    ys = y[sd].double().cpu().numpy()
+    ny = torch.linalg.norm(y.double()).item()
+    key = 64 if prec == 64 else 32
+    assert abs(ny - ref[f"norm_y{key}"]) <= TOL[prec] * ref[f"norm_y{key}"], (ny, ref[f"norm_y{key}"])
+    assert rel(ys, ref[f"y{key}_sample"]) <= TOL[prec], rel(ys, ref[f"y{key}_sample"])
+    assert rel(ys, ref["y64_sample"]) <= TOL[prec]
