@@ -137,6 +137,49 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
 }
 
+// ---- 1D tables ------------------------------------------------------------------
+// B[q][a] (basis a at Gauss point q) and D[q][a] on the symmetric GLL nodes /
+// Gauss points: B[n-1-q][n-1-a] = B[q][a] and D[n-1-q][n-1-a] = -D[q][a]
+// (exact in exact arithmetic; the stored rows q > (n-1)/2 differ from their
+// mirror by rounding only).  With EMF_SYMTAB the sweeps read only the
+// unique half, so a sweep's distinct table operands drop from 2n^2 to
+// ~n^2 (Q4: 50 -> 25 doubles); they then fit the uniform register file as
+// DFMA operands instead of pinning ~50 general registers for the kernel's
+// lifetime (Q4 fp64: 210+ registers -> see DESIGN).  D[c][c] of the centre
+// point (odd n) is an exact zero and its FMAs are dropped.
+#ifndef EMF_SYMTAB
+#define EMF_SYMTAB 1
+#endif
+#ifndef EMF_SYMTAB_ALL
+#define EMF_SYMTAB_ALL 0  // also Q1-Q3 (experiments)
+#endif
+template <int N>
+__host__ __device__ constexpr bool symtab_on() { return EMF_SYMTAB && (N == 5 || EMF_SYMTAB_ALL); }
+template <typename T, int N>
+__device__ __forceinline__ T tB(const T* M, int q, int a) {
+  if (symtab_on<N>()) {
+    if (2 * q > N - 1) { q = N - 1 - q; a = N - 1 - a; }
+    if (2 * q == N - 1 && 2 * a > N - 1) a = N - 1 - a;
+  }
+  return M[q * N + a];
+}
+template <typename T, int N>
+__device__ __forceinline__ T tD(const T* M, int q, int a) {
+  if (symtab_on<N>()) {
+    bool neg = false;
+    if (2 * q > N - 1) { q = N - 1 - q; a = N - 1 - a; neg = true; }
+    if (2 * q == N - 1 && 2 * a > N - 1) { a = N - 1 - a; neg = !neg; }
+    return neg ? -M[q * N + a] : M[q * N + a];
+  }
+  return M[q * N + a];
+}
+// s + D[q][a] u, skipping the structural zero D[c][c]
+template <typename T, int N>
+__device__ __forceinline__ T dacc(T s, const T* M, int q, int a, T u) {
+  if (symtab_on<N>() && 2 * q == N - 1 && 2 * a == N - 1) return s;
+  return s + tD<T, N>(M, q, a) * u;
+}
+
 // ---- pencil sweeps ------------------------------------------------------------
 // Arguments are base pointers of consecutive per-element arrays of N3 values
 // (array t at base + t*N3) with Lay<N>::at addressing.  `w` is the worker
@@ -169,11 +212,11 @@ __device__ __forceinline__ void fw_x(const T* in0, T* tb0, T* td0, const T* Bm, 
     for (int a = 0; a < N; ++a) u[a] = in[c * L::SIZE + lat<N>(a, j, k)];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      T sb = Bm[q * N] * u[0], sd = Dm[q * N] * u[0];
+      T sb = tB<T, N>(Bm, q, 0) * u[0], sd = tD<T, N>(Dm, q, 0) * u[0];
 #pragma unroll
       for (int a = 1; a < N; ++a) {
-        sb += Bm[q * N + a] * u[a];
-        sd += Dm[q * N + a] * u[a];
+        sb += tB<T, N>(Bm, q, a) * u[a];
+        sd = dacc<T, N>(sd, Dm, q, a, u[a]);
       }
       tb[c * L::SIZE + lat<N>(q, j, k)] = sb;
       td[c * L::SIZE + lat<N>(q, j, k)] = sd;
@@ -204,12 +247,12 @@ __device__ __forceinline__ void fw_y(const T* tb0, const T* td0, T* sbb0, T* sbd
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      T s1 = Bm[q * N] * ub[0], s2 = Dm[q * N] * ub[0], s3 = Bm[q * N] * ud[0];
+      T s1 = tB<T, N>(Bm, q, 0) * ub[0], s2 = tD<T, N>(Dm, q, 0) * ub[0], s3 = tB<T, N>(Bm, q, 0) * ud[0];
 #pragma unroll
       for (int b = 1; b < N; ++b) {
-        s1 += Bm[q * N + b] * ub[b];
-        s2 += Dm[q * N + b] * ub[b];
-        s3 += Bm[q * N + b] * ud[b];
+        s1 += tB<T, N>(Bm, q, b) * ub[b];
+        s2 = dacc<T, N>(s2, Dm, q, b, ub[b]);
+        s3 += tB<T, N>(Bm, q, b) * ud[b];
       }
       sbb[c * L::SIZE + lat<N>(i, q, k)] = s1;
       sbd[c * L::SIZE + lat<N>(i, q, k)] = s2;
@@ -241,12 +284,12 @@ __device__ __forceinline__ void fw_z(const T* sbb0, const T* sbd0, const T* sdb0
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      T g0 = Bm[q * N] * u0[0], g1 = Bm[q * N] * u1[0], g2 = Dm[q * N] * u2[0];
+      T g0 = tB<T, N>(Bm, q, 0) * u0[0], g1 = tB<T, N>(Bm, q, 0) * u1[0], g2 = tD<T, N>(Dm, q, 0) * u2[0];
 #pragma unroll
       for (int k = 1; k < N; ++k) {
-        g0 += Bm[q * N + k] * u0[k];
-        g1 += Bm[q * N + k] * u1[k];
-        g2 += Dm[q * N + k] * u2[k];
+        g0 += tB<T, N>(Bm, q, k) * u0[k];
+        g1 += tB<T, N>(Bm, q, k) * u1[k];
+        g2 = dacc<T, N>(g2, Dm, q, k, u2[k]);
       }
       g[(3 * c + 0) * L::SIZE + lat<N>(i, j, q)] = g0;
       g[(3 * c + 1) * L::SIZE + lat<N>(i, j, q)] = g1;
@@ -275,11 +318,11 @@ __device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int
     for (int a = 0; a < N; ++a) u[a] = s[lat<N>(a, j, k)];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      T sb = Bm[q * N] * u[0], sd = Dm[q * N] * u[0];
+      T sb = tB<T, N>(Bm, q, 0) * u[0], sd = tD<T, N>(Dm, q, 0) * u[0];
 #pragma unroll
       for (int a = 1; a < N; ++a) {
-        sb += Bm[q * N + a] * u[a];
-        sd += Dm[q * N + a] * u[a];
+        sb += tB<T, N>(Bm, q, a) * u[a];
+        sd = dacc<T, N>(sd, Dm, q, a, u[a]);
       }
       s[lat<N>(q, j, k)] = sb;
       t[lat<N>(q, j, k)] = sd;
@@ -302,12 +345,12 @@ __device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* D
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      T s1 = Bm[q * N] * ub[0], s2 = Dm[q * N] * ub[0], s3 = Bm[q * N] * ud[0];
+      T s1 = tB<T, N>(Bm, q, 0) * ub[0], s2 = tD<T, N>(Dm, q, 0) * ub[0], s3 = tB<T, N>(Bm, q, 0) * ud[0];
 #pragma unroll
       for (int b = 1; b < N; ++b) {
-        s1 += Bm[q * N + b] * ub[b];
-        s2 += Dm[q * N + b] * ub[b];
-        s3 += Bm[q * N + b] * ud[b];
+        s1 += tB<T, N>(Bm, q, b) * ub[b];
+        s2 = dacc<T, N>(s2, Dm, q, b, ub[b]);
+        s3 += tB<T, N>(Bm, q, b) * ud[b];
       }
       s[lat<N>(i, q, k)] = s1;
       t[lat<N>(i, q, k)] = s2;
@@ -332,12 +375,12 @@ __device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* D
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      T g0 = Bm[q * N] * u0[0], g1 = Bm[q * N] * u1[0], g2 = Dm[q * N] * u2[0];
+      T g0 = tB<T, N>(Bm, q, 0) * u0[0], g1 = tB<T, N>(Bm, q, 0) * u1[0], g2 = tD<T, N>(Dm, q, 0) * u2[0];
 #pragma unroll
       for (int k = 1; k < N; ++k) {
-        g0 += Bm[q * N + k] * u0[k];
-        g1 += Bm[q * N + k] * u1[k];
-        g2 += Dm[q * N + k] * u2[k];
+        g0 += tB<T, N>(Bm, q, k) * u0[k];
+        g1 += tB<T, N>(Bm, q, k) * u1[k];
+        g2 = dacc<T, N>(g2, Dm, q, k, u2[k]);
       }
       u[lat<N>(i, j, q)] = g0;
       t[lat<N>(i, j, q)] = g1;
@@ -366,12 +409,12 @@ __device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T*
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      T a0 = Bm[k] * u0[0], a1 = Bm[k] * u1[0], a2 = Dm[k] * u2[0];
+      T a0 = tB<T, N>(Bm, 0, k) * u0[0], a1 = tB<T, N>(Bm, 0, k) * u1[0], a2 = tD<T, N>(Dm, 0, k) * u2[0];
 #pragma unroll
       for (int q = 1; q < N; ++q) {
-        a0 += Bm[q * N + k] * u0[q];
-        a1 += Bm[q * N + k] * u1[q];
-        a2 += Dm[q * N + k] * u2[q];
+        a0 += tB<T, N>(Bm, q, k) * u0[q];
+        a1 += tB<T, N>(Bm, q, k) * u1[q];
+        a2 = dacc<T, N>(a2, Dm, q, k, u2[q]);
       }
       av[(3 * c + 0) * L::SIZE + lat<N>(i, j, k)] = a0;
       av[(3 * c + 1) * L::SIZE + lat<N>(i, j, k)] = a1;
@@ -413,11 +456,11 @@ __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T*
     }
 #pragma unroll
     for (int b = 0; b < N; ++b) {
-      T q0 = Bm[b] * u0[0], q12 = Dm[b] * u1[0] + Bm[b] * u2[0];
+      T q0 = tB<T, N>(Bm, 0, b) * u0[0], q12 = tD<T, N>(Dm, 0, b) * u1[0] + tB<T, N>(Bm, 0, b) * u2[0];
 #pragma unroll
       for (int q = 1; q < N; ++q) {
-        q0 += Bm[q * N + b] * u0[q];
-        q12 += Dm[q * N + b] * u1[q] + Bm[q * N + b] * u2[q];
+        q0 += tB<T, N>(Bm, q, b) * u0[q];
+        q12 = dacc<T, N>(q12 + tB<T, N>(Bm, q, b) * u2[q], Dm, q, b, u1[q]);
       }
       qv[qv_arr<T>(0, c) * L::SIZE + lat<N>(i, b, k)] = q0;
       qv[qv_arr<T>(1, c) * L::SIZE + lat<N>(i, b, k)] = q12;
@@ -449,9 +492,9 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T
     T o[N];
 #pragma unroll
     for (int a = 0; a < N; ++a) {
-      T s = Dm[a] * u0[0] + Bm[a] * u1[0];
+      T s = tD<T, N>(Dm, 0, a) * u0[0] + tB<T, N>(Bm, 0, a) * u1[0];
 #pragma unroll
-      for (int q = 1; q < N; ++q) s += Dm[q * N + a] * u0[q] + Bm[q * N + a] * u1[q];
+      for (int q = 1; q < N; ++q) s = dacc<T, N>(s + tB<T, N>(Bm, q, a) * u1[q], Dm, q, a, u0[q]);
       o[a] = s;
     }
     T* dst = loc_e + c * L::N3 + (k * N + j) * N;
@@ -461,6 +504,9 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T
 }
 
 // ---- the kernel -------------------------------------------------------------------
+#ifndef EMF_GX_SMEM
+#define EMF_GX_SMEM 1
+#endif
 template <typename T, int P, int MODEL, int STRAT, bool CART>
 struct ApplyV2Smem {
   static constexpr int N = P + 1, N3 = N * N * N, EPB = TileV2<P, sizeof(T)>::EPB;
@@ -471,6 +517,10 @@ struct ApplyV2Smem {
   T geo[2][EPB][10];
   T r1[EPB][9][SZ];
   T r2[EPB][9][SZ];
+  // fp64 Q4 with u_k swept: the x gradient parks in its own arrays until the
+  // integrand needs it, instead of 9 registers held across the u_k sweeps
+  static constexpr bool kGx3 = EMF_GX_SMEM && P == 4 && sizeof(T) == 8 && kUk;
+  T r3[kGx3 ? EPB : 1][kGx3 ? 9 : 1][kGx3 ? SZ : 1];
 };
 
 // CTAs per SM for the launch bounds.  fp64 keeps 3 CTAs/SM (<= 168 registers)
@@ -487,7 +537,13 @@ struct ApplyV2Smem {
 #define EMF_MINB_V2D_FORCE 0
 #endif
 #ifndef EMF_MINB_Q4C
-#define EMF_MINB_Q4C 2
+#define EMF_MINB_Q4C 4
+#endif
+#ifndef EMF_MINB_Q4_CART
+#define EMF_MINB_Q4_CART 3
+#endif
+#ifndef EMF_MINB_Q4_FIBER
+#define EMF_MINB_Q4_FIBER 2
 #endif
 #ifndef EMF_MINB_FIBER_V2D
 #define EMF_MINB_FIBER_V2D 2
@@ -510,14 +566,28 @@ constexpr int minb_v2() {
   // 0.1588 ms, tensor 0.1383 -> 0.1281, cachedF 0.1486 -> 0.1444)
   if (P == 3 && MODEL == CNH && CART && (STRAT == S_SCALAR || STRAT == S_TENSOR || STRAT == S_CACHEDF)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
-  // Q4 curved fp64: 2 CTAs/SM (255 registers) beats 3 with spills
-  // (24^3 Q4 curved iNH none 0.241 -> 0.214 ms, tensor 0.220 -> 0.198 ms);
-  // on axis-aligned meshes 3 stays ahead (0.2028 vs 0.2058 ms)
+  // Q4 fp64: with the half 1D tables (symtab_on) the cNH / iNH variants fit
+  // 128 registers (was 210-250: the 50 table doubles had been pinned in
+  // general registers), so 4 CTAs/SM; the fibre model keeps 2 (spill-free at
+  // up to 255 registers; 3 spilled 100-190 B)
+  if (P == 4 && MODEL == FIBER) return EMF_MINB_Q4_FIBER;
   if (P == 4 && !CART) return EMF_MINB_Q4C;
+  if (P == 4 && CART) return EMF_MINB_Q4_CART;
   // fibre fp64 at Q3: 2 CTAs/SM, spill-free (32^3 curved none 0.278 -> 0.249 ms,
   // scalar 0.261 -> 0.232 ms); Q2 stays at 3 (0.128 vs 0.136 ms)
   if (MODEL == FIBER && P >= 3) return EMF_MINB_FIBER_V2D;
   return TileV2<P>::MINB > 3 ? 3 : TileV2<P>::MINB;
+}
+
+// Push-forward integrand (qp.cuh: push_state / push_integrand) for cNH / iNH
+// with the linearization state computed or half-cached (none, scalar,
+// cachedF); EMF_PUSH=0 builds the material-form algebra everywhere.
+#ifndef EMF_PUSH
+#define EMF_PUSH 1
+#endif
+template <typename T, int P, int MODEL, int STRAT>
+constexpr bool push_form() {
+  return EMF_PUSH && MODEL != FIBER && (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_CACHEDF);
 }
 
 #ifndef EMF_V2_FRESH
@@ -799,9 +869,19 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       esync();
     } else {
       // ---- gradient of x at the qps
-      fwd_sweeps(0, false);
+      if constexpr (SM::kGx3) {
+        T* const R3 = &sm.r3[el][0][0];
+        fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+        esync();
+        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+        esync();
+        fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R3, a.Bm, Dfz, q);
+        esync();
+      } else {
+        fwd_sweeps(0, false);
 #pragma unroll
-      for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
+        for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
+      }
     }
     if (CART) {  // diagonal J0^-1 (entries 0, 4, 8)
       j0inv[0] = sm.geo[buf][el][0];
@@ -813,6 +893,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       for (int m = 0; m < 9; ++m) j0inv[m] = sm.geo[buf][el][m];
       detw = sm.geo[buf][el][9] * wq3;
     }
+    // push-forward form of the cNH / iNH integrand (qp.cuh, push_state)
+    constexpr bool kPush = push_form<T, P, MODEL, STRAT>();
+    PushState<T> ps;
     Bundle<T> cb;
     SpCell<T> sp;
     if constexpr (kSpTenEarly) {
@@ -824,9 +907,21 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       if constexpr (kFused) {
         grad_at(1, gk);
       } else {
-        fwd_sweeps(3, true);
+        if constexpr (SM::kGx3) {
+          // R2 / R1 were last read before the barriers of the x pass
+          fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+          esync();
+          fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+          esync();
+          fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+          esync();
 #pragma unroll
-        for (int m = 0; m < 9; ++m) gk[m] = R1[m * SZ + qs];
+          for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+        } else {
+          fwd_sweeps(3, true);
+#pragma unroll
+          for (int m = 0; m < 9; ++m) gk[m] = R1[m * SZ + qs];
+        }
       }
       if constexpr (CART) {
 #pragma unroll
@@ -834,7 +929,16 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       } else {
         mm(gk, j0inv, gg);
       }
-      if constexpr (is_spatial(STRAT)) {
+      if constexpr (kPush) {
+        if constexpr (kScEarly) {
+          if (!push_state<T, MODEL, STRAT == S_SCALAR, CART>(mq, gg, j0inv, detw, cbs, ps) && valid)
+            atomicMin(a.err, (unsigned long long)qidx);
+        } else {
+          if (STRAT == S_SCALAR) load_scalars<T, MODEL>(cs, st, qidx, cb);
+          if (!push_state<T, MODEL, STRAT == S_SCALAR, CART>(mq, gg, j0inv, detw, cb, ps) && valid)
+            atomicMin(a.err, (unsigned long long)qidx);
+        }
+      } else if constexpr (is_spatial(STRAT)) {
         if (!spatial_bundle<T, MODEL>(STRAT - S_SP_NONE, mq, gg, cs, st, qidx, cb, sp) && valid)
           atomicMin(a.err, (unsigned long long)qidx);
       } else {
@@ -859,16 +963,27 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       T gg[9];
 #pragma unroll
       for (int m = 0; m < 9; ++m) gg[m] = kCfEarly ? gcf[m] : cs[(C_G + m) * st + qidx];
+      if constexpr (kPush) {
+        if (!push_state<T, MODEL, false, CART>(mq, gg, j0inv, detw, cb, ps) && valid)
+          atomicMin(a.err, (unsigned long long)qidx);
+      } else {
       if (!make_strain(gg, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
       cache_scalars<T, MODEL>(mq, cb);
       second_pk<T, MODEL>(mq, cb);
+      }
     } else {  // S_TENSOR
       if constexpr (kTenEarly) cb = cbe;
       else load_tensor_bundle(cb);
     }
     if constexpr (kFused) grad_at(0, gx);
+    if constexpr (SM::kGx3) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gx[m] = sm.r3[el][m][qs];
+    }
     T wv[9];
-    if constexpr (is_spatial(STRAT)) {
+    if constexpr (kPush) {
+      push_integrand<T, MODEL>(ps, gx, wv);
+    } else if constexpr (is_spatial(STRAT)) {
       T jtinv[9];
       inverse3(sj, jtinv);
       const T ssc = (sj[9] * det3(sj)) * wq3;

@@ -427,6 +427,130 @@ __device__ __forceinline__ void tangent_wm(const MatConst<T>& m, const Bundle<T>
   }
 }
 
+// Green-Euler strain bt = (G + G^T + G G^T)/2 (tensor.hpp:259-270).
+template <typename T>
+__device__ __forceinline__ void green_euler(const T* g, T* bt) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const T q = (g[3 * i] * g[3 * j] + g[3 * i + 1] * g[3 * j + 1]) + g[3 * i + 2] * g[3 * j + 2];
+      bt[sidx(i, j)] = T(0.5) * ((g[3 * i + j] + g[3 * j + i]) + q);
+    }
+}
+
+// ---- push-forward form of the material integrand (cNH / iNH) -----------------
+// The reference's integrand w_ref = detw (dg S + F D_uS) J0^-T
+// (operator.hpp:502-504, constitutive.hpp:381-419) rewritten exactly through
+// the push-forward to the current configuration.  With K = J0^-1 F^-1 and
+// l = dg F^-1 = Gref K:
+//   w_ref = detw W K^T,  W = (dg S + F D_uS) F^T
+//   cNH: W = mu l b + h l^T + 2 lam tr(l) I,          h = mu - 2 lam lnJ
+//   iNH: W = beta l b - c1 l^T + (c2 tr l - t l:b) I - t tr(l) b,
+//        beta = mu J^-2/3, t = 2 mu J^-2/3 / 3
+// (dg S F^T = l tau; tau - c1 I = mu J^-2/3 b for iNH and tau + h I = mu b for
+// cNH, so the large volumetric parts of S and c1 C^-1 cancel analytically;
+// dg C^-1 F^T = l, (F^-1 dg F^-1)^T F^T = l^T, F : dg = l : b).  The state a
+// point keeps between the linearization and test halves is b (6), K (9) and
+// 4 scalars with detw folded in (was F^-1, S, C^-1, F, J0^-1, scalars: 43),
+// and the test half is 3 small matrix products (~100 flops instead of ~190).
+// Same quantity as the reference's, different rounding (rel-L2 ~1e-15).
+template <typename T>
+struct PushState {
+  T K[9], b[6];
+  T k_lb, k_lt, k_tr, k_t;  // coefficients of l b, l^T, tr(l) I (and t: l:b I, tr(l) b), times detw
+};
+
+// State at one point from the linearization gradient gg = grad_X u_k (material
+// coordinates), J0^-1 and detw.  Scalars either computed (strategy none /
+// cachedF, constitutive.hpp:335-366) or taken from the scalar cache.
+// Returns false when det(F) <= 0 (make_strain's check, constitutive.hpp:48-52).
+// kDiagJ: J0^-1 diagonal (entries 0, 4, 8 read only).
+template <typename T, int MODEL, bool kCached, bool kDiagJ>
+__device__ __forceinline__ bool push_state(const MatConst<T>& m, const T* gg, const T* j0inv, T detw,
+                                           const Bundle<T>& cached, PushState<T>& ps) {
+  const T jm1 = det_minus_one(gg);
+  if (!(jm1 > T(-1))) return false;
+  T bt[6];
+  green_euler(gg, bt);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) ps.b[k] = T(2) * bt[k];
+  ps.b[0] += T(1);
+  ps.b[1] += T(1);
+  ps.b[2] += T(1);
+  {
+    T F[9], Finv[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) F[i] = gg[i];
+    F[0] += T(1);
+    F[4] += T(1);
+    F[8] += T(1);
+    inverse3_det(F, T(1) + jm1, Finv);
+    if constexpr (kDiagJ) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) ps.K[3 * i + j] = j0inv[4 * i] * Finv[3 * i + j];
+    } else {
+      mm(j0inv, Finv, ps.K);
+    }
+  }
+  if constexpr (MODEL == CNH) {
+    const T lnj = kCached ? cached.lnj : ln_plus_one(jm1);
+    ps.k_lb = m.mu * detw;
+    ps.k_lt = (m.mu - (T(2) * m.lam) * lnj) * detw;
+    ps.k_tr = (T(2) * m.lam) * detw;
+    ps.k_t = T(0);
+  } else {
+    T jp, c1, c2;
+    if constexpr (kCached) {
+      jp = cached.jp;
+      c1 = cached.c1;
+      c2 = cached.c2;
+    } else {
+      jp = fast_jpow(jm1);
+      const T i1 = T(3) + T(2) * ((bt[0] + bt[1]) + bt[2]);
+      const T jac = T(1) + jm1;
+      c1 = m.half_k * (jm1 * (jm1 + T(2))) - (m.mu_3 * jp) * i1;
+      c2 = (m.two_mu_9 * jp) * i1 + (m.kappa * jac) * jac;
+    }
+    ps.k_lb = (m.mu * jp) * detw;
+    ps.k_lt = -c1 * detw;
+    ps.k_tr = c2 * detw;
+    ps.k_t = (m.two_mu_3 * jp) * detw;
+  }
+  return true;
+}
+
+// w_ref = W K^T for the test gradient gref (reference coordinates).
+template <typename T, int MODEL>
+__device__ __forceinline__ void push_integrand(const PushState<T>& ps, const T* gref, T* wref) {
+  T l[9];
+  mm(gref, ps.K, l);
+  const T trl = (l[0] + l[4]) + l[8];
+  T W[9];
+  mm_ts(l, ps.b, W);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) W[3 * i + j] = ps.k_lb * W[3 * i + j] + ps.k_lt * l[3 * j + i];
+  T diag = ps.k_tr * trl;
+  if constexpr (MODEL != CNH) {
+    const T ldb = ((l[0] * ps.b[0] + l[4] * ps.b[1]) + l[8] * ps.b[2]) +
+                  (((l[1] + l[3]) * ps.b[3] + (l[2] + l[6]) * ps.b[4]) + (l[5] + l[7]) * ps.b[5]);
+    diag -= ps.k_t * ldb;
+    const T tt = -ps.k_t * trl;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) W[3 * i + j] += tt * ps.b[sidx(i, j)];
+  }
+  W[0] += diag;
+  W[4] += diag;
+  W[8] += diag;
+  mm_bt(W, ps.K, wref);
+}
+
 // w_ref = detw * (dg S + F D_uS) J0^-T  (operator.hpp:502-504), dg = Gref J0^-1.
 template <typename T, int MODEL>
 __device__ __forceinline__ void tangent_integrand(const MatConst<T>& m, const Bundle<T>& c, const T* gref,
@@ -445,18 +569,6 @@ template <typename T>
 struct SpCell {
   T b[6], tau[6], fh[2][6];
 };
-
-// Green-Euler strain bt = (G + G^T + G G^T)/2 (tensor.hpp:259-270).
-template <typename T>
-__device__ __forceinline__ void green_euler(const T* g, T* bt) {
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = i; j < 3; ++j) {
-      const T q = (g[3 * i] * g[3 * j] + g[3 * i + 1] * g[3 * j + 1]) + g[3 * i + 2] * g[3 * j + 2];
-      bt[sidx(i, j)] = T(0.5) * ((g[3 * i + j] + g[3 * j + i]) + q);
-    }
-}
 
 // b = 2 bt + I, tau = kirchhoff_base (constitutive.hpp:240-283, stable) plus
 // the fibre terms c3 E_i F H_i F^T (push_forward, tensor.hpp:332-341).
