@@ -180,6 +180,50 @@ __device__ __forceinline__ T dacc(T s, const T* M, int q, int a, T u) {
   return s + tD<T, N>(M, q, a) * u;
 }
 
+// Array of gradient entry (component c, direction t) in a 9-array buffer:
+// component-major 3c + t, or with TA direction-major 3t + c, which makes every
+// sweep access's array index "c + constant", so one thread -> pencil map can
+// be bank-conflict-free for all of a sweep's accesses (Q4 fp64, see q4_pen).
+template <bool TA>
+__host__ __device__ constexpr int garr(int c, int t) { return TA ? 3 * t + c : 3 * c + t; }
+// array of gradient entry m = 3c + t (the per-point 3x3 index)
+template <bool TA>
+__host__ __device__ constexpr int garr_m(int m) { return garr<TA>(m / 3, m % 3); }
+
+// Thread -> pencil maps of the Q4 fp64 single-element sweeps (125 threads,
+// 75 pencils per orientation), found by tools/pencil_milp.py (solve_min,
+// layout SY 5, SZ 25, SIZE 125): every half-warp's pencils hit distinct bank
+// pairs for all accesses of the x and y sweeps, and 4 of the 5 half-warps of
+// the z sweeps (the fifth is 2-way); the natural order had 2-way conflicts
+// on most half-warps (profiles/r02_ncu_cfg2_*).  Entry = pencil index in the
+// sweep's own decoding, packed x | y << 8 | z << 16; 255 = no pencil.
+#ifndef EMF_Q4MAP
+#define EMF_Q4MAP 1
+#endif
+struct Q4PenMap {
+  unsigned char x[75], y[75], z[75];
+};
+static constexpr Q4PenMap kQ4Pen = {
+    {7, 9, 15, 16, 17, 24, 42, 43, 46, 47, 49, 51, 52, 54, 60, 72, 11, 12, 19, 20, 21, 30, 32, 33, 39,
+     44, 50, 53, 55, 56, 59, 70, 5, 6, 8, 13, 22, 25, 26, 29, 35, 38, 48, 58, 65, 66, 67, 69, 1, 4,
+     10, 14, 18, 28, 31, 34, 37, 40, 41, 45, 57, 63, 68, 73, 0, 2, 3, 23, 27, 36, 61, 62, 64, 71, 74},
+    {5, 7, 20, 31, 35, 37, 38, 42, 44, 47, 53, 58, 65, 68, 70, 72, 1, 6, 8, 15, 21, 27, 28, 30, 32,
+     33, 39, 46, 56, 59, 61, 62, 11, 12, 13, 19, 22, 24, 25, 26, 29, 50, 51, 52, 64, 67, 69, 74, 0, 4,
+     9, 10, 14, 16, 18, 23, 34, 40, 41, 43, 55, 57, 63, 73, 2, 3, 17, 36, 45, 48, 49, 54, 60, 66, 71},
+    {0, 1, 7, 11, 13, 15, 16, 17, 38, 42, 46, 47, 48, 49, 52, 74, 6, 8, 9, 12, 14, 19, 20, 21, 23,
+     27, 30, 39, 50, 53, 56, 73, 18, 24, 26, 29, 32, 33, 35, 41, 44, 55, 59, 62, 65, 66, 67, 68, 4, 5,
+     10, 28, 31, 34, 36, 37, 40, 43, 51, 54, 57, 58, 63, 69, 2, 3, 22, 25, 45, 60, 61, 64, 70, 71, 72}};
+struct Q4PenPacked {
+  unsigned v[128];
+};
+constexpr Q4PenPacked q4pen_pack() {
+  Q4PenPacked r{};
+  for (int t = 0; t < 128; ++t)
+    r.v[t] = t < 75 ? (unsigned)kQ4Pen.x[t] | (unsigned)kQ4Pen.y[t] << 8 | (unsigned)kQ4Pen.z[t] << 16 : 0xffffffu;
+  return r;
+}
+static __constant__ Q4PenPacked c_q4pen = q4pen_pack();
+
 // ---- pencil sweeps ------------------------------------------------------------
 // Arguments are base pointers of consecutive per-element arrays of N3 values
 // (array t at base + t*N3) with Lay<N>::at addressing.  `w` is the worker
@@ -263,7 +307,7 @@ __device__ __forceinline__ void fw_y(const T* tb0, const T* td0, T* sbb0, T* sbd
 
 // Forward z-sweep: g[c][0] = Bz sDB, g[c][1] = Bz sBD, g[c][2] = Dz sBB.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
-          int SR = 0>
+          int SR = 0, bool TA = false>
 __device__ __forceinline__ void fw_z(const T* sbb0, const T* sbd0, const T* sdb0, T* g0, const T* Bm,
                                      const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
@@ -291,9 +335,9 @@ __device__ __forceinline__ void fw_z(const T* sbb0, const T* sbd0, const T* sdb0
         g1 += tB<T, N>(Bm, q, k) * u1[k];
         g2 = dacc<T, N>(g2, Dm, q, k, u2[k]);
       }
-      g[(3 * c + 0) * L::SIZE + lat<N>(i, j, q)] = g0;
-      g[(3 * c + 1) * L::SIZE + lat<N>(i, j, q)] = g1;
-      g[(3 * c + 2) * L::SIZE + lat<N>(i, j, q)] = g2;
+      g[garr<TA>(c, 0) * L::SIZE + lat<N>(i, j, q)] = g0;
+      g[garr<TA>(c, 1) * L::SIZE + lat<N>(i, j, q)] = g1;
+      g[garr<TA>(c, 2) * L::SIZE + lat<N>(i, j, q)] = g2;
     }
   }
 }
@@ -391,7 +435,7 @@ __device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* D
 
 // Transposed z-sweep (node index along z): A0 = Bz^T w0, A1 = Bz^T w1, A2 = Dz^T w2.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
-          int SR = 0>
+          int SR = 0, bool TA = false>
 __device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
   for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
@@ -403,9 +447,9 @@ __device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T*
     T u0[N], u1[N], u2[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      u0[q] = wv[(3 * c + 0) * L::SIZE + lat<N>(i, j, q)];
-      u1[q] = wv[(3 * c + 1) * L::SIZE + lat<N>(i, j, q)];
-      u2[q] = wv[(3 * c + 2) * L::SIZE + lat<N>(i, j, q)];
+      u0[q] = wv[garr<TA>(c, 0) * L::SIZE + lat<N>(i, j, q)];
+      u1[q] = wv[garr<TA>(c, 1) * L::SIZE + lat<N>(i, j, q)];
+      u2[q] = wv[garr<TA>(c, 2) * L::SIZE + lat<N>(i, j, q)];
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -416,9 +460,9 @@ __device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T*
         a1 += tB<T, N>(Bm, q, k) * u1[q];
         a2 = dacc<T, N>(a2, Dm, q, k, u2[q]);
       }
-      av[(3 * c + 0) * L::SIZE + lat<N>(i, j, k)] = a0;
-      av[(3 * c + 1) * L::SIZE + lat<N>(i, j, k)] = a1;
-      av[(3 * c + 2) * L::SIZE + lat<N>(i, j, k)] = a2;
+      av[garr<TA>(c, 0) * L::SIZE + lat<N>(i, j, k)] = a0;
+      av[garr<TA>(c, 1) * L::SIZE + lat<N>(i, j, k)] = a1;
+      av[garr<TA>(c, 2) * L::SIZE + lat<N>(i, j, k)] = a2;
     }
   }
 }
@@ -438,7 +482,7 @@ __device__ __forceinline__ constexpr int qv_arr(int t, int c) {
 
 // Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
-          int SR = 0>
+          int SR = 0, bool TA = false>
 __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T* Dm, int w) {
   using L = Lay<N, sizeof(T)>;
   for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
@@ -450,9 +494,9 @@ __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T*
     T u0[N], u1[N], u2[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      u0[q] = av[(3 * c + 0) * L::SIZE + lat<N>(i, q, k)];
-      u1[q] = av[(3 * c + 1) * L::SIZE + lat<N>(i, q, k)];
-      u2[q] = av[(3 * c + 2) * L::SIZE + lat<N>(i, q, k)];
+      u0[q] = av[garr<TA>(c, 0) * L::SIZE + lat<N>(i, q, k)];
+      u1[q] = av[garr<TA>(c, 1) * L::SIZE + lat<N>(i, q, k)];
+      u2[q] = av[garr<TA>(c, 2) * L::SIZE + lat<N>(i, q, k)];
     }
 #pragma unroll
     for (int b = 0; b < N; ++b) {
@@ -629,6 +673,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   __shared__ __align__(16) SM sm;
   const int tid = threadIdx.x;
   const int el = tid / N3, q = tid % N3;
+  constexpr bool kMap = EMF_Q4MAP && P == 4 && sizeof(T) == 8 && !(EMF_V2_DENSE && EPB == 2) &&
+                        !(SM::kUk && sizeof(T) == 4);
+  constexpr int kStr = 3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3;
+  const unsigned pen = kMap ? c_q4pen.v[tid] : 0u;
   // Elements of a CTA only share data through their own slices, so when an
   // element spans whole warps it synchronises on its own named barrier.
   // Q3 (two 64-thread elements per CTA): dense pencil mapping over the CTA
@@ -736,6 +784,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   // unit u, staged in buffer buf (its cp.async group complete)
   auto compute = [&](int64_t u, int buf, bool zero_me) {
     EMF_V2_FRESH_POS
+    // this thread's pencil per sweep orientation (kQ4Pen) or its point index
+    const int wx = kMap ? (int)(pen & 255u) : q;
+    const int wy = kMap ? (int)((pen >> 8) & 255u) : q;
+    const int wz = kMap ? (int)(pen >> 16) : q;
     // tensor-product weight of this thread's point (operator.hpp:492)
     const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
     const int64_t e = elem_of(u, el);
@@ -837,11 +889,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       } else {
         T* const P1 = swap ? R2 : R1;
         T* const P2 = swap ? R1 : R2;
-        fw_x<T, N>(&sm.stage[buf][el][f0][0], P2, P2 + 3 * SZ, a.Bm, Dfx, q);
+        fw_x<T, N>(&sm.stage[buf][el][f0][0], P2, P2 + 3 * SZ, a.Bm, Dfx, wx);
         esync();
-        fw_y<T, N>(P2, P2 + 3 * SZ, P1, P1 + 3 * SZ, P1 + 6 * SZ, a.Bm, Dfy, q);
+        fw_y<T, N>(P2, P2 + 3 * SZ, P1, P1 + 3 * SZ, P1 + 6 * SZ, a.Bm, Dfy, wy);
         esync();
-        fw_z<T, N>(P1, P1 + 3 * SZ, P1 + 6 * SZ, P2, a.Bm, Dfz, q);
+        fw_z<T, N, kStr, 1, 0, kMap>(P1, P1 + 3 * SZ, P1 + 6 * SZ, P2, a.Bm, Dfz, wz);
         esync();
       }
     };
@@ -871,16 +923,16 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       // ---- gradient of x at the qps
       if constexpr (SM::kGx3) {
         T* const R3 = &sm.r3[el][0][0];
-        fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+        fw_x<T, N>(&sm.stage[buf][el][0][0], R2, R2 + 3 * SZ, a.Bm, Dfx, wx);
         esync();
-        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+        fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, wy);
         esync();
-        fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R3, a.Bm, Dfz, q);
+        fw_z<T, N, kStr, 1, 0, kMap>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R3, a.Bm, Dfz, wz);
         esync();
       } else {
         fwd_sweeps(0, false);
 #pragma unroll
-        for (int m = 0; m < 9; ++m) gx[m] = R2[m * SZ + qs];
+        for (int m = 0; m < 9; ++m) gx[m] = R2[garr_m<kMap>(m) * SZ + qs];
       }
     }
     if (CART) {  // diagonal J0^-1 (entries 0, 4, 8)
@@ -909,18 +961,18 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       } else {
         if constexpr (SM::kGx3) {
           // R2 / R1 were last read before the barriers of the x pass
-          fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, q);
+          fw_x<T, N>(&sm.stage[buf][el][3][0], R2, R2 + 3 * SZ, a.Bm, Dfx, wx);
           esync();
-          fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, q);
+          fw_y<T, N>(R2, R2 + 3 * SZ, R1, R1 + 3 * SZ, R1 + 6 * SZ, a.Bm, Dfy, wy);
           esync();
-          fw_z<T, N>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, q);
+          fw_z<T, N, kStr, 1, 0, kMap>(R1, R1 + 3 * SZ, R1 + 6 * SZ, R2, a.Bm, Dfz, wz);
           esync();
 #pragma unroll
-          for (int m = 0; m < 9; ++m) gk[m] = R2[m * SZ + qs];
+          for (int m = 0; m < 9; ++m) gk[m] = R2[garr_m<kMap>(m) * SZ + qs];
         } else {
           fwd_sweeps(3, true);
 #pragma unroll
-          for (int m = 0; m < 9; ++m) gk[m] = R1[m * SZ + qs];
+          for (int m = 0; m < 9; ++m) gk[m] = R1[garr_m<kMap>(m) * SZ + qs];
         }
       }
       if constexpr (CART) {
@@ -978,7 +1030,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     if constexpr (kFused) grad_at(0, gx);
     if constexpr (SM::kGx3) {
 #pragma unroll
-      for (int m = 0; m < 9; ++m) gx[m] = sm.r3[el][m][qs];
+      for (int m = 0; m < 9; ++m) gx[m] = sm.r3[el][garr_m<kMap>(m)][qs];
     }
     T wv[9];
     if constexpr (kPush) {
@@ -1004,7 +1056,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       tangent_integrand<T, MODEL>(mq, cb, gx, j0inv, detw, wv);
     // ---- test with the gradients of the basis functions
 #pragma unroll
-    for (int m = 0; m < 9; ++m) R1[m * SZ + qs] = wv[m];
+    for (int m = 0; m < 9; ++m) R1[garr_m<kMap>(m) * SZ + qs] = wv[m];
     esync();
     if constexpr (kDense) {
       constexpr int SR = 9 * SZ, TH = EPB * N3;
@@ -1017,11 +1069,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       const int64_t e0 = e - el;
       tr_x<T, N, TH, EPB, SR>(R1a, a.loc + e0 * 3 * N3, Btx, Dtx, tid, (int)(a.nel - e0 < EPB ? a.nel - e0 : EPB));
     } else {
-      tr_z<T, N>(R1, R2, Btz, Dtz, q);
+      tr_z<T, N, kStr, 1, 0, kMap>(R1, R2, Btz, Dtz, wz);
       esync();
-      tr_y<T, N>(R2, R1, Bty, Dty, q);
+      tr_y<T, N, kStr, 1, 0, kMap>(R2, R1, Bty, Dty, wy);
       esync();
-      if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, q);
+      if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, wx);
     }
     // No closing barrier: before the next unit's first barrier a thread only
     // zeroes its own staged words of the other buffer and issues the next
