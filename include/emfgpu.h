@@ -219,7 +219,10 @@ emfgpu_status emfgpu_mg_update_linearization(emfgpu_mg* mg, const double* d_u_fi
 emfgpu_status emfgpu_mg_precondition(emfgpu_mg* mg, const double* d_r, double* d_z, void* stream);
 /* Preconditioned CG in fp64 (BASELINE cfg4 outer solve; the reference's outer
  * solver is FGMRES, solver.hpp:120-203): x0 = 0, stop at ||r|| <= rtol ||b||.
- * mg may be NULL (unpreconditioned).  history (host, maxit+1) optional. */
+ * mg may be NULL (unpreconditioned).  history (host, maxit+1) optional.
+ * Returns EMFGPU_ERR_NUMERICAL (iterations, history and x still written) when
+ * maxit is reached without ||r|| <= rtol ||b||, or on breakdown (p^T A p <= 0),
+ * like the reference's CgNoConvergence / LinearSolveFailure (solver.hpp:202, 423). */
 emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, double* d_x, double rtol,
                                int maxit, int* iterations, double* history, void* stream);
 

@@ -200,6 +200,9 @@ __host__ __device__ constexpr int garr_m(int m) { return garr<TA>(m / 3, m % 3);
 #ifndef EMF_Q4MAP
 #define EMF_Q4MAP 1
 #endif
+#ifndef EMF_Q4MAP_TENSOR
+#define EMF_Q4MAP_TENSOR 0  // tensor measured slower with the maps (2.63 -> 2.85 ms, profiles/r02_cfg2_tenmap.txt)
+#endif
 struct Q4PenMap {
   unsigned char x[75], y[75], z[75];
 };
@@ -674,7 +677,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   const int tid = threadIdx.x;
   const int el = tid / N3, q = tid % N3;
   constexpr bool kMap = EMF_Q4MAP && P == 4 && sizeof(T) == 8 && !(EMF_V2_DENSE && EPB == 2) &&
-                        !(SM::kUk && sizeof(T) == 4);
+                        !(SM::kUk && sizeof(T) == 4) && (EMF_Q4MAP_TENSOR || STRAT != S_TENSOR);
   constexpr int kStr = 3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3;
   const unsigned pen = kMap ? c_q4pen.v[tid] : 0u;
   // Elements of a CTA only share data through their own slices, so when an

@@ -54,6 +54,36 @@ emfgpu_status guarded(std::string* slot, Fn&& fn) {
 // cuBLAS); the handle's private stream is used only by the *_host entry points.
 cudaStream_t S(void* s, cudaStream_t /*def*/) { return static_cast<cudaStream_t>(s); }
 
+// Calls on one handle are ordered among themselves on the device, whatever
+// streams and host threads they come from (the reference's apply is const and
+// may be called concurrently; here the handle's work buffers --
+// element-local results, ticket counters, staging vectors -- are shared, so
+// concurrent calls are serialised, not overlapped): an entry takes the
+// handle's lock for its enqueue, makes its stream wait for the event the
+// previous entry recorded, and records the event on its stream when it
+// leaves.  Inside a stream capture the caller owns the ordering (no event).
+struct UseGuard {
+  std::unique_lock<std::recursive_mutex> lk;
+  cudaEvent_t* ev;
+  cudaStream_t s;
+  bool active = false;
+  UseGuard(std::recursive_mutex& mu, cudaEvent_t& e, cudaStream_t st, int device) : lk(mu), ev(&e), s(st) {
+    CK(cudaSetDevice(device));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return;
+    if (!*ev) CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    CK(cudaStreamWaitEvent(s, *ev, 0));
+    active = true;
+  }
+  ~UseGuard() {
+    if (active) cudaEventRecord(*ev, s);
+  }
+  UseGuard(const UseGuard&) = delete;
+  UseGuard& operator=(const UseGuard&) = delete;
+};
+#define OP_USE(op, st) UseGuard use_guard_((op)->use_mu, (op)->ev_use, (st), (op)->L->device)
+
 // ---- 1D basis: Gauss-Lobatto nodes, Gauss rule, Lagrange tables ----------
 // Standard Newton iterations on Legendre polynomials (the construction of
 // mesh.cpp:14-120), run on the host once per level.
@@ -360,6 +390,8 @@ struct emfgpu_transfer {
   void* tmp[2] = {nullptr, nullptr};
   size_t tmp_bytes = 0;
   std::string last_error;
+  std::recursive_mutex use_mu;  // entry ordering (UseGuard)
+  cudaEvent_t ev_use = nullptr;
 };
 
 struct emfgpu_cheb {
@@ -650,6 +682,7 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   if (op->s_d2h) cudaStreamDestroy(op->s_d2h);
   if (op->ev_start) cudaEventDestroy(op->ev_start);
   if (op->ev_done) cudaEventDestroy(op->ev_done);
+  if (op->ev_use) cudaEventDestroy(op->ev_use);
   if (op->gexec) cudaGraphExecDestroy(op->gexec);
   for (int i = 0; i < emfgpu_op::kMaxChunks; ++i) {
     if (op->ev_h2d[i]) cudaEventDestroy(op->ev_h2d[i]);
@@ -693,7 +726,7 @@ static void linearize_impl(emfgpu_op* op, int64_t* be, int* bq, cudaStream_t s) 
 emfgpu_status emfgpu_op_update_linearization_host(emfgpu_op* op, const double* u_k, int64_t* be, int* bq) {
   if (!op || !u_k) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, op->stream);
     CK(cudaMemcpyAsync(op->d_ukd, u_k, sizeof(double) * op->L->ndofs, cudaMemcpyHostToDevice, op->stream));
     op->checksum = fnv1a(u_k, sizeof(double) * op->L->ndofs);
     linearize_impl(op, be, bq, op->stream);
@@ -704,8 +737,8 @@ emfgpu_status emfgpu_op_update_linearization(emfgpu_op* op, const double* d_u_k,
                                              void* stream) {
   if (!op || !d_u_k) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
-    CK(cudaSetDevice(op->L->device));
     cudaStream_t s = S(stream, op->stream);
+    OP_USE(op, s);
     CK(cudaMemcpyAsync(op->d_ukd, d_u_k, sizeof(double) * op->L->ndofs, cudaMemcpyDeviceToDevice, s));
     op->checksum = 0;
     linearize_impl(op, be, bq, s);
@@ -717,6 +750,7 @@ emfgpu_status emfgpu_op_apply(emfgpu_op* op, const void* d_x, void* d_y, void* s
   return guarded(&op->last_error, [&] {
     require_linearized(op, "apply_tangent");
     cudaStream_t s = S(stream, op->stream);
+    OP_USE(op, s);
     apply_full(op, d_x, d_y, s);
   });
 }
@@ -821,7 +855,7 @@ emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y) {
   if (!op || !x || !y) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
     require_linearized(op, "apply_tangent");
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, op->stream);
     const size_t bytes = nsize(op) * op->L->ndofs;
     if (!op->d_x) CK(cudaMalloc(&op->d_x, bytes));
     if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
@@ -839,7 +873,7 @@ emfgpu_status emfgpu_op_apply_host(emfgpu_op* op, const void* x, void* y) {
 emfgpu_status emfgpu_op_check(emfgpu_op* op, int64_t* be, int* bq) {
   if (!op) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, op->stream);
     CK(cudaDeviceSynchronize());
     check_err(op, op->stream, be, bq, "apply_tangent");
   });
@@ -877,7 +911,7 @@ static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream
 emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* nbad, void* stream) {
   if (!op || !d_diag) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, S(stream, op->stream));
     diagonal_impl(op, d_diag, nbad, S(stream, op->stream));
   });
 }
@@ -885,7 +919,7 @@ emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* n
 emfgpu_status emfgpu_op_compute_diagonal_host(emfgpu_op* op, void* diag, int64_t* nbad) {
   if (!op || !diag) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, op->stream);
     const size_t bytes = nsize(op) * op->L->ndofs;
     if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
     diagonal_impl(op, op->d_y, nbad, op->stream);
@@ -930,6 +964,7 @@ emfgpu_status emfgpu_op_apply_elements(emfgpu_op* op, const void* d_x, int k0, i
   return guarded(&op->last_error, [&] {
     require_linearized(op, "apply_tangent");
     if (k0 < 0 || k1 > op->L->nz || k0 > k1) throw ApiError(EMFGPU_ERR_CONFIG, "apply_elements: bad layer range");
+    OP_USE(op, S(stream, op->stream));
     apply_elements(op, d_x, k0, k1, S(stream, op->stream));
   });
 }
@@ -939,6 +974,7 @@ emfgpu_status emfgpu_op_apply_nodes(emfgpu_op* op, const void* d_x, void* d_y, i
   if (!op || !d_x || !d_y) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
     if (c0 < 0 || c1 >= op->L->mz || c0 > c1) throw ApiError(EMFGPU_ERR_CONFIG, "apply_nodes: bad plane range");
+    OP_USE(op, S(stream, op->stream));
     apply_nodes(op, d_x, d_y, c0, c1, glo, ghi, op->L->z_offset & 1, S(stream, op->stream));
   });
 }
@@ -954,6 +990,7 @@ emfgpu_status emfgpu_op_pack_face(emfgpu_op* op, int k, int side, void* d_face, 
     const emfgpu_level* L = op->L;
     if (k < 0 || k >= L->nz) throw ApiError(EMFGPU_ERR_CONFIG, "pack_face: bad layer");
     cudaStream_t s = S(stream, op->stream);
+    OP_USE(op, s);
     if (op->precision == 64)
       launch_pack_face<double>(static_cast<const double*>(op->d_loc), static_cast<double*>(d_face), L->nx, L->ny,
                                L->p, k, side, s);
@@ -1052,6 +1089,7 @@ emfgpu_status emfgpu_transfer_create(const emfgpu_level* fine, const emfgpu_leve
 
 void emfgpu_transfer_destroy(emfgpu_transfer* t) {
   if (!t) return;
+  if (t->ev_use) cudaEventDestroy(t->ev_use);
   for (int a = 0; a < 3; ++a) {
     free_axis(t->up[a]);
     free_axis(t->down[a]);
@@ -1087,6 +1125,7 @@ emfgpu_status emfgpu_transfer_apply(emfgpu_transfer* t, int kind, int precision,
   return guarded(&t->last_error, [&] {
     if (kind < 0 || kind > 2) throw ApiError(EMFGPU_ERR_CONFIG, "transfer: kind must be 0,1,2");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    UseGuard g(t->use_mu, t->ev_use, s, t->fine->device);
     if (precision == 64)
       transfer_run<double>(t, kind, static_cast<const double*>(in), static_cast<double*>(out), s);
     else if (precision == 32)
@@ -1168,6 +1207,7 @@ emfgpu_status emfgpu_cheb_smooth(emfgpu_cheb* c, void* d_x, const void* d_b, int
   return guarded(&c->op->last_error, [&] {
     require_linearized(c->op, "chebyshev");
     cudaStream_t s = S(stream, c->op->stream);
+    OP_USE(c->op, s);
     if (c->op->precision == 64)
       cheb_run<double>(c, static_cast<double*>(d_x), static_cast<const double*>(d_b), zero_start, s);
     else
@@ -1292,7 +1332,7 @@ emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, 
   if (!op || !d_diag || !lmin || !lmax) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
     require_linearized(op, "estimate_eigenvalues");
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, op->stream);
     if (op->precision == 64)
       lanczos<double>(op, static_cast<const double*>(d_diag), iterations, seed, lmin, lmax, op->stream);
     else
@@ -1305,6 +1345,8 @@ emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, 
 // hp-multigrid hierarchy (MgHierarchy, solver.hpp:437-581) and outer PCG
 // ============================================================================
 struct emfgpu_mg {
+  std::recursive_mutex use_mu;  // entry ordering (UseGuard)
+  cudaEvent_t ev_use = nullptr;
   emfgpu_mg_config cfg{};
   const emfgpu_level* fine = nullptr;
   std::vector<emfgpu_level*> owned;
@@ -1512,6 +1554,7 @@ void emfgpu_mg_default_config(emfgpu_mg_config* c) {
 
 void emfgpu_mg_destroy(emfgpu_mg* m) {
   if (!m) return;
+  if (m->ev_use) cudaEventDestroy(m->ev_use);
   for (auto* c : m->cheb) emfgpu_cheb_destroy(c);
   for (auto* t : m->tr) emfgpu_transfer_destroy(t);
   for (auto* o : m->ops) emfgpu_op_destroy(o);
@@ -1655,8 +1698,8 @@ static void mg_drop_graph(emfgpu_mg* m) {
 emfgpu_status emfgpu_mg_update_linearization(emfgpu_mg* m, const double* d_u_fine, void* stream) {
   if (!m || !d_u_fine) return EMFGPU_ERR_INVALID;
   return guarded(&m->last_error, [&] {
-    CK(cudaSetDevice(m->fine->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    UseGuard g(m->use_mu, m->ev_use, s, m->fine->device);
     mg_drop_graph(m);
     if (m->cfg.precision == 64)
       mg_linearize<double>(m, d_u_fine, s);
@@ -1725,6 +1768,7 @@ emfgpu_status emfgpu_mg_precondition(emfgpu_mg* m, const double* d_r, double* d_
   if (!m || !d_r || !d_z) return EMFGPU_ERR_INVALID;
   return guarded(&m->last_error, [&] {
     if (!m->ops[0]->linearized) throw ApiError(EMFGPU_ERR_STALE, "mg: update_linearization has not run");
+    UseGuard g(m->use_mu, m->ev_use, static_cast<cudaStream_t>(stream), m->fine->device);
     mg_precondition_any(m, d_r, d_z, static_cast<cudaStream_t>(stream));
   });
 }
@@ -1814,8 +1858,10 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
   return guarded(&op->last_error, [&] {
     if (op->precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "pcg: the outer operator must be fp64");
     require_linearized(op, "pcg");
-    CK(cudaSetDevice(op->L->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    OP_USE(op, s);
+    std::unique_ptr<UseGuard> mg_use;
+    if (mg) mg_use = std::make_unique<UseGuard>(mg->use_mu, mg->ev_use, s, op->L->device);
     const int64_t n = op->L->ndofs;
     // Device-resident PCG: the scalars stay on the device (sc = {rz, pAp, rr,
     // rz_new, ||b||}, ic = {iterations, done}) and, from the second iteration
@@ -1863,7 +1909,7 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
       launch_pcg_check(sc, ic, dhist, rtol, maxit, h, use_h, st);
     };
     CK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, s));
-    CK(cudaMemsetAsync(ic, 0, sizeof(int) * 2, s));
+    CK(cudaMemsetAsync(ic, 0, sizeof(int) * 3, s));  // iterations, stop, breakdown
     CK(cudaMemcpyAsync(r, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     dot_to(d_b, d_b, sc + 4, s);
     launch_pcg_sqrt(sc + 4, s);
@@ -1871,6 +1917,8 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     CK(cudaMemcpyAsync(&bnorm, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     int it = 0;
+    bool breakdown = false;
+    double last_rel = 0.0;
     if (history) history[0] = 1.0;
     if (bnorm != 0 && maxit > 0) {
       // first iteration eagerly (p = z, rz = (r, z))
@@ -1903,12 +1951,23 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
           }
         }
       }
-      CK(cudaMemcpyAsync(&it, ic, sizeof(int), cudaMemcpyDeviceToHost, s));
+      int hic3[3] = {0, 0, 0};
+      CK(cudaMemcpyAsync(hic3, ic, sizeof(hic3), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      it = hic3[0];
+      breakdown = hic3[2] != 0;
+      if (it > 0) CK(cudaMemcpy(&last_rel, dhist + it, sizeof(double), cudaMemcpyDeviceToHost));
       if (history && it > 0) CK(cudaMemcpy(history + 1, dhist + 1, sizeof(double) * it, cudaMemcpyDeviceToHost));
     }
     if (iterations) *iterations = it;
     CK(cudaStreamSynchronize(s));
+    // a solve that stopped without reaching rtol is an error (the reference's
+    // CG / FGMRES throw CgNoConvergence / LinearSolveFailure, solver.hpp:202, 423)
+    if (breakdown)
+      throw ApiError(EMFGPU_ERR_NUMERICAL, "pcg: breakdown (p^T A p <= 0) at iteration " + std::to_string(it));
+    if (it > 0 && !(last_rel <= rtol))
+      throw ApiError(EMFGPU_ERR_NUMERICAL, "pcg: no convergence in " + std::to_string(it) +
+                                               " iterations (relative residual " + std::to_string(last_rel) + ")");
   });
 }
 
@@ -1999,13 +2058,16 @@ static void residual_impl(emfgpu_op* op, const void* u, void* r, cudaStream_t s)
 
 emfgpu_status emfgpu_op_residual(emfgpu_op* op, const void* d_u, void* d_r, void* stream) {
   if (!op || !d_u || !d_r) return EMFGPU_ERR_INVALID;
-  return guarded(&op->last_error, [&] { residual_impl(op, d_u, d_r, S(stream, op->stream)); });
+  return guarded(&op->last_error, [&] {
+    OP_USE(op, S(stream, op->stream));
+    residual_impl(op, d_u, d_r, S(stream, op->stream));
+  });
 }
 
 emfgpu_status emfgpu_op_residual_host(emfgpu_op* op, const void* u, void* r) {
   if (!op || !u || !r) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, op->stream);
     const size_t bytes = nsize(op) * op->L->ndofs;
     if (!op->d_x) CK(cudaMalloc(&op->d_x, bytes));
     if (!op->d_y) CK(cudaMalloc(&op->d_y, bytes));
@@ -2250,7 +2312,9 @@ emfgpu_status emfgpu_fgmres_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_
   return guarded(&op->last_error, [&] {
     if (op->precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "fgmres: the outer operator must be fp64");
     require_linearized(op, "fgmres");
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, static_cast<cudaStream_t>(stream));
+    std::unique_ptr<UseGuard> mg_use;
+    if (mg) mg_use = std::make_unique<UseGuard>(mg->use_mu, mg->ev_use, static_cast<cudaStream_t>(stream), op->L->device);
     Krylov K(op, mg, static_cast<cudaStream_t>(stream));
     int its = 0;
     double res = 0;
@@ -2282,7 +2346,9 @@ emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, con
   if (!op || !d_u) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
     if (op->precision != 64) throw ApiError(EMFGPU_ERR_CONFIG, "newton: the operator must be fp64");
-    CK(cudaSetDevice(op->L->device));
+    OP_USE(op, static_cast<cudaStream_t>(stream));
+    std::unique_ptr<UseGuard> mg_use;
+    if (mg) mg_use = std::make_unique<UseGuard>(mg->use_mu, mg->ev_use, static_cast<cudaStream_t>(stream), op->L->device);
     emfgpu_newton_config c;
     if (cfg)
       c = *cfg;

@@ -177,15 +177,13 @@ void launch_dense_invert(const double* A, double* M, int n, int* d_singular, cud
   const unsigned b = (unsigned)((nn + 255) / 256);
   copy_left_kernel<<<b, 256, 0, st>>>(A, M, n);
   identity_right_kernel<<<b, 256, 0, st>>>(M, n);
-  static int grid = 0;
+  static std::atomic<int> shape[64];
   const int threads = 512;
-  if (grid == 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gauss_jordan_kernel, threads, 0);
-    grid = sms * std::max(1, std::min(per, 1));  // one CTA per SM: grid syncs stay cheap
-  }
+  int sms = 0, per = 0;
+  per_device_shape(shape, sms, per, [&](int& p) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, gauss_jordan_kernel, threads, 0);
+  });
+  const int grid = sms;  // one CTA per SM: grid syncs stay cheap
   void* args[] = {(void*)&M, (void*)&n, (void*)&d_singular};
   cudaLaunchCooperativeKernel((const void*)gauss_jordan_kernel, dim3(grid), dim3(threads), args, 0, st);
 }

@@ -36,17 +36,14 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
     constexpr size_t smem = sizeof(ApplyV3Warp<EMF_T, EMF_P, MODEL, STRAT>) * kV3Warps;
-    static int per_sm3 = 0, sms3 = 0;
-    if (per_sm3 == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms3, cudaDevAttrMultiProcessorCount, dev);
+    static std::atomic<int> shape3[64];
+    int per_sm3 = 0, sms3 = 0;
+    per_device_shape(shape3, sms3, per_sm3, [&](int& p) {
       cudaFuncSetAttribute(apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, apply_v3_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>,
                                                     32 * kV3Warps, smem);
-      if (per_sm3 < 1) per_sm3 = 1;
-    }
+    });
     KArgs<EMF_T> b = a;
     b.e_begin = e0;
     b.nel = e1;
@@ -56,14 +53,11 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
     return;
   }
   // persistent grid: one wave at the kernel's occupancy
-  static int per_sm = 0, sms = 0;
-  if (per_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>, THREADS, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
+  static std::atomic<int> shape[64];
+  int per_sm = 0, sms = 0;
+  per_device_shape(shape, sms, per_sm, [&](int& p) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, apply_v2_kernel<EMF_T, EMF_P, MODEL, STRAT, CART>, THREADS, 0);
+  });
   KArgs<EMF_T> b = a;
   b.e_begin = e0;
   b.nel = e1;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -182,6 +183,9 @@ struct emfgpu_op {
   unsigned* d_ctr = nullptr;
   void* d_uk_el = nullptr;  // Q3 none/scalar: u_k per element in the staging layout (KArgs::uk_el)
   mutable std::atomic<unsigned> ticket_seq{0};  // host threads may launch concurrently
+  // entry-point ordering across streams and host threads (capi.cu, UseGuard)
+  std::recursive_mutex use_mu;
+  cudaEvent_t ev_use = nullptr;
   bool linearized = false;
   uint64_t checksum = 0;
   std::string last_error;

@@ -19,6 +19,7 @@
 //   compute_diagonal        operator.hpp:772-878 (as a per-qp 3x3 quadratic form,
 //                           not 3(p+1)^3 local unit applies)
 #pragma once
+#include <atomic>
 #include "qp.cuh"
 
 namespace emfgpu {
@@ -69,6 +70,27 @@ struct FastDiv {
     return f;
   }
 };
+
+// Per-device launch-shape cache (SM count x resident CTAs per SM), computed on
+// the first launch on each device by `init` (which may also set the kernel's
+// function attributes on that device); safe for concurrent host threads (the
+// computation is idempotent, the store atomic).
+template <typename Init>
+inline void per_device_shape(std::atomic<int>* cache, int& sms, int& per_sm, Init&& init) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = cache[dev & 63].load(std::memory_order_acquire);
+  if (v == 0) {
+    int s = 0, p = 0;
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    init(p);
+    if (p < 1) p = 1;
+    v = s * 64 + p;
+    cache[dev & 63].store(v, std::memory_order_release);
+  }
+  sms = v / 64;
+  per_sm = v % 64;
+}
 
 template <typename T>
 struct KArgs {

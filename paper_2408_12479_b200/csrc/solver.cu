@@ -351,7 +351,10 @@ __global__ void pcg_check_kernel(const double* __restrict__ sc, int* ic, double*
   const int it = ic[0] + 1;
   hist[it] = rel;
   ic[0] = it;
-  const int stop = (rel <= rtol) || it >= maxit;
+  // pAp <= 0: the operator is not positive definite on p (CG breakdown)
+  const int breakdown = !(sc[1] > 0.0);
+  if (breakdown) ic[2] = 1;
+  const int stop = (rel <= rtol) || it >= maxit || breakdown;
   ic[1] = stop;
   if (use_h) cudaGraphSetConditional(h, stop ? 0u : 1u);
 }

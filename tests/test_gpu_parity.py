@@ -837,3 +837,74 @@ def test_cfg2_full_size_vs_reference(G, prec, strategy):
     assert abs(ny - ref[f"norm_y{key}"]) <= TOL[prec] * ref[f"norm_y{key}"], (ny, ref[f"norm_y{key}"])
     assert rel(ys, ref[f"y{key}_sample"]) <= TOL[prec], rel(ys, ref[f"y{key}_sample"])
     assert rel(ys, ref["y64_sample"]) <= TOL[prec]
+
+
+@pytest.mark.gpu
+def test_concurrent_applies_one_operator(G):
+    """apply_tangent is const and may be called concurrently:
+    whole applies of ONE operator issued on two streams at once, a device
+    apply on the legacy stream followed at once by the host-vector apply, and
+    two host threads calling the host-vector apply all give the serial
+    results bitwise (the handle orders its entries, capi.cu UseGuard)."""
+    import threading
+
+    import torch
+    n, p = 6, 4
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+    op.update_linearization(I.make_u0(n, n, n, p))
+    v1, v2 = I.make_v(lev.n_dofs, 1), I.make_v(lev.n_dofs, 7)
+    x1 = torch.tensor(v1, dtype=torch.float64, device="cuda")
+    x2 = torch.tensor(v2, dtype=torch.float64, device="cuda")
+    r1, r2 = torch.empty_like(x1), torch.empty_like(x1)
+    op.apply_tangent_device(x1, r1)
+    op.apply_tangent_device(x2, r2)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(20):
+        y1, y2 = torch.full_like(x1, np.nan), torch.full_like(x1, np.nan)
+        op.apply_tangent_device(x1, y1, stream=s1.cuda_stream)
+        op.apply_tangent_device(x2, y2, stream=s2.cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, r1) and torch.equal(y2, r2)
+    # device apply on the legacy stream, then the host-vector apply right away
+    y1 = torch.full_like(x1, np.nan)
+    op.apply_tangent_device(x1, y1, stream=0)
+    h2 = op.apply_tangent(v2)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, r1)
+    assert np.array_equal(h2, r2.cpu().numpy())
+    # two host threads on the host-vector entry point
+    out = {}
+
+    def worker(k, v):
+        out[k] = [op.apply_tangent(v) for _ in range(5)]
+
+    ts = [threading.Thread(target=worker, args=(k, v)) for k, v in ((1, v1), (2, v2))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for a in out[1]:
+        assert np.array_equal(a, r1.cpu().numpy())
+    for a in out[2]:
+        assert np.array_equal(a, r2.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_pcg_reports_nonconvergence(G):
+    """A PCG solve that stops at maxit above rtol returns EMFGPU_ERR_NUMERICAL
+    (the reference's solvers throw on non-convergence, solver.hpp:202, 423)."""
+    import torch
+    n, p = 4, 2
+    lev = G.FeLevel(n, p=p, map_param=(0.0,))
+    op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+    op.update_linearization(np.zeros(lev.n_dofs))
+    b = torch.tensor(I.make_v(lev.n_dofs, 2), dtype=torch.float64, device="cuda")
+    b[torch.tensor(I.dirichlet_mask(n, n, n, p, 1), device="cuda")] = 0
+    x = torch.zeros_like(b)
+    with pytest.raises(G.EmfGpuError) as ex:
+        G.pcg_solve(op, None, b, x, rtol=1e-12, maxit=3)
+    assert ex.value.code == 2 and "no convergence" in str(ex.value)
+    it, hist = G.pcg_solve(op, None, b, x, rtol=1e-8, maxit=2000)
+    assert hist[-1] <= 1e-8
