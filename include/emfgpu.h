@@ -17,6 +17,11 @@
  *   taken literally: NULL = the legacy default stream) and do not
  *   synchronise; *_host entry points take host vectors, run on the handle's
  *   private stream, synchronise and report numerical errors.
+ *   Calls on one handle (operator, hierarchy, transfer) may come from any
+ *   streams and host threads at once: the handle orders them on the device
+ *   (each call's work starts after the previous call's work on that handle,
+ *   whichever stream it ran on), so they are serialised, never interleaved.
+ *   Inside a CUDA stream capture the capturing caller owns that ordering.
  */
 #ifndef EMFGPU_H
 #define EMFGPU_H
@@ -108,6 +113,25 @@ const char* emfgpu_level_last_error(const emfgpu_level* l);
  * precision: 64 (double) or 32 (float): the Number template argument. */
 emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_material* params, int domain,
                                int strategy, int precision, emfgpu_op** out);
+/* The reference constructor's remaining arguments (operator.hpp:55-70):
+ * Formulation (material.hpp:20-23; stability 1 = stable, the default, 0 =
+ * standard) and KernelConfig (fastscalar.hpp:29-39).  The device kernels
+ * implement the stable formulation with the default KernelConfig (16 ln
+ * terms, 3 J^-2/3 Newton steps, exact exp, Newton J^-2/3); any other value
+ * returns EMFGPU_ERR_CONFIG naming the field.  NULL = the defaults. */
+typedef struct emfgpu_formulation {
+  int stability; /* 0 standard, 1 stable */
+  int domain;    /* 0 material, 1 spatial */
+} emfgpu_formulation;
+typedef struct emfgpu_kernel_config {
+  int ln_series_terms;   /* 16 */
+  int jpow_newton_steps; /* 3 */
+  int exp_mode;          /* 0 exact, 1 fast */
+  int jpow_mode;         /* 0 newton, 1 exact */
+} emfgpu_kernel_config;
+emfgpu_status emfgpu_op_create_ex(const emfgpu_level* l, int model, const emfgpu_material* params,
+                                  const emfgpu_formulation* form, int strategy, int precision,
+                                  const emfgpu_kernel_config* kernel_config, emfgpu_op** out);
 void emfgpu_op_destroy(emfgpu_op* op);
 int64_t emfgpu_op_n_dofs(const emfgpu_op* op);               /* n_dofs, operator.hpp:82 */
 int emfgpu_op_precision(const emfgpu_op* op);
@@ -139,6 +163,12 @@ emfgpu_status emfgpu_op_check(emfgpu_op* op, int64_t* bad_element, int* bad_qpoi
 /* compute_diagonal(), operator.hpp:106-107/772-878: exact diag(K), 1 on
  * constrained rows; *n_nonpositive = number of free rows with diag <= 0. */
 emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* n_nonpositive, void* stream);
+/* Same, also returning compute_diagonal's second member: the DoF indices of
+ * the free rows with diag <= 0, ascending (operator.hpp:869-877), the first
+ * min(*n_nonpositive, capacity) of them in nonpositive_idx (host).
+ * Synchronises the stream. */
+emfgpu_status emfgpu_op_compute_diagonal_indices(emfgpu_op* op, void* d_diag, int64_t* nonpositive_idx,
+                                                 int64_t capacity, int64_t* n_nonpositive, void* stream);
 emfgpu_status emfgpu_op_compute_diagonal_host(emfgpu_op* op, void* diag, int64_t* n_nonpositive);
 
 /* Byte ledger (operator.hpp:109-116, ledger.cpp:22-76): analytic per-qp
@@ -244,6 +274,25 @@ emfgpu_status emfgpu_op_residual_host(emfgpu_op* op, const void* u, void* r);
  * reference geometry of face `face` (-x,+x,-y,+y,-z,+z = 0..5). */
 emfgpu_status emfgpu_op_set_pressure(emfgpu_op* op, double pressure, int face);
 emfgpu_status emfgpu_op_set_load_scale(emfgpu_op* op, double scale); /* set_load_scale, :80 */
+/* The full Loads struct (operator.hpp:23-32): pressure on one face, a body
+ * force B(X) integrated over Omega_0 at the Gauss points, and general
+ * tractions h(X, N) on the faces flagged in traction_faces (bit f = face f);
+ * build_load_vector, operator.hpp:880-1008.  The reference's std::function
+ * members become C callbacks evaluated on the host while the load vector is
+ * built (once, here; the vector is then kept on the device).  NULL callbacks
+ * = absent.  Replaces any earlier loads of the operator. */
+typedef void (*emfgpu_body_force_fn)(const double X[3], double out[3], void* user);
+typedef void (*emfgpu_traction_fn)(const double X[3], const double N[3], double out[3], void* user);
+typedef struct emfgpu_loads {
+  double pressure;
+  int pressure_face;
+  emfgpu_body_force_fn body_force;
+  void* body_force_user;
+  emfgpu_traction_fn traction;
+  void* traction_user;
+  int traction_faces;
+} emfgpu_loads;
+emfgpu_status emfgpu_op_set_loads(emfgpu_op* op, const emfgpu_loads* loads);
 
 /* ---- Newton-Krylov on the device ------------------------
  * fgmres_solve (solver.hpp:120-203): right-preconditioned FGMRES(restart) with

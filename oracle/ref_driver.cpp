@@ -558,6 +558,35 @@ int ref_residual_with_pressure(void* l, int model, const double* params, double 
   });
 }
 
+// Body force and traction fixtures of the loads parity test (the product
+// takes them as C callbacks; tests/test_gpu_parity.py defines the same
+// expressions): B(X) = (0.3 + sin X0, X1 X2 - 0.2, 1 - X0^2),
+// h(X, N) = (N0 + 0.5 X1, 0.25 N1 X2, X0 - N2).
+int ref_residual_with_loads(void* l, int model, const double* params, double pressure, int face, int body,
+                            int traction_faces, double load_scale, const double* u, double* r) {
+  RefLevel* L = static_cast<RefLevel*>(l);
+  return guarded([&] {
+    Loads loads;
+    loads.pressure = pressure;
+    loads.pressure_face = face;
+    if (body)
+      loads.body_force = [](const Vec3d& x) { return Vec3d{{{0.3 + std::sin(x[0]), x[1] * x[2] - 0.2, 1.0 - x[0] * x[0]}}}; };
+    if (traction_faces) {
+      for (int f = 0; f < 6; ++f) loads.traction_faces[f] = (traction_faces >> f) & 1;
+      loads.traction = [](const Vec3d& x, const Vec3d& n) {
+        return Vec3d{{{n[0] + 0.5 * x[1], 0.25 * n[1] * x[2], x[0] - n[2]}}};
+      };
+    }
+    const ModelKind mk = model == 0 ? ModelKind::cnh : model == 1 ? ModelKind::inh : ModelKind::fiber;
+    ElasticOperator<double> op(*L->fe, mk, params_from(params), {Stability::stable, Domain::material},
+                               Strategy::none, KernelConfig{}, loads);
+    op.set_load_scale(load_scale);
+    std::vector<double> uv(u, u + L->fe->dof_count()), rv;
+    op.evaluate_residual(uv, rv);
+    std::memcpy(r, rv.data(), rv.size() * sizeof(double));
+  });
+}
+
 int ref_newton_pressure(void* l, int model, const double* params, double pressure, int face, int degree,
                         double deform_amp, int dirichlet_faces, int64_t coarse_direct_limit, double* u_out,
                         int* newton_its, int* fgmres_its, double* final_res) {

@@ -245,6 +245,20 @@ def residual_with_pressure(level: RefLevel, model, params, pressure, face, u, lo
     return r
 
 
+def residual_with_loads(level: RefLevel, model, params, pressure, face, body, traction_faces, u, load_scale=1.0):
+    """evaluate_residual with Loads{pressure, body_force, traction} (the fixture
+    functions of ref_driver.cpp: ref_residual_with_loads)."""
+    L = lib()
+    L.ref_residual_with_loads.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int,
+                                          C.c_double, C.c_void_p, C.c_void_p]
+    params = np.asarray(params, np.float64)
+    u = np.ascontiguousarray(u, np.float64)
+    r = np.empty_like(u)
+    _check(L.ref_residual_with_loads(level.h, MODELS[model], _p(params), pressure, face, int(body),
+                                     int(traction_faces), load_scale, _p(u), _p(r)))
+    return r
+
+
 def newton_pressure(level: RefLevel, model, params, pressure, face=1, degree=6, deform_amp=0.0, faces=1,
                     coarse_direct_limit=0):
     L = lib()

@@ -659,6 +659,25 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
   return EMFGPU_OK;
 }
 
+emfgpu_status emfgpu_op_create_ex(const emfgpu_level* l, int model, const emfgpu_material* params,
+                                  const emfgpu_formulation* form, int strategy, int precision,
+                                  const emfgpu_kernel_config* kc, emfgpu_op** out) {
+  if (!l || !params || !out) return EMFGPU_ERR_INVALID;
+  *out = nullptr;
+  auto reject = [](const std::string& what) {
+    g_error = "op: " + what + " is not implemented by the device kernels (stable formulation, default KernelConfig)";
+    return EMFGPU_ERR_CONFIG;
+  };
+  if (form && form->stability != 1) return reject("Formulation::stability = standard");
+  if (kc) {
+    if (kc->ln_series_terms != 16) return reject("KernelConfig::ln_series_terms != 16");
+    if (kc->jpow_newton_steps != 3) return reject("KernelConfig::jpow_newton_steps != 3");
+    if (kc->exp_mode != 0) return reject("KernelConfig::exp_mode = fast");
+    if (kc->jpow_mode != 0) return reject("KernelConfig::jpow_mode = exact");
+  }
+  return emfgpu_op_create(l, model, params, form ? form->domain : 0, strategy, precision, out);
+}
+
 void emfgpu_op_destroy(emfgpu_op* op) {
   if (!op) return;
   cudaFree(op->d_cache);
@@ -879,24 +898,27 @@ emfgpu_status emfgpu_op_check(emfgpu_op* op, int64_t* be, int* bq) {
   });
 }
 
-static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream_t s) {
+static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream_t s, int64_t* h_idx = nullptr,
+                          int64_t cap = 0) {
   require_linearized(op, "compute_diagonal");
   const emfgpu_level* L = op->L;
   unsigned long long* d_nbad = nullptr;
+  long long* d_idx = nullptr;
   CK(cudaMallocAsync(&d_nbad, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(d_nbad, 0, sizeof(unsigned long long), s));
+  if (h_idx && cap > 0) CK(cudaMallocAsync(&d_idx, sizeof(long long) * cap, s));
   if (op->precision == 64) {
     dispatch_diagonal<double>(op, kargs<double>(op), s);
     double* d = static_cast<double*>(d_diag);
     launch_node_gather<double>(static_cast<const double*>(op->d_loc), nullptr, nullptr, d, d, L->nx, L->ny, L->nz,
                                L->p, 0, 0, 0, L->mz - 1, L->periodic_y, s);
-    launch_diag_finish<double>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, s);
+    launch_diag_finish<double>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, d_idx, cap, s);
   } else {
     dispatch_diagonal<float>(op, kargs<float>(op), s);
     float* d = static_cast<float*>(d_diag);
     launch_node_gather<float>(static_cast<const float*>(op->d_loc), nullptr, nullptr, d, d, L->nx, L->ny, L->nz,
                               L->p, 0, 0, 0, L->mz - 1, L->periodic_y, s);
-    launch_diag_finish<float>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, s);
+    launch_diag_finish<float>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, d_nbad, d_idx, cap, s);
   }
   CK(cudaGetLastError());
   unsigned long long h = 0;
@@ -906,6 +928,17 @@ static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream
   h = *op->h_err;
   *op->h_err = ~0ull;
   if (nbad) *nbad = (int64_t)h;
+  if (d_idx) {
+    // compute_diagonal's second member: the nonpositive free rows in
+    // ascending DoF order (operator.hpp:869-877)
+    const int64_t m = std::min<int64_t>((int64_t)h, cap);
+    std::vector<long long> tmp(m);
+    if (m) CK(cudaMemcpyAsync(tmp.data(), d_idx, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(d_idx, s));
+    CK(cudaStreamSynchronize(s));
+    std::sort(tmp.begin(), tmp.end());
+    for (int64_t i = 0; i < m; ++i) h_idx[i] = tmp[i];
+  }
 }
 
 emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* nbad, void* stream) {
@@ -913,6 +946,15 @@ emfgpu_status emfgpu_op_compute_diagonal(emfgpu_op* op, void* d_diag, int64_t* n
   return guarded(&op->last_error, [&] {
     OP_USE(op, S(stream, op->stream));
     diagonal_impl(op, d_diag, nbad, S(stream, op->stream));
+  });
+}
+
+emfgpu_status emfgpu_op_compute_diagonal_indices(emfgpu_op* op, void* d_diag, int64_t* nonpositive_idx,
+                                                 int64_t capacity, int64_t* n_nonpositive, void* stream) {
+  if (!op || !d_diag || (capacity > 0 && !nonpositive_idx) || capacity < 0) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    OP_USE(op, S(stream, op->stream));
+    diagonal_impl(op, d_diag, n_nonpositive, S(stream, op->stream), nonpositive_idx, capacity);
   });
 }
 
@@ -2087,81 +2129,188 @@ emfgpu_status emfgpu_op_set_load_scale(emfgpu_op* op, double scale) {
 // Uniform pressure on one face of the (deformed) box: traction -p N on the
 // reference geometry, (p+1)^2 Gauss points per face element
 // (build_load_vector, operator.hpp:933-1001).  Setup-time, on the host.
+namespace {
+// Host sum factorization of one element field: out[(c*nq + b)*nq + a] =
+// sum M0[a][i] M1[b][j] M2[c][k] in[(k*nn + j)*nn + i] (M row-major nq x nn).
+void sf3(const double* M0, const double* M1, const double* M2, const double* in, double* out, int nq, int nn,
+         std::vector<double>& t1, std::vector<double>& t2) {
+  t1.assign((size_t)nn * nn * nq, 0.0);
+  for (int k = 0; k < nn; ++k)
+    for (int j = 0; j < nn; ++j)
+      for (int a = 0; a < nq; ++a) {
+        double v = 0.0;
+        for (int i = 0; i < nn; ++i) v += M0[a * nn + i] * in[(k * nn + j) * nn + i];
+        t1[(k * nn + j) * nq + a] = v;
+      }
+  t2.assign((size_t)nn * nq * nq, 0.0);
+  for (int k = 0; k < nn; ++k)
+    for (int b = 0; b < nq; ++b)
+      for (int a = 0; a < nq; ++a) {
+        double v = 0.0;
+        for (int j = 0; j < nn; ++j) v += M1[b * nn + j] * t1[(k * nn + j) * nq + a];
+        t2[(k * nq + b) * nq + a] = v;
+      }
+  for (int c = 0; c < nq; ++c)
+    for (int b = 0; b < nq; ++b)
+      for (int a = 0; a < nq; ++a) {
+        double v = 0.0;
+        for (int k = 0; k < nn; ++k) v += M2[c * nn + k] * t2[(k * nq + b) * nq + a];
+        out[(c * nq + b) * nq + a] = v;
+      }
+}
+
+// build_load_vector (operator.hpp:880-1008) on the host, restated: body force
+// B(X) at the Gauss points (values by B sweeps, det J0 by D/B sweeps of the
+// node coordinates, tested back by transposed B sweeps), then face tractions
+// with (p+1)^2 Gauss points per face element on the material configuration.
+void build_loads(emfgpu_op* op, const emfgpu_loads& ld) {
+  const emfgpu_level* L = op->L;
+  if (ld.pressure != 0.0 && (ld.pressure_face < 0 || ld.pressure_face > 5))
+    throw ApiError(EMFGPU_ERR_CONFIG, "loads: pressure_face must be 0..5");
+  if (L->periodic_y && ((ld.pressure != 0.0 && (ld.pressure_face == 2 || ld.pressure_face == 3)) ||
+                        (ld.traction && (ld.traction_faces & 12))))
+    throw ApiError(EMFGPU_ERR_CONFIG, "loads: periodic face");
+  std::vector<double> coords(L->ndofs), load(L->ndofs, 0.0);
+  CK(cudaMemcpy(coords.data(), L->d_coords, sizeof(double) * L->ndofs, cudaMemcpyDeviceToHost));
+  const int p = L->p, nn = p + 1, nq = p + 1, nn3 = nn * nn * nn, nq3 = nq * nq * nq;
+  const int ne[3] = {L->nx, L->ny, L->nz};
+  const int m[3] = {L->mx, L->my, L->mz};
+  const std::vector<double>& B = L->B;
+  const std::vector<double>& D = L->D;
+  std::vector<double> Bt((size_t)nn * nq);
+  for (int q = 0; q < nq; ++q)
+    for (int a = 0; a < nn; ++a) Bt[a * nq + q] = B[q * nn + a];
+  auto gnode = [&](const int* ijk, const int* loc) -> int64_t {
+    int g[3];
+    for (int d = 0; d < 3; ++d) g[d] = ijk[d] * p + loc[d];
+    if (L->periodic_y && g[1] >= m[1]) g[1] -= m[1];
+    return ((int64_t)g[2] * m[1] + g[1]) * m[0] + g[0];
+  };
+  if (ld.body_force) {
+    std::vector<int64_t> nodes(nn3);
+    std::vector<double> comp(nn3), xq(3 * (size_t)nq3), jq(9 * (size_t)nq3), vals(nq3), contrib(nn3), t1, t2;
+    for (int k = 0; k < ne[2]; ++k)
+      for (int j = 0; j < ne[1]; ++j)
+        for (int i = 0; i < ne[0]; ++i) {
+          const int ijk[3] = {i, j, k};
+          for (int c3 = 0; c3 < nn; ++c3)
+            for (int b3 = 0; b3 < nn; ++b3)
+              for (int a3 = 0; a3 < nn; ++a3) {
+                const int loc[3] = {a3, b3, c3};
+                nodes[(c3 * nn + b3) * nn + a3] = gnode(ijk, loc);
+              }
+          for (int c = 0; c < 3; ++c) {
+            for (int q = 0; q < nn3; ++q) comp[q] = coords[3 * nodes[q] + c];
+            sf3(B.data(), B.data(), B.data(), comp.data(), &xq[(size_t)c * nq3], nq, nn, t1, t2);
+            // J0 row c: dX_c / dxi_t
+            sf3(D.data(), B.data(), B.data(), comp.data(), &jq[(size_t)(3 * c + 0) * nq3], nq, nn, t1, t2);
+            sf3(B.data(), D.data(), B.data(), comp.data(), &jq[(size_t)(3 * c + 1) * nq3], nq, nn, t1, t2);
+            sf3(B.data(), B.data(), D.data(), comp.data(), &jq[(size_t)(3 * c + 2) * nq3], nq, nn, t1, t2);
+          }
+          std::vector<double> fq(3 * (size_t)nq3);
+          for (int q = 0; q < nq3; ++q) {
+            double J[9], X[3] = {xq[q], xq[nq3 + q], xq[2 * (size_t)nq3 + q]}, f[3] = {0, 0, 0};
+            for (int t = 0; t < 9; ++t) J[t] = jq[(size_t)t * nq3 + q];
+            const double det = (J[0] * (J[4] * J[8] - J[5] * J[7]) - J[1] * (J[3] * J[8] - J[5] * J[6])) +
+                               J[2] * (J[3] * J[7] - J[4] * J[6]);
+            const int qa = q % nq, qb = (q / nq) % nq, qc = q / (nq * nq);
+            const double w = L->qwts[qa] * L->qwts[qb] * L->qwts[qc];
+            ld.body_force(X, f, ld.body_force_user);
+            for (int c = 0; c < 3; ++c) fq[(size_t)c * nq3 + q] = f[c] * det * w;
+          }
+          for (int c = 0; c < 3; ++c) {
+            sf3(Bt.data(), Bt.data(), Bt.data(), &fq[(size_t)c * nq3], contrib.data(), nn, nq, t1, t2);
+            for (int q = 0; q < nn3; ++q) load[3 * nodes[q] + c] += contrib[q];
+          }
+        }
+  }
+  auto add_face = [&](int face, auto&& traction) {
+    const int axis = face / 2, t1 = (axis + 1) % 3, t2 = (axis + 2) % 3;
+    const bool upper = face % 2 == 1;
+    for (int ej = 0; ej < ne[t2]; ++ej)
+      for (int ei = 0; ei < ne[t1]; ++ei) {
+        int idx[3];
+        idx[axis] = upper ? ne[axis] - 1 : 0;
+        idx[t1] = ei;
+        idx[t2] = ej;
+        for (int q2 = 0; q2 < nq; ++q2)
+          for (int q1 = 0; q1 < nq; ++q1) {
+            double x[3] = {0, 0, 0}, g1[3] = {0, 0, 0}, g2[3] = {0, 0, 0};
+            for (int a2 = 0; a2 < nn; ++a2)
+              for (int a1 = 0; a1 < nn; ++a1) {
+                const double v1 = B[q1 * nn + a1], d1 = D[q1 * nn + a1];
+                const double v2 = B[q2 * nn + a2], d2 = D[q2 * nn + a2];
+                int loc[3];
+                loc[axis] = upper ? p : 0;
+                loc[t1] = a1;
+                loc[t2] = a2;
+                const int64_t g = gnode(idx, loc);
+                for (int c = 0; c < 3; ++c) {
+                  const double xc = coords[3 * g + c];
+                  x[c] += v1 * v2 * xc;
+                  g1[c] += d1 * v2 * xc;
+                  g2[c] += v1 * d2 * xc;
+                }
+              }
+            const double nrm[3] = {g1[1] * g2[2] - g1[2] * g2[1], g1[2] * g2[0] - g1[0] * g2[2],
+                                   g1[0] * g2[1] - g1[1] * g2[0]};
+            const double sgn = upper ? 1.0 : -1.0;
+            const double area = std::sqrt((nrm[0] * nrm[0] + nrm[1] * nrm[1]) + nrm[2] * nrm[2]);
+            const double unit[3] = {sgn * nrm[0] / area, sgn * nrm[1] / area, sgn * nrm[2] / area};
+            double h[3] = {0, 0, 0};
+            traction(x, unit, h);
+            const double w = L->qwts[q1] * L->qwts[q2] * area;
+            for (int a2 = 0; a2 < nn; ++a2)
+              for (int a1 = 0; a1 < nn; ++a1) {
+                const double phi = B[q1 * nn + a1] * B[q2 * nn + a2];
+                int loc[3];
+                loc[axis] = upper ? p : 0;
+                loc[t1] = a1;
+                loc[t2] = a2;
+                const int64_t g = gnode(idx, loc);
+                for (int c = 0; c < 3; ++c) load[3 * g + c] += phi * w * h[c];
+              }
+          }
+      }
+  };
+  if (ld.pressure != 0.0) {
+    const double pm = ld.pressure;
+    add_face(ld.pressure_face, [pm](const double*, const double* nrm, double* h) {
+      for (int c = 0; c < 3; ++c) h[c] = -pm * nrm[c];
+    });
+  }
+  if (ld.traction)
+    for (int face = 0; face < 6; ++face)
+      if (ld.traction_faces & (1 << face))
+        add_face(face, [&](const double* x, const double* nrm, double* h) { ld.traction(x, nrm, h, ld.traction_user); });
+  const size_t ns = nsize(op);
+  if (!op->d_load) CK(cudaMalloc(&op->d_load, ns * L->ndofs));
+  if (op->precision == 64) {
+    CK(cudaMemcpy(op->d_load, load.data(), sizeof(double) * L->ndofs, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> lf(load.begin(), load.end());
+    CK(cudaMemcpy(op->d_load, lf.data(), sizeof(float) * L->ndofs, cudaMemcpyHostToDevice));
+  }
+}
+}  // namespace
+
 emfgpu_status emfgpu_op_set_pressure(emfgpu_op* op, double pressure, int face) {
   if (!op) return EMFGPU_ERR_INVALID;
   return guarded(&op->last_error, [&] {
     if (face < 0 || face > 5) throw ApiError(EMFGPU_ERR_CONFIG, "pressure: face must be 0..5");
-    const emfgpu_level* L = op->L;
-    if (L->periodic_y && (face == 2 || face == 3)) throw ApiError(EMFGPU_ERR_CONFIG, "pressure: periodic face");
-    CK(cudaSetDevice(L->device));
-    std::vector<double> coords(L->ndofs), load(L->ndofs, 0.0);
-    CK(cudaMemcpy(coords.data(), L->d_coords, sizeof(double) * L->ndofs, cudaMemcpyDeviceToHost));
-    const int p = L->p, nn = p + 1, nq = p + 1;
-    const int axis = face / 2, t1 = (axis + 1) % 3, t2 = (axis + 2) % 3;
-    const bool upper = face % 2 == 1;
-    const int ne[3] = {L->nx, L->ny, L->nz};
-    const int m[3] = {L->mx, L->my, L->mz};
-    const std::vector<double>& B = L->B;
-    const std::vector<double>& D = L->D;
-    auto gnode = [&](const int* ijk, const int* loc) -> int64_t {
-      int g[3];
-      for (int d = 0; d < 3; ++d) g[d] = ijk[d] * p + loc[d];
-      if (L->periodic_y && g[1] >= m[1]) g[1] -= m[1];
-      return ((int64_t)g[2] * m[1] + g[1]) * m[0] + g[0];
-    };
-    if (pressure != 0.0)
-      for (int ej = 0; ej < ne[t2]; ++ej)
-        for (int ei = 0; ei < ne[t1]; ++ei) {
-          int idx[3];
-          idx[axis] = upper ? ne[axis] - 1 : 0;
-          idx[t1] = ei;
-          idx[t2] = ej;
-          for (int q2 = 0; q2 < nq; ++q2)
-            for (int q1 = 0; q1 < nq; ++q1) {
-              double x[3] = {0, 0, 0}, g1[3] = {0, 0, 0}, g2[3] = {0, 0, 0};
-              for (int a2 = 0; a2 < nn; ++a2)
-                for (int a1 = 0; a1 < nn; ++a1) {
-                  const double v1 = B[q1 * nn + a1], d1 = D[q1 * nn + a1];
-                  const double v2 = B[q2 * nn + a2], d2 = D[q2 * nn + a2];
-                  int loc[3];
-                  loc[axis] = upper ? p : 0;
-                  loc[t1] = a1;
-                  loc[t2] = a2;
-                  const int64_t g = gnode(idx, loc);
-                  for (int c = 0; c < 3; ++c) {
-                    const double xc = coords[3 * g + c];
-                    x[c] += v1 * v2 * xc;
-                    g1[c] += d1 * v2 * xc;
-                    g2[c] += v1 * d2 * xc;
-                  }
-                }
-              const double nrm[3] = {g1[1] * g2[2] - g1[2] * g2[1], g1[2] * g2[0] - g1[0] * g2[2],
-                                     g1[0] * g2[1] - g1[1] * g2[0]};
-              const double sgn = upper ? 1.0 : -1.0;
-              const double area = std::sqrt((nrm[0] * nrm[0] + nrm[1] * nrm[1]) + nrm[2] * nrm[2]);
-              const double h[3] = {-pressure * (sgn * nrm[0] / area), -pressure * (sgn * nrm[1] / area),
-                                   -pressure * (sgn * nrm[2] / area)};
-              const double w = L->qwts[q1] * L->qwts[q2] * area;
-              for (int a2 = 0; a2 < nn; ++a2)
-                for (int a1 = 0; a1 < nn; ++a1) {
-                  const double phi = B[q1 * nn + a1] * B[q2 * nn + a2];
-                  int loc[3];
-                  loc[axis] = upper ? p : 0;
-                  loc[t1] = a1;
-                  loc[t2] = a2;
-                  const int64_t g = gnode(idx, loc);
-                  for (int c = 0; c < 3; ++c) load[3 * g + c] += phi * w * h[c];
-                }
-            }
-        }
-    const size_t ns = nsize(op);
-    if (!op->d_load) CK(cudaMalloc(&op->d_load, ns * L->ndofs));
-    if (op->precision == 64) {
-      CK(cudaMemcpy(op->d_load, load.data(), sizeof(double) * L->ndofs, cudaMemcpyHostToDevice));
-    } else {
-      std::vector<float> lf(load.begin(), load.end());
-      CK(cudaMemcpy(op->d_load, lf.data(), sizeof(float) * L->ndofs, cudaMemcpyHostToDevice));
-    }
+    OP_USE(op, op->stream);
+    emfgpu_loads ld{};
+    ld.pressure = pressure;
+    ld.pressure_face = face;
+    build_loads(op, ld);
+  });
+}
+
+emfgpu_status emfgpu_op_set_loads(emfgpu_op* op, const emfgpu_loads* loads) {
+  if (!op || !loads) return EMFGPU_ERR_INVALID;
+  return guarded(&op->last_error, [&] {
+    OP_USE(op, op->stream);
+    build_loads(op, *loads);
   });
 }
 

@@ -109,7 +109,7 @@ void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int s
 // (operator.hpp:869-877).
 template <typename T>
 __global__ void diag_finish_kernel(T* d, int64_t nnodes, int mx, int my, int mz, int faces,
-                                   unsigned long long* nbad) {
+                                   unsigned long long* nbad, long long* bad_idx, long long cap) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= nnodes) return;
   const int a = (int)(idx % mx), b = (int)((idx / mx) % my), c = (int)(idx / ((int64_t)mx * my));
@@ -117,15 +117,20 @@ __global__ void diag_finish_kernel(T* d, int64_t nnodes, int mx, int my, int mz,
     d[3 * idx] = d[3 * idx + 1] = d[3 * idx + 2] = T(1);
     return;
   }
-  int bad = 0;
-  for (int comp = 0; comp < 3; ++comp) bad += !(d[3 * idx + comp] > T(0));
-  if (bad) atomicAdd(nbad, (unsigned long long)bad);
+  // nonpositive free rows: counted, and their DoF indices appended (unordered;
+  // the host sorts them into the reference's ascending order)
+  for (int comp = 0; comp < 3; ++comp)
+    if (!(d[3 * idx + comp] > T(0))) {
+      const unsigned long long pos = atomicAdd(nbad, 1ull);
+      if (bad_idx && (long long)pos < cap) bad_idx[pos] = 3 * idx + comp;
+    }
 }
 
 template <typename T>
 void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces, unsigned long long* nbad,
-                        cudaStream_t s) {
-  diag_finish_kernel<T><<<(unsigned)((nnodes + 255) / 256), 256, 0, s>>>(d, nnodes, mx, my, mz, faces, nbad);
+                        long long* bad_idx, long long cap, cudaStream_t s) {
+  diag_finish_kernel<T><<<(unsigned)((nnodes + 255) / 256), 256, 0, s>>>(d, nnodes, mx, my, mz, faces, nbad, bad_idx,
+                                                                          cap);
 }
 
 template void launch_node_gather<double>(const double*, const double*, const double*, const double*, double*, int,
@@ -134,7 +139,9 @@ template void launch_node_gather<float>(const float*, const float*, const float*
                                         int, int, int, int, int, int, int, cudaStream_t, bool);
 template void launch_pack_face<double>(const double*, double*, int, int, int, int, int, cudaStream_t);
 template void launch_pack_face<float>(const float*, float*, int, int, int, int, int, cudaStream_t);
-template void launch_diag_finish<double>(double*, int64_t, int, int, int, int, unsigned long long*, cudaStream_t);
-template void launch_diag_finish<float>(float*, int64_t, int, int, int, int, unsigned long long*, cudaStream_t);
+template void launch_diag_finish<double>(double*, int64_t, int, int, int, int, unsigned long long*, long long*,
+                                         long long, cudaStream_t);
+template void launch_diag_finish<float>(float*, int64_t, int, int, int, int, unsigned long long*, long long*,
+                                        long long, cudaStream_t);
 
 }  // namespace emfgpu

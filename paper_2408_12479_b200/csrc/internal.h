@@ -39,7 +39,7 @@ template <typename T>
 void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int side, cudaStream_t s);
 template <typename T>
 void launch_diag_finish(T* d, int64_t nnodes, int mx, int my, int mz, int faces, unsigned long long* nbad,
-                        cudaStream_t s);
+                        long long* bad_idx, long long cap, cudaStream_t s);
 
 // coarse.cu: dense coarse solve (probing assembly, Gauss-Jordan inverse, GEMV)
 template <typename T>

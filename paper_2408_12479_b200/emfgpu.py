@@ -100,6 +100,32 @@ class NewtonConfig(C.Structure):
                 ("max_restarts", C.c_int)]
 
 
+BODY_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+TRACTION_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+
+
+class Loads(C.Structure):
+    """emfgpu_loads (Loads, operator.hpp:23-32)."""
+    _fields_ = [("pressure", C.c_double), ("pressure_face", C.c_int), ("body_force", BODY_FN),
+                ("body_force_user", C.c_void_p), ("traction", TRACTION_FN), ("traction_user", C.c_void_p),
+                ("traction_faces", C.c_int)]
+
+
+class Formulation(C.Structure):
+    """emfgpu_formulation (Formulation, material.hpp:20-23): stability 1 = stable."""
+    _fields_ = [("stability", C.c_int), ("domain", C.c_int)]
+
+
+class KernelConfig(C.Structure):
+    """emfgpu_kernel_config (KernelConfig, fastscalar.hpp:29-39), defaults 16, 3, exact, newton."""
+    _fields_ = [("ln_series_terms", C.c_int), ("jpow_newton_steps", C.c_int), ("exp_mode", C.c_int),
+                ("jpow_mode", C.c_int)]
+
+    @classmethod
+    def default(cls):
+        return cls(16, 3, 0, 0)
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -154,6 +180,10 @@ def lib():
             "emfgpu_op_residual": (st, [vp, vp, vp, vp]),
             "emfgpu_op_residual_host": (st, [vp, vp, vp]),
             "emfgpu_op_set_pressure": (st, [vp, C.c_double, C.c_int]),
+            "emfgpu_op_set_loads": (st, [vp, C.POINTER(Loads)]),
+            "emfgpu_op_compute_diagonal_indices": (st, [vp, vp, vp, i64, C.POINTER(i64), vp]),
+            "emfgpu_op_create_ex": (st, [vp, C.c_int, C.POINTER(Material), C.POINTER(Formulation), C.c_int,
+                                         C.c_int, C.POINTER(KernelConfig), C.POINTER(vp)]),
             "emfgpu_op_set_load_scale": (st, [vp, C.c_double]),
             "emfgpu_fgmres_solve": (st, [vp, vp, vp, vp, C.c_double, C.c_double, C.c_int, C.c_int,
                                          C.POINTER(C.c_int), C.POINTER(C.c_double), vp]),
@@ -271,7 +301,7 @@ class ElasticOperator:
     device tensors and a stream and do not synchronise."""
 
     def __init__(self, level: FeLevel, model="cnh", params: MaterialParams | None = None, strategy="none",
-                 precision=64, domain=0):
+                 precision=64, domain=0, stability="stable", kernel_config: KernelConfig | None = None):
         self.level = level
         self.params = params or MaterialParams()
         if isinstance(domain, str):
@@ -279,9 +309,12 @@ class ElasticOperator:
         self.model, self.strategy, self.precision, self.domain = model, strategy, precision, domain
         self.dtype = np.float64 if precision == 64 else np.float32
         self._mat = self.params.to_c()
+        self._loads_keep = None
         h = C.c_void_p()
-        st = lib().emfgpu_op_create(level.h, MODELS[model], C.byref(self._mat), domain, STRATEGIES[strategy],
-                                    precision, C.byref(h))
+        form = Formulation({"standard": 0, "stable": 1}[stability], domain)
+        kc = kernel_config or KernelConfig.default()
+        st = lib().emfgpu_op_create_ex(level.h, MODELS[model], C.byref(self._mat), C.byref(form),
+                                       STRATEGIES[strategy], precision, C.byref(kc), C.byref(h))
         if st:
             raise EmfGpuError(st, lib().emfgpu_global_last_error().decode())
         self.h = h.value
@@ -353,6 +386,16 @@ class ElasticOperator:
             self._raise(st)
         return d, nb.value
 
+    def compute_diagonal_indices(self, d_diag, capacity=1 << 16, stream=None):
+        """compute_diagonal's pair (operator.hpp:106-107, 869-877) on a device
+        diagonal: returns the ascending DoF indices of the free rows with
+        diag <= 0 (at most `capacity`) and their total count."""
+        idx = np.empty(capacity, np.int64)
+        nb = C.c_int64(0)
+        self._ok(lib().emfgpu_op_compute_diagonal_indices(self.h, _ptr(d_diag), idx.ctypes.data, capacity,
+                                                          C.byref(nb), _stream(stream)))
+        return idx[:min(nb.value, capacity)].copy(), nb.value
+
     def compute_diagonal_device(self, d_diag, stream=None):
         nb = C.c_int64(0)
         st = lib().emfgpu_op_compute_diagonal(self.h, _ptr(d_diag), C.byref(nb), _stream(stream))
@@ -402,6 +445,23 @@ class ElasticOperator:
     def set_pressure(self, pressure, face=1):
         """Loads{pressure, pressure_face} (operator.hpp:23-32): -p N traction on `face`."""
         self._ok(lib().emfgpu_op_set_pressure(self.h, float(pressure), int(face)))
+
+    def set_loads(self, pressure=0.0, pressure_face=1, body_force=None, traction=None, traction_faces=()):
+        """The full Loads struct (operator.hpp:23-32): body_force(X) -> 3 values,
+        traction(X, N) -> 3 values on the faces listed in traction_faces (0..5).
+        The callbacks run on the host while the load vector is built."""
+        def bf(x, out, _u):
+            v = body_force((x[0], x[1], x[2]))
+            out[0], out[1], out[2] = v
+        def tf(x, n, out, _u):
+            v = traction((x[0], x[1], x[2]), (n[0], n[1], n[2]))
+            out[0], out[1], out[2] = v
+        mask = 0
+        for f in traction_faces:
+            mask |= 1 << int(f)
+        ld = Loads(float(pressure), int(pressure_face), BODY_FN(bf) if body_force else BODY_FN(),
+                   None, TRACTION_FN(tf) if traction else TRACTION_FN(), None, mask)
+        self._ok(lib().emfgpu_op_set_loads(self.h, C.byref(ld)))
 
     def set_load_scale(self, scale):
         self._ok(lib().emfgpu_op_set_load_scale(self.h, float(scale)))

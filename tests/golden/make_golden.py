@@ -170,6 +170,30 @@ def newton():
     np.savez_compressed(os.path.join(OUT, "newton.npz"), **out)
 
 
+# loads cases: (name, model, lmax, p, deform amplitude, pressure, face, body force, traction faces)
+LOADS = [
+    ("inh_p2_n4_curved", "inh", 2, 2, 0.05, 0.2, 1, 1, 0b101010),
+    ("cnh_p3_n2_curved", "cnh", 1, 3, 0.05, 0.0, 1, 1, 0b000110),
+    ("fiber_p4_n2_affine", "fiber", 1, 4, 0.0, 0.1, 4, 0, 0b100001),
+]
+
+
+def loads():
+    """evaluate_residual with the full Loads struct (operator.hpp:23-32,
+    880-1008): face pressure, body force B(X) and tractions h(X, N) on flagged
+    faces (the fixture functions of oracle/ref_driver.cpp), at a seeded state."""
+    out = {}
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=KAPPA)
+    for name, model, lmax, p, damp, pres, face, body, tf in LOADS:
+        n = 1 << lmax
+        L = R.RefLevel(1, lmax, p, damp, 1)
+        u = I.make_u0(n, n, n, p, amp=0.05)
+        out[f"{name}_r"] = R.residual_with_loads(L, model, prm, pres, face, body, tf, u, 0.5)
+        print("loads", name, L.ndofs, np.linalg.norm(out[f"{name}_r"]))
+    out["params"] = prm
+    np.savez_compressed(os.path.join(OUT, "loads.npz"), **out)
+
+
 SPATIAL = [("cnh_p3_n2_curved", "cnh", 1, 3, 0.05), ("inh_p2_n4_curved", "inh", 2, 2, 0.05),
            ("fiber_p2_n2_curved", "fiber", 1, 2, 0.05), ("inh_p4_n2_affine", "inh", 1, 4, 0.0)]
 
