@@ -331,7 +331,8 @@ def time_variant(G, args, lev, part, sop_cls, u0, v, model, params, prec, strat,
         ev[0].record(stream)
         # one GPU: the whole apply in one call (element kernel + node kernel
         # as its programmatic dependent); the element kernel is timed alone below
-        sop.apply(x, y, ev_mid=None if world == 1 else ev[1])
+        sop.apply(x, y)
+        ev[1].record(stream)
         ev[2].record(stream)
         tot.append(ev)
     barrier()

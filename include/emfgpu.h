@@ -265,6 +265,47 @@ emfgpu_status emfgpu_op_set_fibre_frame(emfgpu_op* op, int kind);
 /* Per-qp H4,H6 (12 per qp, SoA field-major) and M1_4,M1_6 (6 per qp). */
 emfgpu_status emfgpu_op_fibre_field(const emfgpu_op* op, double* h_out, double* m1_out);
 
+/* ---- z-slab multi-GPU apply ------------------------
+ * One slab per GPU: rank r of `world` owns element layers [k0, k1) of the
+ * global box; its level is created with z_offset = k0, the slab's node
+ * planes [k0 p, k1 p] (interface planes duplicated) and the slab's own
+ * Dirichlet faces.  The reference has no distributed path; these calls replace
+ * ElasticOperator::apply_tangent for a partitioned operator.
+ * Communicator: NCCL, loaded at run time (libnccl.so.2 already in the process,
+ * e.g. torch's, else the system one).  emfgpu_comm_unique_id on one rank, the
+ * 128 bytes shipped to the others by the caller, emfgpu_comm_create on every
+ * rank (ncclGetUniqueId / ncclCommInitRank); or emfgpu_comm_wrap of an
+ * existing ncclComm_t (not destroyed by emfgpu_comm_destroy). */
+typedef struct emfgpu_comm emfgpu_comm;
+typedef struct emfgpu_slab emfgpu_slab;
+emfgpu_status emfgpu_comm_unique_id(unsigned char id[128]);
+emfgpu_status emfgpu_comm_create(const unsigned char id[128], int world, int rank, int device, emfgpu_comm** out);
+emfgpu_status emfgpu_comm_wrap(void* nccl_comm, int world, int rank, emfgpu_comm** out);
+void emfgpu_comm_destroy(emfgpu_comm* c);
+/* comm may be NULL for world == 1 and for single-process groups. */
+emfgpu_status emfgpu_slab_create(emfgpu_op* op, int rank, int world, emfgpu_comm* comm, emfgpu_slab** out);
+void emfgpu_slab_destroy(emfgpu_slab* s);
+const char* emfgpu_slab_last_error(const emfgpu_slab* s);
+/* y = K x on this rank's slab vectors: boundary element layers, interface
+ * faces packed, NCCL send/recv with the z neighbours on the slab's own
+ * communication stream overlapped with the interior layers, node phase with
+ * the ghost faces in the global colour order.  Each rank's y is bitwise the
+ * single-GPU result on its node planes.  Stream-ordered, graph-capturable. */
+emfgpu_status emfgpu_slab_apply(emfgpu_slab* s, const void* d_x, void* d_y, void* stream);
+/* One process driving all n slabs (slabs[r] = rank r of world n; one per
+ * device, or several on one device): the same apply with the ghost faces
+ * copied peer-to-peer (NVLink) instead of NCCL, phases enqueued in order
+ * across the group so no kernel ever waits on another. */
+emfgpu_status emfgpu_slab_group_apply(emfgpu_slab* const* slabs, int n, const void* const* d_x, void* const* d_y,
+                                      void* const* streams);
+/* Global dot of two slab vectors into a device double: each interface plane
+ * counted once (owned by the upper rank); the per-rank fixed-order partials
+ * are all-gathered (NCCL) and summed in rank order on the device --
+ * identical on every rank, no host synchronisation. */
+emfgpu_status emfgpu_slab_dot(emfgpu_slab* s, const void* d_a, const void* d_b, double* d_out, void* stream);
+emfgpu_status emfgpu_slab_group_dot(emfgpu_slab* const* slabs, int n, const void* const* d_a, const void* const* d_b,
+                                    double* const* d_out, void* const* streams);
+
 /* ---- residual and loads ----------------------------------
  * evaluate_residual(u, r), operator.hpp:94-95/623-641 (both domains):
  * r_i = (Grad v_i, F S) - load_scale * load_i, Dirichlet rows zeroed. */

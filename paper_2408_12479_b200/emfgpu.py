@@ -181,6 +181,18 @@ def lib():
             "emfgpu_op_residual_host": (st, [vp, vp, vp]),
             "emfgpu_op_set_pressure": (st, [vp, C.c_double, C.c_int]),
             "emfgpu_op_set_loads": (st, [vp, C.POINTER(Loads)]),
+            "emfgpu_comm_unique_id": (st, [vp]),
+            "emfgpu_comm_create": (st, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+            "emfgpu_comm_wrap": (st, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
+            "emfgpu_comm_destroy": (None, [vp]),
+            "emfgpu_slab_create": (st, [vp, C.c_int, C.c_int, vp, C.POINTER(vp)]),
+            "emfgpu_slab_destroy": (None, [vp]),
+            "emfgpu_slab_last_error": (C.c_char_p, [vp]),
+            "emfgpu_slab_apply": (st, [vp, vp, vp, vp]),
+            "emfgpu_slab_group_apply": (st, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+            "emfgpu_slab_dot": (st, [vp, vp, vp, vp, vp]),
+            "emfgpu_slab_group_dot": (st, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                           C.POINTER(vp)]),
             "emfgpu_op_compute_diagonal_indices": (st, [vp, vp, vp, i64, C.POINTER(i64), vp]),
             "emfgpu_op_create_ex": (st, [vp, C.c_int, C.POINTER(Material), C.POINTER(Formulation), C.c_int,
                                          C.c_int, C.POINTER(KernelConfig), C.POINTER(vp)]),
@@ -685,3 +697,77 @@ def write_sweep_csv(scales, err, inv, path):
                     for q in SWEEP_QUANTITIES:
                         f.write(f"{s:.9e},{m},{fm},{q},{err[i, c]:.9e},{inv[i, c]}\n")
                         c += 1
+
+
+# ---- z-slab multi-GPU (emfgpu_slab_*) ---------------------------
+class Comm:
+    """NCCL communicator of the slab layer (emfgpu_comm_*): rank 0 makes the
+    unique id, the caller ships the 128 bytes to the other ranks."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(lib().emfgpu_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int = 0):
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(lib().emfgpu_comm_create(buf, world, rank, device, C.byref(h)))
+        self.h, self.world, self.rank = h.value, world, rank
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_comm_destroy(self.h)
+            self.h = None
+
+
+class Slab:
+    """emfgpu_slab: rank `rank` of `world` z slabs around an ElasticOperator
+    whose level holds the slab (z_offset = first element layer)."""
+
+    def __init__(self, op: ElasticOperator, rank: int, world: int, comm: Comm | None = None):
+        self.op, self.rank, self.world, self.comm = op, rank, world, comm
+        h = C.c_void_p()
+        st = lib().emfgpu_slab_create(op.h, rank, world, comm.h if comm else None, C.byref(h))
+        if st:
+            op._raise(st)
+        self.h = h.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_slab_destroy(self.h)
+            self.h = None
+
+    def _ok(self, st):
+        if st:
+            raise EmfGpuError(st, lib().emfgpu_slab_last_error(self.h).decode())
+
+    def apply(self, d_x, d_y, stream=None):
+        self._ok(lib().emfgpu_slab_apply(self.h, _ptr(d_x), _ptr(d_y), _stream(stream)))
+
+    def dot(self, d_a, d_b, d_out, stream=None):
+        """Global dot into the device double d_out (no host sync)."""
+        self._ok(lib().emfgpu_slab_dot(self.h, _ptr(d_a), _ptr(d_b), _ptr(d_out), _stream(stream)))
+
+
+def _arr(vals):
+    return (C.c_void_p * len(vals))(*vals)
+
+
+def slab_group_apply(slabs, xs, ys, streams):
+    """One process driving all slabs: peer-copied ghost faces (emfgpu_slab_group_apply)."""
+    n = len(slabs)
+    st = lib().emfgpu_slab_group_apply(_arr([s.h for s in slabs]), n, _arr([_ptr(x) for x in xs]),
+                                       _arr([_ptr(y) for y in ys]), _arr([_stream(t) for t in streams]))
+    if st:
+        raise EmfGpuError(st, lib().emfgpu_slab_last_error(slabs[0].h).decode())
+
+
+def slab_group_dot(slabs, a_s, b_s, outs, streams):
+    n = len(slabs)
+    st = lib().emfgpu_slab_group_dot(_arr([s.h for s in slabs]), n, _arr([_ptr(a) for a in a_s]),
+                                     _arr([_ptr(b) for b in b_s]), _arr([_ptr(o) for o in outs]),
+                                     _arr([_stream(t) for t in streams]))
+    if st:
+        raise EmfGpuError(st, lib().emfgpu_slab_last_error(slabs[0].h).decode())

@@ -12,9 +12,14 @@ GPU, torch.distributed over NCCL).  The reference has no distributed path
   the reference's global colour order, so every rank's result is bitwise the
   single-GPU result (no data-path collective besides the face exchange).
 
-The element "engine" is duck-typed (apply_elements / pack_face / apply_nodes /
-face_values): the CUDA ElasticOperator on GPUs, an oracle-backed engine in
-the CPU gloo tests.
+On GPUs the whole apply runs below the C ABI (emfgpu_slab_apply, csrc/slab.cu:
+NCCL send/recv on the slab's communication stream, event-ordered, graph-
+capturable; emfgpu_slab_dot for the rank-ordered device dot); this module
+only partitions the box, builds the slab's level and creates the NCCL
+communicator (unique id broadcast over torch.distributed).  The Python
+exchange below drives a duck-typed element engine (apply_elements /
+pack_face / apply_nodes / face_values) and serves the CPU gloo tests with an
+oracle-backed engine.
 """
 from __future__ import annotations
 
@@ -98,6 +103,22 @@ class SlabOperator:
         if dist is None and part.world > 1:
             import torch.distributed as dist
         self.dist = dist
+        # the CUDA operator: the slab apply and dot below the C ABI
+        self.native = hasattr(engine, "apply_tangent_device")
+        if self.native:
+            from .emfgpu import Comm, Slab
+            self.comm = None
+            if part.world > 1:
+                uid = [Comm.unique_id() if part.rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                self.comm = Comm(uid[0], part.world, part.rank, device=torch.cuda.current_device())
+            self.slab = Slab(engine, part.rank, part.world, self.comm)
+            self.dot_out = torch.zeros(1, dtype=torch.float64, device=device)
+            nzl = part.nz_local
+            n_el = 1 + (nzl > 1) + (nzl > 2)
+            self.launches_per_apply = 2 if part.world == 1 else n_el + (part.lo is not None) + (
+                part.hi is not None) + 1
+            return
         nf = engine.face_values()
         mk = lambda: torch.empty(nf, dtype=dtype, device=device)  # noqa: E731
         self.send_lo = mk() if part.lo is not None else None
@@ -114,6 +135,12 @@ class SlabOperator:
         part, e = self.part, self.e
         s = self._stream()
         nzl = part.nz_local
+        if self.native:
+            if part.world == 1:
+                e.apply_tangent_device(x, y, stream=s)  # one call: element + node phase
+            else:
+                self.slab.apply(x, y, stream=s)
+            return
         if part.world == 1:
             if ev_mid is None and hasattr(e, "apply_tangent_device"):
                 e.apply_tangent_device(x, y, stream=s)  # one call: element + node phase
@@ -156,9 +183,17 @@ class SlabOperator:
         e.apply_nodes(x, y, 0, part.mz_local - 1, ghost_lo=self.recv_lo, ghost_hi=self.recv_hi, stream=s)
         self.launches_per_apply = launches + 1
 
+    def dot_device(self, a, b):
+        """Global dot product into a device scalar (emfgpu_slab_dot: owned
+        planes, NCCL all-gather of the partials, rank-order sum; no host sync)."""
+        self.slab.dot(a, b, self.dot_out, stream=self._stream())
+        return self.dot_out
+
     def dot(self, a, b):
         """Global dot product of two slab vectors, each interface plane counted
         once (owned by the upper rank), fixed rank-order sum (bit-stable)."""
+        if self.native:
+            return float(self.dot_device(a, b).item())
         t = self.torch
         part = self.part
         plane = 3 * part.mx * part.my

@@ -977,3 +977,57 @@ def test_formulation_and_kernel_config_rejected(G):
         with pytest.raises(G.EmfGpuError) as ex:
             G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), "none", 64, kernel_config=kc)
         assert ex.value.code == 1 and field in str(ex.value)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("splits", [[(0, 1), (1, 4)], [(0, 2), (2, 3), (3, 5)]], ids=["2slabs", "3slabs"])
+def test_slab_group_apply_and_dot_bitwise(G, splits):
+    """The z-slab apply below the C ABI (emfgpu_slab_group_apply: boundary
+    layers, face packs, peer-copied ghost faces on each slab's communication
+    stream overlapped with the interior layers, node phase with ghosts) gives
+    every slab BITWISE the single-level result on its node planes, repeatedly
+    and on separate streams; the group dot counts interface planes once."""
+    import torch
+    n, p = 4, 2
+    nz = splits[-1][1]
+    lev = G.FeLevel(n, n, nz, p=p, dirichlet_faces=1 | 16)
+    u0 = I.make_u0_planes(n, n, nz, p, 0, nz * p, faces=1 | 16, extent=(1.0, 1.0, 1.0))
+    lev = G.FeLevel(n, n, nz, p=p, dirichlet_faces=1 | 16)
+    v = I.make_v(lev.n_dofs)
+    op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+    op.update_linearization(u0)
+    y_full = op.apply_tangent(v)
+    coords = lev.node_coords()
+    m = n * p + 1
+    plane = 3 * m * m
+    ops, xs, slabs, sls = [], [], [], []
+    for r, (k0, k1) in enumerate(splits):
+        sl = slice(k0 * p * plane, (k1 * p + 1) * plane)
+        faces = 1 | (16 if r == 0 else 0) | (32 if r == len(splits) - 1 else 0)
+        lv = G.FeLevel(n, n, k1 - k0, p=p, coords=coords[sl], dirichlet_faces=faces & (1 | 16), z_offset=k0)
+        o = G.ElasticOperator(lv, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+        o.update_linearization(u0[sl])
+        ops.append(o)
+        xs.append(torch.tensor(v[sl], device="cuda"))
+        sls.append(sl)
+    slabs = [G.Slab(o, r, len(splits)) for r, o in enumerate(ops)]
+    streams = [torch.cuda.Stream() for _ in splits]
+    for _ in range(3):
+        ys = [torch.full_like(x, np.nan) for x in xs]
+        G.slab_group_apply(slabs, xs, ys, streams)
+        torch.cuda.synchronize()
+        for r, sl in enumerate(sls):
+            assert np.array_equal(ys[r].cpu().numpy(), y_full[sl]), r
+    outs = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in splits]
+    G.slab_group_dot(slabs, xs, ys, outs, streams)
+    torch.cuda.synchronize()
+    vals = [float(o.item()) for o in outs]
+    assert all(vv == vals[0] for vv in vals)
+    assert abs(vals[0] - float(np.dot(v, y_full))) <= 1e-12 * abs(float(np.dot(v, y_full)))
+    # a single slab (world 1) is the plain apply
+    s1 = G.Slab(op, 0, 1)
+    x = torch.tensor(v, device="cuda")
+    y = torch.empty_like(x)
+    s1.apply(x, y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y_full)
