@@ -200,6 +200,9 @@ __host__ __device__ constexpr int garr_m(int m) { return garr<TA>(m / 3, m % 3);
 #ifndef EMF_Q4MAP
 #define EMF_Q4MAP 1
 #endif
+#ifndef EMF_Q4MAP32
+#define EMF_Q4MAP32 1
+#endif
 #ifndef EMF_Q4MAP_TENSOR
 #define EMF_Q4MAP_TENSOR 0  // tensor measured slower with the maps (2.63 -> 2.85 ms, profiles/r02_cfg2_tenmap.txt)
 #endif
@@ -226,6 +229,71 @@ constexpr Q4PenPacked q4pen_pack() {
   return r;
 }
 static __constant__ Q4PenPacked c_q4pen = q4pen_pack();
+
+// fp32 Q4 maps (4-byte words, 32 banks, whole-warp groups; tools/pencil_milp.py
+// f32_q4_maps): the fused x / u_k forward sweeps (150 pencils, rounds over
+// threads 0-124 then 0-24) and the transposed sweeps (75 pencils), arrays
+// direction-major.  Costs: wavefronts per element-sweep access, ideal 5 / 3.
+struct Q4PenMap32 {
+  unsigned char fx[150], fy[150], fz[150], tx[75], ty[75], tz[75];
+};
+static constexpr Q4PenMap32 kQ4Pen32 = {
+    // fwc_x (MILP cost 5)
+    {8, 9, 16, 20, 37, 39, 45, 47, 54, 55, 56, 57, 58, 59, 62, 81, 83, 92, 95, 97, 98, 100, 106, 107, 110,
+     114, 125, 128, 131, 134, 140, 149, 0, 1, 11, 13, 18, 19, 22, 27, 28, 29, 31, 38, 48, 67, 73, 76, 84, 85,
+     87, 90, 94, 103, 113, 120, 121, 130, 132, 133, 136, 138, 142, 143, 6, 10, 17, 23, 32, 35, 36, 40, 41,
+     43, 60, 65, 66, 69, 71, 78, 79, 80, 82, 88, 89, 91, 93, 108, 109, 116, 117, 118, 122, 126, 127, 147, 2,
+     4, 14, 15, 21, 24, 26, 33, 42, 44, 49, 51, 52, 63, 75, 77, 86, 96, 99, 101, 102, 104, 105, 119, 123,
+     124, 135, 144, 146, 3, 5, 7, 12, 25, 30, 34, 46, 50, 53, 61, 64, 68, 70, 72, 74, 111, 112, 115, 129,
+     137, 139, 141, 145, 148},
+    // fwc_y (MILP cost 5)
+    {7, 8, 9, 16, 17, 23, 36, 42, 45, 47, 48, 55, 58, 68, 69, 71, 72, 74, 76, 78, 82, 87, 98, 101, 103, 107,
+     109, 110, 128, 134, 137, 149, 0, 13, 18, 19, 31, 33, 39, 43, 51, 64, 65, 67, 73, 81, 85, 90, 91, 97, 99,
+     100, 105, 112, 120, 122, 126, 130, 132, 136, 138, 140, 142, 146, 3, 4, 10, 14, 25, 26, 32, 34, 37, 40,
+     41, 49, 52, 56, 57, 60, 61, 63, 66, 79, 106, 108, 111, 114, 116, 117, 118, 121, 127, 131, 143, 147, 2,
+     5, 6, 15, 24, 29, 35, 38, 44, 53, 54, 75, 80, 83, 84, 86, 89, 92, 93, 94, 95, 102, 104, 115, 124, 125,
+     135, 144, 145, 1, 11, 12, 20, 21, 22, 27, 28, 30, 46, 50, 59, 62, 70, 77, 88, 96, 113, 119, 123, 129,
+     133, 139, 141, 148},
+    // fwc_z (MILP cost 6)
+    {0, 1, 4, 5, 7, 8, 33, 37, 39, 45, 47, 53, 54, 55, 57, 58, 59, 68, 71, 78, 87, 88, 90, 97, 109, 114, 118,
+     119, 120, 122, 140, 149, 6, 14, 17, 18, 19, 21, 22, 31, 38, 41, 43, 44, 50, 51, 56, 64, 65, 67, 75, 76,
+     80, 81, 91, 96, 100, 105, 113, 116, 117, 138, 139, 142, 26, 28, 30, 32, 34, 36, 40, 42, 61, 66, 69, 72,
+     73, 74, 83, 85, 99, 106, 108, 121, 123, 127, 128, 129, 130, 131, 132, 133, 135, 137, 143, 147, 3, 11,
+     13, 15, 16, 24, 27, 29, 35, 48, 52, 60, 77, 79, 82, 86, 89, 92, 93, 94, 98, 101, 102, 103, 112, 124,
+     125, 126, 146, 2, 9, 10, 12, 20, 23, 25, 46, 49, 62, 63, 70, 84, 95, 104, 107, 110, 111, 115, 134, 136,
+     141, 144, 145, 148},
+    // tr_x (MILP cost 3)
+    {1, 3, 4, 5, 12, 13, 14, 15, 22, 24, 26, 27, 28, 30, 32, 34, 38, 39, 40, 41, 42, 43, 48, 49, 50, 51, 52,
+     53, 55, 57, 61, 63, 2, 6, 7, 11, 16, 17, 18, 19, 20, 21, 23, 25, 29, 31, 37, 44, 45, 46, 47, 54, 56, 58,
+     59, 60, 62, 64, 65, 67, 68, 72, 73, 74, 0, 8, 9, 10, 33, 35, 36, 66, 69, 70, 71},
+    // tr_y (MILP cost 4)
+    {0, 4, 5, 8, 9, 10, 13, 14, 15, 17, 18, 19, 21, 28, 30, 39, 41, 44, 45, 46, 50, 51, 53, 55, 56, 59, 60,
+     63, 64, 68, 70, 73, 1, 3, 6, 7, 11, 12, 16, 20, 22, 23, 25, 31, 32, 33, 35, 36, 37, 38, 40, 42, 43, 52,
+     54, 57, 58, 61, 62, 65, 69, 71, 72, 74, 2, 24, 26, 27, 29, 34, 47, 48, 49, 66, 67},
+    // tr_z (MILP cost 5)
+    {5, 7, 13, 21, 22, 23, 24, 27, 28, 33, 36, 40, 42, 43, 44, 45, 46, 47, 51, 53, 54, 57, 58, 59, 60, 62,
+     63, 65, 66, 67, 70, 73, 0, 2, 3, 4, 8, 9, 10, 12, 14, 15, 16, 17, 18, 19, 20, 25, 26, 29, 31, 34, 35,
+     37, 38, 39, 41, 49, 50, 52, 55, 61, 68, 71, 1, 6, 11, 30, 32, 48, 56, 64, 69, 72, 74}};
+struct Q4PenPacked32 {
+  unsigned v[128][3];
+};
+// per thread: [0] = fwc x round 1 | x round 2 << 8 | y r1 << 16 | y r2 << 24,
+// [1] = z r1 | z r2 << 8 | tr x << 16 | tr y << 24, [2] = tr z; 255 = none
+constexpr Q4PenPacked32 q4pen32_pack() {
+  Q4PenPacked32 r{};
+  for (int t = 0; t < 128; ++t) {
+    auto f = [&](const unsigned char* m, int round) -> unsigned {
+      const int i = round == 0 ? t : 125 + t;
+      return (round == 0 ? t < 125 : t < 25) ? (unsigned)m[i] : 255u;
+    };
+    auto g = [&](const unsigned char* m) -> unsigned { return t < 75 ? (unsigned)m[t] : 255u; };
+    r.v[t][0] = f(kQ4Pen32.fx, 0) | f(kQ4Pen32.fx, 1) << 8 | f(kQ4Pen32.fy, 0) << 16 | f(kQ4Pen32.fy, 1) << 24;
+    r.v[t][1] = f(kQ4Pen32.fz, 0) | f(kQ4Pen32.fz, 1) << 8 | g(kQ4Pen32.tx) << 16 | g(kQ4Pen32.ty) << 24;
+    r.v[t][2] = g(kQ4Pen32.tz);
+  }
+  return r;
+}
+static __constant__ Q4PenPacked32 c_q4pen32 = q4pen32_pack();
 
 // ---- pencil sweeps ------------------------------------------------------------
 // Arguments are base pointers of consecutive per-element arrays of N3 values
@@ -353,10 +421,12 @@ __device__ __forceinline__ void fw_z(const T* sbb0, const T* sbd0, const T* sdb0
 //   z: U, T, S -> U (d/dx), T (d/dy), S (d/dz)
 // With NV = 2 (x and u_k) 2*3N^2 pencils keep every lane busy for N = 4
 // (96 pencils = 3 warp-rounds of 32, vs 4 half-empty rounds one vector at a time).
-template <typename T, int N, int NV, int STRIDE>
-__device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int w) {
+template <typename T, int N, int NV, int STRIDE, bool PAIR = false>
+__device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int w, int w1 = 0) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
+  // PAIR: the thread's pencils are w and w1 (a thread -> pencil map) instead of w, w + STRIDE, ...
+  for (int it = 0, wk = w; PAIR ? it < 2 : wk < NV * 3 * L::N2; ++it, wk = PAIR ? w1 : wk + STRIDE) {
+    if (PAIR && wk >= NV * 3 * L::N2) continue;
     const int vc = wk / L::N2, r = wk % L::N2, j = r % N, k = r / N;
     T* const s = S + vc * L::SIZE;
     T* const t = Tt + vc * L::SIZE;
@@ -376,10 +446,11 @@ __device__ __forceinline__ void fwc_x(T* S, T* Tt, const T* Bm, const T* Dm, int
     }
   }
 }
-template <typename T, int N, int NV, int STRIDE>
-__device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w) {
+template <typename T, int N, int NV, int STRIDE, bool PAIR = false>
+__device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w, int w1 = 0) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
+  for (int it = 0, wk = w; PAIR ? it < 2 : wk < NV * 3 * L::N2; ++it, wk = PAIR ? w1 : wk + STRIDE) {
+    if (PAIR && wk >= NV * 3 * L::N2) continue;
     const int vc = wk / L::N2, r = wk % L::N2, i = r % N, k = r / N;
     T* const s = S + vc * L::SIZE;
     T* const t = Tt + vc * L::SIZE;
@@ -405,10 +476,11 @@ __device__ __forceinline__ void fwc_y(T* S, T* Tt, T* U, const T* Bm, const T* D
     }
   }
 }
-template <typename T, int N, int NV, int STRIDE>
-__device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w) {
+template <typename T, int N, int NV, int STRIDE, bool PAIR = false>
+__device__ __forceinline__ void fwc_z(T* S, T* Tt, T* U, const T* Bm, const T* Dm, int w, int w1 = 0) {
   using L = Lay<N, sizeof(T)>;
-  for (int wk = w; wk < NV * 3 * L::N2; wk += STRIDE) {
+  for (int it = 0, wk = w; PAIR ? it < 2 : wk < NV * 3 * L::N2; ++it, wk = PAIR ? w1 : wk + STRIDE) {
+    if (PAIR && wk >= NV * 3 * L::N2) continue;
     const int vc = wk / L::N2, r = wk % L::N2, i = r % N, j = r / N;
     T* const s = S + vc * L::SIZE;
     T* const t = Tt + vc * L::SIZE;
@@ -478,9 +550,9 @@ __device__ __forceinline__ void tr_z(const T* wv0, T* av0, const T* Bm, const T*
 #ifndef EMF_QV_SPLIT
 #define EMF_QV_SPLIT 1
 #endif
-template <typename T>
+template <typename T, bool TA = false>
 __device__ __forceinline__ constexpr int qv_arr(int t, int c) {
-  return (sizeof(T) == 8 && EMF_QV_SPLIT) ? t * 3 + c : 2 * c + t;
+  return ((sizeof(T) == 8 && EMF_QV_SPLIT) || TA) ? t * 3 + c : 2 * c + t;
 }
 
 // Transposed y-sweep: Q0 = By^T A0, Q12 = Dy^T A1 + By^T A2.
@@ -509,8 +581,8 @@ __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T*
         q0 += tB<T, N>(Bm, q, b) * u0[q];
         q12 = dacc<T, N>(q12 + tB<T, N>(Bm, q, b) * u2[q], Dm, q, b, u1[q]);
       }
-      qv[qv_arr<T>(0, c) * L::SIZE + lat<N>(i, b, k)] = q0;
-      qv[qv_arr<T>(1, c) * L::SIZE + lat<N>(i, b, k)] = q12;
+      qv[qv_arr<T, TA>(0, c) * L::SIZE + lat<N>(i, b, k)] = q0;
+      qv[qv_arr<T, TA>(1, c) * L::SIZE + lat<N>(i, b, k)] = q12;
     }
   }
 }
@@ -518,7 +590,7 @@ __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T*
 // Transposed x-sweep: out = Dx^T Q0 + Bx^T Q12, written as N contiguous
 // values of loc[(e*3 + c)*N3 + lexicographic m] (component-major).
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
-          int SR = 0>
+          int SR = 0, bool TA = false>
 __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T* Dm, int w, int nvalid = 1) {
   using L = Lay<N, sizeof(T)>;
   for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
@@ -533,8 +605,8 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T
     T u0[N], u1[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      u0[q] = qv[qv_arr<T>(0, c) * L::SIZE + lat<N>(q, j, k)];
-      u1[q] = qv[qv_arr<T>(1, c) * L::SIZE + lat<N>(q, j, k)];
+      u0[q] = qv[qv_arr<T, TA>(0, c) * L::SIZE + lat<N>(q, j, k)];
+      u1[q] = qv[qv_arr<T, TA>(1, c) * L::SIZE + lat<N>(q, j, k)];
     }
     T o[N];
 #pragma unroll
@@ -680,6 +752,15 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
                         !(SM::kUk && sizeof(T) == 4) && (EMF_Q4MAP_TENSOR || STRAT != S_TENSOR);
   constexpr int kStr = 3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3;
   const unsigned pen = kMap ? c_q4pen.v[tid] : 0u;
+  // fp32 Q4 with u_k swept (fused forward sweeps): kQ4Pen32
+  constexpr bool kMap32 = EMF_Q4MAP32 && P == 4 && sizeof(T) == 4 && SM::kUk && !(EMF_V2_DENSE && EPB == 2);
+  constexpr bool kTA = kMap || kMap32;  // direction-major gradient arrays
+  unsigned pen32[3] = {0u, 0u, 0u};
+  if constexpr (kMap32) {
+    pen32[0] = c_q4pen32.v[tid][0];
+    pen32[1] = c_q4pen32.v[tid][1];
+    pen32[2] = c_q4pen32.v[tid][2];
+  }
   // Elements of a CTA only share data through their own slices, so when an
   // element spans whole warps it synchronises on its own named barrier.
   // Q3 (two 64-thread elements per CTA): dense pencil mapping over the CTA
@@ -788,9 +869,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   auto compute = [&](int64_t u, int buf, bool zero_me) {
     EMF_V2_FRESH_POS
     // this thread's pencil per sweep orientation (kQ4Pen) or its point index
-    const int wx = kMap ? (int)(pen & 255u) : q;
-    const int wy = kMap ? (int)((pen >> 8) & 255u) : q;
-    const int wz = kMap ? (int)(pen >> 16) : q;
+    const int wx = kMap ? (int)(pen & 255u) : kMap32 ? (int)((pen32[1] >> 16) & 255u) : q;
+    const int wy = kMap ? (int)((pen >> 8) & 255u) : kMap32 ? (int)(pen32[1] >> 24) : q;
+    const int wz = kMap ? (int)(pen >> 16) : kMap32 ? (int)pen32[2] : q;
     // tensor-product weight of this thread's point (operator.hpp:492)
     const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
     const int64_t e = elem_of(u, el);
@@ -914,7 +995,15 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // sweep, whose shorter live ranges fit its 128/168-register budget
     // (measured: fused sweeps cost fp64 none 0.165 -> 0.175 ms, gave fp32 -3%)
     constexpr bool kFused = kUk && sizeof(T) == 4 && !kDense;
-    if constexpr (kFused) {
+    if constexpr (kFused && kMap32) {
+      // ---- both vectors per sweep, in place, on the thread's mapped pencil pair
+      fwc_x<T, N, 2, N3, true>(S, R2, a.Bm, Dfx, (int)(pen32[0] & 255u), (int)((pen32[0] >> 8) & 255u));
+      esync();
+      fwc_y<T, N, 2, N3, true>(S, R2, R1, a.Bm, Dfy, (int)((pen32[0] >> 16) & 255u), (int)(pen32[0] >> 24));
+      esync();
+      fwc_z<T, N, 2, N3, true>(S, R2, R1, a.Bm, Dfz, (int)(pen32[1] & 255u), (int)((pen32[1] >> 8) & 255u));
+      esync();
+    } else if constexpr (kFused) {
       // ---- gradients of x and u_k at the qps, both vectors per sweep, in place
       fwc_x<T, N, 2, N3>(S, R2, a.Bm, Dfx, q);
       esync();
@@ -1059,7 +1148,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       tangent_integrand<T, MODEL>(mq, cb, gx, j0inv, detw, wv);
     // ---- test with the gradients of the basis functions
 #pragma unroll
-    for (int m = 0; m < 9; ++m) R1[garr_m<kMap>(m) * SZ + qs] = wv[m];
+    for (int m = 0; m < 9; ++m) R1[garr_m<kTA>(m) * SZ + qs] = wv[m];
     esync();
     if constexpr (kDense) {
       constexpr int SR = 9 * SZ, TH = EPB * N3;
@@ -1072,11 +1161,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       const int64_t e0 = e - el;
       tr_x<T, N, TH, EPB, SR>(R1a, a.loc + e0 * 3 * N3, Btx, Dtx, tid, (int)(a.nel - e0 < EPB ? a.nel - e0 : EPB));
     } else {
-      tr_z<T, N, kStr, 1, 0, kMap>(R1, R2, Btz, Dtz, wz);
+      tr_z<T, N, kStr, 1, 0, kTA>(R1, R2, Btz, Dtz, wz);
       esync();
-      tr_y<T, N, kStr, 1, 0, kMap>(R2, R1, Bty, Dty, wy);
+      tr_y<T, N, kStr, 1, 0, kTA>(R2, R1, Bty, Dty, wy);
       esync();
-      if (valid) tr_x<T, N>(R1, a.loc + e * 3 * N3, Btx, Dtx, wx);
+      if (valid) tr_x<T, N, kStr, 1, 0, kTA>(R1, a.loc + e * 3 * N3, Btx, Dtx, wx);
     }
     // No closing barrier: before the next unit's first barrier a thread only
     // zeroes its own staged words of the other buffer and issues the next

@@ -113,3 +113,68 @@ def solve_min(o, SY, SZ, SIZE, k=1):
     for g in range(G):
         lanes += [p for p in range(P) if x[p, g]]
     return int(round(r.fun)), lanes
+
+
+def solve_groups(res, groups, banks, time_limit=60):
+    """Assign pencils (residue list `res`, index = pencil id) to lane groups
+    (list of sizes) minimising the sum over groups of the largest residue
+    multiplicity; returns (cost, [pencil ids in lane order])."""
+    P, G = len(res), len(groups)
+    assert sum(groups) == P
+    nv = P * G + G
+    A, lo, hi = [], [], []
+    for p in range(P):
+        row = np.zeros(nv)
+        row[p * G:(p + 1) * G] = 1
+        A.append(row); lo.append(1); hi.append(1)
+    for g, sz in enumerate(groups):
+        row = np.zeros(nv)
+        row[g:P * G:G] = 1
+        A.append(row); lo.append(sz); hi.append(sz)
+    for g in range(G):
+        for r in range(banks):
+            row = np.zeros(nv)
+            for p in range(P):
+                if res[p] == r:
+                    row[p * G + g] = 1
+            if not row.any():
+                continue
+            row[P * G + g] = -1
+            A.append(row); lo.append(-np.inf); hi.append(0)
+    cost = np.zeros(nv)
+    cost[P * G:] = 1
+    r = milp(c=cost, constraints=LinearConstraint(np.array(A), lo, hi), integrality=np.ones(nv),
+             bounds=Bounds(0, [1] * (P * G) + [32] * G), options={"time_limit": time_limit})
+    x = r.x[:P * G].reshape(P, G).round().astype(int)
+    lanes = []
+    for g in range(G):
+        lanes += [p for p in range(P) if x[p, g]]
+    return int(round(r.fun)), lanes
+
+
+def f32_q4_maps(SY=5, SZ=25, SIZE=125):
+    """fp32 Q4 (4-byte words, 32 banks): the fused x/u_k forward sweeps
+    (fwc_*: 150 pencils, two rounds over 125 threads: lane groups 32, 32, 32,
+    29 then 25) and the transposed sweeps (75 pencils: 32, 32, 11), arrays
+    direction-major (every access c + const)."""
+    lat = lambda a, b, c: a + SY * b + SZ * c
+    out = {}
+    # fused: pencil wk: vc = wk / 25, r = wk % 25; x: j = r % 5, k = r / 5; y: i = r % 5, k = r / 5; z: i, j
+    for o in 'xyz':
+        res = []
+        for wk in range(150):
+            vc, r = wk // 25, wk % 25
+            u, v = r % 5, r // 5
+            base = {'x': lat(0, u, v), 'y': lat(u, 0, v), 'z': lat(u, v, 0)}[o]
+            res.append((vc * SIZE + base) % 32)
+        out['fwc_' + o] = solve_groups(res, [32, 32, 32, 29, 25], 32)
+    # transposed: z / y: c = wk / 25, (i, j) / (i, k); x (fp32 order): c = wk / 25, j = r % 5, k = r / 5
+    for o in 'xyz':
+        res = []
+        for wk in range(75):
+            c, r = wk // 25, wk % 25
+            u, v = r % 5, r // 5
+            base = {'x': lat(0, u, v), 'y': lat(u, 0, v), 'z': lat(u, v, 0)}[o]
+            res.append((c * SIZE + base) % 32)
+        out['tr_' + o] = solve_groups(res, [32, 32, 11], 32)
+    return out
