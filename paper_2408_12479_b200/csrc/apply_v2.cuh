@@ -588,17 +588,20 @@ __device__ __forceinline__ void tr_y(const T* av0, T* qv0, const T* Bm, const T*
 }
 
 // Transposed x-sweep: out = Dx^T Q0 + Bx^T Q12, written as N contiguous
-// values of loc[(e*3 + c)*N3 + lexicographic m] (component-major).
+// values (one element row of one component) of the element-local results
+// (loc_index, kernels.cuh); elements e0 + e_l.
 template <typename T, int N, int STRIDE = (3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3), int NE = 1,
           int SR = 0, bool TA = false>
-__device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T* Dm, int w, int nvalid = 1) {
+__device__ __forceinline__ void tr_x(const T* qv0, T* loc, int64_t e0, int nx, FastDiv fd_nx, const T* Bm,
+                                     const T* Dm, int w, int nvalid = 1) {
   using L = Lay<N, sizeof(T)>;
   for (int wp = w; wp < NE * 3 * L::N2; wp += STRIDE) {
     const int e_l = NE > 1 ? wp / (3 * L::N2) : 0;
     const int wk = wp - e_l * 3 * L::N2;
     if (NE > 1 && e_l >= nvalid) break;
     const T* const qv = qv0 + e_l * SR;
-    T* const loc_e = loc0 + e_l * 3 * L::N3;
+    const int64_t e = e0 + e_l;
+    const int64_t row = fd_nx.div((uint32_t)e);
     const int j = sizeof(T) == 8 ? wk % N : (wk % L::N2) % N;  // pencil order as fw_x
     const int c = sizeof(T) == 8 ? (wk / N) % 3 : wk / L::N2;
     const int k = sizeof(T) == 8 ? wk / (3 * N) : (wk % L::N2) / N;
@@ -616,7 +619,7 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc0, const T* Bm, const T
       for (int q = 1; q < N; ++q) s = dacc<T, N>(s + tB<T, N>(Bm, q, a) * u1[q], Dm, q, a, u0[q]);
       o[a] = s;
     }
-    T* dst = loc_e + c * L::N3 + (k * N + j) * N;
+    T* dst = loc + loc_index<N>(row, (int)(e - row * nx), nx, k, j, 0, c);
 #pragma unroll
     for (int a = 0; a < N; ++a) dst[a] = o[a];
   }
@@ -1159,13 +1162,14 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       tr_y<T, N, TH, EPB, SR>(R2a, R1a, Bty, Dty, tid);
       esync();
       const int64_t e0 = e - el;
-      tr_x<T, N, TH, EPB, SR>(R1a, a.loc + e0 * 3 * N3, Btx, Dtx, tid, (int)(a.nel - e0 < EPB ? a.nel - e0 : EPB));
+      tr_x<T, N, TH, EPB, SR>(R1a, a.loc, e0, a.nx, a.fd_nx, Btx, Dtx, tid,
+                              (int)(a.nel - e0 < EPB ? a.nel - e0 : EPB));
     } else {
       tr_z<T, N, kStr, 1, 0, kTA>(R1, R2, Btz, Dtz, wz);
       esync();
       tr_y<T, N, kStr, 1, 0, kTA>(R2, R1, Bty, Dty, wy);
       esync();
-      if (valid) tr_x<T, N, kStr, 1, 0, kTA>(R1, a.loc + e * 3 * N3, Btx, Dtx, wx);
+      if (valid) tr_x<T, N, kStr, 1, 0, kTA>(R1, a.loc, e, a.nx, a.fd_nx, Btx, Dtx, wx);
     }
     // No closing barrier: before the next unit's first barrier a thread only
     // zeroes its own staged words of the other buffer and issues the next

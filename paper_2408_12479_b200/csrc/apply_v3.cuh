@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(32 * kV3Warps, (minb_v3<T, MODEL, STRAT>())) a
     __syncwarp();
     tr_y<T, N, 32>(R2, R1, Bm, Dm, lane);
     __syncwarp();
-    tr_x<T, N, 32>(R1, a.loc + e * 3 * N3, Bm, Dm, lane);
+    tr_x<T, N, 32>(R1, a.loc, e, a.nx, a.fd_nx, Bm, Dm, lane);
     __syncwarp();
     if constexpr (kTk) {
       int pt = nu;

@@ -17,8 +17,14 @@ namespace emfgpu {
 // Same assembly with the nodes of a plane flattened (a + mx b): every lane
 // of a warp owns a node, where the (32, 8) tiling of an mx = 3n+1 row leaves
 // a quarter of the warps almost empty (the kernel is issue-bound).
+// 8 CTAs/SM (<= 32 registers): the kernel is latency-bound on its loc loads
+// (long-scoreboard stalls), and at 39 registers only 6 CTAs fit (cfg2 fp64:
+// 286 us for 1.18 GB of compulsory DRAM traffic, 4.1 TB/s).
+#ifndef EMF_NODE_MINB
+#define EMF_NODE_MINB 8
+#endif
 template <typename T, int P, bool GHOSTS>
-__global__ void __launch_bounds__(256) node_gather_flat_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
+__global__ void __launch_bounds__(256, EMF_NODE_MINB) node_gather_flat_kernel(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
                                                                const T* __restrict__ ghost_hi, const T* x, T* y, int nx,
                                                                int ny, int nz, int faces, int kpar, int c0,
                                                                int periodic_y, FastDiv fd_mx) {
@@ -82,11 +88,10 @@ void launch_node_gather(const T* loc, const T* ghost_lo, const T* ghost_hi, cons
 
 // Face of element layer k: lower (side 0, local c=0) or upper (side 1, c=p)
 // node plane of each element's local results (read from the component-major
-// loc[(e*3 + c)*N3 + m]), packed as ((j*nx+i)*N2 + b*N + a)*3 + comp.
-template <typename T>
-__global__ void pack_face_kernel(const T* __restrict__ loc, T* __restrict__ face, int nx, int ny, int p, int k,
-                                 int side) {
-  const int N = p + 1, N2 = N * N, N3 = N2 * N;
+// element-local results, loc_index), packed as ((j*nx+i)*N2 + b*N + a)*3 + comp.
+template <typename T, int P>
+__global__ void pack_face_kernel(const T* __restrict__ loc, T* __restrict__ face, int nx, int ny, int k, int side) {
+  constexpr int N = P + 1, N2 = N * N;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)nx * ny * N2 * 3;
   if (idx >= total) return;
@@ -94,15 +99,21 @@ __global__ void pack_face_kernel(const T* __restrict__ loc, T* __restrict__ face
   const int64_t fn = idx / 3;
   const int m2 = (int)(fn % N2);
   const int64_t ij = fn / N2;
-  const int64_t e = (int64_t)k * nx * ny + ij;
-  const int lc = side ? p : 0;
-  face[idx] = loc[(e * 3 + comp) * N3 + lc * N2 + m2];
+  const int64_t j = ij / nx, i = ij - j * nx;
+  const int lc = side ? P : 0;
+  face[idx] = loc[loc_index<N>((int64_t)k * ny + j, (int)i, nx, lc, m2 / N, m2 % N, comp)];
 }
 
 template <typename T>
 void launch_pack_face(const T* loc, T* face, int nx, int ny, int p, int k, int side, cudaStream_t s) {
   const int64_t total = (int64_t)nx * ny * (p + 1) * (p + 1) * 3;
-  pack_face_kernel<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(loc, face, nx, ny, p, k, side);
+  const unsigned g = (unsigned)((total + 255) / 256);
+  switch (p) {
+    case 1: pack_face_kernel<T, 1><<<g, 256, 0, s>>>(loc, face, nx, ny, k, side); break;
+    case 2: pack_face_kernel<T, 2><<<g, 256, 0, s>>>(loc, face, nx, ny, k, side); break;
+    case 3: pack_face_kernel<T, 3><<<g, 256, 0, s>>>(loc, face, nx, ny, k, side); break;
+    case 4: pack_face_kernel<T, 4><<<g, 256, 0, s>>>(loc, face, nx, ny, k, side); break;
+  }
 }
 
 // Diagonal epilogue: constrained rows -> 1, count free rows with d <= 0

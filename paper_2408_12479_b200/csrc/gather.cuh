@@ -82,12 +82,12 @@ __device__ __forceinline__ void assemble_node(const T* __restrict__ loc, const T
           v0 = src[off];
           v1 = src[off + 1];
           v2 = src[off + 2];
-        } else {  // element-local results, component-major loc[(e*3 + c)*N3 + m]
-          const int64_t e = ((int64_t)k * ny + sy.e[tj]) * nx + sx.e[ti];
-          const int64_t off = e * 3 * N3 + (sz.l[tk] * N + sy.l[tj]) * N + sx.l[ti];
+        } else {  // element-local results (loc_index, kernels.cuh)
+          const int64_t off = loc_index<N>((int64_t)k * ny + sy.e[tj], sx.e[ti], nx, sz.l[tk], sy.l[tj], sx.l[ti], 0);
+          const int64_t cs = loc_cstride<N>(nx);
           v0 = ld(loc + off);
-          v1 = ld(loc + off + N3);
-          v2 = ld(loc + off + 2 * N3);
+          v1 = ld(loc + off + cs);
+          v2 = ld(loc + off + 2 * cs);
         }
         s0 += v0;
         s1 += v1;

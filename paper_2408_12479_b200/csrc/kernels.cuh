@@ -92,6 +92,28 @@ inline void per_device_shape(std::atomic<int>* cache, int& sms, int& per_sm, Ini
   per_sm = v % 64;
 }
 
+// Layout of the element-local results (element phase -> node phase):
+// element-major loc[(e*3 + c)*N^3 + m] (each element writes one contiguous
+// 3 N^3 block).  EMF_LOC_ROWS=1 builds the row layout
+// loc[((((row*N + lz)*N + ly)*3 + c)*nx + ei)*N + lx], row = ek*ny + ej, in
+// which the node phase streams whole lattice rows: measured on cfg2 fp64 none
+// (profiles/r02_loc_layout.txt) the node phase 0.31 -> 0.25 ms but the element
+// kernel 2.20 -> 2.57 ms (its stores scatter into 40-byte pieces), so the
+// element-major layout stays.
+#ifndef EMF_LOC_ROWS
+#define EMF_LOC_ROWS 0
+#endif
+template <int N>
+__host__ __device__ __forceinline__ int64_t loc_index(int64_t row, int ei, int nx, int lz, int ly, int lx, int c) {
+  if (EMF_LOC_ROWS) return ((((row * N + lz) * N + ly) * 3 + c) * (int64_t)nx + ei) * N + lx;
+  return ((row * nx + ei) * 3 + c) * (N * N * N) + (lz * N + ly) * N + lx;
+}
+// stride between the components of one value
+template <int N>
+__host__ __device__ __forceinline__ int64_t loc_cstride(int nx) {
+  return EMF_LOC_ROWS ? (int64_t)nx * N : (int64_t)N * N * N;
+}
+
 template <typename T>
 struct KArgs {
   const T* x;          // input vector (3 per node), apply / unused by diag
@@ -668,9 +690,12 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     }
     __syncthreads();
   }
-  if (valid)
+  if (valid) {
+    const int64_t row = a.fd_nx.div((uint32_t)e);
+    const int64_t o = loc_index<N>(row, (int)(e - row * a.nx), a.nx, q / (N * N), (q / N) % N, q % N, 0);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.loc[(e * 3 + c) * N3 + q] = out[c];
+    for (int c = 0; c < 3; ++c) a.loc[o + c * loc_cstride<N>(a.nx)] = out[c];
+  }
 }
 
 }  // namespace emfgpu
@@ -740,9 +765,12 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     for (int m = 0; m < 9; ++m) w[m] *= detw;
   }
   sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
-  if (valid)
+  if (valid) {
+    const int64_t row = a.fd_nx.div((uint32_t)e);
+    const int64_t o = loc_index<N>(row, (int)(e - row * a.nx), a.nx, q / (N * N), (q / N) % N, q % N, 0);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) a.loc[(e * 3 + c) * N3 + q] = out[c];
+    for (int c = 0; c < 3; ++c) a.loc[o + c * loc_cstride<N>(a.nx)] = out[c];
+  }
 }
 
 }  // namespace emfgpu
