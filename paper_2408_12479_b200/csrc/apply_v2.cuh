@@ -601,7 +601,6 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc, int64_t e0, int nx, F
     if (NE > 1 && e_l >= nvalid) break;
     const T* const qv = qv0 + e_l * SR;
     const int64_t e = e0 + e_l;
-    const int64_t row = fd_nx.div((uint32_t)e);
     const int j = sizeof(T) == 8 ? wk % N : (wk % L::N2) % N;  // pencil order as fw_x
     const int c = sizeof(T) == 8 ? (wk / N) % 3 : wk / L::N2;
     const int k = sizeof(T) == 8 ? wk / (3 * N) : (wk % L::N2) / N;
@@ -619,7 +618,13 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc, int64_t e0, int nx, F
       for (int q = 1; q < N; ++q) s = dacc<T, N>(s + tB<T, N>(Bm, q, a) * u1[q], Dm, q, a, u0[q]);
       o[a] = s;
     }
-    T* dst = loc + loc_index<N>(row, (int)(e - row * nx), nx, k, j, 0, c);
+    T* dst;
+    if constexpr (EMF_LOC_ROWS) {
+      const int64_t row = fd_nx.div((uint32_t)e);
+      dst = loc + loc_index<N>(row, (int)(e - row * nx), nx, k, j, 0, c);
+    } else {
+      dst = loc + (e * 3 + c) * L::N3 + (k * N + j) * N;
+    }
 #pragma unroll
     for (int a = 0; a < N; ++a) dst[a] = o[a];
   }

@@ -691,8 +691,11 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     __syncthreads();
   }
   if (valid) {
-    const int64_t row = a.fd_nx.div((uint32_t)e);
-    const int64_t o = loc_index<N>(row, (int)(e - row * a.nx), a.nx, q / (N * N), (q / N) % N, q % N, 0);
+    int64_t o = e * 3 * N3 + q;
+    if constexpr (EMF_LOC_ROWS) {
+      const int64_t row = a.fd_nx.div((uint32_t)e);
+      o = loc_index<N>(row, (int)(e - row * a.nx), a.nx, q / (N * N), (q / N) % N, q % N, 0);
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) a.loc[o + c * loc_cstride<N>(a.nx)] = out[c];
   }
@@ -766,8 +769,11 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   }
   sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
   if (valid) {
-    const int64_t row = a.fd_nx.div((uint32_t)e);
-    const int64_t o = loc_index<N>(row, (int)(e - row * a.nx), a.nx, q / (N * N), (q / N) % N, q % N, 0);
+    int64_t o = e * 3 * N3 + q;
+    if constexpr (EMF_LOC_ROWS) {
+      const int64_t row = a.fd_nx.div((uint32_t)e);
+      o = loc_index<N>(row, (int)(e - row * a.nx), a.nx, q / (N * N), (q / N) % N, q % N, 0);
+    }
 #pragma unroll
     for (int c = 0; c < 3; ++c) a.loc[o + c * loc_cstride<N>(a.nx)] = out[c];
   }

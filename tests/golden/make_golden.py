@@ -385,6 +385,70 @@ def cfg4_full():
         json.dump(res, f, indent=1)
 
 
+def coarse_lu():
+    """Evidence for the reference's DenseLU pivoting defect (solver.hpp:55-78,
+    DESIGN.md §5): on 3^3 and 6^3 Q4 (no h-levels: the coarse Q1 level has
+    192 / 1029 DoFs) the reference's PCG with its dense coarse LU against the
+    same hierarchy with its coarse Jacobi-PCG: iterations, histories, V-cycles
+    (tests/golden/coarse_lu.npz)."""
+    out = {}
+    prm = R.material_params(mu=1.0, lam=10.0, kappa=50.0)
+    for n in (3, 6):
+        L = R.RefLevel(n, 0, 4, 0.0, 1)
+        op = R.RefOperator(L, "inh", prm, "none", 64)
+        op.update_linearization(np.zeros(L.ndofs))
+        b = I.make_v(L.ndofs, 2)
+        b[I.dirichlet_mask(n, n, n, 4, 1)] = 0.0
+        r = I.make_v(L.ndofs, 11)
+        out[f"n{n}_b"] = b
+        out[f"n{n}_r"] = r
+        for lim in (2000, 0):
+            mg = R.RefMg(L, "inh", prm, degree=5, coarse_direct_limit=lim)
+            mg.update_linearization(np.zeros(L.ndofs))
+            out[f"n{n}_lim{lim}_z"] = mg.precondition(r)
+            x, its, hist = R.pcg_solve(op, mg, b, 1e-8, 300)
+            out[f"n{n}_lim{lim}_its"] = its
+            out[f"n{n}_lim{lim}_hist"] = hist
+            print("coarse_lu", n, lim, its)
+    np.savez_compressed(os.path.join(OUT, "coarse_lu.npz"), **out)
+
+
+def cfg4_full_cg():
+    """cfg4 at full size with the reference's coarse Jacobi-PCG
+    (coarse_direct_limit = 0) instead of its dense LU: the reference's
+    DenseLU::solve applies the row interchanges interleaved with the forward
+    elimination although factor() swapped whole rows (solver.hpp:55-78), so
+    its coarse solve is wrong whenever partial pivoting swaps rows (DESIGN.md
+    §5); the CG coarse path is the reference's correct configuration to pin
+    the iteration count against (tests/golden/cfg4_full_cg.json)."""
+    import json
+    import time
+    sys.path.insert(0, ROOT)
+    from paper_2408_12479_b200 import workloads as W
+    w = W.cfg4()
+    L = R.RefLevel(6, 3, 4, 0.0, 1)
+    prm = _inh_params(50.0)
+    res = {"threads": os.cpu_count(), "ndofs": int(L.ndofs), "coarse_direct_limit": 0}
+    t0 = time.perf_counter()
+    op = R.RefOperator(L, "inh", prm, "none", 64)
+    op.update_linearization(np.zeros(L.ndofs))
+    mg = R.RefMg(L, "inh", prm, degree=5, coarse_direct_limit=0)
+    mg.update_linearization(np.zeros(L.ndofs))
+    res["setup_s"] = time.perf_counter() - t0
+    res["mg_levels"] = mg.n_levels
+    print("setup", res["setup_s"], flush=True)
+    b = W.rhs(w)
+    t0 = time.perf_counter()
+    x, its, hist = R.pcg_solve(op, mg, b, 1e-8, 300)
+    res["solve_s"] = time.perf_counter() - t0
+    res["iterations"] = int(its)
+    res["history"] = [float(h) for h in hist]
+    res["norm_x"] = float(np.linalg.norm(x))
+    print("pcg", its, "its", res["solve_s"], "s", flush=True)
+    with open(os.path.join(OUT, "cfg4_full_cg.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for f in sys.argv[1:]:

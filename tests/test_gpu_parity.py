@@ -1031,3 +1031,37 @@ def test_slab_group_apply_and_dot_bitwise(G, splits):
     s1.apply(x, y)
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), y_full)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [3, 6])
+def test_dense_coarse_solve_vs_reference_cg_coarse(G, n):
+    """The reference's DenseLU::solve (solver.hpp:73-78) applies the row
+    interchanges interleaved with the forward elimination although factor()
+    (55-63) swapped whole rows, so its dense coarse solve is wrong once
+    partial pivoting swaps rows (3^3 Q4: 300 PCG iterations without
+    convergence; with its coarse Jacobi-PCG instead: 36).  The device dense
+    coarse solve is the exact one: its V-cycle equals the reference's
+    CG-coarse V-cycle to the coarse CG's 1e-4, and the PCG iterations match
+    the reference's CG-coarse hierarchy within +-1 (the reference's dense
+    ones do not)."""
+    import torch
+    g = np.load(os.path.join(GOLD, "coarse_lu.npz"))
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    lev = G.FeLevel(n, p=4)
+    op = G.ElasticOperator(lev, "inh", prm, "none", 64)
+    op.update_linearization(np.zeros(lev.n_dofs))
+    b = torch.tensor(g[f"n{n}_b"], device="cuda")
+    r = torch.tensor(g[f"n{n}_r"], device="cuda")
+    ref_cg = int(g[f"n{n}_lim0_its"])
+    assert rel(g[f"n{n}_lim2000_z"], g[f"n{n}_lim0_z"]) > 1e-2  # the reference's dense coarse solve is off
+    for lim in (2000, 0):
+        mg = G.MgHierarchy(lev, "inh", prm, degree=5, coarse_n=n, precision=32, coarse_direct_limit=lim)
+        mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+        z = torch.empty_like(r)
+        mg.precondition(r, z)
+        torch.cuda.synchronize()
+        assert rel(z.cpu().numpy(), g[f"n{n}_lim0_z"]) <= 1e-3, (lim, rel(z.cpu().numpy(), g[f"n{n}_lim0_z"]))
+        x = torch.empty_like(b)
+        its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 300)
+        assert abs(its - ref_cg) <= 1, (lim, its, ref_cg)

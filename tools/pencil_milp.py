@@ -178,3 +178,12 @@ def f32_q4_maps(SY=5, SZ=25, SIZE=125):
             res.append((c * SIZE + base) % 32)
         out['tr_' + o] = solve_groups(res, [32, 32, 11], 32)
     return out
+
+
+
+# A sub-pencil variant of the fp64 Q4 y / z sweeps (225 single-line items over
+# two thread rounds, warp-uniform tables, MILP-mapped like the maps above) was
+# built and measured in round 2: 2.21 -> 3.53 ms per element phase with the
+# items processed one after the other (short-scoreboard stalls on the 5-value
+# line loads) and 600-800 B of spills when both items' loads were issued
+# first, so it was dropped.
