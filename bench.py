@@ -610,11 +610,20 @@ def run_extra_workloads(args, flush, peaks):
                                          "solve (1029 DoFs < coarse_direct_limit 2000, as the reference)"}
     if ref4:
         out["cfg4_wellposed"].update({
-            "reference_iterations": ref4["iterations"], "reference_solve_s": ref4["solve_s"],
+            "reference_iterations_dense_lu": ref4["iterations"], "reference_solve_s": ref4["solve_s"],
             "reference_setup_s": ref4["setup_s"], "reference_threads": ref4["threads"],
             "reference_note": "the reference's MgHierarchy<float> + fp64 PCG (oracle/ref_driver.cpp "
-                              "ref_pcg_solve) run once in the build container (tests/golden/cfg4_full.json)"})
+                              "ref_pcg_solve) run once in the build container (tests/golden/cfg4_full.json); "
+                              "its dense coarse LU mishandles row pivots (solver.hpp:55-78, DESIGN.md §5), "
+                              "so its iteration count with the dense coarse solve is not the parity target"})
         out["cfg4_literal"] = ref4.get("literal")
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "cfg4_full_cg.json")) as f:
+            ref4cg = json.load(f)
+        out["cfg4_wellposed"].update({"reference_iterations_cg_coarse": ref4cg["iterations"],
+                                      "reference_cg_coarse_solve_s": ref4cg["solve_s"]})
+    except (OSError, ValueError):
+        pass
     del op, mg, lev, b, x
     # cfg4 literal: rejected like the reference
     w = W.cfg4(wellposed=False)

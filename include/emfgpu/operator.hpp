@@ -9,7 +9,10 @@
 #ifndef EMFGPU_OPERATOR_HPP
 #define EMFGPU_OPERATOR_HPP
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -44,12 +47,31 @@ inline void throw_status(emfgpu_status st, const char* msg, std::int64_t e = -1,
 }
 
 enum class ModelKind { cnh = EMFGPU_CNH, inh = EMFGPU_INH, fiber = EMFGPU_FIBER };
-/// Formulation::domain (material.hpp:18); the stability is always "stable".
+/// Formulation (material.hpp:17-23).  The device kernels implement the stable
+/// formulation; Stability::standard is refused with ConfigError.
 enum class Domain { material = 0, spatial = 1 };
-/// Loads (operator.hpp:23-32): uniform pressure on one face (-x,+x,-y,+y,-z,+z = 0..5).
+enum class Stability { standard = 0, stable = 1 };
+struct Formulation {
+  Stability stability = Stability::stable;
+  Domain domain = Domain::material;
+};
+/// KernelConfig (fastscalar.hpp:29-39); only the defaults are implemented
+/// (other values -> ConfigError naming the field).
+struct KernelConfig {
+  int ln_series_terms = 16;
+  int jpow_newton_steps = 3;
+  int exp_mode = 0;   // ExpMode::exact
+  int jpow_mode = 0;  // JpowMode::newton
+};
+using Vec3d = std::array<double, 3>;
+/// Loads (operator.hpp:23-32): uniform pressure on one face (-x,+x,-y,+y,-z,+z
+/// = 0..5), body force B(X) and tractions h(X, N) on the flagged faces.
 struct Loads {
   double pressure = 0.0;
   int pressure_face = 1;
+  std::function<Vec3d(const Vec3d&)> body_force;
+  std::array<bool, 6> traction_faces{};
+  std::function<Vec3d(const Vec3d&, const Vec3d&)> traction;
 };
 enum class Strategy { none = EMFGPU_NONE, scalar = EMFGPU_SCALAR, tensor = EMFGPU_TENSOR, cached_f = EMFGPU_CACHED_F };
 
@@ -86,16 +108,48 @@ class ElasticOperator {
 
  public:
   ElasticOperator(const FeLevel& level, ModelKind model, const emfgpu_material& params, Strategy strategy)
-      : ElasticOperator(level, model, params, Domain::material, strategy, Loads{}) {}
-  /// operator.hpp:55-70: (level, model, params, formulation, strategy, loads)
+      : ElasticOperator(level, model, params, Formulation{}, strategy, KernelConfig{}, Loads{}) {}
   ElasticOperator(const FeLevel& level, ModelKind model, const emfgpu_material& params, Domain domain,
                   Strategy strategy, const Loads& loads = {})
+      : ElasticOperator(level, model, params, Formulation{Stability::stable, domain}, strategy, KernelConfig{},
+                        loads) {}
+  /// operator.hpp:55-70: (level, model, params, formulation, strategy, cfg, loads)
+  ElasticOperator(const FeLevel& level, ModelKind model, const emfgpu_material& params, Formulation form,
+                  Strategy strategy, const KernelConfig& cfg = {}, const Loads& loads = {})
       : level_(&level) {
-    throw_status(emfgpu_op_create(level.handle(), static_cast<int>(model), &params, static_cast<int>(domain),
-                                  static_cast<int>(strategy), sizeof(Number) == 8 ? 64 : 32, &h_),
+    const emfgpu_formulation f{static_cast<int>(form.stability), static_cast<int>(form.domain)};
+    const emfgpu_kernel_config k{cfg.ln_series_terms, cfg.jpow_newton_steps, cfg.exp_mode, cfg.jpow_mode};
+    throw_status(emfgpu_op_create_ex(level.handle(), static_cast<int>(model), &params, &f,
+                                     static_cast<int>(strategy), sizeof(Number) == 8 ? 64 : 32, &k, &h_),
                  emfgpu_global_last_error());
-    if (loads.pressure != 0.0)
-      throw_status(emfgpu_op_set_pressure(h_, loads.pressure, loads.pressure_face), emfgpu_op_last_error(h_));
+    set_loads(loads);
+  }
+
+  /// build_load_vector (operator.hpp:880-1008): the std::function members are
+  /// evaluated on the host through C callbacks while the vector is built.
+  void set_loads(const Loads& loads) {
+    if (loads.pressure == 0.0 && !loads.body_force && !loads.traction) return;
+    emfgpu_loads c{};
+    c.pressure = loads.pressure;
+    c.pressure_face = loads.pressure_face;
+    if (loads.body_force) {
+      c.body_force = [](const double X[3], double out[3], void* u) {
+        const Vec3d v = (*static_cast<const std::function<Vec3d(const Vec3d&)>*>(u))(Vec3d{X[0], X[1], X[2]});
+        out[0] = v[0], out[1] = v[1], out[2] = v[2];
+      };
+      c.body_force_user = const_cast<void*>(static_cast<const void*>(&loads.body_force));
+    }
+    if (loads.traction) {
+      c.traction = [](const double X[3], const double N[3], double out[3], void* u) {
+        const Vec3d v = (*static_cast<const std::function<Vec3d(const Vec3d&, const Vec3d&)>*>(u))(
+            Vec3d{X[0], X[1], X[2]}, Vec3d{N[0], N[1], N[2]});
+        out[0] = v[0], out[1] = v[1], out[2] = v[2];
+      };
+      c.traction_user = const_cast<void*>(static_cast<const void*>(&loads.traction));
+      for (int f = 0; f < 6; ++f)
+        if (loads.traction_faces[f]) c.traction_faces |= 1 << f;
+    }
+    throw_status(emfgpu_op_set_loads(h_, &c), emfgpu_op_last_error(h_));
   }
   ElasticOperator(const ElasticOperator&) = delete;
   ElasticOperator& operator=(const ElasticOperator&) = delete;
@@ -136,7 +190,7 @@ class ElasticOperator {
     throw_status(emfgpu_op_apply(h_, d_x, d_y, stream), emfgpu_op_last_error(h_));
   }
 
-  /// operator.hpp:106-107: (diag, indices of nonpositive free entries)
+  /// operator.hpp:106-107: (diag, indices of nonpositive free entries, ascending)
   std::pair<std::vector<Number>, std::vector<std::int64_t>> compute_diagonal() const {
     std::vector<Number> d(n_dofs());
     std::int64_t nbad = 0;
@@ -146,6 +200,17 @@ class ElasticOperator {
       for (std::int64_t i = 0; i < (std::int64_t)d.size(); ++i)
         if (!(d[i] > Number(0))) bad.push_back(i);
     return {std::move(d), std::move(bad)};
+  }
+  /// Same on a device diagonal: the index list comes from the device
+  /// (emfgpu_op_compute_diagonal_indices), the diagonal stays in d_diag.
+  std::vector<std::int64_t> compute_diagonal_device(Number* d_diag, std::int64_t capacity = 1 << 16,
+                                                    void* stream = nullptr) const {
+    std::vector<std::int64_t> idx(capacity);
+    std::int64_t n = 0;
+    throw_status(emfgpu_op_compute_diagonal_indices(h_, d_diag, idx.data(), capacity, &n, stream),
+                 emfgpu_op_last_error(h_));
+    idx.resize(static_cast<std::size_t>(std::min(n, capacity)));
+    return idx;
   }
 
   emfgpu_op* handle() const { return h_; }
