@@ -586,7 +586,10 @@ def run_extra_workloads(args, flush, peaks):
     x = torch.empty_like(b)
     # warm-up: two PCG iterations load every kernel of the solve (lazy module
     # loading) before the timed solve
-    G.pcg_solve(op, mg, b, x, 1e-8, 2)
+    try:
+        G.pcg_solve(op, mg, b, x, 1e-8, 2)
+    except G.EmfGpuError:
+        pass  # not converged in 2 iterations: expected
     torch.cuda.synchronize()
     smp = ClockSampler(torch.cuda.current_device())
     smp.__enter__()
