@@ -1065,3 +1065,30 @@ def test_dense_coarse_solve_vs_reference_cg_coarse(G, n):
         x = torch.empty_like(b)
         its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 300)
         assert abs(its - ref_cg) <= 1, (lim, its, ref_cg)
+
+
+@pytest.mark.gpu
+def test_slab_nccl_communicator_single_rank(G):
+    """The NCCL side of the slab layer on one GPU: libnccl.so.2 loaded at run
+    time, a 1-rank communicator from a unique id, a slab apply through it
+    (no neighbours: the plain apply) and the device dot."""
+    import torch
+    n, p = 4, 3
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), "none", 64)
+    op.update_linearization(I.make_u0(n, n, n, p))
+    v = I.make_v(lev.n_dofs)
+    y_ref = op.apply_tangent(v)
+    uid = G.Comm.unique_id()
+    assert len(uid) == 128
+    comm = G.Comm(uid, 1, 0, device=torch.cuda.current_device())
+    slab = G.Slab(op, 0, 1, comm)
+    x = torch.tensor(v, device="cuda")
+    y = torch.empty_like(x)
+    slab.apply(x, y)
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    slab.dot(x, y, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y_ref)
+    assert abs(float(out.item()) - float(np.dot(v, y_ref))) <= 1e-12 * abs(float(np.dot(v, y_ref)))
+    del slab, comm
