@@ -295,6 +295,57 @@ constexpr Q4PenPacked32 q4pen32_pack() {
 }
 static __constant__ Q4PenPacked32 c_q4pen32 = q4pen32_pack();
 
+// fp64 Q4 with the x and u_k forward sweeps fused (fwc_*: 150 pencils over
+// the 6 staged arrays, round 1 on threads 0-124, round 2 on threads 0-24;
+// tools/pencil_milp.py f64_q4_fused_maps): every half-warp conflict-free.
+struct Q4PenMapF64 {
+  unsigned char fx[150], fy[150], fz[150];
+};
+static constexpr Q4PenMapF64 kQ4PenF64 = {
+    // fwc_x (MILP cost 10, ideal 10)
+    {16, 31, 33, 37, 51, 58, 59, 70, 76, 77, 78, 84, 87, 89, 98, 120, 0, 7, 15, 68, 73, 75, 83, 88, 90, 101,
+     109, 114, 118, 124, 126, 129, 8, 11, 26, 39, 49, 57, 60, 67, 69, 102, 116, 125, 128, 130, 142, 143, 9, 13,
+     17, 23, 40, 42, 62, 66, 79, 80, 117, 123, 134, 140, 147, 148, 18, 29, 32, 38, 44, 46, 63, 71, 91, 97, 99,
+     100, 106, 136, 137, 149, 12, 20, 35, 43, 47, 61, 86, 94, 103, 104, 113, 121, 122, 133, 144, 146, 5, 10,
+     19, 22, 27, 30, 34, 48, 72, 92, 95, 105, 119, 132, 141, 145, 2, 25, 28, 52, 54, 65, 74, 85, 107, 110, 112,
+     115, 127, 3, 6, 14, 21, 24, 36, 41, 50, 55, 64, 81, 93, 108, 111, 138, 139, 1, 4, 45, 53, 56, 82, 96, 131,
+     135},
+    // fwc_y (MILP cost 10, ideal 10)
+    {0, 10, 16, 21, 26, 31, 43, 56, 63, 66, 76, 77, 83, 109, 130, 141, 11, 27, 37, 41, 50, 51, 52, 53, 68, 90,
+     103, 108, 129, 134, 136, 138, 2, 5, 14, 15, 18, 28, 49, 61, 67, 71, 84, 91, 96, 114, 117, 120, 8, 9, 13,
+     20, 22, 42, 45, 62, 79, 82, 113, 119, 143, 144, 147, 148, 7, 29, 32, 36, 38, 39, 44, 48, 58, 86, 105, 106,
+     107, 111, 137, 149, 12, 54, 57, 72, 73, 85, 87, 88, 94, 97, 99, 104, 122, 126, 135, 139, 19, 23, 30, 33,
+     34, 40, 47, 60, 70, 74, 81, 89, 92, 95, 116, 145, 65, 69, 75, 80, 98, 110, 112, 115, 123, 127, 128, 133,
+     140, 3, 4, 17, 24, 35, 59, 64, 78, 93, 118, 121, 124, 125, 131, 142, 146, 1, 6, 25, 46, 55, 100, 101, 102,
+     132},
+    // fwc_z (MILP cost 10, ideal 10)
+    {52, 60, 63, 67, 70, 74, 76, 77, 78, 83, 84, 85, 87, 101, 109, 130, 0, 4, 15, 31, 36, 50, 51, 65, 75, 90,
+     97, 114, 117, 125, 136, 138, 8, 18, 21, 39, 42, 57, 71, 96, 102, 105, 119, 122, 128, 137, 140, 143, 11,
+     13, 37, 40, 45, 46, 47, 49, 62, 82, 99, 100, 112, 134, 147, 148, 25, 29, 32, 35, 44, 95, 98, 106, 108,
+     111, 115, 120, 126, 129, 146, 149, 3, 7, 12, 26, 28, 34, 43, 53, 61, 86, 94, 104, 113, 133, 135, 144, 10,
+     19, 20, 23, 27, 30, 54, 68, 72, 79, 81, 89, 92, 93, 118, 141, 2, 6, 24, 55, 66, 73, 80, 88, 91, 110, 123,
+     127, 145, 5, 14, 16, 17, 22, 38, 41, 48, 59, 107, 121, 124, 131, 132, 139, 142, 1, 9, 33, 56, 58, 64, 69,
+     103, 116}};
+struct Q4PenPackedF64 {
+  unsigned v[128][2];
+};
+// [0] = x round 1 | x round 2 << 8 | y r1 << 16 | y r2 << 24, [1] = z r1 | z r2 << 8; 255 = none
+constexpr Q4PenPackedF64 q4penf64_pack() {
+  Q4PenPackedF64 r{};
+  for (int t = 0; t < 128; ++t) {
+    auto f = [&](const unsigned char* m, int round) -> unsigned {
+      return (round == 0 ? t < 125 : t < 25) ? (unsigned)m[round == 0 ? t : 125 + t] : 255u;
+    };
+    r.v[t][0] = f(kQ4PenF64.fx, 0) | f(kQ4PenF64.fx, 1) << 8 | f(kQ4PenF64.fy, 0) << 16 | f(kQ4PenF64.fy, 1) << 24;
+    r.v[t][1] = f(kQ4PenF64.fz, 0) | f(kQ4PenF64.fz, 1) << 8;
+  }
+  return r;
+}
+static __constant__ Q4PenPackedF64 c_q4penf64 = q4penf64_pack();
+#ifndef EMF_FUSED64
+#define EMF_FUSED64 1  // fp64 Q4 on axis-aligned meshes: x and u_k forward sweeps fused on kQ4PenF64
+#endif
+
 // ---- pencil sweeps ------------------------------------------------------------
 // Arguments are base pointers of consecutive per-element arrays of N3 values
 // (array t at base + t*N3) with Lay<N>::at addressing.  `w` is the worker
@@ -646,7 +697,7 @@ struct ApplyV2Smem {
   T r2[EPB][9][SZ];
   // fp64 Q4 with u_k swept: the x gradient parks in its own arrays until the
   // integrand needs it, instead of 9 registers held across the u_k sweeps
-  static constexpr bool kGx3 = EMF_GX_SMEM && P == 4 && sizeof(T) == 8 && kUk;
+  static constexpr bool kGx3 = EMF_GX_SMEM && P == 4 && sizeof(T) == 8 && kUk && !(EMF_FUSED64 && CART);
   T r3[kGx3 ? EPB : 1][kGx3 ? 9 : 1][kGx3 ? SZ : 1];
 };
 
@@ -763,7 +814,16 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   // fp32 Q4 with u_k swept (fused forward sweeps): kQ4Pen32
   constexpr bool kMap32 = EMF_Q4MAP32 && P == 4 && sizeof(T) == 4 && SM::kUk && !(EMF_V2_DENSE && EPB == 2);
   constexpr bool kTA = kMap || kMap32;  // direction-major gradient arrays
+  // fp64 Q4 fused forward sweeps: kQ4PenF64
+  // measured: axis-aligned Q4 cNH none 0.132 -> 0.128 ms (24^3), curved cfg2
+  // iNH none 2.21 -> 2.55 ms (both gradients and the early J0^-1 loads live
+  // through the longer fused sweeps), so axis-aligned meshes only
+  constexpr bool kFused64 = EMF_FUSED64 && kMap && SM::kUk && CART;
   unsigned pen32[3] = {0u, 0u, 0u};
+  if constexpr (kFused64) {
+    pen32[0] = c_q4penf64.v[tid][0];
+    pen32[1] = c_q4penf64.v[tid][1];
+  }
   if constexpr (kMap32) {
     pen32[0] = c_q4pen32.v[tid][0];
     pen32[1] = c_q4pen32.v[tid][1];
@@ -1002,8 +1062,8 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // fp32: x and u_k swept together (full lanes); fp64 keeps one vector per
     // sweep, whose shorter live ranges fit its 128/168-register budget
     // (measured: fused sweeps cost fp64 none 0.165 -> 0.175 ms, gave fp32 -3%)
-    constexpr bool kFused = kUk && sizeof(T) == 4 && !kDense;
-    if constexpr (kFused && kMap32) {
+    constexpr bool kFused = kUk && (sizeof(T) == 4 || kFused64) && !kDense;
+    if constexpr (kFused && (kMap32 || kFused64)) {
       // ---- both vectors per sweep, in place, on the thread's mapped pencil pair
       fwc_x<T, N, 2, N3, true>(S, R2, a.Bm, Dfx, (int)(pen32[0] & 255u), (int)((pen32[0] >> 8) & 255u));
       esync();

@@ -187,3 +187,21 @@ def f32_q4_maps(SY=5, SZ=25, SIZE=125):
 # items processed one after the other (short-scoreboard stalls on the 5-value
 # line loads) and 600-800 B of spills when both items' loads were issued
 # first, so it was dropped.
+
+
+def f64_q4_fused_maps(SY=5, SZ=25, SIZE=125):
+    """fp64 Q4 with the x / u_k forward sweeps fused (fwc_*: 150 pencils,
+    vc = wk / 25 over the 6 staged arrays; round 1 over threads 0-124, round 2
+    over threads 0-24): half-warp groups, 8-byte words (16 bank pairs)."""
+    lat = lambda a, b, c: a + SY * b + SZ * c
+    groups = [16] * 7 + [13] + [16, 9]
+    out = {}
+    for o in 'xyz':
+        res = []
+        for wk in range(150):
+            vc, r = wk // 25, wk % 25
+            u, v = r % 5, r // 5
+            base = {'x': lat(0, u, v), 'y': lat(u, 0, v), 'z': lat(u, v, 0)}[o]
+            res.append((vc * SIZE + base) % 16)
+        out['fwc_' + o] = solve_groups(res, groups, 16)
+    return out
