@@ -382,6 +382,17 @@ def add_roofline(rec, strat, prec, nel, ndofs, n, model, peaks):
     return rec
 
 
+def add_real_traffic(rec, tr, hbm):
+    """Beside the ledger yardstick: the DRAM bytes one launch of this variant
+    really moves (profiles/traffic.json, from an ncu capture) over this run's
+    element-kernel time, as a fraction of the measured HBM bandwidth."""
+    if not tr:
+        return rec
+    rec["dram_bytes_per_launch_ncu"] = tr["dram_bytes_per_launch"]
+    rec["hbm_frac_real_traffic"] = tr["dram_bytes_per_launch"] / (rec["ms_element_kernel"] * 1e-3) / 1e9 / hbm
+    return rec
+
+
 def load_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -495,10 +506,11 @@ def run_gpu(args):
     clocks = sampler.summary() if sampler else None
     peaks = {"nominal64": nominal_fma_tflops(64), "nominal32": nominal_fma_tflops(32), "measured64": fp64_meas,
              "measured32": fp32_meas, "hbm": hbm}
+    traffic = load_traffic()
     for k, r in variants.items():
         prec, strat = (64 if k.startswith("fp64") else 32), k.split("_", 1)[1]
         add_roofline(r, strat, prec, part.nel_local, lev.n_dofs, C2_P + 1, C2_MODEL, peaks)
-    traffic = load_traffic()
+        add_real_traffic(r, traffic.get("cfg2_" + k), hbm)
     head = variants["fp64_none"]
     tr = traffic.get("cfg2_fp64_none")
     fl = flops_per_element("none", C2_P + 1, C2_MODEL) * part.nel_local
@@ -533,6 +545,8 @@ def run_gpu(args):
         line["residual"] = res_rec
     if world == 1 and not args.no_extra:
         line["variants_cfg1"] = run_cfg1_sweep(args, flush, peaks)
+        for k, r in line["variants_cfg1"].items():
+            add_real_traffic(r, traffic.get("cfg1_" + k), hbm)
         line["workloads"] = run_extra_workloads(args, flush, peaks)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(args.cpu_seconds)
