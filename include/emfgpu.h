@@ -281,6 +281,11 @@ typedef struct emfgpu_slab emfgpu_slab;
 emfgpu_status emfgpu_comm_unique_id(unsigned char id[128]);
 emfgpu_status emfgpu_comm_create(const unsigned char id[128], int world, int rank, int device, emfgpu_comm** out);
 emfgpu_status emfgpu_comm_wrap(void* nccl_comm, int world, int rank, emfgpu_comm** out);
+/* One process, one host thread per rank: `world` communicators (out[r] for
+ * rank r, devices[r] its GPU, NULL = all on device 0) joined by a host
+ * rendezvous; the collectives become peer copies.  Rank r's calls must come
+ * from its own thread (every rank makes the same sequence of calls). */
+emfgpu_status emfgpu_comm_create_group(int world, const int* devices, emfgpu_comm** out);
 void emfgpu_comm_destroy(emfgpu_comm* c);
 /* comm may be NULL for world == 1 and for single-process groups. */
 emfgpu_status emfgpu_slab_create(emfgpu_op* op, int rank, int world, emfgpu_comm* comm, emfgpu_slab** out);

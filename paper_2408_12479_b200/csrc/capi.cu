@@ -15,6 +15,7 @@
 
 #include "capi_util.h"
 #include "internal.h"
+#include "krylov_core.h"
 
 using namespace emfgpu;
 using namespace emfgpu::capi;
@@ -1233,51 +1234,17 @@ emfgpu_status emfgpu_dot(int precision, const void* a, const void* b, int64_t n,
   });
 }
 
-namespace {
-int sturm_count(const std::vector<double>& al, const std::vector<double>& be, double sigma) {
-  int count = 0;
-  double d = al[0] - sigma;
-  if (d < 0) ++count;
-  for (size_t i = 1; i < al.size(); ++i) {
-    d = al[i] - sigma - be[i - 1] * be[i - 1] / (d == 0 ? 1e-300 : d);
-    if (d < 0) ++count;
-  }
-  return count;
-}
-double tridiag_extreme(const std::vector<double>& al, const std::vector<double>& be, bool largest) {
-  double lo = al[0], hi = al[0];
-  for (size_t i = 0; i < al.size(); ++i) {
-    const double bl = i > 0 ? std::abs(be[i - 1]) : 0.0;
-    const double br = i < be.size() ? std::abs(be[i]) : 0.0;
-    lo = std::min(lo, al[i] - bl - br);
-    hi = std::max(hi, al[i] + bl + br);
-  }
-  const int nev = (int)al.size();
-  for (int it = 0; it < 200; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    const int below = sturm_count(al, be, mid);
-    if (largest ? below < nev : below < 1)
-      lo = mid;
-    else
-      hi = mid;
-    if (hi - lo < 1e-10 * std::max(1.0, std::abs(hi))) break;
-  }
-  return 0.5 * (lo + hi);
-}
-}  // namespace
+
 
 template <typename T>
 static void lanczos(emfgpu_op* op, const T* diag, int iterations, uint64_t seed, double* lmin, double* lmax,
                     cudaStream_t s) {
-  // estimate_eigenvalues (solver.hpp:262-308): Lanczos on D^-1/2 A D^-1/2 with
-  // full (modified Gram-Schmidt) reorthogonalisation.  Device resident: the
-  // seeded start vector is generated on the device, the MGS coefficients
-  // never leave it, and one host read per step fetches beta (break test).
-  const int64_t n = op->L->ndofs;
-  const int maxit = (int)std::min<int64_t>(iterations, n);
-  const int nd = dot_partial_count() + 1;
-  const size_t need = sizeof(double) * ((size_t)n * (std::max(1, maxit) + 2) + (size_t)nd + 2 * (size_t)maxit + 2) +
-                      2 * sizeof(T) * (size_t)n + 64;
+  // estimate_eigenvalues (solver.hpp:262-308) on one GPU: the generic
+  // device-resident core (krylov_core.h) with the whole-lattice apply and the
+  // node-plane-chunked dot (bitwise the z-slab dot, csrc/slab_solver.cu)
+  const emfgpu_level* L = op->L;
+  const int64_t n = L->ndofs;
+  const size_t need = lanczos_work_bytes<T>(n, iterations, L->mz);
   if (op->lz_bytes < need) {
     cudaFree(op->lz_buf);
     op->lz_buf = nullptr;
@@ -1285,46 +1252,12 @@ static void lanczos(emfgpu_op* op, const T* diag, int iterations, uint64_t seed,
     CK(cudaMalloc(&op->lz_buf, need));
     op->lz_bytes = need;
   }
-  double* basis = op->lz_buf;
-  double* dis = basis + (size_t)n * std::max(1, maxit);
-  double* w = dis + n;
-  double* dbuf = w + n;          // dot partials + result
-  double* coef = dbuf + nd;      // alpha_j, beta_j
-  T* t = reinterpret_cast<T*>(coef + 2 * (size_t)maxit + 2);
-  T* at = t + n;
-  launch_lanczos_start(basis, n, (unsigned long long)seed, s);
-  launch_dot<double>(basis, basis, n, dbuf + 1, dbuf, s);
-  launch_div_sqrt_dev(dbuf, basis, basis, n, s);
-  launch_dinv_sqrt<T>(diag, dis, n, s);
-  std::vector<double> alpha, beta;
-  double hb = 0.0;
-  for (int j = 0; j < maxit; ++j) {
-    double* v = basis + (size_t)j * n;
-    launch_scale_to_T<T>(dis, v, t, n, s);
-    apply_full(op, t, at, s);
-    launch_scale_from_T<T>(dis, at, w, n, s);
-    if (j > 0) launch_axpy_minus(hb, basis + (size_t)(j - 1) * n, w, n, s);
-    launch_dot<double>(w, v, n, dbuf + 1, coef + 2 * j, s);  // alpha_j
-    launch_axpy_dev(coef + 2 * j, v, w, n, s);
-    for (int qb = 0; qb <= j; ++qb) {
-      const double* q = basis + (size_t)qb * n;
-      launch_dot<double>(w, q, n, dbuf + 1, dbuf, s);
-      launch_axpy_dev(dbuf, q, w, n, s);
-    }
-    launch_dot<double>(w, w, n, dbuf + 1, coef + 2 * j + 1, s);  // beta_j^2
-    double ab[2];
-    CK(cudaMemcpyAsync(ab, coef + 2 * j, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    alpha.push_back(ab[0]);
-    const double b = std::sqrt(ab[1]);
-    if (j + 1 < maxit) beta.push_back(b);
-    if (b < 1e-12) break;
-    if (j + 1 < maxit) launch_div(w, b, basis + (size_t)(j + 1) * n, n, s);
-    hb = b;
-  }
-  beta.resize(alpha.empty() ? 0 : alpha.size() - 1);
-  *lmax = tridiag_extreme(alpha, beta, true);
-  *lmin = tridiag_extreme(alpha, beta, false);
+  const int64_t plane = 3 * (int64_t)L->mx * L->my;
+  auto apply = [&](const T* x, T* y) { apply_full(op, x, y, s); };
+  auto dot = [&](const double* a, const double* b, double* part, double* out) {
+    launch_dot_planes<double>(a, b, plane, L->mz, part, out, s);
+  };
+  lanczos_core<T>(n, 0, L->mz, op->lz_buf, diag, iterations, seed, apply, dot, lmin, lmax, s);
 }
 
 emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, int iterations, uint64_t seed,
@@ -1870,7 +1803,11 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     // iteration.  Same arithmetic and order as the host loop it replaced.
     // work space cached on the operator (large cudaMalloc / cudaFree pairs
     // per solve cost 0-200 ms of host time, measured)
-    const size_t need = sizeof(double) * (4 * (size_t)n + dot_partial_count() + 1 + 8 + (size_t)maxit + 1) + 16;
+    // dots over whole node planes (launch_dot_planes): bitwise the z-slab PCG's
+    const int64_t plane = 3 * (int64_t)op->L->mx * op->L->my;
+    const int nplanes = op->L->mz;
+    const size_t ndot = (size_t)std::max(dot_partial_count(), nplanes * dot_plane_split());
+    const size_t need = sizeof(double) * (4 * (size_t)n + ndot + 1 + 8 + (size_t)maxit + 1) + 16;
     if (op->pcg_bytes < need) {
       cudaFree(op->pcg_buf);
       op->pcg_buf = nullptr;
@@ -1884,11 +1821,11 @@ emfgpu_status emfgpu_pcg_solve(emfgpu_op* op, emfgpu_mg* mg, const double* d_b, 
     double* const p = z + n;
     double* const ap = p + n;
     double* const dbuf = ap + n;
-    double* const sc = dbuf + dot_partial_count() + 1;
+    double* const sc = dbuf + ndot + 1;
     double* const dhist = sc + 8;
     int* const ic = reinterpret_cast<int*>(dhist + maxit + 1);
     auto dot_to = [&](const double* a, const double* b, double* out, cudaStream_t st) {
-      launch_dot<double>(a, b, n, dbuf, out, st);
+      launch_dot_planes<double>(a, b, plane, nplanes, dbuf, out, st);
     };
     auto prec = [&](const double* rr, double* zz, cudaStream_t st) {
       if (mg) {

@@ -81,6 +81,16 @@ void launch_inv(const T* d, T* inv, int64_t n, cudaStream_t s);
 template <typename T>
 void launch_dot(const T* a, const T* b, int64_t n, double* partial, double* out, cudaStream_t s);
 int dot_partial_count();
+// node-plane-chunked deterministic dot (solver.cu): partial slots = nplanes * dot_plane_split()
+template <typename T>
+void launch_dot_plane_partials(const T* a, const T* b, int64_t plane_len, int nplanes, int first_plane,
+                               double* partial, cudaStream_t s);
+void launch_sum_ordered(const double* partial, int64_t m, double* out, cudaStream_t s);
+int dot_plane_split();
+template <typename T>
+void launch_dot_planes(const T* a, const T* b, int64_t plane_len, int nplanes, double* partial, double* out,
+                       cudaStream_t s);
+
 template <typename T>
 void launch_scale_to_T(const double* s, const double* v, T* t, int64_t n, cudaStream_t st);
 template <typename T>
@@ -88,7 +98,7 @@ void launch_scale_from_T(const double* s, const T* at, double* w, int64_t n, cud
 template <typename T>
 void launch_dinv_sqrt(const T* d, double* s, int64_t n, cudaStream_t st);
 void launch_axpy_minus(double a, const double* x, double* y, int64_t n, cudaStream_t st);
-void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st);
+void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st, int64_t offset = 0);
 void launch_axpy_dev(const double* c, const double* x, double* y, int64_t n, cudaStream_t st);
 void launch_div_sqrt_dev(const double* d, const double* x, double* y, int64_t n, cudaStream_t st);
 void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st);

@@ -19,64 +19,18 @@
 // NCCL is loaded at run time (dlopen of libnccl.so.2: the copy the process
 // already has, e.g. torch's, else the system one), so the library has no
 // link-time NCCL dependency and single-GPU users never touch it.
-#include <dlfcn.h>
-#include <nccl.h>
-
 #include <cstring>
 #include <memory>
 #include <vector>
 
 #include "capi_util.h"
 #include "internal.h"
+#include "slab_transport.h"
 
 using namespace emfgpu;
 using namespace emfgpu::capi;
 
 namespace {
-
-struct NcclApi {
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-const NcclApi& nccl() {
-  static NcclApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return;
-    api.h = h;
-    auto sym = [h](const char* n) { return dlsym(h, n); };
-    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
-    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
-    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
-    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
-    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
-    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
-    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
-    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
-    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
-  });
-  if (!api.h || !api.Send || !api.Recv || !api.GroupStart || !api.GroupEnd || !api.AllGather)
-    throw ApiError(EMFGPU_ERR_CONFIG, "slab: libnccl.so.2 could not be loaded");
-  return api;
-}
-
-#define NCK(call)                                                                                 \
-  do {                                                                                            \
-    ncclResult_t r_ = (call);                                                                     \
-    if (r_ != ncclSuccess)                                                                        \
-      throw ApiError(EMFGPU_ERR_CUDA, std::string(#call) + ": " + nccl().GetErrorString(r_));     \
-  } while (0)
 
 // out = sum_{r < world} part[r], in rank order (bit-identical on every rank)
 __global__ void rank_sum_kernel(const double* part, int world, double* out) {
@@ -86,12 +40,6 @@ __global__ void rank_sum_kernel(const double* part, int world, double* out) {
 }
 
 }  // namespace
-
-struct emfgpu_comm {
-  ncclComm_t comm = nullptr;
-  bool owned = false;
-  int world = 1, rank = 0;
-};
 
 struct emfgpu_slab {
   emfgpu_op* op = nullptr;
@@ -161,9 +109,31 @@ emfgpu_status emfgpu_comm_create(const unsigned char* id, int world, int rank, i
     auto c = std::make_unique<emfgpu_comm>();
     NCK(nccl().CommInitRank(&c->comm, world, u, rank));
     c->owned = true;
+    c->device = device;
     c->world = world;
     c->rank = rank;
     *out = c.release();
+  });
+}
+
+emfgpu_status emfgpu_comm_create_group(int world, const int* devices, emfgpu_comm** out) {
+  if (world < 1 || !out) return EMFGPU_ERR_INVALID;
+  return guarded(nullptr, [&] {
+    auto g = std::make_shared<GroupState>(world);
+    std::vector<std::unique_ptr<emfgpu_comm>> cs;
+    for (int r = 0; r < world; ++r) {
+      auto c = std::make_unique<emfgpu_comm>();
+      c->world = world;
+      c->rank = r;
+      c->group = g;
+      c->device = devices ? devices[r] : 0;
+      g->dev[r] = c->device;
+      CK(cudaSetDevice(c->device));
+      CK(cudaEventCreateWithFlags(&g->ev_ready[r], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g->ev_read[r], cudaEventDisableTiming));
+      cs.push_back(std::move(c));
+    }
+    for (int r = 0; r < world; ++r) out[r] = cs[r].release();
   });
 }
 
@@ -254,21 +224,7 @@ emfgpu_status emfgpu_slab_apply(emfgpu_slab* s, const void* d_x, void* d_y, void
     slab_enqueue_boundary(s, d_x, st);
     // face exchange on the communication stream, overlapped with the interior layers
     CK(cudaStreamWaitEvent(s->cs, s->ev_packed, 0));
-    if (s->lo >= 0 || s->hi >= 0) {
-      const NcclApi& N = nccl();
-      const ncclDataType_t t = s->esize == 8 ? ncclFloat64 : ncclFloat32;
-      const size_t nf = (size_t)s->face_values;
-      NCK(N.GroupStart());
-      if (s->lo >= 0) {
-        NCK(N.Send(s->send_lo, nf, t, s->lo, s->comm->comm, s->cs));
-        NCK(N.Recv(s->recv_lo, nf, t, s->lo, s->comm->comm, s->cs));
-      }
-      if (s->hi >= 0) {
-        NCK(N.Send(s->send_hi, nf, t, s->hi, s->comm->comm, s->cs));
-        NCK(N.Recv(s->recv_hi, nf, t, s->hi, s->comm->comm, s->cs));
-      }
-      NCK(N.GroupEnd());
-    }
+    s->comm->exchange(s->send_lo, s->recv_lo, s->send_hi, s->recv_hi, s->esize * (size_t)s->face_values, s->cs);
     CK(cudaEventRecord(s->ev_comm, s->cs));
     slab_enqueue_interior_and_nodes(s, d_x, d_y, st);
   });
@@ -337,7 +293,9 @@ emfgpu_status emfgpu_slab_dot(emfgpu_slab* s, const void* a, const void* b, doub
     slab_dot_partial(s, a, b, part + s->rank, st);
     if (s->world > 1) {
       if (!s->comm) throw ApiError(EMFGPU_ERR_CONFIG, "slab dot: no communicator (use slab_group_dot)");
-      NCK(nccl().AllGather(part + s->rank, part, 1, ncclFloat64, s->comm->comm, st));
+      std::vector<long long> off(s->world), len(s->world, 1);
+      for (int q = 0; q < s->world; ++q) off[q] = q;
+      s->comm->allgather_ranges(part, sizeof(double), off, len, st);
     }
     rank_sum_kernel<<<1, 1, 0, st>>>(part, s->world, d_out);
     CK(cudaGetLastError());

@@ -148,6 +148,70 @@ void launch_dot(const T* a, const T* b, int64_t n, double* partial, double* out,
   dot_final_kernel<<<1, 1024, 0, s>>>(partial, out);
 }
 template void launch_dot<double>(const double*, const double*, int64_t, double*, double*, cudaStream_t);
+
+// ---- node-plane-chunked deterministic dot --------------------------------------
+// Partials of whole lattice node planes (kPlaneSplit fixed sub-ranges per plane,
+// each a fixed-order block reduction), then one ordered sum over all partials.
+// A z-slab computes the partials of its owned planes only; since every
+// partial is a function of its plane alone, the slab partials all-reduced
+// (exact: one nonzero per slot) and summed give bitwise the single-GPU dot
+// (csrc/slab_solver.cu).
+constexpr int kPlaneSplit = 4, kPlaneThreads = 256;
+
+template <typename T>
+__global__ void dot_planes_kernel(const T* __restrict__ a, const T* __restrict__ b, int64_t plane_len, int first_plane,
+                                  double* partial) {
+  __shared__ double sm[kPlaneThreads];
+  const int plane = blockIdx.x / kPlaneSplit, part = blockIdx.x % kPlaneSplit;
+  const int64_t chunk = (plane_len + kPlaneSplit - 1) / kPlaneSplit;
+  const int64_t i0 = (int64_t)plane * plane_len + part * chunk;
+  const int64_t i1 = (int64_t)plane * plane_len + min(plane_len, (int64_t)(part + 1) * chunk);
+  double s = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kPlaneThreads) s += double(a[i]) * double(b[i]);
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kPlaneThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(int64_t)(first_plane + plane) * kPlaneSplit + part] = sm[0];
+}
+
+__global__ void sum_ordered_kernel(const double* partial, int64_t m, double* out) {
+  __shared__ double sm[1024];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += 1024) s += partial[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
+template <typename T>
+void launch_dot_plane_partials(const T* a, const T* b, int64_t plane_len, int nplanes, int first_plane,
+                               double* partial, cudaStream_t s) {
+  if (nplanes > 0)
+    dot_planes_kernel<T><<<(unsigned)(nplanes * kPlaneSplit), kPlaneThreads, 0, s>>>(a, b, plane_len, first_plane,
+                                                                                     partial);
+}
+void launch_sum_ordered(const double* partial, int64_t m, double* out, cudaStream_t s) {
+  sum_ordered_kernel<<<1, 1024, 0, s>>>(partial, m, out);
+}
+int dot_plane_split() { return kPlaneSplit; }
+template <typename T>
+void launch_dot_planes(const T* a, const T* b, int64_t plane_len, int nplanes, double* partial, double* out,
+                       cudaStream_t s) {
+  launch_dot_plane_partials<T>(a, b, plane_len, nplanes, 0, partial, s);
+  launch_sum_ordered(partial, (int64_t)nplanes * kPlaneSplit, out, s);
+}
+template void launch_dot_plane_partials<double>(const double*, const double*, int64_t, int, int, double*,
+                                                cudaStream_t);
+template void launch_dot_plane_partials<float>(const float*, const float*, int64_t, int, int, double*, cudaStream_t);
+template void launch_dot_planes<double>(const double*, const double*, int64_t, int, double*, double*, cudaStream_t);
+template void launch_dot_planes<float>(const float*, const float*, int64_t, int, double*, double*, cudaStream_t);
 template void launch_dot<float>(const float*, const float*, int64_t, double*, double*, cudaStream_t);
 int dot_partial_count() { return kDotBlocks; }
 
@@ -180,10 +244,11 @@ __global__ void scal_d_kernel(const double* __restrict__ x, double inv, double* 
 
 // Lanczos start vector (solver.hpp:274-277): element i of the sequential
 // splitmix64 stream is mix(seed + (i+1) gamma), so it is generated in parallel.
-__global__ void lanczos_start_kernel(double* __restrict__ v, int64_t n, unsigned long long seed) {
+__global__ void lanczos_start_kernel(double* __restrict__ v, int64_t n, unsigned long long seed, int64_t offset) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  unsigned long long z = seed + (unsigned long long)(i + 1) * 0x9e3779b97f4a7c15ull;
+  // element (offset + i) of the reference's sequential splitmix64 stream
+  unsigned long long z = seed + (unsigned long long)(offset + i + 1) * 0x9e3779b97f4a7c15ull;
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
   z ^= z >> 31;
@@ -201,8 +266,8 @@ __global__ void div_sqrt_dev_kernel(const double* __restrict__ d, const double* 
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[i] / sqrt(d[0]);
 }
-void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st) {
-  lanczos_start_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, seed);
+void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st, int64_t offset) {
+  lanczos_start_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, seed, offset);
 }
 void launch_axpy_dev(const double* c, const double* x, double* y, int64_t n, cudaStream_t st) {
   axpy_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(c, x, y, n);
