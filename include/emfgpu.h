@@ -311,6 +311,32 @@ emfgpu_status emfgpu_slab_dot(emfgpu_slab* s, const void* d_a, const void* d_b, 
 emfgpu_status emfgpu_slab_group_dot(emfgpu_slab* const* slabs, int n, const void* const* d_a, const void* const* d_b,
                                     double* const* d_out, void* const* streams);
 
+/* ---- the cfg4 solve in z slabs (SURVEY §8(e) ¶3) -------------------------------
+ * fp64 PCG preconditioned by the hp-multigrid V-cycle with the finest level
+ * partitioned like the apply (faces exchanged, node-plane dots all-gathered)
+ * and the next level (p/2, same mesh) and everything below agglomerated:
+ * every rank holds them whole and runs that part of the V-cycle redundantly.
+ * Every rank's iterates are bitwise the single-GPU emfgpu_pcg_solve's with
+ * emfgpu_mg_create(global level, ..., cfg) on its node planes.
+ * slab: the rank's z-slab level of `global` (the SlabPartition split: the
+ * first nz % world ranks take one more element layer; z_offset = first
+ * layer); global: the whole fine level's description (generated map);
+ * fine degree >= 2, >= 2 element layers per rank.  All calls are collective
+ * (SPMD) over the communicator. */
+typedef struct emfgpu_slab_solver emfgpu_slab_solver;
+emfgpu_status emfgpu_slab_solver_create(const emfgpu_level* slab, const emfgpu_level_desc* global, int rank,
+                                        int world, emfgpu_comm* comm, int model, const emfgpu_material* params,
+                                        int strategy, const emfgpu_mg_config* cfg, emfgpu_slab_solver** out);
+void emfgpu_slab_solver_destroy(emfgpu_slab_solver* s);
+const char* emfgpu_slab_solver_last_error(const emfgpu_slab_solver* s);
+/* update_linearization of the outer operator and the whole hierarchy; d_u: the slab's u_k (fp64). */
+emfgpu_status emfgpu_slab_solver_update_linearization(emfgpu_slab_solver* s, const double* d_u, void* stream);
+emfgpu_status emfgpu_slab_solver_apply(emfgpu_slab_solver* s, const double* d_x, double* d_y, void* stream);
+emfgpu_status emfgpu_slab_solver_precondition(emfgpu_slab_solver* s, const double* d_r, double* d_z, void* stream);
+/* emfgpu_pcg_solve on the slab vectors (same status conventions). */
+emfgpu_status emfgpu_slab_pcg_solve(emfgpu_slab_solver* s, const double* d_b, double* d_x, double rtol, int maxit,
+                                    int* iterations, double* history, void* stream);
+
 /* ---- residual and loads ----------------------------------
  * evaluate_residual(u, r), operator.hpp:94-95/623-641 (both domains):
  * r_i = (Grad v_i, F S) - load_scale * load_i, Dirichlet rows zeroed. */

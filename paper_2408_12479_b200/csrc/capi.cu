@@ -1471,6 +1471,42 @@ void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
 
 }  // namespace
 
+// Pieces of the single-GPU operator and hierarchy used by the z-slab solver
+// (slab_solver.cu); callers hold the handles' ordering themselves.
+namespace emfgpu {
+namespace capi {
+void op_diag_elements(emfgpu_op* op, cudaStream_t s) {
+  if (op->precision == 64)
+    dispatch_diagonal<double>(op, kargs<double>(op), s);
+  else
+    dispatch_diagonal<float>(op, kargs<float>(op), s);
+  CK(cudaGetLastError());
+}
+template <typename T>
+void transfer_apply_T(emfgpu_transfer* t, int kind, const T* in, T* out, cudaStream_t s) {
+  transfer_run<T>(t, kind, in, out, s);
+  CK(cudaGetLastError());
+}
+template void transfer_apply_T<double>(emfgpu_transfer*, int, const double*, double*, cudaStream_t);
+template void transfer_apply_T<float>(emfgpu_transfer*, int, const float*, float*, cudaStream_t);
+void mg_linearize_any(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
+  if (m->cfg.precision == 64)
+    mg_linearize<double>(m, d_u, s);
+  else
+    mg_linearize<float>(m, d_u, s);
+}
+void mg_vcycle0(emfgpu_mg* m, cudaStream_t s) {
+  if (m->cfg.precision == 64)
+    v_cycle<double>(m, 0, s);
+  else
+    v_cycle<float>(m, 0, s);
+  CK(cudaGetLastError());
+}
+void* mg_b0(emfgpu_mg* m) { return m->b[0]; }
+void* mg_x0(emfgpu_mg* m) { return m->x[0]; }
+}  // namespace capi
+}  // namespace emfgpu
+
 void emfgpu_mg_default_config(emfgpu_mg_config* c) {
   if (!c) return;
   c->degree = 6;

@@ -84,6 +84,16 @@ struct UseGuard {
 void op_elements(emfgpu_op* op, const void* x, int k0, int k1, cudaStream_t s);
 void op_nodes(emfgpu_op* op, const void* x, void* y, const void* ghost_lo, const void* ghost_hi, cudaStream_t s);
 void op_pack_face(emfgpu_op* op, int k, int side, void* face, cudaStream_t s);
+// element-local diagonal contributions into the operator's local buffer (capi.cu)
+void op_diag_elements(emfgpu_op* op, cudaStream_t s);
+// TransferOp kinds 0 prolongate, 1 restrict, 2 interpolate down (capi.cu)
+template <typename T>
+void transfer_apply_T(emfgpu_transfer* t, int kind, const T* in, T* out, cudaStream_t s);
+// the single-GPU hierarchy from its level 0 (capi.cu)
+void mg_linearize_any(emfgpu_mg* m, const double* d_u, cudaStream_t s);
+void mg_vcycle0(emfgpu_mg* m, cudaStream_t s);  // x0 = V-cycle(b0)
+void* mg_b0(emfgpu_mg* m);
+void* mg_x0(emfgpu_mg* m);
 
 }  // namespace capi
 }  // namespace emfgpu

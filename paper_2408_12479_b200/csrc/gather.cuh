@@ -53,7 +53,7 @@ template <typename T, int P, bool CG = false, bool GHOSTS = true>
 __device__ __forceinline__ void assemble_node(const T* __restrict__ loc, const T* __restrict__ ghost_lo,
                                               const T* __restrict__ ghost_hi, const T* x, T* y, int a, int b, int c,
                                               int nx, int ny, int nz, int faces, int kpar, int periodic_y) {
-  constexpr int N = P + 1, N3 = N * N * N, N2 = N * N;
+  constexpr int N = P + 1, N2 = N * N;
   const int mx = nx * P + 1, my = ny * P + (periodic_y ? 0 : 1), mz = nz * P + 1;
   const int64_t idx = ((int64_t)c * my + b) * mx + a;
   if (node_constrained(a, b, c, mx, my, mz, faces)) {

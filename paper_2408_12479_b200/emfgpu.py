@@ -266,6 +266,7 @@ class FeLevel:
         if st:
             raise EmfGpuError(st, lib().emfgpu_global_last_error().decode())
         self.h = h.value
+        self.desc = d
         self.nx, self.ny, self.nz, self.p = nx, ny, nz, p
         self.faces = dirichlet_faces
         self.periodic_y = bool(periodic_y)
@@ -771,3 +772,86 @@ def slab_group_dot(slabs, a_s, b_s, outs, streams):
                                      _arr([_stream(t) for t in streams]))
     if st:
         raise EmfGpuError(st, lib().emfgpu_slab_last_error(slabs[0].h).decode())
+
+
+def comm_group(world, devices=None):
+    """emfgpu_comm_create_group: `world` communicators for ranks run as host
+    threads of this process (rank r's calls from its own thread)."""
+    arr = (C.c_void_p * world)()
+    dv = (C.c_int * world)(*(devices or [0] * world))
+    L = lib()
+    L.emfgpu_comm_create_group.restype = C.c_int
+    L.emfgpu_comm_create_group.argtypes = [C.c_int, C.c_void_p, C.c_void_p]
+    _check(L.emfgpu_comm_create_group(world, dv, arr))
+    out = []
+    for r in range(world):
+        c = Comm.__new__(Comm)
+        c.h, c.world, c.rank = arr[r], world, r
+        out.append(c)
+    return out
+
+
+class SlabSolver:
+    """emfgpu_slab_solver: the cfg4 PCG + hp-multigrid solve with the finest
+    level on this rank's z slab and the coarser levels agglomerated (all
+    calls collective over the communicator)."""
+
+    def __init__(self, slab: FeLevel, global_level: FeLevel, rank, world, comm: Comm | None, model="inh",
+                 params: MaterialParams | None = None, strategy="none", degree=6, coarse_n=1, precision=32,
+                 coarse_direct_limit=2000, eig_iterations=20):
+        L = lib()
+        for name, (res, args) in {
+            "emfgpu_slab_solver_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                                    C.POINTER(Material), C.c_int, C.POINTER(MgConfig),
+                                                    C.POINTER(C.c_void_p)]),
+            "emfgpu_slab_solver_destroy": (None, [C.c_void_p]),
+            "emfgpu_slab_solver_last_error": (C.c_char_p, [C.c_void_p]),
+            "emfgpu_slab_solver_update_linearization": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+            "emfgpu_slab_solver_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+            "emfgpu_slab_solver_precondition": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+            "emfgpu_slab_pcg_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                                C.POINTER(C.c_int), C.c_void_p, C.c_void_p]),
+            "emfgpu_mg_default_config": (None, [C.POINTER(MgConfig)]),
+        }.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        cfg = MgConfig()
+        L.emfgpu_mg_default_config(C.byref(cfg))
+        cfg.degree, cfg.eig_iterations, cfg.coarse_n, cfg.precision = degree, eig_iterations, coarse_n, precision
+        cfg.coarse_direct_limit = coarse_direct_limit
+        self._cfg = cfg
+        self.params = params or MaterialParams()
+        self._mat = self.params.to_c()
+        self.slab, self.global_level = slab, global_level
+        h = C.c_void_p()
+        st = L.emfgpu_slab_solver_create(slab.h, C.byref(global_level.desc), rank, world, comm.h if comm else None,
+                                         MODELS[model], C.byref(self._mat), STRATEGIES[strategy], C.byref(cfg),
+                                         C.byref(h))
+        if st:
+            raise EmfGpuError(st, L.emfgpu_global_last_error().decode())
+        self.h = h.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.emfgpu_slab_solver_destroy(self.h)
+            self.h = None
+
+    def _ok(self, st):
+        if st:
+            raise EmfGpuError(st, lib().emfgpu_slab_solver_last_error(self.h).decode())
+
+    def update_linearization(self, d_u, stream=None):
+        self._ok(lib().emfgpu_slab_solver_update_linearization(self.h, _ptr(d_u), _stream(stream)))
+
+    def apply(self, d_x, d_y, stream=None):
+        self._ok(lib().emfgpu_slab_solver_apply(self.h, _ptr(d_x), _ptr(d_y), _stream(stream)))
+
+    def precondition(self, d_r, d_z, stream=None):
+        self._ok(lib().emfgpu_slab_solver_precondition(self.h, _ptr(d_r), _ptr(d_z), _stream(stream)))
+
+    def pcg_solve(self, d_b, d_x, rtol=1e-8, maxit=200, stream=None):
+        it = C.c_int()
+        hist = np.zeros(maxit + 1)
+        self._ok(lib().emfgpu_slab_pcg_solve(self.h, _ptr(d_b), _ptr(d_x), rtol, maxit, C.byref(it), hist.ctypes.data,
+                                             _stream(stream)))
+        return it.value, hist[:it.value + 1]

@@ -1092,3 +1092,69 @@ def test_slab_nccl_communicator_single_rank(G):
     assert np.array_equal(y.cpu().numpy(), y_ref)
     assert abs(float(out.item()) - float(np.dot(v, y_ref))) <= 1e-12 * abs(float(np.dot(v, y_ref)))
     del slab, comm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,shear", [(2, 0.0), (3, 0.0), (4, 0.1)])
+def test_slab_pcg_multigrid_bitwise_vs_single_gpu(G, world, shear):
+    """The cfg4 solve partitioned in z slabs (emfgpu_slab_solver: finest
+    level on the slabs with face exchange, ghost-layer restriction and
+    node-plane dots; p/2 level and below agglomerated), ranks run as host
+    threads on one GPU (thread-group transport): iteration count, residual
+    history and every rank's x are bitwise the single-GPU PCG + hp-MG solve."""
+    import threading
+
+    import torch
+    n, p = 12, 4
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    lev = G.FeLevel(n, p=p, map="shear_x", map_param=(shear,)) if shear else G.FeLevel(n, p=p)
+    u0 = np.zeros(lev.n_dofs)  # the well-posed cfg4 variant (u0 = 0)
+    b_np = I.make_v(lev.n_dofs, 2)
+    b_np[I.dirichlet_mask(n, n, n, p, 1)] = 0.0
+    op = G.ElasticOperator(lev, "inh", prm, "none", 64)
+    op.update_linearization(u0)
+    mg = G.MgHierarchy(lev, "inh", prm, degree=5, coarse_n=6, precision=32)
+    mg.update_linearization(torch.tensor(u0, device="cuda"))
+    b = torch.tensor(b_np, device="cuda")
+    x1 = torch.empty_like(b)
+    its1, hist1 = G.pcg_solve(op, mg, b, x1, 1e-8, 200)
+    x1 = x1.cpu().numpy()
+    coords = lev.node_coords()
+    m = n * p + 1
+    plane = 3 * m * m
+    comms = G.comm_group(world)
+    res = [None] * world
+    errs = []
+
+    def rank_main(r):
+        try:
+            from paper_2408_12479_b200.slab import SlabPartition
+            part = SlabPartition(n, n, n, p, world, r, faces=1)
+            sl = slice(part.c0 * plane, (part.c1 + 1) * plane)
+            slab = G.FeLevel(n, n, part.nz_local, p=p, coords=coords[sl], dirichlet_faces=part.local_faces,
+                             z_offset=part.k0)
+            sv = G.SlabSolver(slab, lev, r, world, comms[r], "inh", prm, degree=5, coarse_n=6, precision=32)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                du = torch.tensor(u0[sl], device="cuda")
+                db = torch.tensor(b_np[sl], device="cuda")
+                dx = torch.empty_like(db)
+            sv.update_linearization(du, stream=st)
+            its, hist = sv.pcg_solve(db, dx, 1e-8, 200, stream=st)
+            st.synchronize()
+            res[r] = (its, hist, dx.cpu().numpy(), sl)
+            del sv
+        except Exception as ex:  # noqa: BLE001
+            errs.append(repr(ex))
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for r in range(world):
+        its, hist, x, sl = res[r]
+        assert its == its1, (r, its, its1)
+        assert np.array_equal(hist, hist1), r
+        assert np.array_equal(x, x1[sl]), (r, np.abs(x - x1[sl]).max())
