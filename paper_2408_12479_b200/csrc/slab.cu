@@ -224,7 +224,8 @@ emfgpu_status emfgpu_slab_apply(emfgpu_slab* s, const void* d_x, void* d_y, void
     slab_enqueue_boundary(s, d_x, st);
     // face exchange on the communication stream, overlapped with the interior layers
     CK(cudaStreamWaitEvent(s->cs, s->ev_packed, 0));
-    s->comm->exchange(s->send_lo, s->recv_lo, s->send_hi, s->recv_hi, s->esize * (size_t)s->face_values, s->cs);
+    if (s->comm)  // world 1 needs none (no neighbours)
+      s->comm->exchange(s->send_lo, s->recv_lo, s->send_hi, s->recv_hi, s->esize * (size_t)s->face_values, s->cs);
     CK(cudaEventRecord(s->ev_comm, s->cs));
     slab_enqueue_interior_and_nodes(s, d_x, d_y, st);
   });

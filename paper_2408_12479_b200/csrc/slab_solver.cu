@@ -99,8 +99,9 @@ void slab_apply(emfgpu_slab_solver* S, emfgpu_op* op, const T* x, T* y, cudaStre
   if (S->hi) op_pack_face(op, nzl - 1, 1, S->face_hi, st);
   CK(cudaEventRecord(S->ev_packed, st));
   CK(cudaStreamWaitEvent(S->cs, S->ev_packed, 0));
-  S->comm->exchange(S->face_lo, S->ghost_lo, S->face_hi, S->ghost_hi,
-                    sizeof(T) * (size_t)emfgpu_op_face_values(op), S->cs);
+  if (S->comm)
+    S->comm->exchange(S->face_lo, S->ghost_lo, S->face_hi, S->ghost_hi,
+                      sizeof(T) * (size_t)emfgpu_op_face_values(op), S->cs);
   CK(cudaEventRecord(S->ev_comm, S->cs));
   if (nzl > 2) op_elements(op, x, 1, nzl - 1, st);
   CK(cudaStreamWaitEvent(st, S->ev_comm, 0));
@@ -115,8 +116,9 @@ void slab_diagonal(emfgpu_slab_solver* S, emfgpu_op* op, T* d, cudaStream_t st) 
   op_diag_elements(op, st);
   if (S->lo) op_pack_face(op, 0, 0, S->face_lo, st);
   if (S->hi) op_pack_face(op, L->nz - 1, 1, S->face_hi, st);
-  S->comm->exchange(S->face_lo, S->ghost_lo, S->face_hi, S->ghost_hi, sizeof(T) * (size_t)emfgpu_op_face_values(op),
-                    st);
+  if (S->comm)
+    S->comm->exchange(S->face_lo, S->ghost_lo, S->face_hi, S->ghost_hi,
+                      sizeof(T) * (size_t)emfgpu_op_face_values(op), st);
   op_nodes(op, d, d, S->lo ? S->ghost_lo : nullptr, S->hi ? S->ghost_hi : nullptr, st);
   launch_diag_finish<T>(d, L->nnodes, L->mx, L->my, L->mz, L->faces, S->nbad, nullptr, 0, st);
   CK(cudaGetLastError());
@@ -137,7 +139,7 @@ void slab_dot(emfgpu_slab_solver* S, const T* a, const T* b, double* part, doubl
   }
   const int own = (int)(len[S->rank] / split);
   launch_dot_plane_partials<T>(a, b, S->plane_f, own, S->k0 * S->pf, part, st);
-  S->comm->allgather_ranges(part, sizeof(double), off, len, st);
+  if (S->comm) S->comm->allgather_ranges(part, sizeof(double), off, len, st);
   launch_sum_ordered(part, (int64_t)S->nplanes_g * split, out, st);
 }
 
@@ -180,7 +182,7 @@ void slab_to_coarse(emfgpu_slab_solver* S, int kind, const T* f, T* cg, cudaStre
   T* recv_hi = ext + own_off + (int64_t)L->mz * pf_n;
   const T* send_lo = f + pf_n;                               // local planes 1..pf
   const T* send_hi = f + (int64_t)(L->mz - 1 - S->pf) * pf_n;  // local planes mz-1-pf .. mz-2
-  S->comm->exchange(send_lo, recv_lo, send_hi, recv_hi, gbytes, st);
+  if (S->comm) S->comm->exchange(send_lo, recv_lo, send_hi, recv_hi, gbytes, st);
   T* cext = static_cast<T*>(S->coarse_ext);
   transfer_apply_T<T>(S->tr, kind, ext, cext, st);
   // own coarse planes [k0 pc, k1 pc] sit at extended plane lo*pc
@@ -194,7 +196,7 @@ void slab_to_coarse(emfgpu_slab_solver* S, int kind, const T* f, T* cg, cudaStre
     off[q] = (long long)first * pc_n;
     len[q] = (long long)(last - first + 1) * pc_n;
   }
-  S->comm->allgather_ranges(cg, sizeof(T), off, len, st);
+  if (S->comm) S->comm->allgather_ranges(cg, sizeof(T), off, len, st);
 }
 
 // replicated coarse vector -> fine slab (prolongation), result in the own
