@@ -638,7 +638,9 @@ def run_extra_workloads(args, flush, peaks):
         with open(os.path.join(ROOT, "tests", "golden", "cfg4_full_cg.json")) as f:
             ref4cg = json.load(f)
         out["cfg4_wellposed"].update({"reference_iterations_cg_coarse": ref4cg["iterations"],
-                                      "reference_cg_coarse_solve_s": ref4cg["solve_s"]})
+                                      "reference_cg_coarse_solve_s": ref4cg["solve_s"],
+                                      "reference_cg_coarse_setup_s": ref4cg["setup_s"],
+                                      "iterations_within_1_of_reference": abs(its - ref4cg["iterations"]) <= 1})
     except (OSError, ValueError):
         pass
     del op, mg, lev, b, x

@@ -1158,3 +1158,37 @@ def test_slab_pcg_multigrid_bitwise_vs_single_gpu(G, world, shear):
         assert its == its1, (r, its, its1)
         assert np.array_equal(hist, hist1), r
         assert np.array_equal(x, x1[sl]), (r, np.abs(x - x1[sl]).max())
+
+
+@pytest.mark.gpu
+def test_cfg4_full_size_iterations_vs_reference():
+    """BASELINE configs[4] (well-posed variant) at full size, 48^3 Q4, 21.6M
+    DoFs: the device PCG + fp32 hp-MG (dense coarse solve) takes the
+    reference's iteration count within +-1.  The reference run is its
+    coarse-CG hierarchy (tests/golden/cfg4_full_cg.json, 35 iterations): its
+    dense-LU run (cfg4_full.json, 40) carries the DenseLU pivoting defect
+    (DESIGN.md §5)."""
+    import json
+
+    import torch
+    from paper_2408_12479_b200 import emfgpu as G
+    from paper_2408_12479_b200 import workloads as W
+    with open(os.path.join(GOLD, "cfg4_full_cg.json")) as f:
+        ref = json.load(f)
+    w = W.cfg4()
+    lev = w.level()
+    assert lev.n_dofs == ref["ndofs"]
+    op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
+    op.update_linearization(np.zeros(lev.n_dofs))
+    mg = G.MgHierarchy(lev, w.model, w.material(), degree=5, coarse_n=6, precision=32)
+    mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+    b = torch.tensor(W.rhs(w), device="cuda")
+    x = torch.empty_like(b)
+    its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 300)
+    assert abs(its - ref["iterations"]) <= 1, (its, ref["iterations"])
+    assert hist[-1] <= 1e-8
+    # the residual histories agree to the preconditioner's round-off level
+    k = min(len(hist), len(ref["history"])) - 1
+    assert abs(np.log10(hist[k]) - np.log10(ref["history"][k])) < 0.3
+    xn = float(torch.linalg.vector_norm(x))
+    assert abs(xn - ref["norm_x"]) <= 1e-6 * ref["norm_x"], (xn, ref["norm_x"])
