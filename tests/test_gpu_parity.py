@@ -1191,4 +1191,4 @@ def test_cfg4_full_size_iterations_vs_reference():
     k = min(len(hist), len(ref["history"])) - 1
     assert abs(np.log10(hist[k]) - np.log10(ref["history"][k])) < 0.3
     xn = float(torch.linalg.vector_norm(x))
-    assert abs(xn - ref["norm_x"]) <= 1e-6 * ref["norm_x"], (xn, ref["norm_x"])
+    assert abs(xn - ref["norm_x"]) <= 1e-8 * ref["norm_x"], (xn, ref["norm_x"])  # measured 1.0e-10
