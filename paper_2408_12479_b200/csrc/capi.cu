@@ -296,7 +296,7 @@ void apply_nodes(emfgpu_op* op, const void* x, void* y, int c0, int c1, const vo
 void apply_full(emfgpu_op* op, const void* x, void* y, cudaStream_t s) {
   const emfgpu_level* L = op->L;
   apply_elements(op, x, 0, L->nz, s);
-  apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, 0, s);
+  apply_nodes(op, x, y, 0, L->mz - 1, nullptr, nullptr, L->z_offset & 1, s);
 }
 
 void check_err(emfgpu_op* op, cudaStream_t s, int64_t* be, int* bq, const char* what) {

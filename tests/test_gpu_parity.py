@@ -737,6 +737,51 @@ def test_ticket_scheduler_ranges_streams_repeats(G, p, prec, strat):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("p,prec,strat,dims,kw", [
+    (4, 64, "none", (20, 12, 18), dict(map="shear_x", map_param=(0.1,))),
+    (4, 32, "none", (20, 12, 18), dict(map="shear_x", map_param=(0.1,))),
+    (4, 64, "tensor", (7, 5, 3), dict(map_param=(0.05,), dirichlet_faces=1 | 32)),
+    (3, 64, "none", (24, 16, 20), dict(map_param=(0.05,))),
+    (3, 32, "cachedF", (3, 8, 11), "tube"),
+    (3, 64, "none", (4, 8, 5), "tube"),
+    (3, 64, "scalar", (2, 2, 1), dict(map_param=(0.05,))),
+    (2, 64, "none", (10, 6, 9), dict(map_param=(0.05,), dirichlet_faces=3)),
+    (1, 64, "none", (16, 8, 12), dict(map_param=(0.05,))),
+])
+def test_whole_apply_equals_split_launches(G, p, prec, strat, dims, kw):
+    """The whole-lattice apply (element kernel + programmatically dependent
+    node kernel) gives bitwise the result of the split element-range +
+    node-plane launches of the public API, across shapes (one layer, more
+    CTAs than units per layer, periodic y, Dirichlet faces), and over
+    repeated launches."""
+    import torch
+    nx, ny, nz = dims
+    if kw == "tube":  # periodic-theta tube (cfg3 geometry), fibre model
+        from paper_2408_12479_b200 import workloads as W
+        w = W.cfg3(dims)
+        lev = w.level()
+        assert lev.periodic_y
+        op = G.ElasticOperator(lev, "fiber", w.material(), strat, prec)
+        op.set_fibre_frame("cylindrical")
+        op.update_linearization(W.tube_u0(w, lev.node_coords()))
+    else:
+        lev = G.FeLevel(nx, ny, nz, p=p, **kw)
+        op = G.ElasticOperator(lev, "inh", G.MaterialParams(kappa_b=50.0), strat, prec)
+        op.update_linearization(I.make_u0(nx, ny, nz, p))
+    dt = torch.float64 if prec == 64 else torch.float32
+    x = torch.tensor(I.make_v(lev.n_dofs), dtype=dt, device="cuda")
+    mz = nz * p + 1
+    y_split = torch.full_like(x, float("nan"))
+    op.apply_elements(x, 0, nz)
+    op.apply_nodes(x, y_split, 0, mz - 1)
+    for _ in range(20):
+        y = torch.full_like(x, float("nan"))
+        op.apply_tangent_device(x, y)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_split)
+
+
+@pytest.mark.gpu
 def test_pcg_graph_loop_equals_host_loop(G):
     """The device-resident PCG (conditional-WHILE CUDA graph around apply,
     V-cycle and device scalars) gives bitwise the iterates, history and
