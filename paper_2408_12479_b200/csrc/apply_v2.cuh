@@ -20,6 +20,7 @@
 //    as contiguous vector stores, for the node phase (gather.cu).
 // The quadrature-point algebra is in qp.cuh.
 #pragma once
+#include "eo_sweeps.cuh"
 #include "kernels.cuh"
 
 #ifndef EMF_TEN_EARLY
@@ -42,6 +43,11 @@
 #endif
 #ifndef EMF_MINB_F32Q4
 #define EMF_MINB_F32Q4 0  // fp32 Q4 CTAs/SM override (experiments)
+#endif
+
+// Q4: collocated even-odd sweeps (eo_sweeps.cuh) instead of the B/D sweeps
+#ifndef EMF_COLL
+#define EMF_COLL 1
 #endif
 
 namespace emfgpu {
@@ -681,6 +687,133 @@ __device__ __forceinline__ void tr_x(const T* qv0, T* loc, int64_t e0, int nx, F
   }
 }
 
+// ---- collocated even-odd sweeps (eo_sweeps.cuh) ---------------------------------
+// Arrays: S = the staged vectors (NV*3 arrays: x [, u_k]), interpolated in
+// place to the Gauss points; G = the gradients at the Gauss points, array
+// (3 NV) t + vc for direction t and staged array vc, so every access of a
+// sweep is "vc + constant" (the thread -> pencil maps stay conflict-free).
+template <int NV>
+__host__ __device__ constexpr int coll_gi(int t, int vc) { return 3 * NV * t + vc; }
+
+// Interpolation along DIR, in place; WITHD (the last direction): also the
+// collocated derivative along DIR of the interpolated pencil, into G.
+template <typename T, int N, int NV, int DIR, bool JCK, bool WITHD>
+__device__ __forceinline__ void coll_interp(T* S, T* G, const T* eoB, const T* eoD, int wk) {
+  using L = Lay<N, sizeof(T)>;
+  using E = EO<T, N>;
+  if (wk >= NV * 3 * L::N2) return;
+  int vc, off;
+  pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, vc, off);
+  constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
+  T* const p = S + vc * L::SIZE + off;
+  T u[N], o[N], e[E::CH], d[E::H];
+  pencil_load<T, N, ST>(p, u);
+  E::split(u, e, d);
+  E::B_split(eoB, e, d, o);
+  pencil_store<T, N, ST>(p, o);
+  if (WITHD) {
+    E::split(o, e, d);
+    E::D_split(eoD, e, d, u);
+    pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, vc) * L::SIZE + off, u);
+  }
+}
+// Collocated derivative along DIR of the interpolated arrays: S -> G.
+template <typename T, int N, int NV, int DIR, bool JCK>
+__device__ __forceinline__ void coll_deriv(const T* S, T* G, const T* eoD, int wk) {
+  using L = Lay<N, sizeof(T)>;
+  using E = EO<T, N>;
+  if (wk >= NV * 3 * L::N2) return;
+  int vc, off;
+  pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, vc, off);
+  constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
+  T u[N], o[N], e[E::CH], d[E::H];
+  pencil_load<T, N, ST>(S + vc * L::SIZE + off, u);
+  E::split(u, e, d);
+  E::D_split(eoD, e, d, o);
+  pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, vc) * L::SIZE + off, o);
+}
+// Transposed derivative along DIR of the integrand's column DIR (W = its
+// three component arrays): A[c] = Dc^T W[c].
+template <typename T, int N, int DIR, bool JCK>
+__device__ __forceinline__ void coll_dT(const T* W, T* A, const T* eoD, int wk) {
+  using L = Lay<N, sizeof(T)>;
+  using E = EO<T, N>;
+  if (wk >= 3 * L::N2) return;
+  int c, off;
+  pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, c, off);
+  constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
+  T u[N], o[N], e[E::CH], d[E::H];
+  pencil_load<T, N, ST>(W + c * L::SIZE + off, u);
+  E::split(u, e, d);
+  E::Dt_split(eoD, e, d, o);
+  pencil_store<T, N, ST>(A + c * L::SIZE + off, o);
+}
+// z: Z[c] = Bz^T (A0[c] + A1[c] + Dc_z^T W2[c])
+template <typename T, int N>
+__device__ __forceinline__ void coll_trz(const T* W2, const T* A0, const T* A1, T* Z, const T* eoB, const T* eoD,
+                                         int wk) {
+  using L = Lay<N, sizeof(T)>;
+  using E = EO<T, N>;
+  if (wk >= 3 * L::N2) return;
+  int c, off;
+  pencil_decode<N, L::SY, L::SZ, 2, false>(wk, c, off);
+  constexpr int ST = L::SZ;
+  T u[N], o[N], e[E::CH], d[E::H];
+  pencil_load<T, N, ST>(W2 + c * L::SIZE + off, u);
+  E::split(u, e, d);
+  E::Dt_split(eoD, e, d, o);
+  T a0[N], a1[N];
+  pencil_load<T, N, ST>(A0 + c * L::SIZE + off, a0);
+  pencil_load<T, N, ST>(A1 + c * L::SIZE + off, a1);
+#pragma unroll
+  for (int t = 0; t < N; ++t) o[t] += a0[t] + a1[t];
+  E::split(o, e, d);
+  E::Bt_split(eoB, e, d, u);
+  pencil_store<T, N, ST>(Z + c * L::SIZE + off, u);
+}
+// y: in place
+template <typename T, int N>
+__device__ __forceinline__ void coll_try(T* Z, const T* eoB, int wk) {
+  using L = Lay<N, sizeof(T)>;
+  using E = EO<T, N>;
+  if (wk >= 3 * L::N2) return;
+  int c, off;
+  pencil_decode<N, L::SY, L::SZ, 1, false>(wk, c, off);
+  T* const p = Z + c * L::SIZE + off;
+  T u[N], o[N], e[E::CH], d[E::H];
+  pencil_load<T, N, L::SY>(p, u);
+  E::split(u, e, d);
+  E::Bt_split(eoB, e, d, o);
+  pencil_store<T, N, L::SY>(p, o);
+}
+// x: one element row of one component of the element-local results
+template <typename T, int N, bool JCK>
+__device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx, FastDiv fd_nx, const T* eoB, int wk) {
+  using L = Lay<N, sizeof(T)>;
+  using E = EO<T, N>;
+  if (wk >= 3 * L::N2) return;
+  int c, off;
+  pencil_decode<N, L::SY, L::SZ, 0, JCK>(wk, c, off);
+  T u[N], o[N], e[E::CH], d[E::H];
+  pencil_load<T, N, 1>(Z + c * L::SIZE + off, u);
+  E::split(u, e, d);
+  E::Bt_split(eoB, e, d, o);
+  const int k = off / L::SZ, j = (off - k * L::SZ) / L::SY;
+  T* dst;
+  if constexpr (EMF_LOC_ROWS) {
+    const int64_t row = fd_nx.div((uint32_t)e_);
+    dst = loc + loc_index<N>(row, (int)(e_ - row * nx), nx, k, j, 0, c);
+  } else {
+    dst = loc + (e_ * 3 + c) * L::N3 + (k * N + j) * N;
+  }
+#pragma unroll
+  for (int a = 0; a < N; ++a) dst[a] = o[a];
+}
+template <typename T, int P>
+constexpr bool coll_v2() {
+  return EMF_COLL && P == 4 && TileV2<P, sizeof(T)>::EPB == 1;
+}
+
 // ---- the kernel -------------------------------------------------------------------
 #ifndef EMF_GX_SMEM
 #define EMF_GX_SMEM 1
@@ -691,14 +824,19 @@ struct ApplyV2Smem {
   static constexpr bool kUk = (STRAT == S_NONE || STRAT == S_SCALAR || STRAT == S_SP_NONE || STRAT == S_SP_SCALAR);
   static constexpr int NST = kUk ? 6 : 3;  // staged fields: x (3) [+ u_k (3)]
   static constexpr int SZ = Lay<N, sizeof(T)>::SIZE;
+  static constexpr bool kColl = coll_v2<T, P>();
   T stage[2][EPB][NST][SZ];
   T geo[2][EPB][10];
-  T r1[EPB][9][SZ];
-  T r2[EPB][9][SZ];
+  T r1[kColl ? 1 : EPB][kColl ? 1 : 9][kColl ? 1 : SZ];
+  T r2[kColl ? 1 : EPB][kColl ? 1 : 9][kColl ? 1 : SZ];
   // fp64 Q4 with u_k swept: the x gradient parks in its own arrays until the
   // integrand needs it, instead of 9 registers held across the u_k sweeps
-  static constexpr bool kGx3 = EMF_GX_SMEM && P == 4 && sizeof(T) == 8 && kUk && !(EMF_FUSED64 && CART);
+  static constexpr bool kGx3 = !kColl && EMF_GX_SMEM && P == 4 && sizeof(T) == 8 && kUk && !(EMF_FUSED64 && CART);
   T r3[kGx3 ? EPB : 1][kGx3 ? 9 : 1][kGx3 ? SZ : 1];
+  // collocated sweeps: gradients at the Gauss points, array coll_gi(t, vc);
+  // without u_k three more arrays for the transposed y-derivative
+  T g[kColl ? 3 * NST : 1][kColl ? SZ : 1];
+  T xa[kColl && !kUk ? 3 : 1][kColl && !kUk ? SZ : 1];
 };
 
 // CTAs per SM for the launch bounds.  fp64 keeps 3 CTAs/SM (<= 168 registers)
@@ -807,8 +945,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   __shared__ __align__(16) SM sm;
   const int tid = threadIdx.x;
   const int el = tid / N3, q = tid % N3;
+  constexpr bool kColl = SM::kColl;  // collocated even-odd sweeps (Q4)
   constexpr bool kMap = EMF_Q4MAP && P == 4 && sizeof(T) == 8 && !(EMF_V2_DENSE && EPB == 2) &&
-                        !(SM::kUk && sizeof(T) == 4) && (EMF_Q4MAP_TENSOR || STRAT != S_TENSOR);
+                        !(SM::kUk && sizeof(T) == 4) && (EMF_Q4MAP_TENSOR || STRAT != S_TENSOR || kColl);
   constexpr int kStr = 3 * Lay<N>::N2 <= Lay<N>::N3 ? 3 * Lay<N>::N2 : Lay<N>::N3;
   const unsigned pen = kMap ? c_q4pen.v[tid] : 0u;
   // fp32 Q4 with u_k swept (fused forward sweeps): kQ4Pen32
@@ -818,9 +957,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   // measured: axis-aligned Q4 cNH none 0.132 -> 0.128 ms (24^3), curved cfg2
   // iNH none 2.21 -> 2.55 ms (both gradients and the early J0^-1 loads live
   // through the longer fused sweeps), so axis-aligned meshes only
-  constexpr bool kFused64 = EMF_FUSED64 && kMap && SM::kUk && CART;
+  constexpr bool kFused64 = EMF_FUSED64 && kMap && SM::kUk && CART && !kColl;
+  // the 150-pencil maps also serve the collocated sweeps over x and u_k
+  constexpr bool kMapF64 = kFused64 || (kColl && kMap && SM::kUk);
   unsigned pen32[3] = {0u, 0u, 0u};
-  if constexpr (kFused64) {
+  if constexpr (kMapF64) {
     pen32[0] = c_q4penf64.v[tid][0];
     pen32[1] = c_q4penf64.v[tid][1];
   }
@@ -1062,8 +1203,44 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // fp32: x and u_k swept together (full lanes); fp64 keeps one vector per
     // sweep, whose shorter live ranges fit its 128/168-register budget
     // (measured: fused sweeps cost fp64 none 0.165 -> 0.175 ms, gave fp32 -3%)
-    constexpr bool kFused = kUk && (sizeof(T) == 4 || kFused64) && !kDense;
-    if constexpr (kFused && (kMap32 || kFused64)) {
+    constexpr bool kFused = kUk && (sizeof(T) == 4 || kFused64) && !kDense && !kColl;
+    constexpr bool kJck = sizeof(T) == 8;  // pencil order of the 75-pencil x-sweeps (fw_x / tr_x)
+    constexpr int NVc = kUk ? 2 : 1;
+    T* const G = &sm.g[0][0];
+    if constexpr (kColl) {
+      // ---- interpolate x [and u_k] to the Gauss points in place, then the
+      // collocated derivatives (d/dz from the z pencils' registers)
+      if constexpr (kUk) {
+        constexpr bool kM = kMapF64 || kMap32;
+        const int fx0 = kM ? (int)(pen32[0] & 255u) : q, fx1 = kM ? (int)((pen32[0] >> 8) & 255u) : q + N3;
+        const int fy0 = kM ? (int)((pen32[0] >> 16) & 255u) : q, fy1 = kM ? (int)(pen32[0] >> 24) : q + N3;
+        const int fz0 = kM ? (int)(pen32[1] & 255u) : q, fz1 = kM ? (int)((pen32[1] >> 8) & 255u) : q + N3;
+        coll_interp<T, N, 2, 0, false, false>(S, G, a.eoB, a.eoD, fx0);
+        coll_interp<T, N, 2, 0, false, false>(S, G, a.eoB, a.eoD, fx1);
+        esync();
+        coll_interp<T, N, 2, 1, false, false>(S, G, a.eoB, a.eoD, fy0);
+        coll_interp<T, N, 2, 1, false, false>(S, G, a.eoB, a.eoD, fy1);
+        esync();
+        coll_interp<T, N, 2, 2, false, true>(S, G, a.eoB, a.eoD, fz0);
+        coll_interp<T, N, 2, 2, false, true>(S, G, a.eoB, a.eoD, fz1);
+        esync();
+        coll_deriv<T, N, 2, 0, false>(S, G, a.eoD, fx0);
+        coll_deriv<T, N, 2, 1, false>(S, G, a.eoD, fy0);
+        coll_deriv<T, N, 2, 0, false>(S, G, a.eoD, fx1);
+        coll_deriv<T, N, 2, 1, false>(S, G, a.eoD, fy1);
+        esync();
+      } else {
+        coll_interp<T, N, 1, 0, kJck, false>(S, G, a.eoB, a.eoD, wx);
+        esync();
+        coll_interp<T, N, 1, 1, false, false>(S, G, a.eoB, a.eoD, wy);
+        esync();
+        coll_interp<T, N, 1, 2, false, true>(S, G, a.eoB, a.eoD, wz);
+        esync();
+        coll_deriv<T, N, 1, 0, kJck>(S, G, a.eoD, wx);
+        coll_deriv<T, N, 1, 1, false>(S, G, a.eoD, wy);
+        esync();
+      }
+    } else if constexpr (kFused && (kMap32 || kFused64)) {
       // ---- both vectors per sweep, in place, on the thread's mapped pencil pair
       fwc_x<T, N, 2, N3, true>(S, R2, a.Bm, Dfx, (int)(pen32[0] & 255u), (int)((pen32[0] >> 8) & 255u));
       esync();
@@ -1116,7 +1293,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     }
     if constexpr (kUk) {
       T gk[9], gg[9];
-      if constexpr (kFused) {
+      if constexpr (kColl) {
+#pragma unroll
+        for (int m = 0; m < 9; ++m) gk[m] = G[coll_gi<2>(m % 3, 3 + m / 3) * SZ + qs];
+      } else if constexpr (kFused) {
         grad_at(1, gk);
       } else {
         if constexpr (SM::kGx3) {
@@ -1188,6 +1368,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       else load_tensor_bundle(cb);
     }
     if constexpr (kFused) grad_at(0, gx);
+    if constexpr (kColl) {
+#pragma unroll
+      for (int m = 0; m < 9; ++m) gx[m] = G[coll_gi<NVc>(m % 3, m / 3) * SZ + qs];
+    }
     if constexpr (SM::kGx3) {
 #pragma unroll
       for (int m = 0; m < 9; ++m) gx[m] = sm.r3[el][garr_m<kMap>(m)][qs];
@@ -1215,6 +1399,31 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     } else
       tangent_integrand<T, MODEL>(mq, cb, gx, j0inv, detw, wv);
     // ---- test with the gradients of the basis functions
+    if constexpr (kColl) {
+      // the integrand takes the slots of the last staged vector's gradient
+      // (each thread has read its own point's values)
+      constexpr int v3 = 3 * (NVc - 1);
+#pragma unroll
+      for (int m = 0; m < 9; ++m) G[coll_gi<NVc>(m % 3, v3 + m / 3) * SZ + qs] = wv[m];
+      esync();
+      // A0 = Dc_x^T W0 and A1 = Dc_y^T W1 go to dead arrays: the interpolated
+      // x (and u_k) in the stage; Z takes the slots of the x gradient's d/dx
+      // (with u_k) or of W0 (without), both dead by the z-sweep.  The stage is
+      // last read two barriers before the unit ends (the prefetch of the unit
+      // after next refills it).
+      T* const A0 = S;
+      T* const A1 = kUk ? S + 3 * SZ : &sm.xa[0][0];
+      T* const Z = G;
+      coll_dT<T, N, 0, kJck>(G + coll_gi<NVc>(0, v3) * SZ, A0, a.eoD, wx);
+      coll_dT<T, N, 1, false>(G + coll_gi<NVc>(1, v3) * SZ, A1, a.eoD, wy);
+      esync();
+      coll_trz<T, N>(G + coll_gi<NVc>(2, v3) * SZ, A0, A1, Z, a.eoB, a.eoD, wz);
+      esync();
+      coll_try<T, N>(Z, a.eoB, wy);
+      esync();
+      if (valid) coll_trx<T, N, kJck>(Z, a.loc, e, a.nx, a.fd_nx, a.eoB, wx);
+      return;
+    }
 #pragma unroll
     for (int m = 0; m < 9; ++m) R1[garr_m<kTA>(m) * SZ + qs] = wv[m];
     esync();

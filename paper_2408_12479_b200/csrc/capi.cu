@@ -198,6 +198,23 @@ KArgs<T> kargs(const emfgpu_op* op) {
     a.Dd[t] = L->D[t];
   }
   for (int t = 0; t < n; ++t) a.qwd[t] = L->qwts[t];
+  {
+    // even-odd halves of B and of the collocated derivative Dc[q][r] =
+    // l_r'(g_q) on the Gauss points (D = Dc B, eo_sweeps.cuh)
+    const int H = n / 2, CH = (n + 1) / 2;
+    auto Bq = [&](int q, int i) { return L->B[q * n + i]; };
+    auto Dc = [&](int q, int r) { return L->Dc[q * n + r]; };
+    for (int q = 0; q < CH; ++q)
+      for (int i = 0; i < CH; ++i)
+        a.eoB[q * CH + i] = T(i < H ? 0.5 * (Bq(q, i) + Bq(q, n - 1 - i)) : Bq(q, i));
+    for (int q = 0; q < H; ++q)
+      for (int i = 0; i < H; ++i) a.eoB[CH * CH + q * H + i] = T(0.5 * (Bq(q, i) - Bq(q, n - 1 - i)));
+    for (int q = 0; q < H; ++q)
+      for (int i = 0; i < CH; ++i)
+        a.eoD[q * CH + i] = T(i < H ? 0.5 * (Dc(q, i) + Dc(q, n - 1 - i)) : Dc(q, i));
+    for (int q = 0; q < CH; ++q)
+      for (int i = 0; i < H; ++i) a.eoD[H * CH + q * H + i] = T(0.5 * (Dc(q, i) - Dc(q, n - 1 - i)));
+  }
   a.cartesian = L->cartesian;
   a.hq = static_cast<const T*>(op->d_hq);
   a.hqd = op->d_hqd;
@@ -409,6 +426,9 @@ emfgpu_status emfgpu_level_create(const emfgpu_level_desc* d, emfgpu_level** out
         L->B[q * n + i] = lagrange(L->nodes, i, L->qpts[q]);
         L->D[q * n + i] = dlagrange(L->nodes, i, L->qpts[q]);
       }
+    L->Dc.assign(n * n, 0.0);
+    for (int q = 0; q < n; ++q)
+      for (int r = 0; r < n; ++r) L->Dc[q * n + r] = dlagrange(L->qpts, r, L->qpts[q]);
     // lattice coordinates (mesh.cpp:138-160), then the map
     std::vector<double> coords(3 * L->nnodes);
     if (d->map == EMFGPU_MAP_COORDS) {

@@ -137,6 +137,7 @@ struct emfgpu_level {
   double extent[3] = {1, 1, 1};
   // basis tables (host): GLL nodes, Gauss points/weights, B/D (row = qp)
   std::vector<double> nodes, qpts, qwts, B, D;
+  std::vector<double> Dc;  // collocated derivative on the Gauss points: Dc[q][r] = l_r'(g_q), D = Dc B
   double* d_coords = nullptr;  // 3 per node
   double* d_geo = nullptr;     // SoA, 10 fields: J0^-1 (9), det J0 * w_q (or det J0 if affine)
   float* d_geo_f = nullptr;
