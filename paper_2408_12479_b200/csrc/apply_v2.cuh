@@ -703,7 +703,7 @@ __device__ __forceinline__ void coll_interp(T* S, T* G, const T* eoB, const T* e
   using E = EO<T, N>;
   if (wk >= NV * 3 * L::N2) return;
   int vc, off;
-  pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, vc, off);
+  pencil_decode<N, L::SY, L::SZ, DIR, JCK, 3 * NV>(wk, vc, off);
   constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
   T* const p = S + vc * L::SIZE + off;
   T u[N], o[N], e[E::CH], d[E::H];
@@ -724,7 +724,7 @@ __device__ __forceinline__ void coll_deriv(const T* S, T* G, const T* eoD, int w
   using E = EO<T, N>;
   if (wk >= NV * 3 * L::N2) return;
   int vc, off;
-  pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, vc, off);
+  pencil_decode<N, L::SY, L::SZ, DIR, JCK, 3 * NV>(wk, vc, off);
   constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, ST>(S + vc * L::SIZE + off, u);
@@ -806,12 +806,25 @@ __device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx,
   } else {
     dst = loc + (e_ * 3 + c) * L::N3 + (k * N + j) * N;
   }
+  if constexpr (EMF_LOC_ROWS) {
 #pragma unroll
-  for (int a = 0; a < N; ++a) dst[a] = o[a];
+    for (int a = 0; a < N; ++a) dst[a] = o[a];
+  } else {
+    pencil_store<T, N, 1>(dst, o);
+  }
 }
+// Q4 (one element per CTA, mapped pencils) and Q3 (two elements per CTA on
+// the dense pencil index space)
+#ifndef EMF_COLL_Q3
+#define EMF_COLL_Q3 1
+#endif
+#ifndef EMF_V2_DENSE
+#define EMF_V2_DENSE 1
+#endif
 template <typename T, int P>
 constexpr bool coll_v2() {
-  return EMF_COLL && P == 4 && TileV2<P, sizeof(T)>::EPB == 1;
+  return EMF_COLL && ((P == 4 && TileV2<P, sizeof(T)>::EPB == 1) ||
+                      (EMF_COLL_Q3 && EMF_V2_DENSE && P == 3 && TileV2<P, sizeof(T)>::EPB == 2));
 }
 
 // ---- the kernel -------------------------------------------------------------------
@@ -835,8 +848,8 @@ struct ApplyV2Smem {
   T r3[kGx3 ? EPB : 1][kGx3 ? 9 : 1][kGx3 ? SZ : 1];
   // collocated sweeps: gradients at the Gauss points, array coll_gi(t, vc);
   // without u_k three more arrays for the transposed y-derivative
-  T g[kColl ? 3 * NST : 1][kColl ? SZ : 1];
-  T xa[kColl && !kUk ? 3 : 1][kColl && !kUk ? SZ : 1];
+  alignas(16) T g[kColl ? EPB : 1][kColl ? 3 * NST : 1][kColl ? SZ : 1];
+  alignas(16) T xa[kColl && !kUk ? EPB : 1][kColl && !kUk ? 3 : 1][kColl && !kUk ? SZ : 1];
 };
 
 // CTAs per SM for the launch bounds.  fp64 keeps 3 CTAs/SM (<= 168 registers)
@@ -1206,8 +1219,46 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     constexpr bool kFused = kUk && (sizeof(T) == 4 || kFused64) && !kDense && !kColl;
     constexpr bool kJck = sizeof(T) == 8;  // pencil order of the 75-pencil x-sweeps (fw_x / tr_x)
     constexpr int NVc = kUk ? 2 : 1;
-    T* const G = &sm.g[0][0];
-    if constexpr (kColl) {
+    T* const G = &sm.g[el][0][0];
+    // dense pencil index space of the CTA's EPB elements (Q3): task wp of
+    // NT per element belongs to element wp / NT
+    constexpr int kGS = 3 * SM::NST * SZ, kSS = SM::NST * SZ;
+    T* const S0 = &sm.stage[buf][0][0][0];
+    T* const G0 = &sm.g[0][0][0];
+    auto dense = [&](auto nt, auto&& f) {
+      constexpr int NT = decltype(nt)::value;
+#pragma unroll
+      for (int w0 = 0; w0 < EPB * NT; w0 += EPB * N3) {
+        const int wp = w0 + tid_f;
+        if (wp < EPB * NT) {
+          const int e_l = wp / NT;
+          f(e_l, wp - e_l * NT);
+        }
+      }
+    };
+    constexpr bool kJckD = sizeof(T) == 8;
+    if constexpr (kColl && kDense) {
+      using NTf = std::integral_constant<int, NVc * 3 * N * N>;
+      dense(NTf{}, [&](int e_l, int wk) {
+        coll_interp<T, N, NVc, 0, kJckD, false>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoB, a.eoD, wk);
+      });
+      esync();
+      dense(NTf{}, [&](int e_l, int wk) {
+        coll_interp<T, N, NVc, 1, false, false>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoB, a.eoD, wk);
+      });
+      esync();
+      dense(NTf{}, [&](int e_l, int wk) {
+        coll_interp<T, N, NVc, 2, false, true>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoB, a.eoD, wk);
+      });
+      esync();
+      dense(NTf{}, [&](int e_l, int wk) {
+        coll_deriv<T, N, NVc, 0, kJckD>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoD, wk);
+      });
+      dense(NTf{}, [&](int e_l, int wk) {
+        coll_deriv<T, N, NVc, 1, false>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoD, wk);
+      });
+      esync();
+    } else if constexpr (kColl) {
       // ---- interpolate x [and u_k] to the Gauss points in place, then the
       // collocated derivatives (d/dz from the z pencils' registers)
       if constexpr (kUk) {
@@ -1411,8 +1462,32 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       // (with u_k) or of W0 (without), both dead by the z-sweep.  The stage is
       // last read two barriers before the unit ends (the prefetch of the unit
       // after next refills it).
+      if constexpr (kDense) {
+        using NTb = std::integral_constant<int, 3 * N * N>;
+        T* const X0 = &sm.xa[0][0][0];
+        auto a1_of = [&](int e_l) { return kUk ? S0 + e_l * kSS + 3 * SZ : X0 + e_l * 3 * SZ; };
+        dense(NTb{}, [&](int e_l, int wk) {
+          coll_dT<T, N, 0, kJckD>(G0 + e_l * kGS + coll_gi<NVc>(0, v3) * SZ, S0 + e_l * kSS, a.eoD, wk);
+        });
+        dense(NTb{}, [&](int e_l, int wk) {
+          coll_dT<T, N, 1, false>(G0 + e_l * kGS + coll_gi<NVc>(1, v3) * SZ, a1_of(e_l), a.eoD, wk);
+        });
+        esync();
+        dense(NTb{}, [&](int e_l, int wk) {
+          coll_trz<T, N>(G0 + e_l * kGS + coll_gi<NVc>(2, v3) * SZ, S0 + e_l * kSS, a1_of(e_l), G0 + e_l * kGS, a.eoB,
+                         a.eoD, wk);
+        });
+        esync();
+        dense(NTb{}, [&](int e_l, int wk) { coll_try<T, N>(G0 + e_l * kGS, a.eoB, wk); });
+        esync();
+        const int64_t e0 = e - el;
+        dense(NTb{}, [&](int e_l, int wk) {
+          if (e0 + e_l < a.nel) coll_trx<T, N, kJckD>(G0 + e_l * kGS, a.loc, e0 + e_l, a.nx, a.fd_nx, a.eoB, wk);
+        });
+        return;
+      }
       T* const A0 = S;
-      T* const A1 = kUk ? S + 3 * SZ : &sm.xa[0][0];
+      T* const A1 = kUk ? S + 3 * SZ : &sm.xa[el][0][0];
       T* const Z = G;
       coll_dT<T, N, 0, kJck>(G + coll_gi<NVc>(0, v3) * SZ, A0, a.eoD, wx);
       coll_dT<T, N, 1, false>(G + coll_gi<NVc>(1, v3) * SZ, A1, a.eoD, wy);

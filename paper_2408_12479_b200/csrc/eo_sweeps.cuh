@@ -130,16 +130,16 @@ struct EO {
 // component) and the offset of the pencil's first point inside the array.
 // The decodings are those of fw_x / fw_y / fw_z (apply_v2.cuh), which the
 // thread -> pencil maps (kQ4Pen*, tools/pencil_milp.py) were built for; JCK
-// is the j-c-k order of the fp64 75-pencil x-sweeps.
-template <int N, int SY, int SZ, int DIR, bool JCK>
+// is the j-c-k order of the fp64 x-sweeps (j fastest, then the NA arrays).
+template <int N, int SY, int SZ, int DIR, bool JCK, int NA = 3>
 __device__ __forceinline__ void pencil_decode(int wk, int& vc, int& off) {
   constexpr int N2 = N * N;
   if (DIR == 0) {
     int j, k;
     if (JCK) {
       j = wk % N;
-      vc = (wk / N) % 3;
-      k = wk / (3 * N);
+      vc = (wk / N) % NA;
+      k = wk / (NA * N);
     } else {
       vc = wk / N2;
       const int r = wk % N2;
@@ -156,15 +156,32 @@ __device__ __forceinline__ void pencil_decode(int wk, int& vc, int& off) {
 template <int SY, int SZ, int DIR>
 __host__ __device__ constexpr int pencil_step() { return DIR == 0 ? 1 : DIR == 1 ? SY : SZ; }
 
+// Q3 x-pencils (4 contiguous values, 16-byte aligned in Lay<4>) move as
+// 16-byte words: the j-c-k order then keeps a quarter-warp conflict-free.
 template <typename T, int N, int ST>
 __device__ __forceinline__ void pencil_load(const T* p, T (&u)[N]) {
+  if constexpr (N == 4 && ST == 1 && sizeof(T) == 8) {
+    const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
+    u[0] = a.x, u[1] = a.y, u[2] = b.x, u[3] = b.y;
+  } else if constexpr (N == 4 && ST == 1 && sizeof(T) == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    u[0] = a.x, u[1] = a.y, u[2] = a.z, u[3] = a.w;
+  } else {
 #pragma unroll
-  for (int t = 0; t < N; ++t) u[t] = p[t * ST];
+    for (int t = 0; t < N; ++t) u[t] = p[t * ST];
+  }
 }
 template <typename T, int N, int ST>
 __device__ __forceinline__ void pencil_store(T* p, const T (&o)[N]) {
+  if constexpr (N == 4 && ST == 1 && sizeof(T) == 8) {
+    *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
+    *reinterpret_cast<double2*>(p + 2) = make_double2(o[2], o[3]);
+  } else if constexpr (N == 4 && ST == 1 && sizeof(T) == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  } else {
 #pragma unroll
-  for (int t = 0; t < N; ++t) p[t * ST] = o[t];
+    for (int t = 0; t < N; ++t) p[t * ST] = o[t];
+  }
 }
 
 }  // namespace emfgpu
