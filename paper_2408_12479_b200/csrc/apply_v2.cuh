@@ -886,6 +886,10 @@ constexpr int minb_v2() {
     // 0.0912 -> 0.0871 ms, spatial none 0.1137 -> 0.1076), slower for fibre
     // tensor (0.1178 -> 0.1280) and no better elsewhere
     if (P == 3 && MODEL == CNH && (STRAT == S_TENSOR || STRAT == S_SP_NONE)) return 5;
+    // collocated Q3 sweeps (fewer live values): none / scalar at 5 CTAs/SM
+    // too (cNH axis-aligned none 0.0993 -> 0.0953 ms, scalar 0.0973 -> 0.0952,
+    // curved iNH none 0.1035 -> 0.1014; cachedF slower, 0.0891 -> 0.0911)
+    if (P == 3 && MODEL != FIBER && coll_v2<T, P>() && (STRAT == S_NONE || STRAT == S_SCALAR)) return 5;
     return TileV2<P, 4>::MINB;
   }
   if (EMF_MINB_V2D_FORCE) return EMF_MINB_V2D_FORCE;  // experiments (tools/build_variant.sh)
@@ -895,6 +899,9 @@ constexpr int minb_v2() {
   // 0.1588 ms, tensor 0.1383 -> 0.1281, cachedF 0.1486 -> 0.1444)
   if (P == 3 && MODEL == CNH && CART && (STRAT == S_SCALAR || STRAT == S_TENSOR || STRAT == S_CACHEDF)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
+  // collocated Q3 sweeps: curved iNH none 0.1506 -> 0.1465 ms, cachedF 0.1301 -> 0.1260
+  // (tensor 0.1547 -> 0.2018 and the fibre model stay at 3 / 2)
+  if (P == 3 && MODEL == INH && coll_v2<T, P>() && (STRAT == S_NONE || STRAT == S_CACHEDF)) return 4;
   // Q4 fp64: with the half 1D tables (symtab_on) the cNH / iNH variants fit
   // 128 registers (was 210-250: the 50 table doubles had been pinned in
   // general registers), so 4 CTAs/SM; the fibre model keeps 2 (spill-free at

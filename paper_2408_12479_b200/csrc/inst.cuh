@@ -7,8 +7,11 @@
 #include "apply_v3.cuh"
 #include "internal.h"
 
+// fp32 Q3 none / scalar on axis-aligned meshes ran on the warp-per-element v3
+// until the dense v2 got the collocated sweeps (cNH none 0.1096 -> 0.0953 ms,
+// profiles/r02_q3_collocated_ab.txt); v3 now serves Q2 only.
 #ifndef EMF_F32_V3CART
-#define EMF_F32_V3CART 1
+#define EMF_F32_V3CART 0
 #endif
 #ifndef EMF_V3_ENABLE
 #define EMF_V3_ENABLE 1
@@ -23,8 +26,7 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   const int64_t cnt = e1 - e0;
   if (cnt <= 0) return;
   // Kernel choice measured on B200 (tools/apply_ab.py; profiles/r01_e2e_findings.md):
-  // the warp-per-element v3 for Q2 (fp32, and fp64 tensor / cachedF) and for
-  // fp32 Q3 none / scalar on axis-aligned meshes in the material domain; the
+  // the warp-per-element v3 for Q2 (fp32, and fp64 tensor / cachedF); the
   // dense v2 everywhere else (after the ticket loop and the dense Q3 mapping it
   // beat v3 for Q3 tensor / cachedF in both precisions: fp32 curved iNH tensor
   // 0.169 -> 0.114 ms, fibre 0.169 -> 0.120; fp64 iNH tensor 0.214 -> 0.163,
