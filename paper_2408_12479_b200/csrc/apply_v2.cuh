@@ -41,6 +41,9 @@
 #ifndef EMF_MINB_F32Q3
 #define EMF_MINB_F32Q3 0  // fp32 Q3 CTAs/SM override (experiments)
 #endif
+#ifndef EMF_F32Q4_OCC
+#define EMF_F32Q4_OCC 1  // the per-strategy fp32 Q4 CTAs/SM below
+#endif
 #ifndef EMF_MINB_F32Q4
 #define EMF_MINB_F32Q4 0  // fp32 Q4 CTAs/SM override (experiments)
 #endif
@@ -698,7 +701,7 @@ __host__ __device__ constexpr int coll_gi(int t, int vc) { return 3 * NV * t + v
 // Interpolation along DIR, in place; WITHD (the last direction): also the
 // collocated derivative along DIR of the interpolated pencil, into G.
 template <typename T, int N, int NV, int DIR, bool JCK, bool WITHD>
-__device__ __forceinline__ void coll_interp(T* S, T* G, const T* eoB, const T* eoD, int wk) {
+__device__ __forceinline__ void coll_interp(T* S, T* G, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
   if (wk >= NV * 3 * L::N2) return;
@@ -709,17 +712,17 @@ __device__ __forceinline__ void coll_interp(T* S, T* G, const T* eoB, const T* e
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, ST>(p, u);
   E::split(u, e, d);
-  E::B_split(eoB, e, d, o);
+  E::B_split(t, e, d, o);
   pencil_store<T, N, ST>(p, o);
   if (WITHD) {
     E::split(o, e, d);
-    E::D_split(eoD, e, d, u);
+    E::D_split(t, e, d, u);
     pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, vc) * L::SIZE + off, u);
   }
 }
 // Collocated derivative along DIR of the interpolated arrays: S -> G.
 template <typename T, int N, int NV, int DIR, bool JCK>
-__device__ __forceinline__ void coll_deriv(const T* S, T* G, const T* eoD, int wk) {
+__device__ __forceinline__ void coll_deriv(const T* S, T* G, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
   if (wk >= NV * 3 * L::N2) return;
@@ -729,13 +732,13 @@ __device__ __forceinline__ void coll_deriv(const T* S, T* G, const T* eoD, int w
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, ST>(S + vc * L::SIZE + off, u);
   E::split(u, e, d);
-  E::D_split(eoD, e, d, o);
+  E::D_split(t, e, d, o);
   pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, vc) * L::SIZE + off, o);
 }
 // Transposed derivative along DIR of the integrand's column DIR (W = its
 // three component arrays): A[c] = Dc^T W[c].
 template <typename T, int N, int DIR, bool JCK>
-__device__ __forceinline__ void coll_dT(const T* W, T* A, const T* eoD, int wk) {
+__device__ __forceinline__ void coll_dT(const T* W, T* A, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
   if (wk >= 3 * L::N2) return;
@@ -745,13 +748,12 @@ __device__ __forceinline__ void coll_dT(const T* W, T* A, const T* eoD, int wk) 
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, ST>(W + c * L::SIZE + off, u);
   E::split(u, e, d);
-  E::Dt_split(eoD, e, d, o);
+  E::Dt_split(t, e, d, o);
   pencil_store<T, N, ST>(A + c * L::SIZE + off, o);
 }
 // z: Z[c] = Bz^T (A0[c] + A1[c] + Dc_z^T W2[c])
 template <typename T, int N>
-__device__ __forceinline__ void coll_trz(const T* W2, const T* A0, const T* A1, T* Z, const T* eoB, const T* eoD,
-                                         int wk) {
+__device__ __forceinline__ void coll_trz(const T* W2, const T* A0, const T* A1, T* Z, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
   if (wk >= 3 * L::N2) return;
@@ -761,19 +763,19 @@ __device__ __forceinline__ void coll_trz(const T* W2, const T* A0, const T* A1, 
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, ST>(W2 + c * L::SIZE + off, u);
   E::split(u, e, d);
-  E::Dt_split(eoD, e, d, o);
+  E::Dt_split(t, e, d, o);
   T a0[N], a1[N];
   pencil_load<T, N, ST>(A0 + c * L::SIZE + off, a0);
   pencil_load<T, N, ST>(A1 + c * L::SIZE + off, a1);
 #pragma unroll
   for (int t = 0; t < N; ++t) o[t] += a0[t] + a1[t];
   E::split(o, e, d);
-  E::Bt_split(eoB, e, d, u);
+  E::Bt_split(t, e, d, u);
   pencil_store<T, N, ST>(Z + c * L::SIZE + off, u);
 }
 // y: in place
 template <typename T, int N>
-__device__ __forceinline__ void coll_try(T* Z, const T* eoB, int wk) {
+__device__ __forceinline__ void coll_try(T* Z, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
   if (wk >= 3 * L::N2) return;
@@ -783,12 +785,12 @@ __device__ __forceinline__ void coll_try(T* Z, const T* eoB, int wk) {
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, L::SY>(p, u);
   E::split(u, e, d);
-  E::Bt_split(eoB, e, d, o);
+  E::Bt_split(t, e, d, o);
   pencil_store<T, N, L::SY>(p, o);
 }
 // x: one element row of one component of the element-local results
 template <typename T, int N, bool JCK>
-__device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx, FastDiv fd_nx, const T* eoB, int wk) {
+__device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx, FastDiv fd_nx, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
   if (wk >= 3 * L::N2) return;
@@ -797,7 +799,7 @@ __device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx,
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, 1>(Z + c * L::SIZE + off, u);
   E::split(u, e, d);
-  E::Bt_split(eoB, e, d, o);
+  E::Bt_split(t, e, d, o);
   const int k = off / L::SZ, j = (off - k * L::SZ) / L::SY;
   T* dst;
   if constexpr (EMF_LOC_ROWS) {
@@ -881,10 +883,27 @@ template <typename T, int P, int MODEL, int STRAT, bool CART>
 constexpr int minb_v2() {
   if (sizeof(T) == 4) {
     if (P == 4 && EMF_MINB_F32Q4) return EMF_MINB_F32Q4;
+    // fp32 Q4 on the collocated sweeps is bound by latency and barriers at 4
+    // CTAs/SM (16 warps); more resident CTAs pay even with some spilling
+    // (cfg2 element phase, profiles/r02_fp32_q4_occupancy.txt: none 1.363 ->
+    // 1.211 ms at 6, cachedF 1.278 -> 1.033 at 6, tensor 1.402 -> 1.154 at 7,
+    // scalar 1.364 -> 1.276 at 5)
+    if (P == 4 && EMF_F32Q4_OCC && coll_v2<T, P>() && MODEL != FIBER) {
+      if (STRAT == S_NONE || STRAT == S_CACHEDF) return 6;
+      if (STRAT == S_TENSOR) return 7;
+      if (STRAT == S_SCALAR) return 5;
+    }
     if (P == 3 && EMF_MINB_F32Q3) return EMF_MINB_F32Q3;
     // 5 CTAs/SM measured faster for these cNH fp32 Q3 variants (tensor
     // 0.0912 -> 0.0871 ms, spatial none 0.1137 -> 0.1076), slower for fibre
     // tensor (0.1178 -> 0.1280) and no better elsewhere
+    // collocated Q3 sweeps, cNH (profiles/r02_fp32_q3_occupancy.txt): cachedF
+    // 0.0891 -> 0.0830 ms and tensor 0.0850 -> 0.0810 at 7 CTAs/SM, none /
+    // scalar 0.0953 -> 0.0932 at 6; curved iNH loses beyond 5
+    if (P == 3 && MODEL == CNH && coll_v2<T, P>()) {
+      if (STRAT == S_TENSOR || STRAT == S_CACHEDF) return 7;
+      if (STRAT == S_NONE || STRAT == S_SCALAR) return 6;
+    }
     if (P == 3 && MODEL == CNH && (STRAT == S_TENSOR || STRAT == S_SP_NONE)) return 5;
     // collocated Q3 sweeps (fewer live values): none / scalar at 5 CTAs/SM
     // too (cNH axis-aligned none 0.0993 -> 0.0953 ms, scalar 0.0973 -> 0.0952,
@@ -963,6 +982,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   constexpr bool kUk = SM::kUk;
   constexpr int SZ = Lay<N, sizeof(T)>::SIZE;
   __shared__ __align__(16) SM sm;
+  const EoT<T> eot{a.eoB, a.eoD, a.eoP};
   const int tid = threadIdx.x;
   const int el = tid / N3, q = tid % N3;
   constexpr bool kColl = SM::kColl;  // collocated even-odd sweeps (Q4)
@@ -1247,22 +1267,22 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     if constexpr (kColl && kDense) {
       using NTf = std::integral_constant<int, NVc * 3 * N * N>;
       dense(NTf{}, [&](int e_l, int wk) {
-        coll_interp<T, N, NVc, 0, kJckD, false>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoB, a.eoD, wk);
+        coll_interp<T, N, NVc, 0, kJckD, false>(S0 + e_l * kSS, G0 + e_l * kGS, eot, wk);
       });
       esync();
       dense(NTf{}, [&](int e_l, int wk) {
-        coll_interp<T, N, NVc, 1, false, false>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoB, a.eoD, wk);
+        coll_interp<T, N, NVc, 1, false, false>(S0 + e_l * kSS, G0 + e_l * kGS, eot, wk);
       });
       esync();
       dense(NTf{}, [&](int e_l, int wk) {
-        coll_interp<T, N, NVc, 2, false, true>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoB, a.eoD, wk);
+        coll_interp<T, N, NVc, 2, false, true>(S0 + e_l * kSS, G0 + e_l * kGS, eot, wk);
       });
       esync();
       dense(NTf{}, [&](int e_l, int wk) {
-        coll_deriv<T, N, NVc, 0, kJckD>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoD, wk);
+        coll_deriv<T, N, NVc, 0, kJckD>(S0 + e_l * kSS, G0 + e_l * kGS, eot, wk);
       });
       dense(NTf{}, [&](int e_l, int wk) {
-        coll_deriv<T, N, NVc, 1, false>(S0 + e_l * kSS, G0 + e_l * kGS, a.eoD, wk);
+        coll_deriv<T, N, NVc, 1, false>(S0 + e_l * kSS, G0 + e_l * kGS, eot, wk);
       });
       esync();
     } else if constexpr (kColl) {
@@ -1273,29 +1293,29 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
         const int fx0 = kM ? (int)(pen32[0] & 255u) : q, fx1 = kM ? (int)((pen32[0] >> 8) & 255u) : q + N3;
         const int fy0 = kM ? (int)((pen32[0] >> 16) & 255u) : q, fy1 = kM ? (int)(pen32[0] >> 24) : q + N3;
         const int fz0 = kM ? (int)(pen32[1] & 255u) : q, fz1 = kM ? (int)((pen32[1] >> 8) & 255u) : q + N3;
-        coll_interp<T, N, 2, 0, false, false>(S, G, a.eoB, a.eoD, fx0);
-        coll_interp<T, N, 2, 0, false, false>(S, G, a.eoB, a.eoD, fx1);
+        coll_interp<T, N, 2, 0, false, false>(S, G, eot, fx0);
+        coll_interp<T, N, 2, 0, false, false>(S, G, eot, fx1);
         esync();
-        coll_interp<T, N, 2, 1, false, false>(S, G, a.eoB, a.eoD, fy0);
-        coll_interp<T, N, 2, 1, false, false>(S, G, a.eoB, a.eoD, fy1);
+        coll_interp<T, N, 2, 1, false, false>(S, G, eot, fy0);
+        coll_interp<T, N, 2, 1, false, false>(S, G, eot, fy1);
         esync();
-        coll_interp<T, N, 2, 2, false, true>(S, G, a.eoB, a.eoD, fz0);
-        coll_interp<T, N, 2, 2, false, true>(S, G, a.eoB, a.eoD, fz1);
+        coll_interp<T, N, 2, 2, false, true>(S, G, eot, fz0);
+        coll_interp<T, N, 2, 2, false, true>(S, G, eot, fz1);
         esync();
-        coll_deriv<T, N, 2, 0, false>(S, G, a.eoD, fx0);
-        coll_deriv<T, N, 2, 1, false>(S, G, a.eoD, fy0);
-        coll_deriv<T, N, 2, 0, false>(S, G, a.eoD, fx1);
-        coll_deriv<T, N, 2, 1, false>(S, G, a.eoD, fy1);
+        coll_deriv<T, N, 2, 0, false>(S, G, eot, fx0);
+        coll_deriv<T, N, 2, 1, false>(S, G, eot, fy0);
+        coll_deriv<T, N, 2, 0, false>(S, G, eot, fx1);
+        coll_deriv<T, N, 2, 1, false>(S, G, eot, fy1);
         esync();
       } else {
-        coll_interp<T, N, 1, 0, kJck, false>(S, G, a.eoB, a.eoD, wx);
+        coll_interp<T, N, 1, 0, kJck, false>(S, G, eot, wx);
         esync();
-        coll_interp<T, N, 1, 1, false, false>(S, G, a.eoB, a.eoD, wy);
+        coll_interp<T, N, 1, 1, false, false>(S, G, eot, wy);
         esync();
-        coll_interp<T, N, 1, 2, false, true>(S, G, a.eoB, a.eoD, wz);
+        coll_interp<T, N, 1, 2, false, true>(S, G, eot, wz);
         esync();
-        coll_deriv<T, N, 1, 0, kJck>(S, G, a.eoD, wx);
-        coll_deriv<T, N, 1, 1, false>(S, G, a.eoD, wy);
+        coll_deriv<T, N, 1, 0, kJck>(S, G, eot, wx);
+        coll_deriv<T, N, 1, 1, false>(S, G, eot, wy);
         esync();
       }
     } else if constexpr (kFused && (kMap32 || kFused64)) {
@@ -1474,36 +1494,36 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
         T* const X0 = &sm.xa[0][0][0];
         auto a1_of = [&](int e_l) { return kUk ? S0 + e_l * kSS + 3 * SZ : X0 + e_l * 3 * SZ; };
         dense(NTb{}, [&](int e_l, int wk) {
-          coll_dT<T, N, 0, kJckD>(G0 + e_l * kGS + coll_gi<NVc>(0, v3) * SZ, S0 + e_l * kSS, a.eoD, wk);
+          coll_dT<T, N, 0, kJckD>(G0 + e_l * kGS + coll_gi<NVc>(0, v3) * SZ, S0 + e_l * kSS, eot, wk);
         });
         dense(NTb{}, [&](int e_l, int wk) {
-          coll_dT<T, N, 1, false>(G0 + e_l * kGS + coll_gi<NVc>(1, v3) * SZ, a1_of(e_l), a.eoD, wk);
+          coll_dT<T, N, 1, false>(G0 + e_l * kGS + coll_gi<NVc>(1, v3) * SZ, a1_of(e_l), eot, wk);
         });
         esync();
         dense(NTb{}, [&](int e_l, int wk) {
-          coll_trz<T, N>(G0 + e_l * kGS + coll_gi<NVc>(2, v3) * SZ, S0 + e_l * kSS, a1_of(e_l), G0 + e_l * kGS, a.eoB,
-                         a.eoD, wk);
+          coll_trz<T, N>(G0 + e_l * kGS + coll_gi<NVc>(2, v3) * SZ, S0 + e_l * kSS, a1_of(e_l), G0 + e_l * kGS, eot,
+                         wk);
         });
         esync();
-        dense(NTb{}, [&](int e_l, int wk) { coll_try<T, N>(G0 + e_l * kGS, a.eoB, wk); });
+        dense(NTb{}, [&](int e_l, int wk) { coll_try<T, N>(G0 + e_l * kGS, eot, wk); });
         esync();
         const int64_t e0 = e - el;
         dense(NTb{}, [&](int e_l, int wk) {
-          if (e0 + e_l < a.nel) coll_trx<T, N, kJckD>(G0 + e_l * kGS, a.loc, e0 + e_l, a.nx, a.fd_nx, a.eoB, wk);
+          if (e0 + e_l < a.nel) coll_trx<T, N, kJckD>(G0 + e_l * kGS, a.loc, e0 + e_l, a.nx, a.fd_nx, eot, wk);
         });
         return;
       }
       T* const A0 = S;
       T* const A1 = kUk ? S + 3 * SZ : &sm.xa[el][0][0];
       T* const Z = G;
-      coll_dT<T, N, 0, kJck>(G + coll_gi<NVc>(0, v3) * SZ, A0, a.eoD, wx);
-      coll_dT<T, N, 1, false>(G + coll_gi<NVc>(1, v3) * SZ, A1, a.eoD, wy);
+      coll_dT<T, N, 0, kJck>(G + coll_gi<NVc>(0, v3) * SZ, A0, eot, wx);
+      coll_dT<T, N, 1, false>(G + coll_gi<NVc>(1, v3) * SZ, A1, eot, wy);
       esync();
-      coll_trz<T, N>(G + coll_gi<NVc>(2, v3) * SZ, A0, A1, Z, a.eoB, a.eoD, wz);
+      coll_trz<T, N>(G + coll_gi<NVc>(2, v3) * SZ, A0, A1, Z, eot, wz);
       esync();
-      coll_try<T, N>(Z, a.eoB, wy);
+      coll_try<T, N>(Z, eot, wy);
       esync();
-      if (valid) coll_trx<T, N, kJck>(Z, a.loc, e, a.nx, a.fd_nx, a.eoB, wx);
+      if (valid) coll_trx<T, N, kJck>(Z, a.loc, e, a.nx, a.fd_nx, eot, wx);
       return;
     }
 #pragma unroll

@@ -214,6 +214,26 @@ KArgs<T> kargs(const emfgpu_op* op) {
         a.eoD[q * CH + i] = T(i < H ? 0.5 * (Dc(q, i) + Dc(q, n - 1 - i)) : Dc(q, i));
     for (int q = 0; q < CH; ++q)
       for (int i = 0; i < H; ++i) a.eoD[H * CH + q * H + i] = T(0.5 * (Dc(q, i) - Dc(q, n - 1 - i)));
+    // pairs of the same entries for the packed fp32 sweeps (EoT in eo_sweeps.cuh; H == 2: Q3, Q4)
+    for (auto& v : a.eoP) v = make_float2(0.f, 0.f);
+    if (H == 2) {
+      auto BE = [&](int q, int i) { return (float)a.eoB[q * CH + i]; };
+      auto BO = [&](int q, int i) { return (float)a.eoB[CH * CH + q * H + i]; };
+      auto DE = [&](int q, int i) { return (float)a.eoD[q * CH + i]; };
+      auto DO = [&](int q, int i) { return (float)a.eoD[H * CH + q * H + i]; };
+      for (int i = 0; i < CH; ++i) {
+        a.eoP[0 + i] = make_float2(BE(0, i), BE(1, i));
+        a.eoP[5 + i] = make_float2(DE(0, i), DE(1, i));
+        a.eoP[10 + i] = make_float2(BE(i, 0), BE(i, 1));
+        a.eoP[15 + i] = make_float2(DO(i, 0), DO(i, 1));
+      }
+      for (int i = 0; i < H; ++i) {
+        a.eoP[3 + i] = make_float2(BO(0, i), BO(1, i));
+        a.eoP[8 + i] = make_float2(DO(0, i), DO(1, i));
+        a.eoP[13 + i] = make_float2(BO(i, 0), BO(i, 1));
+        a.eoP[18 + i] = make_float2(DE(i, 0), DE(i, 1));
+      }
+    }
   }
   a.cartesian = L->cartesian;
   a.hq = static_cast<const T*>(op->d_hq);
@@ -1460,8 +1480,18 @@ template <typename T>
 void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
   const int nl = (int)m->lv.size();
   CK(cudaMemcpyAsync(m->u[0], d_u, sizeof(double) * m->lv[0]->ndofs, cudaMemcpyDeviceToDevice, s));
+  // EMFGPU_TRACE=1: per-level stage times of the setup (synchronising; diagnostics only)
+  static const bool trace = std::getenv("EMFGPU_TRACE") != nullptr;
+  auto now = [&]() {
+    if (trace) cudaStreamSynchronize(s);
+    return std::chrono::steady_clock::now();
+  };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
   for (int l = 0; l < nl; ++l) {
     emfgpu_op* op = m->ops[l];
+    const auto t0 = now();
     if (l > 0) {
       transfer_run<double>(m->tr[l - 1], 2, m->u[l - 1], m->u[l], s);
       mask0<double>(m->lv[l], m->u[l], s);  // dirichlet_set_values (zero)
@@ -1470,10 +1500,17 @@ void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
     int64_t be = -1;
     int bq = -1;
     linearize_impl(op, &be, &bq, s);
+    const auto t1 = now();
     int64_t nbad = 0;
     diagonal_impl(op, m->diag[l], &nbad, s);
+    const auto t2 = now();
     double lmin = 0, lmax = 0;
     lanczos<T>(op, static_cast<const T*>(m->diag[l]), m->cfg.eig_iterations, m->cfg.seed, &lmin, &lmax, s);
+    if (trace) {
+      const auto t3 = now();
+      std::fprintf(stderr, "[emfgpu] mg level %d (%lld dofs): linearize %.2f ms, diagonal %.2f ms, lanczos %.2f ms\n", l,
+                   (long long)m->lv[l]->ndofs, ms(t0, t1), ms(t1, t2), ms(t2, t3));
+    }
     if (l + 1 < nl) {
       if (m->cheb[l]) emfgpu_cheb_destroy(m->cheb[l]);
       m->cheb[l] = nullptr;
@@ -1481,7 +1518,9 @@ void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
                              &m->cheb[l]) != EMFGPU_OK)
         throw ApiError(EMFGPU_ERR_CUDA, "mg: smoother setup failed");
     } else if (m->dense) {
+      const auto t4 = now();
       dense_coarse<T>(m, l, s);
+      if (trace) std::fprintf(stderr, "[emfgpu] mg dense coarse setup %.2f ms\n", ms(t4, now()));
     } else {
       launch_inv<T>(static_cast<const T*>(m->diag[l]), static_cast<T*>(m->cg_inv), m->lv[l]->ndofs, s);
     }

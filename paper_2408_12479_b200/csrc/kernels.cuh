@@ -138,6 +138,7 @@ struct KArgs {
   T Bm[25], Dm[25];    // 1D tables, row = quadrature point (P <= 4)
   double Bd[25], Dd[25];
   T eoB[13], eoD[12];  // even-odd halves of B and of the collocated derivative Dc (eo_sweeps.cuh)
+  float2 eoP[20];      // the same entries as pairs for the packed f32x2 sweeps (EoT, eo_sweeps.cuh)
   double qwd[9];  // 1D Gauss weights (affine geometry stores det J0 without them)
   FastDiv fd_nx, fd_nxy;
   // optional per-qp fibre frame field (fibre model): 18 SoA fields H4 (6),
