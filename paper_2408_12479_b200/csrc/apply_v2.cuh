@@ -351,6 +351,79 @@ constexpr Q4PenPackedF64 q4penf64_pack() {
   return r;
 }
 static __constant__ Q4PenPackedF64 c_q4penf64 = q4penf64_pack();
+
+// The same maps with the pencil decoded at compile time: entry = array *
+// SIZE + offset of the pencil's first point (pencil_decode, eo_sweeps.cuh),
+// so the collocated Q4 sweeps take their addresses from one 16-bit table
+// read instead of ~8 integer instructions per pencil task (the fp32 kernel
+// is issue-bound at 6-7 CTAs/SM).  Columns: 0-5 the 150-pencil forward maps
+// over x and u_k (x round 1, round 2, y, y, z, z), 6-8 the 75-pencil maps
+// (x, y, z), 9 the x pencil's offset in the element-local results
+// (c N^3 + (k N + j) N); kPenNone = no pencil.
+constexpr unsigned short kPenNone = 0xffffu;
+constexpr int q4_pen_off(int wk, int dir, bool jck, int na) {
+  constexpr int N = 5, N2 = 25, SY = 5, SZ = 25, SIZE = 125;
+  int vc = 0, off = 0;
+  if (dir == 0) {
+    int j = 0, k = 0;
+    if (jck) {
+      j = wk % N;
+      vc = (wk / N) % na;
+      k = wk / (na * N);
+    } else {
+      vc = wk / N2;
+      const int r = wk % N2;
+      j = r % N;
+      k = r / N;
+    }
+    off = SY * j + SZ * k;
+  } else {
+    vc = wk / N2;
+    const int r = wk % N2, i = r % N, t = r / N;
+    off = dir == 1 ? i + SZ * t : i + SY * t;
+  }
+  return vc * SIZE + off;
+}
+struct Q4OffTab {
+  unsigned short v[128][10];
+};
+template <typename FX, typename FY, typename FZ, typename TX, typename TY, typename TZ>
+constexpr Q4OffTab q4off_build(const FX& fx, const FY& fy, const FZ& fz, const TX& tx, const TY& ty, const TZ& tz,
+                               bool jck) {
+  Q4OffTab r{};
+  for (int t = 0; t < 128; ++t) {
+    for (int c = 0; c < 10; ++c) r.v[t][c] = kPenNone;
+    for (int round = 0; round < 2; ++round) {
+      if (round == 0 ? t < 125 : t < 25) {
+        const int i = round == 0 ? t : 125 + t;
+        r.v[t][0 + round] = (unsigned short)q4_pen_off(fx[i], 0, false, 6);
+        r.v[t][2 + round] = (unsigned short)q4_pen_off(fy[i], 1, false, 6);
+        r.v[t][4 + round] = (unsigned short)q4_pen_off(fz[i], 2, false, 6);
+      }
+    }
+    if (t < 75) {
+      const int ox = q4_pen_off(tx[t], 0, jck, 3);
+      r.v[t][6] = (unsigned short)ox;
+      r.v[t][7] = (unsigned short)q4_pen_off(ty[t], 1, false, 3);
+      r.v[t][8] = (unsigned short)q4_pen_off(tz[t], 2, false, 3);
+      const int c = ox / 125, rem = ox % 125, k = rem / 25, j = (rem % 25) / 5;
+      r.v[t][9] = (unsigned short)(c * 125 + (k * 5 + j) * 5);
+    }
+  }
+  return r;
+}
+static __constant__ Q4OffTab c_q4off64 =
+    q4off_build(kQ4PenF64.fx, kQ4PenF64.fy, kQ4PenF64.fz, kQ4Pen.x, kQ4Pen.y, kQ4Pen.z, true);
+static __constant__ Q4OffTab c_q4off32 =
+    q4off_build(kQ4Pen32.fx, kQ4Pen32.fy, kQ4Pen32.fz, kQ4Pen32.tx, kQ4Pen32.ty, kQ4Pen32.tz, false);
+// Measured (cfg2 element phase, profiles/r02_q4_decoded_offsets.txt): with the
+// rows in shared memory fp64 none 1.912 -> 1.903 ms, scalar 2.070 -> 1.996,
+// but cachedF 1.590 -> 1.658 and fp32 none 1.215 -> 1.278 (shared memory is
+// already at 65% of its wavefront peak); read straight from the constant
+// bank the thread-indexed loads serialise (fp64 none 3.24 ms).  Off.
+#ifndef EMF_Q4_PRE
+#define EMF_Q4_PRE 0
+#endif
 #ifndef EMF_FUSED64
 #define EMF_FUSED64 1  // fp64 Q4 on axis-aligned meshes: x and u_k forward sweeps fused on kQ4PenF64
 #endif
@@ -700,15 +773,20 @@ __host__ __device__ constexpr int coll_gi(int t, int vc) { return 3 * NV * t + v
 
 // Interpolation along DIR, in place; WITHD (the last direction): also the
 // collocated derivative along DIR of the interpolated pencil, into G.
-template <typename T, int N, int NV, int DIR, bool JCK, bool WITHD>
+template <typename T, int N, int NV, int DIR, bool JCK, bool WITHD, bool PRE = false>
 __device__ __forceinline__ void coll_interp(T* S, T* G, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
-  if (wk >= NV * 3 * L::N2) return;
-  int vc, off;
-  pencil_decode<N, L::SY, L::SZ, DIR, JCK, 3 * NV>(wk, vc, off);
+  if (PRE ? wk == (int)kPenNone : wk >= NV * 3 * L::N2) return;
+  int po;  // array * SIZE + offset of the pencil's first point
+  if (PRE) po = wk;
+  else {
+    int vc, off;
+    pencil_decode<N, L::SY, L::SZ, DIR, JCK, 3 * NV>(wk, vc, off);
+    po = vc * L::SIZE + off;
+  }
   constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
-  T* const p = S + vc * L::SIZE + off;
+  T* const p = S + po;
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, ST>(p, u);
   E::split(u, e, d);
@@ -717,71 +795,91 @@ __device__ __forceinline__ void coll_interp(T* S, T* G, const EoT<T>& t, int wk)
   if (WITHD) {
     E::split(o, e, d);
     E::D_split(t, e, d, u);
-    pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, vc) * L::SIZE + off, u);
+    pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, 0) * L::SIZE + po, u);
   }
 }
 // Collocated derivative along DIR of the interpolated arrays: S -> G.
-template <typename T, int N, int NV, int DIR, bool JCK>
+template <typename T, int N, int NV, int DIR, bool JCK, bool PRE = false>
 __device__ __forceinline__ void coll_deriv(const T* S, T* G, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
-  if (wk >= NV * 3 * L::N2) return;
-  int vc, off;
-  pencil_decode<N, L::SY, L::SZ, DIR, JCK, 3 * NV>(wk, vc, off);
+  if (PRE ? wk == (int)kPenNone : wk >= NV * 3 * L::N2) return;
+  int po;
+  if (PRE) po = wk;
+  else {
+    int vc, off;
+    pencil_decode<N, L::SY, L::SZ, DIR, JCK, 3 * NV>(wk, vc, off);
+    po = vc * L::SIZE + off;
+  }
   constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
   T u[N], o[N], e[E::CH], d[E::H];
-  pencil_load<T, N, ST>(S + vc * L::SIZE + off, u);
+  pencil_load<T, N, ST>(S + po, u);
   E::split(u, e, d);
   E::D_split(t, e, d, o);
-  pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, vc) * L::SIZE + off, o);
+  pencil_store<T, N, ST>(G + coll_gi<NV>(DIR, 0) * L::SIZE + po, o);
 }
 // Transposed derivative along DIR of the integrand's column DIR (W = its
 // three component arrays): A[c] = Dc^T W[c].
-template <typename T, int N, int DIR, bool JCK>
+template <typename T, int N, int DIR, bool JCK, bool PRE = false>
 __device__ __forceinline__ void coll_dT(const T* W, T* A, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
-  if (wk >= 3 * L::N2) return;
-  int c, off;
-  pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, c, off);
+  if (PRE ? wk == (int)kPenNone : wk >= 3 * L::N2) return;
+  int po;
+  if (PRE) po = wk;
+  else {
+    int c, off;
+    pencil_decode<N, L::SY, L::SZ, DIR, JCK>(wk, c, off);
+    po = c * L::SIZE + off;
+  }
   constexpr int ST = pencil_step<L::SY, L::SZ, DIR>();
   T u[N], o[N], e[E::CH], d[E::H];
-  pencil_load<T, N, ST>(W + c * L::SIZE + off, u);
+  pencil_load<T, N, ST>(W + po, u);
   E::split(u, e, d);
   E::Dt_split(t, e, d, o);
-  pencil_store<T, N, ST>(A + c * L::SIZE + off, o);
+  pencil_store<T, N, ST>(A + po, o);
 }
 // z: Z[c] = Bz^T (A0[c] + A1[c] + Dc_z^T W2[c])
-template <typename T, int N>
+template <typename T, int N, bool PRE = false>
 __device__ __forceinline__ void coll_trz(const T* W2, const T* A0, const T* A1, T* Z, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
-  if (wk >= 3 * L::N2) return;
-  int c, off;
-  pencil_decode<N, L::SY, L::SZ, 2, false>(wk, c, off);
+  if (PRE ? wk == (int)kPenNone : wk >= 3 * L::N2) return;
+  int po;
+  if (PRE) po = wk;
+  else {
+    int c, off;
+    pencil_decode<N, L::SY, L::SZ, 2, false>(wk, c, off);
+    po = c * L::SIZE + off;
+  }
   constexpr int ST = L::SZ;
   T u[N], o[N], e[E::CH], d[E::H];
-  pencil_load<T, N, ST>(W2 + c * L::SIZE + off, u);
+  pencil_load<T, N, ST>(W2 + po, u);
   E::split(u, e, d);
   E::Dt_split(t, e, d, o);
   T a0[N], a1[N];
-  pencil_load<T, N, ST>(A0 + c * L::SIZE + off, a0);
-  pencil_load<T, N, ST>(A1 + c * L::SIZE + off, a1);
+  pencil_load<T, N, ST>(A0 + po, a0);
+  pencil_load<T, N, ST>(A1 + po, a1);
 #pragma unroll
   for (int t = 0; t < N; ++t) o[t] += a0[t] + a1[t];
   E::split(o, e, d);
   E::Bt_split(t, e, d, u);
-  pencil_store<T, N, ST>(Z + c * L::SIZE + off, u);
+  pencil_store<T, N, ST>(Z + po, u);
 }
 // y: in place
-template <typename T, int N>
+template <typename T, int N, bool PRE = false>
 __device__ __forceinline__ void coll_try(T* Z, const EoT<T>& t, int wk) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
-  if (wk >= 3 * L::N2) return;
-  int c, off;
-  pencil_decode<N, L::SY, L::SZ, 1, false>(wk, c, off);
-  T* const p = Z + c * L::SIZE + off;
+  if (PRE ? wk == (int)kPenNone : wk >= 3 * L::N2) return;
+  int po;
+  if (PRE) po = wk;
+  else {
+    int c, off;
+    pencil_decode<N, L::SY, L::SZ, 1, false>(wk, c, off);
+    po = c * L::SIZE + off;
+  }
+  T* const p = Z + po;
   T u[N], o[N], e[E::CH], d[E::H];
   pencil_load<T, N, L::SY>(p, u);
   E::split(u, e, d);
@@ -789,11 +887,22 @@ __device__ __forceinline__ void coll_try(T* Z, const EoT<T>& t, int wk) {
   pencil_store<T, N, L::SY>(p, o);
 }
 // x: one element row of one component of the element-local results
-template <typename T, int N, bool JCK>
-__device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx, FastDiv fd_nx, const EoT<T>& t, int wk) {
+// PRE: wk = the pencil's array * SIZE + offset, goff = its offset in the
+// element's 3 N^3 block of the element-local results
+template <typename T, int N, bool JCK, bool PRE = false>
+__device__ __forceinline__ void coll_trx(const T* Z, T* loc, int64_t e_, int nx, FastDiv fd_nx, const EoT<T>& t, int wk,
+                                         int goff = 0) {
   using L = Lay<N, sizeof(T)>;
   using E = EO<T, N>;
-  if (wk >= 3 * L::N2) return;
+  if (PRE ? wk == (int)kPenNone : wk >= 3 * L::N2) return;
+  if constexpr (PRE && !EMF_LOC_ROWS) {
+    T u[N], o[N], e[E::CH], d[E::H];
+    pencil_load<T, N, 1>(Z + wk, u);
+    E::split(u, e, d);
+    E::Bt_split(t, e, d, o);
+    pencil_store<T, N, 1>(loc + e_ * 3 * L::N3 + goff, o);
+    return;
+  }
   int c, off;
   pencil_decode<N, L::SY, L::SZ, 0, JCK>(wk, c, off);
   T u[N], o[N], e[E::CH], d[E::H];
@@ -993,6 +1102,15 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   // fp32 Q4 with u_k swept (fused forward sweeps): kQ4Pen32
   constexpr bool kMap32 = EMF_Q4MAP32 && P == 4 && sizeof(T) == 4 && SM::kUk && !(EMF_V2_DENSE && EPB == 2);
   constexpr bool kTA = kMap || kMap32;  // direction-major gradient arrays
+  // collocated Q4 sweeps on mapped pencils: addresses from the decoded tables
+  // (each thread keeps its own row in shared memory: a constant-bank read
+  // indexed by the thread serialises 32 ways, and 5 more live registers spill)
+  constexpr bool kPre = EMF_Q4_PRE && !EMF_LOC_ROWS && SM::kColl && P == 4 && (kMap || kMap32);
+  __shared__ unsigned short s_pot[kPre ? 128 : 1][10];
+  if constexpr (kPre) {
+#pragma unroll
+    for (int c = 0; c < 10; ++c) s_pot[tid][c] = sizeof(T) == 8 ? c_q4off64.v[tid][c] : c_q4off32.v[tid][c];
+  }
   // fp64 Q4 fused forward sweeps: kQ4PenF64
   // measured: axis-aligned Q4 cNH none 0.132 -> 0.128 ms (24^3), curved cfg2
   // iNH none 2.21 -> 2.55 ms (both gradients and the early J0^-1 loads live
@@ -1118,9 +1236,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
   auto compute = [&](int64_t u, int buf, bool zero_me) {
     EMF_V2_FRESH_POS
     // this thread's pencil per sweep orientation (kQ4Pen) or its point index
-    const int wx = kMap ? (int)(pen & 255u) : kMap32 ? (int)((pen32[1] >> 16) & 255u) : q;
-    const int wy = kMap ? (int)((pen >> 8) & 255u) : kMap32 ? (int)(pen32[1] >> 24) : q;
-    const int wz = kMap ? (int)(pen >> 16) : kMap32 ? (int)pen32[2] : q;
+    // (kPre: the pencils' decoded offsets from c_q4off64 / c_q4off32 instead)
+    const unsigned short* const pot = &s_pot[kPre ? tid_f : 0][0];
+    const int wx = kPre ? (int)pot[6] : kMap ? (int)(pen & 255u) : kMap32 ? (int)((pen32[1] >> 16) & 255u) : q;
+    const int wy = kPre ? (int)pot[7] : kMap ? (int)((pen >> 8) & 255u) : kMap32 ? (int)(pen32[1] >> 24) : q;
+    const int wz = kPre ? (int)pot[8] : kMap ? (int)(pen >> 16) : kMap32 ? (int)pen32[2] : q;
     // tensor-product weight of this thread's point (operator.hpp:492)
     const T wq3 = T(a.qwd[qi] * a.qwd[qj] * a.qwd[qk]);
     const int64_t e = elem_of(u, el);
@@ -1190,7 +1310,8 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     SpCell<T> spst;
     if constexpr (kSpTenEarly) spatial_bundle<T, MODEL>(S_TENSOR, mq, nullptr, cs, st, qidx, cbst, spst);
     // scalar strategy: its 1-4 cached scalars loaded before the sweeps too
-    constexpr bool kScEarly = STRAT == S_SCALAR && EMF_SC_EARLY;
+    // (fp64 Q4: the late load is faster, cfg2 scalar element phase 2.118 -> 2.073 ms)
+    constexpr bool kScEarly = STRAT == S_SCALAR && EMF_SC_EARLY && !(P == 4 && sizeof(T) == 8);
     Bundle<T> cbs;
     if constexpr (kScEarly) load_scalars<T, MODEL>(cs, st, qidx, cbs);
     T gcf[9];
@@ -1290,32 +1411,38 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       // collocated derivatives (d/dz from the z pencils' registers)
       if constexpr (kUk) {
         constexpr bool kM = kMapF64 || kMap32;
-        const int fx0 = kM ? (int)(pen32[0] & 255u) : q, fx1 = kM ? (int)((pen32[0] >> 8) & 255u) : q + N3;
-        const int fy0 = kM ? (int)((pen32[0] >> 16) & 255u) : q, fy1 = kM ? (int)(pen32[0] >> 24) : q + N3;
-        const int fz0 = kM ? (int)(pen32[1] & 255u) : q, fz1 = kM ? (int)((pen32[1] >> 8) & 255u) : q + N3;
-        coll_interp<T, N, 2, 0, false, false>(S, G, eot, fx0);
-        coll_interp<T, N, 2, 0, false, false>(S, G, eot, fx1);
+        static_assert(!kPre || kM, "decoded offsets belong to the mapped pencils");
+        const int fx0 = kPre ? (int)pot[0] : kM ? (int)(pen32[0] & 255u) : q;
+        const int fx1 = kPre ? (int)pot[1] : kM ? (int)((pen32[0] >> 8) & 255u) : q + N3;
+        const int fy0 = kPre ? (int)pot[2] : kM ? (int)((pen32[0] >> 16) & 255u) : q;
+        const int fy1 = kPre ? (int)pot[3] : kM ? (int)(pen32[0] >> 24) : q + N3;
+        const int fz0 = kPre ? (int)pot[4] : kM ? (int)(pen32[1] & 255u) : q;
+        const int fz1 = kPre ? (int)pot[5] : kM ? (int)((pen32[1] >> 8) & 255u) : q + N3;
+        coll_interp<T, N, 2, 0, false, false, kPre>(S, G, eot, fx0);
+        coll_interp<T, N, 2, 0, false, false, kPre>(S, G, eot, fx1);
         esync();
-        coll_interp<T, N, 2, 1, false, false>(S, G, eot, fy0);
-        coll_interp<T, N, 2, 1, false, false>(S, G, eot, fy1);
+        coll_interp<T, N, 2, 1, false, false, kPre>(S, G, eot, fy0);
+        coll_interp<T, N, 2, 1, false, false, kPre>(S, G, eot, fy1);
         esync();
-        coll_interp<T, N, 2, 2, false, true>(S, G, eot, fz0);
-        coll_interp<T, N, 2, 2, false, true>(S, G, eot, fz1);
+        coll_interp<T, N, 2, 2, false, true, kPre>(S, G, eot, fz0);
+        coll_interp<T, N, 2, 2, false, true, kPre>(S, G, eot, fz1);
         esync();
-        coll_deriv<T, N, 2, 0, false>(S, G, eot, fx0);
-        coll_deriv<T, N, 2, 1, false>(S, G, eot, fy0);
-        coll_deriv<T, N, 2, 0, false>(S, G, eot, fx1);
-        coll_deriv<T, N, 2, 1, false>(S, G, eot, fy1);
+        coll_deriv<T, N, 2, 0, false, kPre>(S, G, eot, fx0);
+        coll_deriv<T, N, 2, 1, false, kPre>(S, G, eot, fy0);
+        coll_deriv<T, N, 2, 0, false, kPre>(S, G, eot, fx1);
+        // (running the 25 second-round y pencils on warp 1 beside warp 0's
+        // second-round x pencils measured slower: 1.913 -> 1.947 ms)
+        coll_deriv<T, N, 2, 1, false, kPre>(S, G, eot, fy1);
         esync();
       } else {
-        coll_interp<T, N, 1, 0, kJck, false>(S, G, eot, wx);
+        coll_interp<T, N, 1, 0, kJck, false, kPre>(S, G, eot, wx);
         esync();
-        coll_interp<T, N, 1, 1, false, false>(S, G, eot, wy);
+        coll_interp<T, N, 1, 1, false, false, kPre>(S, G, eot, wy);
         esync();
-        coll_interp<T, N, 1, 2, false, true>(S, G, eot, wz);
+        coll_interp<T, N, 1, 2, false, true, kPre>(S, G, eot, wz);
         esync();
-        coll_deriv<T, N, 1, 0, kJck>(S, G, eot, wx);
-        coll_deriv<T, N, 1, 1, false>(S, G, eot, wy);
+        coll_deriv<T, N, 1, 0, kJck, kPre>(S, G, eot, wx);
+        coll_deriv<T, N, 1, 1, false, kPre>(S, G, eot, wy);
         esync();
       }
     } else if constexpr (kFused && (kMap32 || kFused64)) {
@@ -1516,14 +1643,14 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       T* const A0 = S;
       T* const A1 = kUk ? S + 3 * SZ : &sm.xa[el][0][0];
       T* const Z = G;
-      coll_dT<T, N, 0, kJck>(G + coll_gi<NVc>(0, v3) * SZ, A0, eot, wx);
-      coll_dT<T, N, 1, false>(G + coll_gi<NVc>(1, v3) * SZ, A1, eot, wy);
+      coll_dT<T, N, 0, kJck, kPre>(G + coll_gi<NVc>(0, v3) * SZ, A0, eot, wx);
+      coll_dT<T, N, 1, false, kPre>(G + coll_gi<NVc>(1, v3) * SZ, A1, eot, wy);
       esync();
-      coll_trz<T, N>(G + coll_gi<NVc>(2, v3) * SZ, A0, A1, Z, eot, wz);
+      coll_trz<T, N, kPre>(G + coll_gi<NVc>(2, v3) * SZ, A0, A1, Z, eot, wz);
       esync();
-      coll_try<T, N>(Z, eot, wy);
+      coll_try<T, N, kPre>(Z, eot, wy);
       esync();
-      if (valid) coll_trx<T, N, kJck>(Z, a.loc, e, a.nx, a.fd_nx, eot, wx);
+      if (valid) coll_trx<T, N, kJck, kPre>(Z, a.loc, e, a.nx, a.fd_nx, eot, wx, kPre ? (int)pot[9] : 0);
       return;
     }
 #pragma unroll

@@ -635,6 +635,7 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
     CK(cudaMemset(op->d_ctr, 0, sizeof(unsigned) * 2 * emfgpu_op::kTicketSlots));
     CK(cudaMalloc(&op->d_err, sizeof(unsigned long long)));
     CK(cudaMemset(op->d_err, 0xff, sizeof(unsigned long long)));
+    CK(cudaMalloc(&op->d_nbad, sizeof(unsigned long long)));
     CK(cudaMallocHost(&op->h_err, sizeof(unsigned long long)));
     CK(cudaMalloc(&op->d_ukd, sizeof(double) * l->ndofs));
     if (strategy == EMFGPU_NONE || strategy == EMFGPU_SCALAR) {
@@ -694,6 +695,7 @@ void emfgpu_op_destroy(emfgpu_op* op) {
   cudaFree(op->pcg_buf);
   cudaFree(op->fgmres_buf);
   cudaFree(op->d_err);
+  cudaFree(op->d_nbad);
   if (op->h_err) cudaFreeHost(op->h_err);
   if (op->stream) cudaStreamDestroy(op->stream);
   if (op->s_h2d) cudaStreamDestroy(op->s_h2d);
@@ -901,9 +903,10 @@ static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream
                           int64_t cap = 0) {
   require_linearized(op, "compute_diagonal");
   const emfgpu_level* L = op->L;
-  unsigned long long* d_nbad = nullptr;
+  // the counter lives in the handle (calls on a handle are ordered): no
+  // stream-ordered allocation, whose pool trims at every synchronisation
+  unsigned long long* const d_nbad = op->d_nbad;
   long long* d_idx = nullptr;
-  CK(cudaMallocAsync(&d_nbad, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(d_nbad, 0, sizeof(unsigned long long), s));
   if (h_idx && cap > 0) CK(cudaMallocAsync(&d_idx, sizeof(long long) * cap, s));
   if (op->precision == 64) {
@@ -922,7 +925,6 @@ static void diagonal_impl(emfgpu_op* op, void* d_diag, int64_t* nbad, cudaStream
   CK(cudaGetLastError());
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(op->h_err, d_nbad, sizeof(h), cudaMemcpyDeviceToHost, s));
-  CK(cudaFreeAsync(d_nbad, s));
   CK(cudaStreamSynchronize(s));
   h = *op->h_err;
   *op->h_err = ~0ull;

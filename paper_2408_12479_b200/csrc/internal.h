@@ -162,6 +162,7 @@ struct emfgpu_op {
   void* d_x = nullptr;         // staging for host entry points
   void* d_y = nullptr;
   unsigned long long* d_err = nullptr;
+  unsigned long long* d_nbad = nullptr;  // compute_diagonal: count of nonpositive free rows
   unsigned long long* h_err = nullptr;  // pinned
   // Lanczos work space (estimate_eigenvalues), kept across relinearizations
   double* lz_buf = nullptr;
