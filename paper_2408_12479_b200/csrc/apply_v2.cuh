@@ -420,7 +420,9 @@ static __constant__ Q4OffTab c_q4off32 =
 // rows in shared memory fp64 none 1.912 -> 1.903 ms, scalar 2.070 -> 1.996,
 // but cachedF 1.590 -> 1.658 and fp32 none 1.215 -> 1.278 (shared memory is
 // already at 65% of its wavefront peak); read straight from the constant
-// bank the thread-indexed loads serialise (fp64 none 3.24 ms).  Off.
+// bank the thread-indexed loads serialise (fp64 none 3.24 ms); packed into 5
+// registers per thread (fp32 only, which has them to spare) fp32 none 1.213 ->
+// 1.304 ms.  Off.
 #ifndef EMF_Q4_PRE
 #define EMF_Q4_PRE 0
 #endif
