@@ -1000,7 +1000,7 @@ constexpr int minb_v2() {
     // 1.211 ms at 6, cachedF 1.278 -> 1.033 at 6, tensor 1.402 -> 1.154 at 7,
     // scalar 1.364 -> 1.276 at 5)
     if (P == 4 && EMF_F32Q4_OCC && coll_v2<T, P>() && MODEL != FIBER) {
-      if (STRAT == S_NONE || STRAT == S_CACHEDF) return 6;
+      if (STRAT == S_NONE || STRAT == S_CACHEDF || is_resid(STRAT)) return 6;
       if (STRAT == S_TENSOR) return 7;
       if (STRAT == S_SCALAR) return 5;
     }
@@ -1201,7 +1201,8 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     const bool uk_el = kUkEl && a.uk_el != nullptr;
     if (es < a.nel) {
       const ElemPos ep = elem_pos_fast<P>(es, a, si, sj, sk);
-      zero = node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
+      // the residual takes u with its Dirichlet values (no column masking)
+      zero = !is_resid(STRAT) && node_constrained(ep.ga, ep.gb, ep.gc, a.mx, a.my, a.mz, a.faces);
 #pragma unroll
       for (int c = 0; c < 3; ++c) cp_async_T(&sm.stage[b][sel][c][sqs], a.x + 3 * ep.node + c);
       if constexpr (kUk) {
@@ -1570,7 +1571,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       cache_scalars<T, MODEL>(mq, cb);
       second_pk<T, MODEL>(mq, cb);
       }
-    } else {  // S_TENSOR
+    } else if constexpr (STRAT == S_TENSOR) {
       if constexpr (kTenEarly) cb = cbe;
       else load_tensor_bundle(cb);
     }
@@ -1584,7 +1585,13 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       for (int m = 0; m < 9; ++m) gx[m] = sm.r3[el][garr_m<kMap>(m)][qs];
     }
     T wv[9];
-    if constexpr (kPush) {
+    if constexpr (is_resid(STRAT)) {
+      if constexpr (CART) {  // the full J0^-1 from its diagonal
+        j0inv[1] = j0inv[2] = j0inv[3] = j0inv[5] = j0inv[6] = j0inv[7] = T(0);
+      }
+      if (!resid_integrand<T, MODEL, STRAT == S_RESID_SP>(mq, gx, j0inv, detw, wq3, wv) && valid)
+        atomicMin(a.err, (unsigned long long)qidx);
+    } else if constexpr (kPush) {
       push_integrand<T, MODEL>(ps, gx, wv);
     } else if constexpr (is_spatial(STRAT)) {
       T jtinv[9];

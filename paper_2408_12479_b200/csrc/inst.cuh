@@ -34,7 +34,8 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   constexpr bool kTC = STRAT == S_CACHEDF || STRAT == S_TENSOR;
   constexpr bool kF32V3 = EMF_F32_V3CART && sizeof(EMF_T) == 4 && CART && !is_spatial(STRAT) &&
                           (STRAT == S_NONE || STRAT == S_SCALAR);
-  constexpr bool kV3 = EMF_V3_ENABLE && (EMF_P == 2 ? (sizeof(EMF_T) == 4 || kTC) : (EMF_P == 3 && kF32V3));
+  constexpr bool kV3 = EMF_V3_ENABLE && !is_resid(STRAT) &&
+                       (EMF_P == 2 ? (sizeof(EMF_T) == 4 || kTC) : (EMF_P == 3 && kF32V3));
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)
     constexpr size_t smem = sizeof(ApplyV3Warp<EMF_T, EMF_P, MODEL, STRAT>) * kV3Warps;
@@ -110,8 +111,24 @@ void launch_diagonal<EMF_T, EMF_P>(int model, const KArgs<EMF_T>& a, cudaStream_
   if (model == FIBER) diagonal_kernel<EMF_T, EMF_P, FIBER><<<blocks, EPB * N * N * N, 0, s>>>(b);
 }
 
+// evaluate_residual's element phase: the persistent v2 element kernel with the
+// stress integrand (EMF_RESID_V2 = 0: the round-1 thread-per-point kernel)
+#ifndef EMF_RESID_V2
+#define EMF_RESID_V2 1
+#endif
 template <>
 void launch_residual<EMF_T, EMF_P>(int model, const KArgs<EMF_T>& a, cudaStream_t s) {
+  if (EMF_RESID_V2) {
+#define EMF_RCASE(M)                                                                       \
+  if (model == M) {                                                                        \
+    if (a.spatial) return apply_one<M, S_RESID_SP, false>(a, 0, a.nel, s);                 \
+    if (a.cartesian) return apply_one<M, S_RESID, true>(a, 0, a.nel, s);                   \
+    return apply_one<M, S_RESID, false>(a, 0, a.nel, s);                                   \
+  }
+    EMF_RCASE(CNH) EMF_RCASE(INH) EMF_RCASE(FIBER)
+#undef EMF_RCASE
+    return;
+  }
   constexpr int N = EMF_P + 1, EPB = Tile<EMF_P>::EPB;
   KArgs<EMF_T> b = a;
   b.e_begin = 0;

@@ -707,6 +707,49 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
 
 namespace emfgpu {
 
+// Residual integrand at one point (element_residual_batch, operator.hpp:550-590):
+// gref = Grad_xi u, full J0^-1, detw = det J0 w_q, wq3 = w_q.  Material domain:
+// w = detw F S J0^-T; spatial: w = (1/J) det J_t w_q tau J_t^-T with J_t = J0 +
+// Grad_xi u.  Returns false when det(F) <= 0.
+template <typename T, int MODEL, bool SPATIAL>
+__device__ __forceinline__ bool resid_integrand(const MatConst<T>& mq, const T* gref, const T* j0inv, T detw, T wq3,
+                                                T* w) {
+  T g[9];
+  mm(gref, j0inv, g);
+  Bundle<T> cb;
+  const bool ok = make_strain(g, cb);
+  cache_scalars<T, MODEL>(mq, cb);  // lnJ (cNH), J^-2/3, fibre invariants (operator.hpp:557-566)
+  if constexpr (SPATIAL) {
+    // J0 recovered from the stored J0^-1 (operator.hpp:572-588)
+    T j0[9], jt[9], jtinv[9], bt[6], tf[9];
+    inverse3(j0inv, j0);
+#pragma unroll
+    for (int m = 0; m < 9; ++m) jt[m] = j0[m] + gref[m];
+    inverse3(jt, jtinv);
+    const T detjt = det3(jt);
+    const T invj = T(1) / (T(1) + cb.jm1);
+    green_euler(g, bt);
+    SpCell<T> sp;
+    spatial_cell<T, MODEL>(mq, cb, bt, sp);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tf[3 * r + c] = sp.tau[sidx(r, c)];
+    mm_bt(tf, jtinv, w);
+    const T sc = (invj * detjt) * wq3;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) w[m] *= sc;
+  } else {
+    second_pk<T, MODEL>(mq, cb);
+    T fs[9];
+    mm_ts(cb.F, cb.S, fs);  // w_mat = F S (operator.hpp:568)
+    mm_bt(fs, j0inv, w);
+#pragma unroll
+    for (int m = 0; m < 9; ++m) w[m] *= detw;
+  }
+  return ok;
+}
+
 // ---- residual kernel: r_e = (Grad_xi test, det J0 w_q F S J0^-T) -----------
 // element_residual_batch, operator.hpp:532-595 (material domain), thread per
 // qp, shared-memory sweeps.  Not the hot path: one launch per Newton step.
@@ -735,40 +778,11 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   T j0inv[9], detw;
   load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
   const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
-  T g[9], w[9], out[3];
-  mm(gref, j0inv, g);
-  Bundle<T> cb;
-  if (!make_strain(g, cb) && valid) atomicMin(a.err, (unsigned long long)qidx);
-  cache_scalars<T, MODEL>(mq, cb);  // lnJ (cNH), J^-2/3, fibre invariants (operator.hpp:557-566)
-  if (a.spatial) {
-    // J_t = J0 + Grad_xi u, w = (1/J) det J_t w_q tau J_t^-T (operator.hpp:572-588);
-    // J0 recovered from the stored J0^-1
-    T j0[9], jt[9], jtinv[9], bt[6], tf[9];
-    inverse3(j0inv, j0);
-#pragma unroll
-    for (int m = 0; m < 9; ++m) jt[m] = j0[m] + gref[m];
-    inverse3(jt, jtinv);
-    const T detjt = det3(jt);
-    const T invj = T(1) / (T(1) + cb.jm1);
-    green_euler(g, bt);
-    SpCell<T> sp;
-    spatial_cell<T, MODEL>(mq, cb, bt, sp);
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) tf[3 * r + c] = sp.tau[sidx(r, c)];
-    mm_bt(tf, jtinv, w);
-    const T sc = (invj * detjt) * T(a.qwd[i] * a.qwd[j] * a.qwd[k]);
-#pragma unroll
-    for (int m = 0; m < 9; ++m) w[m] *= sc;
-  } else {
-    second_pk<T, MODEL>(mq, cb);
-    T fs[9];
-    mm_ts(cb.F, cb.S, fs);  // w_mat = F S (operator.hpp:568)
-    mm_bt(fs, j0inv, w);
-#pragma unroll
-    for (int m = 0; m < 9; ++m) w[m] *= detw;
-  }
+  T w[9], out[3];
+  const T wq3 = T(a.qwd[i] * a.qwd[j] * a.qwd[k]);
+  const bool ok = a.spatial ? resid_integrand<T, MODEL, true>(mq, gref, j0inv, detw, wq3, w)
+                            : resid_integrand<T, MODEL, false>(mq, gref, j0inv, detw, wq3, w);
+  if (!ok && valid) atomicMin(a.err, (unsigned long long)qidx);
   sf_transpose<T, N>(bufA[el], bufB[el], sB, sD, i, j, k, w, out);
   if (valid) {
     int64_t o = e * 3 * N3 + q;

@@ -25,7 +25,12 @@ enum Model : int { CNH = 0, INH = 1, FIBER = 2 };
 enum Strategy : int { S_NONE = 0, S_SCALAR = 1, S_TENSOR = 2, S_CACHEDF = 3 };
 // element-kernel strategy codes of the spatial (Omega_t) formulation
 enum SpatialStrategy : int { S_SP_NONE = 4, S_SP_SCALAR = 5, S_SP_TENSOR = 6 };
-__host__ __device__ constexpr bool is_spatial(int strat) { return strat >= S_SP_NONE; }
+__host__ __device__ constexpr bool is_spatial(int strat) { return strat >= S_SP_NONE && strat <= S_SP_TENSOR; }
+// element-kernel code of evaluate_residual (operator.hpp:532-595): the same
+// gather / sweeps / element-local results as an apply of strategy tensor,
+// with the stress integrand of the input displacement at the points
+constexpr int S_RESID = 7, S_RESID_SP = 8;  // material / spatial domain
+__host__ __device__ constexpr bool is_resid(int strat) { return strat == S_RESID || strat == S_RESID_SP; }
 
 // Material constants in the operator's number type, rounded from double the
 // way the reference does (N(scalar_of<N>(p.x)), e.g. constitutive.hpp:200).
