@@ -1259,8 +1259,11 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // per-qp geometry / cache loads are issued before the sweeps
     const int64_t qidx = (valid ? e : a.e_begin) * N3 + q;
     const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, qidx);
+    // tensor with the cached push-forward state: K and the coefficients carry
+    // the geometry, nothing else is read per point
+    constexpr bool kTenPush = STRAT == S_TENSOR && tensor_compact(MODEL, 0);
     T j0inv[9], detw;
-    if ((!is_spatial(STRAT) || kUk) && !CART && !a.affine) {
+    if ((!is_spatial(STRAT) || kUk) && !CART && !a.affine && !kTenPush) {
 #pragma unroll
       for (int m = 0; m < 9; ++m) j0inv[m] = a.geo[m * a.geo_stride + qidx];
       detw = a.geo[9 * a.geo_stride + qidx];
@@ -1306,7 +1309,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       }
     };
     Bundle<T> cbe;
-    if constexpr (kTenEarly) load_tensor_bundle(cbe);
+    PushState<T> pse;
+    if constexpr (kTenEarly && kTenPush) load_push_state<T>(cs, st, qidx, pse);
+    else if constexpr (kTenEarly) load_tensor_bundle(cbe);
     // spatial tensor: the cached spatial bundle loaded before the sweeps
     constexpr bool kSpTenEarly = STRAT == S_SP_TENSOR && EMF_SPT_EARLY;
     Bundle<T> cbst;
@@ -1571,6 +1576,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       cache_scalars<T, MODEL>(mq, cb);
       second_pk<T, MODEL>(mq, cb);
       }
+    } else if constexpr (kTenPush) {
+      if constexpr (kTenEarly) ps = pse;
+      else load_push_state<T>(cs, st, qidx, ps);
     } else if constexpr (STRAT == S_TENSOR) {
       if constexpr (kTenEarly) cb = cbe;
       else load_tensor_bundle(cb);
@@ -1591,7 +1599,7 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       }
       if (!resid_integrand<T, MODEL, STRAT == S_RESID_SP>(mq, gx, j0inv, detw, wq3, wv) && valid)
         atomicMin(a.err, (unsigned long long)qidx);
-    } else if constexpr (kPush) {
+    } else if constexpr (kPush || kTenPush) {
       push_integrand<T, MODEL>(ps, gx, wv);
     } else if constexpr (is_spatial(STRAT)) {
       T jtinv[9];

@@ -34,7 +34,9 @@ static void apply_one(const KArgs<EMF_T>& a, int64_t e0, int64_t e1, cudaStream_
   constexpr bool kTC = STRAT == S_CACHEDF || STRAT == S_TENSOR;
   constexpr bool kF32V3 = EMF_F32_V3CART && sizeof(EMF_T) == 4 && CART && !is_spatial(STRAT) &&
                           (STRAT == S_NONE || STRAT == S_SCALAR);
-  constexpr bool kV3 = EMF_V3_ENABLE && !is_resid(STRAT) &&
+  // (v3 reads the material tensor bundle; the cNH / iNH tensor cache holds the
+  // push-forward state, which only v2 consumes -- v2 and v3 measured equal at Q2)
+  constexpr bool kV3 = EMF_V3_ENABLE && !is_resid(STRAT) && !(STRAT == S_TENSOR && tensor_compact(MODEL, 0)) &&
                        (EMF_P == 2 ? (sizeof(EMF_T) == 4 || kTC) : (EMF_P == 3 && kF32V3));
   if constexpr (kV3) {
     // warp-per-element kernel (apply_v3.cuh)

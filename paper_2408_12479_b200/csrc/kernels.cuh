@@ -42,12 +42,24 @@ enum CacheSlot : int {
   C_LNJ = 0, C_JP = 1, C_C1 = 2, C_C2 = 3, C_C3 = 4, C_EF = 6,
   // tensor: then F, Finv, S, Cinv
   C_F = 8, C_FINV = 17, C_S = 26, C_CINV = 32, C_NT = 38,
+  // tensor, cNH / iNH in the material domain: the push-forward state instead
+  // (qp.cuh PushState: K = J0^-1 F^-1 (9), b (6), 4 coefficients with det J0 w
+  // folded in) -- 19 fields and no geometry read in the apply, against 33 + 10
+  C_PK = 0, C_PB = 9, C_PC = 15, C_NTP = 19,
   // cachedF: displacement gradient G = F - I
   C_G = 0, C_NG = 9,
   // spatial formulation (operator.hpp:139-143): scalars as above, then 1/J,
   // J_t (9; all strategies), tau, b, F H4 F^T, F H6 F^T (tensor)
   C_INVJ = 8, C_JT = 9, C_TAU = 18, C_B = 24, C_FH = 30, C_NSP = 42
 };
+
+#ifndef EMF_TENSOR_PUSH
+#define EMF_TENSOR_PUSH 1
+#endif
+// Does strategy tensor cache the push-forward state for this (model, domain)?
+__host__ __device__ constexpr bool tensor_compact(int model, int spatial) {
+  return EMF_TENSOR_PUSH && model != 2 /* FIBER */ && !spatial;
+}
 
 // n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method,
 // Hacker's Delight 10-9): q = (umulhi(n, m) + n) >> l.
@@ -493,6 +505,13 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     for (int m = 0; m < 9; ++m) a.cache[(C_JT + m) * st + qidx] = T(jt[m]);
   }
   if (a.strategy == S_CACHEDF || a.strategy == S_NONE) return;
+  if (a.strategy == S_TENSOR && tensor_compact(MODEL, 0) && !a.spatial) {
+    // the linearization state in its push-forward form, computed in double
+    PushState<double> ps;
+    push_state<double, MODEL, false, false>(md, g, j0inv, detw, cb, ps);
+    store_push_state<T>(a.cache, st, qidx, ps);
+    return;
+  }
   // stored scalars, computed in double (operator.hpp:720-735)
   cache_scalars<double, MODEL>(md, cb);
   if (MODEL == CNH) {
@@ -566,6 +585,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
   const T* cs = a.cache;
   const MatConst<T> mq = mat_at<T, MODEL>(a.mat, a.hq, a.hq_stride, ix);
   Bundle<T> cb;
+  PushState<T> ps;
   T j0inv[9], detw;
   load_geo(a, a.geo, valid, e, qidx, i, j, k, j0inv, detw);
   SpCell<T> sp;
@@ -597,6 +617,8 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     for (int m = 0; m < 9; ++m) g[m] = cs[(C_G + m) * st + ix];
     make_strain(g, cb);
     cache_scalars<T, MODEL>(mq, cb);
+  } else if (tensor_compact(MODEL, 0)) {
+    load_push_state<T>(cs, st, ix, ps);
   } else {
 #pragma unroll
     for (int m = 0; m < 9; ++m) {
@@ -609,7 +631,8 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
       cb.Cinv[m] = cs[(C_CINV + m) * st + ix];
     }
   }
-  if (!a.spatial) {
+  const bool compact = !a.spatial && a.strategy == S_TENSOR && tensor_compact(MODEL, 0);
+  if (!a.spatial && !compact) {
     if (a.strategy == S_SCALAR || a.strategy == S_TENSOR) load_scalars<T, MODEL>(cs, st, ix, cb);
     if (a.strategy != S_TENSOR) second_pk<T, MODEL>(mq, cb);
   }
@@ -628,6 +651,8 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
       gref[3 * c + dp] = T(1);
       if (a.spatial)
         spatial_integrand<T, MODEL>(mq, cb, sp, gref, jtinv, ssc, w);
+      else if (compact)
+        push_integrand<T, MODEL>(ps, gref, w);
       else
         tangent_integrand<T, MODEL>(mq, cb, gref, j0inv, detw, w);
 #pragma unroll

@@ -527,6 +527,31 @@ __device__ __forceinline__ bool push_state(const MatConst<T>& m, const T* gg, co
   return true;
 }
 
+// The state as 19 cache fields (kernels.cuh: C_PK, C_PB, C_PC), computed in
+// TS and stored / loaded as T.
+template <typename T, typename TS>
+__device__ __forceinline__ void store_push_state(T* cache, int64_t st, int64_t qidx, const PushState<TS>& ps) {
+#pragma unroll
+  for (int m = 0; m < 9; ++m) cache[(0 + m) * st + qidx] = T(ps.K[m]);
+#pragma unroll
+  for (int m = 0; m < 6; ++m) cache[(9 + m) * st + qidx] = T(ps.b[m]);
+  cache[15 * st + qidx] = T(ps.k_lb);
+  cache[16 * st + qidx] = T(ps.k_lt);
+  cache[17 * st + qidx] = T(ps.k_tr);
+  cache[18 * st + qidx] = T(ps.k_t);
+}
+template <typename T>
+__device__ __forceinline__ void load_push_state(const T* cs, int64_t st, int64_t qidx, PushState<T>& ps) {
+#pragma unroll
+  for (int m = 0; m < 9; ++m) ps.K[m] = cs[(0 + m) * st + qidx];
+#pragma unroll
+  for (int m = 0; m < 6; ++m) ps.b[m] = cs[(9 + m) * st + qidx];
+  ps.k_lb = cs[15 * st + qidx];
+  ps.k_lt = cs[16 * st + qidx];
+  ps.k_tr = cs[17 * st + qidx];
+  ps.k_t = cs[18 * st + qidx];
+}
+
 // w_ref = W K^T for the test gradient gref (reference coordinates).
 template <typename T, int MODEL>
 __device__ __forceinline__ void push_integrand(const PushState<T>& ps, const T* gref, T* wref) {
