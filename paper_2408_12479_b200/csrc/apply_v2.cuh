@@ -41,6 +41,16 @@
 #ifndef EMF_MINB_F32Q3
 #define EMF_MINB_F32Q3 0  // fp32 Q3 CTAs/SM override (experiments)
 #endif
+// fp64 Q4 tensor on the cached push-forward state (cfg2 element phase,
+// profiles/r02_tensor_push_state.txt): 1.492 ms at 4 CTAs/SM with the late
+// load, 1.353 with the 19 fields loaded before the sweeps, 1.305 with that at
+// 5 CTAs/SM; fp32 keeps the late load (0.853 vs 0.865 ms)
+#ifndef EMF_TENP_EARLY_Q4
+#define EMF_TENP_EARLY_Q4 1
+#endif
+#ifndef EMF_MINB_Q4_TENP
+#define EMF_MINB_Q4_TENP 5
+#endif
 #ifndef EMF_F32Q4_OCC
 #define EMF_F32Q4_OCC 1  // the per-strategy fp32 Q4 CTAs/SM below
 #endif
@@ -1027,6 +1037,8 @@ constexpr int minb_v2() {
   // re-measured after the ticket / dense-mapping / barrier work: cNH on
   // axis-aligned meshes fits 128 registers for these too (scalar 0.1649 ->
   // 0.1588 ms, tensor 0.1383 -> 0.1281, cachedF 0.1486 -> 0.1444)
+  // tensor on the cached push-forward state: 0.1076 -> 0.1036 ms at 5
+  if (P == 3 && MODEL == CNH && CART && STRAT == S_TENSOR && tensor_compact(MODEL, 0)) return 5;
   if (P == 3 && MODEL == CNH && CART && (STRAT == S_SCALAR || STRAT == S_TENSOR || STRAT == S_CACHEDF)) return 4;
   if (P == 3 && MODEL == INH && STRAT == S_SP_TENSOR) return 4;
   // collocated Q3 sweeps: curved iNH none 0.1506 -> 0.1465 ms, cachedF 0.1301 -> 0.1260
@@ -1037,6 +1049,7 @@ constexpr int minb_v2() {
   // general registers), so 4 CTAs/SM; the fibre model keeps 2 (spill-free at
   // up to 255 registers; 3 spilled 100-190 B)
   if (P == 4 && MODEL == FIBER) return EMF_MINB_Q4_FIBER;
+  if (P == 4 && STRAT == S_TENSOR && tensor_compact(MODEL, 0)) return EMF_MINB_Q4_TENP;
   if (P == 4 && !CART) return EMF_MINB_Q4C;
   if (P == 4 && CART) return EMF_MINB_Q4_CART;
   // fibre fp64 at Q3: 2 CTAs/SM, spill-free (32^3 curved none 0.278 -> 0.249 ms,
@@ -1283,7 +1296,9 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     // tensor Q3: the cached bundle loaded before the sweeps, its latency
     // hidden behind them (fp64 cNH 0.1281 -> 0.1219 ms, curved iNH 0.1628 ->
     // 0.1567, fibre 0.2018 -> 0.1854; fp32 2-4%; Q4 iNH slower, 0.1772 -> 0.1874)
-    constexpr bool kTenEarly = STRAT == S_TENSOR && EMF_TEN_EARLY && P == 3 && (sizeof(T) == 8 || EMF_TEN_EARLY_F32);
+    constexpr bool kTenEarly = STRAT == S_TENSOR && EMF_TEN_EARLY &&
+                               (P == 3 || (EMF_TENP_EARLY_Q4 && P == 4 && kTenPush && sizeof(T) == 8)) &&
+                               (sizeof(T) == 8 || EMF_TEN_EARLY_F32);
     auto load_tensor_bundle = [&](Bundle<T>& b) {
       if (MODEL == CNH) b.lnj = cs[C_LNJ * st + qidx];
       else {
