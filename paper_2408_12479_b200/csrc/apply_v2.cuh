@@ -45,6 +45,12 @@
 // profiles/r02_tensor_push_state.txt): 1.492 ms at 4 CTAs/SM with the late
 // load, 1.353 with the 19 fields loaded before the sweeps, 1.305 with that at
 // 5 CTAs/SM; fp32 keeps the late load (0.853 vs 0.865 ms)
+#ifndef EMF_MINB_F32_FIBER_TENP
+#define EMF_MINB_F32_FIBER_TENP 6
+#endif
+#ifndef EMF_MINB_FIBER_TENP
+#define EMF_MINB_FIBER_TENP 4
+#endif
 #ifndef EMF_TENP_EARLY_Q4
 #define EMF_TENP_EARLY_Q4 1
 #endif
@@ -1015,6 +1021,9 @@ constexpr int minb_v2() {
       if (STRAT == S_SCALAR) return 5;
     }
     if (P == 3 && EMF_MINB_F32Q3) return EMF_MINB_F32Q3;
+    // fibre tensor on the cached push-forward state (cfg3 fp32 element phase
+    // 1.111 ms at 4 CTAs/SM, 1.083 at 5, 1.027 at 6)
+    if (P == 3 && MODEL == FIBER && STRAT == S_TENSOR && tensor_compact(MODEL, 0)) return EMF_MINB_F32_FIBER_TENP;
     // 5 CTAs/SM measured faster for these cNH fp32 Q3 variants (tensor
     // 0.0912 -> 0.0871 ms, spatial none 0.1137 -> 0.1076), slower for fibre
     // tensor (0.1178 -> 0.1280) and no better elsewhere
@@ -1048,6 +1057,9 @@ constexpr int minb_v2() {
   // 128 registers (was 210-250: the 50 table doubles had been pinned in
   // general registers), so 4 CTAs/SM; the fibre model keeps 2 (spill-free at
   // up to 255 registers; 3 spilled 100-190 B)
+  // fibre tensor on the cached push-forward state is as light as the iNH one
+  // (curved Q3 0.1588 ms at 2 CTAs/SM, 0.1424 at 3, 0.1383 at 4; Q4 0.1628 -> 0.1301)
+  if (P >= 3 && MODEL == FIBER && STRAT == S_TENSOR && tensor_compact(MODEL, 0)) return EMF_MINB_FIBER_TENP;
   if (P == 4 && MODEL == FIBER) return EMF_MINB_Q4_FIBER;
   if (P == 4 && STRAT == S_TENSOR && tensor_compact(MODEL, 0)) return EMF_MINB_Q4_TENP;
   if (P == 4 && !CART) return EMF_MINB_Q4C;
@@ -1325,7 +1337,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
     };
     Bundle<T> cbe;
     PushState<T> pse;
-    if constexpr (kTenEarly && kTenPush) load_push_state<T>(cs, st, qidx, pse);
+    if constexpr (kTenEarly && kTenPush) {
+      load_push_state<T>(cs, st, qidx, pse);
+      if constexpr (MODEL == FIBER) load_push_state_fibre<T>(cs, st, qidx, pse);
+    }
     else if constexpr (kTenEarly) load_tensor_bundle(cbe);
     // spatial tensor: the cached spatial bundle loaded before the sweeps
     constexpr bool kSpTenEarly = STRAT == S_SP_TENSOR && EMF_SPT_EARLY;
@@ -1593,7 +1608,10 @@ __global__ void __launch_bounds__(TileV2<P, sizeof(T)>::EPB*(P + 1) * (P + 1) * 
       }
     } else if constexpr (kTenPush) {
       if constexpr (kTenEarly) ps = pse;
-      else load_push_state<T>(cs, st, qidx, ps);
+      else {
+        load_push_state<T>(cs, st, qidx, ps);
+        if constexpr (MODEL == FIBER) load_push_state_fibre<T>(cs, st, qidx, ps);
+      }
     } else if constexpr (STRAT == S_TENSOR) {
       if constexpr (kTenEarly) cb = cbe;
       else load_tensor_bundle(cb);

@@ -645,7 +645,7 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
       if (l->p == 3 && precision == 32 && uk_el_enabled())
         CK(cudaMalloc(&op->d_uk_el, ns * l->nel * 3 * (ns == 8 ? 82 : 80)));
     }
-    int nf = strategy == EMFGPU_TENSOR ? (tensor_compact(model, domain) ? C_NTP : C_NT)
+    int nf = strategy == EMFGPU_TENSOR ? (tensor_compact(model, domain) ? tensor_compact_fields(model) : C_NT)
              : strategy == EMFGPU_SCALAR ? 8 : strategy == EMFGPU_CACHED_F ? C_NG : 0;
     if (domain == 1) nf = strategy == EMFGPU_TENSOR ? C_NSP : C_JT + 9;  // J_t, 1/J always (operator.hpp:690-691)
     op->n_cache_fields = nf;
@@ -985,7 +985,7 @@ emfgpu_status emfgpu_op_ledger(const emfgpu_op* op, int* storage, int* traffic, 
   if (op->strategy == EMFGPU_TENSOR) fields += 30;
   bool need_geo = true;
   if (op->strategy == EMFGPU_TENSOR && tensor_compact(op->model, op->domain)) {
-    fields = C_NTP;  // the push-forward state carries the geometry
+    fields = tensor_compact_fields(op->model);  // the push-forward state carries the geometry
     need_geo = false;
   }
   if (op->domain == 1) {  // ledger.cpp:27-70 spatial rows: J_t + 1/J always, tau/b/FHF^T for tensor

@@ -45,7 +45,9 @@ enum CacheSlot : int {
   // tensor, cNH / iNH in the material domain: the push-forward state instead
   // (qp.cuh PushState: K = J0^-1 F^-1 (9), b (6), 4 coefficients with det J0 w
   // folded in) -- 19 fields and no geometry read in the apply, against 33 + 10
-  C_PK = 0, C_PB = 9, C_PC = 15, C_NTP = 19,
+  // (fibre: + 2 x (A_f = F H_f F^T (6), k_s, k_c) = 35, against 37 + 10 + the 12
+  // per-point structure-tensor entries)
+  C_PK = 0, C_PB = 9, C_PC = 15, C_NTP = 19, C_NTPF = 35,
   // cachedF: displacement gradient G = F - I
   C_G = 0, C_NG = 9,
   // spatial formulation (operator.hpp:139-143): scalars as above, then 1/J,
@@ -57,9 +59,13 @@ enum CacheSlot : int {
 #define EMF_TENSOR_PUSH 1
 #endif
 // Does strategy tensor cache the push-forward state for this (model, domain)?
+#ifndef EMF_TENSOR_PUSH_FIBER
+#define EMF_TENSOR_PUSH_FIBER 1
+#endif
 __host__ __device__ constexpr bool tensor_compact(int model, int spatial) {
-  return EMF_TENSOR_PUSH && model != 2 /* FIBER */ && !spatial;
+  return EMF_TENSOR_PUSH && (model != 2 /* FIBER */ || EMF_TENSOR_PUSH_FIBER) && !spatial;
 }
+__host__ __device__ constexpr int tensor_compact_fields(int model) { return model == 2 ? 35 : 19; }
 
 // n / d for 0 <= n < 2^31 with a precomputed multiplier (round-up method,
 // Hacker's Delight 10-9): q = (umulhi(n, m) + n) >> l.
@@ -510,6 +516,11 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     PushState<double> ps;
     push_state<double, MODEL, false, false>(md, g, j0inv, detw, cb, ps);
     store_push_state<T>(a.cache, st, qidx, ps);
+    if constexpr (MODEL == FIBER) {
+      cache_scalars<double, MODEL>(md, cb);
+      push_state_fibre<double>(md, cb, detw, ps);
+      store_push_state_fibre<T>(a.cache, st, qidx, ps);
+    }
     return;
   }
   // stored scalars, computed in double (operator.hpp:720-735)
@@ -619,6 +630,7 @@ __global__ void __launch_bounds__(Tile<P>::EPB*(P + 1) * (P + 1) * (P + 1))
     cache_scalars<T, MODEL>(mq, cb);
   } else if (tensor_compact(MODEL, 0)) {
     load_push_state<T>(cs, st, ix, ps);
+    if constexpr (MODEL == FIBER) load_push_state_fibre<T>(cs, st, ix, ps);
   } else {
 #pragma unroll
     for (int m = 0; m < 9; ++m) {

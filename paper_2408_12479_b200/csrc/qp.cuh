@@ -464,6 +464,12 @@ template <typename T>
 struct PushState {
   T K[9], b[6];
   T k_lb, k_lt, k_tr, k_t;  // coefficients of l b, l^T, tr(l) I (and t: l:b I, tr(l) b), times detw
+  // fibre model (strategy tensor): the pushed structure tensors A_f = F H_f F^T
+  // and, times detw, k_s = c3 e (stress) and k_c = 2 c3 (2 k2 e^2 + 1) (tangent):
+  //   W += sum_f k_s l A_f + k_c (A_f : l) A_f
+  // (dg S_fib F^T = l F S_fib F^T; H_f : sym(F^T dg) = A_f : l;
+  // constitutive.hpp:368-371, 404-417)
+  T Af[2][6], k_s[2], k_c[2];
 };
 
 // State at one point from the linearization gradient gg = grad_X u_k (material
@@ -529,6 +535,45 @@ __device__ __forceinline__ bool push_state(const MatConst<T>& m, const T* gg, co
 
 // The state as 19 cache fields (kernels.cuh: C_PK, C_PB, C_PC), computed in
 // TS and stored / loaded as T.
+// Fibre part of the state from the material bundle (after make_strain and
+// cache_scalars).
+template <typename T>
+__device__ __forceinline__ void push_state_fibre(const MatConst<T>& m, const Bundle<T>& c, T detw, PushState<T>& ps) {
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    T fh[9], a[9];
+    mm_ts(c.F, m.h[f], fh);
+    mm_bt(fh, c.F, a);  // F H F^T
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i; j < 3; ++j) ps.Af[f][sidx(i, j)] = i == j ? a[3 * i + j] : T(0.5) * (a[3 * i + j] + a[3 * j + i]);
+    ps.k_s[f] = (c.c3[f] * c.efib[f]) * detw;
+    ps.k_c[f] = (T(2) * (c.c3[f] * ((((T(2) * m.k2) * c.efib[f]) * c.efib[f]) + T(1)))) * detw;
+  }
+}
+
+template <typename T, typename TS>
+__device__ __forceinline__ void store_push_state_fibre(T* cache, int64_t st, int64_t qidx, const PushState<TS>& ps) {
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+#pragma unroll
+    for (int m = 0; m < 6; ++m) cache[(19 + 8 * f + m) * st + qidx] = T(ps.Af[f][m]);
+    cache[(19 + 8 * f + 6) * st + qidx] = T(ps.k_s[f]);
+    cache[(19 + 8 * f + 7) * st + qidx] = T(ps.k_c[f]);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void load_push_state_fibre(const T* cs, int64_t st, int64_t qidx, PushState<T>& ps) {
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+#pragma unroll
+    for (int m = 0; m < 6; ++m) ps.Af[f][m] = cs[(19 + 8 * f + m) * st + qidx];
+    ps.k_s[f] = cs[(19 + 8 * f + 6) * st + qidx];
+    ps.k_c[f] = cs[(19 + 8 * f + 7) * st + qidx];
+  }
+}
+
 template <typename T, typename TS>
 __device__ __forceinline__ void store_push_state(T* cache, int64_t st, int64_t qidx, const PushState<TS>& ps) {
 #pragma unroll
@@ -578,6 +623,21 @@ __device__ __forceinline__ void push_integrand(const PushState<T>& ps, const T* 
   W[0] += diag;
   W[4] += diag;
   W[8] += diag;
+  if constexpr (MODEL == FIBER) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const T* A = ps.Af[f];
+      T la[9];
+      mm_ts(l, A, la);
+      const T adl = ((l[0] * A[0] + l[4] * A[1]) + l[8] * A[2]) +
+                    (((l[1] + l[3]) * A[3] + (l[2] + l[6]) * A[4]) + (l[5] + l[7]) * A[5]);
+      const T ca = ps.k_c[f] * adl;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) W[3 * i + j] += ps.k_s[f] * la[3 * i + j] + ca * A[sidx(i, j)];
+    }
+  }
   mm_bt(W, ps.K, wref);
 }
 
