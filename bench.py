@@ -696,9 +696,10 @@ def run_extra_workloads(args, flush, peaks):
         t_el = sum(a.elapsed_time(b) for a, b, c in ms) / len(ms)
         nq = lev.n_elements * 64
         by = (ledger_qp_bytes("fiber", "tensor") + 96) * (prec // 8) / 8 * nq + 2 * (prec // 8) * lev.n_dofs
-        rec3[f"fp{prec}_tensor"] = {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all,
-                                    "ms_element_kernel": t_el, "hbm_frac_yardstick": by / (t_el * 1e-3) / 1e9 /
-                                    peaks["hbm"]}
+        rec3[f"fp{prec}_tensor"] = add_real_traffic(
+            {"dofs_per_s": lev.n_dofs / (t_all * 1e-3), "ms_per_apply": t_all, "ms_element_kernel": t_el,
+             "hbm_frac_yardstick": by / (t_el * 1e-3) / 1e9 / peaks["hbm"]},
+            load_traffic().get(f"cfg3_fp{prec}_tensor"), peaks["hbm"])
         del op, x, y
     out["cfg3"] = rec3
     del lev
