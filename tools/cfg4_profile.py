@@ -1,5 +1,5 @@
 """cfg4 (well-posed variant) PCG + fp32 hp-MG solve, for an ncu launch list
-(python tools/cfg4_profile.py [iterations]); prints the solve time."""
+(python tools/cfg4_profile.py [iterations [reps [level strategy]]]); prints the solve time."""
 import os
 import sys
 import time
@@ -17,8 +17,12 @@ w = W.cfg4(wellposed=True)
 lev = w.level()
 op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
 op.update_linearization(np.zeros(lev.n_dofs))
-mg = G.MgHierarchy(lev, w.model, w.material(), degree=5, coarse_n=6, precision=32)
+mg_strategy = sys.argv[3] if len(sys.argv) > 3 else "none"  # storage strategy of the V-cycle's level operators
+t0 = time.perf_counter()
+mg = G.MgHierarchy(lev, w.model, w.material(), strategy=mg_strategy, degree=5, coarse_n=6, precision=32)
 mg.update_linearization(torch.zeros(lev.n_dofs, dtype=torch.float64, device="cuda"))
+torch.cuda.synchronize()
+print("hierarchy (%s levels) create + linearize %.3f s" % (mg_strategy, time.perf_counter() - t0))
 b = torch.tensor(W.rhs(w), device="cuda")
 x = torch.empty_like(b)
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
