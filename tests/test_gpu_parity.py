@@ -817,6 +817,34 @@ print(its, its2, hashlib.sha1(x.cpu().numpy().tobytes() + hist.tobytes() + x2.cp
     assert outs[0] == outs[1], outs
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["cnh", "inh", "fiber"])
+def test_pcg_with_tensor_strategy_levels(G, model):
+    """The V-cycle's level operators on strategy tensor (cNH / iNH / fibre: the
+    cached push-forward state, csrc/qp.cuh PushState) precondition like the
+    on-the-fly levels: same PCG iteration count within 1, same solution."""
+    import torch
+    n, p = 6, 4
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    prm = G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0)
+    u0 = I.make_u0(n, n, n, p, amp=0.003, noise=1e-5)  # small: the tangent stays positive definite
+    op = G.ElasticOperator(lev, model, prm, "none", 64)
+    op.update_linearization(u0)
+    b = torch.tensor(I.make_v(lev.n_dofs, 2), device="cuda")
+    b[torch.tensor(I.dirichlet_mask(n, n, n, p, 1), device="cuda")] = 0
+    du = torch.tensor(u0, device="cuda")
+    res = {}
+    for strat in ("none", "tensor"):
+        mg = G.MgHierarchy(lev, model, prm, strategy=strat, degree=5, coarse_n=3, precision=32)
+        mg.update_linearization(du)
+        x = torch.empty_like(b)
+        its, hist = G.pcg_solve(op, mg, b, x, 1e-8, 200)
+        res[strat] = (its, x)
+    assert abs(res["none"][0] - res["tensor"][0]) <= 1, (res["none"][0], res["tensor"][0])
+    err = float(torch.linalg.vector_norm(res["none"][1] - res["tensor"][1]) / torch.linalg.vector_norm(res["none"][1]))
+    assert err <= 1e-6, err
+
+
 # ---- BASELINE configs[2] shape against the reference itself (shear map)
 
 @pytest.mark.parametrize("n", [2, 4])
