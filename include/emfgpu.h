@@ -146,7 +146,7 @@ emfgpu_status emfgpu_op_update_linearization_host(emfgpu_op* op, const double* u
 emfgpu_status emfgpu_op_update_linearization(emfgpu_op* op, const double* d_u_k, int64_t* bad_element,
                                              int* bad_qpoint, void* stream);
 int emfgpu_op_linearized(const emfgpu_op* op);               /* linearized(), :89 */
-uint64_t emfgpu_op_checksum(const emfgpu_op* op);            /* checksum(), FNV-1a of u_k, :90 */
+uint64_t emfgpu_op_checksum(const emfgpu_op* op);            /* checksum(), FNV-1a of u_k, :90 (computed on demand; synchronises) */
 
 /* apply_tangent(du, y), operator.hpp:99-100/597-621: y = K(u_k) du with the
  * Dirichlet identity.  x, y: device arrays of n_dofs Number values. */

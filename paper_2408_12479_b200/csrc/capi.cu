@@ -716,7 +716,22 @@ int64_t emfgpu_op_n_dofs(const emfgpu_op* op) { return op ? op->L->ndofs : 0; }
 int emfgpu_op_precision(const emfgpu_op* op) { return op ? op->precision : 0; }
 const char* emfgpu_op_last_error(const emfgpu_op* op) { return op ? op->last_error.c_str() : ""; }
 int emfgpu_op_linearized(const emfgpu_op* op) { return op && op->linearized ? 1 : 0; }
-uint64_t emfgpu_op_checksum(const emfgpu_op* op) { return op ? op->checksum : 0; }
+uint64_t emfgpu_op_checksum(const emfgpu_op* op) {
+  if (!op) return 0;
+  if (!op->checksum_valid) {
+    // on demand, from the device copy of the linearization point
+    std::unique_lock<std::recursive_mutex> lk(const_cast<emfgpu_op*>(op)->use_mu);
+    std::vector<double> tmp((size_t)op->L->ndofs);
+    if (cudaSetDevice(op->L->device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(tmp.data(), op->d_ukd, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    op->checksum = fnv1a(tmp.data(), sizeof(double) * tmp.size());
+    op->checksum_valid = true;
+  }
+  return op->checksum;
+}
 
 static void linearize_impl(emfgpu_op* op, int64_t* be, int* bq, cudaStream_t s) {
   const emfgpu_level* L = op->L;
@@ -749,7 +764,7 @@ emfgpu_status emfgpu_op_update_linearization_host(emfgpu_op* op, const double* u
   return guarded(&op->last_error, [&] {
     OP_USE(op, op->stream);
     CK(cudaMemcpyAsync(op->d_ukd, u_k, sizeof(double) * op->L->ndofs, cudaMemcpyHostToDevice, op->stream));
-    op->checksum = fnv1a(u_k, sizeof(double) * op->L->ndofs);
+    op->checksum_valid = false;
     linearize_impl(op, be, bq, op->stream);
   });
 }
@@ -761,7 +776,7 @@ emfgpu_status emfgpu_op_update_linearization(emfgpu_op* op, const double* d_u_k,
     cudaStream_t s = S(stream, op->stream);
     OP_USE(op, s);
     CK(cudaMemcpyAsync(op->d_ukd, d_u_k, sizeof(double) * op->L->ndofs, cudaMemcpyDeviceToDevice, s));
-    op->checksum = 0;
+    op->checksum_valid = false;
     linearize_impl(op, be, bq, s);
   });
 }
@@ -2514,7 +2529,7 @@ emfgpu_status emfgpu_newton_solve(emfgpu_op* op, emfgpu_mg* mg, double* d_u, con
     while (rnorm > c.eps_abs && rnorm > c.eps_rel * r0) {
       if (k >= c.max_iter) throw ApiError(EMFGPU_ERR_NUMERICAL, "newton: iteration budget exhausted");
       CK(cudaMemcpyAsync(op->d_ukd, d_u, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-      op->checksum = 0;
+      op->checksum_valid = false;
       linearize_impl(op, nullptr, nullptr, s);
       if (mg) {
         if (mg->cfg.precision == 64)

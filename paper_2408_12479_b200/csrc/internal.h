@@ -199,6 +199,10 @@ struct emfgpu_op {
   std::recursive_mutex use_mu;
   cudaEvent_t ev_use = nullptr;
   bool linearized = false;
-  uint64_t checksum = 0;
+  // checksum() (operator.hpp:90): FNV-1a of u_k.  The hash is byte-serial
+  // (0.19 s on the host for cfg4's 172 MB), so it is computed on demand from
+  // the device copy of u_k instead of in every update_linearization.
+  mutable uint64_t checksum = 0;
+  mutable bool checksum_valid = true;
   std::string last_error;
 };

@@ -818,6 +818,30 @@ print(its, its2, hashlib.sha1(x.cpu().numpy().tobytes() + hist.tobytes() + x2.cp
 
 
 @pytest.mark.gpu
+def test_checksum_is_fnv1a_of_the_linearization_point(G):
+    """checksum() (operator.hpp:90, 650): FNV-1a over the bytes of u_k, computed
+    on demand from the device copy -- after a host and after a device update."""
+    import torch
+
+    def fnv1a(buf):
+        h = 1469598103934665603
+        for byte in buf:
+            h = ((h ^ byte) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+        return h
+
+    n, p = 3, 2
+    lev = G.FeLevel(n, p=p)
+    op = G.ElasticOperator(lev, "cnh", G.MaterialParams(mu=1.0, lam=10.0), "tensor", 64)
+    u0 = I.make_u0(n, n, n, p)
+    op.update_linearization(u0)
+    assert op.checksum() == fnv1a(np.ascontiguousarray(u0, dtype=np.float64).tobytes())
+    u1 = 0.5 * u0
+    op.update_linearization_device(torch.tensor(u1, device="cuda"))
+    assert op.checksum() == fnv1a(u1.tobytes())
+    assert op.checksum() == fnv1a(u1.tobytes())  # cached
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("model", ["cnh", "inh", "fiber"])
 def test_pcg_with_tensor_strategy_levels(G, model):
     """The V-cycle's level operators on strategy tensor (cNH / iNH / fibre: the
