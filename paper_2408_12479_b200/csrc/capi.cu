@@ -640,8 +640,11 @@ emfgpu_status emfgpu_op_create(const emfgpu_level* l, int model, const emfgpu_ma
     CK(cudaMalloc(&op->d_ukd, sizeof(double) * l->ndofs));
     if (strategy == EMFGPU_NONE || strategy == EMFGPU_SCALAR) {
       CK(cudaMalloc(&op->d_uk, ns * l->ndofs));
-      // per-element u_k copy: measured 1.8% faster for fp32 (curved iNH
-      // 0.1219 -> 0.1197 ms), 1.3% slower for fp64, which keeps the gather
+      // per-element u_k copy: 1.3% slower for fp64, which keeps the gather;
+      // for fp32 re-measured on the collocated v2 kernel (EMFGPU_UK_ELEM=0/1):
+      // cfg1 none 0.0973 -> 0.0932 ms with the copy, scalar 0.0973 -> 0.0932,
+      // curved iNH 0.1036 -> 0.1014 (31.5 MB read as 16-byte copies instead of
+      // 11 MB of scattered 4-byte words)
       if (l->p == 3 && precision == 32 && uk_el_enabled())
         CK(cudaMalloc(&op->d_uk_el, ns * l->nel * 3 * (ns == 8 ? 82 : 80)));
     }
