@@ -60,6 +60,9 @@
 #ifndef EMF_F32Q4_OCC
 #define EMF_F32Q4_OCC 1  // the per-strategy fp32 Q4 CTAs/SM below
 #endif
+#ifndef EMF_MINB_F32Q12
+#define EMF_MINB_F32Q12 0  // fp32 Q1 / Q2 CTAs/SM override (experiments)
+#endif
 #ifndef EMF_MINB_F32Q4
 #define EMF_MINB_F32Q4 0  // fp32 Q4 CTAs/SM override (experiments)
 #endif
@@ -1021,6 +1024,7 @@ constexpr int minb_v2() {
       if (STRAT == S_SCALAR) return 5;
     }
     if (P == 3 && EMF_MINB_F32Q3) return EMF_MINB_F32Q3;
+    if (P <= 2 && EMF_MINB_F32Q12) return EMF_MINB_F32Q12;
     // fibre tensor on the cached push-forward state (cfg3 fp32 element phase
     // 1.111 ms at 4 CTAs/SM, 1.083 at 5, 1.027 at 6)
     if (P == 3 && MODEL == FIBER && STRAT == S_TENSOR && tensor_compact(MODEL, 0)) return EMF_MINB_F32_FIBER_TENP;
