@@ -492,7 +492,8 @@ def run_gpu(args):
         del du, r
     del op, sop, x, y, kept
 
-    for prec, strat in ((64, "tensor"), (64, "scalar"), (64, "cachedF"), (32, "none"), (32, "tensor")):
+    for prec, strat in ((64, "tensor"), (64, "scalar"), (64, "cachedF"), (32, "none"), (32, "tensor"),
+                        (32, "cachedF"), (32, "scalar")):
         rec, _ = time_variant(G, args, lev, part, SlabOperator, u0, v, C2_MODEL, params, prec, strat, flush, world,
                               dist)
         variants[f"fp{prec}_{strat}"] = rec
