@@ -1322,7 +1322,13 @@ static void lanczos(emfgpu_op* op, const T* diag, int iterations, uint64_t seed,
   auto dot = [&](const double* a, const double* b, double* part, double* out) {
     launch_dot_planes<double>(a, b, plane, L->mz, part, out, s);
   };
-  lanczos_core<T>(n, 0, L->mz, op->lz_buf, diag, iterations, seed, apply, dot, lmin, lmax, s);
+  // the reorthogonalisation against the whole basis in two launches (krylov_core.h)
+  const size_t nd = (size_t)std::max(dot_partial_count(), L->mz * dot_plane_split()) + 1;
+  auto reorth = [&](double* w, const double* basis, int k, double* h, double* part) {
+    launch_multi_dot_planes(w, basis, n, k, plane, L->mz, part, (int64_t)nd, h, s);
+    launch_multi_axpy_dev(h, basis, n, k, w, n, s);
+  };
+  lanczos_core<T>(n, 0, L->mz, op->lz_buf, diag, iterations, seed, apply, dot, lmin, lmax, s, reorth);
 }
 
 emfgpu_status emfgpu_op_estimate_eigenvalues(emfgpu_op* op, const void* d_diag, int iterations, uint64_t seed,
@@ -1504,6 +1510,13 @@ void dense_coarse(emfgpu_mg* m, int l, cudaStream_t s) {
 template <typename T>
 void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
   const int nl = (int)m->lv.size();
+  // a cached V-cycle graph carries the old smoother coefficients as kernel
+  // arguments: every relinearisation (update_linearization, the Newton loop,
+  // the slab solver) drops it
+  if (m->vc_exec) cudaGraphExecDestroy(m->vc_exec);
+  m->vc_exec = nullptr;
+  m->vc_r = nullptr;
+  m->vc_z = nullptr;
   CK(cudaMemcpyAsync(m->u[0], d_u, sizeof(double) * m->lv[0]->ndofs, cudaMemcpyDeviceToDevice, s));
   // EMFGPU_TRACE=1: per-level stage times of the setup (synchronising; diagnostics only)
   static const bool trace = std::getenv("EMFGPU_TRACE") != nullptr;
@@ -1537,11 +1550,20 @@ void mg_linearize(emfgpu_mg* m, const double* d_u, cudaStream_t s) {
                    (long long)m->lv[l]->ndofs, ms(t0, t1), ms(t1, t2), ms(t2, t3));
     }
     if (l + 1 < nl) {
-      if (m->cheb[l]) emfgpu_cheb_destroy(m->cheb[l]);
-      m->cheb[l] = nullptr;
-      if (emfgpu_cheb_create(op, m->diag[l], lmax, m->cfg.degree, m->cfg.range_factor, m->cfg.safety,
-                             &m->cheb[l]) != EMFGPU_OK)
-        throw ApiError(EMFGPU_ERR_CUDA, "mg: smoother setup failed");
+      if (m->cheb[l] && m->cheb[l]->op == op && m->cheb[l]->degree == m->cfg.degree) {
+        // relinearisation: the smoother keeps its vectors (no cudaFree / cudaMalloc
+        // round trips), only the spectrum bounds and 1/diag change
+        emfgpu_cheb* c = m->cheb[l];
+        c->lambda_max = m->cfg.safety * lmax;
+        c->lambda_min = c->lambda_max / m->cfg.range_factor;
+        launch_inv<T>(static_cast<const T*>(m->diag[l]), static_cast<T*>(c->inv_diag), m->lv[l]->ndofs, s);
+      } else {
+        if (m->cheb[l]) emfgpu_cheb_destroy(m->cheb[l]);
+        m->cheb[l] = nullptr;
+        if (emfgpu_cheb_create(op, m->diag[l], lmax, m->cfg.degree, m->cfg.range_factor, m->cfg.safety,
+                               &m->cheb[l]) != EMFGPU_OK)
+          throw ApiError(EMFGPU_ERR_CUDA, "mg: smoother setup failed");
+      }
     } else if (m->dense) {
       const auto t4 = now();
       dense_coarse<T>(m, l, s);

@@ -100,6 +100,13 @@ void launch_dinv_sqrt(const T* d, double* s, int64_t n, cudaStream_t st);
 void launch_axpy_minus(double a, const double* x, double* y, int64_t n, cudaStream_t st);
 void launch_lanczos_start(double* v, int64_t n, unsigned long long seed, cudaStream_t st, int64_t offset = 0);
 void launch_axpy_dev(const double* c, const double* x, double* y, int64_t n, cudaStream_t st);
+// k plane-chunked dots of a against basis + v * stride in one pass (out[v], bitwise
+// launch_dot_planes per vector; partial: k rows of pstride doubles), and
+// y -= sum_v c[v] basis_v in order
+void launch_multi_dot_planes(const double* a, const double* basis, int64_t stride, int k, int64_t plane_len,
+                             int nplanes, double* partial, int64_t pstride, double* out, cudaStream_t s);
+void launch_multi_axpy_dev(const double* c, const double* basis, int64_t stride, int k, double* y, int64_t n,
+                           cudaStream_t s);
 void launch_div_sqrt_dev(const double* d, const double* x, double* y, int64_t n, cudaStream_t st);
 void launch_div(const double* x, double b, double* y, int64_t n, cudaStream_t st);
 template <typename T>

@@ -167,7 +167,7 @@ __global__ void dot_planes_kernel(const T* __restrict__ a, const T* __restrict__
   const int64_t i0 = (int64_t)plane * plane_len + part * chunk;
   const int64_t i1 = (int64_t)plane * plane_len + min(plane_len, (int64_t)(part + 1) * chunk);
   double s = 0.0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += kPlaneThreads) s += double(a[i]) * double(b[i]);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kPlaneThreads) s = fma(double(a[i]), double(b[i]), s);
   sm[threadIdx.x] = s;
   __syncthreads();
   for (int w = kPlaneThreads / 2; w > 0; w >>= 1) {
@@ -175,6 +175,78 @@ __global__ void dot_planes_kernel(const T* __restrict__ a, const T* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) partial[(int64_t)(first_plane + plane) * kPlaneSplit + part] = sm[0];
+}
+
+// The same partials for k vectors b_v = basis + v * stride against one a (the
+// Lanczos reorthogonalisation): a is read once per group of kDotGroup vectors;
+// per vector the summation order is dot_planes_kernel's, so partial[v] is
+// bitwise what k separate launches give.
+constexpr int kDotGroup = 4;
+__global__ void multi_dot_planes_kernel(const double* __restrict__ a, const double* __restrict__ basis, int64_t stride,
+                                        int k, int64_t plane_len, int64_t pstride, double* partial) {
+  __shared__ double sm[kDotGroup][kPlaneThreads];
+  const int plane = blockIdx.x / kPlaneSplit, part = blockIdx.x % kPlaneSplit;
+  const int64_t chunk = (plane_len + kPlaneSplit - 1) / kPlaneSplit;
+  const int64_t i0 = (int64_t)plane * plane_len + part * chunk;
+  const int64_t i1 = (int64_t)plane * plane_len + min(plane_len, (int64_t)(part + 1) * chunk);
+  for (int v0 = 0; v0 < k; v0 += kDotGroup) {
+    double s[kDotGroup];
+#pragma unroll
+    for (int g = 0; g < kDotGroup; ++g) s[g] = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += kPlaneThreads) {
+      const double ai = a[i];
+#pragma unroll
+      for (int g = 0; g < kDotGroup; ++g)
+        if (v0 + g < k) s[g] = fma(ai, basis[(int64_t)(v0 + g) * stride + i], s[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < kDotGroup; ++g) sm[g][threadIdx.x] = s[g];
+    __syncthreads();
+    for (int w = kPlaneThreads / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) {
+#pragma unroll
+        for (int g = 0; g < kDotGroup; ++g) sm[g][threadIdx.x] += sm[g][threadIdx.x + w];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x < kDotGroup && v0 + threadIdx.x < k)
+      partial[(int64_t)(v0 + threadIdx.x) * pstride + (int64_t)plane * kPlaneSplit + part] = sm[threadIdx.x][0];
+    __syncthreads();
+  }
+}
+// out[v] = ordered sum of partial[v * pstride .. + m): sum_ordered_kernel per vector
+__global__ void multi_sum_ordered_kernel(const double* partial, int64_t pstride, int64_t m, double* out) {
+  __shared__ double sm[1024];
+  const double* p = partial + (int64_t)blockIdx.x * pstride;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += 1024) s += p[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = sm[0];
+}
+// y -= c[0] x_0, then c[1] x_1, ... in this order (k axpy_dev_kernel launches in one)
+__global__ void multi_axpy_dev_kernel(const double* __restrict__ c, const double* __restrict__ basis, int64_t stride,
+                                      int k, double* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double yi = y[i];
+  for (int v = 0; v < k; ++v) yi = fma(-c[v], basis[(int64_t)v * stride + i], yi);
+  y[i] = yi;
+}
+void launch_multi_dot_planes(const double* a, const double* basis, int64_t stride, int k, int64_t plane_len,
+                             int nplanes, double* partial, int64_t pstride, double* out, cudaStream_t s) {
+  if (k <= 0 || nplanes <= 0) return;
+  multi_dot_planes_kernel<<<(unsigned)(nplanes * kPlaneSplit), kPlaneThreads, 0, s>>>(a, basis, stride, k, plane_len,
+                                                                                    pstride, partial);
+  multi_sum_ordered_kernel<<<(unsigned)k, 1024, 0, s>>>(partial, pstride, (int64_t)nplanes * kPlaneSplit, out);
+}
+void launch_multi_axpy_dev(const double* c, const double* basis, int64_t stride, int k, double* y, int64_t n,
+                           cudaStream_t s) {
+  if (k > 0) multi_axpy_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, basis, stride, k, y, n);
 }
 
 __global__ void sum_ordered_kernel(const double* partial, int64_t m, double* out) {
@@ -258,7 +330,7 @@ __global__ void lanczos_start_kernel(double* __restrict__ v, int64_t n, unsigned
 __global__ void axpy_dev_kernel(const double* __restrict__ c, const double* __restrict__ x, double* __restrict__ y,
                                 int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) y[i] -= c[0] * x[i];
+  if (i < n) y[i] = fma(-c[0], x[i], y[i]);
 }
 // y = x / sqrt(d[0])
 __global__ void div_sqrt_dev_kernel(const double* __restrict__ d, const double* __restrict__ x,
