@@ -54,29 +54,36 @@ __global__ void probe_extract_kernel(const T* y, double* A, int64_t n, int mx, i
   A[i * n + j] = (double)y[i];
 }
 
-// [A | I] -> [I | A^-1] in place on M (n x 2n, row-major), partial pivoting.
+// [A | I] -> A^-1 on M (n x 2n, row-major), partial pivoting with DenseLU's
+// rule (the first row of maximal |a| among the remaining ones, solver.hpp:55-63).
+// One grid synchronisation per column: the row interchanges are logical (every
+// CTA keeps the same position -> row permutation in shared memory and finds
+// the pivot redundantly), and the scaling of the previous pivot row is folded
+// into the elimination pass that first reads it.  The arithmetic per entry is
+// that of the three-pass form (interchange, scale, eliminate).  The inverse's
+// rows end in the left halves of M in their logical order.
 __global__ void gauss_jordan_kernel(double* M, int n, int* singular) {
   cg::grid_group grid = cg::this_grid();
   const int w = 2 * n;
+  extern __shared__ int s_perm[];  // logical position -> physical row
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ int s_piv;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) s_perm[p] = p;
+  __syncthreads();
+  int prev = -1;          // physical row of the previous pivot (still unscaled in memory)
+  double inv_prev = 0.0;  // 1 / its pivot
   for (int c = 0; c < n; ++c) {
-    // (a) scale the previous pivot row, search the pivot of column c
-    if (c > 0) {
-      const int pc = c - 1;
-      const double inv = 1.0 / M[(int64_t)pc * w + pc];
-      for (int64_t k = pc + 1 + gtid; k < w; k += gthreads) M[(int64_t)pc * w + k] *= inv;
-    }
+    // pivot of column c among the logical positions c..n-1
     double best = -1.0;
     int bi = n;
-    for (int r = c + threadIdx.x; r < n; r += blockDim.x) {
-      const double v = fabs(M[(int64_t)r * w + c]);
-      if (v > best) {  // strictly greater: first row of maximal |a| (DenseLU::factor)
+    for (int p = c + threadIdx.x; p < n; p += blockDim.x) {
+      const double v = fabs(M[(int64_t)s_perm[p] * w + c]);
+      if (v > best) {  // strictly greater: first position of maximal |a|
         best = v;
-        bi = r;
+        bi = p;
       }
     }
 #pragma unroll
@@ -101,44 +108,54 @@ __global__ void gauss_jordan_kernel(double* M, int n, int* singular) {
           b2 = s_val[q];
           i2 = s_idx[q];
         }
-      s_piv = i2;
-      if (!(b2 >= 1e-250) && blockIdx.x == 0) atomicExch(singular, 1);
+      if (!(b2 >= 1e-250)) {
+        if (blockIdx.x == 0) atomicExch(singular, 1);
+        i2 = c;  // keep going on a defined row; the caller reports the singular matrix
+      }
+      const int t = s_perm[c];  // the interchange of positions c and i2
+      s_perm[c] = s_perm[i2];
+      s_perm[i2] = t;
+      s_piv = s_perm[c];
     }
     __syncthreads();
-    const int pr = s_piv;
-    grid.sync();  // every CTA has read column c before the swap
-    if (pr != c)
-      for (int64_t k = gtid; k < w; k += gthreads) {
-        const double t = M[(int64_t)pr * w + k];
-        M[(int64_t)pr * w + k] = M[(int64_t)c * w + k];
-        M[(int64_t)c * w + k] = t;
-      }
-    grid.sync();
-    // (b) eliminate column c from every other row (pivot row read unscaled)
-    const double inv = 1.0 / M[(int64_t)c * w + c];
-    const int64_t cols = w - c - 1;
-    const int64_t total = (int64_t)n * cols;
-    for (int64_t t = gtid; t < total; t += gthreads) {
-      const int r = (int)(t / cols);
-      if (r == c) continue;
-      const int64_t k = c + 1 + t % cols;
-      const double f = M[(int64_t)r * w + c] * inv;
-      M[(int64_t)r * w + k] -= f * M[(int64_t)c * w + k];
+    const int prow = s_piv;
+    // eliminate column c from every other row (pivot row read unscaled); the
+    // previous pivot row is scaled by its 1 / pivot as it is read
+    // (a warp per row with lanes over the columns measured slower, 22.7 vs 17.0 ms:
+    // only n of the grid's warps work, each in a long dependent loop)
+    const double inv = 1.0 / M[(int64_t)prow * w + c];
+    const unsigned cols = (unsigned)(w - c - 1);
+    const unsigned total = (unsigned)n * cols;  // n <= coarse_direct_limit: fits 32 bits
+    const double* const prw = M + (int64_t)prow * w + c + 1;
+    for (unsigned t = (unsigned)gtid; t < total; t += (unsigned)gthreads) {
+      const unsigned r = t / cols, k = t - r * cols;
+      if ((int)r == prow) continue;
+      double* const row = M + (int64_t)r * w + c;
+      const double sc = (int)r == prev ? inv_prev : 1.0;  // x * 1.0 is exact
+      const double f = (row[0] * sc) * inv;
+      row[1 + k] = fma(-f, prw[k], row[1 + k] * sc);
     }
+    prev = prow;
+    inv_prev = inv;
     grid.sync();
   }
-  const int pc = n - 1;
-  const double inv = 1.0 / M[(int64_t)pc * w + pc];
-  for (int64_t k = pc + 1 + gtid; k < w; k += gthreads) M[(int64_t)pc * w + k] *= inv;
+  // the last pivot row's scaling, then the rows into logical order (left halves)
+  for (int64_t k = n + gtid; k < w; k += gthreads) M[(int64_t)prev * w + k] *= inv_prev;
+  grid.sync();
+  for (int64_t t = gtid; t < (int64_t)n * n; t += gthreads) {
+    const int p = (int)(t / n);
+    const int64_t k = t % n;
+    M[(int64_t)p * w + k] = M[(int64_t)s_perm[p] * w + n + k];
+  }
 }
 
-// x = T(Ainv * double(b)); Ainv is the right half of M (row stride 2n).
+// x = T(Ainv * double(b)); Ainv is the left half of M (row stride 2n).
 template <typename T>
 __global__ void coarse_gemv_kernel(const double* M, const T* b, T* x, int n) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
-  const double* a = M + (int64_t)row * 2 * n + n;
+  const double* a = M + (int64_t)row * 2 * n;
   double acc = 0.0;
   for (int j = lane; j < n; j += 32) acc += a[j] * (double)b[j];
 #pragma unroll
@@ -181,11 +198,11 @@ void launch_dense_invert(const double* A, double* M, int n, int* d_singular, cud
   const int threads = 512;
   int sms = 0, per = 0;
   per_device_shape(shape, sms, per, [&](int& p) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, gauss_jordan_kernel, threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, gauss_jordan_kernel, threads, sizeof(int) * 2048);
   });
   const int grid = sms;  // one CTA per SM: grid syncs stay cheap
   void* args[] = {(void*)&M, (void*)&n, (void*)&d_singular};
-  cudaLaunchCooperativeKernel((const void*)gauss_jordan_kernel, dim3(grid), dim3(threads), args, 0, st);
+  cudaLaunchCooperativeKernel((const void*)gauss_jordan_kernel, dim3(grid), dim3(threads), args, sizeof(int) * n, st);
 }
 
 template <typename T>
