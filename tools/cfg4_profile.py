@@ -15,7 +15,8 @@ from paper_2408_12479_b200 import workloads as W  # noqa: E402
 its_max = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 w = W.cfg4(wellposed=True)
 lev = w.level()
-op = G.ElasticOperator(lev, w.model, w.material(), "none", 64)
+op_strategy = sys.argv[4] if len(sys.argv) > 4 else "none"  # strategy of the outer fp64 operator
+op = G.ElasticOperator(lev, w.model, w.material(), op_strategy, 64)
 op.update_linearization(np.zeros(lev.n_dofs))
 mg_strategy = sys.argv[3] if len(sys.argv) > 3 else "none"  # storage strategy of the V-cycle's level operators
 t0 = time.perf_counter()
