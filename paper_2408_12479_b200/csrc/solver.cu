@@ -60,11 +60,12 @@ __global__ void cheb_first_kernel(T* __restrict__ x, T* __restrict__ r, T* __res
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   // zero start: r = b, x = 0; else r holds A x on entry
-  const T ri = zero_start ? b[i] : b[i] - r[i];
+  const T ri = b[i] - (zero_start ? T(0) : r[i]);
   const T di = (inv_theta * inv_diag[i]) * ri;
+  const T xi = (zero_start ? T(0) : x[i]) + di;
   r[i] = ri;
   d[i] = di;
-  x[i] = zero_start ? di : x[i] + di;
+  x[i] = xi;
 }
 
 template <typename T>
@@ -73,10 +74,11 @@ __global__ void cheb_step_kernel(T* __restrict__ x, T* __restrict__ r, T* __rest
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const T ri = r[i] - ad[i];
-  const T di = f1 * d[i] + (f2 * inv_diag[i]) * ri;
+  const T di = fma(f1, d[i], (f2 * inv_diag[i]) * ri);
+  const T xi = x[i] + di;
   r[i] = ri;
   d[i] = di;
-  x[i] += di;
+  x[i] = xi;
 }
 
 template <typename T>
