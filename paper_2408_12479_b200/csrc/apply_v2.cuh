@@ -1100,6 +1100,8 @@ constexpr bool fresh_pos_v2() {
   // 0.1772 ms without; scalar 0.1916 vs 0.1936 and Q4 tensor 0.1772 vs 0.1853 do)
   if (sizeof(T) == 8 && MODEL == INH && P == 3 && STRAT == S_SCALAR) return true;
   if (sizeof(T) == 8 && MODEL == INH && P == 4 && STRAT == S_TENSOR) return true;
+  // collocated Q4 kernel, cfg2 fp64 scalar: 2.070 -> 2.016 ms (every other variant 1-9% slower)
+  if (sizeof(T) == 8 && MODEL == INH && P == 4 && STRAT == S_SCALAR) return true;
   return false;
 }
 
