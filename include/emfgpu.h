@@ -44,7 +44,12 @@ typedef enum emfgpu_status {
 
 typedef enum emfgpu_model { EMFGPU_CNH = 0, EMFGPU_INH = 1, EMFGPU_FIBER = 2 } emfgpu_model;
 /* Strategy: the reference's none/scalar/tensor (material.hpp:25) plus the
- * cached displacement gradient (north star "cached F"). */
+ * cached displacement gradient (north star "cached F").  TENSOR caches
+ * everything the apply needs of the linearization point: in the material
+ * domain as the push-forward state K = J0^-1 F^-1, b and the coefficients with
+ * det J0 w folded in (19 values per point, 35 for the fibre model, no geometry
+ * read in the apply) instead of the reference's F, F^-1, S, C^-1 cell -- the
+ * same operator to round-off, 152 B per point in fp64. */
 typedef enum emfgpu_strategy {
   EMFGPU_NONE = 0,
   EMFGPU_SCALAR = 1,
