@@ -818,6 +818,35 @@ print(its, its2, hashlib.sha1(x.cpu().numpy().tobytes() + hist.tobytes() + x2.cp
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", [(11, 3, "cnh", "none", 64), (11, 3, "inh", "tensor", 32), (11, 3, "fiber", "tensor", 64),
+                                  (9, 4, "inh", "none", 64), (9, 4, "inh", "none", 32), (9, 4, "fiber", "tensor", 32),
+                                  (9, 4, "inh", "cachedF", 64), (13, 2, "inh", "tensor", 32)],
+                         ids=lambda c: "-".join(map(str, c)))
+def test_element_kernels_repeat_bitwise(G, case):
+    """Race proxy (no compute-sanitizer on the pool): the collocated Q3 / Q4
+    kernels, the push-forward tensor cache and the v2 residual give bitwise the
+    same vectors run after run, on odd element counts (padding elements in the
+    last CTA) with several CTAs per SM (tools/repeat_bitwise.py is the long form)."""
+    import torch
+    n, p, model, strat, prec = case
+    lev = G.FeLevel(n, p=p, map_param=(0.05,))
+    op = G.ElasticOperator(lev, model, G.MaterialParams(mu=1.0, lam=10.0, kappa_b=50.0), strat, prec)
+    u0 = I.make_u0(n, n, n, p, amp=0.02, noise=1e-4)
+    op.update_linearization(u0)
+    dt = torch.float64 if prec == 64 else torch.float32
+    x = torch.tensor(I.make_v(lev.n_dofs), dtype=dt, device="cuda")
+    du = torch.tensor(u0, dtype=dt, device="cuda")
+    y0, r0, y, r = (torch.empty_like(x) for _ in range(4))
+    op.apply_tangent_device(x, y0)
+    op.evaluate_residual_device(du, r0)
+    assert bool(torch.isfinite(y0).all()) and bool(torch.isfinite(r0).all())
+    for _ in range(8):
+        op.apply_tangent_device(x, y)
+        op.evaluate_residual_device(du, r)
+        assert torch.equal(y, y0) and torch.equal(r, r0)
+
+
+@pytest.mark.gpu
 def test_checksum_is_fnv1a_of_the_linearization_point(G):
     """checksum() (operator.hpp:90, 650): FNV-1a over the bytes of u_k, computed
     on demand from the device copy -- after a host and after a device update."""
